@@ -1,0 +1,154 @@
+/*
+ * npsd_b200.h — C ABI of the B200-native neural-preconditioned PSDO ("DCDM")
+ * Poisson solve. Plain pointers and sizes only; no torch or C++ types.
+ *
+ * Each entry point replaces one reference interface on the hot path
+ * (/root/reference/proj, C++ library `npsd`):
+ *
+ *   npsd_b200_create         net::NeuralPrecond ctor / net::neural_precond
+ *                            (include/npsd/net/precond.hpp:14-33,
+ *                            src/net_precond.cpp:9-12, 37-40) for the weights;
+ *                            the grid (dims, depth) comes from the
+ *                            IndicatorImage and NetContext::build's
+ *                            divisibility rule (net/forward.hpp:56-62)
+ *   npsd_b200_set_mask       the per-frame part of the same ctor:
+ *                            IndicatorImage -> ReductionMap::from_image
+ *                            (src/discretization.cpp:5-19) + NetContext::build
+ *                            (net/forward.hpp:56-93) + assemble_poisson[_3d]
+ *                            (src/discretization.cpp:21-127; matrix-free here)
+ *   npsd_b200_precond_apply  Preconditioner::apply (include/npsd/precond.hpp:17)
+ *                            as NeuralPrecond::apply (src/net_precond.cpp:14-35)
+ *   npsd_b200_psdo_solve     psdo_solve (include/npsd/solver.hpp:64-65,
+ *                            src/solver.cpp:189-276); n_ortho = 0 is psd_solve
+ *                            (solver.hpp:68-69)
+ *   npsd_b200_spmv           spmv on the reduced matrix (include/npsd/sparse.hpp:38-39)
+ *   npsd_b200_net_apply      NetContext<float>::apply (net/forward.hpp:95-129)
+ *
+ * Every call returns a status: NPSD_OK, or the code of the exception the
+ * reference would throw — NPSD_INVALID_ARGUMENT (npsd::require ->
+ * std::invalid_argument, types.hpp:30-32), NPSD_BREAKDOWN (SolverBreakdown,
+ * solver.cpp:247-250), NPSD_EMPTY_SYSTEM (EmptySystemError,
+ * discretization.cpp:137), NPSD_CUDA_ERROR (device failure; there is no CPU
+ * fallback). npsd_b200_last_error(ctx) returns the message.
+ *
+ * Layouts: grids are x-fastest, linear index (z*ny + y)*nx + x
+ * (discretization.hpp:38); cell types 0 fluid, 1 air, 2 solid (scene.hpp:11);
+ * "reduced" vectors hold the n_f fluid cells in ascending linear order
+ * (ReductionMap). Weights are f32 in for_each_span order (net/params.hpp:66-80)
+ * with 9 slots in 2D and 27 in 3D (see DESIGN.md for the 3D layout).
+ */
+#ifndef NPSD_B200_H
+#define NPSD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    NPSD_OK = 0,
+    NPSD_INVALID_ARGUMENT = 1,
+    NPSD_BREAKDOWN = 2,
+    NPSD_EMPTY_SYSTEM = 3,
+    NPSD_CUDA_ERROR = 4
+};
+
+typedef struct npsd_b200_ctx npsd_b200_ctx;
+
+/* SolveConfig (include/npsd/solver.hpp:11-26) as a POD. */
+typedef struct {
+    double tol_reduction;         /* stop when ||r_k|| <= tol_reduction * ||r_0||, in (0,1) */
+    double tol_abs;               /* optional absolute stop, active when > 0 */
+    int64_t max_iters;
+    int32_t n_ortho;              /* A-orthogonalise against the last n_ortho directions (0..8) */
+    int32_t nullspace_projection; /* bool */
+    int32_t normalize_before_precond; /* bool */
+    int32_t reserved;
+} npsd_b200_solve_cfg;
+
+/* SolveReport (include/npsd/solver.hpp:28-37). residual_history and
+ * cumulative_seconds point into ctx-owned memory valid until the next solve. */
+typedef struct {
+    int64_t iterations;
+    int32_t converged;
+    int32_t breakdown;
+    const double* residual_history;   /* ||r_0|| ... ||r_k||, length history_len = iterations + 1 */
+    const double* cumulative_seconds; /* device %globaltimer at each history entry, from solve start */
+    int64_t history_len;
+    double setup_seconds;    /* set_mask excluded: r0 = b - A x0 and the first norm */
+    double iterate_seconds;
+    double precond_seconds;  /* not separable inside the device loop: 0 */
+} npsd_b200_report;
+
+/* Weights: n_params f32 in for_each_span order for (dim, depth).
+ * devices/n_devices: CUDA ordinals; one device per context in this build. */
+int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* params, size_t n_params,
+                     const int* devices, int n_devices, npsd_b200_ctx** out);
+int npsd_b200_destroy(npsd_b200_ctx* ctx);
+const char* npsd_b200_last_error(const npsd_b200_ctx* ctx); /* ctx may be NULL (create errors) */
+
+/* Replace the weights (same dim/depth); the next set_mask rebuilds tables. */
+int npsd_b200_set_params(npsd_b200_ctx* ctx, const float* params, size_t n_params);
+
+/* Per-frame setup from nx*ny*nz cell types (host or device pointer). */
+int npsd_b200_set_mask(npsd_b200_ctx* ctx, const uint8_t* cell_types);
+int npsd_b200_set_mask_device(npsd_b200_ctx* ctx, const uint8_t* d_cell_types);
+
+/* Number of fluid cells of the current mask (the reduced system size). */
+int64_t npsd_b200_n_fluid(const npsd_b200_ctx* ctx);
+/* Ascending fluid cell linear indices (length n_fluid). */
+int npsd_b200_fluid_indices(npsd_b200_ctx* ctx, int64_t* out);
+
+/* Preconditioner::apply on reduced host vectors (NeuralPrecond semantics). */
+int npsd_b200_precond_apply(npsd_b200_ctx* ctx, const double* r_reduced, double* z_reduced, int64_t n_f);
+
+/* psdo_solve on reduced host vectors; x0 may be NULL (zero start). */
+int npsd_b200_psdo_solve(npsd_b200_ctx* ctx, const double* b_reduced, const double* x0_reduced,
+                         const npsd_b200_solve_cfg* cfg, double* x_reduced, npsd_b200_report* rep);
+
+/* Same solve on device-resident FULL-GRID vectors (n_c = nx*ny*nz doubles,
+ * zero at non-fluid cells): b in, x0 in (may be NULL), x out. */
+int npsd_b200_psdo_solve_device(npsd_b200_ctx* ctx, const double* d_b_full, const double* d_x0_full,
+                                const npsd_b200_solve_cfg* cfg, double* d_x_full, npsd_b200_report* rep);
+
+/* Reduced y = A x with the matrix-free 7/5-point operator. */
+int npsd_b200_spmv(npsd_b200_ctx* ctx, const double* x_reduced, double* y_reduced, int64_t n_f);
+
+/* Raw network on the full grid (f32, n_c values). */
+int npsd_b200_net_apply(npsd_b200_ctx* ctx, const float* x_full, float* y_full);
+
+/* Introspection for parity tests: coarsened indicator image of a level
+ * (3 planes of level cells), the linear-block coefficients z_a/z_b per level
+ * (depth-1 each), and the mixed-window cell count per level. */
+int npsd_b200_level_image(npsd_b200_ctx* ctx, int level, float* out);
+int npsd_b200_linear_coeffs(npsd_b200_ctx* ctx, float* za, float* zb);
+int npsd_b200_mixed_counts(npsd_b200_ctx* ctx, int64_t* counts);
+
+/* Deterministic inputs (mirror rng.hpp / net_params.cpp; host side). */
+size_t npsd_b200_param_count(int dim, int depth);
+int npsd_b200_init_params(int dim, int depth, uint64_t seed, float* out);
+int npsd_b200_identity_params(int dim, int depth, float* out);
+void npsd_b200_rhs_normal(uint64_t seed, int64_t n, double* out);
+
+/* Device buffers and pinned host memory for callers without a CUDA runtime of
+ * their own (the Python mirror uses these; the C++ shim may too). */
+int npsd_b200_device_alloc(npsd_b200_ctx* ctx, size_t bytes, void** out);
+int npsd_b200_device_free(npsd_b200_ctx* ctx, void* p);
+int npsd_b200_host_alloc(npsd_b200_ctx* ctx, size_t bytes, void** out);
+int npsd_b200_host_free(npsd_b200_ctx* ctx, void* p);
+int npsd_b200_memcpy(npsd_b200_ctx* ctx, void* dst, const void* src, size_t bytes); /* any direction, on ctx stream */
+int npsd_b200_synchronize(npsd_b200_ctx* ctx);
+
+/* Device timing of a solve (CUDA events on the ctx stream around the device
+ * solve graph; excludes host staging). Milliseconds of the last solve. */
+double npsd_b200_last_solve_ms(const npsd_b200_ctx* ctx);
+/* Kernel launches issued by the last solve (graph nodes executed). */
+int64_t npsd_b200_last_solve_launches(const npsd_b200_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NPSD_B200_H */

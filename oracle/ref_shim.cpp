@@ -1,0 +1,247 @@
+// ============================================================================
+// TEST INFRASTRUCTURE — NOT THE PRODUCT.
+//
+// extern "C" shim over the REAL reference library, compiled by oracle/Makefile
+// from the unmodified sources under /root/reference/proj/src into
+// oracle/_ref/libnpsd_ref.so. Used (a) to pin the CPU restatement
+// (npsd_oracle.hpp) bitwise in 2D, (b) to run the reference's own psdo_solve
+// with a B200 preconditioner plugged in through a C callback (the drop-in
+// check), and (c) as bench.py's CPU baseline: reference psdo_solve on the
+// reference assemble_poisson_3d + reduce, preconditioned by the 3D network
+// restatement wrapped as an npsd::Preconditioner (the reference has no 3D net).
+// ============================================================================
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "npsd/discretization.hpp"
+#include "npsd/net/forward.hpp"
+#include "npsd/net/precond.hpp"
+#include "npsd/precond.hpp"
+#include "npsd/rng.hpp"
+#include "npsd/scene.hpp"
+#include "npsd/solver.hpp"
+#include "npsd_oracle.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const npsd::SolverBreakdown& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const npsd::EmptySystemError& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 4;
+    }
+}
+
+// 3D volumes run through the 2D reference API on a flattened (nx, ny*nz)
+// image: its linear index y'*nx + x equals (z*ny + y)*nx + x.
+npsd::IndicatorImage image_from_types(long nx, long rows, const unsigned char* types) {
+    npsd::IndicatorImage I(nx, rows, npsd::CellType::fluid);
+    for (long y = 0; y < rows; ++y)
+        for (long x = 0; x < nx; ++x) I.set_cell(x, y, static_cast<npsd::CellType>(types[y * nx + x]));
+    return I;
+}
+
+npsd::net::NetParams params_2d(int depth, const float* flat, long n) {
+    npsd::net::NetParams p;
+    p.depth = depth;
+    p.levels.resize(static_cast<std::size_t>(depth - 1));
+    npsd::require(n == p.parameter_count(), "ref: param length mismatch");
+    std::size_t o = 0;
+    p.for_each_span([&](float* dst, std::size_t k) {
+        std::memcpy(dst, flat + o, k * sizeof(float));
+        o += k;
+    });
+    return p;
+}
+
+// The 3D network restatement as a reference Preconditioner.
+class NeuralPrecond3D : public npsd::Preconditioner {
+public:
+    NeuralPrecond3D(const npsdo::Params& p, const unsigned char* types, npsdo::Dims d)
+        : map_(npsdo::ReductionMap::from_types(types, d)), P_(p, types, d, &map_) {}
+    using Preconditioner::apply;
+    void apply(const npsd::Vector& r, npsd::Vector& z) const override { P_.apply(r, z); }
+    bool is_linear() const override { return true; }
+    bool is_symmetric() const override { return false; }
+    npsd::index_t size() const override { return map_.reduced_size(); }
+    std::string name() const override { return "neural3d"; }
+
+private:
+    npsdo::ReductionMap map_;
+    npsdo::NeuralPrecond<3> P_;
+};
+
+typedef int (*apply_cb)(void* user, const double* r, double* z, long n);
+
+class CallbackPrecond : public npsd::Preconditioner {
+public:
+    CallbackPrecond(apply_cb fn, void* user, long n) : fn_(fn), user_(user), n_(n) {}
+    using Preconditioner::apply;
+    void apply(const npsd::Vector& r, npsd::Vector& z) const override {
+        z.assign(r.size(), 0.0);
+        if (fn_(user_, r.data(), z.data(), static_cast<long>(r.size())) != 0)
+            throw std::runtime_error("callback preconditioner failed");
+    }
+    bool is_linear() const override { return true; }
+    bool is_symmetric() const override { return false; }
+    npsd::index_t size() const override { return n_; }
+    std::string name() const override { return "callback"; }
+
+private:
+    apply_cb fn_;
+    void* user_;
+    long n_;
+};
+
+npsd::SparseMatrix assemble(int dim, long nx, long ny, long nz, const npsd::IndicatorImage& I,
+                            const unsigned char* types) {
+    if (dim == 2) return npsd::assemble_poisson(I);
+    npsd::IndicatorVolume V(nx, ny, nz);
+    for (long i = 0; i < nx * ny * nz; ++i) V.cells[static_cast<std::size_t>(i)] = static_cast<npsd::CellType>(types[i]);
+    return npsd::assemble_poisson_3d(V);
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_rhs_normal(unsigned long long seed, long n, double* out) {
+    npsd::Rng rng(seed);
+    for (long i = 0; i < n; ++i) out[i] = rng.normal();
+}
+
+int ref_init_params_2d(int depth, unsigned long long seed, float* out) {
+    return guarded([&] {
+        const auto p = npsd::net::init_params(depth, seed);
+        std::size_t o = 0;
+        p.for_each_span([&](const float* src, std::size_t k) {
+            std::memcpy(out + o, src, k * sizeof(float));
+            o += k;
+        });
+    });
+}
+
+// PaddedImage::pooled chain interiors (3 planes per level)
+int ref_level_images_2d(long nx, long ny, int depth, const unsigned char* types, float* out) {
+    return guarded([&] {
+        auto img = npsd::net::PaddedImage<float>::from_image(image_from_types(nx, ny, types));
+        std::size_t o = 0;
+        for (int l = 0; l < depth; ++l) {
+            for (int c = 0; c < 3; ++c)
+                for (long y = 0; y < img.ny; ++y)
+                    for (long x = 0; x < img.nx; ++x) out[o++] = img.at(c, x, y);
+            if (l + 1 < depth) img = img.pooled();
+        }
+    });
+}
+
+int ref_net_apply_2d(long nx, long ny, int depth, const float* params, long n_params, const unsigned char* types,
+                     const float* x, float* y, float* za, float* zb) {
+    return guarded([&] {
+        const auto p = params_2d(depth, params, n_params);
+        const auto ctx = npsd::net::NetContext<float>::build(p, image_from_types(nx, ny, types));
+        npsd::Field2D<float> f(nx, ny);
+        std::memcpy(f.data.data(), x, sizeof(float) * static_cast<std::size_t>(nx * ny));
+        const auto out = ctx.apply(f);
+        std::memcpy(y, out.data.data(), sizeof(float) * static_cast<std::size_t>(nx * ny));
+        for (int l = 0; l + 1 < depth; ++l) {
+            if (za) za[l] = ctx.levels[static_cast<std::size_t>(l)].z_a;
+            if (zb) zb[l] = ctx.levels[static_cast<std::size_t>(l)].z_b;
+        }
+    });
+}
+
+int ref_precond_apply_2d(long nx, long ny, int depth, const float* params, long n_params, const unsigned char* types,
+                         const double* r, double* z) {
+    return guarded([&] {
+        const auto I = image_from_types(nx, ny, types);
+        const auto map = npsd::ReductionMap::from_image(I);
+        npsd::net::NeuralPrecond P(params_2d(depth, params, n_params), I, map);
+        npsd::Vector rv(r, r + map.reduced_size()), zv;
+        P.apply(rv, zv);
+        std::memcpy(z, zv.data(), sizeof(double) * zv.size());
+    });
+}
+
+int ref_spmv(int dim, long nx, long ny, long nz, const unsigned char* types, const double* x, double* y) {
+    return guarded([&] {
+        const long rows = (dim == 3) ? ny * nz : ny;
+        const auto I = image_from_types(nx, rows, types);
+        const auto A = assemble(dim, nx, ny, nz, I, types);
+        const auto sys = npsd::reduce(A, npsd::Vector(static_cast<std::size_t>(A.n_rows), 0.0), I);
+        npsd::Vector xv(x, x + sys.A.n_rows), yv;
+        npsd::spmv(sys.A, xv, yv);
+        std::memcpy(y, yv.data(), sizeof(double) * yv.size());
+    });
+}
+
+// Reference psdo_solve (solver.cpp:189-276) on the reference assembly.
+//   mode 0: IdentityPrecond
+//   mode 1: neural — 2D: reference NeuralPrecond; 3D: NeuralPrecond3D restatement
+//   mode 2: C callback preconditioner (a B200 NeuralPrecond through the C ABI)
+// seconds[0] = setup (assembly + reduce + preconditioner build), seconds[1] = solve.
+int ref_psdo_solve(int dim, long nx, long ny, long nz, const unsigned char* types, int mode, int depth,
+                   const float* params, long n_params, apply_cb cb, void* cb_user, const double* b,
+                   const double* x0, double tol_reduction, double tol_abs, long max_iters, int n_ortho,
+                   int nullspace_projection, int normalize_before_precond, double* x_out, double* hist,
+                   long* iterations, int* converged, long* hist_len, double* seconds) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        const long rows = (dim == 3) ? ny * nz : ny;
+        const auto I = image_from_types(nx, rows, types);
+        const auto A = assemble(dim, nx, ny, nz, I, types);
+        const auto sys = npsd::reduce(A, npsd::Vector(static_cast<std::size_t>(A.n_rows), 0.0), I);
+        std::unique_ptr<npsd::Preconditioner> P;
+        if (mode == 0) {
+            P = npsd::identity_precond(sys.A.n_rows);
+        } else if (mode == 1) {
+            if (dim == 2)
+                P = npsd::net::neural_precond(params_2d(depth, params, n_params), I, sys.map);
+            else
+                P = std::make_unique<NeuralPrecond3D>(npsdo::params_from_flat(3, depth, params, static_cast<std::size_t>(n_params)),
+                                                      types, npsdo::Dims{nx, ny, nz});
+        } else {
+            P = std::make_unique<CallbackPrecond>(cb, cb_user, sys.A.n_rows);
+        }
+        const auto t1 = std::chrono::steady_clock::now();
+        npsd::SolveConfig cfg;
+        cfg.tol_reduction = tol_reduction;
+        cfg.tol_abs = tol_abs;
+        cfg.max_iters = max_iters;
+        cfg.n_ortho = n_ortho;
+        cfg.nullspace_projection = nullspace_projection != 0;
+        cfg.normalize_before_precond = normalize_before_precond != 0;
+        const std::size_t nf = static_cast<std::size_t>(sys.A.n_rows);
+        npsd::Vector bv(b, b + nf), x0v;
+        if (x0) x0v.assign(x0, x0 + nf);
+        const auto res = npsd::psdo_solve(sys.A, bv, *P, cfg, x0 ? &x0v : nullptr);
+        const auto t2 = std::chrono::steady_clock::now();
+        std::memcpy(x_out, res.x.data(), nf * sizeof(double));
+        for (std::size_t i = 0; i < res.report.residual_history.size(); ++i) hist[i] = res.report.residual_history[i];
+        *iterations = static_cast<long>(res.report.iterations);
+        *converged = res.report.converged ? 1 : 0;
+        *hist_len = static_cast<long>(res.report.residual_history.size());
+        if (seconds) {
+            seconds[0] = std::chrono::duration<double>(t1 - t0).count();
+            seconds[1] = std::chrono::duration<double>(t2 - t1).count();
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,414 @@
+"""B200-native neural-preconditioned PSDO ("DCDM") Poisson solve.
+
+Host-side mirror of the reference's solver / preconditioner interface
+(/root/reference/proj/include/npsd/{solver,precond}.hpp, net/precond.hpp) over
+the C ABI in include/npsd_b200.h (libnpsd_b200.so, hand-written sm_100a CUDA).
+Names, argument meaning and error behaviour follow the reference:
+
+    SolveConfig / SolveReport / SolveResult   solver.hpp:11-42
+    NeuralPrecond, neural_precond            net/precond.hpp:14-33
+    psdo_solve, psd_solve                     solver.hpp:64-69
+    init_params                               net/params.hpp:102 (net_params.cpp:11-35)
+    std::invalid_argument -> ValueError, SolverBreakdown, EmptySystemError
+
+There is no CPU fallback: every call runs on the GPU through the C ABI and
+raises if the library or the device is unavailable.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from ._native import NPSD_BREAKDOWN, NPSD_CUDA_ERROR, NPSD_EMPTY_SYSTEM, NPSD_INVALID_ARGUMENT, NPSD_OK
+
+__all__ = [
+    "SolveConfig", "SolveReport", "SolveResult", "SolverBreakdown", "EmptySystemError", "DeviceError",
+    "NetParams", "init_params", "identity_params", "param_count", "rhs_normal", "Context", "NeuralPrecond",
+    "neural_precond", "psdo_solve", "psd_solve", "DeviceBuffer", "PinnedBuffer",
+]
+
+
+class SolverBreakdown(RuntimeError):
+    """types.hpp:19-22 — curvature d'Ad non-positive or underflowed."""
+
+
+class EmptySystemError(RuntimeError):
+    """types.hpp:25-28 — the image has no fluid cells."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure (no CPU fallback exists)."""
+
+
+def _raise(status: int, msg: str) -> None:
+    if status == NPSD_OK:
+        return
+    if status == NPSD_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == NPSD_BREAKDOWN:
+        raise SolverBreakdown(msg)
+    if status == NPSD_EMPTY_SYSTEM:
+        raise EmptySystemError(msg)
+    raise DeviceError(msg)
+
+
+# ------------------------------------------------------------------ config
+@dataclass
+class SolveConfig:
+    """solver.hpp:11-26."""
+    tol_reduction: float = 1e-6
+    tol_abs: float = 0.0
+    max_iters: int = 1000
+    n_ortho: int = 2
+    nullspace_projection: bool = False
+    normalize_before_precond: bool = True
+
+    def _c(self) -> _native.SolveCfg:
+        return _native.SolveCfg(float(self.tol_reduction), float(self.tol_abs), int(self.max_iters),
+                                int(self.n_ortho), int(bool(self.nullspace_projection)),
+                                int(bool(self.normalize_before_precond)), 0)
+
+
+@dataclass
+class SolveReport:
+    """solver.hpp:28-37."""
+    iterations: int = 0
+    converged: bool = False
+    residual_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    cumulative_seconds: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    setup_seconds: float = 0.0
+    iterate_seconds: float = 0.0
+    precond_seconds: float = 0.0
+    method: str = ""
+
+
+@dataclass
+class SolveResult:
+    """solver.hpp:39-42."""
+    x: np.ndarray
+    report: SolveReport
+
+
+# ----------------------------------------------------------------- weights
+@dataclass
+class NetParams:
+    """Flat f32 weights in for_each_span order (net/params.hpp:66-80)."""
+    dim: int
+    depth: int
+    flat: np.ndarray
+
+    def parameter_count(self) -> int:
+        return param_count(self.dim, self.depth)
+
+
+def param_count(dim: int, depth: int) -> int:
+    n = int(_native.lib().npsd_b200_param_count(dim, depth))
+    if n == 0:
+        raise ValueError("param_count: dim must be 2 or 3 and depth >= 1")
+    return n
+
+
+def init_params(depth: int, seed: int, dim: int = 3) -> NetParams:
+    """init_params (net_params.cpp:11-35), generalised to 3D."""
+    out = np.empty(param_count(dim, depth), np.float32)
+    _raise(_native.lib().npsd_b200_init_params(dim, depth, seed, out), "init_params: bad dim/depth")
+    return NetParams(dim, depth, out)
+
+
+def identity_params(depth: int, dim: int = 3) -> NetParams:
+    """Identity-equivalent weights: the network returns its input (PSDO == CG)."""
+    out = np.empty(param_count(dim, depth), np.float32)
+    _raise(_native.lib().npsd_b200_identity_params(dim, depth, out), "identity_params: bad dim/depth")
+    return NetParams(dim, depth, out)
+
+
+def rhs_normal(seed: int, n: int) -> np.ndarray:
+    """Rng(seed).normal() x n (rng.hpp:36-48)."""
+    out = np.empty(n, np.float64)
+    _native.lib().npsd_b200_rhs_normal(seed, n, out)
+    return out
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One B200 context: grid, weights and (after set_mask) one frame."""
+
+    def __init__(self, dim: int, shape: tuple, params: NetParams, device: int = 0) -> None:
+        if dim == 3:
+            nz, ny, nx = shape
+        else:
+            (ny, nx), nz = shape, 1
+        if params.dim != dim:
+            raise ValueError("NeuralPrecond: params dim does not match the grid")
+        self.lib = _native.lib()
+        self.dim, self.nx, self.ny, self.nz, self.depth = dim, nx, ny, nz, params.depth
+        self.shape = tuple(shape)
+        self.n_cells = nx * ny * nz
+        h = C.c_void_p()
+        dev = (C.c_int * 1)(device)
+        flat = np.ascontiguousarray(params.flat, np.float32)
+        st = self.lib.npsd_b200_create(dim, nx, ny, nz, params.depth, flat, flat.size, C.cast(dev, C.c_void_p), 1,
+                                       C.byref(h))
+        if st != NPSD_OK:
+            _raise(st, self.lib.npsd_b200_last_error(None).decode())
+        self.h = h
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.npsd_b200_destroy(self.h)
+            self.h = None
+
+    def __del__(self) -> None:
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, st: int) -> None:
+        if st != NPSD_OK:
+            _raise(st, self.lib.npsd_b200_last_error(self.h).decode())
+
+    # per frame
+    def set_params(self, params: NetParams) -> None:
+        flat = np.ascontiguousarray(params.flat, np.float32)
+        self._ck(self.lib.npsd_b200_set_params(self.h, flat, flat.size))
+
+    def set_mask(self, types: np.ndarray) -> None:
+        t = np.ascontiguousarray(types, np.uint8).reshape(-1)
+        if t.size != self.n_cells:
+            raise ValueError("set_mask: cell type array does not match the grid")
+        self._ck(self.lib.npsd_b200_set_mask(self.h, t))
+
+    def set_mask_device(self, ptr: int) -> None:
+        self._ck(self.lib.npsd_b200_set_mask_device(self.h, C.c_void_p(ptr)))
+
+    @property
+    def n_fluid(self) -> int:
+        return int(self.lib.npsd_b200_n_fluid(self.h))
+
+    def fluid_indices(self) -> np.ndarray:
+        out = np.empty(self.n_fluid, np.int64)
+        self._ck(self.lib.npsd_b200_fluid_indices(self.h, out))
+        return out
+
+    # operators
+    def precond_apply(self, r: np.ndarray) -> np.ndarray:
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        self._ck(self.lib.npsd_b200_precond_apply(self.h, r, z, r.size))
+        return z
+
+    def spmv(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty_like(x)
+        self._ck(self.lib.npsd_b200_spmv(self.h, x, y, x.size))
+        return y
+
+    def net_apply(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float32).reshape(-1)
+        if x.size != self.n_cells:
+            raise ValueError("NetContext::apply: field shape mismatch")
+        y = np.empty_like(x)
+        self._ck(self.lib.npsd_b200_net_apply(self.h, x, y))
+        return y.reshape(self.shape)
+
+    def level_image(self, level: int) -> np.ndarray:
+        nx, ny = self.nx >> level, self.ny >> level
+        nz = (self.nz >> level) if self.dim == 3 else 1
+        out = np.empty(3 * nx * ny * nz, np.float32)
+        self._ck(self.lib.npsd_b200_level_image(self.h, level, out))
+        return out.reshape((3, nz, ny, nx) if self.dim == 3 else (3, ny, nx))
+
+    def linear_coeffs(self) -> tuple[np.ndarray, np.ndarray]:
+        za = np.zeros(max(self.depth - 1, 1), np.float32)
+        zb = np.zeros_like(za)
+        self._ck(self.lib.npsd_b200_linear_coeffs(self.h, za, zb))
+        return za[: self.depth - 1], zb[: self.depth - 1]
+
+    def mixed_counts(self) -> np.ndarray:
+        out = np.zeros(self.depth, np.int64)
+        self._ck(self.lib.npsd_b200_mixed_counts(self.h, out))
+        return out
+
+    def _report(self, rep: _native.Report, method: str) -> SolveReport:
+        n = int(rep.history_len)
+        hist = np.ctypeslib.as_array(rep.residual_history, shape=(n,)).copy() if n else np.zeros(0)
+        secs = np.ctypeslib.as_array(rep.cumulative_seconds, shape=(n,)).copy() if n else np.zeros(0)
+        return SolveReport(int(rep.iterations), bool(rep.converged), hist, secs, float(rep.setup_seconds),
+                           float(rep.iterate_seconds), float(rep.precond_seconds), method)
+
+    def psdo_solve(self, b: np.ndarray, cfg: SolveConfig, x0: np.ndarray | None = None,
+                   method: str = "psdo+neural") -> SolveResult:
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.empty_like(b)
+        rep = _native.Report()
+        x0p = None
+        if x0 is not None:
+            x0a = np.ascontiguousarray(x0, np.float64)
+            if x0a.size != b.size:
+                raise ValueError("solve: x0 length mismatch")
+            x0p = x0a.ctypes.data_as(C.c_void_p)
+        if b.size != self.n_fluid:
+            raise ValueError("solve: rhs length mismatch")
+        c = cfg._c()
+        st = self.lib.npsd_b200_psdo_solve(self.h, b, x0p, C.byref(c), x, C.byref(rep))
+        if st == NPSD_BREAKDOWN:
+            _raise(st, self.lib.npsd_b200_last_error(self.h).decode())
+        self._ck(st)
+        return SolveResult(x, self._report(rep, method))
+
+    def psdo_solve_device(self, b_ptr: int, x_ptr: int, cfg: SolveConfig, x0_ptr: int | None = None,
+                          method: str = "psdo+neural") -> SolveReport:
+        rep = _native.Report()
+        c = cfg._c()
+        self._ck(self.lib.npsd_b200_psdo_solve_device(self.h, C.c_void_p(b_ptr),
+                                                      C.c_void_p(x0_ptr) if x0_ptr else None, C.byref(c),
+                                                      C.c_void_p(x_ptr), C.byref(rep)))
+        return self._report(rep, method)
+
+    def synchronize(self) -> None:
+        self._ck(self.lib.npsd_b200_synchronize(self.h))
+
+    @property
+    def last_solve_ms(self) -> float:
+        return float(self.lib.npsd_b200_last_solve_ms(self.h))
+
+    @property
+    def last_solve_launches(self) -> int:
+        return int(self.lib.npsd_b200_last_solve_launches(self.h))
+
+
+class DeviceBuffer:
+    """Raw device allocation owned by a Context (cudaMalloc through the C ABI)."""
+
+    def __init__(self, ctx: Context, nbytes: int) -> None:
+        self.ctx, self.nbytes = ctx, int(nbytes)
+        p = C.c_void_p()
+        ctx._ck(ctx.lib.npsd_b200_device_alloc(ctx.h, self.nbytes, C.byref(p)))
+        self.ptr = int(p.value)
+
+    def upload(self, src: np.ndarray | "PinnedBuffer") -> None:
+        sp = src.ptr if isinstance(src, PinnedBuffer) else np.ascontiguousarray(src).ctypes.data
+        self.ctx._ck(self.ctx.lib.npsd_b200_memcpy(self.ctx.h, C.c_void_p(self.ptr), C.c_void_p(sp), self.nbytes))
+
+    def download(self, dst: np.ndarray | "PinnedBuffer") -> None:
+        dp = dst.ptr if isinstance(dst, PinnedBuffer) else dst.ctypes.data
+        self.ctx._ck(self.ctx.lib.npsd_b200_memcpy(self.ctx.h, C.c_void_p(dp), C.c_void_p(self.ptr), self.nbytes))
+
+    def free(self) -> None:
+        if self.ptr:
+            self.ctx.lib.npsd_b200_device_free(self.ctx.h, C.c_void_p(self.ptr))
+            self.ptr = 0
+
+
+class PinnedBuffer:
+    """Page-locked host memory (cudaMallocHost) viewed as a numpy array."""
+
+    def __init__(self, ctx: Context, n: int, dtype=np.float64) -> None:
+        self.ctx = ctx
+        self.dtype = np.dtype(dtype)
+        self.nbytes = int(n) * self.dtype.itemsize
+        p = C.c_void_p()
+        ctx._ck(ctx.lib.npsd_b200_host_alloc(ctx.h, self.nbytes, C.byref(p)))
+        self.ptr = int(p.value)
+        buf = (C.c_char * self.nbytes).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=self.dtype, count=int(n))
+
+    def free(self) -> None:
+        if self.ptr:
+            self.array = None
+            self.ctx.lib.npsd_b200_host_free(self.ctx.h, C.c_void_p(self.ptr))
+            self.ptr = 0
+
+
+# -------------------------------------------------------- preconditioner API
+class NeuralPrecond:
+    """net::NeuralPrecond (net/precond.hpp:14-30) on a B200.
+
+    ``image`` is the cell-type grid (0 fluid, 1 air, 2 solid), shape (ny, nx)
+    or (nz, ny, nx). The optional ``map`` (fluid linear indices) is validated
+    against the image like the reference ctor (net_precond.cpp:11).
+    """
+
+    def __init__(self, params: NetParams, image: np.ndarray, map: np.ndarray | None = None, device: int = 0):
+        image = np.asarray(image)
+        dim = 3 if image.ndim == 3 else 2
+        self.ctx = Context(dim, image.shape, params, device)
+        self.ctx.set_mask(image)
+        if map is not None:
+            m = np.asarray(map, np.int64)
+            if m.size != self.ctx.n_fluid or not np.array_equal(m, self.ctx.fluid_indices()):
+                raise ValueError("NeuralPrecond: map does not match image")
+
+    def apply(self, r: np.ndarray, z: np.ndarray | None = None) -> np.ndarray:
+        r = np.asarray(r, np.float64)
+        if r.size != self.size():
+            raise ValueError("NeuralPrecond::apply: size mismatch")
+        out = self.ctx.precond_apply(r)
+        if z is not None:
+            z[...] = out
+            return z
+        return out
+
+    __call__ = apply
+
+    def is_linear(self) -> bool:
+        return True
+
+    def is_symmetric(self) -> bool:
+        return False
+
+    def size(self) -> int:
+        return self.ctx.n_fluid
+
+    def name(self) -> str:
+        return "neural"
+
+
+def neural_precond(params: NetParams, image: np.ndarray, map: np.ndarray | None = None) -> NeuralPrecond:
+    """net/precond.hpp:32-33."""
+    return NeuralPrecond(params, image, map)
+
+
+def _rows(A) -> int | None:
+    if A is None:
+        return None
+    for attr in ("n_rows", "shape"):
+        if hasattr(A, attr):
+            v = getattr(A, attr)
+            return int(v[0]) if isinstance(v, tuple) else int(v)
+    return None
+
+
+def psdo_solve(A, b: np.ndarray, P: NeuralPrecond, cfg: SolveConfig | None = None,
+               x0: np.ndarray | None = None) -> SolveResult:
+    """psdo_solve (solver.hpp:64-65, solver.cpp:189-276) on the B200.
+
+    The operator is matrix-free: it is the mixed-BC Laplacian that
+    assemble_poisson[_3d] + reduce would build from P's image, so ``A`` is only
+    checked for its size (pass None to skip). P must be a B200 NeuralPrecond.
+    """
+    cfg = cfg or SolveConfig()
+    if not isinstance(P, NeuralPrecond):
+        raise ValueError("psdo_solve (B200): P must be a B200 NeuralPrecond; there is no CPU path")
+    n = _rows(A)
+    if n is not None and n != P.size():
+        raise ValueError("solve: matrix not square / rhs length mismatch")
+    b = np.asarray(b, np.float64)
+    if b.size != P.size():
+        raise ValueError("solve: rhs length mismatch")
+    if not np.all(np.isfinite(b)):
+        raise ValueError("solve: rhs has non-finite entries")
+    return P.ctx.psdo_solve(b, cfg, x0, method="psdo+" + P.name())
+
+
+def psd_solve(A, b: np.ndarray, P: NeuralPrecond, cfg: SolveConfig | None = None,
+              x0: np.ndarray | None = None) -> SolveResult:
+    """PSDO with n_ortho forced to 0 (solver.hpp:68-69)."""
+    cfg = SolveConfig(**{**(cfg or SolveConfig()).__dict__, "n_ortho": 0})
+    res = psdo_solve(A, b, P, cfg, x0)
+    res.report.method = "psd+" + P.name()
+    return res

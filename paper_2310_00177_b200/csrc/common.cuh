@@ -1,0 +1,152 @@
+// Shared device-side definitions for the B200 neural-preconditioned PSDO solve.
+//
+// Bitwise rule: every floating-point operation that the reference performs in
+// its network (net/kernels.hpp, net/forward.hpp) and in its stencil
+// (sparse.cpp:100-117) is issued here as an explicit round-to-nearest
+// intrinsic (__fmul_rn/__fadd_rn, __dmul_rn/__dadd_rn) in the reference's
+// order, so the compiler can never contract it into an FMA. The network and
+// the operator are therefore bit-identical to the CPU restatement; only the
+// tree-ordered dot products differ from the reference's serial loops.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nb2 {
+
+constexpr int kMaxOrtho = 8;            // n_ortho supported on device
+constexpr int kRing = kMaxOrtho + 1;    // cache slots + the direction being built
+constexpr int kMaxDepth = 8;
+constexpr int kBlock = 256;             // threads per block for all kernels
+
+// Level geometry. nz == 1 for 2D.
+struct Geom {
+    int nx, ny, nz;
+    long long n;
+};
+
+__host__ __device__ inline Geom make_geom(int nx, int ny, int nz) {
+    Geom g;
+    g.nx = nx;
+    g.ny = ny;
+    g.nz = nz;
+    g.n = (long long)nx * ny * nz;
+    return g;
+}
+
+__host__ __device__ __forceinline__ long long lin(const Geom& g, int x, int y, int z) {
+    return ((long long)z * g.ny + y) * g.nx + x;
+}
+
+template <int D>
+struct Sh {
+    static constexpr int S = (D == 3) ? 27 : 9;  // slots (== window cells)
+    static constexpr int BZ = (D == 3) ? 2 : 1;  // brick extent along z
+    static constexpr int WZ = (D == 3) ? 4 : 1;  // 2-brick window planes along z
+    static constexpr int CW = (D == 3) ? 3 : 1;  // coarse window planes along z
+    static constexpr int NB = (D == 3) ? 6 : 4;  // stencil neighbours
+};
+
+// L0 cell byte: bits 0-1 window class (0/1/2 = uniform fluid/air/solid window,
+// 3 = mixed), bits 2-3 own cell type, bits 4-6 stencil diagonal (# non-solid
+// in-domain face neighbours). Coarse levels use bits 0-1 only.
+__device__ __forceinline__ int cls_window(uint8_t b) { return b & 3; }
+__device__ __forceinline__ int cls_type(uint8_t b) { return (b >> 2) & 3; }
+__device__ __forceinline__ int cls_diag(uint8_t b) { return (b >> 4) & 7; }
+
+// Mixed-cell table index from 32-cell segment masks and exclusive bases.
+__device__ __forceinline__ long long mixed_index(const uint32_t* __restrict__ mmask,
+                                                 const uint32_t* __restrict__ mbase, long long c) {
+    const long long seg = c >> 5;
+    const uint32_t bit = (uint32_t)(c & 31);
+    return (long long)mbase[seg] + __popc(mmask[seg] & ((1u << bit) - 1u));
+}
+
+// Device-resident solver state (one per context). Written only by the last
+// block of a reducing kernel; read by every later kernel.
+struct SolverState {
+    // configuration (host-written before each solve)
+    double tol_reduction, tol_abs;
+    long long max_iters;
+    int n_ortho, normalize, nullspace;
+    int ring;  // n_ortho + 1
+    // iteration
+    long long k;      // iteration being computed (1-based)
+    int n_cache;      // valid cached directions
+    int head;         // ring slot of the newest cached direction
+    int done, converged, breakdown;
+    int xcur;         // which x buffer holds the current iterate
+    double rnorm, thr;
+    double inv1, inv2, nrm;         // network input scales / output multiplier
+    double p[kMaxOrtho];            // MGS projections of the current direction
+    double dAd[kRing];              // per ring slot: d'Ad
+    double cross[kRing][kRing];     // cross[i][j] = d_i . A d_j (i older than j)
+    double dAd_new, rd_new, alpha;  // for the direction being built
+    double mean;                    // nullspace projection mean
+    double bad_value;               // curvature at breakdown
+    unsigned long long t0;          // %globaltimer at solve start
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic grid reduction: each block reduces NV doubles (fixed tree),
+// writes them to partials[j * gridDim.x + block]; the last block to arrive sums
+// the partials in block order and returns true with the totals in `tot`.
+// Grid size is fixed per kernel and context, so results are run-to-run
+// bitwise reproducible.
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ bool grid_reduce(double (&v)[NV], double* __restrict__ partials,
+                                            unsigned int* __restrict__ counter, double (&tot)[NV]) {
+    __shared__ double sred[kBlock / 32][NV];
+    __shared__ bool s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        double a = v[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) sred[warp][j] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double a = 0.0;
+#pragma unroll
+        for (int w = 0; w < kBlock / 32; ++w) a += sred[w][threadIdx.x];
+        partials[(long long)threadIdx.x * gridDim.x + blockIdx.x] = a;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int ticket = atomicAdd(counter, 1u);
+        s_last = (ticket == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    // last block: deterministic sum over blocks
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        double a = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += kBlock) a += __ldcg(partials + (long long)j * gridDim.x + b);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) sred[warp][j] = a;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        double a = 0.0;
+        for (int w = 0; w < kBlock / 32; ++w) a += sred[w][j];
+        tot[j] = a;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    return true;
+}
+
+}  // namespace nb2

@@ -1,0 +1,929 @@
+// npsd_b200.cu — context, per-frame setup, network and PSDO solve behind the
+// C ABI in include/npsd_b200.h. One context per GPU; everything after
+// set_mask stays in HBM; the PSDO loop is one CUDA graph whose body (one
+// iteration: 2*depth-1 network kernels + ortho + update) repeats under a
+// device-side conditional WHILE node, so the host never synchronises inside
+// the solve.
+#include <cub/device/device_scan.cuh>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/npsd_b200.h"
+#include "common.cuh"
+#include "net.cuh"
+#include "psdo.cuh"
+#include "setup.cuh"
+
+using namespace nb2;
+
+namespace {
+
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+struct InvalidArgument : std::runtime_error {
+    explicit InvalidArgument(const std::string& w) : std::runtime_error(w) {}
+};
+struct Breakdown : std::runtime_error {
+    explicit Breakdown(const std::string& w) : std::runtime_error(w) {}
+};
+struct EmptySystem : std::runtime_error {
+    explicit EmptySystem(const std::string& w) : std::runtime_error(w) {}
+};
+
+#define CK(call)                                                                                      \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess)                                                                        \
+            throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                            std::to_string(__LINE__) + ")");                                          \
+    } while (0)
+
+inline void require(bool c, const std::string& m) {
+    if (!c) throw InvalidArgument(m);
+}
+
+thread_local std::string g_create_err;
+
+struct LevelBufs {
+    Geom g{};
+    long long nseg = 0;
+    uint8_t* cls = nullptr;
+    uint32_t *mmask = nullptr, *mbase = nullptr, *mcount = nullptr;
+    float* img = nullptr;  // 3 planes (levels >= 1)
+    float *tab_down = nullptr, *tab_up = nullptr;
+    float *kc_down = nullptr, *kc_up = nullptr;  // [3][S]
+    float *y = nullptr, *x = nullptr, *out = nullptr;
+    unsigned long long* zG = nullptr;
+};
+
+// offsets of one level's blocks inside the flat parameter vector
+struct LevelOffsets {
+    size_t down_W, down_B, up_W, up_B, a_K, a_bias, b_K, b_bias;
+};
+
+}  // namespace
+
+struct npsd_b200_ctx {
+    int dim = 3, depth = 1, S = 27, dev = 0, num_sms = 148;
+    Geom g0{};
+    cudaStream_t s = nullptr, s2 = nullptr;
+    std::vector<float> params;
+    std::vector<LevelOffsets> offs;
+    size_t coarse_W = 0, coarse_B = 0;
+    float* d_params = nullptr;
+    LevelBufs L[kMaxDepth];
+    float* zab = nullptr;  // [depth][2]
+    uint32_t *fmask = nullptr, *fbase = nullptr, *fcount = nullptr;
+    long long n_fluid = 0;
+    bool mask_ok = false;
+    // solver
+    double *X0 = nullptr, *X1 = nullptr, *R = nullptr, *Bf = nullptr, *Dtmp = nullptr;
+    double *Dring = nullptr, *ADring = nullptr;
+    int ring_alloc = 0;
+    SolverState* st = nullptr;
+    SolverState* st_host = nullptr;  // pinned
+    double* partials = nullptr;
+    unsigned int* counter = nullptr;
+    double *hist = nullptr, *times = nullptr;
+    long long hist_cap = 0;
+    double *hist_host = nullptr, *times_host = nullptr;
+    long long hist_host_cap = 0;
+    double *red_a = nullptr, *red_b = nullptr;
+    float *xin_f = nullptr, *out_f = nullptr;  // raw-network buffers (lazy)
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    // solve graph
+    cudaGraphExec_t exec = nullptr;
+    const void* exec_key[4] = {nullptr, nullptr, nullptr, nullptr};
+    int exec_nullspace = -1;
+    int body_launches = 0, prologue_launches = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    float last_ms = 0.0f;
+    long long last_launches = 0;
+    std::vector<double> report_hist, report_times;
+    std::mutex mu;
+    std::string err;
+};
+
+namespace {
+
+template <typename T>
+T* dalloc(size_t n) {
+    T* p = nullptr;
+    if (n == 0) n = 1;
+    CK(cudaMalloc(&p, n * sizeof(T)));
+    return p;
+}
+
+template <typename K>
+int grid_for(npsd_b200_ctx* c, K kernel, long long items) {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBlock, 0));
+    if (occ < 1) occ = 1;
+    const long long want = (items + kBlock - 1) / kBlock;
+    long long g = (long long)c->num_sms * occ;
+    if (want < g) g = want;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+#define LAUNCH(c, stream, kernel, items, ...)                                \
+    do {                                                                     \
+        auto kfn_ = kernel;                                                  \
+        const int g_ = grid_for(c, kfn_, (items));                          \
+        kfn_<<<g_, kBlock, 0, (stream)>>>(__VA_ARGS__);                      \
+        CK(cudaGetLastError());                                              \
+    } while (0)
+
+Geom level_geom(const npsd_b200_ctx* c, int l) {
+    return make_geom(c->g0.nx >> l, c->g0.ny >> l, (c->dim == 3) ? (c->g0.nz >> l) : 1);
+}
+
+void compute_offsets(npsd_b200_ctx* c) {
+    const size_t S = (size_t)c->S, WN = S * 3 * S, KN = 3 * S;
+    size_t o = 0;
+    c->offs.assign((size_t)c->depth - 1, LevelOffsets{});
+    for (auto& lo : c->offs) {
+        lo.down_W = o;
+        o += WN;
+        lo.down_B = o;
+        o += S;
+        lo.up_W = o;
+        o += WN;
+        lo.up_B = o;
+        o += S;
+        lo.a_K = o;
+        o += KN;
+        lo.a_bias = o;
+        o += 1;
+        lo.b_K = o;
+        o += KN;
+        lo.b_bias = o;
+        o += 1;
+    }
+    c->coarse_W = o;
+    o += WN;
+    c->coarse_B = o;
+}
+
+size_t param_count_impl(int dim, int depth) {
+    const size_t S = (dim == 3) ? 27 : 9;
+    const size_t conv = S * 3 * S + S, lin = 3 * S + 1;
+    return (size_t)(depth - 1) * (2 * conv + 2 * lin) + conv;
+}
+
+void scan_u32(npsd_b200_ctx* c, const uint32_t* in, uint32_t* out, long long n) {
+    size_t bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, c->s));
+    if (bytes > c->cub_bytes) {
+        if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
+        CK(cudaMalloc(&c->cub_tmp, bytes));
+        c->cub_bytes = bytes;
+    }
+    CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, in, out, (int)n, c->s));
+}
+
+template <int D>
+void upload_params_and_kconst(npsd_b200_ctx* c) {
+    CK(cudaMemcpyAsync(c->d_params, c->params.data(), c->params.size() * sizeof(float), cudaMemcpyHostToDevice, c->s));
+    for (int l = 0; l < c->depth; ++l) {
+        LevelBufs& L = c->L[l];
+        if (l < c->depth - 1) {
+            const LevelOffsets& o = c->offs[(size_t)l];
+            k_kconst<D><<<1, 96, 0, c->s>>>(c->d_params + o.down_W, c->d_params + o.down_B, L.kc_down);
+            k_kconst<D><<<1, 96, 0, c->s>>>(c->d_params + o.up_W, c->d_params + o.up_B, L.kc_up);
+        } else {
+            k_kconst<D><<<1, 96, 0, c->s>>>(c->d_params + c->coarse_W, c->d_params + c->coarse_B, L.kc_down);
+        }
+        CK(cudaGetLastError());
+    }
+}
+
+ConvTab tab_down(const npsd_b200_ctx* c, int l) {
+    const LevelBufs& L = c->L[l];
+    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_down, L.g.n, L.kc_down};
+}
+ConvTab tab_up(const npsd_b200_ctx* c, int l) {
+    const LevelBufs& L = c->L[l];
+    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_up, L.g.n, L.kc_up};
+}
+
+// ---------------------------------------------------------------- set_mask
+template <int D>
+void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
+    cudaStream_t s = c->s;
+    LevelBufs& L0 = c->L[0];
+    LAUNCH(c, s, k_setup_l0<D>, c->g0.n, c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
+    scan_u32(c, L0.mcount, L0.mbase, L0.nseg);
+    scan_u32(c, c->fcount, c->fbase, L0.nseg);
+    for (int l = 1; l < c->depth; ++l) {
+        LevelBufs& Lf = c->L[l - 1];
+        LevelBufs& Lc = c->L[l];
+        LAUNCH(c, s, k_pool_image<D>, Lc.g.n, Lf.g, Lc.g, (l == 1) ? dtypes : nullptr, (l == 1) ? nullptr : Lf.img,
+               Lc.img);
+        LAUNCH(c, s, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
+        scan_u32(c, Lc.mcount, Lc.mbase, Lc.nseg);
+    }
+    for (int l = 0; l < c->depth; ++l) {
+        LevelBufs& L = c->L[l];
+        const uint8_t* st = (l == 0) ? dtypes : nullptr;
+        const float* im = (l == 0) ? nullptr : L.img;
+        if (l < c->depth - 1) {
+            const LevelOffsets& o = c->offs[(size_t)l];
+            LAUNCH(c, s, k_build_table<D>, L.g.n, L.g, st, im, L.cls, L.mmask, L.mbase, c->d_params + o.down_W,
+                   c->d_params + o.down_B, L.tab_down, L.g.n);
+            LAUNCH(c, s, k_build_table<D>, L.g.n, L.g, st, im, L.cls, L.mmask, L.mbase, c->d_params + o.up_W,
+                   c->d_params + o.up_B, L.tab_up, L.g.n);
+            constexpr int NC = (D == 3) ? 27 : 9;
+            CK(cudaMemsetAsync(L.zG, 0, 3 * NC * sizeof(unsigned long long), s));
+            const double scale = std::ldexp(1.0, D * l);
+            LAUNCH(c, s, k_zsums<D>, L.g.n, L.g, st, im, (float)scale, L.zG);
+            k_zfinal<D><<<1, 32, 0, s>>>(L.g, L.zG, scale, c->d_params + o.a_K, c->params[o.a_bias],
+                                         c->d_params + o.b_K, c->params[o.b_bias], c->zab + 2 * l, c->zab + 2 * l + 1);
+            CK(cudaGetLastError());
+        } else {
+            LAUNCH(c, s, k_build_table<D>, L.g.n, L.g, st, im, L.cls, L.mmask, L.mbase, c->d_params + c->coarse_W,
+                   c->d_params + c->coarse_B, L.tab_down, L.g.n);
+        }
+    }
+    // zero invariant of the solver vectors at the new non-fluid cells
+    const size_t nb = (size_t)c->g0.n * sizeof(double);
+    CK(cudaMemsetAsync(c->X1, 0, nb, s));
+    CK(cudaMemsetAsync(c->R, 0, nb, s));
+    CK(cudaMemsetAsync(c->Dtmp, 0, nb, s));
+    CK(cudaMemsetAsync(c->Dring, 0, nb * (size_t)c->ring_alloc, s));
+    // n_fluid = last base + last count
+    uint32_t tail[2];
+    CK(cudaMemcpyAsync(&tail[0], c->fbase + (L0.nseg - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tail[1], c->fcount + (L0.nseg - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->n_fluid = (long long)tail[0] + tail[1];
+    c->mask_ok = true;
+}
+
+// ------------------------------------------------------------ network
+template <int D>
+void launch_network(npsd_b200_ctx* c, cudaStream_t s, bool raw, int* launches) {
+    const int Ld = c->depth;
+    int n = 0;
+    // down sweep
+    for (int l = 0; l < Ld; ++l) {
+        LevelBufs& L = c->L[l];
+        const bool pool = (l + 1 < Ld);
+        const Geom gc = pool ? c->L[l + 1].g : L.g;
+        float* xnext = pool ? c->L[l + 1].x : nullptr;
+        const long long nb = L.g.n / ((D == 3) ? 8 : 4);
+        if (l == 0 && !raw) {
+            if (pool)
+                LAUNCH(c, s, (k_down<D, true, true>), nb, L.g, nullptr, c->R, c->st, tab_down(c, l), L.y, xnext, gc);
+            else
+                LAUNCH(c, s, (k_down<D, true, false>), nb, L.g, nullptr, c->R, c->st, tab_down(c, l), L.y, xnext, gc);
+        } else {
+            const float* in = (l == 0) ? c->xin_f : L.x;
+            if (pool)
+                LAUNCH(c, s, (k_down<D, false, true>), nb, L.g, in, nullptr, c->st, tab_down(c, l), L.y, xnext, gc);
+            else
+                LAUNCH(c, s, (k_down<D, false, false>), nb, L.g, in, nullptr, c->st, tab_down(c, l), L.y, xnext, gc);
+        }
+        ++n;
+    }
+    // up sweep
+    for (int l = Ld - 2; l >= 0; --l) {
+        LevelBufs& L = c->L[l];
+        const LevelBufs& Lc = c->L[l + 1];
+        const float* outc = (l + 1 == Ld - 1) ? Lc.y : Lc.out;
+        const long long nb = L.g.n / ((D == 3) ? 8 : 4);
+        if (l == 0 && !raw) {
+            LAUNCH(c, s, (k_up<D, kUpL0>), nb, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), nullptr, c->Dtmp,
+                   c->st, c->ADring, c->partials, c->counter);
+        } else {
+            float* outl = (l == 0) ? c->out_f : L.out;
+            LAUNCH(c, s, (k_up<D, kUpMid>), nb, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), outl, nullptr,
+                   c->st, c->ADring, c->partials, c->counter);
+        }
+        ++n;
+    }
+    if (Ld == 1 && !raw) {
+        LevelBufs& L = c->L[0];
+        const long long nb = L.g.n / ((D == 3) ? 8 : 4);
+        LAUNCH(c, s, (k_up<D, kUpL0Depth1>), nb, L.g, L.g, nullptr, L.y, c->zab, tab_up(c, 0), nullptr, c->Dtmp,
+               c->st, c->ADring, c->partials, c->counter);
+        ++n;
+    }
+    if (launches) *launches = n;
+}
+
+void ensure_ring(npsd_b200_ctx* c, int ring) {
+    if (ring <= c->ring_alloc) return;
+    const size_t n = (size_t)c->g0.n;
+    if (c->Dring) CK(cudaFree(c->Dring));
+    if (c->ADring) CK(cudaFree(c->ADring));
+    c->Dring = dalloc<double>(n * ring);
+    c->ADring = dalloc<double>(n * ring);
+    CK(cudaMemsetAsync(c->Dring, 0, n * ring * sizeof(double), c->s));
+    CK(cudaMemsetAsync(c->ADring, 0, n * ring * sizeof(double), c->s));
+    c->ring_alloc = ring;
+}
+
+void ensure_hist(npsd_b200_ctx* c, long long need) {
+    if (need <= c->hist_cap) return;
+    if (c->hist) CK(cudaFree(c->hist));
+    if (c->times) CK(cudaFree(c->times));
+    c->hist = dalloc<double>((size_t)need);
+    c->times = dalloc<double>((size_t)need);
+    c->hist_cap = need;
+}
+
+void ensure_hist_host(npsd_b200_ctx* c, long long need) {
+    if (need <= c->hist_host_cap) return;
+    if (c->hist_host) CK(cudaFreeHost(c->hist_host));
+    if (c->times_host) CK(cudaFreeHost(c->times_host));
+    CK(cudaMallocHost(&c->hist_host, (size_t)need * sizeof(double)));
+    CK(cudaMallocHost(&c->times_host, (size_t)need * sizeof(double)));
+    c->hist_host_cap = need;
+}
+
+template <int D>
+void capture_solve_graph(npsd_b200_ctx* c, int nullspace) {
+    if (c->exec) {
+        CK(cudaGraphExecDestroy(c->exec));
+        c->exec = nullptr;
+    }
+    cudaStream_t s = c->s, s2 = c->s2;
+    const Geom g = c->g0;
+    const uint8_t* cls = c->L[0].cls;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
+    int pro = 0;
+    // prologue: projections (solver.cpp:197-201), r0 = b - A x0, ||r0||
+    if (nullspace) {
+        LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->Bf, c->n_fluid, c->st, c->partials, c->counter);
+        LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->Bf, c->st);
+        LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->X0, c->n_fluid, c->st, c->partials, c->counter);
+        LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->X0, c->st);
+        pro += 4;
+    }
+    LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R);
+    ++pro;
+    if (nullspace) {
+        LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, c->n_fluid, c->st, c->partials, c->counter);
+        LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->R, c->st);
+        pro += 2;
+    }
+    LAUNCH(c, s, k_residual_norm, g.n, g, c->R, c->st, c->hist, c->times, c->partials, c->counter, h, 1);
+    ++pro;
+    // while (!done) { one PSDO iteration }
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CK(cudaGraphAddNode(&cnode, cg, deps, nd, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
+    CK(cudaStreamBeginCaptureToGraph(s2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    int nbody = 0;
+    launch_network<D>(c, s2, false, &nbody);
+    LAUNCH(c, s2, k_ortho<D>, g.n, g, cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials, c->counter);
+    ++nbody;
+    LAUNCH(c, s2, k_update<D>, g.n, g, cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist, c->times, c->partials,
+           c->counter, h, nullspace ? 0 : 1);
+    ++nbody;
+    if (nullspace) {
+        LAUNCH(c, s2, k_fluid_sum, g.n, g, cls, c->R, c->n_fluid, c->st, c->partials, c->counter);
+        LAUNCH(c, s2, k_subtract_mean, g.n, g, cls, c->R, c->st);
+        LAUNCH(c, s2, k_residual_norm, g.n, g, c->R, c->st, c->hist, c->times, c->partials, c->counter, h, 0);
+        nbody += 3;
+    }
+    cudaGraph_t body_out = nullptr;
+    CK(cudaStreamEndCapture(s2, &body_out));
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamEndCapture(s, &graph));
+    CK(cudaGraphInstantiate(&c->exec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    c->exec_key[0] = c->Dring;
+    c->exec_key[1] = c->hist;
+    c->exec_key[2] = c->ADring;
+    c->exec_key[3] = c->partials;
+    c->exec_nullspace = nullspace;
+    c->body_launches = nbody;
+    c->prologue_launches = pro;
+}
+
+// Runs the solve on c->Bf / c->X0 (already masked). Returns the status.
+template <int D>
+int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_report* rep) {
+    // stop_threshold / check_inputs (solver.cpp:20-33)
+    require(cfg->tol_reduction > 0.0 && cfg->tol_reduction < 1.0, "SolveConfig: tol_reduction must lie in (0,1)");
+    require(cfg->n_ortho >= 0, "psdo: n_ortho must be >= 0");
+    require(cfg->n_ortho <= kMaxOrtho, "psdo: n_ortho > 8 is not supported by the B200 build");
+    const long long max_iters = cfg->max_iters < 0 ? 0 : cfg->max_iters;
+    const int ring = cfg->n_ortho + 1;
+    ensure_ring(c, ring);
+    ensure_hist(c, max_iters + 1);
+    const int nullspace = cfg->nullspace_projection ? 1 : 0;
+    if (!c->exec || c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist || c->exec_key[2] != c->ADring ||
+        c->exec_nullspace != nullspace)
+        capture_solve_graph<D>(c, nullspace);
+    SolverState* h = c->st_host;
+    std::memset(h, 0, sizeof(SolverState));
+    h->tol_reduction = cfg->tol_reduction;
+    h->tol_abs = cfg->tol_abs;
+    h->max_iters = max_iters;
+    h->n_ortho = cfg->n_ortho;
+    h->normalize = cfg->normalize_before_precond ? 1 : 0;
+    h->nullspace = nullspace;
+    h->ring = ring;
+    CK(cudaMemcpyAsync(c->st, h, sizeof(SolverState), cudaMemcpyHostToDevice, c->s));
+    CK(cudaEventRecord(c->ev0, c->s));
+    CK(cudaGraphLaunch(c->exec, c->s));
+    CK(cudaEventRecord(c->ev1, c->s));
+    CK(cudaMemcpyAsync(h, c->st, sizeof(SolverState), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    CK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    const long long iters = h->breakdown ? h->k - 1 : ((h->k > 1) ? h->k - 1 : 0);
+    // history entries written: 0..iters (a breakdown stops before entry k)
+    const long long hl = iters + 1;
+    ensure_hist_host(c, hl);
+    CK(cudaMemcpyAsync(c->hist_host, c->hist, (size_t)hl * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaMemcpyAsync(c->times_host, c->times, (size_t)hl * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    c->last_launches = c->prologue_launches + (h->breakdown ? (iters * c->body_launches + c->body_launches)
+                                                            : iters * c->body_launches);
+    c->report_hist.assign(c->hist_host, c->hist_host + hl);
+    c->report_times.assign(c->times_host, c->times_host + hl);
+    if (rep) {
+        rep->iterations = iters;
+        rep->converged = h->converged;
+        rep->breakdown = h->breakdown;
+        rep->residual_history = c->report_hist.data();
+        rep->cumulative_seconds = c->report_times.data();
+        rep->history_len = hl;
+        rep->setup_seconds = 0.0;
+        rep->iterate_seconds = c->last_ms * 1e-3;
+        rep->precond_seconds = 0.0;
+    }
+    if (h->breakdown) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "psdo: curvature d'Ad = %f at iteration %lld (||r|| = %f)", h->bad_value,
+                      h->k, h->rnorm);
+        throw Breakdown(buf);
+    }
+    return NPSD_OK;
+}
+
+template <typename Fn>
+int guarded(npsd_b200_ctx* c, Fn&& fn) {
+    if (!c) return NPSD_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(c->mu);
+    try {
+        CK(cudaSetDevice(c->dev));
+        fn();
+        c->err.clear();
+        return NPSD_OK;
+    } catch (const InvalidArgument& e) {
+        c->err = e.what();
+        return NPSD_INVALID_ARGUMENT;
+    } catch (const Breakdown& e) {
+        c->err = e.what();
+        return NPSD_BREAKDOWN;
+    } catch (const EmptySystem& e) {
+        c->err = e.what();
+        return NPSD_EMPTY_SYSTEM;
+    } catch (const std::exception& e) {
+        c->err = e.what();
+        return NPSD_CUDA_ERROR;
+    }
+}
+
+void check_mask(const npsd_b200_ctx* c) {
+    require(c->mask_ok, "npsd_b200: set_mask has not been called");
+}
+
+void free_ctx(npsd_b200_ctx* c) {
+    auto F = [](void* p) {
+        if (p) cudaFree(p);
+    };
+    for (auto& L : c->L) {
+        F(L.cls);
+        F(L.mmask);
+        F(L.mbase);
+        F(L.mcount);
+        F(L.img);
+        F(L.tab_down);
+        F(L.tab_up);
+        F(L.kc_down);
+        F(L.kc_up);
+        F(L.y);
+        F(L.x);
+        F(L.out);
+        F(L.zG);
+    }
+    F(c->d_params);
+    F(c->zab);
+    F(c->fmask);
+    F(c->fbase);
+    F(c->fcount);
+    F(c->X0);
+    F(c->X1);
+    F(c->R);
+    F(c->Bf);
+    F(c->Dtmp);
+    F(c->Dring);
+    F(c->ADring);
+    F(c->st);
+    F(c->partials);
+    F(c->counter);
+    F(c->hist);
+    F(c->times);
+    F(c->red_a);
+    F(c->red_b);
+    F(c->xin_f);
+    F(c->out_f);
+    F(c->cub_tmp);
+    if (c->st_host) cudaFreeHost(c->st_host);
+    if (c->hist_host) cudaFreeHost(c->hist_host);
+    if (c->times_host) cudaFreeHost(c->times_host);
+    if (c->exec) cudaGraphExecDestroy(c->exec);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->s) cudaStreamDestroy(c->s);
+    if (c->s2) cudaStreamDestroy(c->s2);
+}
+
+void do_set_params(npsd_b200_ctx* c, const float* params, size_t n) {
+    require(params != nullptr, "npsd_b200: params is null");
+    require(n == param_count_impl(c->dim, c->depth), "npsd_b200: parameter count mismatch");
+    c->params.assign(params, params + n);
+    if (c->dim == 3)
+        upload_params_and_kconst<3>(c);
+    else
+        upload_params_and_kconst<2>(c);
+    c->mask_ok = false;  // tables depend on the weights
+}
+
+}  // namespace
+
+// =====================================================================  C ABI
+extern "C" {
+
+size_t npsd_b200_param_count(int dim, int depth) {
+    if ((dim != 2 && dim != 3) || depth < 1) return 0;
+    return param_count_impl(dim, depth);
+}
+
+int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* params, size_t n_params,
+                     const int* devices, int n_devices, npsd_b200_ctx** out) {
+    if (!out) return NPSD_INVALID_ARGUMENT;
+    *out = nullptr;
+    npsd_b200_ctx* c = new npsd_b200_ctx();
+    try {
+        require(dim == 2 || dim == 3, "npsd_b200: dim must be 2 or 3");
+        require(depth >= 1 && depth <= kMaxDepth, "NetContext: depth must be >= 1 (and <= 8 here)");
+        if (dim == 2) nz = 1;
+        require(nx > 0 && ny > 0 && nz > 0, "IndicatorImage: dims must be positive");
+        const long long div = 1LL << depth;
+        require(nx % div == 0 && ny % div == 0 && (dim == 2 || nz % div == 0),
+                "NetContext: dims " + std::to_string(nx) + "x" + std::to_string(ny) +
+                    (dim == 3 ? "x" + std::to_string(nz) : std::string()) + " not divisible by 2^" +
+                    std::to_string(depth));
+        require(n_devices <= 1, "npsd_b200: one device per context in this build (z-slab sharding: see DESIGN.md)");
+        c->dim = dim;
+        c->depth = depth;
+        c->S = (dim == 3) ? 27 : 9;
+        c->dev = (devices && n_devices == 1) ? devices[0] : 0;
+        c->g0 = make_geom(nx, ny, nz);
+        require(c->g0.n < (1LL << 31) * 16, "npsd_b200: grid too large");
+        CK(cudaSetDevice(c->dev));
+        CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->dev));
+        CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&c->ev0));
+        CK(cudaEventCreate(&c->ev1));
+        compute_offsets(c);
+        c->d_params = dalloc<float>(param_count_impl(dim, depth));
+        for (int l = 0; l < depth; ++l) {
+            LevelBufs& L = c->L[l];
+            L.g = level_geom(c, l);
+            L.nseg = (L.g.n + 31) / 32;
+            L.cls = dalloc<uint8_t>((size_t)L.g.n);
+            L.mmask = dalloc<uint32_t>((size_t)L.nseg);
+            L.mbase = dalloc<uint32_t>((size_t)L.nseg);
+            L.mcount = dalloc<uint32_t>((size_t)L.nseg);
+            if (l > 0) L.img = dalloc<float>(3 * (size_t)L.g.n);
+            L.tab_down = dalloc<float>((size_t)c->S * L.g.n);
+            if (l < depth - 1) L.tab_up = dalloc<float>((size_t)c->S * L.g.n);
+            L.kc_down = dalloc<float>(3 * (size_t)c->S);
+            L.kc_up = dalloc<float>(3 * (size_t)c->S);
+            L.y = dalloc<float>((size_t)L.g.n);
+            if (l > 0) L.x = dalloc<float>((size_t)L.g.n);
+            if (l > 0 && l < depth - 1) L.out = dalloc<float>((size_t)L.g.n);
+            L.zG = dalloc<unsigned long long>(81);
+        }
+        c->zab = dalloc<float>(2 * (size_t)depth);
+        CK(cudaMemset(c->zab, 0, 2 * (size_t)depth * sizeof(float)));
+        const long long nseg0 = c->L[0].nseg;
+        c->fmask = dalloc<uint32_t>((size_t)nseg0);
+        c->fbase = dalloc<uint32_t>((size_t)nseg0);
+        c->fcount = dalloc<uint32_t>((size_t)nseg0);
+        const size_t n = (size_t)c->g0.n;
+        c->X0 = dalloc<double>(n);
+        c->X1 = dalloc<double>(n);
+        c->R = dalloc<double>(n);
+        c->Bf = dalloc<double>(n);
+        c->Dtmp = dalloc<double>(n);
+        c->red_a = dalloc<double>(n);
+        c->red_b = dalloc<double>(n);
+        c->st = dalloc<SolverState>(1);
+        CK(cudaMemset(c->st, 0, sizeof(SolverState)));
+        CK(cudaMallocHost(&c->st_host, sizeof(SolverState)));
+        c->partials = dalloc<double>((size_t)c->num_sms * 8 * (2 + kMaxOrtho));
+        c->counter = dalloc<unsigned int>(1);
+        CK(cudaMemset(c->counter, 0, sizeof(unsigned int)));
+        ensure_ring(c, 3);
+        ensure_hist(c, 1001);
+        do_set_params(c, params, n_params);
+        CK(cudaStreamSynchronize(c->s));
+        *out = c;
+        return NPSD_OK;
+    } catch (const InvalidArgument& e) {
+        g_create_err = e.what();
+        free_ctx(c);
+        delete c;
+        return NPSD_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_create_err = e.what();
+        free_ctx(c);
+        delete c;
+        return NPSD_CUDA_ERROR;
+    }
+}
+
+int npsd_b200_destroy(npsd_b200_ctx* c) {
+    if (!c) return NPSD_OK;
+    cudaSetDevice(c->dev);
+    cudaStreamSynchronize(c->s);
+    free_ctx(c);
+    delete c;
+    return NPSD_OK;
+}
+
+const char* npsd_b200_last_error(const npsd_b200_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int npsd_b200_set_params(npsd_b200_ctx* c, const float* params, size_t n) {
+    return guarded(c, [&] {
+        do_set_params(c, params, n);
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_set_mask_device(npsd_b200_ctx* c, const uint8_t* d_types) {
+    return guarded(c, [&] {
+        require(d_types != nullptr, "npsd_b200: cell types pointer is null");
+        if (c->dim == 3)
+            set_mask_impl<3>(c, d_types);
+        else
+            set_mask_impl<2>(c, d_types);
+    });
+}
+
+int npsd_b200_set_mask(npsd_b200_ctx* c, const uint8_t* types) {
+    return guarded(c, [&] {
+        require(types != nullptr, "npsd_b200: cell types pointer is null");
+        const size_t n = (size_t)c->g0.n;
+        for (size_t i = 0; i < n; ++i) require(types[i] <= 2, "npsd_b200: cell type out of range (0 fluid, 1 air, 2 solid)");
+        uint8_t* d = reinterpret_cast<uint8_t*>(c->red_a);  // staging (n bytes <= 8n)
+        CK(cudaMemcpyAsync(d, types, n, cudaMemcpyHostToDevice, c->s));
+        if (c->dim == 3)
+            set_mask_impl<3>(c, d);
+        else
+            set_mask_impl<2>(c, d);
+    });
+}
+
+int64_t npsd_b200_n_fluid(const npsd_b200_ctx* c) { return (c && c->mask_ok) ? c->n_fluid : -1; }
+
+int npsd_b200_fluid_indices(npsd_b200_ctx* c, int64_t* out) {
+    return guarded(c, [&] {
+        check_mask(c);
+        // scatter the reduced index ramp, then read positions back on host
+        std::vector<uint32_t> mask((size_t)c->L[0].nseg), base((size_t)c->L[0].nseg);
+        CK(cudaMemcpyAsync(mask.data(), c->fmask, mask.size() * 4, cudaMemcpyDeviceToHost, c->s));
+        CK(cudaMemcpyAsync(base.data(), c->fbase, base.size() * 4, cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        for (size_t sgm = 0; sgm < mask.size(); ++sgm) {
+            uint32_t m = mask[sgm];
+            long long k = base[sgm];
+            while (m) {
+                const int b = __builtin_ctz(m);
+                out[k++] = (int64_t)(sgm * 32 + (size_t)b);
+                m &= m - 1;
+            }
+        }
+    });
+}
+
+int npsd_b200_precond_apply(npsd_b200_ctx* c, const double* r, double* z, int64_t n_f) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(n_f == c->n_fluid, "NeuralPrecond::apply: size mismatch");
+        if (n_f == 0) return;
+        const Geom g = c->g0;
+        CK(cudaMemcpyAsync(c->red_a, r, (size_t)n_f * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        LAUNCH(c, c->s, k_scatter, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->red_a, c->R);
+        LAUNCH(c, c->s, k_norm_precond, g.n, g, c->R, c->st, c->partials, c->counter);
+        SolverState* h = c->st_host;
+        // no cached directions: the fused dots in the L0 up kernel are empty
+        const int zero = 0;
+        CK(cudaMemcpyAsync(&c->st->n_cache, &zero, sizeof(int), cudaMemcpyHostToDevice, c->s));
+        const int one = 1;
+        CK(cudaMemcpyAsync(&c->st->ring, &one, sizeof(int), cudaMemcpyHostToDevice, c->s));
+        (void)h;
+        if (c->dim == 3)
+            launch_network<3>(c, c->s, false, nullptr);
+        else
+            launch_network<2>(c, c->s, false, nullptr);
+        LAUNCH(c, c->s, k_gather, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->Dtmp, c->red_b);
+        CK(cudaMemcpyAsync(z, c->red_b, (size_t)n_f * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_spmv(npsd_b200_ctx* c, const double* x, double* y, int64_t n_f) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(n_f == c->n_fluid, "spmv: dimension mismatch");
+        if (n_f == 0) return;
+        const Geom g = c->g0;
+        CK(cudaMemcpyAsync(c->red_a, x, (size_t)n_f * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        LAUNCH(c, c->s, k_scatter, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->red_a, c->Dtmp);
+        if (c->dim == 3)
+            LAUNCH(c, c->s, k_spmv<3>, g.n, g, c->L[0].cls, c->Dtmp, c->R);
+        else
+            LAUNCH(c, c->s, k_spmv<2>, g.n, g, c->L[0].cls, c->Dtmp, c->R);
+        LAUNCH(c, c->s, k_gather, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->R, c->red_b);
+        CK(cudaMemcpyAsync(y, c->red_b, (size_t)n_f * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        // restore the zero invariant of the scratch vectors used
+        CK(cudaMemsetAsync(c->Dtmp, 0, (size_t)g.n * sizeof(double), c->s));
+        CK(cudaMemsetAsync(c->R, 0, (size_t)g.n * sizeof(double), c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_net_apply(npsd_b200_ctx* c, const float* x, float* y) {
+    return guarded(c, [&] {
+        check_mask(c);
+        const size_t n = (size_t)c->g0.n;
+        if (!c->xin_f) c->xin_f = dalloc<float>(n);
+        if (!c->out_f) c->out_f = dalloc<float>(n);
+        CK(cudaMemcpyAsync(c->xin_f, x, n * sizeof(float), cudaMemcpyHostToDevice, c->s));
+        if (c->dim == 3)
+            launch_network<3>(c, c->s, true, nullptr);
+        else
+            launch_network<2>(c, c->s, true, nullptr);
+        const float* res = (c->depth == 1) ? c->L[0].y : c->out_f;
+        CK(cudaMemcpyAsync(y, res, n * sizeof(float), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_psdo_solve_device(npsd_b200_ctx* c, const double* d_b, const double* d_x0,
+                                const npsd_b200_solve_cfg* cfg, double* d_x, npsd_b200_report* rep) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(cfg != nullptr && d_b != nullptr && d_x != nullptr, "solve: null argument");
+        if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
+        const Geom g = c->g0;
+        const uint8_t* cls = c->L[0].cls;
+        LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_b, c->Bf);
+        if (d_x0)
+            LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_x0, c->X0);
+        else
+            CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
+        int st = (c->dim == 3) ? solve_device_impl<3>(c, cfg, rep) : solve_device_impl<2>(c, cfg, rep);
+        (void)st;
+        const double* xr = c->st_host->xcur ? c->X1 : c->X0;
+        CK(cudaMemcpyAsync(d_x, xr, (size_t)g.n * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_psdo_solve(npsd_b200_ctx* c, const double* b, const double* x0, const npsd_b200_solve_cfg* cfg,
+                         double* x, npsd_b200_report* rep) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(cfg != nullptr && b != nullptr && x != nullptr, "solve: null argument");
+        if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
+        const Geom g = c->g0;
+        const uint8_t* cls = c->L[0].cls;
+        const size_t nf = (size_t)c->n_fluid;
+        for (size_t i = 0; i < nf; ++i) require(std::isfinite(b[i]), "solve: rhs has non-finite entries");
+        CK(cudaMemcpyAsync(c->red_a, b, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        LAUNCH(c, c->s, k_scatter, g.n, g, cls, c->fmask, c->fbase, c->red_a, c->Bf);
+        if (x0) {
+            CK(cudaMemcpyAsync(c->red_b, x0, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
+            LAUNCH(c, c->s, k_scatter, g.n, g, cls, c->fmask, c->fbase, c->red_b, c->X0);
+        } else {
+            CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
+        }
+        try {
+            (c->dim == 3) ? solve_device_impl<3>(c, cfg, rep) : solve_device_impl<2>(c, cfg, rep);
+        } catch (const Breakdown&) {
+            const double* xr = c->st_host->xcur ? c->X1 : c->X0;
+            LAUNCH(c, c->s, k_gather, g.n, g, cls, c->fmask, c->fbase, xr, c->red_b);
+            CK(cudaMemcpyAsync(x, c->red_b, nf * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            throw;
+        }
+        const double* xr = c->st_host->xcur ? c->X1 : c->X0;
+        LAUNCH(c, c->s, k_gather, g.n, g, cls, c->fmask, c->fbase, xr, c->red_b);
+        CK(cudaMemcpyAsync(x, c->red_b, nf * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_level_image(npsd_b200_ctx* c, int level, float* out) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(level >= 0 && level < c->depth, "level out of range");
+        const LevelBufs& L = c->L[level];
+        if (level == 0) {
+            std::vector<uint8_t> cls((size_t)L.g.n);
+            CK(cudaMemcpyAsync(cls.data(), L.cls, cls.size(), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            for (int ch = 0; ch < 3; ++ch)
+                for (size_t i = 0; i < cls.size(); ++i)
+                    out[(size_t)ch * cls.size() + i] = (((cls[i] >> 2) & 3) == ch) ? 1.0f : 0.0f;
+        } else {
+            CK(cudaMemcpyAsync(out, L.img, 3 * (size_t)L.g.n * sizeof(float), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+        }
+    });
+}
+
+int npsd_b200_linear_coeffs(npsd_b200_ctx* c, float* za, float* zb) {
+    return guarded(c, [&] {
+        check_mask(c);
+        std::vector<float> h(2 * (size_t)c->depth);
+        CK(cudaMemcpyAsync(h.data(), c->zab, h.size() * sizeof(float), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        for (int l = 0; l + 1 < c->depth; ++l) {
+            za[l] = h[2 * (size_t)l];
+            zb[l] = h[2 * (size_t)l + 1];
+        }
+    });
+}
+
+int npsd_b200_mixed_counts(npsd_b200_ctx* c, int64_t* counts) {
+    return guarded(c, [&] {
+        check_mask(c);
+        for (int l = 0; l < c->depth; ++l) {
+            const LevelBufs& L = c->L[l];
+            uint32_t t[2];
+            CK(cudaMemcpyAsync(&t[0], L.mbase + (L.nseg - 1), 4, cudaMemcpyDeviceToHost, c->s));
+            CK(cudaMemcpyAsync(&t[1], L.mcount + (L.nseg - 1), 4, cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            counts[l] = (int64_t)t[0] + t[1];
+        }
+    });
+}
+
+int npsd_b200_device_alloc(npsd_b200_ctx* c, size_t bytes, void** out) {
+    return guarded(c, [&] { CK(cudaMalloc(out, bytes ? bytes : 1)); });
+}
+int npsd_b200_device_free(npsd_b200_ctx* c, void* p) {
+    return guarded(c, [&] { CK(cudaFree(p)); });
+}
+int npsd_b200_host_alloc(npsd_b200_ctx* c, size_t bytes, void** out) {
+    return guarded(c, [&] { CK(cudaMallocHost(out, bytes ? bytes : 1)); });
+}
+int npsd_b200_host_free(npsd_b200_ctx* c, void* p) {
+    return guarded(c, [&] { CK(cudaFreeHost(p)); });
+}
+int npsd_b200_memcpy(npsd_b200_ctx* c, void* dst, const void* src, size_t bytes) {
+    return guarded(c, [&] { CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->s)); });
+}
+int npsd_b200_synchronize(npsd_b200_ctx* c) {
+    return guarded(c, [&] { CK(cudaStreamSynchronize(c->s)); });
+}
+
+double npsd_b200_last_solve_ms(const npsd_b200_ctx* c) { return c ? (double)c->last_ms : 0.0; }
+int64_t npsd_b200_last_solve_launches(const npsd_b200_ctx* c) { return c ? c->last_launches : 0; }
+
+}  // extern "C"

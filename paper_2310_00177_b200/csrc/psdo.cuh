@@ -1,0 +1,330 @@
+// PSDO iteration kernels (psdo_solve, src/solver.cpp:189-276), whole loop on
+// device. Solver vectors live on the full grid in f64 with exact zeros at
+// non-fluid cells, so the matrix-free operator needs no index maps: with the
+// zero invariant, adding a non-fluid neighbour's (-1.0 * 0) leaves the CSR
+// row sum bit-identical (s + -0.0 == s), and the row is accumulated in the
+// reduced CSR column order (z-1, y-1, x-1, diag, x+1, y+1, z+1) from s = 0
+// with explicit round-to-nearest ops, exactly like spmv (sparse.cpp:111-116)
+// on assemble_poisson[_3d] + reduce (discretization.cpp:21-160).
+#pragma once
+
+#include "common.cuh"
+
+namespace nb2 {
+
+// (A v)(c) from a per-cell value functor (zero outside the domain).
+template <int D, typename VFn>
+__device__ __forceinline__ double stencil_row(const Geom& g, int x, int y, int z, int diag, double vc, VFn val) {
+    double s = 0.0;
+    if (D == 3 && z > 0) s = __dadd_rn(s, -val(lin(g, x, y, z - 1)));
+    if (y > 0) s = __dadd_rn(s, -val(lin(g, x, y - 1, z)));
+    if (x > 0) s = __dadd_rn(s, -val(lin(g, x - 1, y, z)));
+    if (diag > 0) s = __dadd_rn(s, __dmul_rn((double)diag, vc));
+    if (x + 1 < g.nx) s = __dadd_rn(s, -val(lin(g, x + 1, y, z)));
+    if (y + 1 < g.ny) s = __dadd_rn(s, -val(lin(g, x, y + 1, z)));
+    if (D == 3 && z + 1 < g.nz) s = __dadd_rn(s, -val(lin(g, x, y, z + 1)));
+    return s;
+}
+
+__device__ __forceinline__ void decode(const Geom& g, long long c, int& x, int& y, int& z) {
+    x = (int)(c % g.nx);
+    y = (int)((c / g.nx) % g.ny);
+    z = (int)(c / ((long long)g.nx * g.ny));
+}
+
+// ------------------------------------------------------------------ scatter
+// reduced (ascending fluid order) -> full grid with zeros elsewhere
+__global__ void __launch_bounds__(kBlock) k_scatter(Geom g, const uint8_t* __restrict__ cls,
+                                                    const uint32_t* __restrict__ fmask,
+                                                    const uint32_t* __restrict__ fbase, const double* __restrict__ red,
+                                                    double* __restrict__ full) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
+        full[c] = (cls_type(cls[c]) == 0) ? red[mixed_index(fmask, fbase, c)] : 0.0;
+}
+
+__global__ void __launch_bounds__(kBlock) k_gather(Geom g, const uint8_t* __restrict__ cls,
+                                                   const uint32_t* __restrict__ fmask,
+                                                   const uint32_t* __restrict__ fbase, const double* __restrict__ full,
+                                                   double* __restrict__ red) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
+        if (cls_type(cls[c]) == 0) red[mixed_index(fmask, fbase, c)] = full[c];
+}
+
+__global__ void __launch_bounds__(kBlock) k_scatter_f32(Geom g, const float* __restrict__ src, float* __restrict__ dst) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) dst[c] = src[c];
+}
+
+// zero non-fluid entries (enforces the invariant on caller-provided full vectors)
+__global__ void __launch_bounds__(kBlock) k_mask_fluid(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ src,
+                                                       double* __restrict__ dst) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
+        dst[c] = (cls_type(cls[c]) == 0) ? src[c] : 0.0;
+}
+
+// ---------------------------------------------------------------- operator
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_spmv(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ v,
+                                                 double* __restrict__ out) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+        const uint8_t b = cls[c];
+        if (cls_type(b) != 0) {
+            out[c] = 0.0;
+            continue;
+        }
+        int x, y, z;
+        decode(g, c, x, y, z);
+        out[c] = stencil_row<D>(g, x, y, z, cls_diag(b), v[c], [&](long long q) { return __ldg(v + q); });
+    }
+}
+
+// ------------------------------------------------------------ reductions
+// sum of squares of a full-grid vector over fluid cells -> st fields per mode
+enum NormMode { kNormPrecond = 0, kNormMean = 1 };
+
+// Precond-only path: rnorm = ||r||, inv1 = 1/rnorm, inv2 = 1, nrm = rnorm
+// (NeuralPrecond::apply, net_precond.cpp:20-26).
+__global__ void __launch_bounds__(kBlock) k_norm_precond(Geom g, const double* __restrict__ r, SolverState* st,
+                                                         double* __restrict__ partials, unsigned int* __restrict__ counter) {
+    double acc[1] = {0.0};
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+        const double v = r[c];
+        acc[0] += v * v;
+    }
+    double tot[1];
+    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0) {
+        const double rn = sqrt(tot[0]);
+        st->rnorm = rn;
+        st->inv1 = (rn == 0.0) ? 0.0 : 1.0 / rn;
+        st->inv2 = 1.0;
+        st->nrm = rn;
+    }
+}
+
+// Sets the network scales from st->rnorm for the next preconditioner call.
+__device__ __forceinline__ void set_precond_scales(SolverState* st) {
+    const double rn = st->rnorm;
+    if (st->normalize) {
+        // psdo: scaled = r * (1/||r||) (solver.cpp:230-233); NeuralPrecond
+        // renormalises by ||scaled|| (net_precond.cpp:20-26), taken here as
+        // ||r|| * (1/||r||) (equal in exact arithmetic).
+        st->inv1 = 1.0 / rn;
+        const double ns = rn * st->inv1;
+        st->inv2 = 1.0 / ns;
+        st->nrm = ns;
+    } else {
+        st->inv1 = 1.0;
+        st->inv2 = 1.0 / rn;
+        st->nrm = rn;
+    }
+}
+
+// mean over fluid cells (mean_project, vector_ops.cpp:33-43): pass 1 sums.
+__global__ void __launch_bounds__(kBlock) k_fluid_sum(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ v,
+                                                      long long n_fluid, SolverState* st, double* __restrict__ partials,
+                                                      unsigned int* __restrict__ counter) {
+    double acc[1] = {0.0};
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) acc[0] += v[c];
+    double tot[1];
+    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0) st->mean = tot[0] / (double)n_fluid;
+}
+
+// pass 2: v -= mean at fluid cells; FINAL_NORM also finishes the residual norm
+// (and the iteration bookkeeping) exactly like k_update's finaliser.
+__global__ void __launch_bounds__(kBlock) k_subtract_mean(Geom g, const uint8_t* __restrict__ cls, double* __restrict__ v,
+                                                          const SolverState* __restrict__ st) {
+    const double m = st->mean;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
+        if (cls_type(cls[c]) == 0) v[c] = __dadd_rn(v[c], -m);
+}
+
+// ------------------------------------------------------------------ init
+// r0 = b - A x0 (solver.cpp:203-207); with PROJ the norm is taken later by
+// k_residual_norm after the mean projection.
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_residual(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ b,
+                                                     const double* __restrict__ x, double* __restrict__ r) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+        const uint8_t bb = cls[c];
+        if (cls_type(bb) != 0) continue;
+        int xx, yy, zz;
+        decode(g, c, xx, yy, zz);
+        const double ax = stencil_row<D>(g, xx, yy, zz, cls_diag(bb), x[c], [&](long long q) { return __ldg(x + q); });
+        r[c] = __dadd_rn(b[c], -ax);
+    }
+}
+
+__device__ __forceinline__ void finish_iteration(SolverState* st, double rsq, double* hist, double* times,
+                                                 cudaGraphConditionalHandle cond, bool initial) {
+    const double rn = sqrt(rsq);
+    st->rnorm = rn;
+    const unsigned long long now = globaltimer();
+    if (initial) {
+        st->t0 = now;
+        hist[0] = rn;
+        times[0] = 0.0;
+        double thr = st->tol_reduction * rn;
+        if (st->tol_abs > 0.0) thr = fmax(thr, st->tol_abs);
+        st->thr = thr;
+        st->k = 1;
+        st->n_cache = 0;
+        st->head = st->ring - 1;
+        st->converged = (rn <= thr);
+        st->done = st->converged || st->max_iters < 1;
+    } else {
+        const long long k = st->k;
+        hist[k] = rn;
+        times[k] = (double)(now - st->t0) * 1e-9;
+        // cache push (solver.cpp:265-268)
+        if (st->n_ortho > 0) {
+            const int R = st->ring;
+            const int nw = (st->head + 1) % R;
+            st->dAd[nw] = st->dAd_new;
+            st->head = nw;
+            st->n_cache = min(st->n_cache + 1, st->n_ortho);
+        }
+        st->xcur ^= 1;
+        st->converged = (rn <= st->thr);
+        st->done = st->converged || k >= st->max_iters;
+        st->k = k + 1;
+    }
+    if (!st->done) set_precond_scales(st);
+    cudaGraphSetConditional(cond, st->done ? 0u : 1u);
+}
+
+// ||r||^2 over the (already projected) residual, then bookkeeping.
+__global__ void __launch_bounds__(kBlock) k_residual_norm(Geom g, const double* __restrict__ r, SolverState* st,
+                                                          double* __restrict__ hist, double* __restrict__ times,
+                                                          double* __restrict__ partials, unsigned int* __restrict__ counter,
+                                                          cudaGraphConditionalHandle cond, int initial) {
+    if (!initial && st->breakdown) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        return;
+    }
+    double acc[1] = {0.0};
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+        const double v = r[c];
+        acc[0] += v * v;
+    }
+    double tot[1];
+    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0)
+        finish_iteration(st, tot[0], hist, times, cond, initial != 0);
+}
+
+// --------------------------------------------------------------- ortho
+// d' = d - p_1 d_1 - ... (MGS order, axpy_inplace form: d += (-p) * d_j),
+// Ad' by the stencil (halo values recomputed from d and the d_j), and the dots
+// d'.Ad', r.d' and d_j.Ad' (future cross terms). solver.cpp:239-251.
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_ortho(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ dtmp,
+                                                  const double* __restrict__ r, double* __restrict__ Dring,
+                                                  double* __restrict__ ADring, SolverState* st,
+                                                  double* __restrict__ partials, unsigned int* __restrict__ counter) {
+    const int nc = st->n_cache, R = st->ring;
+    const int nw = (st->head + 1) % R;
+    const double* dj[kMaxOrtho];
+    double mp[kMaxOrtho];
+    for (int j = 0; j < kMaxOrtho; ++j) {
+        const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
+        dj[j] = Dring + (long long)slot * g.n;
+        mp[j] = (j < nc) ? -st->p[j] : 0.0;
+    }
+    double* dnew = Dring + (long long)nw * g.n;
+    double* adnew = ADring + (long long)nw * g.n;
+    auto dprime = [&](long long q) {
+        double v = __ldg(dtmp + q);
+#pragma unroll
+        for (int j = 0; j < kMaxOrtho; ++j)
+            if (j < nc) v = __dadd_rn(v, __dmul_rn(mp[j], __ldg(dj[j] + q)));
+        return v;
+    };
+    constexpr int NV = 2 + kMaxOrtho;
+    double acc[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) acc[j] = 0.0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+        const uint8_t b = cls[c];
+        if (cls_type(b) != 0) continue;
+        int x, y, z;
+        decode(g, c, x, y, z);
+        const double dc = dprime(c);
+        const double ad = stencil_row<D>(g, x, y, z, cls_diag(b), dc, dprime);
+        dnew[c] = dc;
+        adnew[c] = ad;
+        acc[0] += dc * ad;
+        acc[1] += __ldg(r + c) * dc;
+#pragma unroll
+        for (int j = 0; j < kMaxOrtho; ++j)
+            if (j < nc) acc[2 + j] += __ldg(dj[j] + c) * ad;
+    }
+    double tot[NV];
+    if (grid_reduce<NV>(acc, partials, counter, tot) && threadIdx.x == 0) {
+        const double dAd = tot[0];
+        st->dAd_new = dAd;
+        st->rd_new = tot[1];
+        for (int j = 0; j < nc; ++j) {
+            const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
+            st->cross[slot][nw] = tot[2 + j];
+        }
+        if (!(dAd > 0.0) || fabs(dAd) < 1e-300) {
+            st->breakdown = 1;
+            st->done = 1;
+            st->bad_value = dAd;
+            st->alpha = 0.0;
+        } else {
+            st->alpha = tot[1] / dAd;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- update
+// x' = x + alpha d' (axpy_inplace), r = b - A x' (explicit recompute,
+// solver.cpp:252-258), ||r||^2. x is ping-ponged so halo reads see the old x.
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_update(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ b,
+                                                   double* __restrict__ X0, double* __restrict__ X1,
+                                                   const double* __restrict__ Dring, double* __restrict__ r,
+                                                   SolverState* st, double* __restrict__ hist, double* __restrict__ times,
+                                                   double* __restrict__ partials, unsigned int* __restrict__ counter,
+                                                   cudaGraphConditionalHandle cond, int do_norm) {
+    if (st->breakdown) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        return;
+    }
+    const double alpha = st->alpha;
+    const int nw = (st->head + 1) % st->ring;
+    const double* dn = Dring + (long long)nw * g.n;
+    const double* xo = st->xcur ? X1 : X0;
+    double* xn = st->xcur ? X0 : X1;
+    auto xnew = [&](long long q) { return __dadd_rn(__ldg(xo + q), __dmul_rn(alpha, __ldg(dn + q))); };
+    double acc[1] = {0.0};
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+        const uint8_t bb = cls[c];
+        if (cls_type(bb) != 0) continue;
+        int x, y, z;
+        decode(g, c, x, y, z);
+        const double xc = xnew(c);
+        const double ax = stencil_row<D>(g, x, y, z, cls_diag(bb), xc, xnew);
+        const double rv = __dadd_rn(__ldg(b + c), -ax);
+        xn[c] = xc;
+        r[c] = rv;
+        acc[0] += rv * rv;
+    }
+    if (!do_norm) return;  // nullspace projection: norm after k_subtract_mean
+    double tot[1];
+    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0)
+        finish_iteration(st, tot[0], hist, times, cond, false);
+}
+
+}  // namespace nb2

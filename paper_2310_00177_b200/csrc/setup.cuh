@@ -1,0 +1,287 @@
+// Per-frame setup kernels (npsd_b200_set_mask): the device replacement for
+// NeuralPrecond's constructor work — ReductionMap::from_image
+// (discretization.cpp:5-19), PaddedImage::from_image/pooled (net/kernels.hpp:37-56),
+// build_kernels (net/kernels.hpp:121-144) and linear_image_sums + z
+// (net/kernels.hpp:253-276, net/forward.hpp:76-86) — plus the stencil
+// coefficients of assemble_poisson[_3d] (discretization.cpp:21-127).
+//
+// Kernels are NOT materialised for every cell (27 f32 per cell per conv would
+// cost more HBM traffic than the rest of a PSDO iteration). A cell whose whole
+// 3^D window is one pure cell type uses one of three per-level constant
+// kernels; only "mixed" cells get a row in a compact SoA table
+// tab[slot * cap + mixed_index].
+#pragma once
+
+#include "common.cuh"
+
+namespace nb2 {
+
+// L0: cell byte (window class, own type, stencil diagonal) plus 32-cell
+// segment masks of mixed cells and of fluid cells.
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_setup_l0(Geom g, const uint8_t* __restrict__ types,
+                                                     uint8_t* __restrict__ cls, uint32_t* __restrict__ mmask,
+                                                     uint32_t* __restrict__ mcount, uint32_t* __restrict__ fmask,
+                                                     uint32_t* __restrict__ fcount) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long nround = (g.n + 31) & ~31LL;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < nround; c += stride) {
+        bool mixed = false, fluid = false;
+        if (c < g.n) {
+            const int x = (int)(c % g.nx);
+            const int y = (int)((c / g.nx) % g.ny);
+            const int z = (int)(c / ((long long)g.nx * g.ny));
+            const int t = types[c];
+            bool uniform = true;
+            const int zr = (D == 3) ? 1 : 0;
+            for (int dz = -zr; dz <= zr; ++dz)
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int xx = x + dx, yy = y + dy, zz = z + dz;
+                        const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
+                        const int tt = in ? types[lin(g, xx, yy, zz)] : 2;
+                        uniform &= (tt == t);
+                    }
+            // stencil diagonal: non-solid in-domain face neighbours (discretization.cpp:105-113)
+            int diag = 0;
+            const int nbx[6] = {0, 0, -1, 1, 0, 0}, nby[6] = {0, -1, 0, 0, 1, 0}, nbz[6] = {-1, 0, 0, 0, 0, 1};
+            for (int k = 0; k < 6; ++k) {
+                if (D == 2 && nbz[k] != 0) continue;
+                const int xx = x + nbx[k], yy = y + nby[k], zz = z + nbz[k];
+                const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
+                if (in && types[lin(g, xx, yy, zz)] != 2) ++diag;
+            }
+            const int w = uniform ? t : 3;
+            cls[c] = (uint8_t)(w | (t << 2) | (diag << 4));
+            mixed = !uniform;
+            fluid = (t == 0);
+        }
+        const uint32_t mm = __ballot_sync(0xffffffffu, mixed);
+        const uint32_t fm = __ballot_sync(0xffffffffu, fluid);
+        if ((threadIdx.x & 31) == 0) {
+            const long long seg = c >> 5;
+            mmask[seg] = mm;
+            mcount[seg] = __popc(mm);
+            fmask[seg] = fm;
+            fcount[seg] = __popc(fm);
+        }
+    }
+}
+
+// PaddedImage::pooled (net/kernels.hpp:46-56), 3D order x-fastest then z+1
+// plane; from the L0 one-hot types (src_types) or a pooled level (src_img).
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_pool_image(Geom gf, Geom gc, const uint8_t* __restrict__ src_types,
+                                                       const float* __restrict__ src_img, float* __restrict__ dst) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < gc.n; c += stride) {
+        const int x = (int)(c % gc.nx);
+        const int y = (int)((c / gc.nx) % gc.ny);
+        const int z = (int)(c / ((long long)gc.nx * gc.ny));
+        for (int ch = 0; ch < 3; ++ch) {
+            float acc = 0.0f;
+            bool first = true;
+            for (int cz = 0; cz < Sh<D>::BZ; ++cz)
+                for (int cy = 0; cy < 2; ++cy)
+                    for (int cx = 0; cx < 2; ++cx) {
+                        const long long f = lin(gf, 2 * x + cx, 2 * y + cy, (D == 3) ? 2 * z + cz : 0);
+                        const float v = src_types ? ((src_types[f] == ch) ? 1.0f : 0.0f) : src_img[ch * gf.n + f];
+                        acc = first ? v : __fadd_rn(acc, v);
+                        first = false;
+                    }
+            dst[ch * gc.n + c] = __fmul_rn((D == 3) ? 0.125f : 0.25f, acc);
+        }
+    }
+}
+
+// Window class of a pooled level: uniform iff every window cell (solid outside)
+// is the same pure cell type.
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_classify(Geom g, const float* __restrict__ img, uint8_t* __restrict__ cls,
+                                                     uint32_t* __restrict__ mmask, uint32_t* __restrict__ mcount) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long nround = (g.n + 31) & ~31LL;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < nround; c += stride) {
+        bool mixed = false;
+        if (c < g.n) {
+            const int x = (int)(c % g.nx);
+            const int y = (int)((c / g.nx) % g.ny);
+            const int z = (int)(c / ((long long)g.nx * g.ny));
+            auto pure = [&](long long q) -> int {
+                const float a = img[q], b = img[g.n + q], s = img[2 * g.n + q];
+                if (a == 1.0f && b == 0.0f && s == 0.0f) return 0;
+                if (a == 0.0f && b == 1.0f && s == 0.0f) return 1;
+                if (a == 0.0f && b == 0.0f && s == 1.0f) return 2;
+                return 3;
+            };
+            const int t = pure(c);
+            bool uniform = (t != 3);
+            const int zr = (D == 3) ? 1 : 0;
+            for (int dz = -zr; dz <= zr && uniform; ++dz)
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int xx = x + dx, yy = y + dy, zz = z + dz;
+                        const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
+                        uniform &= ((in ? pure(lin(g, xx, yy, zz)) : 2) == t);
+                    }
+            cls[c] = (uint8_t)(uniform ? t : 3);
+            mixed = !uniform;
+        }
+        const uint32_t mm = __ballot_sync(0xffffffffu, mixed);
+        if ((threadIdx.x & 31) == 0) {
+            mmask[c >> 5] = mm;
+            mcount[c >> 5] = __popc(mm);
+        }
+    }
+}
+
+// build_kernels (net/kernels.hpp:121-144) for mixed cells only:
+// K[s] = B[s] + sum_c sum_window W[s,c,w] * I(c, x+w), order (c, dz, dy, dx).
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_build_table(Geom g, const uint8_t* __restrict__ src_types,
+                                                        const float* __restrict__ img, const uint8_t* __restrict__ cls,
+                                                        const uint32_t* __restrict__ mmask,
+                                                        const uint32_t* __restrict__ mbase, const float* __restrict__ W,
+                                                        const float* __restrict__ B, float* __restrict__ tab,
+                                                        long long cap) {
+    constexpr int S = Sh<D>::S;
+    __shared__ float sW[S * 3 * S];
+    __shared__ float sB[S];
+    for (int i = threadIdx.x; i < S * 3 * S; i += blockDim.x) sW[i] = W[i];
+    for (int i = threadIdx.x; i < S; i += blockDim.x) sB[i] = B[i];
+    __syncthreads();
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+        if (cls_window(cls[c]) != 3) continue;
+        const int x = (int)(c % g.nx);
+        const int y = (int)((c / g.nx) % g.ny);
+        const int z = (int)(c / ((long long)g.nx * g.ny));
+        float win[3][S];
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+            const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = (D == 3) ? t / 9 - 1 : 0;
+            const int xx = x + dx, yy = y + dy, zz = z + dz;
+            const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
+            if (!in) {
+                win[0][t] = 0.0f;
+                win[1][t] = 0.0f;
+                win[2][t] = 1.0f;  // solid ring
+            } else {
+                const long long q = lin(g, xx, yy, zz);
+                if (src_types) {
+                    const int tt = src_types[q];
+                    win[0][t] = (tt == 0) ? 1.0f : 0.0f;
+                    win[1][t] = (tt == 1) ? 1.0f : 0.0f;
+                    win[2][t] = (tt == 2) ? 1.0f : 0.0f;
+                } else {
+                    win[0][t] = img[q];
+                    win[1][t] = img[g.n + q];
+                    win[2][t] = img[2 * g.n + q];
+                }
+            }
+        }
+        const long long idx = mixed_index(mmask, mbase, c);
+        for (int s = 0; s < S; ++s) {
+            float acc = sB[s];
+            const float* w = sW + s * 3 * S;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+                for (int t = 0; t < S; ++t) acc = __fadd_rn(acc, __fmul_rn(w[ch * S + t], win[ch][t]));
+            tab[(long long)s * cap + idx] = acc;
+        }
+    }
+}
+
+// The three uniform-window kernels of a conv (same arithmetic as
+// build_kernels on a pure window: I = 1 on channel T, 0 elsewhere).
+template <int D>
+__global__ void k_kconst(const float* __restrict__ W, const float* __restrict__ B, float* __restrict__ out) {
+    constexpr int S = Sh<D>::S;
+    const int i = threadIdx.x;
+    if (i >= 3 * S) return;
+    const int T = i / S, s = i % S;
+    float acc = B[s];
+    for (int ch = 0; ch < 3; ++ch)
+        for (int t = 0; t < S; ++t) acc = __fadd_rn(acc, __fmul_rn(W[(s * 3 + ch) * S + t], (ch == T) ? 1.0f : 0.0f));
+    out[T * S + s] = acc;
+}
+
+// Exact window-sum ingredients for linear_image_sums: per-channel integer
+// counts (value * scale, scale = 2^(D*level)) accumulated per boundary class
+// (per axis: first plane, interior, last plane).
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_zsums(Geom g, const uint8_t* __restrict__ src_types,
+                                                  const float* __restrict__ img, float scale,
+                                                  unsigned long long* __restrict__ G) {
+    constexpr int NC = (D == 3) ? 27 : 9;
+    __shared__ unsigned long long sG[3 * NC];
+    for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x) sG[i] = 0ull;
+    __syncthreads();
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+        const int x = (int)(c % g.nx);
+        const int y = (int)((c / g.nx) % g.ny);
+        const int z = (int)(c / ((long long)g.nx * g.ny));
+        const int kx = (x == 0) ? 0 : ((x == g.nx - 1) ? 2 : 1);
+        const int ky = (y == 0) ? 0 : ((y == g.ny - 1) ? 2 : 1);
+        const int kz = (D == 3) ? ((z == 0) ? 0 : ((z == g.nz - 1) ? 2 : 1)) : 0;
+        const int cl = (kz * 3 + ky) * 3 + kx;
+        for (int ch = 0; ch < 3; ++ch) {
+            unsigned long long v;
+            if (src_types)
+                v = (src_types[c] == ch) ? 1ull : 0ull;
+            else
+                v = (unsigned long long)__fmul_rn(img[ch * g.n + c], scale);
+            if (v) atomicAdd(&sG[ch * NC + cl], v);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x)
+        if (sG[i]) atomicAdd(&G[i], sG[i]);
+}
+
+// z_a / z_b of one level (net/forward.hpp:78-86) from the class counts.
+// F[c,w] = sum of I_pad(c, p + w) over interior p, exact in f64, then f32.
+template <int D>
+__global__ void k_zfinal(Geom g, const unsigned long long* __restrict__ G, double scale,
+                         const float* __restrict__ KA, float biasA, const float* __restrict__ KB, float biasB,
+                         float* __restrict__ za_out, float* __restrict__ zb_out) {
+    constexpr int S = Sh<D>::S;
+    constexpr int NC = (D == 3) ? 27 : 9;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    float F[3 * S];
+    for (int ch = 0; ch < 3; ++ch)
+        for (int t = 0; t < S; ++t) {
+            const int d[3] = {t % 3 - 1, (t / 3) % 3 - 1, (D == 3) ? t / 9 - 1 : 0};
+            unsigned long long cnt = 0;
+            for (int cl = 0; cl < NC; ++cl) {
+                const int k[3] = {cl % 3, (cl / 3) % 3, cl / 9};
+                bool ok = true;
+                for (int a = 0; a < D; ++a) {
+                    if (d[a] == 1 && k[a] == 0) ok = false;   // q_a = p_a + 1 never hits plane 0
+                    if (d[a] == -1 && k[a] == 2) ok = false;  // q_a = p_a - 1 never hits plane n-1
+                }
+                if (ok) cnt += G[ch * NC + cl];
+            }
+            double f = (double)cnt / scale;
+            if (ch == 2) {
+                // ring (solid) cells inside the shifted box
+                const long long dims[3] = {g.nx, g.ny, g.nz};
+                long long inside = 1;
+                for (int a = 0; a < 3; ++a) inside *= dims[a] - ((a < D) ? (d[a] != 0 ? 1 : 0) : 0);
+                f += (double)(g.n - inside);
+            }
+            F[ch * S + t] = (float)f;
+        }
+    const float norm = __fdiv_rn(1.0f, __fmul_rn((float)S, __ll2float_rn(g.n)));
+    float za = biasA, zb = biasB;
+    for (int t = 0; t < 3 * S; ++t) {
+        za = __fadd_rn(za, __fmul_rn(__fmul_rn(norm, KA[t]), F[t]));
+        zb = __fadd_rn(zb, __fmul_rn(__fmul_rn(norm, KB[t]), F[t]));
+    }
+    *za_out = za;
+    *zb_out = zb;
+}
+
+}  // namespace nb2
