@@ -1,0 +1,258 @@
+"""GPU parity: the B200 path (through the C ABI) against the CPU oracle and the
+reference build, on identical seeded inputs.
+
+Bars (north_star): flag/mask coarsening bit-exact; network / preconditioner
+output within 1e-5 relative L2 (the kernels are in fact bitwise for a given f32
+input, asserted where it holds); iteration count to rel-res 1e-6 within +-1 of
+the reference psdo_solve; residual history over a fixed budget within 1e-6
+relative (random weights)."""
+import numpy as np
+import pytest
+
+from paper_2310_00177_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-5  # preconditioner output tolerance (north_star)
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def make(b200, oracle, types, depth, params):
+    dim = types.ndim
+    P = b200.NetParams(dim, depth, params)
+    ctx = b200.Context(dim, types.shape, P)
+    ctx.set_mask(types)
+    octx = oracle.context(types, params, depth)
+    return ctx, octx
+
+
+CASES = [
+    ((16, 16, 16), 1, 0), ((16, 16, 16), 2, 1), ((16, 16, 16), 3, 2), ((32, 32, 32), 4, 3),
+    ((16, 32, 48), 3, 4), ((32, 32), 3, 5), ((64, 32), 4, 6), ((16, 16), 1, 7),
+]
+
+
+@pytest.mark.parametrize("shape,depth,seed", CASES)
+def test_level_images_and_z_bitexact(b200, oracle, shape, depth, seed):
+    t = scenes.random_types(shape, 10 + seed)
+    p = oracle.init_params(len(shape), depth, 20 + seed)
+    ctx, octx = make(b200, oracle, t, depth, p)
+    for l, want in enumerate(oracle.level_images(t, depth)):
+        got = ctx.level_image(l)
+        assert np.array_equal(got, want), f"level {l}"
+    za, zb = ctx.linear_coeffs()
+    oza, ozb = octx.z()
+    assert np.array_equal(za, oza) and np.array_equal(zb, ozb)
+    assert np.array_equal(ctx.fluid_indices(), octx.fluid_indices())
+
+
+@pytest.mark.parametrize("shape,depth,seed", CASES)
+def test_net_apply_bitwise(b200, oracle, shape, depth, seed):
+    t = scenes.random_types(shape, 30 + seed)
+    p = oracle.init_params(len(shape), depth, 40 + seed)
+    ctx, octx = make(b200, oracle, t, depth, p)
+    x = np.random.default_rng(seed).standard_normal(shape).astype(np.float32)
+    got = ctx.net_apply(x)
+    want = octx.net_apply(x)
+    assert rel_l2(got, want) <= REL_L2
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("shape,depth,seed", [((32, 32), 3, 0), ((64, 64), 4, 1), ((16, 48), 2, 2)])
+def test_net_apply_2d_vs_reference_bitwise(b200, oracle, ref, shape, depth, seed):
+    t = scenes.random_types(shape, 50 + seed)
+    p = oracle.init_params(2, depth, 60 + seed)
+    ctx, _ = make(b200, oracle, t, depth, p)
+    x = np.random.default_rng(seed).standard_normal(shape).astype(np.float32)
+    want, _, _ = ref.net_apply_2d(t, p, depth, x)
+    assert np.array_equal(ctx.net_apply(x).view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("shape,depth,seed", CASES)
+def test_precond_apply(b200, oracle, shape, depth, seed):
+    t = scenes.random_types(shape, 70 + seed)
+    p = oracle.init_params(len(shape), depth, 80 + seed)
+    ctx, octx = make(b200, oracle, t, depth, p)
+    r = np.random.default_rng(seed).standard_normal(ctx.n_fluid)
+    assert rel_l2(ctx.precond_apply(r), octx.precond_apply(r)) <= REL_L2
+    assert np.all(ctx.precond_apply(np.zeros_like(r)) == 0.0)  # test_neural.cpp:258-261
+
+
+@pytest.mark.parametrize("shape,seed", [((16, 16, 16), 0), ((32, 24, 16), 1), ((32, 32), 2), ((8, 8, 8), 3)])
+def test_spmv_bitwise(b200, oracle, shape, seed):
+    t = scenes.random_types(shape, 90 + seed)
+    p = oracle.identity_params(len(shape), 1)
+    ctx, octx = make(b200, oracle, t, 1, p)
+    x = np.random.default_rng(seed).standard_normal(ctx.n_fluid)
+    assert np.array_equal(ctx.spmv(x), octx.spmv(x))
+
+
+@pytest.mark.parametrize("name,n,depth", [("C1", 32, 4), ("C2", 32, 3), ("C3", 32, 4), ("C1", 64, 4)])
+def test_psdo_identity_weights_iteration_parity(b200, oracle, name, n, depth):
+    """Identity-equivalent weights (the only convergent weights):
+    iterations to rel-res 1e-6 within +-1 of the oracle psdo_solve (which is
+    bitwise the reference solver, tests/test_oracle_pinning.py)."""
+    t, seed = scenes.config(name, n)
+    p = oracle.identity_params(3, depth)
+    ctx, octx = make(b200, oracle, t, depth, p)
+    b = oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    cfg = b200.SolveConfig(max_iters=5000)
+    got = ctx.psdo_solve(b, cfg)
+    want = octx.psdo_solve(b, max_iters=5000)
+    assert got.report.converged and want["converged"]
+    assert abs(got.report.iterations - want["iterations"]) <= 1
+    assert got.report.residual_history[-1] <= 1e-6 * got.report.residual_history[0]
+    assert rel_l2(got.x, want["x"]) <= 1e-5
+
+
+@pytest.mark.parametrize("n_ortho", [0, 1, 2, 4])
+def test_psdo_random_weights_history(b200, oracle, n_ortho):
+    """Fixed 50-iteration budget with random weights: residual history within
+    1e-6 relative of the oracle."""
+    t = scenes.dam_break(16)
+    p = oracle.init_params(3, 3, 42)
+    ctx, octx = make(b200, oracle, t, 3, p)
+    b = oracle.rhs_normal(1235, t.size)[t.reshape(-1) == 0]
+    got = ctx.psdo_solve(b, b200.SolveConfig(max_iters=50, tol_reduction=1e-300, n_ortho=n_ortho))
+    want = octx.psdo_solve(b, max_iters=50, tol_reduction=1e-300, n_ortho=n_ortho)
+    assert got.report.iterations == want["iterations"] == 50
+    h, w = got.report.residual_history, want["residual_history"]
+    assert np.max(np.abs(h - w) / w) <= 1e-6
+
+
+def test_psdo_2d_vs_reference(b200, oracle, ref):
+    t = np.zeros((64, 64), np.uint8)
+    c = np.arange(64) + 0.5
+    y, x = np.meshgrid(c, c, indexing="ij")
+    t[y >= 48] = 1
+    t[(x < 19.2) & (y < 12.8)] = 2
+    p = oracle.identity_params(2, 3)
+    ctx, _ = make(b200, oracle, t, 3, p)
+    b = ref.rhs_normal(13, ctx.n_fluid)
+    got = ctx.psdo_solve(b, b200.SolveConfig(max_iters=3000))
+    want = ref.psdo_solve(t, b, mode="neural", params=p, depth=3, max_iters=3000)
+    assert got.report.converged and want["converged"]
+    assert abs(got.report.iterations - want["iterations"]) <= 1
+
+
+def test_nullspace_projection_pure_neumann(b200, oracle):
+    """test_solvers.cpp:307-320 on the B200: all-fluid closed box, singular
+    system, solved under mean projection."""
+    t = np.zeros((16, 16, 16), np.uint8)
+    p = oracle.identity_params(3, 2)
+    ctx, octx = make(b200, oracle, t, 2, p)
+    b = oracle.rhs_normal(21, t.size)
+    b -= b.mean()
+    cfg = b200.SolveConfig(max_iters=2000, nullspace_projection=True)
+    got = ctx.psdo_solve(b, cfg)
+    want = octx.psdo_solve(b, max_iters=2000, nullspace_projection=True)
+    assert got.report.converged and want["converged"]
+    assert abs(got.report.iterations - want["iterations"]) <= 1
+
+
+def test_max_iters_and_history_length(b200, oracle):
+    t = scenes.closed_box_half(16)
+    ctx, _ = make(b200, oracle, t, 2, oracle.identity_params(3, 2))
+    b = oracle.rhs_normal(22, t.size)[t.reshape(-1) == 0]
+    res = ctx.psdo_solve(b, b200.SolveConfig(max_iters=3))
+    assert not res.report.converged
+    assert res.report.iterations == 3 and res.report.residual_history.size == 4  # test_solvers.cpp:322-331
+
+
+def test_errors(b200, oracle):
+    t = scenes.closed_box_half(16)
+    P = b200.NeuralPrecond(b200.init_params(2, 5), t)
+    b = np.ones(P.size())
+    with pytest.raises(ValueError):
+        b200.psdo_solve(None, b, P, b200.SolveConfig(tol_reduction=1.5))
+    with pytest.raises(ValueError):
+        b200.psdo_solve(None, np.ones(3), P)
+    bad = b.copy()
+    bad[3] = np.nan
+    with pytest.raises(ValueError):
+        b200.psdo_solve(None, bad, P)
+    with pytest.raises(ValueError):
+        b200.Context(3, (12, 12, 12), b200.init_params(3, 1))  # not divisible by 2^3
+    with pytest.raises(b200.EmptySystemError):
+        Q = b200.NeuralPrecond(b200.init_params(2, 5), np.full((16, 16, 16), 1, np.uint8))
+        b200.psdo_solve(None, np.zeros(0), Q)
+
+
+def test_breakdown_raises(b200, oracle):
+    """A preconditioner whose output is A-orthogonal to nothing useful: zero
+    weights give d = 0 -> curvature 0 -> SolverBreakdown (solver.cpp:247-250)."""
+    t = scenes.closed_box_half(16)
+    p = np.zeros(oracle.param_count(3, 2), np.float32)
+    P = b200.NeuralPrecond(b200.NetParams(3, 2, p), t)
+    b = oracle.rhs_normal(1, t.size)[t.reshape(-1) == 0]
+    with pytest.raises(b200.SolverBreakdown):
+        b200.psdo_solve(None, b, P, b200.SolveConfig(max_iters=10))
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("dim", [2, 3])
+def test_dropin_reference_solver_with_b200_precond(b200, oracle, ref, dim):
+    """The drop-in check: the reference's own psdo_solve (solver.cpp:189-276)
+    driving the B200 NeuralPrecond through the C ABI (a C callback), against the
+    same reference solver driving the CPU network."""
+    if dim == 2:
+        t = scenes.random_types((32, 32), 5, p=(0.7, 0.2, 0.1))
+    else:
+        t = scenes.dam_break(16)
+    depth = 3
+    p = oracle.init_params(dim, depth, 9)
+    P = b200.NeuralPrecond(b200.NetParams(dim, depth, p), t)
+    n = P.size()
+
+    def cb(user, r_ptr, z_ptr, nn):
+        r = np.ctypeslib.as_array(r_ptr, shape=(nn,))
+        z = np.ctypeslib.as_array(z_ptr, shape=(nn,))
+        z[:] = P.apply(r.copy())
+        return 0
+
+    b = ref.rhs_normal(3, n)
+    got = ref.psdo_solve(t, b, mode="callback", callback=cb, max_iters=15, tol_reduction=1e-300)
+    want = ref.psdo_solve(t, b, mode="neural", params=p, depth=depth, max_iters=15, tol_reduction=1e-300)
+    h, w = got["residual_history"], want["residual_history"]
+    assert np.max(np.abs(h - w) / w) <= 1e-6
+
+
+def test_set_mask_frames_no_resetup(b200, oracle):
+    """C4 pattern: one context, per-frame set_mask only; each frame matches a
+    fresh oracle context."""
+    p = oracle.init_params(3, 3, 5)
+    ctx = b200.Context(3, (32, 32, 32), b200.NetParams(3, 3, p))
+    for f, t in enumerate(scenes.droplet_frames(32, 4)):
+        ctx.set_mask(t)
+        octx = oracle.context(t, p, 3)
+        r = np.random.default_rng(f).standard_normal(ctx.n_fluid)
+        assert rel_l2(ctx.precond_apply(r), octx.precond_apply(r)) <= REL_L2
+
+
+def test_solve_device_path(b200, oracle):
+    """Device-resident full-grid API == host reduced API."""
+    t = scenes.closed_box_half(32)
+    P = b200.identity_params(4)
+    ctx = b200.Context(3, t.shape, P)
+    ctx.set_mask(t)
+    bf = scenes.full_rhs(t, 1234, oracle.rhs_normal)
+    cfg = b200.SolveConfig(max_iters=2000)
+    host = ctx.psdo_solve(bf[t.reshape(-1) == 0], cfg)
+    db = b200.DeviceBuffer(ctx, bf.nbytes)
+    dx = b200.DeviceBuffer(ctx, bf.nbytes)
+    db.upload(bf)
+    rep = ctx.psdo_solve_device(db.ptr, dx.ptr, cfg)
+    xf = np.empty_like(bf)
+    dx.download(xf)
+    ctx.synchronize()
+    assert rep.iterations == host.report.iterations
+    assert np.array_equal(xf[t.reshape(-1) == 0], host.x)
+    assert np.all(xf[t.reshape(-1) != 0] == 0.0)
+    db.free()
+    dx.free()
