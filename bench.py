@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py — neural-preconditioned PSDO ("DCDM") time-to-solution on B200.
+
+Metric (BASELINE.json): time-to-solution in ms to relative residual 1e-6 at
+256^3 (config C3: free-surface droplet-in-pool), plus per-
+iteration ms and HBM GB/s. One step = one frame: set_mask (flags, coarsened
+masks, mixed-window kernel tables, linear-block coefficients) + the whole PSDO
+solve to 1e-6, with the cell types and the RHS already resident in HBM.
+Identity-equivalent weights (the only deterministic convergent
+weight set — no trained 3D weights exist); the network still runs in full every
+iteration, and per-iteration cost does not depend on weight values.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 (torchrun): replicas — every rank solves its own copy of the frame
+(weak scaling); the z-slab sharded path is not built yet.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "DCDM time-to-solution ms (rel-res 1e-6) at 256^3; per-iter ms; HBM GB/s"
+UNIT = "ms"
+
+
+# ------------------------------------------------------------ byte model
+def canonical_bytes_per_cell(depth: int) -> dict[str, float]:
+    """SURVEY.md §8d canonical algorithmic bytes per fine cell per PSDO
+    iteration, split by the kernel that implements each phase."""
+    m = {"net_down_L0": 13.5, "net_up_L0": 45.5, "ortho": 49.0, "update": 41.0}
+    for l in range(1, depth - 1):
+        m[f"net_down_L{l}"] = 20.5 / 8 ** l
+        m[f"net_up_L{l}"] = 20.5 / 8 ** l
+    m[f"net_coarse_L{depth - 1}"] = 20.0 / 8 ** (depth - 1)
+    return m
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int) -> None:
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self) -> None:
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        loaded = [s for s in sm if s > 0.5 * smax] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+# -------------------------------------------------------------- workload
+def workload(args):
+    from paper_2310_00177_b200 import scenes
+
+    types, seed = scenes.config(args.config, args.n)
+    return types, seed
+
+
+def iteration_count_fixture(config: str) -> int | None:
+    p = ROOT / "tests" / "golden" / "iteration_counts.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        if config in d:
+            return int(d[config]["iterations"])
+    return None
+
+
+# ------------------------------------------------------------- CPU legs
+def cpu_reference_sample(types, seed, depth, iters_to_solution, sample_iters, cores):
+    """Reference psdo_solve (oracle/_ref: the unmodified reference solver,
+    assembly and reduce, with the 3D network restatement as its
+    Preconditioner) on a bounded sample: full setup + `sample_iters` PSDO
+    iterations on the same 256^3 frame. Time-to-solution = setup +
+    iterations-to-solution x measured per-iteration time."""
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import Ref  # checker / baseline only
+
+    ref = Ref()
+    import paper_2310_00177_b200 as b200
+
+    p = b200.identity_params(depth).flat
+    b = ref.rhs_normal(seed, types.size)[types.reshape(-1) == 0]
+    t0 = time.perf_counter()
+    r = ref.psdo_solve(types, b, mode="neural", params=p, depth=depth, max_iters=sample_iters,
+                       tol_reduction=1e-300)
+    wall = time.perf_counter() - t0
+    per_iter_ms = 1e3 * r["solve_seconds"] / sample_iters
+    setup_ms = 1e3 * r["setup_seconds"]
+    return {
+        "value": setup_ms + iters_to_solution * per_iter_ms,
+        "unit": UNIT,
+        "cores": cores,
+        "kind": "reference",
+        "sample": (f"{types.shape[0]}^3 {args_config_name}: reference assemble_poisson_3d+reduce+NeuralPrecond3D setup "
+                   f"({setup_ms:.0f} ms) + {sample_iters} PSDO iterations ({per_iter_ms:.1f} ms/iter); TTS = setup + "
+                   f"{iters_to_solution} iterations x per-iter (extrapolated); {wall:.1f} s wall"),
+        "setup_ms": setup_ms,
+        "per_iter_ms": per_iter_ms,
+    }
+
+
+args_config_name = "C3"
+
+
+# ------------------------------------------------------------- reference arm
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    global args_config_name
+    args_config_name = args.config
+    types, seed = workload(args)
+    n_iters = iteration_count_fixture(args.config) if args.n is None else None
+    if n_iters is None:
+        n_iters = args.ref_iters
+    cores = os.cpu_count() or 1
+    vals, samples = [], []
+    for step in range(args.warmup + args.steps):
+        s = cpu_reference_sample(types, seed, args.depth, n_iters, args.cpu_sample_iters, cores)
+        if step >= args.warmup:
+            vals.append(s["value"])
+            samples.append(s)
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 solver / f32 network", "data": "synthetic",
+        "config": {"workload": f"{args.config} {types.shape[0]}^3 (SURVEY §8d)", "weights": "identity-equivalent",
+                   "depth": args.depth, "iterations_to_solution": n_iters,
+                   "iterations_source": "tests/golden/iteration_counts.json (reference psdo_solve run to 1e-6)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": samples[-1]["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "per_iter_ms": float(np.mean([s["per_iter_ms"] for s in samples])),
+        "setup_ms": float(np.mean([s["setup_ms"] for s in samples])),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args) -> None:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # plumbing only: barrier + max over ranks (CPU/gloo)
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    import paper_2310_00177_b200 as b200
+    from paper_2310_00177_b200 import scenes
+
+    global args_config_name
+    args_config_name = args.config
+    types, seed = workload(args)
+    n_c = types.size
+    depth = args.depth
+    params = b200.identity_params(depth) if args.weights == "identity" else b200.init_params(depth, 42)
+    ctx = b200.Context(3, types.shape, params, device=local)
+    bfull = scenes.full_rhs(types, seed, b200.rhs_normal)
+    cfg = b200.SolveConfig(tol_reduction=1e-6, max_iters=args.max_iters, n_ortho=2)
+
+    # device-resident inputs
+    d_types = b200.DeviceBuffer(ctx, n_c)
+    d_b = b200.DeviceBuffer(ctx, 8 * n_c)
+    d_x = b200.DeviceBuffer(ctx, 8 * n_c)
+    d_types.upload(np.ascontiguousarray(types.reshape(-1)))
+    d_b.upload(bfull)
+    ctx.synchronize()
+
+    def step():
+        ctx.event_record(0)
+        ctx.set_mask_device(d_types.ptr)
+        rep = ctx.psdo_solve_device(d_b.ptr, d_x.ptr, cfg)
+        ctx.event_record(1)
+        return ctx.event_elapsed_ms(0, 1), rep, ctx.last_solve_ms
+
+    for _ in range(args.warmup):
+        step()
+    if dist:
+        dist.barrier()
+    ctx.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    launches0 = ctx.launch_count
+    ms, iters, solve_ms, converged = [], [], [], []
+    for _ in range(args.steps):
+        t, rep, sm = step()
+        ms.append(t)
+        iters.append(rep.iterations)
+        solve_ms.append(sm)
+        converged.append(rep.converged)
+    ctx.synchronize()
+    launches = (ctx.launch_count - launches0) / args.steps
+    clocks = clk.stop()
+    step_ms = float(np.mean(ms))
+    if dist:
+        import torch
+
+        t = torch.tensor([step_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = float(t.item())
+    n_it = int(np.median(iters))
+    per_iter_ms = float(np.mean([s / max(i, 1) for s, i in zip(solve_ms, iters)]))
+    setup_ms = step_ms - float(np.mean(solve_ms))
+    model = canonical_bytes_per_cell(depth)
+    b_iter = sum(model.values()) * n_c
+    peaks = load_peaks()
+    iter_gbs = b_iter / (per_iter_ms * 1e-3) / 1e9
+
+    # per-kernel device times (kernels launched one by one between events)
+    prof = ctx.profile_iterations(d_b.ptr, cfg, args.profile_iters)
+    dom = max(prof, key=prof.get)
+    dom_bytes = model.get(dom, 0.0) * n_c
+    dom_gbs = dom_bytes / (prof[dom] * 1e-3) / 1e9
+    prof_total = sum(prof.values())
+
+    # end to end through the public host API: pinned host inputs, H2D each step,
+    # solution read back each step (host wall clock around the synchronous calls)
+    n_f = int((types == 0).sum())
+    p_types = b200.PinnedBuffer(ctx, n_c, np.uint8)
+    p_b = b200.PinnedBuffer(ctx, n_f, np.float64)
+    p_x = b200.PinnedBuffer(ctx, n_f, np.float64)
+    p_types.array[:] = types.reshape(-1)
+    p_b.array[:] = bfull[types.reshape(-1) == 0]
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        ctx.set_mask(p_types.array)
+        res = ctx.psdo_solve(p_b.array, cfg, out=p_x.array)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e.append(1e3 * (t1 - t0))
+    e2e_ms = float(np.mean(e2e))
+    hist_bytes = 8 * (res.report.iterations + 1) * 2
+    if dist:
+        import torch
+
+        t = torch.tensor([e2e_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(types, seed, depth, n_it, args.cpu_sample_iters, os.cpu_count() or 1)
+            cpu.pop("setup_ms", None)
+            cpu.pop("per_iter_ms", None)
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": step_ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64 solver / f32 network", "data": "synthetic",
+            "config": {
+                "workload": f"{args.config} {types.shape[0]}^3 droplet-in-pool (SURVEY §8d), one frame per step: "
+                            "set_mask + PSDO to rel-res 1e-6",
+                "n_fluid": n_f, "depth": depth, "n_ortho": 2, "weights": args.weights,
+                "iterations": n_it, "converged": bool(all(converged)),
+                "parallelism": "replicas" if world > 1 else "single",
+                "l2": "inputs larger than L2 (solver vectors 8 B x n_c each, ~134 MB at 256^3, >= 126 MB L2)",
+            },
+            "per_iter_ms": per_iter_ms,
+            "setup_ms": setup_ms,
+            "hbm_gbs_iteration": iter_gbs,
+            "iteration_roofline": {"bound": "hbm", "achieved": iter_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                   "frac": iter_gbs / peaks["hbm_gbs"],
+                                   "bytes": f"canonical B_iter = {sum(model.values()):.2f} B x n_c (SURVEY §8d)",
+                                   "peak_source": peaks["source"]},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": dom_gbs / peaks["hbm_gbs"], "traffic": None,
+                         "bytes_per_launch": dom_bytes, "ms_per_launch": prof[dom],
+                         "share_of_iteration": prof[dom] / prof_total, "peak_source": peaks["source"]},
+            "kernel_ms": prof,
+            "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(n_c + 8 * n_f),
+                    "d2h_bytes_per_step": int(8 * n_f + hist_bytes),
+                    "how": "Context.set_mask(pinned types) + Context.psdo_solve(pinned b) -> pinned x; host wall clock"},
+            "gpu_launches": int(round(launches)),
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    for buf in (d_types, d_b, d_x):
+        buf.free()
+    for buf in (p_types, p_b, p_x):
+        buf.free()
+    ctx.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3"])
+    ap.add_argument("--n", type=int, default=None, help="override the grid size of the config")
+    ap.add_argument("--depth", type=int, default=4)
+    ap.add_argument("--weights", default="identity", choices=["identity", "random"])
+    ap.add_argument("--max-iters", type=int, default=20000)
+    ap.add_argument("--profile-iters", type=int, default=5)
+    ap.add_argument("--cpu-sample-iters", type=int, default=2)
+    ap.add_argument("--ref-iters", type=int, default=1000, help="iterations-to-solution if no fixture exists")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,19 @@ int npsd_b200_synchronize(npsd_b200_ctx* ctx);
 double npsd_b200_last_solve_ms(const npsd_b200_ctx* ctx);
 /* Kernel launches issued by the last solve (graph nodes executed). */
 int64_t npsd_b200_last_solve_launches(const npsd_b200_ctx* ctx);
+/* Cumulative kernel launches executed for this context (all calls). */
+int64_t npsd_b200_launch_count(const npsd_b200_ctx* ctx);
+
+/* CUDA events on the context stream (16 slots) for caller-side device timing. */
+int npsd_b200_event_record(npsd_b200_ctx* ctx, int slot);
+double npsd_b200_event_elapsed_ms(npsd_b200_ctx* ctx, int slot_a, int slot_b); /* waits for b; <0 on error */
+
+/* Per-kernel device time of `iters` PSDO iterations launched one by one
+ * between CUDA events (no graph) on device full-grid b; writes the mean ms per
+ * kernel into ms_out and NUL-terminated kernel names (name_len bytes each).
+ * *n_kernels: capacity in, count out. Leaves no solve state behind. */
+int npsd_b200_profile_iterations(npsd_b200_ctx* ctx, const double* d_b_full, const npsd_b200_solve_cfg* cfg,
+                                 int iters, double* ms_out, int* n_kernels, char* names, int name_len);
 
 #ifdef __cplusplus
 }

@@ -241,9 +241,11 @@ class Context:
                            float(rep.iterate_seconds), float(rep.precond_seconds), method)
 
     def psdo_solve(self, b: np.ndarray, cfg: SolveConfig, x0: np.ndarray | None = None,
-                   method: str = "psdo+neural") -> SolveResult:
+                   method: str = "psdo+neural", out: np.ndarray | None = None) -> SolveResult:
         b = np.ascontiguousarray(b, np.float64)
-        x = np.empty_like(b)
+        x = np.empty_like(b) if out is None else out
+        if x.dtype != np.float64 or x.size != b.size or not x.flags.c_contiguous:
+            raise ValueError("solve: out must be a contiguous f64 array of the rhs length")
         rep = _native.Report()
         x0p = None
         if x0 is not None:
@@ -279,6 +281,32 @@ class Context:
     @property
     def last_solve_launches(self) -> int:
         return int(self.lib.npsd_b200_last_solve_launches(self.h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.npsd_b200_launch_count(self.h))
+
+    def event_record(self, slot: int) -> None:
+        self._ck(self.lib.npsd_b200_event_record(self.h, slot))
+
+    def event_elapsed_ms(self, a: int, b: int) -> float:
+        ms = float(self.lib.npsd_b200_event_elapsed_ms(self.h, a, b))
+        if ms < 0:
+            raise DeviceError("event_elapsed_ms failed")
+        return ms
+
+    def profile_iterations(self, b_ptr: int, cfg: SolveConfig, iters: int) -> dict[str, float]:
+        """Mean device ms per kernel of `iters` PSDO iterations, kernels launched
+        one by one between CUDA events on the context stream."""
+        cap, nl = 64, 32
+        ms = np.zeros(cap, np.float64)
+        n = C.c_int(cap)
+        names = C.create_string_buffer(cap * nl)
+        c = cfg._c()
+        self._ck(self.lib.npsd_b200_profile_iterations(self.h, C.c_void_p(b_ptr), C.byref(c), int(iters), ms,
+                                                       C.byref(n), names, nl))
+        raw = names.raw
+        return {raw[k * nl:(k + 1) * nl].split(b"\0")[0].decode(): float(ms[k]) for k in range(n.value)}
 
 
 class DeviceBuffer:

@@ -19,6 +19,8 @@ EXPORTED_SYMBOLS = (
     "npsd_b200_param_count", "npsd_b200_init_params", "npsd_b200_identity_params", "npsd_b200_rhs_normal",
     "npsd_b200_device_alloc", "npsd_b200_device_free", "npsd_b200_host_alloc", "npsd_b200_host_free",
     "npsd_b200_memcpy", "npsd_b200_synchronize", "npsd_b200_last_solve_ms", "npsd_b200_last_solve_launches",
+    "npsd_b200_launch_count", "npsd_b200_event_record", "npsd_b200_event_elapsed_ms",
+    "npsd_b200_profile_iterations",
 )
 
 
@@ -85,5 +87,12 @@ def lib() -> C.CDLL:
     L.npsd_b200_last_solve_ms.argtypes = [_vp]
     L.npsd_b200_last_solve_launches.restype = C.c_int64
     L.npsd_b200_last_solve_launches.argtypes = [_vp]
+    L.npsd_b200_launch_count.restype = C.c_int64
+    L.npsd_b200_launch_count.argtypes = [_vp]
+    L.npsd_b200_event_record.argtypes = [_vp, C.c_int]
+    L.npsd_b200_event_elapsed_ms.restype = C.c_double
+    L.npsd_b200_event_elapsed_ms.argtypes = [_vp, C.c_int, C.c_int]
+    L.npsd_b200_profile_iterations.argtypes = [_vp, _vp, C.POINTER(SolveCfg), C.c_int, _f64p, C.POINTER(C.c_int),
+                                               C.c_char_p, C.c_int]
     _lib = L
     return L

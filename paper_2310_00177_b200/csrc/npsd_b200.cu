@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -105,6 +106,9 @@ struct npsd_b200_ctx {
     int exec_nullspace = -1;
     int body_launches = 0, prologue_launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t user_ev[16] = {};
+    std::vector<cudaEvent_t> prof_ev;
+    long long launches = 0;  // kernels executed on behalf of API calls
     float last_ms = 0.0f;
     long long last_launches = 0;
     std::vector<double> report_hist, report_times;
@@ -140,6 +144,7 @@ int grid_for(npsd_b200_ctx* c, K kernel, long long items) {
         const int g_ = grid_for(c, kfn_, (items));                          \
         kfn_<<<g_, kBlock, 0, (stream)>>>(__VA_ARGS__);                      \
         CK(cudaGetLastError());                                              \
+        ++(c)->launches;                                                     \
     } while (0)
 
 Geom level_geom(const npsd_b200_ctx* c, int l) {
@@ -188,6 +193,7 @@ void scan_u32(npsd_b200_ctx* c, const uint32_t* in, uint32_t* out, long long n) 
         c->cub_bytes = bytes;
     }
     CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, in, out, (int)n, c->s));
+    c->launches += 2;  // cub: tile-state init + scan
 }
 
 template <int D>
@@ -203,6 +209,7 @@ void upload_params_and_kconst(npsd_b200_ctx* c) {
             k_kconst<D><<<1, 96, 0, c->s>>>(c->d_params + c->coarse_W, c->d_params + c->coarse_B, L.kc_down);
         }
         CK(cudaGetLastError());
+        c->launches += (l < c->depth - 1) ? 2 : 1;
     }
 }
 
@@ -248,6 +255,7 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
             k_zfinal<D><<<1, 32, 0, s>>>(L.g, L.zG, scale, c->d_params + o.a_K, c->params[o.a_bias],
                                          c->d_params + o.b_K, c->params[o.b_bias], c->zab + 2 * l, c->zab + 2 * l + 1);
             CK(cudaGetLastError());
+            ++c->launches;
         } else {
             LAUNCH(c, s, k_build_table<D>, L.g.n, L.g, st, im, L.cls, L.mmask, L.mbase, c->d_params + c->coarse_W,
                    c->d_params + c->coarse_B, L.tab_down, L.g.n);
@@ -269,55 +277,131 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
 }
 
 // ------------------------------------------------------------ network
+// One named launcher per kernel of an iteration: the graph body is captured
+// from these, and the profiler runs them one by one between CUDA events.
+struct Step {
+    std::string name;
+    std::function<void(cudaStream_t)> run;
+};
+
 template <int D>
-void launch_network(npsd_b200_ctx* c, cudaStream_t s, bool raw, int* launches) {
+std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw) {
+    std::vector<Step> v;
     const int Ld = c->depth;
-    int n = 0;
-    // down sweep
     for (int l = 0; l < Ld; ++l) {
-        LevelBufs& L = c->L[l];
         const bool pool = (l + 1 < Ld);
-        const Geom gc = pool ? c->L[l + 1].g : L.g;
-        float* xnext = pool ? c->L[l + 1].x : nullptr;
-        const long long nb = L.g.n / ((D == 3) ? 8 : 4);
-        if (l == 0 && !raw) {
-            if (pool)
-                LAUNCH(c, s, (k_down<D, true, true>), nb, L.g, nullptr, c->R, c->st, tab_down(c, l), L.y, xnext, gc);
-            else
-                LAUNCH(c, s, (k_down<D, true, false>), nb, L.g, nullptr, c->R, c->st, tab_down(c, l), L.y, xnext, gc);
-        } else {
-            const float* in = (l == 0) ? c->xin_f : L.x;
-            if (pool)
-                LAUNCH(c, s, (k_down<D, false, true>), nb, L.g, in, nullptr, c->st, tab_down(c, l), L.y, xnext, gc);
-            else
-                LAUNCH(c, s, (k_down<D, false, false>), nb, L.g, in, nullptr, c->st, tab_down(c, l), L.y, xnext, gc);
-        }
-        ++n;
+        const std::string nm = (l == Ld - 1) ? "net_coarse_L" + std::to_string(l) : "net_down_L" + std::to_string(l);
+        v.push_back({nm, [c, l, pool, raw](cudaStream_t s) {
+                         LevelBufs& L = c->L[l];
+                         const Geom gc = pool ? c->L[l + 1].g : L.g;
+                         float* xnext = pool ? c->L[l + 1].x : nullptr;
+                         const long long nb = L.g.n / ((D == 3) ? 8 : 4);
+                         if (l == 0 && !raw) {
+                             if (pool)
+                                 LAUNCH(c, s, (k_down<D, true, true>), nb, L.g, nullptr, c->R, c->st, tab_down(c, l), L.y,
+                                        xnext, gc);
+                             else
+                                 LAUNCH(c, s, (k_down<D, true, false>), nb, L.g, nullptr, c->R, c->st, tab_down(c, l), L.y,
+                                        xnext, gc);
+                         } else {
+                             const float* in = (l == 0) ? c->xin_f : L.x;
+                             if (pool)
+                                 LAUNCH(c, s, (k_down<D, false, true>), nb, L.g, in, nullptr, c->st, tab_down(c, l), L.y,
+                                        xnext, gc);
+                             else
+                                 LAUNCH(c, s, (k_down<D, false, false>), nb, L.g, in, nullptr, c->st, tab_down(c, l),
+                                        L.y, xnext, gc);
+                         }
+                     }});
     }
-    // up sweep
     for (int l = Ld - 2; l >= 0; --l) {
-        LevelBufs& L = c->L[l];
-        const LevelBufs& Lc = c->L[l + 1];
-        const float* outc = (l + 1 == Ld - 1) ? Lc.y : Lc.out;
-        const long long nb = L.g.n / ((D == 3) ? 8 : 4);
-        if (l == 0 && !raw) {
-            LAUNCH(c, s, (k_up<D, kUpL0>), nb, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), nullptr, c->Dtmp,
-                   c->st, c->ADring, c->partials, c->counter);
-        } else {
-            float* outl = (l == 0) ? c->out_f : L.out;
-            LAUNCH(c, s, (k_up<D, kUpMid>), nb, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), outl, nullptr,
-                   c->st, c->ADring, c->partials, c->counter);
-        }
-        ++n;
+        v.push_back({"net_up_L" + std::to_string(l), [c, l, Ld, raw](cudaStream_t s) {
+                         LevelBufs& L = c->L[l];
+                         const LevelBufs& Lc = c->L[l + 1];
+                         const float* outc = (l + 1 == Ld - 1) ? Lc.y : Lc.out;
+                         const long long nb = L.g.n / ((D == 3) ? 8 : 4);
+                         if (l == 0 && !raw) {
+                             LAUNCH(c, s, (k_up<D, kUpL0>), nb, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), nullptr,
+                                    c->Dtmp, c->st, c->ADring, c->partials, c->counter);
+                         } else {
+                             float* outl = (l == 0) ? c->out_f : L.out;
+                             LAUNCH(c, s, (k_up<D, kUpMid>), nb, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), outl,
+                                    nullptr, c->st, c->ADring, c->partials, c->counter);
+                         }
+                     }});
     }
     if (Ld == 1 && !raw) {
-        LevelBufs& L = c->L[0];
-        const long long nb = L.g.n / ((D == 3) ? 8 : 4);
-        LAUNCH(c, s, (k_up<D, kUpL0Depth1>), nb, L.g, L.g, nullptr, L.y, c->zab, tab_up(c, 0), nullptr, c->Dtmp,
-               c->st, c->ADring, c->partials, c->counter);
-        ++n;
+        v.push_back({"net_out_L0", [c](cudaStream_t s) {
+                         LevelBufs& L = c->L[0];
+                         const long long nb = L.g.n / ((D == 3) ? 8 : 4);
+                         LAUNCH(c, s, (k_up<D, kUpL0Depth1>), nb, L.g, L.g, nullptr, L.y, c->zab, tab_up(c, 0), nullptr,
+                                c->Dtmp, c->st, c->ADring, c->partials, c->counter);
+                     }});
     }
-    if (launches) *launches = n;
+    return v;
+}
+
+template <int D>
+void launch_network(npsd_b200_ctx* c, cudaStream_t s, bool raw, int* launches) {
+    const auto steps = network_steps<D>(c, raw);
+    for (const auto& st : steps) st.run(s);
+    if (launches) *launches = (int)steps.size();
+}
+
+template <int D>
+std::vector<Step> prologue_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h, int use_cond, int nullspace) {
+    std::vector<Step> v;
+    const Geom g = c->g0;
+    const uint8_t* cls = c->L[0].cls;
+    // projections (solver.cpp:197-201), r0 = b - A x0, ||r0||
+    if (nullspace) {
+        v.push_back({"proj_b_sum", [=](cudaStream_t s) {
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->Bf, c->n_fluid, c->st, c->partials, c->counter);
+                     }});
+        v.push_back({"proj_b_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->Bf, c->st); }});
+        v.push_back({"proj_x_sum", [=](cudaStream_t s) {
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->X0, c->n_fluid, c->st, c->partials, c->counter);
+                     }});
+        v.push_back({"proj_x_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->X0, c->st); }});
+    }
+    v.push_back({"residual0", [=](cudaStream_t s) { LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R); }});
+    if (nullspace) {
+        v.push_back({"proj_r0_sum", [=](cudaStream_t s) {
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, c->n_fluid, c->st, c->partials, c->counter);
+                     }});
+        v.push_back({"proj_r0_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->R, c->st); }});
+    }
+    v.push_back({"norm0", [=](cudaStream_t s) {
+                     LAUNCH(c, s, k_residual_norm, g.n, g, c->R, c->st, c->hist, c->times, c->partials, c->counter, h,
+                            use_cond, 1);
+                 }});
+    return v;
+}
+
+template <int D>
+std::vector<Step> body_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h, int use_cond, int nullspace) {
+    std::vector<Step> v = network_steps<D>(c, false);
+    const Geom g = c->g0;
+    const uint8_t* cls = c->L[0].cls;
+    v.push_back({"ortho", [=](cudaStream_t s) {
+                     LAUNCH(c, s, k_ortho<D>, g.n, g, cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
+                            c->counter);
+                 }});
+    v.push_back({"update", [=](cudaStream_t s) {
+                     LAUNCH(c, s, k_update<D>, g.n, g, cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist, c->times,
+                            c->partials, c->counter, h, use_cond, nullspace ? 0 : 1);
+                 }});
+    if (nullspace) {
+        v.push_back({"proj_r_sum", [=](cudaStream_t s) {
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, c->n_fluid, c->st, c->partials, c->counter);
+                     }});
+        v.push_back({"proj_r_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->R, c->st); }});
+        v.push_back({"norm", [=](cudaStream_t s) {
+                         LAUNCH(c, s, k_residual_norm, g.n, g, c->R, c->st, c->hist, c->times, c->partials, c->counter,
+                                h, use_cond, 0);
+                     }});
+    }
+    return v;
 }
 
 void ensure_ring(npsd_b200_ctx* c, int ring) {
@@ -357,8 +441,6 @@ void capture_solve_graph(npsd_b200_ctx* c, int nullspace) {
         c->exec = nullptr;
     }
     cudaStream_t s = c->s, s2 = c->s2;
-    const Geom g = c->g0;
-    const uint8_t* cls = c->L[0].cls;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     cudaStreamCaptureStatus cs;
     cudaGraph_t cg = nullptr;
@@ -367,24 +449,8 @@ void capture_solve_graph(npsd_b200_ctx* c, int nullspace) {
     CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
     cudaGraphConditionalHandle h;
     CK(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
-    int pro = 0;
-    // prologue: projections (solver.cpp:197-201), r0 = b - A x0, ||r0||
-    if (nullspace) {
-        LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->Bf, c->n_fluid, c->st, c->partials, c->counter);
-        LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->Bf, c->st);
-        LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->X0, c->n_fluid, c->st, c->partials, c->counter);
-        LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->X0, c->st);
-        pro += 4;
-    }
-    LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R);
-    ++pro;
-    if (nullspace) {
-        LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, c->n_fluid, c->st, c->partials, c->counter);
-        LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->R, c->st);
-        pro += 2;
-    }
-    LAUNCH(c, s, k_residual_norm, g.n, g, c->R, c->st, c->hist, c->times, c->partials, c->counter, h, 1);
-    ++pro;
+    const auto pro = prologue_steps<D>(c, h, 1, nullspace);
+    for (const auto& st : pro) st.run(s);
     // while (!done) { one PSDO iteration }
     CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
     cudaGraphNodeParams cp = {};
@@ -397,19 +463,8 @@ void capture_solve_graph(npsd_b200_ctx* c, int nullspace) {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
     CK(cudaStreamBeginCaptureToGraph(s2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    int nbody = 0;
-    launch_network<D>(c, s2, false, &nbody);
-    LAUNCH(c, s2, k_ortho<D>, g.n, g, cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials, c->counter);
-    ++nbody;
-    LAUNCH(c, s2, k_update<D>, g.n, g, cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist, c->times, c->partials,
-           c->counter, h, nullspace ? 0 : 1);
-    ++nbody;
-    if (nullspace) {
-        LAUNCH(c, s2, k_fluid_sum, g.n, g, cls, c->R, c->n_fluid, c->st, c->partials, c->counter);
-        LAUNCH(c, s2, k_subtract_mean, g.n, g, cls, c->R, c->st);
-        LAUNCH(c, s2, k_residual_norm, g.n, g, c->R, c->st, c->hist, c->times, c->partials, c->counter, h, 0);
-        nbody += 3;
-    }
+    const auto bod = body_steps<D>(c, h, 1, nullspace);
+    for (const auto& st : bod) st.run(s2);
     cudaGraph_t body_out = nullptr;
     CK(cudaStreamEndCapture(s2, &body_out));
     cudaGraph_t graph = nullptr;
@@ -421,8 +476,9 @@ void capture_solve_graph(npsd_b200_ctx* c, int nullspace) {
     c->exec_key[2] = c->ADring;
     c->exec_key[3] = c->partials;
     c->exec_nullspace = nullspace;
-    c->body_launches = nbody;
-    c->prologue_launches = pro;
+    c->body_launches = (int)bod.size();
+    c->prologue_launches = (int)pro.size();
+    c->launches -= (long long)(bod.size() + pro.size());  // captured, not executed
 }
 
 // Runs the solve on c->Bf / c->X0 (already masked). Returns the status.
@@ -465,6 +521,7 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
     CK(cudaStreamSynchronize(c->s));
     c->last_launches = c->prologue_launches + (h->breakdown ? (iters * c->body_launches + c->body_launches)
                                                             : iters * c->body_launches);
+    c->launches += c->last_launches;
     c->report_hist.assign(c->hist_host, c->hist_host + hl);
     c->report_times.assign(c->times_host, c->times_host + hl);
     if (rep) {
@@ -925,5 +982,92 @@ int npsd_b200_synchronize(npsd_b200_ctx* c) {
 
 double npsd_b200_last_solve_ms(const npsd_b200_ctx* c) { return c ? (double)c->last_ms : 0.0; }
 int64_t npsd_b200_last_solve_launches(const npsd_b200_ctx* c) { return c ? c->last_launches : 0; }
+
+int npsd_b200_event_record(npsd_b200_ctx* c, int slot) {
+    return guarded(c, [&] {
+        require(slot >= 0 && slot < 16, "event slot out of range");
+        if (!c->user_ev[slot]) CK(cudaEventCreate(&c->user_ev[slot]));
+        CK(cudaEventRecord(c->user_ev[slot], c->s));
+    });
+}
+
+double npsd_b200_event_elapsed_ms(npsd_b200_ctx* c, int a, int b) {
+    if (!c || a < 0 || b < 0 || a >= 16 || b >= 16 || !c->user_ev[a] || !c->user_ev[b]) return -1.0;
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaSetDevice(c->dev);
+    if (cudaEventSynchronize(c->user_ev[b]) != cudaSuccess) return -1.0;
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, c->user_ev[a], c->user_ev[b]) != cudaSuccess) return -1.0;
+    return (double)ms;
+}
+
+int64_t npsd_b200_launch_count(const npsd_b200_ctx* c) { return c ? c->launches : 0; }
+
+int npsd_b200_profile_iterations(npsd_b200_ctx* c, const double* d_b, const npsd_b200_solve_cfg* cfg, int iters,
+                                 double* ms_out, int* n_out, char* names, int name_len) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(cfg != nullptr && d_b != nullptr && iters > 0 && n_out != nullptr, "profile: bad arguments");
+        if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
+        const Geom g = c->g0;
+        const uint8_t* cls = c->L[0].cls;
+        LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_b, c->Bf);
+        CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
+        const int ring = cfg->n_ortho + 1;
+        require(cfg->n_ortho >= 0 && cfg->n_ortho <= kMaxOrtho, "psdo: n_ortho out of range");
+        ensure_ring(c, ring);
+        ensure_hist(c, (long long)iters + 1);
+        SolverState* h = c->st_host;
+        std::memset(h, 0, sizeof(SolverState));
+        h->tol_reduction = 1e-300;
+        h->max_iters = iters;
+        h->n_ortho = cfg->n_ortho;
+        h->normalize = cfg->normalize_before_precond ? 1 : 0;
+        h->ring = ring;
+        CK(cudaMemcpyAsync(c->st, h, sizeof(SolverState), cudaMemcpyHostToDevice, c->s));
+        const int ns = cfg->nullspace_projection ? 1 : 0;
+        std::vector<Step> pro, bod;
+        if (c->dim == 3) {
+            pro = prologue_steps<3>(c, 0, 0, ns);
+            bod = body_steps<3>(c, 0, 0, ns);
+        } else {
+            pro = prologue_steps<2>(c, 0, 0, ns);
+            bod = body_steps<2>(c, 0, 0, ns);
+        }
+        for (const auto& st : pro) st.run(c->s);
+        const size_t nk = bod.size();
+        while (c->prof_ev.size() < nk + 1) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            c->prof_ev.push_back(e);
+        }
+        std::vector<double> acc(nk, 0.0);
+        for (int it = 0; it < iters; ++it) {
+            for (size_t k = 0; k < nk; ++k) {
+                CK(cudaEventRecord(c->prof_ev[k], c->s));
+                bod[k].run(c->s);
+            }
+            CK(cudaEventRecord(c->prof_ev[nk], c->s));
+            CK(cudaEventSynchronize(c->prof_ev[nk]));
+            for (size_t k = 0; k < nk; ++k) {
+                float ms = 0.0f;
+                CK(cudaEventElapsedTime(&ms, c->prof_ev[k], c->prof_ev[k + 1]));
+                acc[k] += ms;
+            }
+        }
+        const int cap = *n_out;
+        *n_out = (int)nk;
+        for (size_t k = 0; k < nk && (int)k < cap; ++k) {
+            if (ms_out) ms_out[k] = acc[k] / iters;
+            if (names && name_len > 0) {
+                std::strncpy(names + k * (size_t)name_len, bod[k].name.c_str(), (size_t)name_len - 1);
+                names[k * (size_t)name_len + name_len - 1] = 0;
+            }
+        }
+        CK(cudaStreamSynchronize(c->s));
+        // the profiled iterations leave the solver vectors dirty at fluid cells
+        // only; the zero invariant at non-fluid cells still holds.
+    });
+}
 
 }  // extern "C"

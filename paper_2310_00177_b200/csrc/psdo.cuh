@@ -162,8 +162,12 @@ __global__ void __launch_bounds__(kBlock) k_residual(Geom g, const uint8_t* __re
     }
 }
 
+__device__ __forceinline__ void set_cond(cudaGraphConditionalHandle cond, int use_cond, unsigned v) {
+    if (use_cond) cudaGraphSetConditional(cond, v);
+}
+
 __device__ __forceinline__ void finish_iteration(SolverState* st, double rsq, double* hist, double* times,
-                                                 cudaGraphConditionalHandle cond, bool initial) {
+                                                 cudaGraphConditionalHandle cond, int use_cond, bool initial) {
     const double rn = sqrt(rsq);
     st->rnorm = rn;
     const unsigned long long now = globaltimer();
@@ -197,16 +201,16 @@ __device__ __forceinline__ void finish_iteration(SolverState* st, double rsq, do
         st->k = k + 1;
     }
     if (!st->done) set_precond_scales(st);
-    cudaGraphSetConditional(cond, st->done ? 0u : 1u);
+    set_cond(cond, use_cond, st->done ? 0u : 1u);
 }
 
 // ||r||^2 over the (already projected) residual, then bookkeeping.
 __global__ void __launch_bounds__(kBlock) k_residual_norm(Geom g, const double* __restrict__ r, SolverState* st,
                                                           double* __restrict__ hist, double* __restrict__ times,
                                                           double* __restrict__ partials, unsigned int* __restrict__ counter,
-                                                          cudaGraphConditionalHandle cond, int initial) {
+                                                          cudaGraphConditionalHandle cond, int use_cond, int initial) {
     if (!initial && st->breakdown) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cond, use_cond, 0u);
         return;
     }
     double acc[1] = {0.0};
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(kBlock) k_residual_norm(Geom g, const double* 
     }
     double tot[1];
     if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0)
-        finish_iteration(st, tot[0], hist, times, cond, initial != 0);
+        finish_iteration(st, tot[0], hist, times, cond, use_cond, initial != 0);
 }
 
 // --------------------------------------------------------------- ortho
@@ -296,9 +300,9 @@ __global__ void __launch_bounds__(kBlock) k_update(Geom g, const uint8_t* __rest
                                                    const double* __restrict__ Dring, double* __restrict__ r,
                                                    SolverState* st, double* __restrict__ hist, double* __restrict__ times,
                                                    double* __restrict__ partials, unsigned int* __restrict__ counter,
-                                                   cudaGraphConditionalHandle cond, int do_norm) {
+                                                   cudaGraphConditionalHandle cond, int use_cond, int do_norm) {
     if (st->breakdown) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cond, use_cond, 0u);
         return;
     }
     const double alpha = st->alpha;
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(kBlock) k_update(Geom g, const uint8_t* __rest
     if (!do_norm) return;  // nullspace projection: norm after k_subtract_mean
     double tot[1];
     if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0)
-        finish_iteration(st, tot[0], hist, times, cond, false);
+        finish_iteration(st, tot[0], hist, times, cond, use_cond, false);
 }
 
 }  // namespace nb2

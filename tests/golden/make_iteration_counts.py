@@ -1,0 +1,32 @@
+"""Generates tests/golden/iteration_counts.json: iterations to rel-res 1e-6 of the
+REFERENCE psdo_solve (oracle/_ref: solver.cpp:189-276 on assemble_poisson_3d +
+reduce, IdentityPrecond — what identity-equivalent network weights reduce to,
+SURVEY.md §0.4) on the benchmark domains. bench.py's --impl reference arm uses
+the count to turn its bounded per-iteration sample into a time-to-solution.
+Run here (needs oracle/_ref); takes minutes at 256^3."""
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+from oracle_lib import Ref  # noqa: E402
+from paper_2310_00177_b200 import scenes  # noqa: E402
+
+out = ROOT / "tests" / "golden" / "iteration_counts.json"
+res = json.loads(out.read_text()) if out.exists() else {}
+ref = Ref()
+for name in sys.argv[1:] or ["C1", "C2", "C3"]:
+    t, seed = scenes.config(name)
+    b = ref.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    t0 = time.time()
+    r = ref.psdo_solve(t, b, mode="identity", max_iters=20000, tol_reduction=1e-6, n_ortho=2)
+    res[name] = {"n": int(t.shape[0]), "n_fluid": int(b.size), "iterations": r["iterations"],
+                 "converged": r["converged"], "final_rel_res": float(r["residual_history"][-1] / r["residual_history"][0]),
+                 "solver": "reference psdo_solve + IdentityPrecond, n_ortho=2, tol 1e-6",
+                 "cpu_seconds": time.time() - t0}
+    print(name, res[name], flush=True)
+    out.write_text(json.dumps(res, indent=1) + "\n")
