@@ -20,6 +20,8 @@
 #include "net.cuh"
 #include "psdo.cuh"
 #include "setup.cuh"
+#include "stencil.cuh"
+#include "net2.cuh"
 
 using namespace nb2;
 
@@ -81,6 +83,7 @@ struct npsd_b200_ctx {
     float* d_params = nullptr;
     LevelBufs L[kMaxDepth];
     float* zab = nullptr;  // [depth][2]
+    KC kc_down[kMaxDepth], kc_up[kMaxDepth], kc_coarse;  // host copies of the uniform kernels
     uint32_t *fmask = nullptr, *fbase = nullptr, *fcount = nullptr;
     long long n_fluid = 0;
     bool mask_ok = false;
@@ -92,6 +95,8 @@ struct npsd_b200_ctx {
     SolverState* st_host = nullptr;  // pinned
     double* partials = nullptr;
     unsigned int* counter = nullptr;
+    double* partials2 = nullptr;      // grid_reduce2: group partials
+    unsigned int* counters2 = nullptr;  // grid_reduce2: [final, per-group]
     double *hist = nullptr, *times = nullptr;
     long long hist_cap = 0;
     double *hist_host = nullptr, *times_host = nullptr;
@@ -103,7 +108,7 @@ struct npsd_b200_ctx {
     // solve graph
     cudaGraphExec_t exec = nullptr;
     const void* exec_key[4] = {nullptr, nullptr, nullptr, nullptr};
-    int exec_nullspace = -1;
+    int exec_nullspace = -1, exec_no = -1;
     int body_launches = 0, prologue_launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t user_ev[16] = {};
@@ -211,6 +216,29 @@ void upload_params_and_kconst(npsd_b200_ctx* c) {
         CK(cudaGetLastError());
         c->launches += (l < c->depth - 1) ? 2 : 1;
     }
+    // host copies, passed by value to the tiled network kernels
+    const size_t kb = 3 * (size_t)c->S * sizeof(float);
+    for (int l = 0; l < c->depth; ++l) {
+        std::memset(&c->kc_down[l], 0, sizeof(KC));
+        std::memset(&c->kc_up[l], 0, sizeof(KC));
+        float tmp[81];
+        if (l < c->depth - 1) {
+            CK(cudaMemcpyAsync(tmp, c->L[l].kc_down, kb, cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            for (int t = 0; t < 3; ++t)
+                for (int k = 0; k < c->S; ++k) c->kc_down[l].k[t][k] = tmp[t * c->S + k];
+            CK(cudaMemcpyAsync(tmp, c->L[l].kc_up, kb, cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            for (int t = 0; t < 3; ++t)
+                for (int k = 0; k < c->S; ++k) c->kc_up[l].k[t][k] = tmp[t * c->S + k];
+        } else {
+            CK(cudaMemcpyAsync(tmp, c->L[l].kc_down, kb, cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            std::memset(&c->kc_coarse, 0, sizeof(KC));
+            for (int t = 0; t < 3; ++t)
+                for (int k = 0; k < c->S; ++k) c->kc_coarse.k[t][k] = tmp[t * c->S + k];
+        }
+    }
 }
 
 ConvTab tab_down(const npsd_b200_ctx* c, int l) {
@@ -284,50 +312,157 @@ struct Step {
     std::function<void(cudaStream_t)> run;
 };
 
+// Launch of a tiled kernel on an explicit 3D grid.
+#define LAUNCH3(c, stream, kernel, grid, block, ...)                         \
+    do {                                                                     \
+        auto kfn_ = kernel;                                                  \
+        kfn_<<<(grid), (block), 0, (stream)>>>(__VA_ARGS__);                 \
+        CK(cudaGetLastError());                                              \
+        ++(c)->launches;                                                     \
+    } while (0)
+
+// Launch with dynamic shared memory.
+#define LAUNCH3S(c, stream, kernel, grid, block, smem, ...)                  \
+    do {                                                                     \
+        auto kfn_ = kernel;                                                  \
+        kfn_<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
+        CK(cudaGetLastError());                                              \
+        ++(c)->launches;                                                     \
+    } while (0)
+
+// z-chunk (in bricks or planes) so that a launch has about two waves of blocks.
+template <typename K>
+int zchunk_for(npsd_b200_ctx* c, K kernel, int threads, long long tiles_xy, int nz_units, size_t smem = 0) {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
+    if (occ < 1) occ = 1;
+    const long long target = 2LL * c->num_sms * occ;
+    long long zc = (tiles_xy * nz_units + target - 1) / target;
+    if (zc < 1) zc = 1;
+    if (zc > nz_units) zc = nz_units;
+    return (int)zc;
+}
+
+template <int D, bool L0, bool POOL>
+void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, const double* in_d) {
+    LevelBufs& L = c->L[l];
+    const Geom gc = POOL ? c->L[l + 1].g : L.g;
+    float* xnext = POOL ? c->L[l + 1].x : nullptr;
+    const dim3 block(kNX, kNY);
+    const int gx = (L.g.nx + 2 * kNX - 1) / (2 * kNX), gy = (L.g.ny + 2 * kNY - 1) / (2 * kNY);
+    const int nbz = (D == 3) ? (L.g.nz >> 1) : 1;
+    auto k = k_down3<D, L0, POOL>;
+    const int zc = zchunk_for(c, k, kNX * kNY, (long long)gx * gy, nbz);
+    const dim3 grid(gx, gy, (nbz + zc - 1) / zc);
+    const KC& kc = (l == c->depth - 1) ? c->kc_coarse : c->kc_down[l];
+    LAUNCH3(c, s, k, grid, block, L.g, in_f, in_d, c->st, tab_down(c, l), kc, L.y, xnext, gc, zc);
+}
+
+template <int D, int MODE, int NO>
+void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dout) {
+    LevelBufs& L = c->L[l];
+    const LevelBufs& Lc = c->L[l + 1];
+    const float* outc = (l + 1 == c->depth - 1) ? Lc.y : Lc.out;
+    const dim3 block(kNX, kNY);
+    const int gx = (Lc.g.nx + kNX - 1) / kNX, gy = (Lc.g.ny + kNY - 1) / kNY;
+    const int nbz = (D == 3) ? Lc.g.nz : 1;
+    auto k = k_up3<D, MODE, NO>;
+    const int zc = zchunk_for(c, k, kNX * kNY, (long long)gx * gy, nbz);
+    const dim3 grid(gx, gy, (nbz + zc - 1) / zc);
+    LAUNCH3(c, s, k, grid, block, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), c->kc_up[l], outl, dout, c->st,
+            c->ADring, c->partials, c->counter, zc);
+}
+
+template <int D, int NO>
+void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
+    launch_up<D, kUpL0, NO>(c, s, 0, nullptr, c->Dtmp);
+}
+
+// n_ortho (the cache bound) is a template parameter of the kernels that loop
+// over the cached directions; dispatch once at launch-build time.
 template <int D>
-std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw) {
+void launch_up0_no(npsd_b200_ctx* c, cudaStream_t s, int no) {
+    switch (no) {
+        case 0: launch_up0<D, 0>(c, s); break;
+        case 1: launch_up0<D, 1>(c, s); break;
+        case 2: launch_up0<D, 2>(c, s); break;
+        case 3: launch_up0<D, 3>(c, s); break;
+        case 4: launch_up0<D, 4>(c, s); break;
+        default: launch_up0<D, kMaxOrtho>(c, s); break;
+    }
+}
+
+template <int D, int NO>
+void launch_ortho(npsd_b200_ctx* c, cudaStream_t s) {
+    const Geom g = c->g0;
+    const dim3 block(kSX, kSY);
+    const int gx = (g.nx + kTX - 1) / kTX, gy = (g.ny + kTY - 1) / kTY;
+    auto k = k_ortho2<D, NO>;
+    const size_t sm = march_smem_bytes<OrthoOp<NO>>();
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int zc = zchunk_for(c, k, kSX * kSY, (long long)gx * gy, g.nz, sm);
+    const dim3 grid(gx, gy, (g.nz + zc - 1) / zc);
+    LAUNCH3S(c, s, k, grid, block, sm, g, c->L[0].cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
+             c->counter, zc);
+}
+
+template <int D>
+void launch_ortho_no(npsd_b200_ctx* c, cudaStream_t s, int no) {
+    switch (no) {
+        case 0: launch_ortho<D, 0>(c, s); break;
+        case 1: launch_ortho<D, 1>(c, s); break;
+        case 2: launch_ortho<D, 2>(c, s); break;
+        case 3: launch_ortho<D, 3>(c, s); break;
+        case 4: launch_ortho<D, 4>(c, s); break;
+        default: launch_ortho<D, kMaxOrtho>(c, s); break;
+    }
+}
+
+template <int D>
+void launch_update(npsd_b200_ctx* c, cudaStream_t s, cudaGraphConditionalHandle h, int use_cond, int do_norm) {
+    const Geom g = c->g0;
+    const dim3 block(kSX, kSY);
+    const int gx = (g.nx + kTX - 1) / kTX, gy = (g.ny + kTY - 1) / kTY;
+    auto k = k_update2<D>;
+    const size_t sm = march_smem_bytes<UpdateOp>();
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int zc = zchunk_for(c, k, kSX * kSY, (long long)gx * gy, g.nz, sm);
+    const dim3 grid(gx, gy, (g.nz + zc - 1) / zc);
+    LAUNCH3S(c, s, k, grid, block, sm, g, c->L[0].cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist, c->times,
+             c->partials, c->counter, h, use_cond, do_norm, zc);
+}
+
+// One named launcher per kernel of an iteration: the graph body is captured
+// from these, and the profiler runs them one by one between CUDA events.
+// raw: the network on an f32 full-grid input (xin_f -> out_f), no solver.
+template <int D>
+std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     std::vector<Step> v;
     const int Ld = c->depth;
     for (int l = 0; l < Ld; ++l) {
         const bool pool = (l + 1 < Ld);
         const std::string nm = (l == Ld - 1) ? "net_coarse_L" + std::to_string(l) : "net_down_L" + std::to_string(l);
         v.push_back({nm, [c, l, pool, raw](cudaStream_t s) {
-                         LevelBufs& L = c->L[l];
-                         const Geom gc = pool ? c->L[l + 1].g : L.g;
-                         float* xnext = pool ? c->L[l + 1].x : nullptr;
-                         const long long nb = L.g.n / ((D == 3) ? 8 : 4);
                          if (l == 0 && !raw) {
                              if (pool)
-                                 LAUNCH(c, s, (k_down<D, true, true>), nb, L.g, nullptr, c->R, c->st, tab_down(c, l), L.y,
-                                        xnext, gc);
+                                 launch_down<D, true, true>(c, s, 0, nullptr, c->R);
                              else
-                                 LAUNCH(c, s, (k_down<D, true, false>), nb, L.g, nullptr, c->R, c->st, tab_down(c, l), L.y,
-                                        xnext, gc);
+                                 launch_down<D, true, false>(c, s, 0, nullptr, c->R);
                          } else {
-                             const float* in = (l == 0) ? c->xin_f : L.x;
+                             const float* in = (l == 0) ? c->xin_f : c->L[l].x;
                              if (pool)
-                                 LAUNCH(c, s, (k_down<D, false, true>), nb, L.g, in, nullptr, c->st, tab_down(c, l), L.y,
-                                        xnext, gc);
+                                 launch_down<D, false, true>(c, s, l, in, nullptr);
                              else
-                                 LAUNCH(c, s, (k_down<D, false, false>), nb, L.g, in, nullptr, c->st, tab_down(c, l),
-                                        L.y, xnext, gc);
+                                 launch_down<D, false, false>(c, s, l, in, nullptr);
                          }
                      }});
     }
     for (int l = Ld - 2; l >= 0; --l) {
-        v.push_back({"net_up_L" + std::to_string(l), [c, l, Ld, raw](cudaStream_t s) {
-                         LevelBufs& L = c->L[l];
-                         const LevelBufs& Lc = c->L[l + 1];
-                         const float* outc = (l + 1 == Ld - 1) ? Lc.y : Lc.out;
-                         const long long nb = L.g.n / ((D == 3) ? 8 : 4);
-                         if (l == 0 && !raw) {
-                             LAUNCH(c, s, (k_up<D, kUpL0>), nb, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), nullptr,
-                                    c->Dtmp, c->st, c->ADring, c->partials, c->counter);
-                         } else {
-                             float* outl = (l == 0) ? c->out_f : L.out;
-                             LAUNCH(c, s, (k_up<D, kUpMid>), nb, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), outl,
-                                    nullptr, c->st, c->ADring, c->partials, c->counter);
-                         }
+        v.push_back({"net_up_L" + std::to_string(l), [c, l, raw, no](cudaStream_t s) {
+                         if (l == 0 && !raw)
+                             launch_up0_no<D>(c, s, no);
+                         else
+                             launch_up<D, kUpMid, 0>(c, s, l, (l == 0) ? c->out_f : c->L[l].out, nullptr);
                      }});
     }
     if (Ld == 1 && !raw) {
@@ -343,7 +478,7 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw) {
 
 template <int D>
 void launch_network(npsd_b200_ctx* c, cudaStream_t s, bool raw, int* launches) {
-    const auto steps = network_steps<D>(c, raw);
+    const auto steps = network_steps<D>(c, raw, 0);
     for (const auto& st : steps) st.run(s);
     if (launches) *launches = (int)steps.size();
 }
@@ -379,18 +514,12 @@ std::vector<Step> prologue_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h,
 }
 
 template <int D>
-std::vector<Step> body_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h, int use_cond, int nullspace) {
-    std::vector<Step> v = network_steps<D>(c, false);
+std::vector<Step> body_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h, int use_cond, int nullspace, int no) {
+    std::vector<Step> v = network_steps<D>(c, false, no);
     const Geom g = c->g0;
     const uint8_t* cls = c->L[0].cls;
-    v.push_back({"ortho", [=](cudaStream_t s) {
-                     LAUNCH(c, s, k_ortho<D>, g.n, g, cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
-                            c->counter);
-                 }});
-    v.push_back({"update", [=](cudaStream_t s) {
-                     LAUNCH(c, s, k_update<D>, g.n, g, cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist, c->times,
-                            c->partials, c->counter, h, use_cond, nullspace ? 0 : 1);
-                 }});
+    v.push_back({"ortho", [=](cudaStream_t s) { launch_ortho_no<D>(c, s, no); }});
+    v.push_back({"update", [=](cudaStream_t s) { launch_update<D>(c, s, h, use_cond, nullspace ? 0 : 1); }});
     if (nullspace) {
         v.push_back({"proj_r_sum", [=](cudaStream_t s) {
                          LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, c->n_fluid, c->st, c->partials, c->counter);
@@ -435,7 +564,7 @@ void ensure_hist_host(npsd_b200_ctx* c, long long need) {
 }
 
 template <int D>
-void capture_solve_graph(npsd_b200_ctx* c, int nullspace) {
+void capture_solve_graph(npsd_b200_ctx* c, int nullspace, int no) {
     if (c->exec) {
         CK(cudaGraphExecDestroy(c->exec));
         c->exec = nullptr;
@@ -463,7 +592,7 @@ void capture_solve_graph(npsd_b200_ctx* c, int nullspace) {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
     CK(cudaStreamBeginCaptureToGraph(s2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    const auto bod = body_steps<D>(c, h, 1, nullspace);
+    const auto bod = body_steps<D>(c, h, 1, nullspace, no);
     for (const auto& st : bod) st.run(s2);
     cudaGraph_t body_out = nullptr;
     CK(cudaStreamEndCapture(s2, &body_out));
@@ -476,6 +605,7 @@ void capture_solve_graph(npsd_b200_ctx* c, int nullspace) {
     c->exec_key[2] = c->ADring;
     c->exec_key[3] = c->partials;
     c->exec_nullspace = nullspace;
+    c->exec_no = no;
     c->body_launches = (int)bod.size();
     c->prologue_launches = (int)pro.size();
     c->launches -= (long long)(bod.size() + pro.size());  // captured, not executed
@@ -494,8 +624,8 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
     ensure_hist(c, max_iters + 1);
     const int nullspace = cfg->nullspace_projection ? 1 : 0;
     if (!c->exec || c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist || c->exec_key[2] != c->ADring ||
-        c->exec_nullspace != nullspace)
-        capture_solve_graph<D>(c, nullspace);
+        c->exec_nullspace != nullspace || c->exec_no != cfg->n_ortho)
+        capture_solve_graph<D>(c, nullspace, cfg->n_ortho);
     SolverState* h = c->st_host;
     std::memset(h, 0, sizeof(SolverState));
     h->tol_reduction = cfg->tol_reduction;
@@ -605,6 +735,8 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->ADring);
     F(c->st);
     F(c->partials);
+    F(c->partials2);
+    F(c->counters2);
     F(c->counter);
     F(c->hist);
     F(c->times);
@@ -709,9 +841,17 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
         c->st = dalloc<SolverState>(1);
         CK(cudaMemset(c->st, 0, sizeof(SolverState)));
         CK(cudaMallocHost(&c->st_host, sizeof(SolverState)));
-        c->partials = dalloc<double>((size_t)c->num_sms * 8 * (2 + kMaxOrtho));
         c->counter = dalloc<unsigned int>(1);
         CK(cudaMemset(c->counter, 0, sizeof(unsigned int)));
+        {
+            // the pair-stencil grids: one block per 64 x 4 x 1 tile
+            const long long nblk = ((long long)(nx + 63) / 64) * ((ny + 3) / 4) * nz;
+            const long long ngrp = (nblk + 127) / 128;
+            c->partials = dalloc<double>((size_t)std::max<long long>(65536, nblk) * (2 + kMaxOrtho));
+            c->partials2 = dalloc<double>((size_t)ngrp * (2 + kMaxOrtho));
+            c->counters2 = dalloc<unsigned int>((size_t)ngrp + 1);
+            CK(cudaMemset(c->counters2, 0, ((size_t)ngrp + 1) * sizeof(unsigned int)));
+        }
         ensure_ring(c, 3);
         ensure_hist(c, 1001);
         do_set_params(c, params, n_params);
@@ -1029,10 +1169,10 @@ int npsd_b200_profile_iterations(npsd_b200_ctx* c, const double* d_b, const npsd
         std::vector<Step> pro, bod;
         if (c->dim == 3) {
             pro = prologue_steps<3>(c, 0, 0, ns);
-            bod = body_steps<3>(c, 0, 0, ns);
+            bod = body_steps<3>(c, 0, 0, ns, cfg->n_ortho);
         } else {
             pro = prologue_steps<2>(c, 0, 0, ns);
-            bod = body_steps<2>(c, 0, 0, ns);
+            bod = body_steps<2>(c, 0, 0, ns, cfg->n_ortho);
         }
         for (const auto& st : pro) st.run(c->s);
         const size_t nk = bod.size();

@@ -1,0 +1,375 @@
+// Kernels for the two stencil phases of a PSDO iteration (solver.cpp:239-258):
+// k_ortho2 (d' = MGS(d), A d', dots) and k_update2 (x' = x + alpha d',
+// r = b - A x', ||r||^2).
+//
+// Asynchronous-copy pipeline. A 32 x 8 block owns a 64 x 8 x-y tile (each
+// thread a pair of x-adjacent cells) and marches a z-chunk. Each thread
+// copies, with cp.async (LDGSTS, no register staging), the inputs of its own
+// pair and of its halo assignment for the plane PF steps ahead into a ring of
+// shared-memory stages; a copy whose pair holds no fluid cell is issued with
+// src-size 0, which zero-fills without touching DRAM (exact, by the zero
+// invariant of the solver vectors). Every thread reads back only what it
+// copied itself, so the input ring needs no barriers. The operand v (d' or
+// x') is formed once per cell into a 4-plane shared ring with its halo; one
+// barrier per step; the 7-point rows are then evaluated from shared memory in
+// reduced-CSR column order with round-to-nearest ops, bit-identical to spmv
+// (sparse.cpp:111-116) on assemble_poisson_3d + reduce.
+#pragma once
+
+#include "common.cuh"
+#include "psdo.cuh"
+
+namespace nb2 {
+
+constexpr int kSX = 32, kSY = 8;          // threads per block (x lanes, y rows)
+constexpr int kTX = 2 * kSX, kTY = kSY;    // cells per block tile (64 x 8)
+constexpr int kVW = kTX + 4, kVH = kTY + 2;  // staged plane: cols x0-2..x0+65, rows y0-1..y0+8
+constexpr int kPF = 2;                     // planes prefetched ahead
+constexpr int kST = kPF + 1;               // input ring stages
+constexpr unsigned kOut2 = 0x0C0Cu;        // pair bytes outside the domain: type 3
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Row sum in the reduced-CSR column order; out-of-domain / non-fluid
+// neighbours are exact zeros and `s + -0.0 == s`, so adding them is bitwise
+// neutral (see psdo.cuh).
+__device__ __forceinline__ double row_sum(double vzm, double vym, double vxm, int diag, double vc, double vxp, double vyp,
+                                          double vzp) {
+    double s = 0.0;
+    s = __dadd_rn(s, -vzm);
+    s = __dadd_rn(s, -vym);
+    s = __dadd_rn(s, -vxm);
+    if (diag > 0) s = __dadd_rn(s, __dmul_rn((double)diag, vc));
+    s = __dadd_rn(s, -vxp);
+    s = __dadd_rn(s, -vyp);
+    s = __dadd_rn(s, -vzp);
+    return s;
+}
+
+__device__ __forceinline__ bool fluid(unsigned b) { return ((b >> 2) & 3u) == 0u; }
+__device__ __forceinline__ bool pair_live(unsigned b2) { return fluid(b2 & 0xffu) || fluid(b2 >> 8); }
+
+// Ortho operand (NA = 1 + NO inputs): d' = d + (-p_1) d_1 + ... (axpy order).
+template <int NO>
+struct OrthoOp {
+    static constexpr int NA = 1 + NO;  // d, d_1..d_NO
+    static constexpr int NC = 1;       // r (centre only)
+    const double* in[NA];
+    const double* ctr[NC];
+    double mp[NO > 0 ? NO : 1];
+    int nc;
+    __device__ __forceinline__ double value(const double (&a)[NA]) const {
+        double r = a[0];
+#pragma unroll
+        for (int j = 0; j < NO; ++j)
+            if (j < nc) r = __dadd_rn(r, __dmul_rn(mp[j], a[1 + j]));
+        return r;
+    }
+};
+// Update operand: x' = x + alpha d'.
+struct UpdateOp {
+    static constexpr int NA = 2;  // x, d'
+    static constexpr int NC = 1;  // b (centre only)
+    const double* in[NA];
+    const double* ctr[NC];
+    double alpha;
+    __device__ __forceinline__ double value(const double (&a)[NA]) const {
+        return __dadd_rn(a[0], __dmul_rn(alpha, a[1]));
+    }
+};
+
+template <typename Op>
+struct MarchSmem {
+    double raw[kST][Op::NA][kVH][kVW];  // operand inputs, tile + halo
+    double ctr[kST][Op::NC][kTY][kTX];  // centre-only inputs
+    double v[4][kVH][kVW];              // operand ring
+};
+
+// Epi(q, v2 own pair, s2 rows, pair bytes, own raw inputs [NA] x 2, centre [NC] x 2, acc)
+template <int D, int NV, typename Op, typename Epi>
+__device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __restrict__ cls, const Op& op, int zc0,
+                                              int zc1, double (&acc)[NV], Epi epi) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    MarchSmem<Op>& S = *reinterpret_cast<MarchSmem<Op>*>(smem_raw);
+    const int lane = threadIdx.x, row = threadIdx.y;
+    const int X0 = blockIdx.x * kTX, Y0 = blockIdx.y * kTY;
+    const int x = X0 + 2 * lane, y = Y0 + row;
+    const bool own = x < g.nx && y < g.ny;  // nx even: the pair is whole
+    const long long nx = g.nx, plane = nx * g.ny;
+    // halo assignment: rows 0/1 -> pair of row y0-1 / y0+8; row 2, lanes 0..15 -> column x0-1 / x0+64
+    int hx = 0, hy = 0, hsr = 0, hsc = 0;
+    int hkind = 0;  // 0 none, 1 pair, 2 single cell
+    if (row == 0 || row == 1) {
+        hkind = 1;
+        hx = x;
+        hy = (row == 0) ? Y0 - 1 : Y0 + kTY;
+        hsr = (row == 0) ? 0 : kVH - 1;
+        hsc = 2 + 2 * lane;
+    } else if (row == 2 && lane < 2 * kTY) {
+        hkind = 2;
+        hx = (lane < kTY) ? X0 - 1 : X0 + kTX;
+        hy = Y0 + (lane & (kTY - 1));
+        hsr = 1 + (lane & (kTY - 1));
+        hsc = (lane < kTY) ? 1 : kTX + 2;  // smem column c <-> global x0 - 2 + c
+    }
+    const bool h_in = hkind != 0 && hx >= 0 && hx < g.nx && hy >= 0 && hy < g.ny;
+    const long long qo = (long long)(own ? y : 0) * nx + (own ? x : 0);
+    const long long qh = h_in ? (long long)hy * nx + hx : 0;
+    auto zin = [&](int z) { return z >= 0 && z < g.nz; };
+    auto own_bytes = [&](int z) -> unsigned {
+        return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
+    };
+    auto halo_live = [&](int z) -> bool {
+        if (!h_in || !zin(z)) return false;
+        if (hkind == 1) return pair_live(__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qh)));
+        return fluid(__ldg(cls + z * plane + qh));
+    };
+    auto slot = [&](int z) { return (z - zc0 + 1 + kST * 1024) % kST; };
+    // issue the copies of plane z (one commit group per plane, even if empty)
+    auto issue = [&](int z, unsigned ob, bool hl) {
+        if (zin(z)) {
+            const int s = slot(z);
+            const bool ol = own && pair_live(ob);
+            const long long qz = z * plane;
+#pragma unroll
+            for (int a = 0; a < Op::NA; ++a) {
+                cp_async16(&S.raw[s][a][row + 1][2 + 2 * lane], op.in[a] + (ol ? qz + qo : 0), ol);
+                if (hkind == 1)
+                    cp_async16(&S.raw[s][a][hsr][hsc], op.in[a] + (hl ? qz + qh : 0), hl);
+                else if (hkind == 2)
+                    cp_async8(&S.raw[s][a][hsr][hsc], op.in[a] + (hl ? qz + qh : 0), hl);
+            }
+#pragma unroll
+            for (int a = 0; a < Op::NC; ++a)
+                cp_async16(&S.ctr[s][a][row][2 * lane], op.ctr[a] + (ol ? qz + qo : 0), ol);
+        }
+        cp_commit();
+    };
+    // form v of plane z for my positions (own pair, halo) into v slot z & 3
+    auto form = [&](int z) {
+        const int s = slot(z), vs = (z + 1024) & 3;
+        double a0[Op::NA], a1[Op::NA];
+        if (zin(z)) {
+#pragma unroll
+            for (int a = 0; a < Op::NA; ++a) {
+                a0[a] = S.raw[s][a][row + 1][2 + 2 * lane];
+                a1[a] = S.raw[s][a][row + 1][3 + 2 * lane];
+            }
+            S.v[vs][row + 1][2 + 2 * lane] = op.value(a0);
+            S.v[vs][row + 1][3 + 2 * lane] = op.value(a1);
+            if (hkind != 0) {
+#pragma unroll
+                for (int a = 0; a < Op::NA; ++a) a0[a] = S.raw[s][a][hsr][hsc];
+                S.v[vs][hsr][hsc] = op.value(a0);
+                if (hkind == 1) {
+#pragma unroll
+                    for (int a = 0; a < Op::NA; ++a) a1[a] = S.raw[s][a][hsr][hsc + 1];
+                    S.v[vs][hsr][hsc + 1] = op.value(a1);
+                }
+            }
+        } else {
+            S.v[vs][row + 1][2 + 2 * lane] = 0.0;
+            S.v[vs][row + 1][3 + 2 * lane] = 0.0;
+            if (hkind != 0) S.v[vs][hsr][hsc] = 0.0;
+            if (hkind == 1) S.v[vs][hsr][hsc + 1] = 0.0;
+        }
+    };
+
+    // prologue: bytes and copies of planes zc0-1 .. zc0+PF-1
+    const int zlo = (D == 3) ? zc0 - 1 : zc0;
+    unsigned ob[kPF + 2];  // own bytes of planes z .. z+PF+1 (rotating)
+    bool hl[kPF + 2];
+    unsigned ob_m = own_bytes(zlo);
+    issue(zlo, ob_m, halo_live(zlo));
+    if (D == 3) {
+#pragma unroll
+        for (int k = 0; k < kPF + 2; ++k) {
+            ob[k] = own_bytes(zc0 + k);
+            hl[k] = halo_live(zc0 + k);
+        }
+#pragma unroll
+        for (int k = 0; k < kPF; ++k) issue(zc0 + k, ob[k], hl[k]);
+        cp_wait<kPF - 1>();  // planes zc0-1, zc0 landed (own copies)
+        form(zc0 - 1);
+        form(zc0);
+    } else {
+        ob[0] = ob_m;
+        cp_wait<0>();
+        form(zc0);
+    }
+    for (int z = zc0; z < zc1; ++z) {
+        if (D == 3) {
+            issue(z + kPF, ob[kPF], hl[kPF]);  // the plane kPF steps ahead
+            cp_wait<kPF - 1>();                 // plane z+1 landed
+            form(z + 1);
+        }
+        __syncthreads();  // v of planes z-1, z, z+1 complete (halos included)
+        const unsigned bc = ob[0];
+        if (own && pair_live(bc)) {
+            const int vm = (z + 1023) & 3, vc = (z + 1024) & 3, vp = (z + 1025) & 3;
+            const int c0 = 2 + 2 * lane, r0 = row + 1;
+            const double v0 = S.v[vc][r0][c0], v1 = S.v[vc][r0][c0 + 1];
+            const double zm0 = (D == 3) ? S.v[vm][r0][c0] : 0.0, zm1 = (D == 3) ? S.v[vm][r0][c0 + 1] : 0.0;
+            const double zp0 = (D == 3) ? S.v[vp][r0][c0] : 0.0, zp1 = (D == 3) ? S.v[vp][r0][c0 + 1] : 0.0;
+            double2 s;
+            s.x = fluid(bc & 0xffu) ? row_sum(zm0, S.v[vc][r0 - 1][c0], S.v[vc][r0][c0 - 1], cls_diag(bc & 0xffu), v0,
+                                              v1, S.v[vc][r0 + 1][c0], zp0)
+                                    : 0.0;
+            s.y = fluid(bc >> 8) ? row_sum(zm1, S.v[vc][r0 - 1][c0 + 1], v0, cls_diag(bc >> 8), v1,
+                                           S.v[vc][r0][c0 + 2], S.v[vc][r0 + 1][c0 + 1], zp1)
+                                 : 0.0;
+            const int sl = slot(z);
+            double raw0[Op::NA], raw1[Op::NA], c0v[Op::NC], c1v[Op::NC];
+#pragma unroll
+            for (int a = 0; a < Op::NA; ++a) {
+                raw0[a] = S.raw[sl][a][r0][c0];
+                raw1[a] = S.raw[sl][a][r0][c0 + 1];
+            }
+#pragma unroll
+            for (int a = 0; a < Op::NC; ++a) {
+                c0v[a] = S.ctr[sl][a][row][2 * lane];
+                c1v[a] = S.ctr[sl][a][row][2 * lane + 1];
+            }
+            epi(z * plane + qo, make_double2(v0, v1), s, bc, raw0, raw1, c0v, c1v, acc);
+        }
+        // rotate the byte queues
+#pragma unroll
+        for (int k = 0; k < kPF + 1; ++k) {
+            ob[k] = ob[k + 1];
+            hl[k] = hl[k + 1];
+        }
+        if (D == 3) {
+            ob[kPF + 1] = own_bytes(z + kPF + 2);
+            hl[kPF + 1] = halo_live(z + kPF + 2);
+        }
+    }
+    cp_wait<0>();
+}
+
+// d' = MGS(d); Ad'; dots d'.Ad', r.d', d_j.Ad'. NO = n_ortho (cache bound).
+template <int D, int NO>
+__global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __restrict__ cls,
+                                                     const double* __restrict__ dtmp, const double* __restrict__ r,
+                                                     double* __restrict__ Dring, double* __restrict__ ADring,
+                                                     SolverState* st, double* __restrict__ partials,
+                                                     unsigned int* __restrict__ counter, int zchunk) {
+    const int nc = st->n_cache, R = st->ring;
+    const int nw = (st->head + 1) % R;
+    using Op = OrthoOp<NO>;
+    Op op;
+    op.in[0] = dtmp;
+    op.ctr[0] = r;
+    op.nc = nc;
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+        const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
+        op.in[1 + j] = Dring + (long long)slot * g.n;
+        op.mp[j] = (j < nc) ? -st->p[j] : 0.0;
+    }
+    double* dnew = Dring + (long long)nw * g.n;
+    double* adnew = ADring + (long long)nw * g.n;
+    constexpr int NV = 2 + (NO > 0 ? NO : 1);
+    double acc[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) acc[j] = 0.0;
+    const int zc0 = blockIdx.z * zchunk;
+    const int zc1 = min(zc0 + zchunk, g.nz);
+    stencil_march<D, NV>(g, cls, op, zc0, zc1, acc,
+                         [&](long long q, double2 v, double2 s, unsigned bc, const double(&i0)[Op::NA],
+                             const double(&i1)[Op::NA], const double(&c0)[1], const double(&c1)[1], double(&a)[NV]) {
+                             *reinterpret_cast<double2*>(dnew + q) = v;
+                             *reinterpret_cast<double2*>(adnew + q) = s;
+                             // non-fluid halves are exact zeros: their terms vanish
+                             a[0] += v.x * s.x;
+                             a[0] += v.y * s.y;
+                             a[1] += c0[0] * v.x;
+                             a[1] += c1[0] * v.y;
+#pragma unroll
+                             for (int j = 0; j < NO; ++j)
+                                 if (j < nc) {
+                                     a[2 + j] += i0[1 + j] * s.x;
+                                     a[2 + j] += i1[1 + j] * s.y;
+                                 }
+                         });
+    double tot[NV];
+    if (grid_reduce<NV>(acc, partials, counter, tot)) {
+        if (threadIdx.x == 0 && threadIdx.y == 0) {
+            const double dAd = tot[0];
+            st->dAd_new = dAd;
+            st->rd_new = tot[1];
+            for (int j = 0; j < nc && j < NO; ++j) {
+                const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
+                st->cross[slot][nw] = tot[2 + j];
+            }
+            if (!(dAd > 0.0) || fabs(dAd) < 1e-300) {
+                st->breakdown = 1;
+                st->done = 1;
+                st->bad_value = dAd;
+                st->alpha = 0.0;
+            } else {
+                st->alpha = tot[1] / dAd;
+            }
+        }
+    }
+}
+
+// x' = x + alpha d'; r = b - A x'; ||r||^2 (solver.cpp:252-260).
+template <int D>
+__global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __restrict__ cls,
+                                                      const double* __restrict__ b, double* __restrict__ X0,
+                                                      double* __restrict__ X1, const double* __restrict__ Dring,
+                                                      double* __restrict__ r, SolverState* st, double* __restrict__ hist,
+                                                      double* __restrict__ times, double* __restrict__ partials,
+                                                      unsigned int* __restrict__ counter,
+                                                      cudaGraphConditionalHandle cond, int use_cond, int do_norm,
+                                                      int zchunk) {
+    if (st->breakdown) {
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+            set_cond(cond, use_cond, 0u);
+        return;
+    }
+    const int nw = (st->head + 1) % st->ring;
+    UpdateOp op;
+    op.in[0] = st->xcur ? X1 : X0;
+    op.in[1] = Dring + (long long)nw * g.n;
+    op.ctr[0] = b;
+    op.alpha = st->alpha;
+    double* xn = st->xcur ? X0 : X1;
+    double acc[1] = {0.0};
+    const int zc0 = blockIdx.z * zchunk;
+    const int zc1 = min(zc0 + zchunk, g.nz);
+    stencil_march<D, 1>(g, cls, op, zc0, zc1, acc,
+                        [&](long long q, double2 v, double2 s, unsigned bc, const double(&)[2], const double(&)[2],
+                            const double(&c0)[1], const double(&c1)[1], double(&a)[1]) {
+                            double2 rv;
+                            rv.x = fluid(bc & 0xffu) ? __dadd_rn(c0[0], -s.x) : 0.0;
+                            rv.y = fluid(bc >> 8) ? __dadd_rn(c1[0], -s.y) : 0.0;
+                            *reinterpret_cast<double2*>(xn + q) = v;
+                            *reinterpret_cast<double2*>(r + q) = rv;
+                            a[0] += rv.x * rv.x;
+                            a[0] += rv.y * rv.y;
+                        });
+    if (!do_norm) return;
+    double tot[1];
+    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0)
+        finish_iteration(st, tot[0], hist, times, cond, use_cond, false);
+}
+
+template <typename Op>
+constexpr size_t march_smem_bytes() {
+    return sizeof(MarchSmem<Op>);
+}
+
+}  // namespace nb2
