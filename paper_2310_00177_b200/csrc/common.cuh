@@ -237,4 +237,32 @@ __device__ __forceinline__ bool grid_reduce2(double (&v)[NV], double* __restrict
     return true;
 }
 
+// L0 tile occupancy (k_tile_flags): 32 x 8 tiles per plane, dilated by one
+// cell; flags == nullptr disables skipping (raw-network calls).
+constexpr int kFlagTX = 32, kFlagTY = 8;
+struct Occ {
+    const uint8_t* flags;
+    int ntx, nty;
+};
+
+// Block-wide: does the region [tx0, tx1) x [ty0, ty1) x [z0, z1] (flag tiles,
+// planes clamped to the grid) hold fluid? Every thread of the block calls it.
+__device__ __forceinline__ bool region_has_fluid(const uint8_t* __restrict__ flags, int ntx, int nty, int nz, int tx0,
+                                                 int tx1, int ty0, int ty1, int z0, int z1) {
+    tx1 = min(tx1, ntx);
+    ty1 = min(ty1, nty);
+    z0 = max(z0, 0);
+    z1 = min(z1, nz - 1);
+    const int wx = tx1 - tx0, wy = ty1 - ty0;
+    const int cnt = (wx > 0 && wy > 0 && z1 >= z0) ? wx * wy * (z1 - z0 + 1) : 0;
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int nthr = blockDim.x * blockDim.y * blockDim.z;
+    int any = 0;
+    for (int i = tid; i < cnt; i += nthr) {
+        const int xx = i % wx, yy = (i / wx) % wy, zz = i / (wx * wy);
+        any |= flags[((long long)(z0 + zz) * nty + (ty0 + yy)) * ntx + (tx0 + xx)];
+    }
+    return __syncthreads_or(any) != 0;
+}
+
 }  // namespace nb2

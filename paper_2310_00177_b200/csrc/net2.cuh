@@ -46,10 +46,17 @@ __device__ __forceinline__ float conv27(const ConvTab& ct, const KC& kc, long lo
                                         const float (&w)[Sh<D>::S]) {
     constexpr int S = Sh<D>::S;
     float acc = 0.0f;
-    if (wc < 3) {
-        const float* K = kc.k[wc];
+    // uniform windows: one branch per class so every kernel value is a
+    // compile-time offset into the parameter bank (no dynamic LDC)
+    if (wc == 0) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(K[s], w[s]));
+        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(kc.k[0][s], w[s]));
+    } else if (wc == 1) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(kc.k[1][s], w[s]));
+    } else if (wc == 2) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(kc.k[2][s], w[s]));
     } else {
         const long long idx = mixed_index(ct.mmask, ct.mbase, c);
         const float* K = ct.tab + idx;
@@ -69,7 +76,7 @@ template <int D, bool L0, bool POOL>
 __global__ void __launch_bounds__(kNT) k_down3(Geom g, const float* __restrict__ in_f,
                                                const double* __restrict__ in_d, const SolverState* __restrict__ st,
                                                ConvTab ct, const __grid_constant__ KC kc, float* __restrict__ y,
-                                               float* __restrict__ xnext, Geom gc, int zchunk) {
+                                               float* __restrict__ xnext, Geom gc, int zchunk, Occ occ) {
     constexpr int S = Sh<D>::S, WZ = Sh<D>::WZ, NP = (D == 3) ? 2 : 1;  // planes staged per step
     using Raw = typename std::conditional<L0, double, float>::type;
     __shared__ float sp[2][NP][kPH][kPW];
@@ -87,6 +94,18 @@ __global__ void __launch_bounds__(kNT) k_down3(Geom g, const float* __restrict__
     const int bz0 = blockIdx.z * zchunk;
     const int bz1 = min(bz0 + zchunk, nbz);
     if (bz0 >= bz1) return;
+    if (L0 && occ.flags) {
+        // fluid-free region (tile dilated by one cell, one plane each side):
+        // the input window is all zero, so y_0 = +0 (not stored: non-fluid)
+        // and x_1 = +0
+        const int zlo = (D == 3) ? 2 * bz0 - 1 : 0, zhi = (D == 3) ? 2 * bz1 : 0;
+        if (!region_has_fluid(occ.flags, occ.ntx, occ.nty, g.nz, blockIdx.x, blockIdx.x + 1, 2 * blockIdx.y,
+                              2 * blockIdx.y + 2, zlo, zhi)) {
+            if (POOL && own)
+                for (int bz = bz0; bz < bz1; ++bz) xnext[lin(gc, x0 >> 1, y0 >> 1, bz)] = 0.0f;
+            return;
+        }
+    }
 
     Raw pre[NP][kNE];
     // issue the loads of planes z, z+1 (zero outside the domain)
@@ -235,7 +254,7 @@ __global__ void __launch_bounds__(kNT) k_up3(Geom g, Geom gc, const float* __res
                                              const __grid_constant__ KC kc, float* __restrict__ outl,
                                              double* __restrict__ dout, SolverState* __restrict__ st,
                                              const double* __restrict__ ADring, double* __restrict__ partials,
-                                             unsigned int* __restrict__ counter, int zchunk) {
+                                             unsigned int* __restrict__ counter, int zchunk, Occ occ) {
     constexpr int S = Sh<D>::S, CW = Sh<D>::CW, BZ = Sh<D>::BZ;
     constexpr bool SOLVE = (MODE == kUpL0);
     constexpr int NA = (NO > 0) ? NO : 1;
@@ -297,7 +316,13 @@ __global__ void __launch_bounds__(kNT) k_up3(Geom g, Geom gc, const float* __res
 #pragma unroll
             for (int i = 0; i < 3; ++i) cw[slot][j][i] = sc[b][ty + j][tx + i];
     };
-    if (bz0 < bz1) {
+    // L0: a fluid-free tile has no output and no dot contribution (the block
+    // still joins the grid reduction below)
+    bool active = bz0 < bz1;
+    if (SOLVE && occ.flags && active)
+        active = region_has_fluid(occ.flags, occ.ntx, occ.nty, g.nz, blockIdx.x, blockIdx.x + 1, 2 * blockIdx.y,
+                                  2 * blockIdx.y + 2, (D == 3) ? 2 * bz0 : 0, (D == 3) ? 2 * bz1 - 1 : 0);
+    if (active) {
         int buf = 0;
         if (D == 3) {
             issue(bz0 - 1);

@@ -85,6 +85,8 @@ struct npsd_b200_ctx {
     float* zab = nullptr;  // [depth][2]
     KC kc_down[kMaxDepth], kc_up[kMaxDepth], kc_coarse;  // host copies of the uniform kernels
     uint32_t *fmask = nullptr, *fbase = nullptr, *fcount = nullptr;
+    uint8_t* tflags = nullptr;  // L0 tile occupancy (k_tile_flags)
+    int tf_ntx = 0, tf_nty = 0;
     long long n_fluid = 0;
     bool mask_ok = false;
     // solver
@@ -258,6 +260,8 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     LAUNCH(c, s, k_setup_l0<D>, c->g0.n, c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
     scan_u32(c, L0.mcount, L0.mbase, L0.nseg);
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
+    LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
+           c->tflags);
     for (int l = 1; l < c->depth; ++l) {
         LevelBufs& Lf = c->L[l - 1];
         LevelBufs& Lc = c->L[l];
@@ -355,7 +359,8 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
     const int zc = zchunk_for(c, k, kNX * kNY, (long long)gx * gy, nbz);
     const dim3 grid(gx, gy, (nbz + zc - 1) / zc);
     const KC& kc = (l == c->depth - 1) ? c->kc_coarse : c->kc_down[l];
-    LAUNCH3(c, s, k, grid, block, L.g, in_f, in_d, c->st, tab_down(c, l), kc, L.y, xnext, gc, zc);
+    const Occ occ = (L0 && c->tflags) ? Occ{c->tflags, c->tf_ntx, c->tf_nty} : Occ{nullptr, 0, 0};
+    LAUNCH3(c, s, k, grid, block, L.g, in_f, in_d, c->st, tab_down(c, l), kc, L.y, xnext, gc, zc, occ);
 }
 
 template <int D, int MODE, int NO>
@@ -370,7 +375,8 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
     const int zc = zchunk_for(c, k, kNX * kNY, (long long)gx * gy, nbz);
     const dim3 grid(gx, gy, (nbz + zc - 1) / zc);
     LAUNCH3(c, s, k, grid, block, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), c->kc_up[l], outl, dout, c->st,
-            c->ADring, c->partials, c->counter, zc);
+            c->ADring, c->partials, c->counter, zc,
+            (MODE == kUpL0) ? Occ{c->tflags, c->tf_ntx, c->tf_nty} : Occ{nullptr, 0, 0});
 }
 
 template <int D, int NO>
@@ -403,7 +409,7 @@ void launch_ortho(npsd_b200_ctx* c, cudaStream_t s) {
     const int zc = zchunk_for(c, k, kSX * kSY, (long long)gx * gy, g.nz, sm);
     const dim3 grid(gx, gy, (g.nz + zc - 1) / zc);
     LAUNCH3S(c, s, k, grid, block, sm, g, c->L[0].cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
-             c->counter, zc);
+             c->counter, zc, Occ{c->tflags, c->tf_ntx, c->tf_nty});
 }
 
 template <int D>
@@ -429,7 +435,7 @@ void launch_update(npsd_b200_ctx* c, cudaStream_t s, cudaGraphConditionalHandle 
     const int zc = zchunk_for(c, k, kSX * kSY, (long long)gx * gy, g.nz, sm);
     const dim3 grid(gx, gy, (g.nz + zc - 1) / zc);
     LAUNCH3S(c, s, k, grid, block, sm, g, c->L[0].cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist, c->times,
-             c->partials, c->counter, h, use_cond, do_norm, zc);
+             c->partials, c->counter, h, use_cond, do_norm, zc, Occ{c->tflags, c->tf_ntx, c->tf_nty});
 }
 
 // One named launcher per kernel of an iteration: the graph body is captured
@@ -726,6 +732,7 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->fmask);
     F(c->fbase);
     F(c->fcount);
+    F(c->tflags);
     F(c->X0);
     F(c->X1);
     F(c->R);
@@ -830,6 +837,9 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
         c->fmask = dalloc<uint32_t>((size_t)nseg0);
         c->fbase = dalloc<uint32_t>((size_t)nseg0);
         c->fcount = dalloc<uint32_t>((size_t)nseg0);
+        c->tf_ntx = (nx + kFlagTX - 1) / kFlagTX;
+        c->tf_nty = (ny + kFlagTY - 1) / kFlagTY;
+        c->tflags = dalloc<uint8_t>((size_t)c->tf_ntx * c->tf_nty * nz);
         const size_t n = (size_t)c->g0.n;
         c->X0 = dalloc<double>(n);
         c->X1 = dalloc<double>(n);

@@ -68,6 +68,29 @@ __global__ void __launch_bounds__(kBlock) k_setup_l0(Geom g, const uint8_t* __re
     }
 }
 
+// Tile occupancy at L0: flags[(z * nty + ty) * ntx + tx] = any fluid cell in
+// the 32 x 8 tile (tx, ty) of plane z dilated by one cell in x and y. Kernels
+// OR the flags of their region (plus one plane each side in z) and skip
+// fluid-free blocks: every input they would read there is exactly zero.
+__global__ void __launch_bounds__(kBlock) k_tile_flags(Geom g, const uint8_t* __restrict__ types, int ntx, int nty,
+                                                       uint8_t* __restrict__ flags) {
+    const long long n = (long long)ntx * nty * g.nz;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int tx = (int)(i % ntx), ty = (int)((i / ntx) % nty), z = (int)(i / ((long long)ntx * nty));
+        const int x0 = max(tx * kFlagTX - 1, 0), x1 = min(tx * kFlagTX + kFlagTX + 1, g.nx);
+        const int y0 = max(ty * kFlagTY - 1, 0), y1 = min(ty * kFlagTY + kFlagTY + 1, g.ny);
+        bool any = false;
+        for (int y = y0; y < y1 && !any; ++y)
+            for (int x = x0; x < x1; ++x)
+                if (types[lin(g, x, y, z)] == 0) {
+                    any = true;
+                    break;
+                }
+        flags[i] = any ? 1 : 0;
+    }
+}
+
 // PaddedImage::pooled (net/kernels.hpp:46-56), 3D order x-fastest then z+1
 // plane; from the L0 one-hot types (src_types) or a pooled level (src_img).
 template <int D>

@@ -100,7 +100,12 @@ struct MarchSmem {
 // Epi(q, v2 own pair, s2 rows, pair bytes, own raw inputs [NA] x 2, centre [NC] x 2, acc)
 template <int D, int NV, typename Op, typename Epi>
 __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __restrict__ cls, const Op& op, int zc0,
-                                              int zc1, double (&acc)[NV], Epi epi) {
+                                              int zc1, double (&acc)[NV], Epi epi, const Occ& occ) {
+    // a fluid-free tile has no rows to evaluate (block-uniform early exit,
+    // before any barrier; the caller's reduction still runs)
+    if (occ.flags && !region_has_fluid(occ.flags, occ.ntx, occ.nty, g.nz, 2 * blockIdx.x, 2 * blockIdx.x + 2,
+                                       blockIdx.y, blockIdx.y + 1, zc0, zc1 - 1))
+        return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem<Op>& S = *reinterpret_cast<MarchSmem<Op>*>(smem_raw);
     const int lane = threadIdx.x, row = threadIdx.y;
@@ -264,7 +269,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
                                                      const double* __restrict__ dtmp, const double* __restrict__ r,
                                                      double* __restrict__ Dring, double* __restrict__ ADring,
                                                      SolverState* st, double* __restrict__ partials,
-                                                     unsigned int* __restrict__ counter, int zchunk) {
+                                                     unsigned int* __restrict__ counter, int zchunk, Occ occ) {
     const int nc = st->n_cache, R = st->ring;
     const int nw = (st->head + 1) % R;
     using Op = OrthoOp<NO>;
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
                                      a[2 + j] += i0[1 + j] * s.x;
                                      a[2 + j] += i1[1 + j] * s.y;
                                  }
-                         });
+                         }, occ);
     double tot[NV];
     if (grid_reduce<NV>(acc, partials, counter, tot)) {
         if (threadIdx.x == 0 && threadIdx.y == 0) {
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
                                                       double* __restrict__ times, double* __restrict__ partials,
                                                       unsigned int* __restrict__ counter,
                                                       cudaGraphConditionalHandle cond, int use_cond, int do_norm,
-                                                      int zchunk) {
+                                                      int zchunk, Occ occ) {
     if (st->breakdown) {
         if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && threadIdx.y == 0)
             set_cond(cond, use_cond, 0u);
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
                             *reinterpret_cast<double2*>(r + q) = rv;
                             a[0] += rv.x * rv.x;
                             a[0] += rv.y * rv.y;
-                        });
+                        }, occ);
     if (!do_norm) return;
     double tot[1];
     if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0)
