@@ -79,6 +79,7 @@ struct SolverState {
     double rnorm, thr;
     double inv1, inv2, nrm;         // network input scales / output multiplier
     double p[kMaxOrtho];            // MGS projections of the current direction
+    double dot_main[kMaxOrtho];     // d.Ad_j over the tiled kernel's cells (mixed cells added later)
     double dAd[kRing];              // per ring slot: d'Ad
     double cross[kRing][kRing];     // cross[i][j] = d_i . A d_j (i older than j)
     double dAd_new, rd_new, alpha;  // for the direction being built

@@ -1,0 +1,138 @@
+// Level-0 mixed-window cells, processed apart from the tiled network kernels.
+//
+// A cell whose 3^D window is not one pure cell type needs its own kernel (a
+// row of the compact table, build_kernels net/kernels.hpp:121-144). Inside the
+// tiled kernels such cells cost a dependent chain (cell byte -> mixed index ->
+// 27 table loads) that stalls whole warps at every wall and interface. Here
+// they are a compact list: one thread per mixed cell, table rows read with
+// consecutive indices (fully coalesced SoA), window taps gathered (L2 hits).
+//
+// k_mixed_down0: y_0 at every mixed cell, before k_down3<L0> (which loads it
+//   instead of convolving, so the pooling order is unchanged).
+// k_mixed_up0:   d at every mixed fluid cell, after k_up3<kUpL0> (which skips
+//   them); its last block adds the main kernel's dot totals (st->dot_main) to
+//   its own in a fixed order and finalises the MGS projections.
+// Arithmetic order per cell is the restatement's (bit-identical outputs).
+#pragma once
+
+#include "common.cuh"
+
+namespace nb2 {
+
+// compact list of mixed cells: list[mixed_index(c)] = c
+__global__ void __launch_bounds__(kBlock) k_mixed_list(Geom g, const uint8_t* __restrict__ cls,
+                                                       const uint32_t* __restrict__ mmask,
+                                                       const uint32_t* __restrict__ mbase, uint32_t* __restrict__ list) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
+        if (cls_window(cls[c]) == 3) list[mixed_index(mmask, mbase, c)] = (uint32_t)c;
+}
+
+// number of mixed cells = last exclusive base + last count
+__global__ void k_seg_total(const uint32_t* __restrict__ base, const uint32_t* __restrict__ cnt, long long nseg,
+                            uint32_t* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *out = base[nseg - 1] + cnt[nseg - 1];
+}
+
+__device__ __forceinline__ void decode32(const Geom& g, uint32_t c, int& x, int& y, int& z) {
+    const uint32_t nx = (uint32_t)g.nx, ny = (uint32_t)g.ny;
+    const uint32_t row = c / nx;
+    x = (int)(c - row * nx);
+    z = (int)(row / ny);
+    y = (int)(row - (uint32_t)z * ny);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* __restrict__ list,
+                                                        const uint32_t* __restrict__ count, const double* __restrict__ r,
+                                                        const SolverState* __restrict__ st,
+                                                        const float* __restrict__ tab, long long cap,
+                                                        float* __restrict__ y) {
+    constexpr int S = Sh<D>::S;
+    const uint32_t n = *count;
+    const double inv1 = st->inv1, inv2 = st->inv2;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t c = list[i];
+        int x, yy, z;
+        decode32(g, c, x, yy, z);
+        float w[S], k[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
+            const int xx = x + dx, y2 = yy + dy, zz = z + dz;
+            const bool in = xx >= 0 && xx < g.nx && y2 >= 0 && y2 < g.ny && zz >= 0 && zz < g.nz;
+            w[s] = in ? __double2float_rn(__dmul_rn(__dmul_rn(__ldg(r + lin(g, xx, y2, zz)), inv1), inv2)) : 0.0f;
+            k[s] = __ldg(tab + (long long)s * cap + i);
+        }
+        float acc = 0.0f;
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(k[s], w[s]));
+        y[c] = acc;
+    }
+}
+
+template <int D, int NO>
+__global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uint32_t* __restrict__ list,
+                                                      const uint32_t* __restrict__ count, const uint8_t* __restrict__ cls,
+                                                      const float* __restrict__ outc, const float* __restrict__ y0,
+                                                      const float* __restrict__ zab, const float* __restrict__ tab,
+                                                      long long cap, double* __restrict__ dout, SolverState* st,
+                                                      const double* __restrict__ ADring, double* __restrict__ partials,
+                                                      unsigned int* __restrict__ counter) {
+    constexpr int S = Sh<D>::S;
+    constexpr int NA = (NO > 0) ? NO : 1;
+    const uint32_t n = *count;
+    const float za = zab[0], zb = zab[1];
+    const double nrm = st->nrm;
+    const int nc = st->n_cache, R = st->ring;
+    const double* adp[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+        const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
+        adp[j] = ADring + (long long)slot * g.n;
+    }
+    double acc[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t c = list[i];
+        if (cls_type(__ldg(cls + c)) != 0) continue;  // only fluid cells have an output
+        int x, yy, z;
+        decode32(g, c, x, yy, z);
+        float w[S], k[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
+            const int xx = x + dx, y2 = yy + dy, zz = z + dz;
+            // upsample2: fine (xx, y2, zz) -> coarse (xx>>1, y2>>1, zz>>1); zero outside
+            const bool in = xx >= 0 && xx < g.nx && y2 >= 0 && y2 < g.ny && zz >= 0 && zz < g.nz;
+            w[s] = in ? __ldg(outc + lin(gc, xx >> 1, y2 >> 1, (D == 3) ? zz >> 1 : 0)) : 0.0f;
+            k[s] = __ldg(tab + (long long)s * cap + i);
+        }
+        float u = 0.0f;
+#pragma unroll
+        for (int s = 0; s < S; ++s) u = __fadd_rn(u, __fmul_rn(k[s], w[s]));
+        const float o = __fadd_rn(__fmul_rn(za, __ldg(y0 + c)), __fmul_rn(zb, u));
+        const double dv = __dmul_rn((double)o, nrm);
+        dout[c] = dv;
+#pragma unroll
+        for (int j = 0; j < NO; ++j)
+            if (j < nc) acc[j] += dv * __ldg(adp[j] + c);
+    }
+    double tot[NA];
+    if (grid_reduce<NA>(acc, partials, counter, tot) && threadIdx.x == 0) {
+        // totals of the tiled kernel first, then this kernel's (fixed order)
+        const int Rr = st->ring;
+        int slot[NA];
+        for (int j = 0; j < nc && j < NA; ++j) slot[j] = (st->head - (nc - 1) + j + 2 * Rr) % Rr;
+        for (int j = 0; j < nc && j < NO; ++j) {
+            double num = st->dot_main[j] + tot[j];
+            for (int i = 0; i < j; ++i) num -= st->p[i] * st->cross[slot[i]][slot[j]];
+            st->p[j] = num / st->dAd[slot[j]];
+        }
+    }
+}
+
+}  // namespace nb2

@@ -208,7 +208,9 @@ __global__ void __launch_bounds__(kNT) k_down3(Geom g, const float* __restrict__
                         const long long c = lin(g, x0 + cx, y0 + cy, z0 + cz);
                         const uint8_t bb = (uint8_t)(cb[cz][cy] >> (8 * cx));
                         float yv = 0.0f;
-                        if (need) {
+                        if (L0 && cls_window(bb) == 3) {
+                            yv = y[c];  // mixed window: computed by k_mixed_down0
+                        } else if (need) {
                             float win[S];
 #pragma unroll
                             for (int s = 0; s < S; ++s) {
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(kNT) k_down3(Geom g, const float* __restrict__
                             }
                             yv = conv27<D>(ct, kc, c, cls_window(bb), win);
                         }
-                        if (!L0 || cls_type(bb) == 0) y[c] = yv;
+                        if ((!L0 || cls_type(bb) == 0) && !(L0 && cls_window(bb) == 3)) y[c] = yv;
                         if (POOL) psum = (cz == 0 && cy == 0 && cx == 0) ? yv : __fadd_rn(psum, yv);
                     }
             }
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(kNT) k_up3(Geom g, Geom gc, const float* __res
 #pragma unroll
                         for (int cx = 0; cx < 2; ++cx) {
                             const uint8_t bb = (uint8_t)(cb[cz][cy] >> (8 * cx));
-                            if (SOLVE && cls_type(bb) != 0) continue;
+                            if (SOLVE && (cls_type(bb) != 0 || cls_window(bb) == 3)) continue;  // mixed: k_mixed_up0
                             const long long c = lin(g, x0 + cx, y0 + cy, z0 + cz);
                             float win[S];
 #pragma unroll
@@ -413,18 +415,10 @@ __global__ void __launch_bounds__(kNT) k_up3(Geom g, Geom gc, const float* __res
     }
     if (SOLVE) {
         double tot[NA];
-        if (grid_reduce<NA>(acc, partials, counter, tot) && tid == 0) {
-            // MGS projections, oldest first (solver.cpp:239-243), fused form:
-            // p_j = (d.Ad_j - sum_{i<j} p_i d_i.Ad_j) / d_j'Ad_j
-            const int R = st->ring;
-            int slot[NA];
-            for (int j = 0; j < nc && j < NA; ++j) slot[j] = (st->head - (nc - 1) + j + 2 * R) % R;
-            for (int j = 0; j < nc && j < NO; ++j) {
-                double num = tot[j];
-                for (int i = 0; i < j; ++i) num -= st->p[i] * st->cross[slot[i]][slot[j]];
-                st->p[j] = num / st->dAd[slot[j]];
-            }
-        }
+        // the mixed fluid cells follow in k_mixed_up0, which finalises the
+        // MGS projections from these totals plus its own
+        if (grid_reduce<NA>(acc, partials, counter, tot) && tid == 0)
+            for (int j = 0; j < NA; ++j) st->dot_main[j] = tot[j];
     }
 }
 

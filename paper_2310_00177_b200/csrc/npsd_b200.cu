@@ -22,6 +22,7 @@
 #include "setup.cuh"
 #include "stencil.cuh"
 #include "net2.cuh"
+#include "mixed.cuh"
 
 using namespace nb2;
 
@@ -86,6 +87,8 @@ struct npsd_b200_ctx {
     KC kc_down[kMaxDepth], kc_up[kMaxDepth], kc_coarse;  // host copies of the uniform kernels
     uint32_t *fmask = nullptr, *fbase = nullptr, *fcount = nullptr;
     uint8_t* tflags = nullptr;  // L0 tile occupancy (k_tile_flags)
+    uint32_t* mlist0 = nullptr;  // L0 mixed cells, compact (k_mixed_list)
+    uint32_t* mcount0 = nullptr;
     int tf_ntx = 0, tf_nty = 0;
     long long n_fluid = 0;
     bool mask_ok = false;
@@ -262,6 +265,10 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
     LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
            c->tflags);
+    LAUNCH(c, s, k_mixed_list, c->g0.n, c->g0, L0.cls, L0.mmask, L0.mbase, c->mlist0);
+    k_seg_total<<<1, 32, 0, s>>>(L0.mbase, L0.mcount, L0.nseg, c->mcount0);
+    CK(cudaGetLastError());
+    ++c->launches;
     for (int l = 1; l < c->depth; ++l) {
         LevelBufs& Lf = c->L[l - 1];
         LevelBufs& Lc = c->L[l];
@@ -442,9 +449,38 @@ void launch_update(npsd_b200_ctx* c, cudaStream_t s, cudaGraphConditionalHandle 
 // from these, and the profiler runs them one by one between CUDA events.
 // raw: the network on an f32 full-grid input (xin_f -> out_f), no solver.
 template <int D>
+void launch_mixed_down0(npsd_b200_ctx* c, cudaStream_t s) {
+    const LevelBufs& L = c->L[0];
+    LAUNCH(c, s, k_mixed_down0<D>, L.g.n, L.g, c->mlist0, c->mcount0, c->R, c->st, L.tab_down, L.g.n, L.y);
+}
+
+template <int D, int NO>
+void launch_mixed_up0(npsd_b200_ctx* c, cudaStream_t s) {
+    const LevelBufs& L = c->L[0];
+    const LevelBufs& L1 = c->L[1];
+    const float* outc = (c->depth == 2) ? L1.y : L1.out;
+    LAUNCH(c, s, (k_mixed_up0<D, NO>), L.g.n, L.g, L1.g, c->mlist0, c->mcount0, L.cls, outc, L.y, c->zab, L.tab_up,
+           L.g.n, c->Dtmp, c->st, c->ADring, c->partials, c->counter);
+}
+
+template <int D>
+void launch_mixed_up0_no(npsd_b200_ctx* c, cudaStream_t s, int no) {
+    switch (no) {
+        case 0: launch_mixed_up0<D, 0>(c, s); break;
+        case 1: launch_mixed_up0<D, 1>(c, s); break;
+        case 2: launch_mixed_up0<D, 2>(c, s); break;
+        case 3: launch_mixed_up0<D, 3>(c, s); break;
+        case 4: launch_mixed_up0<D, 4>(c, s); break;
+        default: launch_mixed_up0<D, kMaxOrtho>(c, s); break;
+    }
+}
+
+template <int D>
 std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     std::vector<Step> v;
     const int Ld = c->depth;
+    // solve path: level-0 mixed-window cells are computed apart (mixed.cuh)
+    if (!raw) v.push_back({"net_mixed_down_L0", [c](cudaStream_t s) { launch_mixed_down0<D>(c, s); }});
     for (int l = 0; l < Ld; ++l) {
         const bool pool = (l + 1 < Ld);
         const std::string nm = (l == Ld - 1) ? "net_coarse_L" + std::to_string(l) : "net_down_L" + std::to_string(l);
@@ -471,6 +507,8 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
                              launch_up<D, kUpMid, 0>(c, s, l, (l == 0) ? c->out_f : c->L[l].out, nullptr);
                      }});
     }
+    if (!raw && Ld > 1)
+        v.push_back({"net_mixed_up_L0", [c, no](cudaStream_t s) { launch_mixed_up0_no<D>(c, s, no); }});
     if (Ld == 1 && !raw) {
         v.push_back({"net_out_L0", [c](cudaStream_t s) {
                          LevelBufs& L = c->L[0];
@@ -733,6 +771,8 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->fbase);
     F(c->fcount);
     F(c->tflags);
+    F(c->mlist0);
+    F(c->mcount0);
     F(c->X0);
     F(c->X1);
     F(c->R);
@@ -840,6 +880,8 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
         c->tf_ntx = (nx + kFlagTX - 1) / kFlagTX;
         c->tf_nty = (ny + kFlagTY - 1) / kFlagTY;
         c->tflags = dalloc<uint8_t>((size_t)c->tf_ntx * c->tf_nty * nz);
+        c->mlist0 = dalloc<uint32_t>((size_t)c->g0.n);
+        c->mcount0 = dalloc<uint32_t>(1);
         const size_t n = (size_t)c->g0.n;
         c->X0 = dalloc<double>(n);
         c->X1 = dalloc<double>(n);
