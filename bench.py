@@ -39,13 +39,40 @@ UNIT = "ms"
 # ------------------------------------------------------------ byte model
 def canonical_bytes_per_cell(depth: int) -> dict[str, float]:
     """SURVEY.md §8d canonical algorithmic bytes per fine cell per PSDO
-    iteration, split by the kernel that implements each phase."""
-    m = {"net_down_L0": 13.5, "net_up_L0": 45.5, "ortho": 49.0, "update": 41.0}
+    iteration, split by phase (P1 level-0 down, P2 per coarse kernel, P3
+    level-0 up, P4 ortho, P5 update)."""
+    m = {"P1": 13.5, "P3": 45.5, "P4": 49.0, "P5": 41.0}
     for l in range(1, depth - 1):
-        m[f"net_down_L{l}"] = 20.5 / 8 ** l
-        m[f"net_up_L{l}"] = 20.5 / 8 ** l
-    m[f"net_coarse_L{depth - 1}"] = 20.0 / 8 ** (depth - 1)
+        m[f"P2_down_L{l}"] = 20.5 / 8 ** l
+        m[f"P2_up_L{l}"] = 20.5 / 8 ** l
+    m[f"P2_coarse_L{depth - 1}"] = 20.0 / 8 ** (depth - 1)
     return m
+
+
+def phase_of(kernel: str) -> str:
+    """Kernel step name (Context.profile_iterations) -> canonical phase."""
+    if kernel in ("net_mixed_down_L0", "net_down_L0"):
+        return "P1"
+    if kernel in ("net_up_L0", "net_mixed_up_L0", "net_out_L0"):
+        return "P3"
+    if kernel == "ortho":
+        return "P4"
+    if kernel == "update":
+        return "P5"
+    return "P2_" + kernel[len("net_"):]
+
+
+def ncu_traffic(kernels: list, n: int):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
+    the given kernel steps, from the committed ncu capture of this workload
+    (profiles/ncu_traffic_<n>.json, written by tools/ncu_traffic.py); None if
+    no capture exists."""
+    p = ROOT / "profiles" / f"ncu_traffic_{n}.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    vals = [d["bytes"].get(k) for k in kernels]
+    return None if any(v is None for v in vals) else float(sum(vals))
 
 
 def load_peaks() -> dict:
@@ -266,9 +293,15 @@ def run_b200(args) -> None:
 
     # per-kernel device times (kernels launched one by one between events)
     prof = ctx.profile_iterations(d_b.ptr, cfg, args.profile_iters)
-    dom = max(prof, key=prof.get)
+    phase_ms: dict[str, float] = {}
+    phase_kernels: dict[str, list] = {}
+    for k, v in prof.items():
+        ph = phase_of(k)
+        phase_ms[ph] = phase_ms.get(ph, 0.0) + v
+        phase_kernels.setdefault(ph, []).append(k)
+    dom = max(phase_ms, key=phase_ms.get)
     dom_bytes = model.get(dom, 0.0) * n_c
-    dom_gbs = dom_bytes / (prof[dom] * 1e-3) / 1e9
+    dom_gbs = dom_bytes / (phase_ms[dom] * 1e-3) / 1e9
     prof_total = sum(prof.values())
 
     # end to end through the public host API: pinned host inputs, H2D each step,
@@ -326,10 +359,12 @@ def run_b200(args) -> None:
                                    "frac": iter_gbs / peaks["hbm_gbs"],
                                    "bytes": f"canonical B_iter = {sum(model.values()):.2f} B x n_c (SURVEY §8d)",
                                    "peak_source": peaks["source"]},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": dom_gbs / peaks["hbm_gbs"], "traffic": None,
-                         "bytes_per_launch": dom_bytes, "ms_per_launch": prof[dom],
-                         "share_of_iteration": prof[dom] / prof_total, "peak_source": peaks["source"]},
+            "roofline": {"bound": "hbm", "kernel": "+".join(phase_kernels[dom]), "phase": dom, "achieved": dom_gbs,
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": dom_gbs / peaks["hbm_gbs"],
+                         "traffic": ncu_traffic(phase_kernels[dom], types.shape[0]),
+                         "bytes_per_launch": dom_bytes, "ms_per_launch": phase_ms[dom],
+                         "share_of_iteration": phase_ms[dom] / prof_total, "peak_source": peaks["source"],
+                         "bytes_model": f"SURVEY §8d canonical {model[dom]:.3f} B/cell x {n_c} cells ({dom})"},
             "kernel_ms": prof,
             "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(n_c + 8 * n_f),
                     "d2h_bytes_per_step": int(8 * n_f + hist_bytes),

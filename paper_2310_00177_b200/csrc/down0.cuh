@@ -1,0 +1,198 @@
+// Level-0 down sweep of the solve (P1), 3D: y_0 = conv_down_0(x_0) and
+// x_1 = avg_pool(y_0), with x_0 = f32((r * inv1) * inv2) (net_precond.cpp:24-29,
+// net/forward.hpp:105-113).
+//
+// At level 0 the window classes make the work sparse: a uniform air/solid
+// window has an all-zero input (y_0 = +0), a mixed window's y_0 was computed by
+// k_mixed_down0, so only uniform-fluid cells convolve — with one constant
+// kernel (compile-time offsets into the parameter bank). The kernel is the
+// stencil pipeline of stencil.cuh: a 32 x 8 block owns a 64 x 8 tile (one
+// thread per x pair) and marches z; each thread cp.async-copies the residual
+// of its pair and halo assignment PF planes ahead (src-size 0 for pairs
+// without fluid: zero-fill, no DRAM read; r is exactly 0 there) and converts
+// its own copies into a 4-plane f32 ring; one barrier per plane; taps are read
+// from shared memory. Pooling: the even row of each row pair sums the 2x2x2
+// blocks in the restatement's order at odd planes. Arithmetic order per cell
+// is apply_kernels' (net/kernels.hpp:147-172): bit-identical.
+#pragma once
+
+#include "common.cuh"
+#include "net.cuh"
+#include "stencil.cuh"
+
+namespace nb2 {
+
+struct KC0 {
+    float k[27];
+};
+
+struct Down0Smem {
+    double raw[kST][kVH][kVW];  // residual copies (tile + halo)
+    float xin[4][kVH][kVW];     // converted network input x_0
+    float yp[2][kTY][kTX];      // y_0 of the last two planes (pooling)
+};
+
+// zchunk even; grid (nx/64, ny/8, nz/zchunk); dynamic smem = sizeof(Down0Smem)
+__global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __restrict__ cls,
+                                                      const double* __restrict__ r, const SolverState* __restrict__ st,
+                                                      const __grid_constant__ KC0 kc, float* __restrict__ y,
+                                                      float* __restrict__ xnext, Geom gc, int zchunk, Occ occ) {
+    const int zc0 = blockIdx.z * zchunk;
+    const int zc1 = min(zc0 + zchunk, g.nz);
+    const int lane = threadIdx.x, row = threadIdx.y;
+    const int X0 = blockIdx.x * kTX, Y0 = blockIdx.y * kTY;
+    const int x = X0 + 2 * lane, yy = Y0 + row;
+    const bool own = x < g.nx && yy < g.ny;  // nx even: the pair is whole
+    if (occ.flags && !region_has_fluid(occ.flags, occ.ntx, occ.nty, g.nz, 2 * blockIdx.x, 2 * blockIdx.x + 2,
+                                       blockIdx.y, blockIdx.y + 1, zc0 - 1, zc1)) {
+        // all inputs zero: x_1 = +0 on this tile's coarse cells
+        if (own && !(row & 1))
+            for (int z = zc0 + 1; z < zc1; z += 2) xnext[lin(gc, x >> 1, yy >> 1, z >> 1)] = 0.0f;
+        return;
+    }
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Down0Smem& S = *reinterpret_cast<Down0Smem*>(smem_raw);
+    const long long nx = g.nx, plane = nx * g.ny;
+    const double inv1 = st->inv1, inv2 = st->inv2;
+    // halo assignment (as stencil_march)
+    int hx = 0, hy = 0, hsr = 0, hsc = 0, hkind = 0;
+    if (row == 0 || row == 1) {
+        hkind = 1;
+        hx = x;
+        hy = (row == 0) ? Y0 - 1 : Y0 + kTY;
+        hsr = (row == 0) ? 0 : kVH - 1;
+        hsc = 2 + 2 * lane;
+    } else if (row == 2 && lane < 2 * kTY) {
+        hkind = 2;
+        hx = (lane < kTY) ? X0 - 1 : X0 + kTX;
+        hy = Y0 + (lane & (kTY - 1));
+        hsr = 1 + (lane & (kTY - 1));
+        hsc = (lane < kTY) ? 1 : kTX + 2;
+    } else if (row == 3 && lane < 4) {
+        // the 27-point window also reads the four corners of the halo ring
+        hkind = 2;
+        hx = (lane & 1) ? X0 + kTX : X0 - 1;
+        hy = (lane & 2) ? Y0 + kTY : Y0 - 1;
+        hsr = (lane & 2) ? kVH - 1 : 0;
+        hsc = (lane & 1) ? kTX + 2 : 1;
+    }
+    const bool h_in = hkind != 0 && hx >= 0 && hx < g.nx && hy >= 0 && hy < g.ny;
+    const long long qo = (long long)(own ? yy : 0) * nx + (own ? x : 0);
+    const long long qh = h_in ? (long long)hy * nx + hx : 0;
+    auto zin = [&](int z) { return z >= 0 && z < g.nz; };
+    auto own_bytes = [&](int z) -> unsigned {
+        return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
+    };
+    auto halo_live = [&](int z) -> bool {
+        if (!h_in || !zin(z)) return false;
+        if (hkind == 1) return pair_live(__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qh)));
+        return fluid(__ldg(cls + z * plane + qh));
+    };
+    auto slot = [&](int z) { return (z - zc0 + 1 + kST * 1024) % kST; };
+    auto issue = [&](int z, unsigned ob, bool hl) {
+        if (zin(z)) {
+            const int s = slot(z);
+            const bool ol = own && pair_live(ob);
+            const long long qz = z * plane;
+            cp_async16(&S.raw[s][row + 1][2 + 2 * lane], r + (ol ? qz + qo : 0), ol);
+            if (hkind == 1)
+                cp_async16(&S.raw[s][hsr][hsc], r + (hl ? qz + qh : 0), hl);
+            else if (hkind == 2)
+                cp_async8(&S.raw[s][hsr][hsc], r + (hl ? qz + qh : 0), hl);
+        }
+        cp_commit();
+    };
+    auto cvt = [&](double v) { return __double2float_rn(__dmul_rn(__dmul_rn(v, inv1), inv2)); };
+    auto form = [&](int z) {
+        const int s = slot(z), vs = (z + 1024) & 3;
+        const bool zi = zin(z);
+        S.xin[vs][row + 1][2 + 2 * lane] = zi ? cvt(S.raw[s][row + 1][2 + 2 * lane]) : 0.0f;
+        S.xin[vs][row + 1][3 + 2 * lane] = zi ? cvt(S.raw[s][row + 1][3 + 2 * lane]) : 0.0f;
+        if (hkind != 0) S.xin[vs][hsr][hsc] = zi ? cvt(S.raw[s][hsr][hsc]) : 0.0f;
+        if (hkind == 1) S.xin[vs][hsr][hsc + 1] = zi ? cvt(S.raw[s][hsr][hsc + 1]) : 0.0f;
+    };
+    // prologue (as stencil_march): planes zc0-1 .. zc0+PF-1 issued, zc0-1 and zc0 formed
+    unsigned ob[kPF + 2];
+    bool hl[kPF + 2];
+    issue(zc0 - 1, own_bytes(zc0 - 1), halo_live(zc0 - 1));
+#pragma unroll
+    for (int k = 0; k < kPF + 2; ++k) {
+        ob[k] = own_bytes(zc0 + k);
+        hl[k] = halo_live(zc0 + k);
+    }
+#pragma unroll
+    for (int k = 0; k < kPF; ++k) issue(zc0 + k, ob[k], hl[k]);
+    cp_wait<kPF - 1>();
+    form(zc0 - 1);
+    form(zc0);
+    // mixed cells' y_0 (k_mixed_down0), loaded one plane ahead
+    auto mixed_y = [&](int z, unsigned b2, float& ya, float& yb) {
+        const long long q = z * plane + qo;
+        ya = (own && cls_window((uint8_t)(b2 & 0xffu)) == 3) ? __ldg(y + q) : 0.0f;
+        yb = (own && cls_window((uint8_t)(b2 >> 8)) == 3) ? __ldg(y + q + 1) : 0.0f;
+    };
+    float mya, myb;
+    mixed_y(zc0, ob[0], mya, myb);
+    for (int z = zc0; z < zc1; ++z) {
+        issue(z + kPF, ob[kPF], hl[kPF]);
+        cp_wait<kPF - 1>();
+        form(z + 1);
+        float nya = 0.0f, nyb = 0.0f;
+        if (z + 1 < zc1) mixed_y(z + 1, ob[1], nya, nyb);
+        __syncthreads();  // x_0 of planes z-1, z, z+1 complete (halos included)
+        const unsigned bc = ob[0];
+        const int vm = (z + 1023) & 3, vc = (z + 1024) & 3, vp = (z + 1025) & 3;
+        const int c0 = 2 + 2 * lane, r0 = row + 1;
+        float ya = 0.0f, yb = 0.0f;
+        const uint8_t ba = (uint8_t)(bc & 0xffu), bb = (uint8_t)(bc >> 8);
+        if (own) {
+            // uniform-fluid windows convolve with the constant kernel, slot order
+            auto conv = [&](int cc) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int s = 0; s < 27; ++s) {
+                    const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
+                    const int ps = dz < 0 ? vm : (dz > 0 ? vp : vc);
+                    acc = __fadd_rn(acc, __fmul_rn(kc.k[s], S.xin[ps][r0 + dy][cc + dx]));
+                }
+                return acc;
+            };
+            const int wa = cls_window(ba), wb = cls_window(bb);
+            ya = (wa == 0) ? conv(c0) : (wa == 3 ? mya : 0.0f);
+            yb = (wb == 0) ? conv(c0 + 1) : (wb == 3 ? myb : 0.0f);
+            // y_0 is stored at fluid cells; mixed ones already hold it
+            const long long q = z * plane + qo;
+            if (cls_type(ba) == 0 && wa != 3) y[q] = ya;
+            if (cls_type(bb) == 0 && wb != 3) y[q + 1] = yb;
+        }
+        // pooling (restatement order: x fastest, then y, then z)
+        S.yp[z & 1][row][2 * lane] = ya;
+        S.yp[z & 1][row][2 * lane + 1] = yb;
+        if (z & 1) {
+            __syncthreads();
+            if (own && !(row & 1)) {
+                float ps = S.yp[0][row][2 * lane];
+                ps = __fadd_rn(ps, S.yp[0][row][2 * lane + 1]);
+                ps = __fadd_rn(ps, S.yp[0][row + 1][2 * lane]);
+                ps = __fadd_rn(ps, S.yp[0][row + 1][2 * lane + 1]);
+                ps = __fadd_rn(ps, S.yp[1][row][2 * lane]);
+                ps = __fadd_rn(ps, S.yp[1][row][2 * lane + 1]);
+                ps = __fadd_rn(ps, S.yp[1][row + 1][2 * lane]);
+                ps = __fadd_rn(ps, S.yp[1][row + 1][2 * lane + 1]);
+                xnext[lin(gc, x >> 1, yy >> 1, z >> 1)] = __fmul_rn(0.125f, ps);
+            }
+        }
+        mya = nya;
+        myb = nyb;
+#pragma unroll
+        for (int k = 0; k < kPF + 1; ++k) {
+            ob[k] = ob[k + 1];
+            hl[k] = hl[k + 1];
+        }
+        ob[kPF + 1] = own_bytes(z + kPF + 2);
+        hl[kPF + 1] = halo_live(z + kPF + 2);
+    }
+    cp_wait<0>();
+}
+
+}  // namespace nb2

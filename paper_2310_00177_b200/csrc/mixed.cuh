@@ -46,7 +46,7 @@ template <int D>
 __global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* __restrict__ list,
                                                         const uint32_t* __restrict__ count, const double* __restrict__ r,
                                                         const SolverState* __restrict__ st,
-                                                        const float* __restrict__ tab, long long cap,
+                                                        const float* __restrict__ tab, const uint32_t* __restrict__ kid,
                                                         float* __restrict__ y) {
     constexpr int S = Sh<D>::S;
     const uint32_t n = *count;
@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* 
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint32_t c = list[i];
+        const float* K = tab + (kid ? (long long)__ldg(kid + i) : (long long)i) * kRowW;
         int x, yy, z;
         decode32(g, c, x, yy, z);
         float w[S], k[S];
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* 
             const int xx = x + dx, y2 = yy + dy, zz = z + dz;
             const bool in = xx >= 0 && xx < g.nx && y2 >= 0 && y2 < g.ny && zz >= 0 && zz < g.nz;
             w[s] = in ? __double2float_rn(__dmul_rn(__dmul_rn(__ldg(r + lin(g, xx, y2, zz)), inv1), inv2)) : 0.0f;
-            k[s] = __ldg(tab + (long long)s * cap + i);
+            k[s] = __ldg(K + s);
         }
         float acc = 0.0f;
 #pragma unroll
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uin
                                                       const uint32_t* __restrict__ count, const uint8_t* __restrict__ cls,
                                                       const float* __restrict__ outc, const float* __restrict__ y0,
                                                       const float* __restrict__ zab, const float* __restrict__ tab,
-                                                      long long cap, double* __restrict__ dout, SolverState* st,
+                                                      const uint32_t* __restrict__ kid, double* __restrict__ dout, SolverState* st,
                                                       const double* __restrict__ ADring, double* __restrict__ partials,
                                                       unsigned int* __restrict__ counter) {
     constexpr int S = Sh<D>::S;
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uin
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint32_t c = list[i];
         if (cls_type(__ldg(cls + c)) != 0) continue;  // only fluid cells have an output
+        const float* K = tab + (kid ? (long long)__ldg(kid + i) : (long long)i) * kRowW;
         int x, yy, z;
         decode32(g, c, x, yy, z);
         float w[S], k[S];
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uin
             // upsample2: fine (xx, y2, zz) -> coarse (xx>>1, y2>>1, zz>>1); zero outside
             const bool in = xx >= 0 && xx < g.nx && y2 >= 0 && y2 < g.ny && zz >= 0 && zz < g.nz;
             w[s] = in ? __ldg(outc + lin(gc, xx >> 1, y2 >> 1, (D == 3) ? zz >> 1 : 0)) : 0.0f;
-            k[s] = __ldg(tab + (long long)s * cap + i);
+            k[s] = __ldg(K + s);
         }
         float u = 0.0f;
 #pragma unroll

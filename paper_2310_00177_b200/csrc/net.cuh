@@ -23,14 +23,25 @@
 
 namespace nb2 {
 
+// Mixed-window kernels are AoS rows of kRowW floats (27 used). Row of a mixed
+// cell = kid[mixed_index] (level 0: window-pattern dictionary) or the mixed
+// index itself (kid == nullptr, coarse levels).
+constexpr int kRowW = 28;
+
 struct ConvTab {
     const uint8_t* cls;
     const uint32_t* mmask;
     const uint32_t* mbase;
-    const float* tab;
-    long long cap;
+    const float* tab;     // rows [row][kRowW]
+    const uint32_t* kid;  // mixed index -> row, or nullptr (identity)
     const float* kconst;  // [3][S]
 };
+
+__device__ __forceinline__ const float* kernel_row(const ConvTab& ct, long long c) {
+    const long long idx = mixed_index(ct.mmask, ct.mbase, c);
+    const long long row = ct.kid ? (long long)__ldg(ct.kid + idx) : idx;
+    return ct.tab + row * kRowW;
+}
 
 // y = sum_s K[s] * win(s), slot order, round-to-nearest (apply_kernels order).
 template <int D, typename WinFn>
@@ -43,10 +54,9 @@ __device__ __forceinline__ float conv_cell(const ConvTab& ct, const float* sK, l
 #pragma unroll
         for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(K[s], win(s)));
     } else {
-        const long long idx = mixed_index(ct.mmask, ct.mbase, c);
-        const float* K = ct.tab + idx;
+        const float* K = kernel_row(ct, c);
 #pragma unroll
-        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(__ldg(K + (long long)s * ct.cap), win(s)));
+        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(__ldg(K + s), win(s)));
     }
     return acc;
 }

@@ -58,10 +58,9 @@ __device__ __forceinline__ float conv27(const ConvTab& ct, const KC& kc, long lo
 #pragma unroll
         for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(kc.k[2][s], w[s]));
     } else {
-        const long long idx = mixed_index(ct.mmask, ct.mbase, c);
-        const float* K = ct.tab + idx;
+        const float* K = kernel_row(ct, c);
 #pragma unroll
-        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(__ldg(K + (long long)s * ct.cap), w[s]));
+        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(__ldg(K + s), w[s]));
     }
     return acc;
 }

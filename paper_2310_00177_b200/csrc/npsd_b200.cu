@@ -4,6 +4,7 @@
 // iteration: 2*depth-1 network kernels + ortho + update) repeats under a
 // device-side conditional WHILE node, so the host never synchronises inside
 // the solve.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <cmath>
@@ -23,6 +24,7 @@
 #include "stencil.cuh"
 #include "net2.cuh"
 #include "mixed.cuh"
+#include "down0.cuh"
 
 using namespace nb2;
 
@@ -65,6 +67,8 @@ struct LevelBufs {
     float *kc_down = nullptr, *kc_up = nullptr;  // [3][S]
     float *y = nullptr, *x = nullptr, *out = nullptr;
     unsigned long long* zG = nullptr;
+    uint32_t* mlist = nullptr;  // compact mixed cells (k_mixed_list)
+    uint32_t* mcnt = nullptr;   // their number (device)
 };
 
 // offsets of one level's blocks inside the flat parameter vector
@@ -87,8 +91,10 @@ struct npsd_b200_ctx {
     KC kc_down[kMaxDepth], kc_up[kMaxDepth], kc_coarse;  // host copies of the uniform kernels
     uint32_t *fmask = nullptr, *fbase = nullptr, *fcount = nullptr;
     uint8_t* tflags = nullptr;  // L0 tile occupancy (k_tile_flags)
-    uint32_t* mlist0 = nullptr;  // L0 mixed cells, compact (k_mixed_list)
-    uint32_t* mcount0 = nullptr;
+    // level-0 window-pattern dictionary (setup.cuh)
+    unsigned long long *dkeys = nullptr, *dskeys = nullptr;
+    uint32_t *dvals = nullptr, *dsidx = nullptr, *dhead = nullptr, *dscan = nullptr;
+    uint32_t *pid0 = nullptr, *repcell0 = nullptr, *npat0 = nullptr;
     int tf_ntx = 0, tf_nty = 0;
     long long n_fluid = 0;
     bool mask_ok = false;
@@ -248,11 +254,11 @@ void upload_params_and_kconst(npsd_b200_ctx* c) {
 
 ConvTab tab_down(const npsd_b200_ctx* c, int l) {
     const LevelBufs& L = c->L[l];
-    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_down, L.g.n, L.kc_down};
+    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_down, (l == 0) ? c->pid0 : nullptr, L.kc_down};
 }
 ConvTab tab_up(const npsd_b200_ctx* c, int l) {
     const LevelBufs& L = c->L[l];
-    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_up, L.g.n, L.kc_up};
+    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_up, (l == 0) ? c->pid0 : nullptr, L.kc_up};
 }
 
 // ---------------------------------------------------------------- set_mask
@@ -265,10 +271,6 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
     LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
            c->tflags);
-    LAUNCH(c, s, k_mixed_list, c->g0.n, c->g0, L0.cls, L0.mmask, L0.mbase, c->mlist0);
-    k_seg_total<<<1, 32, 0, s>>>(L0.mbase, L0.mcount, L0.nseg, c->mcount0);
-    CK(cudaGetLastError());
-    ++c->launches;
     for (int l = 1; l < c->depth; ++l) {
         LevelBufs& Lf = c->L[l - 1];
         LevelBufs& Lc = c->L[l];
@@ -277,16 +279,61 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         LAUNCH(c, s, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
         scan_u32(c, Lc.mcount, Lc.mbase, Lc.nseg);
     }
+    // compact mixed-cell lists per level
+    for (int l = 0; l < c->depth; ++l) {
+        LevelBufs& L = c->L[l];
+        LAUNCH(c, s, k_mixed_list, L.g.n, L.g, L.cls, L.mmask, L.mbase, L.mlist);
+        k_seg_total<<<1, 32, 0, s>>>(L.mbase, L.mcount, L.nseg, L.mcnt);
+        CK(cudaGetLastError());
+        ++c->launches;
+    }
+    // level 0: window-pattern dictionary (pid per mixed cell, one row per pattern)
+    uint32_t n_mixed0 = 0;
+    CK(cudaMemcpyAsync(&n_mixed0, L0.mcnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (n_mixed0 > 0) {
+        LAUNCH(c, s, k_window_keys<D>, (long long)n_mixed0, c->g0, dtypes, L0.mlist, L0.mcnt, c->dkeys, c->dvals);
+        size_t bytes = 0;
+        const int nbits = 2 * Sh<D>::S;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n_mixed0, 0,
+                                           nbits, s));
+        if (bytes > c->cub_bytes) {
+            if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
+            CK(cudaMalloc(&c->cub_tmp, bytes));
+            c->cub_bytes = bytes;
+        }
+        CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n_mixed0,
+                                           0, nbits, s));
+        c->launches += 4;  // cub onesweep: histogram + passes (approximate)
+        LAUNCH(c, s, k_run_heads, (long long)n_mixed0, c->dskeys, L0.mcnt, c->dhead);
+        bytes = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, c->dhead, c->dscan, (int)n_mixed0, s));
+        if (bytes > c->cub_bytes) {
+            if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
+            CK(cudaMalloc(&c->cub_tmp, bytes));
+            c->cub_bytes = bytes;
+        }
+        CK(cub::DeviceScan::InclusiveSum(c->cub_tmp, bytes, c->dhead, c->dscan, (int)n_mixed0, s));
+        c->launches += 2;
+        LAUNCH(c, s, k_pattern_ids, (long long)n_mixed0, c->dsidx, c->dscan, c->dhead, L0.mlist, L0.mcnt, c->pid0,
+               c->repcell0, c->npat0);
+    } else {
+        CK(cudaMemsetAsync(c->npat0, 0, sizeof(uint32_t), s));
+    }
     for (int l = 0; l < c->depth; ++l) {
         LevelBufs& L = c->L[l];
         const uint8_t* st = (l == 0) ? dtypes : nullptr;
         const float* im = (l == 0) ? nullptr : L.img;
+        // rows: one per window pattern at level 0, one per mixed cell above
+        const uint32_t* cells = (l == 0) ? c->repcell0 : L.mlist;
+        const uint32_t* ncells = (l == 0) ? c->npat0 : L.mcnt;
+        const long long rows_cap = (l == 0) ? (long long)n_mixed0 : L.g.n;
         if (l < c->depth - 1) {
             const LevelOffsets& o = c->offs[(size_t)l];
-            LAUNCH(c, s, k_build_table<D>, L.g.n, L.g, st, im, L.cls, L.mmask, L.mbase, c->d_params + o.down_W,
-                   c->d_params + o.down_B, L.tab_down, L.g.n);
-            LAUNCH(c, s, k_build_table<D>, L.g.n, L.g, st, im, L.cls, L.mmask, L.mbase, c->d_params + o.up_W,
-                   c->d_params + o.up_B, L.tab_up, L.g.n);
+            LAUNCH(c, s, k_build_rows<D>, rows_cap, L.g, st, im, cells, ncells, c->d_params + o.down_W,
+                   c->d_params + o.down_B, L.tab_down);
+            LAUNCH(c, s, k_build_rows<D>, rows_cap, L.g, st, im, cells, ncells, c->d_params + o.up_W,
+                   c->d_params + o.up_B, L.tab_up);
             constexpr int NC = (D == 3) ? 27 : 9;
             CK(cudaMemsetAsync(L.zG, 0, 3 * NC * sizeof(unsigned long long), s));
             const double scale = std::ldexp(1.0, D * l);
@@ -296,8 +343,8 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
             CK(cudaGetLastError());
             ++c->launches;
         } else {
-            LAUNCH(c, s, k_build_table<D>, L.g.n, L.g, st, im, L.cls, L.mmask, L.mbase, c->d_params + c->coarse_W,
-                   c->d_params + c->coarse_B, L.tab_down, L.g.n);
+            LAUNCH(c, s, k_build_rows<D>, rows_cap, L.g, st, im, cells, ncells, c->d_params + c->coarse_W,
+                   c->d_params + c->coarse_B, L.tab_down);
         }
     }
     // zero invariant of the solver vectors at the new non-fluid cells
@@ -363,7 +410,8 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
     const int gx = (L.g.nx + 2 * kNX - 1) / (2 * kNX), gy = (L.g.ny + 2 * kNY - 1) / (2 * kNY);
     const int nbz = (D == 3) ? (L.g.nz >> 1) : 1;
     auto k = k_down3<D, L0, POOL>;
-    const int zc = zchunk_for(c, k, kNX * kNY, (long long)gx * gy, nbz);
+    // coarse levels are small: one brick plane per block keeps the serial chain short
+    const int zc = (l > 0) ? 1 : zchunk_for(c, k, kNX * kNY, (long long)gx * gy, nbz);
     const dim3 grid(gx, gy, (nbz + zc - 1) / zc);
     const KC& kc = (l == c->depth - 1) ? c->kc_coarse : c->kc_down[l];
     const Occ occ = (L0 && c->tflags) ? Occ{c->tflags, c->tf_ntx, c->tf_nty} : Occ{nullptr, 0, 0};
@@ -379,7 +427,7 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
     const int gx = (Lc.g.nx + kNX - 1) / kNX, gy = (Lc.g.ny + kNY - 1) / kNY;
     const int nbz = (D == 3) ? Lc.g.nz : 1;
     auto k = k_up3<D, MODE, NO>;
-    const int zc = zchunk_for(c, k, kNX * kNY, (long long)gx * gy, nbz);
+    const int zc = (l > 0) ? 1 : zchunk_for(c, k, kNX * kNY, (long long)gx * gy, nbz);
     const dim3 grid(gx, gy, (nbz + zc - 1) / zc);
     LAUNCH3(c, s, k, grid, block, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), c->kc_up[l], outl, dout, c->st,
             c->ADring, c->partials, c->counter, zc,
@@ -448,10 +496,27 @@ void launch_update(npsd_b200_ctx* c, cudaStream_t s, cudaGraphConditionalHandle 
 // One named launcher per kernel of an iteration: the graph body is captured
 // from these, and the profiler runs them one by one between CUDA events.
 // raw: the network on an f32 full-grid input (xin_f -> out_f), no solver.
+// 3D level-0 down sweep with pooling (down0.cuh)
+void launch_down_l0(npsd_b200_ctx* c, cudaStream_t s) {
+    const LevelBufs& L = c->L[0];
+    const Geom g = L.g;
+    const dim3 block(kSX, kSY);
+    const int gx = (g.nx + kTX - 1) / kTX, gy = (g.ny + kTY - 1) / kTY;
+    const size_t sm = sizeof(Down0Smem);
+    CK(cudaFuncSetAttribute(k_down_l0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int zc = zchunk_for(c, k_down_l0, kSX * kSY, (long long)gx * gy, g.nz, sm);
+    zc = (zc + 1) & ~1;  // pooling pairs stay inside a block
+    const dim3 grid(gx, gy, (g.nz + zc - 1) / zc);
+    KC0 kc0;
+    for (int i = 0; i < 27; ++i) kc0.k[i] = c->kc_down[0].k[0][i];  // the uniform-fluid kernel
+    LAUNCH3S(c, s, k_down_l0, grid, block, sm, g, L.cls, c->R, c->st, kc0, L.y, c->L[1].x, c->L[1].g, zc,
+             Occ{c->tflags, c->tf_ntx, c->tf_nty});
+}
+
 template <int D>
 void launch_mixed_down0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
-    LAUNCH(c, s, k_mixed_down0<D>, L.g.n, L.g, c->mlist0, c->mcount0, c->R, c->st, L.tab_down, L.g.n, L.y);
+    LAUNCH(c, s, k_mixed_down0<D>, L.g.n, L.g, L.mlist, L.mcnt, c->R, c->st, L.tab_down, c->pid0, L.y);
 }
 
 template <int D, int NO>
@@ -459,8 +524,8 @@ void launch_mixed_up0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
     const LevelBufs& L1 = c->L[1];
     const float* outc = (c->depth == 2) ? L1.y : L1.out;
-    LAUNCH(c, s, (k_mixed_up0<D, NO>), L.g.n, L.g, L1.g, c->mlist0, c->mcount0, L.cls, outc, L.y, c->zab, L.tab_up,
-           L.g.n, c->Dtmp, c->st, c->ADring, c->partials, c->counter);
+    LAUNCH(c, s, (k_mixed_up0<D, NO>), L.g.n, L.g, L1.g, L.mlist, L.mcnt, L.cls, outc, L.y, c->zab, L.tab_up,
+           c->pid0, c->Dtmp, c->st, c->ADring, c->partials, c->counter);
 }
 
 template <int D>
@@ -486,7 +551,9 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
         const std::string nm = (l == Ld - 1) ? "net_coarse_L" + std::to_string(l) : "net_down_L" + std::to_string(l);
         v.push_back({nm, [c, l, pool, raw](cudaStream_t s) {
                          if (l == 0 && !raw) {
-                             if (pool)
+                             if (pool && D == 3)
+                                 launch_down_l0(c, s);
+                             else if (pool)
                                  launch_down<D, true, true>(c, s, 0, nullptr, c->R);
                              else
                                  launch_down<D, true, false>(c, s, 0, nullptr, c->R);
@@ -764,6 +831,8 @@ void free_ctx(npsd_b200_ctx* c) {
         F(L.x);
         F(L.out);
         F(L.zG);
+        F(L.mlist);
+        F(L.mcnt);
     }
     F(c->d_params);
     F(c->zab);
@@ -771,8 +840,9 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->fbase);
     F(c->fcount);
     F(c->tflags);
-    F(c->mlist0);
-    F(c->mcount0);
+    for (void* p : {(void*)c->dkeys, (void*)c->dskeys, (void*)c->dvals, (void*)c->dsidx, (void*)c->dhead,
+                    (void*)c->dscan, (void*)c->pid0, (void*)c->repcell0, (void*)c->npat0})
+        F(p);
     F(c->X0);
     F(c->X1);
     F(c->R);
@@ -862,8 +932,10 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
             L.mbase = dalloc<uint32_t>((size_t)L.nseg);
             L.mcount = dalloc<uint32_t>((size_t)L.nseg);
             if (l > 0) L.img = dalloc<float>(3 * (size_t)L.g.n);
-            L.tab_down = dalloc<float>((size_t)c->S * L.g.n);
-            if (l < depth - 1) L.tab_up = dalloc<float>((size_t)c->S * L.g.n);
+            L.tab_down = dalloc<float>((size_t)kRowW * L.g.n);
+            if (l < depth - 1) L.tab_up = dalloc<float>((size_t)kRowW * L.g.n);
+            L.mlist = dalloc<uint32_t>((size_t)L.g.n);
+            L.mcnt = dalloc<uint32_t>(1);
             L.kc_down = dalloc<float>(3 * (size_t)c->S);
             L.kc_up = dalloc<float>(3 * (size_t)c->S);
             L.y = dalloc<float>((size_t)L.g.n);
@@ -880,8 +952,15 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
         c->tf_ntx = (nx + kFlagTX - 1) / kFlagTX;
         c->tf_nty = (ny + kFlagTY - 1) / kFlagTY;
         c->tflags = dalloc<uint8_t>((size_t)c->tf_ntx * c->tf_nty * nz);
-        c->mlist0 = dalloc<uint32_t>((size_t)c->g0.n);
-        c->mcount0 = dalloc<uint32_t>(1);
+        c->dkeys = dalloc<unsigned long long>((size_t)c->g0.n);
+        c->dskeys = dalloc<unsigned long long>((size_t)c->g0.n);
+        c->dvals = dalloc<uint32_t>((size_t)c->g0.n);
+        c->dsidx = dalloc<uint32_t>((size_t)c->g0.n);
+        c->dhead = dalloc<uint32_t>((size_t)c->g0.n);
+        c->dscan = dalloc<uint32_t>((size_t)c->g0.n);
+        c->pid0 = dalloc<uint32_t>((size_t)c->g0.n);
+        c->repcell0 = dalloc<uint32_t>((size_t)c->g0.n);
+        c->npat0 = dalloc<uint32_t>(1);
         const size_t n = (size_t)c->g0.n;
         c->X0 = dalloc<double>(n);
         c->X1 = dalloc<double>(n);
@@ -955,7 +1034,9 @@ int npsd_b200_set_mask(npsd_b200_ctx* c, const uint8_t* types) {
     return guarded(c, [&] {
         require(types != nullptr, "npsd_b200: cell types pointer is null");
         const size_t n = (size_t)c->g0.n;
-        for (size_t i = 0; i < n; ++i) require(types[i] <= 2, "npsd_b200: cell type out of range (0 fluid, 1 air, 2 solid)");
+        uint8_t worst = 0;  // plain loop: no per-element message construction
+        for (size_t i = 0; i < n; ++i) worst = types[i] > worst ? types[i] : worst;
+        require(worst <= 2, "npsd_b200: cell type out of range (0 fluid, 1 air, 2 solid)");
         uint8_t* d = reinterpret_cast<uint8_t*>(c->red_a);  // staging (n bytes <= 8n)
         CK(cudaMemcpyAsync(d, types, n, cudaMemcpyHostToDevice, c->s));
         if (c->dim == 3)
@@ -1082,7 +1163,9 @@ int npsd_b200_psdo_solve(npsd_b200_ctx* c, const double* b, const double* x0, co
         const Geom g = c->g0;
         const uint8_t* cls = c->L[0].cls;
         const size_t nf = (size_t)c->n_fluid;
-        for (size_t i = 0; i < nf; ++i) require(std::isfinite(b[i]), "solve: rhs has non-finite entries");
+        bool finite = true;  // check_inputs (solver.cpp:28-33), without per-element messages
+        for (size_t i = 0; i < nf; ++i) finite &= std::isfinite(b[i]);
+        require(finite, "solve: rhs has non-finite entries");
         CK(cudaMemcpyAsync(c->red_a, b, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
         LAUNCH(c, c->s, k_scatter, g.n, g, cls, c->fmask, c->fbase, c->red_a, c->Bf);
         if (x0) {

@@ -158,24 +158,26 @@ __global__ void __launch_bounds__(kBlock) k_classify(Geom g, const float* __rest
     }
 }
 
-// build_kernels (net/kernels.hpp:121-144) for mixed cells only:
-// K[s] = B[s] + sum_c sum_window W[s,c,w] * I(c, x+w), order (c, dz, dy, dx).
+// build_kernels (net/kernels.hpp:121-144) for a list of cells (the mixed
+// cells of a coarse level, or one representative cell per window pattern at
+// level 0): K[s] = B[s] + sum_c sum_window W[s,c,w] * I(c, x+w), order
+// (c, dz, dy, dx); row i of `tab` (kRowW floats) for cells[i], i < *count.
 template <int D>
-__global__ void __launch_bounds__(kBlock) k_build_table(Geom g, const uint8_t* __restrict__ src_types,
-                                                        const float* __restrict__ img, const uint8_t* __restrict__ cls,
-                                                        const uint32_t* __restrict__ mmask,
-                                                        const uint32_t* __restrict__ mbase, const float* __restrict__ W,
-                                                        const float* __restrict__ B, float* __restrict__ tab,
-                                                        long long cap) {
+__global__ void __launch_bounds__(kBlock) k_build_rows(Geom g, const uint8_t* __restrict__ src_types,
+                                                       const float* __restrict__ img,
+                                                       const uint32_t* __restrict__ cells,
+                                                       const uint32_t* __restrict__ count, const float* __restrict__ W,
+                                                       const float* __restrict__ B, float* __restrict__ tab) {
     constexpr int S = Sh<D>::S;
     __shared__ float sW[S * 3 * S];
     __shared__ float sB[S];
     for (int i = threadIdx.x; i < S * 3 * S; i += blockDim.x) sW[i] = W[i];
     for (int i = threadIdx.x; i < S; i += blockDim.x) sB[i] = B[i];
     __syncthreads();
+    const long long n = *count;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
-        if (cls_window(cls[c]) != 3) continue;
+    for (long long ii = (long long)blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
+        const long long c = cells[ii];
         const int x = (int)(c % g.nx);
         const int y = (int)((c / g.nx) % g.ny);
         const int z = (int)(c / ((long long)g.nx * g.ny));
@@ -203,7 +205,6 @@ __global__ void __launch_bounds__(kBlock) k_build_table(Geom g, const uint8_t* _
                 }
             }
         }
-        const long long idx = mixed_index(mmask, mbase, c);
         for (int s = 0; s < S; ++s) {
             float acc = sB[s];
             const float* w = sW + s * 3 * S;
@@ -211,9 +212,65 @@ __global__ void __launch_bounds__(kBlock) k_build_table(Geom g, const uint8_t* _
             for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
                 for (int t = 0; t < S; ++t) acc = __fadd_rn(acc, __fmul_rn(w[ch * S + t], win[ch][t]));
-            tab[(long long)s * cap + idx] = acc;
+            tab[ii * kRowW + s] = acc;
         }
     }
+}
+
+// ---- level-0 window-pattern dictionary -----------------------------------
+// At level 0 a mixed cell's kernel depends only on the cell types of its
+// window (3^D two-bit codes, exact 54-bit key in 3D), and few patterns exist
+// (C3 256^3: 926k mixed cells, 3,064 patterns). Keys are sorted, runs get a
+// pattern id, one representative cell per pattern gets a kernel row.
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_window_keys(Geom g, const uint8_t* __restrict__ types,
+                                                        const uint32_t* __restrict__ list,
+                                                        const uint32_t* __restrict__ count,
+                                                        unsigned long long* __restrict__ keys,
+                                                        uint32_t* __restrict__ vals) {
+    const long long n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const long long c = list[i];
+        const int x = (int)(c % g.nx), y = (int)((c / g.nx) % g.ny), z = (int)(c / ((long long)g.nx * g.ny));
+        unsigned long long key = 0;
+#pragma unroll
+        for (int t = 0; t < Sh<D>::S; ++t) {
+            const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = (D == 3) ? t / 9 - 1 : 0;
+            const int xx = x + dx, yy = y + dy, zz = z + dz;
+            const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
+            const unsigned long long tt = in ? types[lin(g, xx, yy, zz)] : 2ull;
+            key |= tt << (2 * t);
+        }
+        keys[i] = key;
+        vals[i] = (uint32_t)i;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_run_heads(const unsigned long long* __restrict__ skeys,
+                                                      const uint32_t* __restrict__ count, uint32_t* __restrict__ head) {
+    const long long n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        head[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1u : 0u;
+}
+
+// pid[mixed idx] = pattern id; repcell[pattern] = its first cell; npat
+__global__ void __launch_bounds__(kBlock) k_pattern_ids(const uint32_t* __restrict__ sidx,
+                                                        const uint32_t* __restrict__ scan,
+                                                        const uint32_t* __restrict__ head,
+                                                        const uint32_t* __restrict__ list,
+                                                        const uint32_t* __restrict__ count, uint32_t* __restrict__ pid,
+                                                        uint32_t* __restrict__ repcell, uint32_t* __restrict__ npat) {
+    const long long n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t p = scan[i] - 1;
+        pid[sidx[i]] = p;
+        if (head[i]) repcell[p] = list[sidx[i]];
+        if (i == n - 1) *npat = scan[i];
+    }
+    if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) *npat = 0;
 }
 
 // The three uniform-window kernels of a conv (same arithmetic as

@@ -84,6 +84,30 @@ def test_precond_apply(b200, oracle, shape, depth, seed):
     assert np.all(ctx.precond_apply(np.zeros_like(r)) == 0.0)  # test_neural.cpp:258-261
 
 
+@pytest.mark.parametrize("shape,depth,seed", [((64, 64, 128), 4, 0), ((48, 96, 64), 3, 1)])
+def test_precond_apply_interior_tiles(b200, oracle, shape, depth, seed):
+    """Grids large enough that tiles have interior halos on every side (the
+    small cases above are all-boundary tiles)."""
+    t = scenes.random_types(shape, 170 + seed, p=(0.6, 0.3, 0.1), blobs=6)
+    p = oracle.init_params(3, depth, 180 + seed)
+    ctx, octx = make(b200, oracle, t, depth, p)
+    r = np.random.default_rng(seed).standard_normal(ctx.n_fluid)
+    z = ctx.precond_apply(r)
+    assert np.all(np.isfinite(z))
+    assert rel_l2(z, octx.precond_apply(r)) <= REL_L2
+
+
+def test_psdo_history_c3_64_random_weights(b200, oracle):
+    t, seed = scenes.config("C3", 64)
+    p = oracle.init_params(3, 4, 9)
+    ctx, octx = make(b200, oracle, t, 4, p)
+    b = oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    got = ctx.psdo_solve(b, b200.SolveConfig(max_iters=20, tol_reduction=1e-300))
+    want = octx.psdo_solve(b, max_iters=20, tol_reduction=1e-300)
+    h, w = got.report.residual_history, want["residual_history"]
+    assert np.max(np.abs(h - w) / w) <= 1e-6
+
+
 @pytest.mark.parametrize("shape,seed", [((16, 16, 16), 0), ((32, 24, 16), 1), ((32, 32), 2), ((8, 8, 8), 3)])
 def test_spmv_bitwise(b200, oracle, shape, seed):
     t = scenes.random_types(shape, 90 + seed)
