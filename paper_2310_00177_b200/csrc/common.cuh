@@ -49,10 +49,14 @@ struct Sh {
 
 // L0 cell byte: bits 0-1 window class (0/1/2 = uniform fluid/air/solid window,
 // 3 = mixed), bits 2-3 own cell type, bits 4-6 stencil diagonal (# non-solid
-// in-domain face neighbours). Coarse levels use bits 0-1 only.
+// in-domain face neighbours), bit 7 window holds a fluid cell. Coarse levels
+// use bits 0-1 only.
 __device__ __forceinline__ int cls_window(uint8_t b) { return b & 3; }
 __device__ __forceinline__ int cls_type(uint8_t b) { return (b >> 2) & 3; }
 __device__ __forceinline__ int cls_diag(uint8_t b) { return (b >> 4) & 7; }
+// level 0 only: the 3^D window holds a fluid cell (else the solve's input is
+// zero over it and y_0 = +0 exactly)
+__device__ __forceinline__ bool cls_wfluid(uint8_t b) { return (b >> 7) != 0; }
 
 // Mixed-cell table index from 32-cell segment masks and exclusive bases.
 __device__ __forceinline__ long long mixed_index(const uint32_t* __restrict__ mmask,

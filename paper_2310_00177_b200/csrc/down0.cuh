@@ -128,8 +128,9 @@ __global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __r
     // mixed cells' y_0 (k_mixed_down0), loaded one plane ahead
     auto mixed_y = [&](int z, unsigned b2, float& ya, float& yb) {
         const long long q = z * plane + qo;
-        ya = (own && cls_window((uint8_t)(b2 & 0xffu)) == 3) ? __ldg(y + q) : 0.0f;
-        yb = (own && cls_window((uint8_t)(b2 >> 8)) == 3) ? __ldg(y + q + 1) : 0.0f;
+        const uint8_t ba = (uint8_t)(b2 & 0xffu), bb = (uint8_t)(b2 >> 8);
+        ya = (own && cls_window(ba) == 3 && cls_wfluid(ba)) ? __ldg(y + q) : 0.0f;
+        yb = (own && cls_window(bb) == 3 && cls_wfluid(bb)) ? __ldg(y + q + 1) : 0.0f;
     };
     float mya, myb;
     mixed_y(zc0, ob[0], mya, myb);

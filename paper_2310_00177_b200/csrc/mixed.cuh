@@ -7,8 +7,9 @@
 // they are a compact list: one thread per mixed cell, table rows read with
 // consecutive indices (fully coalesced SoA), window taps gathered (L2 hits).
 //
-// k_mixed_down0: y_0 at every mixed cell, before k_down3<L0> (which loads it
-//   instead of convolving, so the pooling order is unchanged).
+// k_mixed_down0: y_0 at every mixed cell whose window holds fluid, before the
+//   level-0 down kernel (which loads it instead of convolving, so the pooling
+//   order is unchanged).
 // k_mixed_up0:   d at every mixed fluid cell, after k_up3<kUpL0> (which skips
 //   them); its last block adds the main kernel's dot totals (st->dot_main) to
 //   its own in a fixed order and finalises the MGS projections.
@@ -26,6 +27,45 @@ __global__ void __launch_bounds__(kBlock) k_mixed_list(Geom g, const uint8_t* __
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
         if (cls_window(cls[c]) == 3) list[mixed_index(mmask, mbase, c)] = (uint32_t)c;
+}
+
+// The solve needs y_0 only at mixed cells whose window holds a fluid cell (the
+// input is zero over the others: y_0 = +0, never computed or read) and the up
+// output only at fluid cells. set_mask splits the level-0 list (and the cells'
+// pattern ids) into those two sublists, ascending cell order kept.
+__global__ void __launch_bounds__(kBlock) k_mixed_flags(const uint32_t* __restrict__ list,
+                                                        const uint32_t* __restrict__ count,
+                                                        const uint8_t* __restrict__ cls, uint32_t* __restrict__ fd,
+                                                        uint32_t* __restrict__ fu) {
+    const uint32_t n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint8_t b = cls[list[i]];
+        fd[i] = cls_wfluid(b) ? 1u : 0u;
+        fu[i] = (cls_type(b) == 0) ? 1u : 0u;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_mixed_split(const uint32_t* __restrict__ list,
+                                                        const uint32_t* __restrict__ kid,
+                                                        const uint32_t* __restrict__ count,
+                                                        const uint32_t* __restrict__ fd, const uint32_t* __restrict__ sd,
+                                                        const uint32_t* __restrict__ fu, const uint32_t* __restrict__ su,
+                                                        uint32_t* __restrict__ dlist, uint32_t* __restrict__ dkid,
+                                                        uint32_t* __restrict__ ulist, uint32_t* __restrict__ ukid) {
+    const uint32_t n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t c = list[i], k = kid[i];
+        if (fd[i]) {
+            dlist[sd[i]] = c;
+            dkid[sd[i]] = k;
+        }
+        if (fu[i]) {
+            ulist[su[i]] = c;
+            ukid[su[i]] = k;
+        }
+    }
 }
 
 // number of mixed cells = last exclusive base + last count
@@ -54,7 +94,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* 
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint32_t c = list[i];
-        const float* K = tab + (kid ? (long long)__ldg(kid + i) : (long long)i) * kRowW;
+        const float* K = tab + (long long)__ldg(kid + i) * kRowW;
         int x, yy, z;
         decode32(g, c, x, yy, z);
         float w[S], k[S];
@@ -75,7 +115,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* 
 
 template <int D, int NO>
 __global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uint32_t* __restrict__ list,
-                                                      const uint32_t* __restrict__ count, const uint8_t* __restrict__ cls,
+                                                      const uint32_t* __restrict__ count,
                                                       const float* __restrict__ outc, const float* __restrict__ y0,
                                                       const float* __restrict__ zab, const float* __restrict__ tab,
                                                       const uint32_t* __restrict__ kid, double* __restrict__ dout, SolverState* st,
@@ -99,8 +139,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uin
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint32_t c = list[i];
-        if (cls_type(__ldg(cls + c)) != 0) continue;  // only fluid cells have an output
-        const float* K = tab + (kid ? (long long)__ldg(kid + i) : (long long)i) * kRowW;
+        const float* K = tab + (long long)__ldg(kid + i) * kRowW;
         int x, yy, z;
         decode32(g, c, x, yy, z);
         float w[S], k[S];

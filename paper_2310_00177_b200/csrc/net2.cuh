@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(kNT) k_down3(Geom g, const float* __restrict__
                         const uint8_t bb = (uint8_t)(cb[cz][cy] >> (8 * cx));
                         float yv = 0.0f;
                         if (L0 && cls_window(bb) == 3) {
-                            yv = y[c];  // mixed window: computed by k_mixed_down0
+                            // mixed window: computed by k_mixed_down0 (+0 without fluid)
+                            yv = cls_wfluid(bb) ? y[c] : 0.0f;
                         } else if (need) {
                             float win[S];
 #pragma unroll

@@ -95,6 +95,10 @@ struct npsd_b200_ctx {
     unsigned long long *dkeys = nullptr, *dskeys = nullptr;
     uint32_t *dvals = nullptr, *dsidx = nullptr, *dhead = nullptr, *dscan = nullptr;
     uint32_t *pid0 = nullptr, *repcell0 = nullptr, *npat0 = nullptr;
+    // level-0 mixed sublists the solve reads (mixed.cuh): windows holding fluid
+    // (down) and fluid cells (up), with their pattern ids
+    uint32_t *dlist0 = nullptr, *dkid0 = nullptr, *dcnt0 = nullptr;
+    uint32_t *ulist0 = nullptr, *ukid0 = nullptr, *ucnt0 = nullptr;
     int tf_ntx = 0, tf_nty = 0;
     long long n_fluid = 0;
     bool mask_ok = false;
@@ -317,8 +321,21 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         c->launches += 2;
         LAUNCH(c, s, k_pattern_ids, (long long)n_mixed0, c->dsidx, c->dscan, c->dhead, L0.mlist, L0.mcnt, c->pid0,
                c->repcell0, c->npat0);
+        // split into the solve's down/up sublists (dictionary scratch reused)
+        uint32_t *fd = c->dvals, *fu = c->dsidx, *sd = c->dhead, *su = c->dscan;
+        LAUNCH(c, s, k_mixed_flags, (long long)n_mixed0, L0.mlist, L0.mcnt, L0.cls, fd, fu);
+        scan_u32(c, fd, sd, (long long)n_mixed0);
+        scan_u32(c, fu, su, (long long)n_mixed0);
+        LAUNCH(c, s, k_mixed_split, (long long)n_mixed0, L0.mlist, c->pid0, L0.mcnt, fd, sd, fu, su, c->dlist0,
+               c->dkid0, c->ulist0, c->ukid0);
+        k_seg_total<<<1, 32, 0, s>>>(sd, fd, (long long)n_mixed0, c->dcnt0);
+        k_seg_total<<<1, 32, 0, s>>>(su, fu, (long long)n_mixed0, c->ucnt0);
+        CK(cudaGetLastError());
+        c->launches += 2;
     } else {
         CK(cudaMemsetAsync(c->npat0, 0, sizeof(uint32_t), s));
+        CK(cudaMemsetAsync(c->dcnt0, 0, sizeof(uint32_t), s));
+        CK(cudaMemsetAsync(c->ucnt0, 0, sizeof(uint32_t), s));
     }
     for (int l = 0; l < c->depth; ++l) {
         LevelBufs& L = c->L[l];
@@ -516,7 +533,7 @@ void launch_down_l0(npsd_b200_ctx* c, cudaStream_t s) {
 template <int D>
 void launch_mixed_down0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
-    LAUNCH(c, s, k_mixed_down0<D>, L.g.n, L.g, L.mlist, L.mcnt, c->R, c->st, L.tab_down, c->pid0, L.y);
+    LAUNCH(c, s, k_mixed_down0<D>, L.g.n, L.g, c->dlist0, c->dcnt0, c->R, c->st, L.tab_down, c->dkid0, L.y);
 }
 
 template <int D, int NO>
@@ -524,8 +541,8 @@ void launch_mixed_up0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
     const LevelBufs& L1 = c->L[1];
     const float* outc = (c->depth == 2) ? L1.y : L1.out;
-    LAUNCH(c, s, (k_mixed_up0<D, NO>), L.g.n, L.g, L1.g, L.mlist, L.mcnt, L.cls, outc, L.y, c->zab, L.tab_up,
-           c->pid0, c->Dtmp, c->st, c->ADring, c->partials, c->counter);
+    LAUNCH(c, s, (k_mixed_up0<D, NO>), L.g.n, L.g, L1.g, c->ulist0, c->ucnt0, outc, L.y, c->zab, L.tab_up,
+           c->ukid0, c->Dtmp, c->st, c->ADring, c->partials, c->counter);
 }
 
 template <int D>
@@ -841,7 +858,9 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->fcount);
     F(c->tflags);
     for (void* p : {(void*)c->dkeys, (void*)c->dskeys, (void*)c->dvals, (void*)c->dsidx, (void*)c->dhead,
-                    (void*)c->dscan, (void*)c->pid0, (void*)c->repcell0, (void*)c->npat0})
+                    (void*)c->dscan, (void*)c->pid0, (void*)c->repcell0, (void*)c->npat0,
+                    (void*)c->dlist0, (void*)c->dkid0, (void*)c->dcnt0, (void*)c->ulist0, (void*)c->ukid0,
+                    (void*)c->ucnt0})
         F(p);
     F(c->X0);
     F(c->X1);
@@ -960,6 +979,12 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
         c->dscan = dalloc<uint32_t>((size_t)c->g0.n);
         c->pid0 = dalloc<uint32_t>((size_t)c->g0.n);
         c->repcell0 = dalloc<uint32_t>((size_t)c->g0.n);
+        c->dlist0 = dalloc<uint32_t>((size_t)c->g0.n);
+        c->dkid0 = dalloc<uint32_t>((size_t)c->g0.n);
+        c->ulist0 = dalloc<uint32_t>((size_t)c->g0.n);
+        c->ukid0 = dalloc<uint32_t>((size_t)c->g0.n);
+        c->dcnt0 = dalloc<uint32_t>(1);
+        c->ucnt0 = dalloc<uint32_t>(1);
         c->npat0 = dalloc<uint32_t>(1);
         const size_t n = (size_t)c->g0.n;
         c->X0 = dalloc<double>(n);

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kBlock) k_setup_l0(Geom g, const uint8_t* __re
             const int y = (int)((c / g.nx) % g.ny);
             const int z = (int)(c / ((long long)g.nx * g.ny));
             const int t = types[c];
-            bool uniform = true;
+            bool uniform = true, wfluid = false;
             const int zr = (D == 3) ? 1 : 0;
             for (int dz = -zr; dz <= zr; ++dz)
                 for (int dy = -1; dy <= 1; ++dy)
@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(kBlock) k_setup_l0(Geom g, const uint8_t* __re
                         const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
                         const int tt = in ? types[lin(g, xx, yy, zz)] : 2;
                         uniform &= (tt == t);
+                        wfluid |= (tt == 0);
                     }
             // stencil diagonal: non-solid in-domain face neighbours (discretization.cpp:105-113)
             int diag = 0;
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(kBlock) k_setup_l0(Geom g, const uint8_t* __re
                 if (in && types[lin(g, xx, yy, zz)] != 2) ++diag;
             }
             const int w = uniform ? t : 3;
-            cls[c] = (uint8_t)(w | (t << 2) | (diag << 4));
+            cls[c] = (uint8_t)(w | (t << 2) | (diag << 4) | ((int)wfluid << 7));
             mixed = !uniform;
             fluid = (t == 0);
         }
