@@ -71,6 +71,13 @@ struct LevelBufs {
     uint32_t* mcnt = nullptr;   // their number (device)
 };
 
+// one balanced schedule (common.cuh Sched) over L0 tile columns
+struct SchedBufs {
+    int *pre = nullptr, *zlo = nullptr, *len = nullptr;
+    int ncol = 0, ntx = 0;
+    Sched view() const { return Sched{pre, zlo, ncol, ntx}; }
+};
+
 // offsets of one level's blocks inside the flat parameter vector
 struct LevelOffsets {
     size_t down_W, down_B, up_W, up_B, a_K, a_bias, b_K, b_bias;
@@ -91,6 +98,7 @@ struct npsd_b200_ctx {
     KC kc_down[kMaxDepth], kc_up[kMaxDepth], kc_coarse;  // host copies of the uniform kernels
     uint32_t *fmask = nullptr, *fbase = nullptr, *fcount = nullptr;
     uint8_t* tflags = nullptr;  // L0 tile occupancy (k_tile_flags)
+    SchedBufs sch_stencil;      // 64 x 8 tile columns, plane units (k_ortho2, k_update2)
     // level-0 window-pattern dictionary (setup.cuh)
     unsigned long long *dkeys = nullptr, *dskeys = nullptr;
     uint32_t *dvals = nullptr, *dsidx = nullptr, *dhead = nullptr, *dscan = nullptr;
@@ -266,6 +274,35 @@ ConvTab tab_up(const npsd_b200_ctx* c, int l) {
 }
 
 // ---------------------------------------------------------------- set_mask
+// Balanced schedule over the L0 tile columns of a tx x ty tiling (units of
+// `unit` planes, live within zdil planes of a fluid flag): k_sched_cols then
+// the prefix. Sizes are fixed per context; buffers are made on first use.
+void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int zdil) {
+    const int ntx = (c->g0.nx + tx - 1) / tx, nty = (c->g0.ny + ty - 1) / ty;
+    if (!sb.pre) {
+        sb.ncol = ntx * nty;
+        sb.ntx = ntx;
+        sb.pre = dalloc<int>((size_t)sb.ncol + 1);
+        sb.zlo = dalloc<int>((size_t)sb.ncol);
+        sb.len = dalloc<int>((size_t)sb.ncol);
+    }
+    const int nb = (sb.ncol + kBlock - 1) / kBlock;
+    k_sched_cols<<<nb, kBlock, 0, c->s>>>(c->tflags, c->tf_ntx, c->tf_nty, c->g0.nz, tx / kFlagTX, ty / kFlagTY, ntx,
+                                          nty, unit, zdil, sb.zlo, sb.len);
+    k_sched_prefix<<<1, 32, 0, c->s>>>(sb.len, sb.ncol, sb.pre);
+    CK(cudaGetLastError());
+    c->launches += 2;
+}
+
+// one wave of k's blocks (the schedule's grid)
+template <typename K>
+int wave_blocks(npsd_b200_ctx* c, K kernel, int threads, size_t smem) {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
+    if (occ < 1) occ = 1;
+    return c->num_sms * occ;
+}
+
 template <int D>
 void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     cudaStream_t s = c->s;
@@ -275,6 +312,7 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
     LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
            c->tflags);
+    build_sched(c, c->sch_stencil, kTX, kTY, 1, 0);
     for (int l = 1; l < c->depth; ++l) {
         LevelBufs& Lf = c->L[l - 1];
         LevelBufs& Lc = c->L[l];
@@ -474,14 +512,12 @@ template <int D, int NO>
 void launch_ortho(npsd_b200_ctx* c, cudaStream_t s) {
     const Geom g = c->g0;
     const dim3 block(kSX, kSY);
-    const int gx = (g.nx + kTX - 1) / kTX, gy = (g.ny + kTY - 1) / kTY;
     auto k = k_ortho2<D, NO>;
     const size_t sm = march_smem_bytes<OrthoOp<NO>>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const int zc = zchunk_for(c, k, kSX * kSY, (long long)gx * gy, g.nz, sm);
-    const dim3 grid(gx, gy, (g.nz + zc - 1) / zc);
+    const dim3 grid(wave_blocks(c, k, kSX * kSY, sm));
     LAUNCH3S(c, s, k, grid, block, sm, g, c->L[0].cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
-             c->counter, zc, Occ{c->tflags, c->tf_ntx, c->tf_nty});
+             c->counter, c->sch_stencil.view());
 }
 
 template <int D>
@@ -500,14 +536,12 @@ template <int D>
 void launch_update(npsd_b200_ctx* c, cudaStream_t s, cudaGraphConditionalHandle h, int use_cond, int do_norm) {
     const Geom g = c->g0;
     const dim3 block(kSX, kSY);
-    const int gx = (g.nx + kTX - 1) / kTX, gy = (g.ny + kTY - 1) / kTY;
     auto k = k_update2<D>;
     const size_t sm = march_smem_bytes<UpdateOp>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const int zc = zchunk_for(c, k, kSX * kSY, (long long)gx * gy, g.nz, sm);
-    const dim3 grid(gx, gy, (g.nz + zc - 1) / zc);
+    const dim3 grid(wave_blocks(c, k, kSX * kSY, sm));
     LAUNCH3S(c, s, k, grid, block, sm, g, c->L[0].cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist, c->times,
-             c->partials, c->counter, h, use_cond, do_norm, zc, Occ{c->tflags, c->tf_ntx, c->tf_nty});
+             c->partials, c->counter, h, use_cond, do_norm, c->sch_stencil.view());
 }
 
 // One named launcher per kernel of an iteration: the graph body is captured
@@ -834,6 +868,11 @@ void free_ctx(npsd_b200_ctx* c) {
     auto F = [](void* p) {
         if (p) cudaFree(p);
     };
+    for (SchedBufs* sb : {&c->sch_stencil}) {
+        F(sb->pre);
+        F(sb->zlo);
+        F(sb->len);
+    }
     for (auto& L : c->L) {
         F(L.cls);
         F(L.mmask);

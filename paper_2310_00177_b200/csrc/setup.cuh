@@ -92,6 +92,48 @@ __global__ void __launch_bounds__(kBlock) k_tile_flags(Geom g, const uint8_t* __
     }
 }
 
+// Live unit range of each tile column for a Sched: a column covers cw x ch
+// flag tiles; unit u (planes [u * unit, (u + 1) * unit)) is live when a flag of
+// the column is set within zdil planes of it. Units outside [zlo, zlo + len)
+// have every input zero (their outputs are the zeros already in place).
+__global__ void __launch_bounds__(kBlock) k_sched_cols(const uint8_t* __restrict__ flags, int ftx, int fty, int nz,
+                                                       int cw, int ch, int ntx, int nty, int unit, int zdil,
+                                                       int* __restrict__ zlo, int* __restrict__ len) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntx * nty) return;
+    const int fx0 = (t % ntx) * cw, fy0 = (t / ntx) * ch;
+    const int fx1 = min(fx0 + cw, ftx), fy1 = min(fy0 + ch, fty);
+    int first = -1, last = -1;
+    for (int z = 0; z < nz; ++z) {
+        bool any = false;
+        for (int fy = fy0; fy < fy1 && !any; ++fy)
+            for (int fx = fx0; fx < fx1; ++fx) any |= flags[((long long)z * fty + fy) * ftx + fx] != 0;
+        if (any) {
+            if (first < 0) first = z;
+            last = z;
+        }
+    }
+    if (first < 0) {
+        zlo[t] = 0;
+        len[t] = 0;
+        return;
+    }
+    const int u0 = max(first - zdil, 0) / unit;
+    const int u1 = min(last + zdil, nz - 1) / unit;
+    zlo[t] = u0;
+    len[t] = u1 - u0 + 1;
+}
+
+__global__ void k_sched_prefix(const int* __restrict__ len, int n, int* __restrict__ pre) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int acc = 0;
+    for (int t = 0; t < n; ++t) {
+        pre[t] = acc;
+        acc += len[t];
+    }
+    pre[n] = acc;
+}
+
 // PaddedImage::pooled (net/kernels.hpp:46-56), 3D order x-fastest then z+1
 // plane; from the L0 one-hot types (src_types) or a pooled level (src_img).
 template <int D>

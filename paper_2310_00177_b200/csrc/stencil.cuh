@@ -24,7 +24,13 @@ namespace nb2 {
 constexpr int kSX = 32, kSY = 8;          // threads per block (x lanes, y rows)
 constexpr int kTX = 2 * kSX, kTY = kSY;    // cells per block tile (64 x 8)
 constexpr int kVW = kTX + 4, kVH = kTY + 2;  // staged plane: cols x0-2..x0+65, rows y0-1..y0+8
-constexpr int kPF = 2;                     // planes prefetched ahead
+constexpr int kPF = 2;                     // planes prefetched ahead (down0.cuh)
+#ifndef STENCIL_PF_ORTHO
+#define STENCIL_PF_ORTHO 3
+#endif
+#ifndef STENCIL_PF_UPDATE
+#define STENCIL_PF_UPDATE 2
+#endif
 constexpr int kST = kPF + 1;               // input ring stages
 constexpr unsigned kOut2 = 0x0C0Cu;        // pair bytes outside the domain: type 3
 
@@ -66,6 +72,7 @@ template <int NO>
 struct OrthoOp {
     static constexpr int NA = 1 + NO;  // d, d_1..d_NO
     static constexpr int NC = 1;       // r (centre only)
+    static constexpr int PF = STENCIL_PF_ORTHO;  // planes prefetched ahead
     const double* in[NA];
     const double* ctr[NC];
     double mp[NO > 0 ? NO : 1];
@@ -82,6 +89,7 @@ struct OrthoOp {
 struct UpdateOp {
     static constexpr int NA = 2;  // x, d'
     static constexpr int NC = 1;  // b (centre only)
+    static constexpr int PF = STENCIL_PF_UPDATE;
     const double* in[NA];
     const double* ctr[NC];
     double alpha;
@@ -92,24 +100,21 @@ struct UpdateOp {
 
 template <typename Op>
 struct MarchSmem {
-    double raw[kST][Op::NA][kVH][kVW];  // operand inputs, tile + halo
-    double ctr[kST][Op::NC][kTY][kTX];  // centre-only inputs
+    double raw[Op::PF + 1][Op::NA][kVH][kVW];  // operand inputs, tile + halo
+    double ctr[Op::PF + 1][Op::NC][kTY][kTX];  // centre-only inputs
     double v[4][kVH][kVW];              // operand ring
 };
 
 // Epi(q, v2 own pair, s2 rows, pair bytes, own raw inputs [NA] x 2, centre [NC] x 2, acc)
 template <int D, int NV, typename Op, typename Epi>
-__device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __restrict__ cls, const Op& op, int zc0,
-                                              int zc1, double (&acc)[NV], Epi epi, const Occ& occ) {
-    // a fluid-free tile has no rows to evaluate (block-uniform early exit,
-    // before any barrier; the caller's reduction still runs)
-    if (occ.flags && !region_has_fluid(occ.flags, occ.ntx, occ.nty, g.nz, 2 * blockIdx.x, 2 * blockIdx.x + 2,
-                                       blockIdx.y, blockIdx.y + 1, zc0, zc1 - 1))
-        return;
+__device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __restrict__ cls, const Op& op, int tx,
+                                              int ty, int zc0, int zc1, double (&acc)[NV], Epi epi) {
+    constexpr int PF = Op::PF, ST = PF + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem<Op>& S = *reinterpret_cast<MarchSmem<Op>*>(smem_raw);
+    __syncthreads();  // the previous segment's last reads of S are done
     const int lane = threadIdx.x, row = threadIdx.y;
-    const int X0 = blockIdx.x * kTX, Y0 = blockIdx.y * kTY;
+    const int X0 = tx * kTX, Y0 = ty * kTY;
     const int x = X0 + 2 * lane, y = Y0 + row;
     const bool own = x < g.nx && y < g.ny;  // nx even: the pair is whole
     const long long nx = g.nx, plane = nx * g.ny;
@@ -136,15 +141,14 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
     auto own_bytes = [&](int z) -> unsigned {
         return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
     };
-    auto halo_live = [&](int z) -> bool {
-        if (!h_in || !zin(z)) return false;
-        if (hkind == 1) return pair_live(__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qh)));
-        return fluid(__ldg(cls + z * plane + qh));
-    };
-    auto slot = [&](int z) { return (z - zc0 + 1 + kST * 1024) % kST; };
-    // issue the copies of plane z (one commit group per plane, even if empty)
-    auto issue = [&](int z, unsigned ob, bool hl) {
+    auto slot = [&](int z) { return (z - zc0 + 1 + ST * 1024) % ST; };
+    // issue the copies of plane z (one commit group per plane, even if empty).
+    // Own pairs without fluid are zero-filled (no traffic); halo cells are
+    // always copied when in the domain: their non-fluid values are the exact
+    // zeros of the solver vectors, so no byte test sits on the issue path.
+    auto issue = [&](int z, unsigned ob) {
         if (zin(z)) {
+            const bool hl = h_in;
             const int s = slot(z);
             const bool ol = own && pair_live(ob);
             const long long qz = z * plane;
@@ -194,19 +198,15 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
 
     // prologue: bytes and copies of planes zc0-1 .. zc0+PF-1
     const int zlo = (D == 3) ? zc0 - 1 : zc0;
-    unsigned ob[kPF + 2];  // own bytes of planes z .. z+PF+1 (rotating)
-    bool hl[kPF + 2];
+    unsigned ob[PF + 2];  // own bytes of planes z .. z+PF+1 (rotating)
     unsigned ob_m = own_bytes(zlo);
-    issue(zlo, ob_m, halo_live(zlo));
+    issue(zlo, ob_m);
     if (D == 3) {
 #pragma unroll
-        for (int k = 0; k < kPF + 2; ++k) {
-            ob[k] = own_bytes(zc0 + k);
-            hl[k] = halo_live(zc0 + k);
-        }
+        for (int k = 0; k < PF + 2; ++k) ob[k] = own_bytes(zc0 + k);
 #pragma unroll
-        for (int k = 0; k < kPF; ++k) issue(zc0 + k, ob[k], hl[k]);
-        cp_wait<kPF - 1>();  // planes zc0-1, zc0 landed (own copies)
+        for (int k = 0; k < PF; ++k) issue(zc0 + k, ob[k]);
+        cp_wait<PF - 1>();  // planes zc0-1, zc0 landed (own copies)
         form(zc0 - 1);
         form(zc0);
     } else {
@@ -214,10 +214,13 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
         cp_wait<0>();
         form(zc0);
     }
+    // unrolled by the queue length: the rotation below becomes register
+    // renaming instead of moves that would wait on the in-flight byte loads
+#pragma unroll(PF + 2)
     for (int z = zc0; z < zc1; ++z) {
         if (D == 3) {
-            issue(z + kPF, ob[kPF], hl[kPF]);  // the plane kPF steps ahead
-            cp_wait<kPF - 1>();                 // plane z+1 landed
+            issue(z + PF, ob[PF]);  // the plane PF steps ahead
+            cp_wait<PF - 1>();                 // plane z+1 landed
             form(z + 1);
         }
         __syncthreads();  // v of planes z-1, z, z+1 complete (halos included)
@@ -251,14 +254,8 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
         }
         // rotate the byte queues
 #pragma unroll
-        for (int k = 0; k < kPF + 1; ++k) {
-            ob[k] = ob[k + 1];
-            hl[k] = hl[k + 1];
-        }
-        if (D == 3) {
-            ob[kPF + 1] = own_bytes(z + kPF + 2);
-            hl[kPF + 1] = halo_live(z + kPF + 2);
-        }
+        for (int k = 0; k < PF + 1; ++k) ob[k] = ob[k + 1];
+        if (D == 3) ob[PF + 1] = own_bytes(z + PF + 2);
     }
     cp_wait<0>();
 }
@@ -269,7 +266,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
                                                      const double* __restrict__ dtmp, const double* __restrict__ r,
                                                      double* __restrict__ Dring, double* __restrict__ ADring,
                                                      SolverState* st, double* __restrict__ partials,
-                                                     unsigned int* __restrict__ counter, int zchunk, Occ occ) {
+                                                     unsigned int* __restrict__ counter, Sched sc) {
     const int nc = st->n_cache, R = st->ring;
     const int nw = (st->head + 1) % R;
     using Op = OrthoOp<NO>;
@@ -289,9 +286,8 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
     double acc[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc[j] = 0.0;
-    const int zc0 = blockIdx.z * zchunk;
-    const int zc1 = min(zc0 + zchunk, g.nz);
-    stencil_march<D, NV>(g, cls, op, zc0, zc1, acc,
+    sched_for_each(sc, [&](int tx, int ty, int zc0, int zc1) {
+    stencil_march<D, NV>(g, cls, op, tx, ty, zc0, zc1, acc,
                          [&](long long q, double2 v, double2 s, unsigned bc, const double(&i0)[Op::NA],
                              const double(&i1)[Op::NA], const double(&c0)[1], const double(&c1)[1], double(&a)[NV]) {
                              *reinterpret_cast<double2*>(dnew + q) = v;
@@ -307,7 +303,8 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
                                      a[2 + j] += i0[1 + j] * s.x;
                                      a[2 + j] += i1[1 + j] * s.y;
                                  }
-                         }, occ);
+                         });
+    });
     double tot[NV];
     if (grid_reduce<NV>(acc, partials, counter, tot)) {
         if (threadIdx.x == 0 && threadIdx.y == 0) {
@@ -339,9 +336,9 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
                                                       double* __restrict__ times, double* __restrict__ partials,
                                                       unsigned int* __restrict__ counter,
                                                       cudaGraphConditionalHandle cond, int use_cond, int do_norm,
-                                                      int zchunk, Occ occ) {
+                                                      Sched sc) {
     if (st->breakdown) {
-        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+        if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0)
             set_cond(cond, use_cond, 0u);
         return;
     }
@@ -353,9 +350,8 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
     op.alpha = st->alpha;
     double* xn = st->xcur ? X0 : X1;
     double acc[1] = {0.0};
-    const int zc0 = blockIdx.z * zchunk;
-    const int zc1 = min(zc0 + zchunk, g.nz);
-    stencil_march<D, 1>(g, cls, op, zc0, zc1, acc,
+    sched_for_each(sc, [&](int tx, int ty, int zc0, int zc1) {
+    stencil_march<D, 1>(g, cls, op, tx, ty, zc0, zc1, acc,
                         [&](long long q, double2 v, double2 s, unsigned bc, const double(&)[2], const double(&)[2],
                             const double(&c0)[1], const double(&c1)[1], double(&a)[1]) {
                             double2 rv;
@@ -365,7 +361,8 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
                             *reinterpret_cast<double2*>(r + q) = rv;
                             a[0] += rv.x * rv.x;
                             a[0] += rv.y * rv.y;
-                        }, occ);
+                        });
+    });
     if (!do_norm) return;
     double tot[1];
     if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0)
