@@ -32,26 +32,18 @@ struct Down0Smem {
     float yp[2][kTY][kTX];      // y_0 of the last two planes (pooling)
 };
 
-// zchunk even; grid (nx/64, ny/8, nz/zchunk); dynamic smem = sizeof(Down0Smem)
-__global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __restrict__ cls,
-                                                      const double* __restrict__ r, const SolverState* __restrict__ st,
-                                                      const __grid_constant__ KC0 kc, float* __restrict__ y,
-                                                      float* __restrict__ xnext, Geom gc, int zchunk, Occ occ) {
-    const int zc0 = blockIdx.z * zchunk;
-    const int zc1 = min(zc0 + zchunk, g.nz);
+// One column segment: tile (tx, ty), planes [zc0, zc1) (zc0 even)
+__device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __restrict__ cls,
+                                                const double* __restrict__ r, const SolverState* __restrict__ st,
+                                                const KC0& kc, float* __restrict__ y, float* __restrict__ xnext,
+                                                const Geom& gc, int tx, int ty, int zc0, int zc1) {
     const int lane = threadIdx.x, row = threadIdx.y;
-    const int X0 = blockIdx.x * kTX, Y0 = blockIdx.y * kTY;
+    const int X0 = tx * kTX, Y0 = ty * kTY;
     const int x = X0 + 2 * lane, yy = Y0 + row;
     const bool own = x < g.nx && yy < g.ny;  // nx even: the pair is whole
-    if (occ.flags && !region_has_fluid(occ.flags, occ.ntx, occ.nty, g.nz, 2 * blockIdx.x, 2 * blockIdx.x + 2,
-                                       blockIdx.y, blockIdx.y + 1, zc0 - 1, zc1)) {
-        // all inputs zero: x_1 = +0 on this tile's coarse cells
-        if (own && !(row & 1))
-            for (int z = zc0 + 1; z < zc1; z += 2) xnext[lin(gc, x >> 1, yy >> 1, z >> 1)] = 0.0f;
-        return;
-    }
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Down0Smem& S = *reinterpret_cast<Down0Smem*>(smem_raw);
+    __syncthreads();  // the previous segment's last reads of S are done
     const long long nx = g.nx, plane = nx * g.ny;
     const double inv1 = st->inv1, inv2 = st->inv2;
     // halo assignment (as stencil_march)
@@ -83,14 +75,11 @@ __global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __r
     auto own_bytes = [&](int z) -> unsigned {
         return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
     };
-    auto halo_live = [&](int z) -> bool {
-        if (!h_in || !zin(z)) return false;
-        if (hkind == 1) return pair_live(__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qh)));
-        return fluid(__ldg(cls + z * plane + qh));
-    };
     auto slot = [&](int z) { return (z - zc0 + 1 + kST * 1024) % kST; };
-    auto issue = [&](int z, unsigned ob, bool hl) {
+    // own pairs without fluid zero-filled; halo always copied (exact zeros)
+    auto issue = [&](int z, unsigned ob) {
         if (zin(z)) {
+            const bool hl = h_in;
             const int s = slot(z);
             const bool ol = own && pair_live(ob);
             const long long qz = z * plane;
@@ -113,15 +102,11 @@ __global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __r
     };
     // prologue (as stencil_march): planes zc0-1 .. zc0+PF-1 issued, zc0-1 and zc0 formed
     unsigned ob[kPF + 2];
-    bool hl[kPF + 2];
-    issue(zc0 - 1, own_bytes(zc0 - 1), halo_live(zc0 - 1));
+    issue(zc0 - 1, own_bytes(zc0 - 1));
 #pragma unroll
-    for (int k = 0; k < kPF + 2; ++k) {
-        ob[k] = own_bytes(zc0 + k);
-        hl[k] = halo_live(zc0 + k);
-    }
+    for (int k = 0; k < kPF + 2; ++k) ob[k] = own_bytes(zc0 + k);
 #pragma unroll
-    for (int k = 0; k < kPF; ++k) issue(zc0 + k, ob[k], hl[k]);
+    for (int k = 0; k < kPF; ++k) issue(zc0 + k, ob[k]);
     cp_wait<kPF - 1>();
     form(zc0 - 1);
     form(zc0);
@@ -134,8 +119,9 @@ __global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __r
     };
     float mya, myb;
     mixed_y(zc0, ob[0], mya, myb);
+#pragma unroll(kPF + 2)
     for (int z = zc0; z < zc1; ++z) {
-        issue(z + kPF, ob[kPF], hl[kPF]);
+        issue(z + kPF, ob[kPF]);
         cp_wait<kPF - 1>();
         form(z + 1);
         float nya = 0.0f, nyb = 0.0f;
@@ -186,14 +172,22 @@ __global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __r
         mya = nya;
         myb = nyb;
 #pragma unroll
-        for (int k = 0; k < kPF + 1; ++k) {
-            ob[k] = ob[k + 1];
-            hl[k] = hl[k + 1];
-        }
+        for (int k = 0; k < kPF + 1; ++k) ob[k] = ob[k + 1];
         ob[kPF + 1] = own_bytes(z + kPF + 2);
-        hl[kPF + 1] = halo_live(z + kPF + 2);
     }
     cp_wait<0>();
+}
+
+// Balanced schedule (Sched, units of two planes: pooling pairs stay inside a
+// segment); dynamic smem = sizeof(Down0Smem). Units outside the schedule have
+// an all-zero window: their x_1 cells keep the zeros set before the solve.
+__global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __restrict__ cls,
+                                                      const double* __restrict__ r, const SolverState* __restrict__ st,
+                                                      const __grid_constant__ KC0 kc, float* __restrict__ y,
+                                                      float* __restrict__ xnext, Geom gc, Sched sc) {
+    sched_for_each(sc, [&](int tx, int ty, int u0, int u1) {
+        down_l0_segment(g, cls, r, st, kc, y, xnext, gc, tx, ty, 2 * u0, min(2 * u1, g.nz));
+    });
 }
 
 }  // namespace nb2

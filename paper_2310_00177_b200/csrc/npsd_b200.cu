@@ -99,6 +99,8 @@ struct npsd_b200_ctx {
     uint32_t *fmask = nullptr, *fbase = nullptr, *fcount = nullptr;
     uint8_t* tflags = nullptr;  // L0 tile occupancy (k_tile_flags)
     SchedBufs sch_stencil;      // 64 x 8 tile columns, plane units (k_ortho2, k_update2)
+    SchedBufs sch_down0;        // 64 x 8 tile columns, plane-pair units, window dilation (k_down_l0)
+    bool x1_clean = false;      // L1.x is zero outside sch_down0's units
     // level-0 window-pattern dictionary (setup.cuh)
     unsigned long long *dkeys = nullptr, *dskeys = nullptr;
     uint32_t *dvals = nullptr, *dsidx = nullptr, *dhead = nullptr, *dscan = nullptr;
@@ -313,6 +315,8 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
            c->tflags);
     build_sched(c, c->sch_stencil, kTX, kTY, 1, 0);
+    if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1);
+    c->x1_clean = false;
     for (int l = 1; l < c->depth; ++l) {
         LevelBufs& Lf = c->L[l - 1];
         LevelBufs& Lc = c->L[l];
@@ -552,16 +556,13 @@ void launch_down_l0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
     const Geom g = L.g;
     const dim3 block(kSX, kSY);
-    const int gx = (g.nx + kTX - 1) / kTX, gy = (g.ny + kTY - 1) / kTY;
     const size_t sm = sizeof(Down0Smem);
     CK(cudaFuncSetAttribute(k_down_l0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    int zc = zchunk_for(c, k_down_l0, kSX * kSY, (long long)gx * gy, g.nz, sm);
-    zc = (zc + 1) & ~1;  // pooling pairs stay inside a block
-    const dim3 grid(gx, gy, (g.nz + zc - 1) / zc);
+    const dim3 grid(wave_blocks(c, k_down_l0, kSX * kSY, sm));
     KC0 kc0;
     for (int i = 0; i < 27; ++i) kc0.k[i] = c->kc_down[0].k[0][i];  // the uniform-fluid kernel
-    LAUNCH3S(c, s, k_down_l0, grid, block, sm, g, L.cls, c->R, c->st, kc0, L.y, c->L[1].x, c->L[1].g, zc,
-             Occ{c->tflags, c->tf_ntx, c->tf_nty});
+    LAUNCH3S(c, s, k_down_l0, grid, block, sm, g, L.cls, c->R, c->st, kc0, L.y, c->L[1].x, c->L[1].g,
+             c->sch_down0.view());
 }
 
 template <int D>
@@ -638,8 +639,20 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     return v;
 }
 
+// k_down_l0 visits only live units: x_1 must hold zeros elsewhere before a
+// solve-path network runs (set_mask and raw-network calls leave it dirty)
+void ensure_x1_clean(npsd_b200_ctx* c, cudaStream_t s) {
+    if (c->x1_clean || c->dim != 3 || c->depth < 2) return;
+    CK(cudaMemsetAsync(c->L[1].x, 0, (size_t)c->L[1].g.n * sizeof(float), s));
+    c->x1_clean = true;
+}
+
 template <int D>
 void launch_network(npsd_b200_ctx* c, cudaStream_t s, bool raw, int* launches) {
+    if (raw)
+        c->x1_clean = false;
+    else
+        ensure_x1_clean(c, s);
     const auto steps = network_steps<D>(c, raw, 0);
     for (const auto& st : steps) st.run(s);
     if (launches) *launches = (int)steps.size();
@@ -798,6 +811,7 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
     h->nullspace = nullspace;
     h->ring = ring;
     CK(cudaMemcpyAsync(c->st, h, sizeof(SolverState), cudaMemcpyHostToDevice, c->s));
+    ensure_x1_clean(c, c->s);
     CK(cudaEventRecord(c->ev0, c->s));
     CK(cudaGraphLaunch(c->exec, c->s));
     CK(cudaEventRecord(c->ev1, c->s));
@@ -868,7 +882,7 @@ void free_ctx(npsd_b200_ctx* c) {
     auto F = [](void* p) {
         if (p) cudaFree(p);
     };
-    for (SchedBufs* sb : {&c->sch_stencil}) {
+    for (SchedBufs* sb : {&c->sch_stencil, &c->sch_down0}) {
         F(sb->pre);
         F(sb->zlo);
         F(sb->len);
@@ -1365,6 +1379,7 @@ int npsd_b200_profile_iterations(npsd_b200_ctx* c, const double* d_b, const npsd
         h->ring = ring;
         CK(cudaMemcpyAsync(c->st, h, sizeof(SolverState), cudaMemcpyHostToDevice, c->s));
         const int ns = cfg->nullspace_projection ? 1 : 0;
+        ensure_x1_clean(c, c->s);
         std::vector<Step> pro, bod;
         if (c->dim == 3) {
             pro = prologue_steps<3>(c, 0, 0, ns);

@@ -280,3 +280,25 @@ def test_solve_device_path(b200, oracle):
     assert np.all(xf[t.reshape(-1) != 0] == 0.0)
     db.free()
     dx.free()
+
+
+def test_raw_network_then_solve_unchanged(b200, oracle):
+    """The solve path visits live tiles only and relies on zeros elsewhere in
+    its network buffers; a raw net_apply (dense input, writes every cell) and a
+    frame change in between must not leak into the next solve."""
+    t, seed = scenes.config("C3", 64)
+    p = oracle.init_params(3, 4, 11)
+    ctx = b200.Context(3, t.shape, b200.NetParams(3, 4, p))
+    ctx.set_mask(t)
+    b = oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    cfg = b200.SolveConfig(max_iters=15, tol_reduction=1e-300)
+    first = ctx.psdo_solve(b, cfg).report.residual_history
+    r = np.random.default_rng(0).standard_normal(ctx.n_fluid)
+    z1 = ctx.precond_apply(r)
+    ctx.net_apply(np.random.default_rng(1).standard_normal(t.size).astype(np.float32).reshape(t.shape))
+    assert np.array_equal(ctx.precond_apply(r), z1)
+    assert np.array_equal(ctx.psdo_solve(b, cfg).report.residual_history, first)
+    # another frame, then back: bitwise the same again
+    ctx.set_mask(list(scenes.droplet_frames(64, 2))[1])
+    ctx.set_mask(t)
+    assert np.array_equal(ctx.psdo_solve(b, cfg).report.residual_history, first)
