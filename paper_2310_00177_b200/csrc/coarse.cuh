@@ -1,0 +1,213 @@
+// Network levels above the solve's level 0, 3D (and every level of the raw
+// network): NetContext::apply's down and up steps (net/forward.hpp:95-129)
+// with one thread per cell.
+//
+// These grids are small (128^3 and below at 256^3) and their kernels are
+// latency-bound, not bandwidth-bound: what matters is enough independent
+// cells in flight and short dependent chains. A 32 x 4 x 2 block stages its
+// input tile plus a one-cell halo (f32) in shared memory, one warp per row;
+// each thread reads its kernel as one 28-float row (seven 16-byte loads)
+// through a single pointer — the shared copy of its uniform class's kernel or
+// its mixed row in global memory — so uniform and mixed cells of a warp run
+// the same code. One barrier, then the 27 taps in slot order with
+// round-to-nearest ops (apply_kernels, net/kernels.hpp:147-172): outputs are
+// bit-identical to the restatement.
+//
+// k_cdown<POOL>: y_l = conv_down_l(x_l); x_{l+1} = avg_pool(y_l) from the
+//   block's y tile in shared memory, summed x fastest, then y, then z
+//   (avg_pool2, kernels.hpp:279-292, 3D order). Without POOL: the coarsest
+//   level's single conv (forward.hpp:89,116).
+// k_cup: out_l = z_a y_l + z_b conv_up_l(upsample2(out_{l+1}))
+//   (forward.hpp:118-127); the coarse tile (halo included) is staged, and a
+//   fine tap reads coarse cell (x >> 1, y >> 1, z >> 1), zero outside.
+#pragma once
+
+#include "common.cuh"
+#include "net.cuh"
+#include "net2.cuh"
+
+namespace nb2 {
+
+constexpr int kKX = 32, kKY = 4, kKZ = 2, kKT = kKX * kKY * kKZ;  // block tile = threads (256)
+
+// The three uniform-window kernels in shared memory as 28-float rows, so every
+// cell reads its kernel through one pointer: no per-class code paths, no warp
+// divergence between uniform and mixed cells.
+struct UniRows {
+    float4 r[3][7];
+};
+
+__device__ __forceinline__ void load_uni_rows(UniRows& U, const KC& kc, int tid) {
+    if (tid < 84) {
+        const int w = tid / 28, s = tid - 28 * w;
+        reinterpret_cast<float*>(&U.r[w][0])[s] = (s < 27) ? kc.k[w][s] : 0.0f;
+    }
+}
+
+__device__ __forceinline__ void load_row(const float4* row, float (&k)[28]) {
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+        const float4 v = row[i];  // generic: shared or global
+        k[4 * i] = v.x;
+        k[4 * i + 1] = v.y;
+        k[4 * i + 2] = v.z;
+        k[4 * i + 3] = v.w;
+    }
+}
+
+// A (NZ x NY x NX) box at (bx, by, bz) of level geometry gg, zero outside,
+// staged one warp per row: every load is issued (compile-time trip counts)
+// before any shared store, so the loads of a thread overlap.
+template <int NX, int NY, int NZ, int NW>
+struct BoxStager {
+    static constexpr int RPW = (NY * NZ + NW - 1) / NW;  // rows per warp
+    static constexpr int EPL = (NX + 31) / 32;            // elements per lane per row
+    float v[RPW][EPL];
+    __device__ __forceinline__ void load(const float* __restrict__ src, const Geom& gg, int bx, int by, int bz,
+                                         int warp, int lane) {
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int r = warp + NW * k;
+            const int ly = r % NY, lz = r / NY;
+            const int gy = by + ly, gz = bz + lz;
+            const bool rin = r < NY * NZ && gy >= 0 && gy < gg.ny && gz >= 0 && gz < gg.nz;
+            const float* rowp = src + ((long long)(rin ? gz : 0) * gg.ny + (rin ? gy : 0)) * gg.nx;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+                const int lx = lane + 32 * e, gx = bx + lx;
+                v[k][e] = (rin && lx < NX && gx >= 0 && gx < gg.nx) ? __ldg(rowp + gx) : 0.0f;
+            }
+        }
+    }
+    __device__ __forceinline__ void store(float (&dst)[NZ][NY][NX], int warp, int lane) const {
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int r = warp + NW * k;
+            if (r < NY * NZ) {
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const int lx = lane + 32 * e;
+                    if (lx < NX) dst[r / NY][r % NY][lx] = v[k][e];
+                }
+            }
+        }
+    }
+};
+
+// The cell's 28-float kernel row: a mixed cell loads its row from global
+// memory before the barrier (mixed_start), a uniform cell reads its class's
+// shared row after it (uniform_finish).
+struct CellRow {
+    float k[28];
+    int wc;
+    // own: the cell is inside the grid (else it reads as a uniform-air cell)
+    __device__ __forceinline__ void mixed_start(const ConvTab& ct, long long c, bool own) {
+        if (!own) {
+            wc = 1;
+        } else if (ct.rcode) {
+            const uint32_t rc = __ldg(ct.rcode + c);
+            wc = (int)(rc >> 30);
+            if (wc == 3) load_row(reinterpret_cast<const float4*>(ct.tab + (long long)(rc & 0x3fffffffu) * kRowW), k);
+        } else {
+            wc = cls_window(__ldg(ct.cls + c));
+            if (wc == 3) load_row(reinterpret_cast<const float4*>(kernel_row(ct, c)), k);
+        }
+    }
+    __device__ __forceinline__ void uniform_finish(const UniRows& U) {
+        if (wc < 3) load_row(&U.r[wc][0], k);
+    }
+};
+
+// grid (ceil(nx/32), ceil(ny/4), nz/2), block (32, 4, 2)
+template <bool POOL>
+__global__ void __launch_bounds__(kKT) k_cdown(Geom g, const float* __restrict__ x, ConvTab ct,
+                                               const __grid_constant__ KC kc, float* __restrict__ y,
+                                               float* __restrict__ xnext, Geom gc) {
+    constexpr int SX = kKX + 2, SY = kKY + 2, SZ = kKZ + 2;
+    __shared__ float sx[SZ][SY][SX];
+    __shared__ float sy[kKZ][kKY][kKX];
+    __shared__ UniRows U;
+    const int tx = threadIdx.x, ty = threadIdx.y, tz = threadIdx.z;
+    const int tid = tx + kKX * (ty + kKY * tz), warp = tid >> 5, lane = tid & 31;
+    const int X0 = blockIdx.x * kKX, Y0 = blockIdx.y * kKY, Z0 = blockIdx.z * kKZ;
+    const int cx = X0 + tx, cy = Y0 + ty, cz = Z0 + tz;
+    const bool own = cx < g.nx && cy < g.ny && cz < g.nz;
+    const long long c = own ? lin(g, cx, cy, cz) : 0;
+    BoxStager<SX, SY, SZ, kKT / 32> box;
+    box.load(x, g, X0 - 1, Y0 - 1, Z0 - 1, warp, lane);
+    CellRow K;
+    K.mixed_start(ct, c, own);
+    load_uni_rows(U, kc, tid);
+    box.store(sx, warp, lane);
+    __syncthreads();
+    K.uniform_finish(U);
+    float yv = 0.0f;
+    if (own) {
+#pragma unroll
+        for (int s = 0; s < 27; ++s) {
+            const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
+            yv = __fadd_rn(yv, __fmul_rn(K.k[s], sx[tz + 1 + dz][ty + 1 + dy][tx + 1 + dx]));
+        }
+        y[c] = yv;
+    }
+    if (POOL) {
+        sy[tz][ty][tx] = yv;
+        __syncthreads();
+        constexpr int PX = kKX / 2, PY = kKY / 2;
+        if (tid < PX * PY) {
+            const int px = tid % PX, py = tid / PX;
+            const int qx = (X0 >> 1) + px, qy = (Y0 >> 1) + py, qz = Z0 >> 1;
+            if (qx < gc.nx && qy < gc.ny && qz < gc.nz) {
+                float ps = sy[0][2 * py][2 * px];
+                ps = __fadd_rn(ps, sy[0][2 * py][2 * px + 1]);
+                ps = __fadd_rn(ps, sy[0][2 * py + 1][2 * px]);
+                ps = __fadd_rn(ps, sy[0][2 * py + 1][2 * px + 1]);
+                ps = __fadd_rn(ps, sy[1][2 * py][2 * px]);
+                ps = __fadd_rn(ps, sy[1][2 * py][2 * px + 1]);
+                ps = __fadd_rn(ps, sy[1][2 * py + 1][2 * px]);
+                ps = __fadd_rn(ps, sy[1][2 * py + 1][2 * px + 1]);
+                xnext[lin(gc, qx, qy, qz)] = __fmul_rn(0.125f, ps);
+            }
+        }
+    }
+}
+
+// grid (ceil(nx/32), ceil(ny/4), nz/2), block (32, 4, 2); outc is level l+1
+template <int D = 3>
+__global__ void __launch_bounds__(kKT) k_cup(Geom g, Geom gc, const float* __restrict__ outc,
+                                             const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
+                                             const __grid_constant__ KC kc, float* __restrict__ outl) {
+    // coarse box: (X0/2 - 1 .. X0/2 + 16) x (Y0/2 - 1 .. Y0/2 + 2) x (Z0/2 - 1 .. Z0/2 + 1)
+    constexpr int CX = kKX / 2 + 2, CY = kKY / 2 + 2, CZ = kKZ / 2 + 2;
+    __shared__ float sc[CZ][CY][CX];
+    __shared__ UniRows U;
+    const int tx = threadIdx.x, ty = threadIdx.y, tz = threadIdx.z;
+    const int tid = tx + kKX * (ty + kKY * tz), warp = tid >> 5, lane = tid & 31;
+    const int X0 = blockIdx.x * kKX, Y0 = blockIdx.y * kKY, Z0 = blockIdx.z * kKZ;
+    const int BX = (X0 >> 1) - 1, BY = (Y0 >> 1) - 1, BZ = (Z0 >> 1) - 1;
+    const int cx = X0 + tx, cy = Y0 + ty, cz = Z0 + tz;
+    const bool own = cx < g.nx && cy < g.ny && cz < g.nz;
+    const long long c = own ? lin(g, cx, cy, cz) : 0;
+    BoxStager<CX, CY, CZ, kKT / 32> box;
+    box.load(outc, gc, BX, BY, BZ, warp, lane);
+    CellRow K;
+    K.mixed_start(ct, c, own);
+    const float yv = own ? __ldg(yl + c) : 0.0f;
+    const float za = zab[0], zb = zab[1];
+    load_uni_rows(U, kc, tid);
+    box.store(sc, warp, lane);
+    __syncthreads();
+    if (!own) return;
+    K.uniform_finish(U);
+    // fine tap (cx + dx, ...) -> coarse ((cx + dx) >> 1, ...); out-of-domain
+    // fine cells map to out-of-domain coarse cells (dims even): staged zeros
+    float u = 0.0f;
+#pragma unroll
+    for (int s = 0; s < 27; ++s) {
+        const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
+        u = __fadd_rn(u, __fmul_rn(K.k[s], sc[((cz + dz) >> 1) - BZ][((cy + dy) >> 1) - BY][((cx + dx) >> 1) - BX]));
+    }
+    outl[c] = __fadd_rn(__fmul_rn(za, yv), __fmul_rn(zb, u));
+}
+
+}  // namespace nb2

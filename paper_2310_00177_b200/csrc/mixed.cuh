@@ -68,6 +68,24 @@ __global__ void __launch_bounds__(kBlock) k_mixed_split(const uint32_t* __restri
     }
 }
 
+// levels >= 1: one word per cell, (window class << 30) | mixed row, so the
+// coarse kernels reach a mixed cell's row with one load (coarse.cuh)
+__global__ void __launch_bounds__(kBlock) k_row_codes(Geom g, const uint8_t* __restrict__ cls,
+                                                      const uint32_t* __restrict__ mmask,
+                                                      const uint32_t* __restrict__ mbase,
+                                                      const uint32_t* __restrict__ kid, uint32_t* __restrict__ rcode) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+        const uint32_t w = (uint32_t)cls_window(cls[c]);
+        uint32_t row = 0;
+        if (w == 3) {
+            row = (uint32_t)mixed_index(mmask, mbase, c);
+            if (kid) row = kid[row];
+        }
+        rcode[c] = (w << 30) | row;
+    }
+}
+
 // number of mixed cells = last exclusive base + last count
 __global__ void k_seg_total(const uint32_t* __restrict__ base, const uint32_t* __restrict__ cnt, long long nseg,
                             uint32_t* __restrict__ out) {

@@ -35,6 +35,7 @@ struct ConvTab {
     const float* tab;     // rows [row][kRowW]
     const uint32_t* kid;  // mixed index -> row, or nullptr (identity)
     const float* kconst;  // [3][S]
+    const uint32_t* rcode;  // levels >= 1: per cell (window class << 30) | row, or nullptr
 };
 
 __device__ __forceinline__ const float* kernel_row(const ConvTab& ct, long long c) {

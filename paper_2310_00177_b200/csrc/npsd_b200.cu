@@ -25,6 +25,7 @@
 #include "net2.cuh"
 #include "mixed.cuh"
 #include "down0.cuh"
+#include "coarse.cuh"
 
 using namespace nb2;
 
@@ -69,6 +70,9 @@ struct LevelBufs {
     unsigned long long* zG = nullptr;
     uint32_t* mlist = nullptr;  // compact mixed cells (k_mixed_list)
     uint32_t* mcnt = nullptr;   // their number (device)
+    uint32_t* rcode = nullptr;  // levels >= 1: (window class << 30) | row per cell (k_row_codes)
+    uint32_t* pid = nullptr;    // levels >= 1: mixed index -> dictionary row (coarse_dictionary)
+    const uint32_t* kid = nullptr;  // pid when the level's dictionary verified, else nullptr
 };
 
 // one balanced schedule (common.cuh Sched) over L0 tile columns
@@ -107,6 +111,7 @@ struct npsd_b200_ctx {
     uint32_t *pid0 = nullptr, *repcell0 = nullptr, *npat0 = nullptr;
     // level-0 mixed sublists the solve reads (mixed.cuh): windows holding fluid
     // (down) and fluid cells (up), with their pattern ids
+    uint32_t *crep = nullptr, *cnpat = nullptr, *cflag = nullptr;  // coarse dictionaries (scratch)
     uint32_t *dlist0 = nullptr, *dkid0 = nullptr, *dcnt0 = nullptr;
     uint32_t *ulist0 = nullptr, *ukid0 = nullptr, *ucnt0 = nullptr;
     int tf_ntx = 0, tf_nty = 0;
@@ -268,11 +273,11 @@ void upload_params_and_kconst(npsd_b200_ctx* c) {
 
 ConvTab tab_down(const npsd_b200_ctx* c, int l) {
     const LevelBufs& L = c->L[l];
-    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_down, (l == 0) ? c->pid0 : nullptr, L.kc_down};
+    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_down, (l == 0) ? c->pid0 : L.kid, L.kc_down, L.rcode};
 }
 ConvTab tab_up(const npsd_b200_ctx* c, int l) {
     const LevelBufs& L = c->L[l];
-    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_up, (l == 0) ? c->pid0 : nullptr, L.kc_up};
+    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_up, (l == 0) ? c->pid0 : L.kid, L.kc_up, L.rcode};
 }
 
 // ---------------------------------------------------------------- set_mask
@@ -305,6 +310,43 @@ int wave_blocks(npsd_b200_ctx* c, K kernel, int threads, size_t smem) {
     return c->num_sms * occ;
 }
 
+// Hashed window-pattern dictionary of coarse level l (setup.cuh): L.pid[mixed
+// index] = pattern, c->crep / c->cnpat = representative cells. Returns false
+// (per-cell rows) when any window differs from its pattern's representative.
+template <int D>
+bool coarse_dictionary(npsd_b200_ctx* c, int l, uint32_t n) {
+    cudaStream_t s = c->s;
+    LevelBufs& L = c->L[l];
+    LAUNCH(c, s, k_window_hash<D>, (long long)n, L.g, L.img, L.mlist, L.mcnt, c->dkeys, c->dvals);
+    size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n, 0, 64, s));
+    if (bytes > c->cub_bytes) {
+        if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
+        CK(cudaMalloc(&c->cub_tmp, bytes));
+        c->cub_bytes = bytes;
+    }
+    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n, 0, 64, s));
+    c->launches += 4;
+    LAUNCH(c, s, k_run_heads, (long long)n, c->dskeys, L.mcnt, c->dhead);
+    bytes = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, c->dhead, c->dscan, (int)n, s));
+    if (bytes > c->cub_bytes) {
+        if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
+        CK(cudaMalloc(&c->cub_tmp, bytes));
+        c->cub_bytes = bytes;
+    }
+    CK(cub::DeviceScan::InclusiveSum(c->cub_tmp, bytes, c->dhead, c->dscan, (int)n, s));
+    c->launches += 2;
+    LAUNCH(c, s, k_pattern_ids, (long long)n, c->dsidx, c->dscan, c->dhead, L.mlist, L.mcnt, L.pid, c->crep,
+           c->cnpat);
+    CK(cudaMemsetAsync(c->cflag, 0, sizeof(uint32_t), s));
+    LAUNCH(c, s, k_verify_windows<D>, (long long)n, L.g, L.img, L.mlist, L.mcnt, L.pid, c->crep, c->cflag);
+    uint32_t bad = 1;
+    CK(cudaMemcpyAsync(&bad, c->cflag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return bad == 0;
+}
+
 template <int D>
 void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     cudaStream_t s = c->s;
@@ -333,10 +375,13 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         CK(cudaGetLastError());
         ++c->launches;
     }
-    // level 0: window-pattern dictionary (pid per mixed cell, one row per pattern)
-    uint32_t n_mixed0 = 0;
-    CK(cudaMemcpyAsync(&n_mixed0, L0.mcnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    // mixed counts of every level (host: sort sizes)
+    uint32_t n_mixed[kMaxDepth] = {};
+    for (int l = 0; l < c->depth; ++l)
+        CK(cudaMemcpyAsync(&n_mixed[l], c->L[l].mcnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    // level 0: window-pattern dictionary (pid per mixed cell, one row per pattern)
+    const uint32_t n_mixed0 = n_mixed[0];
     if (n_mixed0 > 0) {
         LAUNCH(c, s, k_window_keys<D>, (long long)n_mixed0, c->g0, dtypes, L0.mlist, L0.mcnt, c->dkeys, c->dvals);
         size_t bytes = 0;
@@ -383,10 +428,21 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         LevelBufs& L = c->L[l];
         const uint8_t* st = (l == 0) ? dtypes : nullptr;
         const float* im = (l == 0) ? nullptr : L.img;
-        // rows: one per window pattern at level 0, one per mixed cell above
+        // rows: one per window pattern (level 0 always; above when the hashed
+        // dictionary verifies), else one per mixed cell
         const uint32_t* cells = (l == 0) ? c->repcell0 : L.mlist;
         const uint32_t* ncells = (l == 0) ? c->npat0 : L.mcnt;
-        const long long rows_cap = (l == 0) ? (long long)n_mixed0 : L.g.n;
+        long long rows_cap = (l == 0) ? (long long)n_mixed0 : L.g.n;
+        if (l > 0) {
+            L.kid = nullptr;
+            if (n_mixed[l] > 0 && coarse_dictionary<D>(c, l, n_mixed[l])) {
+                L.kid = L.pid;
+                cells = c->crep;
+                ncells = c->cnpat;
+                rows_cap = n_mixed[l];
+            }
+            LAUNCH(c, s, k_row_codes, L.g.n, L.g, L.cls, L.mmask, L.mbase, L.kid, L.rcode);
+        }
         if (l < c->depth - 1) {
             const LevelOffsets& o = c->offs[(size_t)l];
             LAUNCH(c, s, k_build_rows<D>, rows_cap, L.g, st, im, cells, ncells, c->d_params + o.down_W,
@@ -465,6 +521,13 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
     LevelBufs& L = c->L[l];
     const Geom gc = POOL ? c->L[l + 1].g : L.g;
     float* xnext = POOL ? c->L[l + 1].x : nullptr;
+    if (D == 3 && !L0) {
+        // f32 input (levels >= 1, raw level 0): one thread per cell (coarse.cuh)
+        const KC& kc = (l == c->depth - 1) ? c->kc_coarse : c->kc_down[l];
+        const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.nz + kKZ - 1) / kKZ);
+        LAUNCH3(c, s, k_cdown<POOL>, grid, dim3(kKX, kKY, kKZ), L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc);
+        return;
+    }
     const dim3 block(kNX, kNY);
     const int gx = (L.g.nx + 2 * kNX - 1) / (2 * kNX), gy = (L.g.ny + 2 * kNY - 1) / (2 * kNY);
     const int nbz = (D == 3) ? (L.g.nz >> 1) : 1;
@@ -482,6 +545,12 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
     LevelBufs& L = c->L[l];
     const LevelBufs& Lc = c->L[l + 1];
     const float* outc = (l + 1 == c->depth - 1) ? Lc.y : Lc.out;
+    if (D == 3 && MODE == kUpMid) {
+        const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.nz + kKZ - 1) / kKZ);
+        LAUNCH3(c, s, k_cup<3>, grid, dim3(kKX, kKY, kKZ), L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
+                c->kc_up[l], outl);
+        return;
+    }
     const dim3 block(kNX, kNY);
     const int gx = (Lc.g.nx + kNX - 1) / kNX, gy = (Lc.g.ny + kNY - 1) / kNY;
     const int nbz = (D == 3) ? Lc.g.nz : 1;
@@ -902,6 +971,8 @@ void free_ctx(npsd_b200_ctx* c) {
         F(L.out);
         F(L.zG);
         F(L.mlist);
+        F(L.rcode);
+        F(L.pid);
         F(L.mcnt);
     }
     F(c->d_params);
@@ -913,7 +984,7 @@ void free_ctx(npsd_b200_ctx* c) {
     for (void* p : {(void*)c->dkeys, (void*)c->dskeys, (void*)c->dvals, (void*)c->dsidx, (void*)c->dhead,
                     (void*)c->dscan, (void*)c->pid0, (void*)c->repcell0, (void*)c->npat0,
                     (void*)c->dlist0, (void*)c->dkid0, (void*)c->dcnt0, (void*)c->ulist0, (void*)c->ukid0,
-                    (void*)c->ucnt0})
+                    (void*)c->ucnt0, (void*)c->crep, (void*)c->cnpat, (void*)c->cflag})
         F(p);
     F(c->X0);
     F(c->X1);
@@ -1007,6 +1078,10 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
             L.tab_down = dalloc<float>((size_t)kRowW * L.g.n);
             if (l < depth - 1) L.tab_up = dalloc<float>((size_t)kRowW * L.g.n);
             L.mlist = dalloc<uint32_t>((size_t)L.g.n);
+            if (l > 0) {
+                L.rcode = dalloc<uint32_t>((size_t)L.g.n);
+                L.pid = dalloc<uint32_t>((size_t)L.g.n);
+            }
             L.mcnt = dalloc<uint32_t>(1);
             L.kc_down = dalloc<float>(3 * (size_t)c->S);
             L.kc_up = dalloc<float>(3 * (size_t)c->S);
@@ -1037,6 +1112,9 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
         c->ulist0 = dalloc<uint32_t>((size_t)c->g0.n);
         c->ukid0 = dalloc<uint32_t>((size_t)c->g0.n);
         c->dcnt0 = dalloc<uint32_t>(1);
+        c->crep = dalloc<uint32_t>((size_t)std::max<long long>(c->depth > 1 ? c->L[1].g.n : 1, 1));
+        c->cnpat = dalloc<uint32_t>(1);
+        c->cflag = dalloc<uint32_t>(1);
         c->ucnt0 = dalloc<uint32_t>(1);
         c->npat0 = dalloc<uint32_t>(1);
         const size_t n = (size_t)c->g0.n;

@@ -290,6 +290,72 @@ __global__ void __launch_bounds__(kBlock) k_window_keys(Geom g, const uint8_t* _
     }
 }
 
+// Coarse levels: the pooled window of a mixed cell (3 channels x 3^D cells,
+// the solid ring outside) keyed by a 64-bit hash for the pattern dictionary.
+// A hash is not exact, so k_verify_windows compares every cell's window with
+// its pattern's representative bit for bit; set_mask drops the dictionary
+// (per-cell rows) on any mismatch.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t window_bits(const Geom& g, const float* __restrict__ img, int x, int y, int z,
+                                                int t, int ch) {
+    const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = (D == 3) ? t / 9 - 1 : 0;
+    const int xx = x + dx, yy = y + dy, zz = z + dz;
+    const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
+    const float v = in ? img[(long long)ch * g.n + lin(g, xx, yy, zz)] : (ch == 2 ? 1.0f : 0.0f);
+    return __float_as_uint(v);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_window_hash(Geom g, const float* __restrict__ img,
+                                                        const uint32_t* __restrict__ list,
+                                                        const uint32_t* __restrict__ count,
+                                                        unsigned long long* __restrict__ keys,
+                                                        uint32_t* __restrict__ vals) {
+    const long long n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const long long c = list[i];
+        const int x = (int)(c % g.nx), y = (int)((c / g.nx) % g.ny), z = (int)(c / ((long long)g.nx * g.ny));
+        unsigned long long h = 0x6a09e667f3bcc909ull;
+        for (int t = 0; t < Sh<D>::S; ++t)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+                h = mix64(h ^ ((unsigned long long)window_bits<D>(g, img, x, y, z, t, ch) +
+                               ((unsigned long long)(3 * t + ch) << 40)));
+        keys[i] = h;
+        vals[i] = (uint32_t)i;
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_verify_windows(Geom g, const float* __restrict__ img,
+                                                           const uint32_t* __restrict__ list,
+                                                           const uint32_t* __restrict__ count,
+                                                           const uint32_t* __restrict__ pid,
+                                                           const uint32_t* __restrict__ repcell,
+                                                           uint32_t* __restrict__ mismatch) {
+    const long long n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const long long c = list[i], r = repcell[pid[i]];
+        if (c == r) continue;
+        const int x = (int)(c % g.nx), y = (int)((c / g.nx) % g.ny), z = (int)(c / ((long long)g.nx * g.ny));
+        const int rx = (int)(r % g.nx), ry = (int)((r / g.nx) % g.ny), rz = (int)(r / ((long long)g.nx * g.ny));
+        bool same = true;
+        for (int t = 0; t < Sh<D>::S; ++t)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+                same &= window_bits<D>(g, img, x, y, z, t, ch) == window_bits<D>(g, img, rx, ry, rz, t, ch);
+        if (!same) atomicOr(mismatch, 1u);
+    }
+}
+
 __global__ void __launch_bounds__(kBlock) k_run_heads(const unsigned long long* __restrict__ skeys,
                                                       const uint32_t* __restrict__ count, uint32_t* __restrict__ head) {
     const long long n = *count;
