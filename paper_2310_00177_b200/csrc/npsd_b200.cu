@@ -26,6 +26,7 @@
 #include "mixed.cuh"
 #include "down0.cuh"
 #include "coarse.cuh"
+#include "up0.cuh"
 
 using namespace nb2;
 
@@ -564,6 +565,20 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
 
 template <int D, int NO>
 void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
+    if (D == 3) {
+        // 3D: the pipelined level-0 up sweep on the balanced schedule (up0.cuh)
+        const LevelBufs& L = c->L[0];
+        const LevelBufs& L1 = c->L[1];
+        const float* outc = (c->depth == 2) ? L1.y : L1.out;
+        auto k = k_up_l0<NO>;
+        const size_t sm = sizeof(Up0Smem<NO>);
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        KC0 kc0;
+        for (int i = 0; i < 27; ++i) kc0.k[i] = c->kc_up[0].k[0][i];  // the uniform-fluid kernel
+        LAUNCH3S(c, s, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y,
+                 c->zab, kc0, c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_stencil.view());
+        return;
+    }
     launch_up<D, kUpL0, NO>(c, s, 0, nullptr, c->Dtmp);
 }
 

@@ -1,0 +1,175 @@
+// Level-0 up sweep of the solve (P3), 3D: at every fluid cell with a
+// uniform-fluid window
+//     o = z_a y_0 + z_b conv_up_0(upsample2(out_1))     (net/forward.hpp:118-127)
+//     d = f64(o) * nrm                                  (net_precond.cpp:31-34)
+// fused with the A-orthogonalisation dots d.Ad_j (solver.cpp:239-243). Mixed
+// fluid cells follow in k_mixed_up0, which adds these dot totals
+// (st->dot_main) to its own and finalises the projections.
+//
+// The stencil pipeline of stencil.cuh / down0.cuh on the balanced schedule: a
+// 32 x 8 block owns a 64 x 8 tile (thread = x pair) and marches z. Each thread
+// cp.async-copies its pair's y_0 and Ad_j PF planes ahead (src-size 0 — no
+// traffic — for pairs without such a cell); out_1 is staged as 34 x 6 coarse
+// planes (tile + halo, zero outside) in a 4-plane ring, one new coarse plane
+// every second fine plane. One barrier per plane; a fine tap (x+dx, y+dy,
+// z+dz) reads coarse ((x+dx)>>1, (y+dy)>>1, (z+dz)>>1). Slot-order
+// round-to-nearest arithmetic: bit-identical to the restatement.
+#pragma once
+
+#include "common.cuh"
+#include "down0.cuh"
+#include "stencil.cuh"
+
+namespace nb2 {
+
+constexpr int kUPF = 2, kUST = kUPF + 1;      // fine planes prefetched ahead, own-input stages
+constexpr int kOW = kTX / 2 + 2, kOH = kTY / 2 + 2;  // coarse plane tile (34 x 6)
+
+template <int NO>
+struct Up0Smem {
+    static constexpr int NA = (NO > 0) ? NO : 1;
+    double ad[kUST][NA][kTY][kTX];  // Ad_j, own pairs
+    float y[kUST][kTY][kTX];        // y_0, own pairs
+    float oc[4][kOH][kOW];          // out_1 coarse planes (ring by coarse z & 3)
+};
+
+// the pair has a cell this kernel computes (fluid, uniform-fluid window)
+__device__ __forceinline__ bool up_cell(unsigned b) { return (b & 0xfu) == 0u; }  // window 0, type 0
+__device__ __forceinline__ bool up_pair(unsigned b2) { return up_cell(b2 & 0xffu) || up_cell(b2 >> 8); }
+
+template <int NO>
+__device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, const uint8_t* __restrict__ cls,
+                                              const float* __restrict__ outc, const float* __restrict__ y0,
+                                              const KC0& kc, float za, float zb, double nrm, int nc,
+                                              const double* const (&adp)[(NO > 0) ? NO : 1],
+                                              double* __restrict__ dout, double (&acc)[(NO > 0) ? NO : 1], int tx,
+                                              int ty, int zc0, int zc1) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Up0Smem<NO>& S = *reinterpret_cast<Up0Smem<NO>*>(smem_raw);
+    __syncthreads();  // the previous segment's last reads of S are done
+    const int lane = threadIdx.x, row = threadIdx.y, tid = row * kSX + lane;
+    const int X0 = tx * kTX, Y0 = ty * kTY;
+    const int x = X0 + 2 * lane, yy = Y0 + row;
+    const bool own = x < g.nx && yy < g.ny;
+    const long long nx = g.nx, plane = nx * g.ny;
+    const long long qo = (long long)(own ? yy : 0) * nx + (own ? x : 0);
+    // coarse staging role: element tid of the 34 x 6 coarse tile
+    const int CX0 = (X0 >> 1) - 1, CY0 = (Y0 >> 1) - 1;
+    const bool crole = tid < kOW * kOH;
+    const int cr = crole ? tid / kOW : 0, ccol = crole ? tid - cr * kOW : 0;
+    const int cgx = CX0 + ccol, cgy = CY0 + cr;
+    const bool cxy_in = crole && cgx >= 0 && cgx < gc.nx && cgy >= 0 && cgy < gc.ny;
+    const long long cqo = cxy_in ? (long long)cgy * gc.nx + cgx : 0;
+    const long long cplane = (long long)gc.nx * gc.ny;
+    auto zin = [&](int z) { return z >= 0 && z < g.nz; };
+    auto own_bytes = [&](int z) -> unsigned {
+        return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
+    };
+    auto coarse = [&](int k) {  // stage coarse plane k (zero outside)
+        if (crole) {
+            const bool ok = cxy_in && k >= 0 && k < gc.nz;
+            cp_async4(&S.oc[k & 3][cr][ccol], outc + (ok ? k * cplane + cqo : 0), ok);
+        }
+    };
+    auto slot = [&](int z) { return (z - zc0 + kUST * 1024) % kUST; };
+    auto issue = [&](int z, unsigned ob) {
+        if (zin(z)) {
+            const int s = slot(z);
+            const bool ol = own && up_pair(ob);
+            const long long q = z * plane + qo;
+            cp_async8(&S.y[s][row][2 * lane], y0 + (ol ? q : 0), ol);
+#pragma unroll
+            for (int j = 0; j < NO; ++j) {
+                const bool lj = ol && j < nc;
+                cp_async16(&S.ad[s][j][row][2 * lane], adp[j] + (lj ? q : 0), lj);
+            }
+            if (z == zc0) {
+                for (int k = (z - 1) >> 1; k <= (z + 1) >> 1; ++k) coarse(k);
+            } else if (z & 1) {
+                coarse((z + 1) >> 1);
+            }
+        }
+        cp_commit();
+    };
+    // fine row offsets into the coarse tile (per thread): (yy + dy) >> 1 - CY0
+    int crow[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) crow[d] = ((yy + d - 1) >> 1) - CY0;
+
+    unsigned ob[kUPF + 2];
+#pragma unroll
+    for (int k = 0; k < kUPF + 2; ++k) ob[k] = own_bytes(zc0 + k);
+#pragma unroll
+    for (int k = 0; k < kUPF; ++k) issue(zc0 + k, ob[k]);
+#pragma unroll(kUPF + 2)
+    for (int z = zc0; z < zc1; ++z) {
+        issue(z + kUPF, ob[kUPF]);
+        cp_wait<kUPF>();  // plane z's group landed (own thread)
+        __syncthreads();  // and every thread's coarse copies
+        const unsigned bc = ob[0];
+        if (own && up_pair(bc)) {
+            const int s = slot(z);
+            const float2 yv = *reinterpret_cast<const float2*>(&S.y[s][row][2 * lane]);
+            float u[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float a = 0.0f;
+#pragma unroll
+                for (int t = 0; t < 27; ++t) {
+                    const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = t / 9 - 1;
+                    const int kz = ((z + dz) >> 1) & 3;
+                    const int col = lane + ((h + dx) >> 1) + 1;  // ((x + h + dx) >> 1) - CX0
+                    a = __fadd_rn(a, __fmul_rn(kc.k[t], S.oc[kz][crow[dy + 1]][col]));
+                }
+                u[h] = a;
+            }
+            const long long q = z * plane + qo;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (!up_cell((bc >> (8 * h)) & 0xffu)) continue;
+                const float o = __fadd_rn(__fmul_rn(za, h ? yv.y : yv.x), __fmul_rn(zb, u[h]));
+                const double dv = __dmul_rn((double)o, nrm);
+                dout[q + h] = dv;
+#pragma unroll
+                for (int j = 0; j < NO; ++j)
+                    if (j < nc) acc[j] += dv * S.ad[s][j][row][2 * lane + h];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kUPF + 1; ++k) ob[k] = ob[k + 1];
+        ob[kUPF + 1] = own_bytes(z + kUPF + 2);
+    }
+    cp_wait<0>();
+}
+
+template <int NO>
+__global__ void __launch_bounds__(kSX* kSY) k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ cls,
+                                                    const float* __restrict__ outc, const float* __restrict__ y0,
+                                                    const float* __restrict__ zab, const __grid_constant__ KC0 kc,
+                                                    double* __restrict__ dout, SolverState* st,
+                                                    const double* __restrict__ ADring, double* __restrict__ partials,
+                                                    unsigned int* __restrict__ counter, Sched sc) {
+    constexpr int NA = (NO > 0) ? NO : 1;
+    const float za = zab[0], zb = zab[1];
+    const double nrm = st->nrm;
+    const int nc = st->n_cache, R = st->ring;
+    const double* adp[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+        const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
+        adp[j] = ADring + (long long)slot * g.n;
+    }
+    double acc[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+    sched_for_each(sc, [&](int tx, int ty, int u0, int u1) {
+        up_l0_segment<NO>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, u0, u1);
+    });
+    double tot[NA];
+    // the mixed fluid cells follow in k_mixed_up0, which finalises the MGS
+    // projections from these totals plus its own
+    if (grid_reduce<NA>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0)
+        for (int j = 0; j < NA; ++j) st->dot_main[j] = tot[j];
+}
+
+}  // namespace nb2
