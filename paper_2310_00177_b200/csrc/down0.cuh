@@ -26,13 +26,19 @@ struct KC0 {
     float k[27];
 };
 
+// Two planes per step: planes z, z+1 (z even) are convolved after ONE barrier
+// (four independent accumulation chains per thread), and their 2x2x2 pools
+// are summed after the next step's barrier.
+constexpr int kD0R = 4;  // raw (f64) plane stages: planes z+1 .. z+4
+constexpr int kD0X = 8;  // x_0 (f32) plane ring: z-3 .. z+2 in use around a barrier
+
 struct Down0Smem {
-    double raw[kST][kVH][kVW];  // residual copies (tile + halo)
-    float xin[4][kVH][kVW];     // converted network input x_0
-    float yp[2][kTY][kTX];      // y_0 of the last two planes (pooling)
+    double raw[kD0R][kVH][kVW];  // residual copies (tile + halo)
+    float xin[kD0X][kVH][kVW];   // converted network input x_0
+    float yp[2][2][kTY][kTX];    // y_0 of a step's two planes, double-buffered (pooling)
 };
 
-// One column segment: tile (tx, ty), planes [zc0, zc1) (zc0 even)
+// One column segment: tile (tx, ty), planes [zc0, zc1) (both even)
 __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __restrict__ cls,
                                                 const double* __restrict__ r, const SolverState* __restrict__ st,
                                                 const KC0& kc, float* __restrict__ y, float* __restrict__ xnext,
@@ -75,12 +81,13 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
     auto own_bytes = [&](int z) -> unsigned {
         return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
     };
-    auto slot = [&](int z) { return (z - zc0 + 1 + kST * 1024) % kST; };
+    auto rslot = [&](int z) { return (z - zc0 + 1 + kD0R * 1024) % kD0R; };
+    auto xslot = [&](int z) { return (z + kD0X * 1024) % kD0X; };
     // own pairs without fluid zero-filled; halo always copied (exact zeros)
     auto issue = [&](int z, unsigned ob) {
         if (zin(z)) {
             const bool hl = h_in;
-            const int s = slot(z);
+            const int s = rslot(z);
             const bool ol = own && pair_live(ob);
             const long long qz = z * plane;
             cp_async16(&S.raw[s][row + 1][2 + 2 * lane], r + (ol ? qz + qo : 0), ol);
@@ -93,89 +100,113 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
     };
     auto cvt = [&](double v) { return __double2float_rn(__dmul_rn(__dmul_rn(v, inv1), inv2)); };
     auto form = [&](int z) {
-        const int s = slot(z), vs = (z + 1024) & 3;
+        const int s = rslot(z), vs = xslot(z);
         const bool zi = zin(z);
         S.xin[vs][row + 1][2 + 2 * lane] = zi ? cvt(S.raw[s][row + 1][2 + 2 * lane]) : 0.0f;
         S.xin[vs][row + 1][3 + 2 * lane] = zi ? cvt(S.raw[s][row + 1][3 + 2 * lane]) : 0.0f;
         if (hkind != 0) S.xin[vs][hsr][hsc] = zi ? cvt(S.raw[s][hsr][hsc]) : 0.0f;
         if (hkind == 1) S.xin[vs][hsr][hsc + 1] = zi ? cvt(S.raw[s][hsr][hsc + 1]) : 0.0f;
     };
-    // prologue (as stencil_march): planes zc0-1 .. zc0+PF-1 issued, zc0-1 and zc0 formed
-    unsigned ob[kPF + 2];
-    issue(zc0 - 1, own_bytes(zc0 - 1));
-#pragma unroll
-    for (int k = 0; k < kPF + 2; ++k) ob[k] = own_bytes(zc0 + k);
-#pragma unroll
-    for (int k = 0; k < kPF; ++k) issue(zc0 + k, ob[k]);
-    cp_wait<kPF - 1>();
-    form(zc0 - 1);
-    form(zc0);
-    // mixed cells' y_0 (k_mixed_down0), loaded one plane ahead
+    // mixed cells' y_0 (k_mixed_down0), loaded a step ahead
     auto mixed_y = [&](int z, unsigned b2, float& ya, float& yb) {
         const long long q = z * plane + qo;
         const uint8_t ba = (uint8_t)(b2 & 0xffu), bb = (uint8_t)(b2 >> 8);
-        ya = (own && cls_window(ba) == 3 && cls_wfluid(ba)) ? __ldg(y + q) : 0.0f;
-        yb = (own && cls_window(bb) == 3 && cls_wfluid(bb)) ? __ldg(y + q + 1) : 0.0f;
+        ya = (own && zin(z) && cls_window(ba) == 3 && cls_wfluid(ba)) ? __ldg(y + q) : 0.0f;
+        yb = (own && zin(z) && cls_window(bb) == 3 && cls_wfluid(bb)) ? __ldg(y + q + 1) : 0.0f;
     };
-    float mya, myb;
-    mixed_y(zc0, ob[0], mya, myb);
-#pragma unroll(kPF + 2)
-    for (int z = zc0; z < zc1; ++z) {
-        issue(z + kPF, ob[kPF]);
-        cp_wait<kPF - 1>();
-        form(z + 1);
-        float nya = 0.0f, nyb = 0.0f;
-        if (z + 1 < zc1) mixed_y(z + 1, ob[1], nya, nyb);
-        __syncthreads();  // x_0 of planes z-1, z, z+1 complete (halos included)
-        const unsigned bc = ob[0];
-        const int vm = (z + 1023) & 3, vc = (z + 1024) & 3, vp = (z + 1025) & 3;
-        const int c0 = 2 + 2 * lane, r0 = row + 1;
-        float ya = 0.0f, yb = 0.0f;
-        const uint8_t ba = (uint8_t)(bc & 0xffu), bb = (uint8_t)(bc >> 8);
-        if (own) {
-            // uniform-fluid windows convolve with the constant kernel, slot order
-            auto conv = [&](int cc) {
-                float acc = 0.0f;
-#pragma unroll
-                for (int s = 0; s < 27; ++s) {
-                    const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
-                    const int ps = dz < 0 ? vm : (dz > 0 ? vp : vc);
-                    acc = __fadd_rn(acc, __fmul_rn(kc.k[s], S.xin[ps][r0 + dy][cc + dx]));
-                }
-                return acc;
-            };
-            const int wa = cls_window(ba), wb = cls_window(bb);
-            ya = (wa == 0) ? conv(c0) : (wa == 3 ? mya : 0.0f);
-            yb = (wb == 0) ? conv(c0 + 1) : (wb == 3 ? myb : 0.0f);
-            // y_0 is stored at fluid cells; mixed ones already hold it
-            const long long q = z * plane + qo;
-            if (cls_type(ba) == 0 && wa != 3) y[q] = ya;
-            if (cls_type(bb) == 0 && wb != 3) y[q + 1] = yb;
+    // 2x2x2 pool of the step at z (its y_0 tile in yp[b]), restatement order:
+    // x fastest, then y, then z (avg_pool2, net/kernels.hpp:279-292)
+    auto pool = [&](int z, int b) {
+        if (own && !(row & 1)) {
+            float ps = S.yp[b][0][row][2 * lane];
+            ps = __fadd_rn(ps, S.yp[b][0][row][2 * lane + 1]);
+            ps = __fadd_rn(ps, S.yp[b][0][row + 1][2 * lane]);
+            ps = __fadd_rn(ps, S.yp[b][0][row + 1][2 * lane + 1]);
+            ps = __fadd_rn(ps, S.yp[b][1][row][2 * lane]);
+            ps = __fadd_rn(ps, S.yp[b][1][row][2 * lane + 1]);
+            ps = __fadd_rn(ps, S.yp[b][1][row + 1][2 * lane]);
+            ps = __fadd_rn(ps, S.yp[b][1][row + 1][2 * lane + 1]);
+            xnext[lin(gc, x >> 1, yy >> 1, z >> 1)] = __fmul_rn(0.125f, ps);
         }
-        // pooling (restatement order: x fastest, then y, then z)
-        S.yp[z & 1][row][2 * lane] = ya;
-        S.yp[z & 1][row][2 * lane + 1] = yb;
-        if (z & 1) {
-            __syncthreads();
-            if (own && !(row & 1)) {
-                float ps = S.yp[0][row][2 * lane];
-                ps = __fadd_rn(ps, S.yp[0][row][2 * lane + 1]);
-                ps = __fadd_rn(ps, S.yp[0][row + 1][2 * lane]);
-                ps = __fadd_rn(ps, S.yp[0][row + 1][2 * lane + 1]);
-                ps = __fadd_rn(ps, S.yp[1][row][2 * lane]);
-                ps = __fadd_rn(ps, S.yp[1][row][2 * lane + 1]);
-                ps = __fadd_rn(ps, S.yp[1][row + 1][2 * lane]);
-                ps = __fadd_rn(ps, S.yp[1][row + 1][2 * lane + 1]);
-                xnext[lin(gc, x >> 1, yy >> 1, z >> 1)] = __fmul_rn(0.125f, ps);
+    };
+
+    // prologue: planes zc0-1 .. zc0+2 issued, zc0-1 and zc0 formed
+    unsigned ob[8];  // own bytes of planes z .. z+7 (shifted by two per step)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ob[k] = own_bytes(zc0 + k);
+    issue(zc0 - 1, own_bytes(zc0 - 1));
+    issue(zc0, ob[0]);
+    issue(zc0 + 1, ob[1]);
+    issue(zc0 + 2, ob[2]);
+    cp_wait<2>();
+    form(zc0 - 1);
+    form(zc0);
+    float my[2][2];
+    mixed_y(zc0, ob[0], my[0][0], my[0][1]);
+    mixed_y(zc0 + 1, ob[1], my[1][0], my[1][1]);
+    int pb = 0;  // yp buffer of this step
+#pragma unroll 4
+    for (int z = zc0; z < zc1; z += 2) {
+        issue(z + 3, ob[3]);
+        issue(z + 4, ob[4]);
+        cp_wait<2>();  // planes z+1, z+2 landed (own copies)
+        form(z + 1);
+        form(z + 2);
+        float ny[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
+        if (z + 2 < zc1) {
+            mixed_y(z + 2, ob[2], ny[0][0], ny[0][1]);
+            mixed_y(z + 3, ob[3], ny[1][0], ny[1][1]);
+        }
+        __syncthreads();  // x_0 of planes z-1 .. z+2 complete; yp of the last step too
+        if (z > zc0) pool(z - 2, pb ^ 1);
+        const int c0 = 2 + 2 * lane, r0 = row + 1;
+        float yv[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
+        if (own) {
+            // uniform-fluid windows convolve with the constant kernel, slot order;
+            // the four cells' chains are independent
+            float acc[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
+#pragma unroll
+            for (int s = 0; s < 27; ++s) {
+                const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const int ps = xslot(z + p + dz);
+                    acc[p][0] = __fadd_rn(acc[p][0], __fmul_rn(kc.k[s], S.xin[ps][r0 + dy][c0 + dx]));
+                    acc[p][1] = __fadd_rn(acc[p][1], __fmul_rn(kc.k[s], S.xin[ps][r0 + dy][c0 + 1 + dx]));
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const unsigned bc = ob[p];
+                const uint8_t ba = (uint8_t)(bc & 0xffu), bb = (uint8_t)(bc >> 8);
+                const int wa = cls_window(ba), wb = cls_window(bb);
+                yv[p][0] = (wa == 0) ? acc[p][0] : (wa == 3 ? my[p][0] : 0.0f);
+                yv[p][1] = (wb == 0) ? acc[p][1] : (wb == 3 ? my[p][1] : 0.0f);
+                // y_0 is stored at fluid cells; mixed ones already hold it
+                const long long q = (z + p) * plane + qo;
+                if (cls_type(ba) == 0 && wa != 3) y[q] = yv[p][0];
+                if (cls_type(bb) == 0 && wb != 3) y[q + 1] = yv[p][1];
             }
         }
-        mya = nya;
-        myb = nyb;
 #pragma unroll
-        for (int k = 0; k < kPF + 1; ++k) ob[k] = ob[k + 1];
-        ob[kPF + 1] = own_bytes(z + kPF + 2);
+        for (int p = 0; p < 2; ++p) {
+            S.yp[pb][p][row][2 * lane] = yv[p][0];
+            S.yp[pb][p][row][2 * lane + 1] = yv[p][1];
+        }
+        pb ^= 1;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            my[p][0] = ny[p][0];
+            my[p][1] = ny[p][1];
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) ob[k] = ob[k + 2];
+        ob[6] = own_bytes(z + 8);
+        ob[7] = own_bytes(z + 9);
     }
     cp_wait<0>();
+    __syncthreads();
+    pool(zc1 - 2, pb ^ 1);
 }
 
 // Balanced schedule (Sched, units of two planes: pooling pairs stay inside a
