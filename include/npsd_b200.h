@@ -52,7 +52,8 @@ enum {
     NPSD_INVALID_ARGUMENT = 1,
     NPSD_BREAKDOWN = 2,
     NPSD_EMPTY_SYSTEM = 3,
-    NPSD_CUDA_ERROR = 4
+    NPSD_CUDA_ERROR = 4,
+    NPSD_IO_ERROR = 5
 };
 
 typedef struct npsd_b200_ctx npsd_b200_ctx;
@@ -131,6 +132,19 @@ size_t npsd_b200_param_count(int dim, int depth);
 int npsd_b200_init_params(int dim, int depth, uint64_t seed, float* out);
 int npsd_b200_identity_params(int dim, int depth, float* out);
 void npsd_b200_rhs_normal(uint64_t seed, int64_t n, double* out);
+
+/* Model files, replacing npsd::net::save_npm / load_npm (net_params.cpp:42-78):
+ * "NPMW", u32 version 1, u32 dim, u32 depth, then the weights in
+ * for_each_span order as little-endian f32. dim 2 files are byte-identical to
+ * the reference's; dim 3 is the 3D variant of the same layout (the reference
+ * writes and accepts dim 2 only, net_params.cpp:45,64). Errors return
+ * NPSD_IO_ERROR (the reference's std::runtime_error) with the reference's
+ * message in npsd_b200_npm_last_error(); NPSD_INVALID_ARGUMENT for bad
+ * arguments. load: out == NULL queries dim/depth/count only; otherwise cap
+ * must hold the whole parameter vector. */
+int npsd_b200_save_npm(const char* path, int dim, int depth, const float* params, size_t n);
+int npsd_b200_load_npm(const char* path, int* dim, int* depth, float* out, size_t cap, size_t* n_out);
+const char* npsd_b200_npm_last_error(void);
 
 /* Device buffers and pinned host memory for callers without a CUDA runtime of
  * their own (the Python mirror uses these; the C++ shim may too). */

@@ -137,6 +137,23 @@ int ref_init_params_2d(int depth, unsigned long long seed, float* out) {
     });
 }
 
+// the reference's own model-file writer / reader (net_params.cpp:42-78)
+int ref_save_npm_2d(int depth, unsigned long long seed, const char* path) {
+    return guarded([&] { npsd::net::save_npm(npsd::net::init_params(depth, seed), path); });
+}
+
+int ref_load_npm_2d(const char* path, float* out, long cap, int* depth) {
+    return guarded([&] {
+        const auto p = npsd::net::load_npm(path);
+        *depth = p.depth;
+        long o = 0;
+        p.for_each_span([&](const float* src, std::size_t k) {
+            if (o + (long)k <= cap) std::memcpy(out + o, src, k * sizeof(float));
+            o += (long)k;
+        });
+    });
+}
+
 // PaddedImage::pooled chain interiors (3 planes per level)
 int ref_level_images_2d(long nx, long ny, int depth, const unsigned char* types, float* out) {
     return guarded([&] {

@@ -22,12 +22,12 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from ._native import NPSD_BREAKDOWN, NPSD_CUDA_ERROR, NPSD_EMPTY_SYSTEM, NPSD_INVALID_ARGUMENT, NPSD_OK
+from ._native import NPSD_BREAKDOWN, NPSD_CUDA_ERROR, NPSD_EMPTY_SYSTEM, NPSD_INVALID_ARGUMENT, NPSD_IO_ERROR, NPSD_OK
 
 __all__ = [
     "SolveConfig", "SolveReport", "SolveResult", "SolverBreakdown", "EmptySystemError", "DeviceError",
     "NetParams", "init_params", "identity_params", "param_count", "rhs_normal", "Context", "NeuralPrecond",
-    "neural_precond", "psdo_solve", "psd_solve", "DeviceBuffer", "PinnedBuffer",
+    "neural_precond", "psdo_solve", "psd_solve", "DeviceBuffer", "PinnedBuffer", "save_npm", "load_npm",
 ]
 
 
@@ -116,6 +116,34 @@ def init_params(depth: int, seed: int, dim: int = 3) -> NetParams:
     out = np.empty(param_count(dim, depth), np.float32)
     _raise(_native.lib().npsd_b200_init_params(dim, depth, seed, out), "init_params: bad dim/depth")
     return NetParams(dim, depth, out)
+
+
+def save_npm(params: NetParams, path) -> None:
+    """save_npm (net_params.cpp:42-52): "NPMW", u32 version 1, dim, depth, f32
+    weights in for_each_span order. dim 2 files are the reference's bytes;
+    dim 3 is the 3D variant of the layout."""
+    flat = np.ascontiguousarray(params.flat, np.float32)
+    st = _native.lib().npsd_b200_save_npm(str(path).encode(), params.dim, params.depth, flat, flat.size)
+    if st == NPSD_IO_ERROR:
+        raise RuntimeError(_native.lib().npsd_b200_npm_last_error().decode())
+    _raise(st, _native.lib().npsd_b200_npm_last_error().decode())
+
+
+def load_npm(path) -> NetParams:
+    """load_npm (net_params.cpp:54-78): rejects a bad magic, version, dim or
+    depth and truncated data with the reference's runtime_error messages."""
+    L = _native.lib()
+    dim, depth, n = C.c_int(0), C.c_int(0), C.c_size_t(0)
+    p = str(path).encode()
+    st = L.npsd_b200_load_npm(p, C.byref(dim), C.byref(depth), None, 0, C.byref(n))
+    if st == NPSD_OK:
+        out = np.empty(n.value, np.float32)
+        st = L.npsd_b200_load_npm(p, C.byref(dim), C.byref(depth), out.ctypes.data, out.size,
+                                  C.byref(n))
+    if st == NPSD_IO_ERROR:
+        raise RuntimeError(L.npsd_b200_npm_last_error().decode())
+    _raise(st, L.npsd_b200_npm_last_error().decode())
+    return NetParams(dim.value, depth.value, out)
 
 
 def identity_params(depth: int, dim: int = 3) -> NetParams:

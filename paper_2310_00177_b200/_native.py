@@ -9,7 +9,7 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libnpsd_b200.so"
 
-NPSD_OK, NPSD_INVALID_ARGUMENT, NPSD_BREAKDOWN, NPSD_EMPTY_SYSTEM, NPSD_CUDA_ERROR = range(5)
+NPSD_OK, NPSD_INVALID_ARGUMENT, NPSD_BREAKDOWN, NPSD_EMPTY_SYSTEM, NPSD_CUDA_ERROR, NPSD_IO_ERROR = range(6)
 
 EXPORTED_SYMBOLS = (
     "npsd_b200_create", "npsd_b200_destroy", "npsd_b200_last_error", "npsd_b200_set_params",
@@ -20,7 +20,7 @@ EXPORTED_SYMBOLS = (
     "npsd_b200_device_alloc", "npsd_b200_device_free", "npsd_b200_host_alloc", "npsd_b200_host_free",
     "npsd_b200_memcpy", "npsd_b200_synchronize", "npsd_b200_last_solve_ms", "npsd_b200_last_solve_launches",
     "npsd_b200_launch_count", "npsd_b200_event_record", "npsd_b200_event_elapsed_ms",
-    "npsd_b200_profile_iterations",
+    "npsd_b200_profile_iterations", "npsd_b200_save_npm", "npsd_b200_load_npm", "npsd_b200_npm_last_error",
 )
 
 
@@ -57,6 +57,11 @@ def lib() -> C.CDLL:
                                    C.c_int, C.POINTER(_vp)]
     L.npsd_b200_destroy.argtypes = [_vp]
     L.npsd_b200_last_error.restype = C.c_char_p
+    L.npsd_b200_npm_last_error.restype = C.c_char_p
+    L.npsd_b200_npm_last_error.argtypes = []
+    L.npsd_b200_save_npm.argtypes = [C.c_char_p, C.c_int, C.c_int, _f32p, C.c_size_t]
+    L.npsd_b200_load_npm.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p, C.c_size_t,
+                                     C.POINTER(C.c_size_t)]
     L.npsd_b200_last_error.argtypes = [_vp]
     L.npsd_b200_set_params.argtypes = [_vp, _f32p, C.c_size_t]
     L.npsd_b200_set_mask.argtypes = [_vp, _u8p]

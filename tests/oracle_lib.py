@@ -210,6 +210,8 @@ class Ref:
         L.ref_last_error.restype = C.c_char_p
         L.ref_rhs_normal.argtypes = [C.c_ulonglong, C.c_long, _f64p]
         L.ref_init_params_2d.argtypes = [C.c_int, C.c_ulonglong, _f32p]
+        L.ref_save_npm_2d.argtypes = [C.c_int, C.c_ulonglong, C.c_char_p]
+        L.ref_load_npm_2d.argtypes = [C.c_char_p, _f32p, C.c_long, C.POINTER(C.c_int)]
         L.ref_level_images_2d.argtypes = [C.c_long, C.c_long, C.c_int, _u8p, _f32p]
         L.ref_net_apply_2d.argtypes = [C.c_long, C.c_long, C.c_int, _f32p, C.c_long, _u8p, _f32p, _f32p,
                                        _f32p, _f32p]
@@ -234,6 +236,15 @@ class Ref:
         out = np.empty(n, np.float32)
         self._check(self.lib.ref_init_params_2d(depth, seed, out))
         return out
+
+    def save_npm_2d(self, depth: int, seed: int, path) -> None:
+        self._check(self.lib.ref_save_npm_2d(depth, seed, str(path).encode()))
+
+    def load_npm_2d(self, path, n: int) -> tuple[int, np.ndarray]:
+        out = np.zeros(n, np.float32)
+        depth = C.c_int(0)
+        self._check(self.lib.ref_load_npm_2d(str(path).encode(), out, n, C.byref(depth)))
+        return depth.value, out
 
     def level_images_2d(self, types: np.ndarray, depth: int) -> list[np.ndarray]:
         ny, nx = types.shape
