@@ -186,6 +186,25 @@ int oracle_ctx_precond_apply(void* h, const double* r, double* z) {
 }
 
 // reduced A·x (assemble_poisson[_3d] + reduce + spmv)
+// y = A x on the reduced system of a cell-type grid, without a network
+// context (matrix-free PoissonOp; large-grid residual checks)
+int oracle_spmv(int D, long nx, long ny, long nz, const unsigned char* types, const double* x, double* y) {
+    return guarded([&] {
+        const Dims d = make_dims(D, nx, ny, nz);
+        const auto map = ReductionMap::from_types(types, d);
+        const std::size_t nf = static_cast<std::size_t>(map.reduced_size());
+        Vector xv(x, x + nf), yv;
+        if (D == 2) {
+            PoissonOp<2> A{d, types, &map};
+            A.spmv(xv, yv);
+        } else {
+            PoissonOp<3> A{d, types, &map};
+            A.spmv(xv, yv);
+        }
+        std::memcpy(y, yv.data(), nf * sizeof(double));
+    });
+}
+
 int oracle_ctx_spmv(void* h, const double* x, double* y) {
     return guarded([&] {
         auto* c = static_cast<OracleCtx*>(h);

@@ -72,6 +72,7 @@ class Oracle:
         L.oracle_ctx_net_apply.argtypes = [C.c_void_p, _f32p, _f32p]
         L.oracle_ctx_precond_apply.argtypes = [C.c_void_p, _f64p, _f64p]
         L.oracle_ctx_spmv.argtypes = [C.c_void_p, _f64p, _f64p]
+        L.oracle_spmv.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, _f64p, _f64p]
         L.oracle_ctx_psdo_solve.argtypes = [C.c_void_p, C.c_int, _f64p, C.c_void_p, C.c_double, C.c_double,
                                             C.c_long, C.c_int, C.c_int, C.c_int, _f64p, _f64p,
                                             C.POINTER(C.c_long), C.POINTER(C.c_int), C.POINTER(C.c_long),
@@ -112,6 +113,14 @@ class Oracle:
             res.append(out[o:o + 3 * s].reshape(shp))
             o += 3 * s
         return res
+
+    def spmv(self, types: np.ndarray, x: np.ndarray) -> np.ndarray:
+        """A x (reduced system of `types`), matrix-free, no network context."""
+        dim, (nx, ny, nz) = _dims_of(types)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty_like(x)
+        self._check(self.lib.oracle_spmv(dim, nx, ny, nz, _u8(types), x, y))
+        return y
 
     def context(self, types: np.ndarray, params: np.ndarray, depth: int) -> "OracleCtx":
         return OracleCtx(self, types, params, depth)

@@ -302,3 +302,38 @@ def test_raw_network_then_solve_unchanged(b200, oracle):
     ctx.set_mask(list(scenes.droplet_frames(64, 2))[1])
     ctx.set_mask(t)
     assert np.array_equal(ctx.psdo_solve(b, cfg).report.residual_history, first)
+
+
+def test_c5_512_identity_solve_explicit_residual(b200, oracle):
+    """C5 at 512^3 (beyond the oracle's network; size-independent checks):
+    PSDO with identity-equivalent weights converges, and the oracle's
+    matrix-free A recomputes the final residual the history reports."""
+    t, seed = scenes.config("C5")
+    mask = t.reshape(-1) == 0
+    ctx = b200.Context(3, t.shape, b200.identity_params(4))
+    ctx.set_mask(t)
+    b = oracle.rhs_normal(seed, t.size)[mask]
+    res = ctx.psdo_solve(b, b200.SolveConfig(max_iters=10000))
+    hist = res.report.residual_history
+    assert res.report.converged and np.all(np.isfinite(res.x))
+    r = b - oracle.spmv(t, res.x)
+    nb, nr = np.linalg.norm(b), np.linalg.norm(r)
+    assert nr <= 1e-6 * nb * (1 + 1e-9)
+    assert abs(nr - hist[-1]) <= 1e-9 * nb
+    assert hist[0] == pytest.approx(nb, rel=1e-12)
+
+
+def test_c5_512_random_weights_precond_scaling_and_linearity(b200, oracle):
+    """512^3, random weights: P(2r) == 2 P(r) bitwise (power-of-two scaling is
+    exact through the normalisation, net_precond.cpp:20-34) and P is linear up
+    to f32 rounding (the reference's linearity test, test_neural.cpp:182-210)."""
+    t, _ = scenes.config("C5")
+    ctx = b200.Context(3, t.shape, b200.init_params(4, 17))
+    ctx.set_mask(t)
+    rng = np.random.default_rng(5)
+    r1, r2 = rng.standard_normal(ctx.n_fluid), rng.standard_normal(ctx.n_fluid)
+    z1, z2 = ctx.precond_apply(r1), ctx.precond_apply(r2)
+    assert np.all(np.isfinite(z1))
+    assert np.array_equal(ctx.precond_apply(2.0 * r1), 2.0 * z1)
+    z12 = ctx.precond_apply(r1 + r2)
+    assert rel_l2(z12, z1 + z2) <= 1e-4
