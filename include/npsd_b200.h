@@ -57,6 +57,7 @@ enum {
 };
 
 typedef struct npsd_b200_ctx npsd_b200_ctx;
+typedef struct npsd_b200_comm npsd_b200_comm;
 
 /* SolveConfig (include/npsd/solver.hpp:11-26) as a POD. */
 typedef struct {
@@ -132,6 +133,32 @@ size_t npsd_b200_param_count(int dim, int depth);
 int npsd_b200_init_params(int dim, int depth, uint64_t seed, float* out);
 int npsd_b200_identity_params(int dim, int depth, float* out);
 void npsd_b200_rhs_normal(uint64_t seed, int64_t n, double* out);
+
+/* z-slab decomposition across GPUs ("Multi-GPU"): one process
+ * (or, for tests, one host thread) and one context per rank; rank r owns
+ * global planes [z0, z0 + nz_own) of an nx x ny x nz grid (3D, depth >= 2;
+ * z0 and nz_own multiples of 2^(depth-1)). The per-rank calls are the
+ * single-domain ones: set_mask takes the owned planes' types, precond_apply
+ * / psdo_solve take the owned fluid cells' entries in ascending global order
+ * (fluid_indices returns their global linear indices), and every rank gets
+ * the same iteration count and residual history. Halo planes move over NCCL
+ * (NVLink) before each stencil / conv level; dot products are gathered and
+ * summed in rank order, so all ranks hold identical solver state.
+ *
+ * npsd_b200_nccl_unique_id: rank 0 makes the id (128 bytes) and the caller
+ * broadcasts it (e.g. torch.distributed); every rank then creates its NCCL
+ * communicator on its device. npsd_b200_comm_create_local: one communicator
+ * shared by n contexts of one process on one device, each driven by its own
+ * host thread (correctness tests of the decomposition; not a performance
+ * path). net_apply, level_image, spmv and profile_iterations are single-domain
+ * only. */
+int npsd_b200_nccl_unique_id(void* id128);
+int npsd_b200_comm_create_nccl(const void* id128, int rank, int nranks, int device, npsd_b200_comm** out);
+int npsd_b200_comm_create_local(int nranks, npsd_b200_comm** out);
+int npsd_b200_comm_destroy(npsd_b200_comm* comm);
+const char* npsd_b200_comm_last_error(void);
+int npsd_b200_create_slab(int nx, int ny, int nz, int z0, int nz_own, int depth, const float* params,
+                          size_t n_params, int device, npsd_b200_comm* comm, int rank, npsd_b200_ctx** out);
 
 /* Model files, replacing npsd::net::save_npm / load_npm (net_params.cpp:42-78):
  * "NPMW", u32 version 1, u32 dim, u32 depth, then the weights in

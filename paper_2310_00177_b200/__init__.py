@@ -28,6 +28,7 @@ __all__ = [
     "SolveConfig", "SolveReport", "SolveResult", "SolverBreakdown", "EmptySystemError", "DeviceError",
     "NetParams", "init_params", "identity_params", "param_count", "rhs_normal", "Context", "NeuralPrecond",
     "neural_precond", "psdo_solve", "psd_solve", "DeviceBuffer", "PinnedBuffer", "save_npm", "load_npm",
+    "Comm", "partition",
 ]
 
 
@@ -161,6 +162,57 @@ def rhs_normal(seed: int, n: int) -> np.ndarray:
 
 
 # ------------------------------------------------------------------ context
+def partition(nz: int, nranks: int, depth: int) -> list[tuple[int, int]]:
+    """z-slab bounds (z0, nz_own) per rank: contiguous planes in units of
+    2^(depth-1) (the pooling alignment of every level), as equal as possible."""
+    unit = 1 << (depth - 1)
+    if nz % unit or nranks < 1 or nz // unit < nranks:
+        raise ValueError(f"partition: {nz} planes cannot form {nranks} slabs of multiples of {unit}")
+    units = nz // unit
+    out, z0 = [], 0
+    for r in range(nranks):
+        k = units // nranks + (1 if r < units % nranks else 0)
+        out.append((z0, k * unit))
+        z0 += k * unit
+    return out
+
+
+class Comm:
+    """Communicator of a z-slab decomposition (include/npsd_b200.h)."""
+
+    def __init__(self, handle, nranks: int) -> None:
+        self.h, self.nranks, self.lib = handle, nranks, _native.lib()
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        st = _native.lib().npsd_b200_nccl_unique_id(buf)
+        if st != NPSD_OK:
+            raise DeviceError(_native.lib().npsd_b200_comm_last_error().decode())
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, uid: bytes, rank: int, nranks: int, device: int = 0) -> "Comm":
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        st = _native.lib().npsd_b200_comm_create_nccl(buf, rank, nranks, device, C.byref(h))
+        if st != NPSD_OK:
+            raise DeviceError(_native.lib().npsd_b200_comm_last_error().decode())
+        return cls(h, nranks)
+
+    @classmethod
+    def local(cls, nranks: int) -> "Comm":
+        """In-process ranks (one host thread each, one device): tests only."""
+        h = C.c_void_p()
+        _raise(_native.lib().npsd_b200_comm_create_local(nranks, C.byref(h)), "comm: bad nranks")
+        return cls(h, nranks)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.npsd_b200_comm_destroy(self.h)
+            self.h = None
+
+
 class Context:
     """One B200 context: grid, weights and (after set_mask) one frame."""
 
@@ -183,6 +235,30 @@ class Context:
         if st != NPSD_OK:
             _raise(st, self.lib.npsd_b200_last_error(None).decode())
         self.h = h
+
+    @classmethod
+    def slab(cls, comm: Comm, rank: int, shape: tuple, z0: int, nz_own: int, params: NetParams,
+             device: int = 0) -> "Context":
+        """Rank `rank`'s z-slab [z0, z0 + nz_own) of a 3D grid of `shape`
+        (nz, ny, nx): set_mask takes the owned planes (nz_own, ny, nx); solver
+        vectors are the owned fluid cells in ascending global order."""
+        nz, ny, nx = shape
+        if params.dim != 3:
+            raise ValueError("NeuralPrecond: params dim does not match the grid")
+        self = cls.__new__(cls)
+        self.lib = _native.lib()
+        self.dim, self.nx, self.ny, self.nz, self.depth = 3, nx, ny, nz, params.depth
+        self.shape = (nz_own, ny, nx)
+        self.n_cells = nx * ny * nz_own
+        self.z0, self.nz_own, self.comm = z0, nz_own, comm
+        h = C.c_void_p()
+        flat = np.ascontiguousarray(params.flat, np.float32)
+        st = self.lib.npsd_b200_create_slab(nx, ny, nz, z0, nz_own, params.depth, flat, flat.size, device, comm.h,
+                                            rank, C.byref(h))
+        if st != NPSD_OK:
+            _raise(st, self.lib.npsd_b200_last_error(None).decode())
+        self.h = h
+        return self
 
     def close(self) -> None:
         if getattr(self, "h", None):

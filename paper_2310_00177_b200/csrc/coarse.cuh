@@ -118,20 +118,22 @@ struct CellRow {
     }
 };
 
-// grid (ceil(nx/32), ceil(ny/4), nz/2), block (32, 4, 2)
+// grid (ceil(nx/32), ceil(ny/4), ceil(owned planes/2)), block (32, 4, 2)
 template <bool POOL>
 __global__ void __launch_bounds__(kKT) k_cdown(Geom g, const float* __restrict__ x, ConvTab ct,
                                                const __grid_constant__ KC kc, float* __restrict__ y,
-                                               float* __restrict__ xnext, Geom gc) {
+                                               float* __restrict__ xnext, Geom gc,
+                                               const int* __restrict__ done) {
+    if (done && *done) return;  // z-slab chunked loop: the solve has finished
     constexpr int SX = kKX + 2, SY = kKY + 2, SZ = kKZ + 2;
     __shared__ float sx[SZ][SY][SX];
     __shared__ float sy[kKZ][kKY][kKX];
     __shared__ UniRows U;
     const int tx = threadIdx.x, ty = threadIdx.y, tz = threadIdx.z;
     const int tid = tx + kKX * (ty + kKY * tz), warp = tid >> 5, lane = tid & 31;
-    const int X0 = blockIdx.x * kKX, Y0 = blockIdx.y * kKY, Z0 = blockIdx.z * kKZ;
+    const int X0 = blockIdx.x * kKX, Y0 = blockIdx.y * kKY, Z0 = g.zo0 + blockIdx.z * kKZ;
     const int cx = X0 + tx, cy = Y0 + ty, cz = Z0 + tz;
-    const bool own = cx < g.nx && cy < g.ny && cz < g.nz;
+    const bool own = cx < g.nx && cy < g.ny && cz < g.zo1;
     const long long c = own ? lin(g, cx, cy, cz) : 0;
     BoxStager<SX, SY, SZ, kKT / 32> box;
     box.load(x, g, X0 - 1, Y0 - 1, Z0 - 1, warp, lane);
@@ -172,21 +174,23 @@ __global__ void __launch_bounds__(kKT) k_cdown(Geom g, const float* __restrict__
     }
 }
 
-// grid (ceil(nx/32), ceil(ny/4), nz/2), block (32, 4, 2); outc is level l+1
+// grid (ceil(nx/32), ceil(ny/4), ceil(owned planes/2)), block (32, 4, 2); outc is level l+1
 template <int D = 3>
 __global__ void __launch_bounds__(kKT) k_cup(Geom g, Geom gc, const float* __restrict__ outc,
                                              const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
-                                             const __grid_constant__ KC kc, float* __restrict__ outl) {
+                                             const __grid_constant__ KC kc, float* __restrict__ outl,
+                                             const int* __restrict__ done) {
+    if (done && *done) return;  // z-slab chunked loop: the solve has finished
     // coarse box: (X0/2 - 1 .. X0/2 + 16) x (Y0/2 - 1 .. Y0/2 + 2) x (Z0/2 - 1 .. Z0/2 + 1)
     constexpr int CX = kKX / 2 + 2, CY = kKY / 2 + 2, CZ = kKZ / 2 + 2;
     __shared__ float sc[CZ][CY][CX];
     __shared__ UniRows U;
     const int tx = threadIdx.x, ty = threadIdx.y, tz = threadIdx.z;
     const int tid = tx + kKX * (ty + kKY * tz), warp = tid >> 5, lane = tid & 31;
-    const int X0 = blockIdx.x * kKX, Y0 = blockIdx.y * kKY, Z0 = blockIdx.z * kKZ;
+    const int X0 = blockIdx.x * kKX, Y0 = blockIdx.y * kKY, Z0 = g.zo0 + blockIdx.z * kKZ;
     const int BX = (X0 >> 1) - 1, BY = (Y0 >> 1) - 1, BZ = (Z0 >> 1) - 1;
     const int cx = X0 + tx, cy = Y0 + ty, cz = Z0 + tz;
-    const bool own = cx < g.nx && cy < g.ny && cz < g.nz;
+    const bool own = cx < g.nx && cy < g.ny && cz < g.zo1;
     const long long c = own ? lin(g, cx, cy, cz) : 0;
     BoxStager<CX, CY, CZ, kKT / 32> box;
     box.load(outc, gc, BX, BY, BZ, warp, lane);

@@ -20,9 +20,15 @@ constexpr int kMaxDepth = 8;
 constexpr int kBlock = 256;             // threads per block for all kernels
 
 // Level geometry. nz == 1 for 2D.
+// A level's local grid. nz counts every stored plane; [zo0, zo1) are the
+// planes this context owns. Single-domain: zo0 = 0, zo1 = nz. A z-slab adds
+// ghost planes on both sides (neighbour copies, or the outside of the domain
+// at its faces): kernels read through them but compute, store and reduce
+// over owned planes only.
 struct Geom {
     int nx, ny, nz;
     long long n;
+    int zo0, zo1;
 };
 
 __host__ __device__ inline Geom make_geom(int nx, int ny, int nz) {
@@ -31,8 +37,18 @@ __host__ __device__ inline Geom make_geom(int nx, int ny, int nz) {
     g.ny = ny;
     g.nz = nz;
     g.n = (long long)nx * ny * nz;
+    g.zo0 = 0;
+    g.zo1 = nz;
     return g;
 }
+
+__host__ __device__ inline long long owned_lo(const Geom& g) { return (long long)g.zo0 * g.nx * g.ny; }
+__host__ __device__ inline long long owned_hi(const Geom& g) { return (long long)g.zo1 * g.nx * g.ny; }
+
+// grid-stride loop over the owned cells of g
+#define FOR_OWNED(g, c)                                                                    \
+    for (long long c = owned_lo(g) + (long long)blockIdx.x * blockDim.x + threadIdx.x; \
+         c < owned_hi(g); c += (long long)gridDim.x * blockDim.x)
 
 __host__ __device__ __forceinline__ long long lin(const Geom& g, int x, int y, int z) {
     return ((long long)z * g.ny + y) * g.nx + x;
@@ -68,6 +84,8 @@ __device__ __forceinline__ long long mixed_index(const uint32_t* __restrict__ mm
 
 // Device-resident solver state (one per context). Written only by the last
 // block of a reducing kernel; read by every later kernel.
+constexpr int kPart = 2 + kMaxOrtho;  // doubles per reduction point (z-slab partials)
+
 struct SolverState {
     // configuration (host-written before each solve)
     double tol_reduction, tol_abs;
@@ -90,6 +108,9 @@ struct SolverState {
     double mean;                    // nullspace projection mean
     double bad_value;               // curvature at breakdown
     unsigned long long t0;          // %globaltimer at solve start
+    double part[kPart];             // z-slab: this rank's totals at a reduction point
+    int dist;                       // z-slab: reductions stop at part[], k_finalize finishes them;
+                                    // iteration kernels return at once when done (chunked loop)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {

@@ -20,13 +20,12 @@
 
 namespace nb2 {
 
-// compact list of mixed cells: list[mixed_index(c)] = c
+// compact list of the owned mixed cells: list[mixed_index(c)] = c
 __global__ void __launch_bounds__(kBlock) k_mixed_list(Geom g, const uint8_t* __restrict__ cls,
                                                        const uint32_t* __restrict__ mmask,
                                                        const uint32_t* __restrict__ mbase, uint32_t* __restrict__ list) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
-        if (cls_window(cls[c]) == 3) list[mixed_index(mmask, mbase, c)] = (uint32_t)c;
+    FOR_OWNED(g, c)
+    if (cls_window(cls[c]) == 3) list[mixed_index(mmask, mbase, c)] = (uint32_t)c;
 }
 
 // The solve needs y_0 only at mixed cells whose window holds a fluid cell (the
@@ -74,8 +73,7 @@ __global__ void __launch_bounds__(kBlock) k_row_codes(Geom g, const uint8_t* __r
                                                       const uint32_t* __restrict__ mmask,
                                                       const uint32_t* __restrict__ mbase,
                                                       const uint32_t* __restrict__ kid, uint32_t* __restrict__ rcode) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    FOR_OWNED(g, c) {
         const uint32_t w = (uint32_t)cls_window(cls[c]);
         uint32_t row = 0;
         if (w == 3) {
@@ -107,6 +105,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* 
                                                         const float* __restrict__ tab, const uint32_t* __restrict__ kid,
                                                         float* __restrict__ y) {
     constexpr int S = Sh<D>::S;
+    if (st->dist && st->done) return;
     const uint32_t n = *count;
     const double inv1 = st->inv1, inv2 = st->inv2;
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -131,6 +130,19 @@ __global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* 
     }
 }
 
+// MGS projections from the dots d.Ad_j (solver.cpp:240-243, classical form
+// on the cached cross terms)
+__device__ __forceinline__ void fin_projections(SolverState* st, const double* dots) {
+    const int nc = st->n_cache, R = st->ring;
+    int slot[kMaxOrtho];
+    for (int j = 0; j < nc && j < kMaxOrtho; ++j) slot[j] = (st->head - (nc - 1) + j + 2 * R) % R;
+    for (int j = 0; j < nc && j < kMaxOrtho; ++j) {
+        double num = dots[j];
+        for (int i = 0; i < j; ++i) num -= st->p[i] * st->cross[slot[i]][slot[j]];
+        st->p[j] = num / st->dAd[slot[j]];
+    }
+}
+
 template <int D, int NO>
 __global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uint32_t* __restrict__ list,
                                                       const uint32_t* __restrict__ count,
@@ -141,6 +153,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uin
                                                       unsigned int* __restrict__ counter) {
     constexpr int S = Sh<D>::S;
     constexpr int NA = (NO > 0) ? NO : 1;
+    if (st->dist && st->done) return;
     const uint32_t n = *count;
     const float za = zab[0], zb = zab[1];
     const double nrm = st->nrm;
@@ -183,13 +196,12 @@ __global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uin
     double tot[NA];
     if (grid_reduce<NA>(acc, partials, counter, tot) && threadIdx.x == 0) {
         // totals of the tiled kernel first, then this kernel's (fixed order)
-        const int Rr = st->ring;
-        int slot[NA];
-        for (int j = 0; j < nc && j < NA; ++j) slot[j] = (st->head - (nc - 1) + j + 2 * Rr) % Rr;
-        for (int j = 0; j < nc && j < NO; ++j) {
-            double num = st->dot_main[j] + tot[j];
-            for (int i = 0; i < j; ++i) num -= st->p[i] * st->cross[slot[i]][slot[j]];
-            st->p[j] = num / st->dAd[slot[j]];
+        double dots[kMaxOrtho];
+        for (int j = 0; j < nc && j < NO; ++j) dots[j] = st->dot_main[j] + tot[j];
+        if (st->dist) {
+            for (int j = 0; j < kMaxOrtho; ++j) st->part[j] = (j < nc && j < NO) ? dots[j] : 0.0;
+        } else {
+            fin_projections(st, dots);
         }
     }
 }

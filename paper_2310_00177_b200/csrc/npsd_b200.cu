@@ -7,10 +7,15 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <condition_variable>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -27,6 +32,7 @@
 #include "down0.cuh"
 #include "coarse.cuh"
 #include "up0.cuh"
+#include "slab.cuh"
 
 using namespace nb2;
 
@@ -90,9 +96,161 @@ struct LevelOffsets {
 
 }  // namespace
 
+// ------------------------------------------------------------------ z-slab
+// Communicator of a z-slab decomposition ("Multi-GPU"): ghost-plane
+// exchange with the two neighbours and an allgather of per-rank partials.
+// NCCL ranks enqueue both on the context's stream (graph-capturable); the
+// in-process communicator (one host thread per rank, one device) uses host
+// barriers and device copies and is for correctness tests only.
+struct npsd_b200_comm {
+    int nranks = 1;
+    virtual ~npsd_b200_comm() = default;
+    virtual bool capturable() const = 0;
+    // planes zo0 / zo1-1 of the field at base go to rank-1 / rank+1, whose
+    // boundary planes arrive in zo0-1 / zo1 (plane = pb bytes)
+    virtual void exchange(int rank, cudaStream_t s, char* base, size_t pb, int zo0, int zo1) = 0;
+    // all[r * bytes ...] = rank r's part, on every rank, rank order
+    virtual void allgather(int rank, cudaStream_t s, const void* part, void* all, size_t bytes) = 0;
+};
+
+namespace {
+
+// NCCL, resolved at run time (no link dependency for single-GPU use)
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!api.h) return;
+        auto sym = [](const char* n) { return dlsym(api.h, n); };
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+        api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+        api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+        api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    });
+    if (!api.h || !api.CommInitRank || !api.Send || !api.Recv || !api.AllGather)
+        throw CudaError("npsd_b200: libnccl.so.2 not found (z-slab contexts need NCCL)");
+    return api;
+}
+
+#define NCK(call)                                                                                  \
+    do {                                                                                           \
+        ncclResult_t r_ = (call);                                                                  \
+        if (r_ != ncclSuccess)                                                                     \
+            throw CudaError(std::string(#call) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r_) : "nccl error")); \
+    } while (0)
+
+struct NcclComm : npsd_b200_comm {
+    ncclComm_t comm = nullptr;
+    int rank = 0;
+    bool capturable() const override { return true; }
+    void exchange(int, cudaStream_t s, char* base, size_t pb, int zo0, int zo1) override {
+        NcclApi& A = nccl();
+        NCK(A.GroupStart());
+        if (rank > 0) {
+            NCK(A.Send(base + (size_t)zo0 * pb, pb, ncclUint8, rank - 1, comm, s));
+            NCK(A.Recv(base + (size_t)(zo0 - 1) * pb, pb, ncclUint8, rank - 1, comm, s));
+        }
+        if (rank + 1 < nranks) {
+            NCK(A.Send(base + (size_t)(zo1 - 1) * pb, pb, ncclUint8, rank + 1, comm, s));
+            NCK(A.Recv(base + (size_t)zo1 * pb, pb, ncclUint8, rank + 1, comm, s));
+        }
+        NCK(A.GroupEnd());
+    }
+    void allgather(int, cudaStream_t s, const void* part, void* all, size_t bytes) override {
+        NCK(nccl().AllGather(part, all, bytes, ncclUint8, comm, s));
+    }
+    ~NcclComm() override {
+        if (comm) nccl().CommDestroy(comm);
+    }
+};
+
+// In-process ranks (threads) on one device: each collective is two barriers
+// around device copies between the ranks' buffers; no device-side waiting.
+struct LocalComm : npsd_b200_comm {
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long gen = 0;
+    std::vector<char*> base;
+    std::vector<const void*> src;
+    std::vector<int> zo0v, zo1v;
+    explicit LocalComm(int n) : base(n), src(n), zo0v(n), zo1v(n) { nranks = n; }
+    bool capturable() const override { return false; }
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const long long g = gen;
+        if (++arrived == nranks) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g; })) {
+            throw CudaError("local comm: a rank did not reach the barrier within 120 s");
+        }
+    }
+    void exchange(int rank, cudaStream_t s, char* b, size_t pb, int zo0, int zo1) override {
+        CK(cudaStreamSynchronize(s));  // this rank's owned planes are final
+        base[rank] = b;
+        zo0v[rank] = zo0;
+        zo1v[rank] = zo1;
+        barrier();
+        if (rank > 0)
+            CK(cudaMemcpyAsync(b + (size_t)(zo0 - 1) * pb, base[rank - 1] + (size_t)(zo1v[rank - 1] - 1) * pb, pb,
+                               cudaMemcpyDeviceToDevice, s));
+        if (rank + 1 < nranks)
+            CK(cudaMemcpyAsync(b + (size_t)zo1 * pb, base[rank + 1] + (size_t)zo0v[rank + 1] * pb, pb,
+                               cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        barrier();  // no rank overwrites its planes before every copy is done
+    }
+    void allgather(int rank, cudaStream_t s, const void* part, void* all, size_t bytes) override {
+        CK(cudaStreamSynchronize(s));
+        src[rank] = part;
+        barrier();
+        for (int r = 0; r < nranks; ++r)
+            CK(cudaMemcpyAsync(static_cast<char*>(all) + (size_t)r * bytes, src[r], bytes, cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        barrier();
+    }
+};
+
+struct SlabInfo {
+    bool on = false;
+    int rank = 0, nranks = 1;
+    int z0 = 0, nz_own = 0, nz_global = 0;  // level-0 planes
+    int ghost[kMaxDepth] = {};              // ghost planes per side, level l: 2^(depth-1-l)
+    npsd_b200_comm* comm = nullptr;
+    double* all = nullptr;                  // [nranks][kPart] gathered partials
+    unsigned long long* allu = nullptr;     // [nranks][81] gathered window counts
+};
+
+}  // namespace
+
 struct npsd_b200_ctx {
     int dim = 3, depth = 1, S = 27, dev = 0, num_sms = 148;
     Geom g0{};
+    SlabInfo slab;                // z-slab decomposition (single domain: off)
+    Geom gglob[kMaxDepth] = {};   // the full grid per level (z-slab: all ranks)
+    cudaGraphExec_t slab_exec = nullptr;  // z-slab: a chunk of iterations (NCCL ranks)
+    int slab_exec_no = -1, slab_exec_k0 = -1;
     cudaStream_t s = nullptr, s2 = nullptr;
     std::vector<float> params;
     std::vector<LevelOffsets> offs;
@@ -184,7 +342,37 @@ int grid_for(npsd_b200_ctx* c, K kernel, long long items) {
     } while (0)
 
 Geom level_geom(const npsd_b200_ctx* c, int l) {
-    return make_geom(c->g0.nx >> l, c->g0.ny >> l, (c->dim == 3) ? (c->g0.nz >> l) : 1);
+    if (!c->slab.on) return c->gglob[l];
+    // z-slab: owned planes between ghost[l] planes on each side (ghost widths
+    // halve per level, so local fine plane = 2 x local coarse plane holds)
+    const int G = c->slab.ghost[l], own = c->slab.nz_own >> l;
+    Geom g = make_geom(c->gglob[l].nx, c->gglob[l].ny, own + 2 * G);
+    g.zo0 = G;
+    g.zo1 = G + own;
+    return g;
+}
+
+// global index of local plane 0 at level l
+int zg_offset(const npsd_b200_ctx* c, int l) {
+    return c->slab.on ? (c->slab.z0 >> l) - c->slab.ghost[l] : 0;
+}
+
+// z-slab collectives on the context's stream
+void slab_exchange(npsd_b200_ctx* c, cudaStream_t s, void* base, size_t elem, int l) {
+    const Geom& g = c->L[l].g;
+    c->slab.comm->exchange(c->slab.rank, s, static_cast<char*>(base), (size_t)g.nx * g.ny * elem, g.zo0, g.zo1);
+}
+
+void slab_allreduce_u64(npsd_b200_ctx* c, cudaStream_t s, unsigned long long* v, int k) {
+    c->slab.comm->allgather(c->slab.rank, s, v, c->slab.allu, (size_t)k * sizeof(unsigned long long));
+    k_sum_u64<<<1, 128, 0, s>>>(c->slab.allu, c->slab.nranks, k, v);
+    CK(cudaGetLastError());
+}
+
+void slab_reduce(npsd_b200_ctx* c, cudaStream_t s, int kind) {
+    c->slab.comm->allgather(c->slab.rank, s, c->st->part, c->slab.all, kPart * sizeof(double));
+    k_finalize<<<1, 32, 0, s>>>(kind, c->st, c->slab.all, c->slab.nranks, c->hist, c->times);
+    CK(cudaGetLastError());
 }
 
 void compute_offsets(npsd_b200_ctx* c) {
@@ -295,8 +483,8 @@ void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int 
         sb.len = dalloc<int>((size_t)sb.ncol);
     }
     const int nb = (sb.ncol + kBlock - 1) / kBlock;
-    k_sched_cols<<<nb, kBlock, 0, c->s>>>(c->tflags, c->tf_ntx, c->tf_nty, c->g0.nz, tx / kFlagTX, ty / kFlagTY, ntx,
-                                          nty, unit, zdil, sb.zlo, sb.len);
+    k_sched_cols<<<nb, kBlock, 0, c->s>>>(c->tflags, c->tf_ntx, c->tf_nty, c->g0.nz, c->g0.zo0, c->g0.zo1,
+                                          tx / kFlagTX, ty / kFlagTY, ntx, nty, unit, zdil, sb.zlo, sb.len);
     k_sched_prefix<<<1, 32, 0, c->s>>>(sb.len, sb.ncol, sb.pre);
     CK(cudaGetLastError());
     c->launches += 2;
@@ -365,6 +553,14 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         LevelBufs& Lc = c->L[l];
         LAUNCH(c, s, k_pool_image<D>, Lc.g.n, Lf.g, Lc.g, (l == 1) ? dtypes : nullptr, (l == 1) ? nullptr : Lf.img,
                Lc.img);
+        if (c->slab.on) {
+            // ghost planes: the outside of the domain, then the neighbours' planes
+            if (Lc.g.zo0 > 0) LAUNCH(c, s, k_solid_planes, (long long)Lc.g.zo0 * Lc.g.nx * Lc.g.ny, Lc.g, Lc.img, 0, Lc.g.zo0);
+            if (Lc.g.zo1 < Lc.g.nz)
+                LAUNCH(c, s, k_solid_planes, (long long)(Lc.g.nz - Lc.g.zo1) * Lc.g.nx * Lc.g.ny, Lc.g, Lc.img, Lc.g.zo1,
+                       Lc.g.nz);
+            for (int ch = 0; ch < 3; ++ch) slab_exchange(c, s, Lc.img + (size_t)ch * Lc.g.n, sizeof(float), l);
+        }
         LAUNCH(c, s, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
         scan_u32(c, Lc.mcount, Lc.mbase, Lc.nseg);
     }
@@ -453,8 +649,9 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
             constexpr int NC = (D == 3) ? 27 : 9;
             CK(cudaMemsetAsync(L.zG, 0, 3 * NC * sizeof(unsigned long long), s));
             const double scale = std::ldexp(1.0, D * l);
-            LAUNCH(c, s, k_zsums<D>, L.g.n, L.g, st, im, (float)scale, L.zG);
-            k_zfinal<D><<<1, 32, 0, s>>>(L.g, L.zG, scale, c->d_params + o.a_K, c->params[o.a_bias],
+            LAUNCH(c, s, k_zsums<D>, L.g.n, L.g, st, im, (float)scale, zg_offset(c, l), c->gglob[l].nz, L.zG);
+            if (c->slab.on) slab_allreduce_u64(c, s, L.zG, 3 * NC);
+            k_zfinal<D><<<1, 32, 0, s>>>(c->gglob[l], L.zG, scale, c->d_params + o.a_K, c->params[o.a_bias],
                                          c->d_params + o.b_K, c->params[o.b_bias], c->zab + 2 * l, c->zab + 2 * l + 1);
             CK(cudaGetLastError());
             ++c->launches;
@@ -525,8 +722,9 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
     if (D == 3 && !L0) {
         // f32 input (levels >= 1, raw level 0): one thread per cell (coarse.cuh)
         const KC& kc = (l == c->depth - 1) ? c->kc_coarse : c->kc_down[l];
-        const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.nz + kKZ - 1) / kKZ);
-        LAUNCH3(c, s, k_cdown<POOL>, grid, dim3(kKX, kKY, kKZ), L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc);
+        const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
+        LAUNCH3(c, s, k_cdown<POOL>, grid, dim3(kKX, kKY, kKZ), L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc,
+                c->slab.on ? &c->st->done : nullptr);
         return;
     }
     const dim3 block(kNX, kNY);
@@ -547,9 +745,9 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
     const LevelBufs& Lc = c->L[l + 1];
     const float* outc = (l + 1 == c->depth - 1) ? Lc.y : Lc.out;
     if (D == 3 && MODE == kUpMid) {
-        const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.nz + kKZ - 1) / kKZ);
+        const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
         LAUNCH3(c, s, k_cup<3>, grid, dim3(kKX, kKY, kKZ), L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
-                c->kc_up[l], outl);
+                c->kc_up[l], outl, c->slab.on ? &c->st->done : nullptr);
         return;
     }
     const dim3 block(kNX, kNY);
@@ -676,10 +874,20 @@ void launch_mixed_up0_no(npsd_b200_ctx* c, cudaStream_t s, int no) {
     }
 }
 
+// z-slab: ghost planes of a level-l field refreshed from the neighbours
+Step xchg_step(npsd_b200_ctx* c, const std::string& name, std::function<void*()> ptr, size_t elem, int l) {
+    return {name, [c, ptr, elem, l](cudaStream_t s) { slab_exchange(c, s, ptr(), elem, l); }};
+}
+
+Step reduce_step(npsd_b200_ctx* c, const std::string& name, int kind) {
+    return {name, [c, kind](cudaStream_t s) { slab_reduce(c, s, kind); }};
+}
+
 template <int D>
 std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     std::vector<Step> v;
     const int Ld = c->depth;
+    const bool xg = c->slab.on && !raw;  // z-slab: halos before every conv level
     // solve path: level-0 mixed-window cells are computed apart (mixed.cuh)
     if (!raw) v.push_back({"net_mixed_down_L0", [c](cudaStream_t s) { launch_mixed_down0<D>(c, s); }});
     for (int l = 0; l < Ld; ++l) {
@@ -701,6 +909,12 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
                                  launch_down<D, false, false>(c, s, l, in, nullptr);
                          }
                      }});
+        if (xg && pool)
+            v.push_back(xchg_step(c, "xchg_x_L" + std::to_string(l + 1), [c, l] { return (void*)c->L[l + 1].x; },
+                                  sizeof(float), l + 1));
+        else if (xg)
+            v.push_back(xchg_step(c, "xchg_y_L" + std::to_string(l), [c, l] { return (void*)c->L[l].y; }, sizeof(float),
+                                  l));
     }
     for (int l = Ld - 2; l >= 0; --l) {
         v.push_back({"net_up_L" + std::to_string(l), [c, l, raw, no](cudaStream_t s) {
@@ -709,6 +923,9 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
                          else
                              launch_up<D, kUpMid, 0>(c, s, l, (l == 0) ? c->out_f : c->L[l].out, nullptr);
                      }});
+        if (xg && l > 0)
+            v.push_back(xchg_step(c, "xchg_out_L" + std::to_string(l), [c, l] { return (void*)c->L[l].out; },
+                                  sizeof(float), l));
     }
     if (!raw && Ld > 1)
         v.push_back({"net_mixed_up_L0", [c, no](cudaStream_t s) { launch_mixed_up0_no<D>(c, s, no); }});
@@ -934,6 +1151,136 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
     return NPSD_OK;
 }
 
+// ------------------------------------------------------------ z-slab solve
+// One iteration for iteration index k (1-based): the ring slot and the x
+// buffer an iteration writes follow from k (head and xcur advance once per
+// iteration), so a chunk of lcm(2, ring) * m iterations repeats exactly.
+template <int D>
+std::vector<Step> slab_body_steps(npsd_b200_ctx* c, int no, long long k) {
+    std::vector<Step> v = network_steps<D>(c, false, no);
+    const int R = no + 1;
+    const int nw = (int)((R - 1 + k) % R);
+    double* dnew = c->Dring + (size_t)nw * (size_t)c->g0.n;
+    double* xnew = ((k - 1) & 1) ? c->X0 : c->X1;
+    v.push_back(reduce_step(c, "reduce_proj", kFinProj));
+    v.push_back(xchg_step(c, "xchg_d", [c] { return (void*)c->Dtmp; }, sizeof(double), 0));
+    v.push_back({"ortho", [c, no](cudaStream_t s) { launch_ortho_no<D>(c, s, no); }});
+    v.push_back(reduce_step(c, "reduce_ortho", kFinOrtho));
+    v.push_back(xchg_step(c, "xchg_dnew", [dnew] { return (void*)dnew; }, sizeof(double), 0));
+    v.push_back({"update", [c](cudaStream_t s) { launch_update<D>(c, s, 0, 0, 1); }});
+    v.push_back(reduce_step(c, "reduce_update", kFinUpdate));
+    v.push_back(xchg_step(c, "xchg_xnew", [xnew] { return (void*)xnew; }, sizeof(double), 0));
+    v.push_back(xchg_step(c, "xchg_r", [c] { return (void*)c->R; }, sizeof(double), 0));
+    return v;
+}
+
+int slab_chunk(int ring) {
+    const int p = (ring % 2 == 0) ? ring : 2 * ring;  // lcm(2, ring)
+    return p * ((12 + p - 1) / p);
+}
+
+// psdo_solve over a z-slab (c->Bf / c->X0 set on the owned planes). The
+// iterations run in chunks — one captured graph of slab_chunk() iterations per
+// launch for NCCL ranks, eager steps for the in-process communicator — with
+// every iteration kernel returning at once after the solve has finished.
+template <int D>
+int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_report* rep) {
+    require(cfg->tol_reduction > 0.0 && cfg->tol_reduction < 1.0, "SolveConfig: tol_reduction must lie in (0,1)");
+    require(cfg->n_ortho >= 0, "psdo: n_ortho must be >= 0");
+    require(cfg->n_ortho <= kMaxOrtho, "psdo: n_ortho > 8 is not supported by the B200 build");
+    require(!cfg->nullspace_projection, "psdo: nullspace projection is not supported on a z-slab context");
+    cudaStream_t s = c->s;
+    const long long max_iters = cfg->max_iters < 0 ? 0 : cfg->max_iters;
+    const int no = cfg->n_ortho, ring = no + 1;
+    ensure_ring(c, ring);
+    ensure_hist(c, max_iters + 1);
+    SolverState* h = c->st_host;
+    std::memset(h, 0, sizeof(SolverState));
+    h->tol_reduction = cfg->tol_reduction;
+    h->tol_abs = cfg->tol_abs;
+    h->max_iters = max_iters;
+    h->n_ortho = no;
+    h->normalize = cfg->normalize_before_precond ? 1 : 0;
+    h->ring = ring;
+    h->dist = 1;
+    CK(cudaMemcpyAsync(c->st, h, sizeof(SolverState), cudaMemcpyHostToDevice, s));
+    ensure_x1_clean(c, s);
+    const Geom g = c->g0;
+    const uint8_t* cls = c->L[0].cls;
+    CK(cudaEventRecord(c->ev0, s));
+    // prologue: r0 = b - A x0 (x0's ghosts first), ||r0|| over all ranks
+    slab_exchange(c, s, c->X0, sizeof(double), 0);
+    LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R);
+    LAUNCH(c, s, k_residual_norm, g.n, g, c->R, c->st, c->hist, c->times, c->partials, c->counter,
+           (cudaGraphConditionalHandle)0, 0, 1);
+    slab_reduce(c, s, kFinNorm0);
+    slab_exchange(c, s, c->R, sizeof(double), 0);
+    const int K = slab_chunk(ring);
+    const bool graph = c->slab.comm->capturable();
+    if (graph && (!c->slab_exec || c->slab_exec_no != no || c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist ||
+                  c->exec_key[2] != c->ADring)) {
+        if (c->slab_exec) CK(cudaGraphExecDestroy(c->slab_exec));
+        c->slab_exec = nullptr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        for (long long k = 1; k <= K; ++k)
+            for (const auto& st : slab_body_steps<D>(c, no, k)) st.run(s);
+        cudaGraph_t gr = nullptr;
+        CK(cudaStreamEndCapture(s, &gr));
+        CK(cudaGraphInstantiate(&c->slab_exec, gr, 0));
+        CK(cudaGraphDestroy(gr));
+        c->slab_exec_no = no;
+        c->exec_key[0] = c->Dring;
+        c->exec_key[1] = c->hist;
+        c->exec_key[2] = c->ADring;
+    }
+    for (long long k0 = 1;; k0 += K) {
+        CK(cudaMemcpyAsync(&h->done, &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (h->done) break;
+        if (graph) {
+            CK(cudaGraphLaunch(c->slab_exec, s));
+        } else {
+            for (long long k = k0; k < k0 + K; ++k)
+                for (const auto& st : slab_body_steps<D>(c, no, k)) st.run(s);
+        }
+    }
+    CK(cudaEventRecord(c->ev1, s));
+    CK(cudaMemcpyAsync(h, c->st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    const long long iters = h->breakdown ? h->k - 1 : ((h->k > 1) ? h->k - 1 : 0);
+    const long long hl = iters + 1;
+    ensure_hist_host(c, hl);
+    CK(cudaMemcpyAsync(c->hist_host, c->hist, (size_t)hl * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->times_host, c->times, (size_t)hl * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->report_hist.assign(c->hist_host, c->hist_host + hl);
+    c->report_times.assign(c->times_host, c->times_host + hl);
+    if (rep) {
+        rep->iterations = iters;
+        rep->converged = h->converged;
+        rep->breakdown = h->breakdown;
+        rep->residual_history = c->report_hist.data();
+        rep->cumulative_seconds = c->report_times.data();
+        rep->history_len = hl;
+        rep->setup_seconds = 0.0;
+        rep->iterate_seconds = c->last_ms * 1e-3;
+        rep->precond_seconds = 0.0;
+    }
+    if (h->breakdown) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "psdo: curvature d'Ad = %f at iteration %lld (||r|| = %f)", h->bad_value,
+                      h->k, h->rnorm);
+        throw Breakdown(buf);
+    }
+    return NPSD_OK;
+}
+
+int solve_any(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_report* rep) {
+    if (c->slab.on) return slab_solve_impl<3>(c, cfg, rep);
+    return (c->dim == 3) ? solve_device_impl<3>(c, cfg, rep) : solve_device_impl<2>(c, cfg, rep);
+}
+
 template <typename Fn>
 int guarded(npsd_b200_ctx* c, Fn&& fn) {
     if (!c) return NPSD_INVALID_ARGUMENT;
@@ -966,6 +1313,9 @@ void free_ctx(npsd_b200_ctx* c) {
     auto F = [](void* p) {
         if (p) cudaFree(p);
     };
+    F(c->slab.all);
+    F(c->slab.allu);
+    if (c->slab_exec) cudaGraphExecDestroy(c->slab_exec);
     for (SchedBufs* sb : {&c->sch_stencil, &c->sch_down0}) {
         F(sb->pre);
         F(sb->zlo);
@@ -1051,8 +1401,11 @@ size_t npsd_b200_param_count(int dim, int depth) {
     return param_count_impl(dim, depth);
 }
 
-int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* params, size_t n_params,
-                     const int* devices, int n_devices, npsd_b200_ctx** out) {
+namespace {
+
+// One context: the whole grid, or (slab != nullptr) one rank's z-slab.
+int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params, size_t n_params, int device,
+                const SlabInfo* slab, npsd_b200_ctx** out) {
     if (!out) return NPSD_INVALID_ARGUMENT;
     *out = nullptr;
     npsd_b200_ctx* c = new npsd_b200_ctx();
@@ -1066,12 +1419,17 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
                 "NetContext: dims " + std::to_string(nx) + "x" + std::to_string(ny) +
                     (dim == 3 ? "x" + std::to_string(nz) : std::string()) + " not divisible by 2^" +
                     std::to_string(depth));
-        require(n_devices <= 1, "npsd_b200: one device per context in this build (z-slab sharding: see DESIGN.md)");
         c->dim = dim;
         c->depth = depth;
         c->S = (dim == 3) ? 27 : 9;
-        c->dev = (devices && n_devices == 1) ? devices[0] : 0;
-        c->g0 = make_geom(nx, ny, nz);
+        c->dev = device;
+        if (slab) {
+            c->slab = *slab;
+            for (int l = 0; l < depth; ++l) c->slab.ghost[l] = 1 << (depth - 1 - l);
+        }
+        for (int l = 0; l < depth; ++l)
+            c->gglob[l] = make_geom(nx >> l, ny >> l, (dim == 3) ? (nz >> l) : 1);
+        c->g0 = level_geom(c, 0);
         require(c->g0.n < (1LL << 31) * 16, "npsd_b200: grid too large");
         CK(cudaSetDevice(c->dev));
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->dev));
@@ -1156,6 +1514,13 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
         }
         ensure_ring(c, 3);
         ensure_hist(c, 1001);
+        if (c->slab.on) {
+            c->slab.all = dalloc<double>((size_t)c->slab.nranks * kPart);
+            c->slab.allu = dalloc<unsigned long long>((size_t)c->slab.nranks * 81);
+            // ghost planes start as the outside of the domain (zeros)
+            const size_t n = (size_t)c->g0.n;
+            for (double* v : {c->X0, c->X1, c->R, c->Bf, c->Dtmp}) CK(cudaMemsetAsync(v, 0, n * sizeof(double), c->s));
+        }
         do_set_params(c, params, n_params);
         CK(cudaStreamSynchronize(c->s));
         *out = c;
@@ -1172,6 +1537,101 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
         return NPSD_CUDA_ERROR;
     }
 }
+
+thread_local std::string g_comm_err;
+
+}  // namespace
+
+int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* params, size_t n_params,
+                     const int* devices, int n_devices, npsd_b200_ctx** out) {
+    if (n_devices > 1) {
+        g_create_err = "npsd_b200: one device per context; shard a grid with npsd_b200_create_slab";
+        if (out) *out = nullptr;
+        return NPSD_INVALID_ARGUMENT;
+    }
+    return create_impl(dim, nx, ny, nz, depth, params, n_params, (devices && n_devices == 1) ? devices[0] : 0,
+                       nullptr, out);
+}
+
+int npsd_b200_create_slab(int nx, int ny, int nz, int z0, int nz_own, int depth, const float* params,
+                          size_t n_params, int device, npsd_b200_comm* comm, int rank, npsd_b200_ctx** out) {
+    if (out) *out = nullptr;
+    if (!comm || !out) {
+        g_create_err = "create_slab: null communicator or output";
+        return NPSD_INVALID_ARGUMENT;
+    }
+    const int unit = 1 << (depth > 0 ? depth - 1 : 0);
+    std::string why;
+    if (depth < 2 || depth > kMaxDepth) why = "create_slab: depth must be in [2, 8]";
+    else if (rank < 0 || rank >= comm->nranks) why = "create_slab: rank out of range";
+    else if (nz_own <= 0 || z0 < 0 || z0 + nz_own > nz) why = "create_slab: slab outside the grid";
+    else if (z0 % unit != 0 || nz_own % unit != 0)
+        why = "create_slab: slab bounds must be multiples of 2^(depth-1) = " + std::to_string(unit);
+    else if (((long long)nx * ny) % 32 != 0) why = "create_slab: nx * ny must be a multiple of 32";
+    if (!why.empty()) {
+        g_create_err = why;
+        return NPSD_INVALID_ARGUMENT;
+    }
+    SlabInfo si;
+    si.on = true;
+    si.rank = rank;
+    si.nranks = comm->nranks;
+    si.z0 = z0;
+    si.nz_own = nz_own;
+    si.nz_global = nz;
+    si.comm = comm;
+    return create_impl(3, nx, ny, nz, depth, params, n_params, device, &si, out);
+}
+
+int npsd_b200_nccl_unique_id(void* id128) {
+    try {
+        if (!id128) return NPSD_INVALID_ARGUMENT;
+        ncclUniqueId id;
+        NCK(nccl().GetUniqueId(&id));
+        std::memcpy(id128, &id, sizeof(id));
+        return NPSD_OK;
+    } catch (const std::exception& e) {
+        g_comm_err = e.what();
+        return NPSD_CUDA_ERROR;
+    }
+}
+
+int npsd_b200_comm_create_nccl(const void* id128, int rank, int nranks, int device, npsd_b200_comm** out) {
+    if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return NPSD_INVALID_ARGUMENT;
+    *out = nullptr;
+    try {
+        CK(cudaSetDevice(device));
+        auto* cm = new NcclComm();
+        cm->nranks = nranks;
+        cm->rank = rank;
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        try {
+            NCK(nccl().CommInitRank(&cm->comm, nranks, id, rank));
+        } catch (...) {
+            delete cm;
+            throw;
+        }
+        *out = cm;
+        return NPSD_OK;
+    } catch (const std::exception& e) {
+        g_comm_err = e.what();
+        return NPSD_CUDA_ERROR;
+    }
+}
+
+int npsd_b200_comm_create_local(int nranks, npsd_b200_comm** out) {
+    if (!out || nranks < 1) return NPSD_INVALID_ARGUMENT;
+    *out = new LocalComm(nranks);
+    return NPSD_OK;
+}
+
+int npsd_b200_comm_destroy(npsd_b200_comm* comm) {
+    delete comm;
+    return NPSD_OK;
+}
+
+const char* npsd_b200_comm_last_error(void) { return g_comm_err.c_str(); }
 
 int npsd_b200_destroy(npsd_b200_ctx* c) {
     if (!c) return NPSD_OK;
@@ -1191,9 +1651,25 @@ int npsd_b200_set_params(npsd_b200_ctx* c, const float* params, size_t n) {
     });
 }
 
+// z-slab: the owned planes' types (host or device) into the local layout,
+// ghost planes = solid outside the domain, then the neighbours' planes
+void slab_stage_types(npsd_b200_ctx* c, const uint8_t* types, cudaMemcpyKind kind) {
+    const Geom& g = c->g0;
+    const size_t plane = (size_t)g.nx * g.ny;
+    uint8_t* d = reinterpret_cast<uint8_t*>(c->red_a);
+    CK(cudaMemsetAsync(d, 2, (size_t)g.n, c->s));
+    CK(cudaMemcpyAsync(d + (size_t)g.zo0 * plane, types, (size_t)(g.zo1 - g.zo0) * plane, kind, c->s));
+    slab_exchange(c, c->s, d, 1, 0);
+    set_mask_impl<3>(c, d);
+}
+
 int npsd_b200_set_mask_device(npsd_b200_ctx* c, const uint8_t* d_types) {
     return guarded(c, [&] {
         require(d_types != nullptr, "npsd_b200: cell types pointer is null");
+        if (c->slab.on) {
+            slab_stage_types(c, d_types, cudaMemcpyDeviceToDevice);
+            return;
+        }
         if (c->dim == 3)
             set_mask_impl<3>(c, d_types);
         else
@@ -1204,10 +1680,14 @@ int npsd_b200_set_mask_device(npsd_b200_ctx* c, const uint8_t* d_types) {
 int npsd_b200_set_mask(npsd_b200_ctx* c, const uint8_t* types) {
     return guarded(c, [&] {
         require(types != nullptr, "npsd_b200: cell types pointer is null");
-        const size_t n = (size_t)c->g0.n;
+        const size_t n = c->slab.on ? (size_t)(c->g0.zo1 - c->g0.zo0) * c->g0.nx * c->g0.ny : (size_t)c->g0.n;
         uint8_t worst = 0;  // plain loop: no per-element message construction
         for (size_t i = 0; i < n; ++i) worst = types[i] > worst ? types[i] : worst;
         require(worst <= 2, "npsd_b200: cell type out of range (0 fluid, 1 air, 2 solid)");
+        if (c->slab.on) {
+            slab_stage_types(c, types, cudaMemcpyHostToDevice);
+            return;
+        }
         uint8_t* d = reinterpret_cast<uint8_t*>(c->red_a);  // staging (n bytes <= 8n)
         CK(cudaMemcpyAsync(d, types, n, cudaMemcpyHostToDevice, c->s));
         if (c->dim == 3)
@@ -1227,12 +1707,15 @@ int npsd_b200_fluid_indices(npsd_b200_ctx* c, int64_t* out) {
         CK(cudaMemcpyAsync(mask.data(), c->fmask, mask.size() * 4, cudaMemcpyDeviceToHost, c->s));
         CK(cudaMemcpyAsync(base.data(), c->fbase, base.size() * 4, cudaMemcpyDeviceToHost, c->s));
         CK(cudaStreamSynchronize(c->s));
+        // z-slab: global linear indices (local plane zo0 is global plane z0)
+        const long long plane = (long long)c->g0.nx * c->g0.ny;
+        const long long shift = c->slab.on ? ((long long)c->slab.z0 - c->g0.zo0) * plane : 0;
         for (size_t sgm = 0; sgm < mask.size(); ++sgm) {
             uint32_t m = mask[sgm];
             long long k = base[sgm];
             while (m) {
                 const int b = __builtin_ctz(m);
-                out[k++] = (int64_t)(sgm * 32 + (size_t)b);
+                out[k++] = (int64_t)(sgm * 32 + (size_t)b) + shift;
                 m &= m - 1;
             }
         }
@@ -1247,7 +1730,17 @@ int npsd_b200_precond_apply(npsd_b200_ctx* c, const double* r, double* z, int64_
         const Geom g = c->g0;
         CK(cudaMemcpyAsync(c->red_a, r, (size_t)n_f * sizeof(double), cudaMemcpyHostToDevice, c->s));
         LAUNCH(c, c->s, k_scatter, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->red_a, c->R);
+        if (c->slab.on) {
+            // ||r|| over every rank, then r's ghost planes
+            const int flags[2] = {1, 0};  // dist, done
+            CK(cudaMemcpyAsync(&c->st->dist, &flags[0], sizeof(int), cudaMemcpyHostToDevice, c->s));
+            CK(cudaMemcpyAsync(&c->st->done, &flags[1], sizeof(int), cudaMemcpyHostToDevice, c->s));
+        }
         LAUNCH(c, c->s, k_norm_precond, g.n, g, c->R, c->st, c->partials, c->counter);
+        if (c->slab.on) {
+            slab_reduce(c, c->s, kFinNormPrecond);
+            slab_exchange(c, c->s, c->R, sizeof(double), 0);
+        }
         SolverState* h = c->st_host;
         // no cached directions: the fused dots in the L0 up kernel are empty
         const int zero = 0;
@@ -1268,6 +1761,7 @@ int npsd_b200_precond_apply(npsd_b200_ctx* c, const double* r, double* z, int64_
 int npsd_b200_spmv(npsd_b200_ctx* c, const double* x, double* y, int64_t n_f) {
     return guarded(c, [&] {
         check_mask(c);
+        require(!c->slab.on, "spmv: not available on a z-slab context");
         require(n_f == c->n_fluid, "spmv: dimension mismatch");
         if (n_f == 0) return;
         const Geom g = c->g0;
@@ -1290,6 +1784,7 @@ int npsd_b200_spmv(npsd_b200_ctx* c, const double* x, double* y, int64_t n_f) {
 int npsd_b200_net_apply(npsd_b200_ctx* c, const float* x, float* y) {
     return guarded(c, [&] {
         check_mask(c);
+        require(!c->slab.on, "net_apply: not available on a z-slab context");
         const size_t n = (size_t)c->g0.n;
         if (!c->xin_f) c->xin_f = dalloc<float>(n);
         if (!c->out_f) c->out_f = dalloc<float>(n);
@@ -1312,15 +1807,25 @@ int npsd_b200_psdo_solve_device(npsd_b200_ctx* c, const double* d_b, const doubl
         if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
         const Geom g = c->g0;
         const uint8_t* cls = c->L[0].cls;
+        // z-slab: caller buffers hold the owned planes only
+        const size_t off = (size_t)owned_lo(g), cnt = (size_t)(owned_hi(g) - owned_lo(g));
+        if (c->slab.on) {
+            CK(cudaMemcpyAsync(c->Bf + off, d_b, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
+            d_b = c->Bf;
+            if (d_x0) {
+                CK(cudaMemcpyAsync(c->X0 + off, d_x0, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
+                d_x0 = c->X0;
+            }
+        }
         LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_b, c->Bf);
         if (d_x0)
             LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_x0, c->X0);
         else
             CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
-        int st = (c->dim == 3) ? solve_device_impl<3>(c, cfg, rep) : solve_device_impl<2>(c, cfg, rep);
+        int st = solve_any(c, cfg, rep);
         (void)st;
         const double* xr = c->st_host->xcur ? c->X1 : c->X0;
-        CK(cudaMemcpyAsync(d_x, xr, (size_t)g.n * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
+        CK(cudaMemcpyAsync(d_x, xr + off, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
         CK(cudaStreamSynchronize(c->s));
     });
 }
@@ -1346,7 +1851,7 @@ int npsd_b200_psdo_solve(npsd_b200_ctx* c, const double* b, const double* x0, co
             CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
         }
         try {
-            (c->dim == 3) ? solve_device_impl<3>(c, cfg, rep) : solve_device_impl<2>(c, cfg, rep);
+            solve_any(c, cfg, rep);
         } catch (const Breakdown&) {
             const double* xr = c->st_host->xcur ? c->X1 : c->X0;
             LAUNCH(c, c->s, k_gather, g.n, g, cls, c->fmask, c->fbase, xr, c->red_b);
@@ -1364,6 +1869,7 @@ int npsd_b200_psdo_solve(npsd_b200_ctx* c, const double* b, const double* x0, co
 int npsd_b200_level_image(npsd_b200_ctx* c, int level, float* out) {
     return guarded(c, [&] {
         check_mask(c);
+        require(!c->slab.on, "level_image: not available on a z-slab context");
         require(level >= 0 && level < c->depth, "level out of range");
         const LevelBufs& L = c->L[level];
         if (level == 0) {
@@ -1453,6 +1959,7 @@ int npsd_b200_profile_iterations(npsd_b200_ctx* c, const double* d_b, const npsd
                                  double* ms_out, int* n_out, char* names, int name_len) {
     return guarded(c, [&] {
         check_mask(c);
+        require(!c->slab.on, "profile_iterations: not available on a z-slab context");
         require(cfg != nullptr && d_b != nullptr && iters > 0 && n_out != nullptr, "profile: bad arguments");
         if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
         const Geom g = c->g0;

@@ -38,8 +38,7 @@ __global__ void __launch_bounds__(kBlock) k_scatter(Geom g, const uint8_t* __res
                                                     const uint32_t* __restrict__ fmask,
                                                     const uint32_t* __restrict__ fbase, const double* __restrict__ red,
                                                     double* __restrict__ full) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
+    FOR_OWNED(g, c)
         full[c] = (cls_type(cls[c]) == 0) ? red[mixed_index(fmask, fbase, c)] : 0.0;
 }
 
@@ -47,21 +46,18 @@ __global__ void __launch_bounds__(kBlock) k_gather(Geom g, const uint8_t* __rest
                                                    const uint32_t* __restrict__ fmask,
                                                    const uint32_t* __restrict__ fbase, const double* __restrict__ full,
                                                    double* __restrict__ red) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
+    FOR_OWNED(g, c)
         if (cls_type(cls[c]) == 0) red[mixed_index(fmask, fbase, c)] = full[c];
 }
 
 __global__ void __launch_bounds__(kBlock) k_scatter_f32(Geom g, const float* __restrict__ src, float* __restrict__ dst) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) dst[c] = src[c];
+    FOR_OWNED(g, c) dst[c] = src[c];
 }
 
 // zero non-fluid entries (enforces the invariant on caller-provided full vectors)
 __global__ void __launch_bounds__(kBlock) k_mask_fluid(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ src,
                                                        double* __restrict__ dst) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
+    FOR_OWNED(g, c)
         dst[c] = (cls_type(cls[c]) == 0) ? src[c] : 0.0;
 }
 
@@ -69,8 +65,7 @@ __global__ void __launch_bounds__(kBlock) k_mask_fluid(Geom g, const uint8_t* __
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_spmv(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ v,
                                                  double* __restrict__ out) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    FOR_OWNED(g, c) {
         const uint8_t b = cls[c];
         if (cls_type(b) != 0) {
             out[c] = 0.0;
@@ -88,21 +83,27 @@ enum NormMode { kNormPrecond = 0, kNormMean = 1 };
 
 // Precond-only path: rnorm = ||r||, inv1 = 1/rnorm, inv2 = 1, nrm = rnorm
 // (NeuralPrecond::apply, net_precond.cpp:20-26).
+__device__ __forceinline__ void fin_norm_precond(SolverState* st, double rsq) {
+    const double rn = sqrt(rsq);
+    st->rnorm = rn;
+    st->inv1 = (rn == 0.0) ? 0.0 : 1.0 / rn;
+    st->inv2 = 1.0;
+    st->nrm = rn;
+}
+
 __global__ void __launch_bounds__(kBlock) k_norm_precond(Geom g, const double* __restrict__ r, SolverState* st,
                                                          double* __restrict__ partials, unsigned int* __restrict__ counter) {
     double acc[1] = {0.0};
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    FOR_OWNED(g, c) {
         const double v = r[c];
         acc[0] += v * v;
     }
     double tot[1];
     if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0) {
-        const double rn = sqrt(tot[0]);
-        st->rnorm = rn;
-        st->inv1 = (rn == 0.0) ? 0.0 : 1.0 / rn;
-        st->inv2 = 1.0;
-        st->nrm = rn;
+        if (st->dist)
+            st->part[0] = tot[0];
+        else
+            fin_norm_precond(st, tot[0]);
     }
 }
 
@@ -129,8 +130,7 @@ __global__ void __launch_bounds__(kBlock) k_fluid_sum(Geom g, const uint8_t* __r
                                                       long long n_fluid, SolverState* st, double* __restrict__ partials,
                                                       unsigned int* __restrict__ counter) {
     double acc[1] = {0.0};
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) acc[0] += v[c];
+    FOR_OWNED(g, c) acc[0] += v[c];
     double tot[1];
     if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0) st->mean = tot[0] / (double)n_fluid;
 }
@@ -140,8 +140,7 @@ __global__ void __launch_bounds__(kBlock) k_fluid_sum(Geom g, const uint8_t* __r
 __global__ void __launch_bounds__(kBlock) k_subtract_mean(Geom g, const uint8_t* __restrict__ cls, double* __restrict__ v,
                                                           const SolverState* __restrict__ st) {
     const double m = st->mean;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride)
+    FOR_OWNED(g, c)
         if (cls_type(cls[c]) == 0) v[c] = __dadd_rn(v[c], -m);
 }
 
@@ -151,8 +150,7 @@ __global__ void __launch_bounds__(kBlock) k_subtract_mean(Geom g, const uint8_t*
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_residual(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ b,
                                                      const double* __restrict__ x, double* __restrict__ r) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    FOR_OWNED(g, c) {
         const uint8_t bb = cls[c];
         if (cls_type(bb) != 0) continue;
         int xx, yy, zz;
@@ -214,121 +212,17 @@ __global__ void __launch_bounds__(kBlock) k_residual_norm(Geom g, const double* 
         return;
     }
     double acc[1] = {0.0};
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    FOR_OWNED(g, c) {
         const double v = r[c];
         acc[0] += v * v;
     }
     double tot[1];
-    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0)
-        finish_iteration(st, tot[0], hist, times, cond, use_cond, initial != 0);
-}
-
-// --------------------------------------------------------------- ortho
-// d' = d - p_1 d_1 - ... (MGS order, axpy_inplace form: d += (-p) * d_j),
-// Ad' by the stencil (halo values recomputed from d and the d_j), and the dots
-// d'.Ad', r.d' and d_j.Ad' (future cross terms). solver.cpp:239-251.
-template <int D>
-__global__ void __launch_bounds__(kBlock) k_ortho(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ dtmp,
-                                                  const double* __restrict__ r, double* __restrict__ Dring,
-                                                  double* __restrict__ ADring, SolverState* st,
-                                                  double* __restrict__ partials, unsigned int* __restrict__ counter) {
-    const int nc = st->n_cache, R = st->ring;
-    const int nw = (st->head + 1) % R;
-    const double* dj[kMaxOrtho];
-    double mp[kMaxOrtho];
-    for (int j = 0; j < kMaxOrtho; ++j) {
-        const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
-        dj[j] = Dring + (long long)slot * g.n;
-        mp[j] = (j < nc) ? -st->p[j] : 0.0;
+    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0) {
+        if (st->dist)
+            st->part[0] = tot[0];
+        else
+            finish_iteration(st, tot[0], hist, times, cond, use_cond, initial != 0);
     }
-    double* dnew = Dring + (long long)nw * g.n;
-    double* adnew = ADring + (long long)nw * g.n;
-    auto dprime = [&](long long q) {
-        double v = __ldg(dtmp + q);
-#pragma unroll
-        for (int j = 0; j < kMaxOrtho; ++j)
-            if (j < nc) v = __dadd_rn(v, __dmul_rn(mp[j], __ldg(dj[j] + q)));
-        return v;
-    };
-    constexpr int NV = 2 + kMaxOrtho;
-    double acc[NV];
-#pragma unroll
-    for (int j = 0; j < NV; ++j) acc[j] = 0.0;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
-        const uint8_t b = cls[c];
-        if (cls_type(b) != 0) continue;
-        int x, y, z;
-        decode(g, c, x, y, z);
-        const double dc = dprime(c);
-        const double ad = stencil_row<D>(g, x, y, z, cls_diag(b), dc, dprime);
-        dnew[c] = dc;
-        adnew[c] = ad;
-        acc[0] += dc * ad;
-        acc[1] += __ldg(r + c) * dc;
-#pragma unroll
-        for (int j = 0; j < kMaxOrtho; ++j)
-            if (j < nc) acc[2 + j] += __ldg(dj[j] + c) * ad;
-    }
-    double tot[NV];
-    if (grid_reduce<NV>(acc, partials, counter, tot) && threadIdx.x == 0) {
-        const double dAd = tot[0];
-        st->dAd_new = dAd;
-        st->rd_new = tot[1];
-        for (int j = 0; j < nc; ++j) {
-            const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
-            st->cross[slot][nw] = tot[2 + j];
-        }
-        if (!(dAd > 0.0) || fabs(dAd) < 1e-300) {
-            st->breakdown = 1;
-            st->done = 1;
-            st->bad_value = dAd;
-            st->alpha = 0.0;
-        } else {
-            st->alpha = tot[1] / dAd;
-        }
-    }
-}
-
-// ---------------------------------------------------------------- update
-// x' = x + alpha d' (axpy_inplace), r = b - A x' (explicit recompute,
-// solver.cpp:252-258), ||r||^2. x is ping-ponged so halo reads see the old x.
-template <int D>
-__global__ void __launch_bounds__(kBlock) k_update(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ b,
-                                                   double* __restrict__ X0, double* __restrict__ X1,
-                                                   const double* __restrict__ Dring, double* __restrict__ r,
-                                                   SolverState* st, double* __restrict__ hist, double* __restrict__ times,
-                                                   double* __restrict__ partials, unsigned int* __restrict__ counter,
-                                                   cudaGraphConditionalHandle cond, int use_cond, int do_norm) {
-    if (st->breakdown) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cond, use_cond, 0u);
-        return;
-    }
-    const double alpha = st->alpha;
-    const int nw = (st->head + 1) % st->ring;
-    const double* dn = Dring + (long long)nw * g.n;
-    const double* xo = st->xcur ? X1 : X0;
-    double* xn = st->xcur ? X0 : X1;
-    auto xnew = [&](long long q) { return __dadd_rn(__ldg(xo + q), __dmul_rn(alpha, __ldg(dn + q))); };
-    double acc[1] = {0.0};
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
-        const uint8_t bb = cls[c];
-        if (cls_type(bb) != 0) continue;
-        int x, y, z;
-        decode(g, c, x, y, z);
-        const double xc = xnew(c);
-        const double ax = stencil_row<D>(g, x, y, z, cls_diag(bb), xc, xnew);
-        const double rv = __dadd_rn(__ldg(b + c), -ax);
-        xn[c] = xc;
-        r[c] = rv;
-        acc[0] += rv * rv;
-    }
-    if (!do_norm) return;  // nullspace projection: norm after k_subtract_mean
-    double tot[1];
-    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0)
-        finish_iteration(st, tot[0], hist, times, cond, use_cond, false);
 }
 
 }  // namespace nb2

@@ -54,8 +54,11 @@ __global__ void __launch_bounds__(kBlock) k_setup_l0(Geom g, const uint8_t* __re
             }
             const int w = uniform ? t : 3;
             cls[c] = (uint8_t)(w | (t << 2) | (diag << 4) | ((int)wfluid << 7));
-            mixed = !uniform;
-            fluid = (t == 0);
+            // mixed / fluid masks count owned cells only (ghost planes are
+            // the neighbours' or the outside of the domain)
+            const bool owned = c >= owned_lo(g) && c < owned_hi(g);
+            mixed = !uniform && owned;
+            fluid = (t == 0) && owned;
         }
         const uint32_t mm = __ballot_sync(0xffffffffu, mixed);
         const uint32_t fm = __ballot_sync(0xffffffffu, fluid);
@@ -94,17 +97,18 @@ __global__ void __launch_bounds__(kBlock) k_tile_flags(Geom g, const uint8_t* __
 
 // Live unit range of each tile column for a Sched: a column covers cw x ch
 // flag tiles; unit u (planes [u * unit, (u + 1) * unit)) is live when a flag of
-// the column is set within zdil planes of it. Units outside [zlo, zlo + len)
+// the column is set within zdil planes of it; only owned planes [zo0, zo1)
+// are scheduled. Units outside [zlo, zlo + len)
 // have every input zero (their outputs are the zeros already in place).
 __global__ void __launch_bounds__(kBlock) k_sched_cols(const uint8_t* __restrict__ flags, int ftx, int fty, int nz,
-                                                       int cw, int ch, int ntx, int nty, int unit, int zdil,
-                                                       int* __restrict__ zlo, int* __restrict__ len) {
+                                                       int zo0, int zo1, int cw, int ch, int ntx, int nty, int unit,
+                                                       int zdil, int* __restrict__ zlo, int* __restrict__ len) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntx * nty) return;
     const int fx0 = (t % ntx) * cw, fy0 = (t / ntx) * ch;
     const int fx1 = min(fx0 + cw, ftx), fy1 = min(fy0 + ch, fty);
     int first = -1, last = -1;
-    for (int z = 0; z < nz; ++z) {
+    for (int z = max(zo0 - zdil, 0); z < min(zo1 + zdil, nz); ++z) {
         bool any = false;
         for (int fy = fy0; fy < fy1 && !any; ++fy)
             for (int fx = fx0; fx < fx1; ++fx) any |= flags[((long long)z * fty + fy) * ftx + fx] != 0;
@@ -118,8 +122,14 @@ __global__ void __launch_bounds__(kBlock) k_sched_cols(const uint8_t* __restrict
         len[t] = 0;
         return;
     }
-    const int u0 = max(first - zdil, 0) / unit;
-    const int u1 = min(last + zdil, nz - 1) / unit;
+    const int lo = max(first - zdil, zo0), hi = min(last + zdil, zo1 - 1);
+    if (lo > hi) {
+        zlo[t] = 0;
+        len[t] = 0;
+        return;
+    }
+    const int u0 = lo / unit;
+    const int u1 = hi / unit;
     zlo[t] = u0;
     len[t] = u1 - u0 + 1;
 }
@@ -191,7 +201,7 @@ __global__ void __launch_bounds__(kBlock) k_classify(Geom g, const float* __rest
                         uniform &= ((in ? pure(lin(g, xx, yy, zz)) : 2) == t);
                     }
             cls[c] = (uint8_t)(uniform ? t : 3);
-            mixed = !uniform;
+            mixed = !uniform && c >= owned_lo(g) && c < owned_hi(g);
         }
         const uint32_t mm = __ballot_sync(0xffffffffu, mixed);
         if ((threadIdx.x & 31) == 0) {
@@ -398,23 +408,24 @@ __global__ void k_kconst(const float* __restrict__ W, const float* __restrict__ 
 
 // Exact window-sum ingredients for linear_image_sums: per-channel integer
 // counts (value * scale, scale = 2^(D*level)) accumulated per boundary class
-// (per axis: first plane, interior, last plane).
+// (per axis: first plane, interior, last plane) over the owned cells; a z-slab
+// classifies by global plane (zg_off: global index of local plane 0, nzg: the
+// level's global plane count) so the ranks' counts add up to the full grid's.
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_zsums(Geom g, const uint8_t* __restrict__ src_types,
-                                                  const float* __restrict__ img, float scale,
+                                                  const float* __restrict__ img, float scale, int zg_off, int nzg,
                                                   unsigned long long* __restrict__ G) {
     constexpr int NC = (D == 3) ? 27 : 9;
     __shared__ unsigned long long sG[3 * NC];
     for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x) sG[i] = 0ull;
     __syncthreads();
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    FOR_OWNED(g, c) {
         const int x = (int)(c % g.nx);
         const int y = (int)((c / g.nx) % g.ny);
-        const int z = (int)(c / ((long long)g.nx * g.ny));
+        const int z = (int)(c / ((long long)g.nx * g.ny)) + zg_off;  // global plane
         const int kx = (x == 0) ? 0 : ((x == g.nx - 1) ? 2 : 1);
         const int ky = (y == 0) ? 0 : ((y == g.ny - 1) ? 2 : 1);
-        const int kz = (D == 3) ? ((z == 0) ? 0 : ((z == g.nz - 1) ? 2 : 1)) : 0;
+        const int kz = (D == 3) ? ((z == 0) ? 0 : ((z == nzg - 1) ? 2 : 1)) : 0;
         const int cl = (kz * 3 + ky) * 3 + kx;
         for (int ch = 0; ch < 3; ++ch) {
             unsigned long long v;

@@ -264,6 +264,29 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
     cp_wait<0>();
 }
 
+// d'.Ad' and r.d' -> alpha, or a breakdown (solver.cpp:245-251); d_j.Ad' are
+// the cross terms of the direction's future projections. tot = {d'Ad', r.d',
+// d_1.Ad', ...}.
+__device__ __forceinline__ void fin_ortho(SolverState* st, const double* tot) {
+    const int nc = st->n_cache, R = st->ring;
+    const int nw = (st->head + 1) % R;
+    const double dAd = tot[0];
+    st->dAd_new = dAd;
+    st->rd_new = tot[1];
+    for (int j = 0; j < nc && j < kMaxOrtho; ++j) {
+        const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
+        st->cross[slot][nw] = tot[2 + j];
+    }
+    if (!(dAd > 0.0) || fabs(dAd) < 1e-300) {
+        st->breakdown = 1;
+        st->done = 1;
+        st->bad_value = dAd;
+        st->alpha = 0.0;
+    } else {
+        st->alpha = tot[1] / dAd;
+    }
+}
+
 // d' = MGS(d); Ad'; dots d'.Ad', r.d', d_j.Ad'. NO = n_ortho (cache bound).
 template <int D, int NO>
 __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __restrict__ cls,
@@ -271,6 +294,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
                                                      double* __restrict__ Dring, double* __restrict__ ADring,
                                                      SolverState* st, double* __restrict__ partials,
                                                      unsigned int* __restrict__ counter, Sched sc) {
+    if (st->dist && st->done) return;
     const int nc = st->n_cache, R = st->ring;
     const int nw = (st->head + 1) % R;
     using Op = OrthoOp<NO>;
@@ -312,20 +336,10 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
     double tot[NV];
     if (grid_reduce<NV>(acc, partials, counter, tot)) {
         if (threadIdx.x == 0 && threadIdx.y == 0) {
-            const double dAd = tot[0];
-            st->dAd_new = dAd;
-            st->rd_new = tot[1];
-            for (int j = 0; j < nc && j < NO; ++j) {
-                const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
-                st->cross[slot][nw] = tot[2 + j];
-            }
-            if (!(dAd > 0.0) || fabs(dAd) < 1e-300) {
-                st->breakdown = 1;
-                st->done = 1;
-                st->bad_value = dAd;
-                st->alpha = 0.0;
+            if (st->dist) {
+                for (int j = 0; j < kPart; ++j) st->part[j] = (j < NV) ? tot[j] : 0.0;
             } else {
-                st->alpha = tot[1] / dAd;
+                fin_ortho(st, tot);
             }
         }
     }
@@ -346,6 +360,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
             set_cond(cond, use_cond, 0u);
         return;
     }
+    if (st->dist && st->done) return;
     const int nw = (st->head + 1) % st->ring;
     UpdateOp op;
     op.in[0] = st->xcur ? X1 : X0;
@@ -369,8 +384,12 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
     });
     if (!do_norm) return;
     double tot[1];
-    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0)
-        finish_iteration(st, tot[0], hist, times, cond, use_cond, false);
+    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0) {
+        if (st->dist)
+            st->part[0] = tot[0];
+        else
+            finish_iteration(st, tot[0], hist, times, cond, use_cond, false);
+    }
 }
 
 template <typename Op>
