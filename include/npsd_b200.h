@@ -157,6 +157,9 @@ int npsd_b200_comm_create_nccl(const void* id128, int rank, int nranks, int devi
 int npsd_b200_comm_create_local(int nranks, npsd_b200_comm** out);
 int npsd_b200_comm_destroy(npsd_b200_comm* comm);
 const char* npsd_b200_comm_last_error(void);
+/* 1 when the slab's last solve ran its iterations as captured chunk graphs
+ * (NCCL communicators), 0 for eager launches */
+int npsd_b200_slab_graph(const npsd_b200_ctx* c);
 int npsd_b200_create_slab(int nx, int ny, int nz, int z0, int nz_own, int depth, const float* params,
                           size_t n_params, int device, npsd_b200_comm* comm, int rank, npsd_b200_ctx** out);
 

@@ -260,6 +260,11 @@ class Context:
         self.h = h
         return self
 
+    @property
+    def slab_graph(self) -> bool:
+        """z-slab: the last solve's iterations ran as captured chunk graphs."""
+        return bool(self.lib.npsd_b200_slab_graph(self.h))
+
     def close(self) -> None:
         if getattr(self, "h", None):
             self.lib.npsd_b200_destroy(self.h)

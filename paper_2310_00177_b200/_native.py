@@ -22,7 +22,7 @@ EXPORTED_SYMBOLS = (
     "npsd_b200_launch_count", "npsd_b200_event_record", "npsd_b200_event_elapsed_ms",
     "npsd_b200_profile_iterations", "npsd_b200_save_npm", "npsd_b200_load_npm", "npsd_b200_npm_last_error",
     "npsd_b200_nccl_unique_id", "npsd_b200_comm_create_nccl", "npsd_b200_comm_create_local",
-    "npsd_b200_comm_destroy", "npsd_b200_comm_last_error", "npsd_b200_create_slab",
+    "npsd_b200_comm_destroy", "npsd_b200_comm_last_error", "npsd_b200_create_slab", "npsd_b200_slab_graph",
 )
 
 
@@ -65,6 +65,7 @@ def lib() -> C.CDLL:
     L.npsd_b200_comm_create_nccl.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
     L.npsd_b200_comm_create_local.argtypes = [C.c_int, C.POINTER(_vp)]
     L.npsd_b200_comm_destroy.argtypes = [_vp]
+    L.npsd_b200_slab_graph.argtypes = [_vp]
     L.npsd_b200_create_slab.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f32p, C.c_size_t,
                                         C.c_int, _vp, C.c_int, C.POINTER(_vp)]
     L.npsd_b200_npm_last_error.restype = C.c_char_p

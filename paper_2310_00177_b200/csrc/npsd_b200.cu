@@ -251,6 +251,7 @@ struct npsd_b200_ctx {
     Geom gglob[kMaxDepth] = {};   // the full grid per level (z-slab: all ranks)
     cudaGraphExec_t slab_exec = nullptr;  // z-slab: a chunk of iterations (NCCL ranks)
     int slab_exec_no = -1, slab_exec_k0 = -1;
+    bool slab_no_graph = false;   // the chunk graph could not be captured: eager chunks
     cudaStream_t s = nullptr, s2 = nullptr;
     std::vector<float> params;
     std::vector<LevelOffsets> offs;
@@ -1216,22 +1217,40 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
     slab_reduce(c, s, kFinNorm0);
     slab_exchange(c, s, c->R, sizeof(double), 0);
     const int K = slab_chunk(ring);
-    const bool graph = c->slab.comm->capturable();
+    bool graph = c->slab.comm->capturable() && !c->slab_no_graph;
     if (graph && (!c->slab_exec || c->slab_exec_no != no || c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist ||
                   c->exec_key[2] != c->ADring)) {
         if (c->slab_exec) CK(cudaGraphExecDestroy(c->slab_exec));
         c->slab_exec = nullptr;
-        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        for (long long k = 1; k <= K; ++k)
-            for (const auto& st : slab_body_steps<D>(c, no, k)) st.run(s);
-        cudaGraph_t gr = nullptr;
-        CK(cudaStreamEndCapture(s, &gr));
-        CK(cudaGraphInstantiate(&c->slab_exec, gr, 0));
-        CK(cudaGraphDestroy(gr));
-        c->slab_exec_no = no;
-        c->exec_key[0] = c->Dring;
-        c->exec_key[1] = c->hist;
-        c->exec_key[2] = c->ADring;
+        // the chunk: K iterations of kernels and NCCL calls in one graph; if the
+        // capture is refused, the chunk runs as eager launches instead
+        CK(cudaStreamSynchronize(s));
+        try {
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            try {
+                for (long long k = 1; k <= K; ++k)
+                    for (const auto& st : slab_body_steps<D>(c, no, k)) st.run(s);
+            } catch (...) {
+                cudaGraph_t junk = nullptr;
+                cudaStreamEndCapture(s, &junk);
+                if (junk) cudaGraphDestroy(junk);
+                throw;
+            }
+            cudaGraph_t gr = nullptr;
+            CK(cudaStreamEndCapture(s, &gr));
+            const cudaError_t ie = cudaGraphInstantiate(&c->slab_exec, gr, 0);
+            cudaGraphDestroy(gr);
+            CK(ie);
+            c->slab_exec_no = no;
+            c->exec_key[0] = c->Dring;
+            c->exec_key[1] = c->hist;
+            c->exec_key[2] = c->ADring;
+        } catch (const std::exception&) {
+            cudaGetLastError();
+            c->slab_exec = nullptr;
+            c->slab_no_graph = true;
+            graph = false;
+        }
     }
     for (long long k0 = 1;; k0 += K) {
         CK(cudaMemcpyAsync(&h->done, &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1632,6 +1651,10 @@ int npsd_b200_comm_destroy(npsd_b200_comm* comm) {
 }
 
 const char* npsd_b200_comm_last_error(void) { return g_comm_err.c_str(); }
+
+int npsd_b200_slab_graph(const npsd_b200_ctx* c) {
+    return (c && c->slab.on && c->slab_exec && !c->slab_no_graph) ? 1 : 0;
+}
 
 int npsd_b200_destroy(npsd_b200_ctx* c) {
     if (!c) return NPSD_OK;
