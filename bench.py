@@ -12,8 +12,11 @@ iteration, and per-iteration cost does not depend on weight values.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N > 1 (torchrun): replicas — every rank solves its own copy of the frame
-(weak scaling); the z-slab sharded path is not built yet.
+N > 1 (torchrun, one rank per GPU): the same frame z-slab sharded across the
+ranks (strong scaling): rank r owns a contiguous block of z-planes, ghost planes
+move over NCCL before each stencil / conv level, dot products are gathered and
+summed in rank order. `--slab` forces that path at N=1
+(a one-rank NCCL communicator) to exercise it on one GPU.
 """
 from __future__ import annotations
 
@@ -384,13 +387,163 @@ def run_b200(args) -> None:
         dist.destroy_process_group()
 
 
+# --------------------------------------------------------- B200 arm, z-slab
+def run_b200_slab(args, world: int, rank: int, local: int) -> None:
+    import threading
+
+    import torch
+    import torch.distributed as dist  # plumbing: NCCL id broadcast, barrier, max over ranks (gloo)
+
+    import paper_2310_00177_b200 as b200
+    from paper_2310_00177_b200 import scenes
+
+    # a rank that dies mid-collective must not hang the others forever
+    def watchdog():
+        time.sleep(args.watchdog_s)
+        print(json.dumps({"error": f"rank {rank}: watchdog after {args.watchdog_s} s"}), flush=True)
+        os._exit(3)
+
+    threading.Thread(target=watchdog, daemon=True).start()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    os.environ.setdefault("RANK", str(rank))
+    os.environ.setdefault("WORLD_SIZE", str(world))
+    if not dist.is_initialized():
+        dist.init_process_group("gloo")
+    uid = [b200.Comm.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = b200.Comm.nccl(uid[0], rank, world, device=local)
+
+    global args_config_name
+    args_config_name = args.config
+    types, seed = workload(args)
+    nz, ny, nx = types.shape
+    n_c = types.size
+    depth = args.depth
+    z0, nk = b200.partition(nz, world, depth)[rank]
+    own = np.ascontiguousarray(types[z0:z0 + nk])
+    params = b200.identity_params(depth) if args.weights == "identity" else b200.init_params(depth, 42)
+    ctx = b200.Context.slab(comm, rank, types.shape, z0, nk, params, device=local)
+    bfull = scenes.full_rhs(types, seed, b200.rhs_normal)
+    bown = np.ascontiguousarray(bfull.reshape(nz, ny, nx)[z0:z0 + nk]).reshape(-1)
+    cfg = b200.SolveConfig(tol_reduction=1e-6, max_iters=args.max_iters, n_ortho=2)
+    d_types = b200.DeviceBuffer(ctx, own.size)
+    d_b = b200.DeviceBuffer(ctx, bown.nbytes)
+    d_x = b200.DeviceBuffer(ctx, bown.nbytes)
+    d_types.upload(own.reshape(-1))
+    d_b.upload(bown)
+    ctx.synchronize()
+
+    def step():
+        ctx.event_record(0)
+        ctx.set_mask_device(d_types.ptr)
+        rep = ctx.psdo_solve_device(d_b.ptr, d_x.ptr, cfg)
+        ctx.event_record(1)
+        return ctx.event_elapsed_ms(0, 1), rep, ctx.last_solve_ms
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    ctx.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    launches0 = ctx.launch_count
+    ms, iters, solve_ms, converged = [], [], [], []
+    for _ in range(args.steps):
+        t, rep, sm = step()
+        ms.append(t)
+        iters.append(rep.iterations)
+        solve_ms.append(sm)
+        converged.append(rep.converged)
+    ctx.synchronize()
+    launches = (ctx.launch_count - launches0) / args.steps
+    clocks = clk.stop()
+
+    def max_over_ranks(v: float) -> float:
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    step_ms = max_over_ranks(float(np.mean(ms)))
+    per_iter_ms = max_over_ranks(float(np.mean([s / max(i, 1) for s, i in zip(solve_ms, iters)])))
+    solve_mean = max_over_ranks(float(np.mean(solve_ms)))
+    n_it = int(np.median(iters))
+
+    # end to end through the host API on every rank: pinned owned types and
+    # owned fluid entries in, owned solution out
+    n_f = int((own == 0).sum())
+    p_types = b200.PinnedBuffer(ctx, own.size, np.uint8)
+    p_b = b200.PinnedBuffer(ctx, n_f, np.float64)
+    p_x = b200.PinnedBuffer(ctx, n_f, np.float64)
+    p_types.array[:] = own.reshape(-1)
+    p_b.array[:] = bown[own.reshape(-1) == 0]
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        dist.barrier()
+        t0 = time.perf_counter()
+        ctx.set_mask(p_types.array)
+        res = ctx.psdo_solve(p_b.array, cfg, out=p_x.array)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e.append(1e3 * (t1 - t0))
+    e2e_ms = max_over_ranks(float(np.mean(e2e)))
+    hist_bytes = 8 * (res.report.iterations + 1) * 2
+    model = canonical_bytes_per_cell(depth)
+    b_iter = sum(model.values()) * n_c  # whole grid, all ranks
+    peaks = load_peaks()
+    agg_gbs = b_iter / (per_iter_ms * 1e-3) / 1e9
+    peak_all = world * peaks["hbm_gbs"]
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": step_ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64 solver / f32 network", "data": "synthetic",
+            "config": {
+                "workload": f"{args.config} {nz}^3 (SURVEY §8d), one frame per step: set_mask + PSDO to rel-res 1e-6, "
+                            f"z-slab sharded over {world} GPU(s)",
+                "depth": depth, "n_ortho": 2, "weights": args.weights, "iterations": n_it,
+                "converged": bool(all(converged)), "parallelism": f"zslab{world}",
+                "slabs": b200.partition(nz, world, depth), "chunk_graphs": ctx.slab_graph,
+                "l2": "inputs larger than L2 (solver vectors 8 B x n_c each)",
+            },
+            "per_iter_ms": per_iter_ms,
+            "setup_ms": step_ms - solve_mean,
+            "hbm_gbs_iteration": agg_gbs,
+            "iteration_roofline": {"bound": "hbm", "achieved": agg_gbs, "peak": peak_all, "unit": "GB/s",
+                                   "frac": agg_gbs / peak_all,
+                                   "bytes": f"canonical B_iter = {sum(model.values()):.2f} B x n_c (SURVEY §8d), "
+                                            "whole grid over all ranks",
+                                   "peak_source": f"{world} x {peaks['source']}"},
+            "roofline": {"bound": "hbm", "kernel": "whole iteration (all ranks)", "achieved": agg_gbs,
+                         "peak": peak_all, "unit": "GB/s", "frac": agg_gbs / peak_all, "traffic": None,
+                         "peak_source": f"{world} x {peaks['source']}"},
+            "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(own.size + 8 * n_f),
+                    "d2h_bytes_per_step": int(8 * n_f + hist_bytes),
+                    "how": "per rank: Context.set_mask(pinned owned types) + psdo_solve(pinned owned b) -> pinned x; "
+                           "host wall clock, max over ranks (rank 0's slab bytes)"},
+            "gpu_launches": int(round(launches)),
+            "clocks": clocks,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    for buf in (d_types, d_b, d_x):
+        buf.free()
+    for buf in (p_types, p_b, p_x):
+        buf.free()
+    ctx.close()
+    dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+    os._exit(0)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
     ap.add_argument("--n", type=int, default=None, help="override the grid size of the config")
     ap.add_argument("--depth", type=int, default=4)
     ap.add_argument("--weights", default="identity", choices=["identity", "random"])
@@ -399,9 +552,15 @@ def main() -> None:
     ap.add_argument("--cpu-sample-iters", type=int, default=2)
     ap.add_argument("--ref-iters", type=int, default=1000, help="iterations-to-solution if no fixture exists")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true", help="z-slab path even at N=1 (one-rank NCCL)")
+    ap.add_argument("--watchdog-s", type=float, default=900.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.slab:
+        run_b200_slab(args, world, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")))
     else:
         run_b200(args)
 

@@ -252,6 +252,7 @@ struct npsd_b200_ctx {
     cudaGraphExec_t slab_exec = nullptr;  // z-slab: a chunk of iterations (NCCL ranks)
     int slab_exec_no = -1, slab_exec_k0 = -1;
     bool slab_no_graph = false;   // the chunk graph could not be captured: eager chunks
+    long long slab_chunk_launches = 0;
     cudaStream_t s = nullptr, s2 = nullptr;
     std::vector<float> params;
     std::vector<LevelOffsets> offs;
@@ -368,12 +369,14 @@ void slab_allreduce_u64(npsd_b200_ctx* c, cudaStream_t s, unsigned long long* v,
     c->slab.comm->allgather(c->slab.rank, s, v, c->slab.allu, (size_t)k * sizeof(unsigned long long));
     k_sum_u64<<<1, 128, 0, s>>>(c->slab.allu, c->slab.nranks, k, v);
     CK(cudaGetLastError());
+    ++c->launches;
 }
 
 void slab_reduce(npsd_b200_ctx* c, cudaStream_t s, int kind) {
     c->slab.comm->allgather(c->slab.rank, s, c->st->part, c->slab.all, kPart * sizeof(double));
     k_finalize<<<1, 32, 0, s>>>(kind, c->st, c->slab.all, c->slab.nranks, c->hist, c->times);
     CK(cudaGetLastError());
+    ++c->launches;
 }
 
 void compute_offsets(npsd_b200_ctx* c) {
@@ -1227,9 +1230,12 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
         CK(cudaStreamSynchronize(s));
         try {
             CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            const long long before = c->launches;
             try {
                 for (long long k = 1; k <= K; ++k)
                     for (const auto& st : slab_body_steps<D>(c, no, k)) st.run(s);
+                c->slab_chunk_launches = c->launches - before;  // kernels per chunk replay
+                c->launches = before;                            // captured, not executed
             } catch (...) {
                 cudaGraph_t junk = nullptr;
                 cudaStreamEndCapture(s, &junk);
@@ -1258,6 +1264,7 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
         if (h->done) break;
         if (graph) {
             CK(cudaGraphLaunch(c->slab_exec, s));
+            c->launches += c->slab_chunk_launches;
         } else {
             for (long long k = k0; k < k0 + K; ++k)
                 for (const auto& st : slab_body_steps<D>(c, no, k)) st.run(s);
