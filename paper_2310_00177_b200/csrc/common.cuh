@@ -291,25 +291,27 @@ __device__ __forceinline__ bool region_has_fluid(const uint8_t* __restrict__ fla
     return __syncthreads_or(any) != 0;
 }
 
-// Balanced schedule over the live L0 tile columns (setup.cuh k_sched_cols):
-// column t = ty * ntx + tx holds units [zlo[t], zlo[t] + pre[t+1] - pre[t])
+// Balanced schedule over the live L0 tile columns (setup.cuh k_col_range,
+// k_sched_pieces): piece p = chunk * ncol + t, column t = ty * ntx + tx,
+// holds units [zlo[t], zlo[t] + pre[t+1] - pre[t])
 // (a unit = `unit` planes). The pre[ncol] live units are split evenly over the
 // blocks of a one-wave 1D grid, so the work is balanced whatever the geometry
 // and the grid never runs a second, mostly idle wave.
 struct Sched {
-    const int* pre;  // [ncol + 1] exclusive prefix of the live lengths
-    const int* zlo;  // [ncol] first live unit
-    int ncol, ntx;
+    const int* pre;  // [npiece + 1] exclusive prefix of the live lengths
+    const int* zlo;  // [npiece] first live unit
+    int npiece;      // pieces p = chunk * ncol + column
+    int ncol, ntx;   // columns x fastest: t = ty * ntx + tx
 };
 
 // f(tx, ty, u0, u1) for each column segment of this block's share (block-uniform)
 template <typename F>
 __device__ __forceinline__ void sched_for_each(const Sched& sc, F f) {
-    const long long W = sc.pre[sc.ncol];
+    const long long W = sc.pre[sc.npiece];
     long long s = W * blockIdx.x / gridDim.x;
     const long long e = W * (blockIdx.x + 1) / gridDim.x;
     if (s >= e) return;
-    int lo = 0, hi = sc.ncol - 1;  // last column with pre[t] <= s
+    int lo = 0, hi = sc.npiece - 1;  // last piece with pre[t] <= s
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (sc.pre[mid] <= s)
@@ -322,7 +324,8 @@ __device__ __forceinline__ void sched_for_each(const Sched& sc, F f) {
         if (cend <= s) continue;
         const long long n = min(cend, e) - s;
         const int u0 = sc.zlo[t] + (int)(s - sc.pre[t]);
-        f(t % sc.ntx, t / sc.ntx, u0, u0 + (int)n);
+        const int col = t % sc.ncol;
+        f(col % sc.ntx, col / sc.ntx, u0, u0 + (int)n);
         s += n;
     }
 }

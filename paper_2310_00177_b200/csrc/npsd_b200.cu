@@ -84,9 +84,9 @@ struct LevelBufs {
 
 // one balanced schedule (common.cuh Sched) over L0 tile columns
 struct SchedBufs {
-    int *pre = nullptr, *zlo = nullptr, *len = nullptr;
-    int ncol = 0, ntx = 0;
-    Sched view() const { return Sched{pre, zlo, ncol, ntx}; }
+    int *pre = nullptr, *zlo = nullptr, *len = nullptr, *first = nullptr, *last = nullptr;
+    int ncol = 0, ntx = 0, nchunk = 0, hu = 0, npiece = 0;
+    Sched view() const { return Sched{pre, zlo, npiece, ncol, ntx}; }
 };
 
 // offsets of one level's blocks inside the flat parameter vector
@@ -479,19 +479,38 @@ ConvTab tab_up(const npsd_b200_ctx* c, int l) {
 // the prefix. Sizes are fixed per context; buffers are made on first use.
 void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int zdil) {
     const int ntx = (c->g0.nx + tx - 1) / tx, nty = (c->g0.ny + ty - 1) / ty;
+    // one piece per column: chunking columns into z pieces (chunk-major, so
+    // halo rows come from L2) was measured slower — every piece restarts the
+    // pipeline — so a piece is a whole column's live range
+    const int hu = c->g0.nz / unit + 1;
+    const int nchunk = 1;
     if (!sb.pre) {
         sb.ncol = ntx * nty;
         sb.ntx = ntx;
-        sb.pre = dalloc<int>((size_t)sb.ncol + 1);
-        sb.zlo = dalloc<int>((size_t)sb.ncol);
-        sb.len = dalloc<int>((size_t)sb.ncol);
+        sb.nchunk = nchunk;
+        sb.hu = hu;
+        sb.npiece = sb.ncol * nchunk;
+        sb.pre = dalloc<int>((size_t)sb.npiece + 1);
+        sb.zlo = dalloc<int>((size_t)sb.npiece);
+        sb.len = dalloc<int>((size_t)sb.npiece);
+        sb.first = dalloc<int>((size_t)sb.ncol);
+        sb.last = dalloc<int>((size_t)sb.ncol);
     }
-    const int nb = (sb.ncol + kBlock - 1) / kBlock;
-    k_sched_cols<<<nb, kBlock, 0, c->s>>>(c->tflags, c->tf_ntx, c->tf_nty, c->g0.nz, c->g0.zo0, c->g0.zo1,
-                                          tx / kFlagTX, ty / kFlagTY, ntx, nty, unit, zdil, sb.zlo, sb.len);
-    k_sched_prefix<<<1, 32, 0, c->s>>>(sb.len, sb.ncol, sb.pre);
+    const Geom& g = c->g0;
+    k_col_range<<<(sb.ncol * 32 + kBlock - 1) / kBlock, kBlock, 0, c->s>>>(
+        c->tflags, c->tf_ntx, c->tf_nty, g.nz, g.zo0, g.zo1, tx / kFlagTX, ty / kFlagTY, ntx, nty, zdil, sb.first,
+        sb.last);
+    k_sched_pieces<<<(sb.npiece + kBlock - 1) / kBlock, kBlock, 0, c->s>>>(sb.first, sb.last, sb.ncol, sb.nchunk, sb.hu,
+                                                                         g.zo0, g.zo1, unit, zdil, sb.zlo, sb.len);
     CK(cudaGetLastError());
     c->launches += 2;
+    // exclusive prefix (lengths are non-negative: scanned as u32), then the total
+    auto* len = reinterpret_cast<uint32_t*>(sb.len);
+    auto* pre = reinterpret_cast<uint32_t*>(sb.pre);
+    scan_u32(c, len, pre, sb.npiece);
+    k_seg_total<<<1, 32, 0, c->s>>>(pre, len, sb.npiece, pre + sb.npiece);
+    CK(cudaGetLastError());
+    ++c->launches;
 }
 
 // one wave of k's blocks (the schedule's grid)
@@ -1346,6 +1365,8 @@ void free_ctx(npsd_b200_ctx* c) {
         F(sb->pre);
         F(sb->zlo);
         F(sb->len);
+        F(sb->first);
+        F(sb->last);
     }
     for (auto& L : c->L) {
         F(L.cls);

@@ -12,6 +12,8 @@
 // tab[slot * cap + mixed_index].
 #pragma once
 
+#include <climits>
+
 #include "common.cuh"
 
 namespace nb2 {
@@ -95,43 +97,56 @@ __global__ void __launch_bounds__(kBlock) k_tile_flags(Geom g, const uint8_t* __
     }
 }
 
-// Live unit range of each tile column for a Sched: a column covers cw x ch
-// flag tiles; unit u (planes [u * unit, (u + 1) * unit)) is live when a flag of
-// the column is set within zdil planes of it; only owned planes [zo0, zo1)
-// are scheduled. Units outside [zlo, zlo + len)
-// have every input zero (their outputs are the zeros already in place).
-__global__ void __launch_bounds__(kBlock) k_sched_cols(const uint8_t* __restrict__ flags, int ftx, int fty, int nz,
-                                                       int zo0, int zo1, int cw, int ch, int ntx, int nty, int unit,
-                                                       int zdil, int* __restrict__ zlo, int* __restrict__ len) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+// Live plane range of each tile column (a column covers cw x ch flag tiles):
+// first / last plane in [zo0 - zdil, zo1 + zdil) whose flags are set, or -1.
+// One warp per column, planes lane-strided.
+__global__ void __launch_bounds__(kBlock) k_col_range(const uint8_t* __restrict__ flags, int ftx, int fty, int nz,
+                                                      int zo0, int zo1, int cw, int ch, int ntx, int nty, int zdil,
+                                                      int* __restrict__ first, int* __restrict__ last) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (t >= ntx * nty) return;
-    const int fx0 = (t % ntx) * cw, fy0 = (t / ntx) * ch;
+    const int fx0 = (t % ntx) * cw, fy0 = (t / ntx) * ch;  // x fastest (common.cuh Sched)
     const int fx1 = min(fx0 + cw, ftx), fy1 = min(fy0 + ch, fty);
-    int first = -1, last = -1;
-    for (int z = max(zo0 - zdil, 0); z < min(zo1 + zdil, nz); ++z) {
+    int lo = INT_MAX, hi = -1;
+    for (int z = max(zo0 - zdil, 0) + lane; z < min(zo1 + zdil, nz); z += 32) {
         bool any = false;
         for (int fy = fy0; fy < fy1 && !any; ++fy)
             for (int fx = fx0; fx < fx1; ++fx) any |= flags[((long long)z * fty + fy) * ftx + fx] != 0;
         if (any) {
-            if (first < 0) first = z;
-            last = z;
+            lo = min(lo, z);
+            hi = max(hi, z);
         }
     }
-    if (first < 0) {
-        zlo[t] = 0;
-        len[t] = 0;
-        return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    const int lo = max(first - zdil, zo0), hi = min(last + zdil, zo1 - 1);
-    if (lo > hi) {
-        zlo[t] = 0;
-        len[t] = 0;
-        return;
+    if (lane == 0) {
+        first[t] = (hi < 0) ? -1 : lo;
+        last[t] = hi;
     }
-    const int u0 = lo / unit;
-    const int u1 = hi / unit;
-    zlo[t] = u0;
-    len[t] = u1 - u0 + 1;
+}
+
+// Schedule pieces: piece p = c * ncol + t is column t's live units within
+// chunk c (units [c * hu, (c + 1) * hu); a unit = `unit` planes). Chunk-major
+// order (build_sched uses a single chunk: chunked orders measured slower).
+// Units are live within zdil planes of a set flag, and owned.
+__global__ void __launch_bounds__(kBlock) k_sched_pieces(const int* __restrict__ first, const int* __restrict__ last,
+                                                         int ncol, int nchunk, int hu, int zo0, int zo1, int unit,
+                                                         int zdil, int* __restrict__ zlo, int* __restrict__ len) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= ncol * nchunk) return;
+    const int t = p % ncol, c = p / ncol;
+    zlo[p] = 0;
+    len[p] = 0;
+    if (first[t] < 0) return;
+    const int lo = max(first[t] - zdil, zo0), hi = min(last[t] + zdil, zo1 - 1);
+    if (lo > hi) return;
+    const int u0 = max(lo / unit, c * hu), u1 = min(hi / unit, (c + 1) * hu - 1);
+    if (u0 > u1) return;
+    zlo[p] = u0;
+    len[p] = u1 - u0 + 1;
 }
 
 __global__ void k_sched_prefix(const int* __restrict__ len, int n, int* __restrict__ pre) {
