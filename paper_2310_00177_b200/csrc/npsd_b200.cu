@@ -674,7 +674,7 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
             const double scale = std::ldexp(1.0, D * l);
             LAUNCH(c, s, k_zsums<D>, L.g.n, L.g, st, im, (float)scale, zg_offset(c, l), c->gglob[l].nz, L.zG);
             if (c->slab.on) slab_allreduce_u64(c, s, L.zG, 3 * NC);
-            k_zfinal<D><<<1, 32, 0, s>>>(c->gglob[l], L.zG, scale, c->d_params + o.a_K, c->params[o.a_bias],
+            k_zfinal<D><<<1, 128, 0, s>>>(c->gglob[l], L.zG, scale, c->d_params + o.a_K, c->params[o.a_bias],
                                          c->d_params + o.b_K, c->params[o.b_bias], c->zab + 2 * l, c->zab + 2 * l + 1);
             CK(cudaGetLastError());
             ++c->launches;

@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(Geom g, const uint8_t* __
     constexpr int S = Sh<D>::S;
     __shared__ float sW[S * 3 * S];
     __shared__ float sB[S];
+    if ((long long)blockIdx.x * blockDim.x >= (long long)*count) return;  // grid sized for the capacity
     for (int i = threadIdx.x; i < S * 3 * S; i += blockDim.x) sW[i] = W[i];
     for (int i = threadIdx.x; i < S; i += blockDim.x) sB[i] = B[i];
     __syncthreads();
@@ -434,6 +435,10 @@ __global__ void __launch_bounds__(kBlock) k_zsums(Geom g, const uint8_t* __restr
     __shared__ unsigned long long sG[3 * NC];
     for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x) sG[i] = 0ull;
     __syncthreads();
+    // interior cells (the all-interior class, nearly every cell) are counted
+    // in registers and reduced per warp; boundary cells go to shared atomics
+    constexpr int kInterior = (D == 3) ? 13 : 4;
+    unsigned long long inner[3] = {0ull, 0ull, 0ull};
     FOR_OWNED(g, c) {
         const int x = (int)(c % g.nx);
         const int y = (int)((c / g.nx) % g.ny);
@@ -448,8 +453,17 @@ __global__ void __launch_bounds__(kBlock) k_zsums(Geom g, const uint8_t* __restr
                 v = (src_types[c] == ch) ? 1ull : 0ull;
             else
                 v = (unsigned long long)__fmul_rn(img[ch * g.n + c], scale);
-            if (v) atomicAdd(&sG[ch * NC + cl], v);
+            if (cl == kInterior)
+                inner[ch] += v;
+            else if (v)
+                atomicAdd(&sG[ch * NC + cl], v);
         }
+    }
+    for (int ch = 0; ch < 3; ++ch) {
+        unsigned long long v = inner[ch];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sG[ch * NC + kInterior], v);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x)
@@ -464,31 +478,37 @@ __global__ void k_zfinal(Geom g, const unsigned long long* __restrict__ G, doubl
                          float* __restrict__ za_out, float* __restrict__ zb_out) {
     constexpr int S = Sh<D>::S;
     constexpr int NC = (D == 3) ? 27 : 9;
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    float F[3 * S];
-    for (int ch = 0; ch < 3; ++ch)
-        for (int t = 0; t < S; ++t) {
-            const int d[3] = {t % 3 - 1, (t / 3) % 3 - 1, (D == 3) ? t / 9 - 1 : 0};
-            unsigned long long cnt = 0;
-            for (int cl = 0; cl < NC; ++cl) {
-                const int k[3] = {cl % 3, (cl / 3) % 3, cl / 9};
-                bool ok = true;
-                for (int a = 0; a < D; ++a) {
-                    if (d[a] == 1 && k[a] == 0) ok = false;   // q_a = p_a + 1 never hits plane 0
-                    if (d[a] == -1 && k[a] == 2) ok = false;  // q_a = p_a - 1 never hits plane n-1
-                }
-                if (ok) cnt += G[ch * NC + cl];
+    __shared__ unsigned long long sG[3 * NC];
+    __shared__ float F[3 * S];
+    for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x) sG[i] = G[i];
+    __syncthreads();
+    // one thread per (channel, tap): F = the exact count of the shifted box
+    for (int i = threadIdx.x; i < 3 * S; i += blockDim.x) {
+        const int ch = i / S, t = i % S;
+        const int d[3] = {t % 3 - 1, (t / 3) % 3 - 1, (D == 3) ? t / 9 - 1 : 0};
+        unsigned long long cnt = 0;
+        for (int cl = 0; cl < NC; ++cl) {
+            const int k[3] = {cl % 3, (cl / 3) % 3, cl / 9};
+            bool ok = true;
+            for (int a = 0; a < D; ++a) {
+                if (d[a] == 1 && k[a] == 0) ok = false;   // q_a = p_a + 1 never hits plane 0
+                if (d[a] == -1 && k[a] == 2) ok = false;  // q_a = p_a - 1 never hits plane n-1
             }
-            double f = (double)cnt / scale;
-            if (ch == 2) {
-                // ring (solid) cells inside the shifted box
-                const long long dims[3] = {g.nx, g.ny, g.nz};
-                long long inside = 1;
-                for (int a = 0; a < 3; ++a) inside *= dims[a] - ((a < D) ? (d[a] != 0 ? 1 : 0) : 0);
-                f += (double)(g.n - inside);
-            }
-            F[ch * S + t] = (float)f;
+            if (ok) cnt += sG[ch * NC + cl];
         }
+        double f = (double)cnt / scale;
+        if (ch == 2) {
+            // ring (solid) cells inside the shifted box
+            const long long dims[3] = {g.nx, g.ny, g.nz};
+            long long inside = 1;
+            for (int a = 0; a < 3; ++a) inside *= dims[a] - ((a < D) ? (d[a] != 0 ? 1 : 0) : 0);
+            f += (double)(g.n - inside);
+        }
+        F[i] = (float)f;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    // z = bias + sum_t (norm * K[t]) * F[t], serial in t (forward.hpp:78-86)
     const float norm = __fdiv_rn(1.0f, __fmul_rn((float)S, __ll2float_rn(g.n)));
     float za = biasA, zb = biasB;
     for (int t = 0; t < 3 * S; ++t) {
