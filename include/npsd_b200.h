@@ -134,6 +134,22 @@ int npsd_b200_init_params(int dim, int depth, uint64_t seed, float* out);
 int npsd_b200_identity_params(int dim, int depth, float* out);
 void npsd_b200_rhs_normal(uint64_t seed, int64_t n, double* out);
 
+/* Right-hand side from a MAC velocity field, replacing mac_divergence_rhs
+ * (discretization.cpp:193-227) + reduce: b = -(rho*h/dt) * (signed sum of face
+ * velocities) at fluid cells, a face whose opposite cell is solid (or outside
+ * the domain) taking the boundary value (bc arrays NULL: 0). 3D adds w faces
+ * (the reference is 2D only). Face arrays x fastest: u (nx+1, ny, nz),
+ * v (nx, ny+1, nz), w (nx, ny, nz+1); 2D passes w = bc_w = NULL. Needs the
+ * frame's set_mask. Host variant: b_reduced (n_fluid entries, the solve's
+ * ordering). Device variant: d_b_full on the full grid (zeros off fluid), the
+ * input of psdo_solve_device — flags + velocity -> solve without leaving HBM. */
+int npsd_b200_mac_divergence_rhs(npsd_b200_ctx* ctx, const double* u, const double* v, const double* w, double h,
+                                 double dt, double rho, const double* bc_u, const double* bc_v, const double* bc_w,
+                                 double* b_reduced);
+int npsd_b200_mac_divergence_rhs_device(npsd_b200_ctx* ctx, const double* d_u, const double* d_v, const double* d_w,
+                                        double h, double dt, double rho, const double* d_bc_u, const double* d_bc_v,
+                                        const double* d_bc_w, double* d_b_full);
+
 /* z-slab decomposition across GPUs ("Multi-GPU"): one process
  * (or, for tests, one host thread) and one context per rank; rank r owns
  * global planes [z0, z0 + nz_own) of an nx x ny x nz grid (3D, depth >= 2;

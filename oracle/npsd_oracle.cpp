@@ -186,6 +186,48 @@ int oracle_ctx_precond_apply(void* h, const double* r, double* z) {
 }
 
 // reduced A·x (assemble_poisson[_3d] + reduce + spmv)
+// mac_divergence_rhs (discretization.cpp:193-227), restated on cell types and
+// generalised to 3D: b = scale * (((uR - uL) + (vT - vB)) + (wF - wB)) at fluid
+// cells (2D: the first two terms), scale = -(rho * h) / dt; a face whose
+// opposite cell is solid (or outside the domain) takes the boundary value
+// (0 without one); non-fluid cells 0. Face arrays x fastest: u (nx+1, ny, nz),
+// v (nx, ny+1, nz), w (nx, ny, nz+1).
+int oracle_mac_rhs(int D, long nx, long ny, long nz, const unsigned char* types, const double* u, const double* v,
+                   const double* w, double h, double dt, double rho, const double* bu, const double* bv,
+                   const double* bw, double* b) {
+    return guarded([&] {
+        if (D == 2) nz = 1;
+        auto solid = [&](long x, long y, long z) {
+            if (x < 0 || x >= nx || y < 0 || y >= ny || z < 0 || z >= nz) return true;
+            return types[(z * ny + y) * nx + x] == 2;
+        };
+        auto ui = [&](long x, long y, long z) { return (z * ny + y) * (nx + 1) + x; };
+        auto vi = [&](long x, long y, long z) { return (z * (ny + 1) + y) * nx + x; };
+        auto wi = [&](long x, long y, long z) { return (z * ny + y) * nx + x; };
+        const double scale = -(rho * h) / dt;
+        for (long z = 0; z < nz; ++z)
+            for (long y = 0; y < ny; ++y)
+                for (long x = 0; x < nx; ++x) {
+                    const long c = (z * ny + y) * nx + x;
+                    if (types[c] != 0) {
+                        b[c] = 0.0;
+                        continue;
+                    }
+                    const double uR = solid(x + 1, y, z) ? (bu ? bu[ui(x + 1, y, z)] : 0.0) : u[ui(x + 1, y, z)];
+                    const double uL = solid(x - 1, y, z) ? (bu ? bu[ui(x, y, z)] : 0.0) : u[ui(x, y, z)];
+                    const double vT = solid(x, y + 1, z) ? (bv ? bv[vi(x, y + 1, z)] : 0.0) : v[vi(x, y + 1, z)];
+                    const double vB = solid(x, y - 1, z) ? (bv ? bv[vi(x, y, z)] : 0.0) : v[vi(x, y, z)];
+                    double div = (uR - uL) + (vT - vB);
+                    if (D == 3) {
+                        const double wF = solid(x, y, z + 1) ? (bw ? bw[wi(x, y, z + 1)] : 0.0) : w[wi(x, y, z + 1)];
+                        const double wB = solid(x, y, z - 1) ? (bw ? bw[wi(x, y, z)] : 0.0) : w[wi(x, y, z)];
+                        div = div + (wF - wB);
+                    }
+                    b[c] = scale * div;
+                }
+    });
+}
+
 // y = A x on the reduced system of a cell-type grid, without a network
 // context (matrix-free PoissonOp; large-grid residual checks)
 int oracle_spmv(int D, long nx, long ny, long nz, const unsigned char* types, const double* x, double* y) {

@@ -137,6 +137,25 @@ int ref_init_params_2d(int depth, unsigned long long seed, float* out) {
     });
 }
 
+// the reference's mac_divergence_rhs (2D) on a cell-type grid, full-grid output
+int ref_mac_rhs_2d(long nx, long ny, const unsigned char* types, const double* u, const double* v, double h,
+                   double dt, double rho, const double* bu, const double* bv, double* out) {
+    return guarded([&] {
+        npsd::MacVelocity vel(nx, ny, h, dt, rho);
+        std::memcpy(vel.u.data.data(), u, vel.u.data.size() * sizeof(double));
+        std::memcpy(vel.v.data.data(), v, vel.v.data.size() * sizeof(double));
+        npsd::BoundaryVelocity bc;
+        if (bu) {
+            bc.u = vel.u;
+            bc.v = vel.v;
+            std::memcpy(bc.u.data.data(), bu, bc.u.data.size() * sizeof(double));
+            std::memcpy(bc.v.data.data(), bv, bc.v.data.size() * sizeof(double));
+        }
+        const auto b = npsd::mac_divergence_rhs(vel, image_from_types(nx, ny, types), bu ? &bc : nullptr);
+        std::memcpy(out, b.data(), b.size() * sizeof(double));
+    });
+}
+
 // the reference's own model-file writer / reader (net_params.cpp:42-78)
 int ref_save_npm_2d(int depth, unsigned long long seed, const char* path) {
     return guarded([&] { npsd::net::save_npm(npsd::net::init_params(depth, seed), path); });

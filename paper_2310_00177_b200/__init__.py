@@ -260,6 +260,29 @@ class Context:
         self.h = h
         return self
 
+    def mac_divergence_rhs(self, u, v, w=None, h: float = 1.0, dt: float = 0.05, rho: float = 1.0,
+                           bc=None) -> np.ndarray:
+        """mac_divergence_rhs + reduce (discretization.cpp:193-227) on the
+        device for this frame: the solve's reduced b. Faces x fastest (numpy
+        shapes (nz, ny, nx+1), (nz, ny+1, nx), (nz+1, ny, nx)); bc = (bu, bv[,
+        bw]) prescribed normal velocities on solid faces, or None (zero)."""
+        arrs = [np.ascontiguousarray(a, np.float64) if a is not None else None
+                for a in (u, v, w, *(list(bc) + [None] * 3)[:3]) ] if bc else \
+            [np.ascontiguousarray(a, np.float64) if a is not None else None for a in (u, v, w, None, None, None)]
+        ptr = [a.ctypes.data if a is not None else None for a in arrs]
+        out = np.empty(self.n_fluid, np.float64)
+        self._ck(self.lib.npsd_b200_mac_divergence_rhs(self.h, ptr[0], ptr[1], ptr[2], h, dt, rho, ptr[3], ptr[4],
+                                                       ptr[5], out.ctypes.data))
+        return out
+
+    def mac_divergence_rhs_device(self, d_u: int, d_v: int, d_w: int | None, d_b_full: int, h: float = 1.0,
+                                  dt: float = 0.05, rho: float = 1.0, d_bc=None) -> None:
+        """Device pointers in, the full-grid b (zeros off fluid) out: the input
+        of psdo_solve_device."""
+        bu, bv, bw = (list(d_bc) + [None] * 3)[:3] if d_bc else (None, None, None)
+        self._ck(self.lib.npsd_b200_mac_divergence_rhs_device(self.h, d_u, d_v, d_w, h, dt, rho, bu, bv, bw,
+                                                              d_b_full))
+
     @property
     def slab_graph(self) -> bool:
         """z-slab: the last solve's iterations ran as captured chunk graphs."""

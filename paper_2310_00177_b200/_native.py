@@ -23,6 +23,7 @@ EXPORTED_SYMBOLS = (
     "npsd_b200_profile_iterations", "npsd_b200_save_npm", "npsd_b200_load_npm", "npsd_b200_npm_last_error",
     "npsd_b200_nccl_unique_id", "npsd_b200_comm_create_nccl", "npsd_b200_comm_create_local",
     "npsd_b200_comm_destroy", "npsd_b200_comm_last_error", "npsd_b200_create_slab", "npsd_b200_slab_graph",
+    "npsd_b200_mac_divergence_rhs", "npsd_b200_mac_divergence_rhs_device",
 )
 
 
@@ -66,6 +67,10 @@ def lib() -> C.CDLL:
     L.npsd_b200_comm_create_local.argtypes = [C.c_int, C.POINTER(_vp)]
     L.npsd_b200_comm_destroy.argtypes = [_vp]
     L.npsd_b200_slab_graph.argtypes = [_vp]
+    L.npsd_b200_mac_divergence_rhs.argtypes = [_vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp,
+                                               _vp, _vp]
+    L.npsd_b200_mac_divergence_rhs_device.argtypes = [_vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double, _vp,
+                                                      _vp, _vp, _vp]
     L.npsd_b200_create_slab.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f32p, C.c_size_t,
                                         C.c_int, _vp, C.c_int, C.POINTER(_vp)]
     L.npsd_b200_npm_last_error.restype = C.c_char_p

@@ -294,6 +294,8 @@ struct npsd_b200_ctx {
     long long hist_host_cap = 0;
     double *red_a = nullptr, *red_b = nullptr;
     float *xin_f = nullptr, *out_f = nullptr;  // raw-network buffers (lazy)
+    double* mac = nullptr;                      // face arrays of the host mac_divergence_rhs (lazy)
+    size_t mac_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
     // solve graph
@@ -1360,6 +1362,7 @@ void free_ctx(npsd_b200_ctx* c) {
     };
     F(c->slab.all);
     F(c->slab.allu);
+    F(c->mac);
     if (c->slab_exec) cudaGraphExecDestroy(c->slab_exec);
     for (SchedBufs* sb : {&c->sch_stencil, &c->sch_down0}) {
         F(sb->pre);
@@ -1829,6 +1832,76 @@ int npsd_b200_spmv(npsd_b200_ctx* c, const double* x, double* y, int64_t n_f) {
         CK(cudaMemsetAsync(c->Dtmp, 0, (size_t)g.n * sizeof(double), c->s));
         CK(cudaMemsetAsync(c->R, 0, (size_t)g.n * sizeof(double), c->s));
         CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+namespace {
+// face-array element counts: u (nx+1, ny, nz), v (nx, ny+1, nz), w (nx, ny, nz+1)
+void mac_sizes(const npsd_b200_ctx* c, size_t n[3]) {
+    const size_t nx = c->g0.nx, ny = c->g0.ny, nz = c->g0.nz;
+    n[0] = (nx + 1) * ny * nz;
+    n[1] = nx * (ny + 1) * nz;
+    n[2] = (c->dim == 3) ? nx * ny * (nz + 1) : 0;
+}
+
+void launch_mac_rhs(npsd_b200_ctx* c, const double* const f[6], double h, double dt, double rho, double* b) {
+    require(c->dim == 2 || f[2] != nullptr, "mac_divergence_rhs: w is null");
+    require(!c->slab.on, "mac_divergence_rhs: not available on a z-slab context");
+    require(dt != 0.0, "mac_divergence_rhs: dt must be nonzero");
+    const bool bc = f[3] != nullptr;
+    require(!bc || (f[4] != nullptr && (c->dim == 2 || f[5] != nullptr)),
+            "mac_divergence_rhs: boundary value shape mismatch");
+    const double scale = -(rho * h) / dt;
+    const Geom g = c->g0;
+    if (c->dim == 3)
+        LAUNCH(c, c->s, k_mac_rhs<3>, g.n, g, c->L[0].cls, f[0], f[1], f[2], f[3], f[4], f[5], scale, b);
+    else
+        LAUNCH(c, c->s, k_mac_rhs<2>, g.n, g, c->L[0].cls, f[0], f[1], nullptr, f[3], f[4], nullptr, scale, b);
+}
+}  // namespace
+
+int npsd_b200_mac_divergence_rhs(npsd_b200_ctx* c, const double* u, const double* v, const double* w, double h,
+                                 double dt, double rho, const double* bc_u, const double* bc_v, const double* bc_w,
+                                 double* b_reduced) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(u && v && b_reduced, "mac_divergence_rhs: null argument");
+        size_t n[3];
+        mac_sizes(c, n);
+        const size_t tot = n[0] + n[1] + n[2];
+        if (c->mac_cap < 2 * tot) {
+            if (c->mac) CK(cudaFree(c->mac));
+            c->mac = dalloc<double>(2 * tot);
+            c->mac_cap = 2 * tot;
+        }
+        const double* host[6] = {u, v, w, bc_u, bc_v, bc_w};
+        const double* dev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        size_t off = 0;
+        for (int i = 0; i < 6; ++i) {
+            const size_t k = n[i % 3];
+            if (host[i] && k) {
+                CK(cudaMemcpyAsync(c->mac + off, host[i], k * sizeof(double), cudaMemcpyHostToDevice, c->s));
+                dev[i] = c->mac + off;
+            }
+            off += k;
+        }
+        double* full = c->red_a;  // scratch (n doubles)
+        launch_mac_rhs(c, dev, h, dt, rho, full);
+        const Geom g = c->g0;
+        LAUNCH(c, c->s, k_gather, g.n, g, c->L[0].cls, c->fmask, c->fbase, full, c->red_b);
+        CK(cudaMemcpyAsync(b_reduced, c->red_b, (size_t)c->n_fluid * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_mac_divergence_rhs_device(npsd_b200_ctx* c, const double* d_u, const double* d_v, const double* d_w,
+                                        double h, double dt, double rho, const double* d_bc_u, const double* d_bc_v,
+                                        const double* d_bc_w, double* d_b_full) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(d_u && d_v && d_b_full, "mac_divergence_rhs: null argument");
+        const double* dev[6] = {d_u, d_v, d_w, d_bc_u, d_bc_v, d_bc_w};
+        launch_mac_rhs(c, dev, h, dt, rho, d_b_full);
     });
 }
 

@@ -61,6 +61,48 @@ __global__ void __launch_bounds__(kBlock) k_mask_fluid(Geom g, const uint8_t* __
         dst[c] = (cls_type(cls[c]) == 0) ? src[c] : 0.0;
 }
 
+// ------------------------------------------------------------ right-hand side
+// mac_divergence_rhs (discretization.cpp:193-227) on the device, generalised
+// to 3D: b = scale * (((uR - uL) + (vT - vB)) + (wF - wB)) at fluid cells,
+// scale = -(rho * h) / dt; a face whose opposite cell is solid (or outside the
+// domain) takes the boundary value (0 without one); 0 elsewhere (the zero
+// invariant of the solver vectors). Faces x fastest: u (nx+1, ny, nz),
+// v (nx, ny+1, nz), w (nx, ny, nz+1).
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_mac_rhs(Geom g, const uint8_t* __restrict__ cls,
+                                                    const double* __restrict__ u, const double* __restrict__ v,
+                                                    const double* __restrict__ w, const double* __restrict__ bu,
+                                                    const double* __restrict__ bv, const double* __restrict__ bw,
+                                                    double scale, double* __restrict__ b) {
+    const long long nx = g.nx, ny = g.ny;
+    FOR_OWNED(g, c) {
+        if (cls_type(cls[c]) != 0) {
+            b[c] = 0.0;
+            continue;
+        }
+        int x, y, z;
+        decode(g, c, x, y, z);
+        auto solid = [&](int xx, int yy, int zz) {
+            if (xx < 0 || xx >= g.nx || yy < 0 || yy >= g.ny || zz < 0 || zz >= g.nz) return true;
+            return cls_type(cls[lin(g, xx, yy, zz)]) == 2;
+        };
+        auto ui = [&](long long fx, long long fy, long long fz) { return (fz * ny + fy) * (nx + 1) + fx; };
+        auto vi = [&](long long fx, long long fy, long long fz) { return (fz * (ny + 1) + fy) * nx + fx; };
+        auto wi = [&](long long fx, long long fy, long long fz) { return (fz * ny + fy) * nx + fx; };
+        const double uR = solid(x + 1, y, z) ? (bu ? bu[ui(x + 1, y, z)] : 0.0) : u[ui(x + 1, y, z)];
+        const double uL = solid(x - 1, y, z) ? (bu ? bu[ui(x, y, z)] : 0.0) : u[ui(x, y, z)];
+        const double vT = solid(x, y + 1, z) ? (bv ? bv[vi(x, y + 1, z)] : 0.0) : v[vi(x, y + 1, z)];
+        const double vB = solid(x, y - 1, z) ? (bv ? bv[vi(x, y, z)] : 0.0) : v[vi(x, y, z)];
+        double div = __dadd_rn(__dadd_rn(uR, -uL), __dadd_rn(vT, -vB));
+        if (D == 3) {
+            const double wF = solid(x, y, z + 1) ? (bw ? bw[wi(x, y, z + 1)] : 0.0) : w[wi(x, y, z + 1)];
+            const double wB = solid(x, y, z - 1) ? (bw ? bw[wi(x, y, z)] : 0.0) : w[wi(x, y, z)];
+            div = __dadd_rn(div, __dadd_rn(wF, -wB));
+        }
+        b[c] = __dmul_rn(scale, div);
+    }
+}
+
 // ---------------------------------------------------------------- operator
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_spmv(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ v,

@@ -73,6 +73,8 @@ class Oracle:
         L.oracle_ctx_precond_apply.argtypes = [C.c_void_p, _f64p, _f64p]
         L.oracle_ctx_spmv.argtypes = [C.c_void_p, _f64p, _f64p]
         L.oracle_spmv.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, _f64p, _f64p]
+        L.oracle_mac_rhs.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, _f64p, _f64p, C.c_void_p,
+                                     C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, _f64p]
         L.oracle_ctx_psdo_solve.argtypes = [C.c_void_p, C.c_int, _f64p, C.c_void_p, C.c_double, C.c_double,
                                             C.c_long, C.c_int, C.c_int, C.c_int, _f64p, _f64p,
                                             C.POINTER(C.c_long), C.POINTER(C.c_int), C.POINTER(C.c_long),
@@ -113,6 +115,18 @@ class Oracle:
             res.append(out[o:o + 3 * s].reshape(shp))
             o += 3 * s
         return res
+
+    def mac_rhs(self, types, u, v, w=None, h=1.0, dt=0.05, rho=1.0, bc=None) -> np.ndarray:
+        """mac_divergence_rhs restated (full grid, zeros off fluid); bc = (bu, bv[, bw]) or None."""
+        dim, (nx, ny, nz) = _dims_of(types)
+        out = np.empty(types.size, np.float64)
+        bc = list(bc or []) + [None] * (3 - len(bc or []))
+        opt = [None if a is None else np.ascontiguousarray(a, np.float64) for a in (w, *bc)]
+        ptr = [None if a is None else a.ctypes.data_as(C.c_void_p) for a in opt]
+        self._check(self.lib.oracle_mac_rhs(dim, nx, ny, nz, _u8(types), np.ascontiguousarray(u, np.float64),
+                                            np.ascontiguousarray(v, np.float64), ptr[0], h, dt, rho, ptr[1], ptr[2],
+                                            ptr[3], out))
+        return out
 
     def spmv(self, types: np.ndarray, x: np.ndarray) -> np.ndarray:
         """A x (reduced system of `types`), matrix-free, no network context."""
@@ -220,6 +234,8 @@ class Ref:
         L.ref_rhs_normal.argtypes = [C.c_ulonglong, C.c_long, _f64p]
         L.ref_init_params_2d.argtypes = [C.c_int, C.c_ulonglong, _f32p]
         L.ref_save_npm_2d.argtypes = [C.c_int, C.c_ulonglong, C.c_char_p]
+        L.ref_mac_rhs_2d.argtypes = [C.c_long, C.c_long, _u8p, _f64p, _f64p, C.c_double, C.c_double, C.c_double,
+                                     C.c_void_p, C.c_void_p, _f64p]
         L.ref_load_npm_2d.argtypes = [C.c_char_p, _f32p, C.c_long, C.POINTER(C.c_int)]
         L.ref_level_images_2d.argtypes = [C.c_long, C.c_long, C.c_int, _u8p, _f32p]
         L.ref_net_apply_2d.argtypes = [C.c_long, C.c_long, C.c_int, _f32p, C.c_long, _u8p, _f32p, _f32p,
@@ -244,6 +260,16 @@ class Ref:
         n = (depth - 1) * (2 * 252 + 2 * 28) + 252
         out = np.empty(n, np.float32)
         self._check(self.lib.ref_init_params_2d(depth, seed, out))
+        return out
+
+    def mac_rhs_2d(self, types, u, v, h=1.0, dt=0.05, rho=1.0, bc=None) -> np.ndarray:
+        ny, nx = types.shape
+        out = np.empty(types.size, np.float64)
+        bu, bv = (np.ascontiguousarray(bc[0], np.float64), np.ascontiguousarray(bc[1], np.float64)) if bc else (None, None)
+        self._check(self.lib.ref_mac_rhs_2d(nx, ny, _u8(types), np.ascontiguousarray(u, np.float64),
+                                            np.ascontiguousarray(v, np.float64), h, dt, rho,
+                                            None if bu is None else bu.ctypes.data_as(C.c_void_p),
+                                            None if bv is None else bv.ctypes.data_as(C.c_void_p), out))
         return out
 
     def save_npm_2d(self, depth: int, seed: int, path) -> None:

@@ -337,3 +337,54 @@ def test_c5_512_random_weights_precond_scaling_and_linearity(b200, oracle):
     assert np.array_equal(ctx.precond_apply(2.0 * r1), 2.0 * z1)
     z12 = ctx.precond_apply(r1 + r2)
     assert rel_l2(z12, z1 + z2) <= 1e-4
+
+
+@pytest.mark.parametrize("shape,with_bc", [((16, 24, 32), False), ((16, 24, 32), True), ((40, 24), True)])
+def test_mac_rhs_bitwise(b200, oracle, shape, with_bc):
+    """mac_divergence_rhs on the device (discretization.cpp:193-227; 3D
+    generalisation): bitwise equal to the restatement (3D) and to the
+    reference (2D, when present), reduced to the solve's ordering."""
+    t = scenes.random_types(shape, 41)
+    rng = np.random.default_rng(6)
+    if len(shape) == 3:
+        nz, ny, nx = shape
+        u, v, w = rng.standard_normal((nz, ny, nx + 1)), rng.standard_normal((nz, ny + 1, nx)), \
+            rng.standard_normal((nz + 1, ny, nx))
+        bc = tuple(rng.standard_normal(a.shape) for a in (u, v, w)) if with_bc else None
+        ctx = b200.Context(3, shape, b200.identity_params(1))
+    else:
+        ny, nx = shape
+        u, v, w = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx)), None
+        bc = tuple(rng.standard_normal(a.shape) for a in (u, v)) if with_bc else None
+        ctx = b200.Context(2, shape, b200.identity_params(1, dim=2))
+    ctx.set_mask(t)
+    got = ctx.mac_divergence_rhs(u, v, w, h=0.5, dt=0.02, rho=1.5, bc=bc)
+    want = oracle.mac_rhs(t, u, v, w, h=0.5, dt=0.02, rho=1.5, bc=bc)[t.reshape(-1) == 0]
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_mac_rhs_device_pipeline(b200, oracle):
+    """flags + velocity -> rhs -> solve without leaving HBM: identical to the
+    host path (rhs on the host API, then the solve)."""
+    t, _ = scenes.config("C3", 32)
+    nz, ny, nx = t.shape
+    rng = np.random.default_rng(8)
+    u, v, w = rng.standard_normal((nz, ny, nx + 1)), rng.standard_normal((nz, ny + 1, nx)), \
+        rng.standard_normal((nz + 1, ny, nx))
+    ctx = b200.Context(3, t.shape, b200.identity_params(4))
+    ctx.set_mask(t)
+    cfg = b200.SolveConfig(max_iters=2000)
+    host = ctx.psdo_solve(ctx.mac_divergence_rhs(u, v, w), cfg)
+    bufs = [b200.DeviceBuffer(ctx, a.nbytes) for a in (u, v, w)]
+    for bf, a in zip(bufs, (u, v, w)):
+        bf.upload(np.ascontiguousarray(a))
+    db, dx = b200.DeviceBuffer(ctx, 8 * t.size), b200.DeviceBuffer(ctx, 8 * t.size)
+    ctx.mac_divergence_rhs_device(bufs[0].ptr, bufs[1].ptr, bufs[2].ptr, db.ptr)
+    rep = ctx.psdo_solve_device(db.ptr, dx.ptr, cfg)
+    xf = np.empty(t.size)
+    dx.download(xf)
+    ctx.synchronize()
+    assert rep.iterations == host.report.iterations and rep.converged
+    assert np.array_equal(xf[t.reshape(-1) == 0], host.x)
+    for bf in (*bufs, db, dx):
+        bf.free()
