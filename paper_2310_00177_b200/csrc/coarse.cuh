@@ -29,6 +29,9 @@
 namespace nb2 {
 
 constexpr int kKX = 32, kKY = 4, kKZ = 2, kKT = kKX * kKY * kKZ;  // block tile = threads (256)
+#ifndef COARSE_MINB
+#define COARSE_MINB 1  // a register cap (more resident blocks) measured slower: it spills
+#endif
 
 // The three uniform-window kernels in shared memory as 28-float rows, so every
 // cell reads its kernel through one pointer: no per-class code paths, no warp
@@ -120,7 +123,7 @@ struct CellRow {
 
 // grid (ceil(nx/32), ceil(ny/4), ceil(owned planes/2)), block (32, 4, 2)
 template <bool POOL>
-__global__ void __launch_bounds__(kKT) k_cdown(Geom g, const float* __restrict__ x, ConvTab ct,
+__global__ void __launch_bounds__(kKT, COARSE_MINB) k_cdown(Geom g, const float* __restrict__ x, ConvTab ct,
                                                const __grid_constant__ KC kc, float* __restrict__ y,
                                                float* __restrict__ xnext, Geom gc,
                                                const int* __restrict__ done) {
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(kKT) k_cdown(Geom g, const float* __restrict__
 
 // grid (ceil(nx/32), ceil(ny/4), ceil(owned planes/2)), block (32, 4, 2); outc is level l+1
 template <int D = 3>
-__global__ void __launch_bounds__(kKT) k_cup(Geom g, Geom gc, const float* __restrict__ outc,
+__global__ void __launch_bounds__(kKT, COARSE_MINB) k_cup(Geom g, Geom gc, const float* __restrict__ outc,
                                              const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
                                              const __grid_constant__ KC kc, float* __restrict__ outl,
                                              const int* __restrict__ done) {

@@ -295,6 +295,8 @@ struct npsd_b200_ctx {
     double *red_a = nullptr, *red_b = nullptr;
     float *xin_f = nullptr, *out_f = nullptr;  // raw-network buffers (lazy)
     double* mac = nullptr;                      // face arrays of the host mac_divergence_rhs (lazy)
+    char* l2pool = nullptr;                     // levels >= 1 per-cell arrays, L2-persisting window
+    size_t l2pool_bytes = 0;
     size_t mac_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -1371,6 +1373,15 @@ void free_ctx(npsd_b200_ctx* c) {
         F(sb->first);
         F(sb->last);
     }
+    for (int l = 1; l < kMaxDepth; ++l) {  // carved from the L2 pool
+        LevelBufs& L = c->L[l];
+        L.cls = nullptr;
+        L.rcode = nullptr;
+        L.y = nullptr;
+        L.x = nullptr;
+        L.out = nullptr;
+    }
+    F(c->l2pool);
     for (auto& L : c->L) {
         F(L.cls);
         F(L.mmask);
@@ -1489,11 +1500,46 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         CK(cudaEventCreate(&c->ev1));
         compute_offsets(c);
         c->d_params = dalloc<float>(param_count_impl(dim, depth));
+        // L2-resident pool: the per-cell arrays of levels >= 1 (class bytes, row
+        // codes, x, y, out; ~2.3 B x n_c at depth 4) live in one allocation that
+        // an access-policy window keeps persisting in L2, so the coarse levels'
+        // latency chains hit L2 instead of DRAM after the L0 phases stream
+        {
+            size_t bytes = 0;
+            auto add = [&](size_t b) { bytes += (b + 255) & ~(size_t)255; };
+            for (int l = 1; l < depth; ++l) {
+                const size_t n = (size_t)level_geom(c, l).n;
+                add(n);                                         // cls
+                add(4 * n);                                     // rcode
+                add(4 * n);                                     // y
+                add(4 * n);                                     // x
+                if (l < depth - 1) add(4 * n);                  // out
+            }
+            if (bytes) {
+                CK(cudaMalloc(&c->l2pool, bytes));
+                c->l2pool_bytes = bytes;
+            }
+        }
+        size_t pool_off = 0;
+        auto carve = [&](size_t b) {
+            void* p = c->l2pool + pool_off;
+            pool_off += (b + 255) & ~(size_t)255;
+            return p;
+        };
         for (int l = 0; l < depth; ++l) {
             LevelBufs& L = c->L[l];
             L.g = level_geom(c, l);
             L.nseg = (L.g.n + 31) / 32;
-            L.cls = dalloc<uint8_t>((size_t)L.g.n);
+            const size_t nl = (size_t)L.g.n;
+            if (l > 0) {
+                L.cls = static_cast<uint8_t*>(carve(nl));
+                L.rcode = static_cast<uint32_t*>(carve(4 * nl));
+                L.y = static_cast<float*>(carve(4 * nl));
+                L.x = static_cast<float*>(carve(4 * nl));
+                if (l < depth - 1) L.out = static_cast<float*>(carve(4 * nl));
+            } else {
+                L.cls = dalloc<uint8_t>(nl);
+            }
             L.mmask = dalloc<uint32_t>((size_t)L.nseg);
             L.mbase = dalloc<uint32_t>((size_t)L.nseg);
             L.mcount = dalloc<uint32_t>((size_t)L.nseg);
@@ -1501,17 +1547,33 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
             L.tab_down = dalloc<float>((size_t)kRowW * L.g.n);
             if (l < depth - 1) L.tab_up = dalloc<float>((size_t)kRowW * L.g.n);
             L.mlist = dalloc<uint32_t>((size_t)L.g.n);
-            if (l > 0) {
-                L.rcode = dalloc<uint32_t>((size_t)L.g.n);
-                L.pid = dalloc<uint32_t>((size_t)L.g.n);
-            }
+            if (l > 0) L.pid = dalloc<uint32_t>((size_t)L.g.n);
             L.mcnt = dalloc<uint32_t>(1);
             L.kc_down = dalloc<float>(3 * (size_t)c->S);
             L.kc_up = dalloc<float>(3 * (size_t)c->S);
-            L.y = dalloc<float>((size_t)L.g.n);
-            if (l > 0) L.x = dalloc<float>((size_t)L.g.n);
-            if (l > 0 && l < depth - 1) L.out = dalloc<float>((size_t)L.g.n);
+            if (l == 0) L.y = dalloc<float>((size_t)L.g.n);
             L.zG = dalloc<unsigned long long>(81);
+        }
+        if (c->l2pool) {
+            int maxp = 0, maxw = 0;
+            CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->dev));
+            CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, c->dev));
+            if (maxp > 0 && maxw > 0) {
+                size_t cur = 0;
+                CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+                const size_t want = std::min(c->l2pool_bytes, (size_t)maxp);
+                if (want > cur) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+                CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+                const size_t win = std::min(c->l2pool_bytes, (size_t)maxw);
+                cudaStreamAttrValue v = {};
+                v.accessPolicyWindow.base_ptr = c->l2pool;
+                v.accessPolicyWindow.num_bytes = win;
+                v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)cur / (double)win);
+                v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                CK(cudaStreamSetAttribute(c->s, cudaStreamAttributeAccessPolicyWindow, &v));
+                CK(cudaStreamSetAttribute(c->s2, cudaStreamAttributeAccessPolicyWindow, &v));
+            }
         }
         c->zab = dalloc<float>(2 * (size_t)depth);
         CK(cudaMemset(c->zab, 0, 2 * (size_t)depth * sizeof(float)));
