@@ -296,6 +296,9 @@ struct npsd_b200_ctx {
     float *xin_f = nullptr, *out_f = nullptr;  // raw-network buffers (lazy)
     double* mac = nullptr;                      // face arrays of the host mac_divergence_rhs (lazy)
     char* l2pool = nullptr;                     // levels >= 1 per-cell arrays, L2-persisting window
+    long long tab_cap[kMaxDepth] = {};          // kernel-row table capacity (rows) per level
+    unsigned buf_gen = 0;                       // bumped when a buffer a captured graph uses moves
+    unsigned exec_gen = 0, slab_exec_gen = 0;
     size_t l2pool_bytes = 0;
     size_t mac_cap = 0;
     void* cub_tmp = nullptr;
@@ -647,6 +650,22 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         CK(cudaMemsetAsync(c->npat0, 0, sizeof(uint32_t), s));
         CK(cudaMemsetAsync(c->dcnt0, 0, sizeof(uint32_t), s));
         CK(cudaMemsetAsync(c->ucnt0, 0, sizeof(uint32_t), s));
+    }
+    // kernel-row tables: at most one row per mixed cell (grow only)
+    for (int l = 0; l < c->depth; ++l) {
+        LevelBufs& L = c->L[l];
+        const long long need = std::max<long long>(n_mixed[l], 1);
+        if (need > c->tab_cap[l]) {
+            const long long cap = need + need / 4;
+            CK(cudaFree(L.tab_down));
+            L.tab_down = dalloc<float>((size_t)kRowW * cap);
+            if (L.tab_up) {
+                CK(cudaFree(L.tab_up));
+                L.tab_up = dalloc<float>((size_t)kRowW * cap);
+            }
+            c->tab_cap[l] = cap;
+            ++c->buf_gen;
+        }
     }
     for (int l = 0; l < c->depth; ++l) {
         LevelBufs& L = c->L[l];
@@ -1109,6 +1128,7 @@ void capture_solve_graph(npsd_b200_ctx* c, int nullspace, int no) {
     c->exec_key[3] = c->partials;
     c->exec_nullspace = nullspace;
     c->exec_no = no;
+    c->exec_gen = c->buf_gen;
     c->body_launches = (int)bod.size();
     c->prologue_launches = (int)pro.size();
     c->launches -= (long long)(bod.size() + pro.size());  // captured, not executed
@@ -1126,7 +1146,8 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
     ensure_ring(c, ring);
     ensure_hist(c, max_iters + 1);
     const int nullspace = cfg->nullspace_projection ? 1 : 0;
-    if (!c->exec || c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist || c->exec_key[2] != c->ADring ||
+    if (!c->exec || c->exec_gen != c->buf_gen || c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist ||
+        c->exec_key[2] != c->ADring ||
         c->exec_nullspace != nullspace || c->exec_no != cfg->n_ortho)
         capture_solve_graph<D>(c, nullspace, cfg->n_ortho);
     SolverState* h = c->st_host;
@@ -1244,7 +1265,8 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
     slab_exchange(c, s, c->R, sizeof(double), 0);
     const int K = slab_chunk(ring);
     bool graph = c->slab.comm->capturable() && !c->slab_no_graph;
-    if (graph && (!c->slab_exec || c->slab_exec_no != no || c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist ||
+    if (graph && (!c->slab_exec || c->slab_exec_gen != c->buf_gen || c->slab_exec_no != no ||
+                  c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist ||
                   c->exec_key[2] != c->ADring)) {
         if (c->slab_exec) CK(cudaGraphExecDestroy(c->slab_exec));
         c->slab_exec = nullptr;
@@ -1271,6 +1293,7 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
             cudaGraphDestroy(gr);
             CK(ie);
             c->slab_exec_no = no;
+            c->slab_exec_gen = c->buf_gen;
             c->exec_key[0] = c->Dring;
             c->exec_key[1] = c->hist;
             c->exec_key[2] = c->ADring;
@@ -1544,8 +1567,10 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
             L.mbase = dalloc<uint32_t>((size_t)L.nseg);
             L.mcount = dalloc<uint32_t>((size_t)L.nseg);
             if (l > 0) L.img = dalloc<float>(3 * (size_t)L.g.n);
-            L.tab_down = dalloc<float>((size_t)kRowW * L.g.n);
-            if (l < depth - 1) L.tab_up = dalloc<float>((size_t)kRowW * L.g.n);
+            // kernel-row tables grow with the frame's mixed-cell count (set_mask)
+            L.tab_down = dalloc<float>((size_t)kRowW);
+            if (l < depth - 1) L.tab_up = dalloc<float>((size_t)kRowW);
+            c->tab_cap[l] = 1;
             L.mlist = dalloc<uint32_t>((size_t)L.g.n);
             if (l > 0) L.pid = dalloc<uint32_t>((size_t)L.g.n);
             L.mcnt = dalloc<uint32_t>(1);
