@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kKT, COARSE_MINB) k_cdown(Geom g, const float*
                                                const __grid_constant__ KC kc, float* __restrict__ y,
                                                float* __restrict__ xnext, Geom gc,
                                                const int* __restrict__ done) {
+    pdl_launch_wait();
     if (done && *done) return;  // z-slab chunked loop: the solve has finished
     constexpr int SX = kKX + 2, SY = kKY + 2, SZ = kKZ + 2;
     __shared__ float sx[SZ][SY][SX];
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(kKT, COARSE_MINB) k_cup(Geom g, Geom gc, const
                                              const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
                                              const __grid_constant__ KC kc, float* __restrict__ outl,
                                              const int* __restrict__ done) {
+    pdl_launch_wait();
     if (done && *done) return;  // z-slab chunked loop: the solve has finished
     // coarse box: (X0/2 - 1 .. X0/2 + 16) x (Y0/2 - 1 .. Y0/2 + 2) x (Z0/2 - 1 .. Z0/2 + 1)
     constexpr int CX = kKX / 2 + 2, CY = kKY / 2 + 2, CZ = kKZ / 2 + 2;

@@ -113,6 +113,15 @@ struct SolverState {
                                     // iteration kernels return at once when done (chunked loop)
 };
 
+// Programmatic dependent launch (the iteration kernels): let the next kernel
+// in the stream launch now, then wait for the previous one's completion and
+// memory before touching anything it wrote. Without the launch attribute both
+// are no-ops.
+__device__ __forceinline__ void pdl_launch_wait() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

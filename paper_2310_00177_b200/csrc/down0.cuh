@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __r
                                                       const double* __restrict__ r, const SolverState* __restrict__ st,
                                                       const __grid_constant__ KC0 kc, float* __restrict__ y,
                                                       float* __restrict__ xnext, Geom gc, Sched sc) {
+    pdl_launch_wait();
     if (st->dist && st->done) return;
     sched_for_each(sc, [&](int tx, int ty, int u0, int u1) {
         down_l0_segment(g, cls, r, st, kc, y, xnext, gc, tx, ty, 2 * u0, min(2 * u1, g.nz));

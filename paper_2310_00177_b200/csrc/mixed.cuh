@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* 
                                                         const float* __restrict__ tab, const uint32_t* __restrict__ kid,
                                                         float* __restrict__ y) {
     constexpr int S = Sh<D>::S;
+    pdl_launch_wait();
     if (st->dist && st->done) return;
     const uint32_t n = *count;
     const double inv1 = st->inv1, inv2 = st->inv2;
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uin
                                                       unsigned int* __restrict__ counter) {
     constexpr int S = Sh<D>::S;
     constexpr int NA = (NO > 0) ? NO : 1;
+    pdl_launch_wait();
     if (st->dist && st->done) return;
     const uint32_t n = *count;
     const float za = zab[0], zb = zab[1];

@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <condition_variable>
@@ -252,6 +253,9 @@ struct npsd_b200_ctx {
     cudaGraphExec_t slab_exec = nullptr;  // z-slab: a chunk of iterations (NCCL ranks)
     int slab_exec_no = -1, slab_exec_k0 = -1;
     bool slab_no_graph = false;   // the chunk graph could not be captured: eager chunks
+    // programmatic dependent launch of the iteration kernels: measured neutral
+    // in the solve graph (C3 256^3: 386.0 vs 384.8 ms), so opt-in (NPSD_PDL=1)
+    bool pdl = false;
     long long slab_chunk_launches = 0;
     cudaStream_t s = nullptr, s2 = nullptr;
     std::vector<float> params;
@@ -747,6 +751,26 @@ struct Step {
         ++(c)->launches;                                                     \
     } while (0)
 
+// Launch of an iteration kernel (one that starts with pdl_launch_wait()) with
+// programmatic stream serialisation: its blocks may launch while the previous
+// kernel drains; in a captured graph this becomes a programmatic edge.
+template <typename... KArgs, typename... Args>
+void launch_pdl(npsd_b200_ctx* c, cudaStream_t s, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = c->pdl ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+    ++c->launches;
+}
+
 // z-chunk (in bricks or planes) so that a launch has about two waves of blocks.
 template <typename K>
 int zchunk_for(npsd_b200_ctx* c, K kernel, int threads, long long tiles_xy, int nz_units, size_t smem = 0) {
@@ -769,8 +793,8 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
         // f32 input (levels >= 1, raw level 0): one thread per cell (coarse.cuh)
         const KC& kc = (l == c->depth - 1) ? c->kc_coarse : c->kc_down[l];
         const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
-        LAUNCH3(c, s, k_cdown<POOL>, grid, dim3(kKX, kKY, kKZ), L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc,
-                c->slab.on ? &c->st->done : nullptr);
+        launch_pdl(c, s, k_cdown<POOL>, grid, dim3(kKX, kKY, kKZ), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc,
+                   c->slab.on ? &c->st->done : nullptr);
         return;
     }
     const dim3 block(kNX, kNY);
@@ -792,8 +816,8 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
     const float* outc = (l + 1 == c->depth - 1) ? Lc.y : Lc.out;
     if (D == 3 && MODE == kUpMid) {
         const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
-        LAUNCH3(c, s, k_cup<3>, grid, dim3(kKX, kKY, kKZ), L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
-                c->kc_up[l], outl, c->slab.on ? &c->st->done : nullptr);
+        launch_pdl(c, s, k_cup<3>, grid, dim3(kKX, kKY, kKZ), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
+                   c->kc_up[l], outl, c->slab.on ? &c->st->done : nullptr);
         return;
     }
     const dim3 block(kNX, kNY);
@@ -819,8 +843,8 @@ void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         KC0 kc0;
         for (int i = 0; i < 27; ++i) kc0.k[i] = c->kc_up[0].k[0][i];  // the uniform-fluid kernel
-        LAUNCH3S(c, s, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y,
-                 c->zab, kc0, c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_stencil.view());
+        launch_pdl(c, s, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y,
+                   c->zab, kc0, c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_stencil.view());
         return;
     }
     launch_up<D, kUpL0, NO>(c, s, 0, nullptr, c->Dtmp);
@@ -848,8 +872,8 @@ void launch_ortho(npsd_b200_ctx* c, cudaStream_t s) {
     const size_t sm = march_smem_bytes<OrthoOp<NO>>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const dim3 grid(wave_blocks(c, k, kSX * kSY, sm));
-    LAUNCH3S(c, s, k, grid, block, sm, g, c->L[0].cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
-             c->counter, c->sch_stencil.view());
+    launch_pdl(c, s, k, grid, block, sm, g, c->L[0].cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
+               c->counter, c->sch_stencil.view());
 }
 
 template <int D>
@@ -872,8 +896,8 @@ void launch_update(npsd_b200_ctx* c, cudaStream_t s, cudaGraphConditionalHandle 
     const size_t sm = march_smem_bytes<UpdateOp>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const dim3 grid(wave_blocks(c, k, kSX * kSY, sm));
-    LAUNCH3S(c, s, k, grid, block, sm, g, c->L[0].cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist, c->times,
-             c->partials, c->counter, h, use_cond, do_norm, c->sch_stencil.view());
+    launch_pdl(c, s, k, grid, block, sm, g, c->L[0].cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist,
+               c->times, c->partials, c->counter, h, use_cond, do_norm, c->sch_stencil.view());
 }
 
 // One named launcher per kernel of an iteration: the graph body is captured
@@ -889,14 +913,15 @@ void launch_down_l0(npsd_b200_ctx* c, cudaStream_t s) {
     const dim3 grid(wave_blocks(c, k_down_l0, kSX * kSY, sm));
     KC0 kc0;
     for (int i = 0; i < 27; ++i) kc0.k[i] = c->kc_down[0].k[0][i];  // the uniform-fluid kernel
-    LAUNCH3S(c, s, k_down_l0, grid, block, sm, g, L.cls, c->R, c->st, kc0, L.y, c->L[1].x, c->L[1].g,
-             c->sch_down0.view());
+    launch_pdl(c, s, k_down_l0, grid, block, sm, g, L.cls, c->R, (const SolverState*)c->st, kc0, L.y, c->L[1].x,
+               c->L[1].g, c->sch_down0.view());
 }
 
 template <int D>
 void launch_mixed_down0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
-    LAUNCH(c, s, k_mixed_down0<D>, L.g.n, L.g, c->dlist0, c->dcnt0, c->R, c->st, L.tab_down, c->dkid0, L.y);
+    launch_pdl(c, s, k_mixed_down0<D>, dim3(grid_for(c, k_mixed_down0<D>, L.g.n)), dim3(kBlock), 0, L.g, c->dlist0,
+               c->dcnt0, c->R, (const SolverState*)c->st, L.tab_down, c->dkid0, L.y);
 }
 
 template <int D, int NO>
@@ -904,8 +929,9 @@ void launch_mixed_up0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
     const LevelBufs& L1 = c->L[1];
     const float* outc = (c->depth == 2) ? L1.y : L1.out;
-    LAUNCH(c, s, (k_mixed_up0<D, NO>), L.g.n, L.g, L1.g, c->ulist0, c->ucnt0, outc, L.y, c->zab, L.tab_up,
-           c->ukid0, c->Dtmp, c->st, c->ADring, c->partials, c->counter);
+    launch_pdl(c, s, k_mixed_up0<D, NO>, dim3(grid_for(c, k_mixed_up0<D, NO>, L.g.n)), dim3(kBlock), 0, L.g, L1.g,
+               c->ulist0, c->ucnt0, outc, L.y, c->zab, L.tab_up, c->ukid0, c->Dtmp, c->st, c->ADring, c->partials,
+               c->counter);
 }
 
 template <int D>
@@ -1507,6 +1533,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->depth = depth;
         c->S = (dim == 3) ? 27 : 9;
         c->dev = device;
+        if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
         if (slab) {
             c->slab = *slab;
             for (int l = 0; l < depth; ++l) c->slab.ghost[l] = 1 << (depth - 1 - l);

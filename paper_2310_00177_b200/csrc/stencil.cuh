@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
                                                      double* __restrict__ Dring, double* __restrict__ ADring,
                                                      SolverState* st, double* __restrict__ partials,
                                                      unsigned int* __restrict__ counter, Sched sc) {
+    pdl_launch_wait();
     if (st->dist && st->done) return;
     const int nc = st->n_cache, R = st->ring;
     const int nw = (st->head + 1) % R;
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
                                                       unsigned int* __restrict__ counter,
                                                       cudaGraphConditionalHandle cond, int use_cond, int do_norm,
                                                       Sched sc) {
+    pdl_launch_wait();
     if (st->breakdown) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0)
             set_cond(cond, use_cond, 0u);

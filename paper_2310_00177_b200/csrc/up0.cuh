@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_up_l0(Geom g, Geom gc, const uint8
                                                     const double* __restrict__ ADring, double* __restrict__ partials,
                                                     unsigned int* __restrict__ counter, Sched sc) {
     constexpr int NA = (NO > 0) ? NO : 1;
+    pdl_launch_wait();
     if (st->dist && st->done) return;
     const float za = zab[0], zb = zab[1];
     const double nrm = st->nrm;
