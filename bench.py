@@ -332,6 +332,19 @@ def run_b200(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # the paper's comparison columns on the same device and frame: GPU CG and
+    # Jacobi-PCG (pcg_solve, solver.cpp:36-109), device-resident inputs
+    baselines = {}
+    for kind, name in (("identity", "gpu_cg"), ("jacobi", "gpu_pcg_jacobi")):
+        ms_k, it_k = [], []
+        for i in range(2):
+            rep_k = ctx.pcg_solve_device(d_b.ptr, d_x.ptr, cfg, precond=kind)
+            if i:
+                ms_k.append(ctx.last_solve_ms)
+                it_k.append(rep_k.iterations)
+        baselines[name] = {"solve_ms": float(np.mean(ms_k)), "iterations": int(it_k[-1]),
+                           "per_iter_ms": float(np.mean(ms_k)) / max(it_k[-1], 1), "converged": bool(rep_k.converged)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -375,6 +388,7 @@ def run_b200(args) -> None:
             "gpu_launches": int(round(launches)),
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "baselines_same_gpu": baselines,
         }
         print(json.dumps(line), flush=True)
     for buf in (d_types, d_b, d_x):

@@ -134,6 +134,17 @@ int npsd_b200_init_params(int dim, int depth, uint64_t seed, float* out);
 int npsd_b200_identity_params(int dim, int depth, float* out);
 void npsd_b200_rhs_normal(uint64_t seed, int64_t n, double* out);
 
+/* Preconditioned CG on the device, replacing pcg_solve / cg_solve
+ * (solver.cpp:36-109): precond 0 = identity (cg_solve), 1 = Jacobi
+ * (precond.cpp:12-26; NPSD_INVALID_ARGUMENT "jacobi precond: zero diagonal"
+ * like the reference's constructor). Same vectors, report and errors as
+ * psdo_solve; n_ortho and normalize_before_precond are ignored, nullspace
+ * projection is not supported. The baseline the paper compares NPSDO with. */
+int npsd_b200_pcg_solve(npsd_b200_ctx* ctx, const double* b, const double* x0, const npsd_b200_solve_cfg* cfg,
+                        int precond, double* x, npsd_b200_report* rep);
+int npsd_b200_pcg_solve_device(npsd_b200_ctx* ctx, const double* d_b, const double* d_x0,
+                               const npsd_b200_solve_cfg* cfg, int precond, double* d_x, npsd_b200_report* rep);
+
 /* Right-hand side from a MAC velocity field, replacing mac_divergence_rhs
  * (discretization.cpp:193-227) + reduce: b = -(rho*h/dt) * (signed sum of face
  * velocities) at fluid cells, a face whose opposite cell is solid (or outside

@@ -280,4 +280,29 @@ int ref_psdo_solve(int dim, long nx, long ny, long nz, const unsigned char* type
     });
 }
 
+// Reference pcg_solve (solver.cpp:36-102) on the reference assembly:
+// precond 0 = IdentityPrecond (cg_solve), 1 = JacobiPrecond.
+int ref_pcg_solve(int dim, long nx, long ny, long nz, const unsigned char* types, int precond, const double* b,
+                  double tol_reduction, long max_iters, double* x_out, double* hist, long* iterations, int* converged,
+                  long* hist_len) {
+    return guarded([&] {
+        const long rows = (dim == 3) ? ny * nz : ny;
+        const auto I = image_from_types(nx, rows, types);
+        const auto A = assemble(dim, nx, ny, nz, I, types);
+        const auto sys = npsd::reduce(A, npsd::Vector(static_cast<std::size_t>(A.n_rows), 0.0), I);
+        auto P = precond ? npsd::jacobi_precond(sys.A) : npsd::identity_precond(sys.A.n_rows);
+        npsd::SolveConfig cfg;
+        cfg.tol_reduction = tol_reduction;
+        cfg.max_iters = max_iters;
+        const std::size_t nf = static_cast<std::size_t>(sys.A.n_rows);
+        npsd::Vector bv(b, b + nf);
+        const auto res = npsd::pcg_solve(sys.A, bv, *P, cfg, nullptr);
+        std::memcpy(x_out, res.x.data(), nf * sizeof(double));
+        for (std::size_t i = 0; i < res.report.residual_history.size(); ++i) hist[i] = res.report.residual_history[i];
+        *iterations = static_cast<long>(res.report.iterations);
+        *converged = res.report.converged ? 1 : 0;
+        *hist_len = static_cast<long>(res.report.residual_history.size());
+    });
+}
+
 }  // extern "C"

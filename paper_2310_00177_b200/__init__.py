@@ -394,6 +394,34 @@ class Context:
         self._ck(st)
         return SolveResult(x, self._report(rep, method))
 
+    def pcg_solve(self, b: np.ndarray, cfg: SolveConfig, precond: str = "identity", x0: np.ndarray | None = None,
+                  out: np.ndarray | None = None) -> SolveResult:
+        """pcg_solve / cg_solve (solver.cpp:36-109) on the device: precond
+        "identity" (method "cg") or "jacobi" ("pcg+jacobi")."""
+        kind = {"identity": 0, "jacobi": 1}[precond]
+        b = np.ascontiguousarray(b, np.float64)
+        if b.size != self.n_fluid:
+            raise ValueError("solve: rhs length mismatch")
+        x = np.empty_like(b) if out is None else out
+        x0p = None
+        if x0 is not None:
+            x0a = np.ascontiguousarray(x0, np.float64)
+            x0p = x0a.ctypes.data_as(C.c_void_p)
+        rep = _native.Report()
+        c = cfg._c()
+        st = self.lib.npsd_b200_pcg_solve(self.h, b, x0p, C.byref(c), kind, x, C.byref(rep))
+        self._ck(st)
+        return SolveResult(x, self._report(rep, "cg" if kind == 0 else "pcg+jacobi"))
+
+    def pcg_solve_device(self, b_ptr: int, x_ptr: int, cfg: SolveConfig, precond: str = "identity",
+                         x0_ptr: int | None = None) -> SolveReport:
+        kind = {"identity": 0, "jacobi": 1}[precond]
+        rep = _native.Report()
+        c = cfg._c()
+        self._ck(self.lib.npsd_b200_pcg_solve_device(self.h, C.c_void_p(b_ptr), C.c_void_p(x0_ptr) if x0_ptr else None,
+                                                     C.byref(c), kind, C.c_void_p(x_ptr), C.byref(rep)))
+        return self._report(rep, "cg" if kind == 0 else "pcg+jacobi")
+
     def psdo_solve_device(self, b_ptr: int, x_ptr: int, cfg: SolveConfig, x0_ptr: int | None = None,
                           method: str = "psdo+neural") -> SolveReport:
         rep = _native.Report()

@@ -23,7 +23,8 @@ EXPORTED_SYMBOLS = (
     "npsd_b200_profile_iterations", "npsd_b200_save_npm", "npsd_b200_load_npm", "npsd_b200_npm_last_error",
     "npsd_b200_nccl_unique_id", "npsd_b200_comm_create_nccl", "npsd_b200_comm_create_local",
     "npsd_b200_comm_destroy", "npsd_b200_comm_last_error", "npsd_b200_create_slab", "npsd_b200_slab_graph",
-    "npsd_b200_mac_divergence_rhs", "npsd_b200_mac_divergence_rhs_device",
+    "npsd_b200_mac_divergence_rhs", "npsd_b200_mac_divergence_rhs_device", "npsd_b200_pcg_solve",
+    "npsd_b200_pcg_solve_device",
 )
 
 
@@ -67,6 +68,8 @@ def lib() -> C.CDLL:
     L.npsd_b200_comm_create_local.argtypes = [C.c_int, C.POINTER(_vp)]
     L.npsd_b200_comm_destroy.argtypes = [_vp]
     L.npsd_b200_slab_graph.argtypes = [_vp]
+    L.npsd_b200_pcg_solve.argtypes = [_vp, _f64p, _vp, C.c_void_p, C.c_int, _f64p, C.c_void_p]
+    L.npsd_b200_pcg_solve_device.argtypes = [_vp, _vp, _vp, C.c_void_p, C.c_int, _vp, C.c_void_p]
     L.npsd_b200_mac_divergence_rhs.argtypes = [_vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp,
                                                _vp, _vp]
     L.npsd_b200_mac_divergence_rhs_device.argtypes = [_vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double, _vp,

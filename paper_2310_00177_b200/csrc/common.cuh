@@ -106,6 +106,8 @@ struct SolverState {
     double cross[kRing][kRing];     // cross[i][j] = d_i . A d_j (i older than j)
     double dAd_new, rd_new, alpha;  // for the direction being built
     double mean;                    // nullspace projection mean
+    double rz, beta;                // pcg: r.z and the direction update's beta (cg.cuh)
+    int pcur;                       // pcg: which p buffer holds the current direction
     double bad_value;               // curvature at breakdown
     unsigned long long t0;          // %globaltimer at solve start
     double part[kPart];             // z-slab: this rank's totals at a reduction point

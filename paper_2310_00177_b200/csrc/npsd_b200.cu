@@ -34,6 +34,7 @@
 #include "coarse.cuh"
 #include "up0.cuh"
 #include "slab.cuh"
+#include "cg.cuh"
 
 using namespace nb2;
 
@@ -301,6 +302,12 @@ struct npsd_b200_ctx {
     double* mac = nullptr;                      // face arrays of the host mac_divergence_rhs (lazy)
     char* l2pool = nullptr;                     // levels >= 1 per-cell arrays, L2-persisting window
     long long tab_cap[kMaxDepth] = {};          // kernel-row table capacity (rows) per level
+    // pcg (cg.cuh): two direction buffers, A p, z (Jacobi); graph per preconditioner
+    double *cgP0 = nullptr, *cgP1 = nullptr, *cgAp = nullptr, *cgZ = nullptr;
+    cudaGraphExec_t cg_exec = nullptr;
+    int cg_exec_kind = -1;
+    unsigned cg_exec_gen = 0;
+    const void* cg_exec_key = nullptr;
     unsigned buf_gen = 0;                       // bumped when a buffer a captured graph uses moves
     unsigned exec_gen = 0, slab_exec_gen = 0;
     size_t l2pool_bytes = 0;
@@ -1374,6 +1381,146 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
     return NPSD_OK;
 }
 
+// ------------------------------------------------------------------- pcg
+// pcg_solve (solver.cpp:36-102) on the device: identity (cg_solve) or Jacobi.
+long long first_zero_diag_row(npsd_b200_ctx* c) {
+    unsigned int* d = reinterpret_cast<unsigned int*>(c->red_b);
+    const unsigned int none = 0xffffffffu;
+    CK(cudaMemcpyAsync(d, &none, sizeof none, cudaMemcpyHostToDevice, c->s));
+    LAUNCH(c, c->s, k_zero_diag, c->g0.n, c->g0, c->L[0].cls, c->fmask, c->fbase, d);
+    unsigned int row = none;
+    CK(cudaMemcpyAsync(&row, d, sizeof row, cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    return row == none ? -1 : (long long)row;
+}
+
+template <int D, bool J>
+void capture_cg_graph(npsd_b200_ctx* c) {
+    if (c->cg_exec) {
+        CK(cudaGraphExecDestroy(c->cg_exec));
+        c->cg_exec = nullptr;
+    }
+    cudaStream_t s = c->s, s2 = c->s2;
+    const Geom g = c->g0;
+    const uint8_t* cls = c->L[0].cls;
+    double* z = J ? c->cgZ : c->R;
+    const long long before = c->launches;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
+    // prologue: r0 = b - A x0, z0 = M r0, ||r0||, r0.z0
+    LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R);
+    LAUNCH(c, s, (k_cg_update<J, true>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st, c->hist,
+           c->times, c->partials, c->counter, h, 1);
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CK(cudaGraphAddNode(&cnode, cg, deps, nd, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
+    CK(cudaStreamBeginCaptureToGraph(s2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    {
+        auto k = k_cg_dir<D>;
+        const size_t sm = march_smem_bytes<CgOp>();
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        LAUNCH3S(c, s2, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, g, cls, (const double*)z,
+                 c->cgP0, c->cgP1, c->cgAp, c->st, c->partials, c->counter, c->sch_stencil.view());
+        LAUNCH(c, s2, (k_cg_update<J, false>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st,
+               c->hist, c->times, c->partials, c->counter, h, 1);
+    }
+    cudaGraph_t body_out = nullptr;
+    CK(cudaStreamEndCapture(s2, &body_out));
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamEndCapture(s, &graph));
+    CK(cudaGraphInstantiate(&c->cg_exec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    c->launches = before;
+    c->cg_exec_kind = J ? 1 : 0;
+    c->cg_exec_gen = c->buf_gen;
+    c->cg_exec_key = c->hist;
+}
+
+// the solve on c->Bf / c->X0 (masked); x ends in c->X0
+int pcg_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, int precond, npsd_b200_report* rep) {
+    require(cfg->tol_reduction > 0.0 && cfg->tol_reduction < 1.0, "SolveConfig: tol_reduction must lie in (0,1)");
+    require(precond == 0 || precond == 1, "pcg: preconditioner must be 0 (identity) or 1 (jacobi)");
+    require(!cfg->nullspace_projection, "pcg: nullspace projection is not supported by the B200 build");
+    require(!c->slab.on, "pcg: not available on a z-slab context");
+    cudaStream_t s = c->s;
+    const Geom g = c->g0;
+    const size_t nb = (size_t)g.n * sizeof(double);
+    if (!c->cgP0) {
+        c->cgP0 = dalloc<double>((size_t)g.n);
+        c->cgP1 = dalloc<double>((size_t)g.n);
+        c->cgAp = dalloc<double>((size_t)g.n);
+        c->cgZ = dalloc<double>((size_t)g.n);
+        ++c->buf_gen;
+    }
+    if (precond == 1) {
+        // JacobiPrecond: a fluid cell without a non-solid neighbour has no diagonal
+        const long long row = first_zero_diag_row(c);
+        require(row < 0, "jacobi precond: zero diagonal at row " + std::to_string(row));
+    }
+    const long long max_iters = cfg->max_iters < 0 ? 0 : cfg->max_iters;
+    ensure_hist(c, max_iters + 1);
+    // the zero invariant of the directions, A p and z on this frame
+    for (double* v : {c->cgP0, c->cgP1, c->cgAp, c->cgZ}) CK(cudaMemsetAsync(v, 0, nb, s));
+    if (!c->cg_exec || c->cg_exec_kind != precond || c->cg_exec_gen != c->buf_gen || c->cg_exec_key != c->hist) {
+        if (c->dim == 3)
+            precond ? capture_cg_graph<3, true>(c) : capture_cg_graph<3, false>(c);
+        else
+            precond ? capture_cg_graph<2, true>(c) : capture_cg_graph<2, false>(c);
+    }
+    SolverState* h = c->st_host;
+    std::memset(h, 0, sizeof(SolverState));
+    h->tol_reduction = cfg->tol_reduction;
+    h->tol_abs = cfg->tol_abs;
+    h->max_iters = max_iters;
+    CK(cudaMemcpyAsync(c->st, h, sizeof(SolverState), cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(c->ev0, s));
+    CK(cudaGraphLaunch(c->cg_exec, s));
+    CK(cudaEventRecord(c->ev1, s));
+    CK(cudaMemcpyAsync(h, c->st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    const long long iters = h->breakdown ? h->k - 1 : ((h->k > 1) ? h->k - 1 : 0);
+    const long long hl = iters + 1;
+    ensure_hist_host(c, hl);
+    CK(cudaMemcpyAsync(c->hist_host, c->hist, (size_t)hl * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->times_host, c->times, (size_t)hl * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->report_hist.assign(c->hist_host, c->hist_host + hl);
+    c->report_times.assign(c->times_host, c->times_host + hl);
+    c->last_launches = 2 + 2 * iters;
+    c->launches += c->last_launches;
+    if (rep) {
+        rep->iterations = iters;
+        rep->converged = h->converged;
+        rep->breakdown = h->breakdown;
+        rep->residual_history = c->report_hist.data();
+        rep->cumulative_seconds = c->report_times.data();
+        rep->history_len = hl;
+        rep->setup_seconds = 0.0;
+        rep->iterate_seconds = c->last_ms * 1e-3;
+        rep->precond_seconds = 0.0;
+    }
+    if (h->breakdown) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "pcg: non-positive curvature p'Ap = %f at iteration %lld", h->bad_value, h->k);
+        throw Breakdown(buf);
+    }
+    return NPSD_OK;
+}
+
 int solve_any(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_report* rep) {
     if (c->slab.on) return slab_solve_impl<3>(c, cfg, rep);
     return (c->dim == 3) ? solve_device_impl<3>(c, cfg, rep) : solve_device_impl<2>(c, cfg, rep);
@@ -1414,6 +1561,11 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->slab.all);
     F(c->slab.allu);
     F(c->mac);
+    F(c->cgP0);
+    F(c->cgP1);
+    F(c->cgAp);
+    F(c->cgZ);
+    if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
     if (c->slab_exec) cudaGraphExecDestroy(c->slab_exec);
     for (SchedBufs* sb : {&c->sch_stencil, &c->sch_down0}) {
         F(sb->pre);
@@ -2100,6 +2252,60 @@ int npsd_b200_psdo_solve(npsd_b200_ctx* c, const double* b, const double* x0, co
         const double* xr = c->st_host->xcur ? c->X1 : c->X0;
         LAUNCH(c, c->s, k_gather, g.n, g, cls, c->fmask, c->fbase, xr, c->red_b);
         CK(cudaMemcpyAsync(x, c->red_b, nf * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_pcg_solve(npsd_b200_ctx* c, const double* b, const double* x0, const npsd_b200_solve_cfg* cfg,
+                        int precond, double* x, npsd_b200_report* rep) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(cfg != nullptr && b != nullptr && x != nullptr, "solve: null argument");
+        if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
+        const Geom g = c->g0;
+        const uint8_t* cls = c->L[0].cls;
+        const size_t nf = (size_t)c->n_fluid;
+        bool finite = true;
+        for (size_t i = 0; i < nf; ++i) finite &= std::isfinite(b[i]);
+        require(finite, "solve: rhs has non-finite entries");
+        CK(cudaMemcpyAsync(c->red_a, b, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        LAUNCH(c, c->s, k_scatter, g.n, g, cls, c->fmask, c->fbase, c->red_a, c->Bf);
+        if (x0) {
+            CK(cudaMemcpyAsync(c->red_b, x0, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
+            LAUNCH(c, c->s, k_scatter, g.n, g, cls, c->fmask, c->fbase, c->red_b, c->X0);
+        } else {
+            CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
+        }
+        auto gather = [&] {
+            LAUNCH(c, c->s, k_gather, g.n, g, cls, c->fmask, c->fbase, c->X0, c->red_b);
+            CK(cudaMemcpyAsync(x, c->red_b, nf * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+        };
+        try {
+            pcg_solve_impl(c, cfg, precond, rep);
+        } catch (const Breakdown&) {
+            gather();
+            throw;
+        }
+        gather();
+    });
+}
+
+int npsd_b200_pcg_solve_device(npsd_b200_ctx* c, const double* d_b, const double* d_x0,
+                               const npsd_b200_solve_cfg* cfg, int precond, double* d_x, npsd_b200_report* rep) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(cfg != nullptr && d_b != nullptr && d_x != nullptr, "solve: null argument");
+        if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
+        const Geom g = c->g0;
+        const uint8_t* cls = c->L[0].cls;
+        LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_b, c->Bf);
+        if (d_x0)
+            LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_x0, c->X0);
+        else
+            CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
+        pcg_solve_impl(c, cfg, precond, rep);
+        CK(cudaMemcpyAsync(d_x, c->X0, (size_t)g.n * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
         CK(cudaStreamSynchronize(c->s));
     });
 }

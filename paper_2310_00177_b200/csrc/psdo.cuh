@@ -103,6 +103,17 @@ __global__ void __launch_bounds__(kBlock) k_mac_rhs(Geom g, const uint8_t* __res
     }
 }
 
+// JacobiPrecond's check (precond.cpp:15-18): the smallest reduced row index of
+// a fluid cell with a zero diagonal (no non-solid face neighbour), or none
+__global__ void __launch_bounds__(kBlock) k_zero_diag(Geom g, const uint8_t* __restrict__ cls,
+                                                      const uint32_t* __restrict__ fmask,
+                                                      const uint32_t* __restrict__ fbase, unsigned int* __restrict__ row) {
+    FOR_OWNED(g, c) {
+        const uint8_t b = cls[c];
+        if (cls_type(b) == 0 && cls_diag(b) == 0) atomicMin(row, (unsigned int)mixed_index(fmask, fbase, c));
+    }
+}
+
 // ---------------------------------------------------------------- operator
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_spmv(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ v,

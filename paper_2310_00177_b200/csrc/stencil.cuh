@@ -105,7 +105,7 @@ struct UpdateOp {
 template <typename Op>
 struct MarchSmem {
     double raw[Op::PF + 1][Op::NA][kVH][kVW];  // operand inputs, tile + halo
-    double ctr[Op::PF + 1][Op::NC][kTY][kTX];  // centre-only inputs
+    double ctr[Op::PF + 1][Op::NC > 0 ? Op::NC : 1][kTY][kTX];  // centre-only inputs
     double v[4][kVH][kVW];              // operand ring
 };
 
@@ -243,7 +243,7 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
                                            S.v[vc][r0][c0 + 2], S.v[vc][r0 + 1][c0 + 1], zp1)
                                  : 0.0;
             const int sl = slot(z);
-            double raw0[Op::NA], raw1[Op::NA], c0v[Op::NC], c1v[Op::NC];
+            double raw0[Op::NA], raw1[Op::NA], c0v[Op::NC > 0 ? Op::NC : 1] = {}, c1v[Op::NC > 0 ? Op::NC : 1] = {};
 #pragma unroll
             for (int a = 0; a < Op::NA; ++a) {
                 raw0[a] = S.raw[sl][a][r0][c0];

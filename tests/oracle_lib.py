@@ -234,6 +234,8 @@ class Ref:
         L.ref_rhs_normal.argtypes = [C.c_ulonglong, C.c_long, _f64p]
         L.ref_init_params_2d.argtypes = [C.c_int, C.c_ulonglong, _f32p]
         L.ref_save_npm_2d.argtypes = [C.c_int, C.c_ulonglong, C.c_char_p]
+        L.ref_pcg_solve.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, C.c_int, _f64p, C.c_double, C.c_long,
+                                    _f64p, _f64p, C.POINTER(C.c_long), C.POINTER(C.c_int), C.POINTER(C.c_long)]
         L.ref_mac_rhs_2d.argtypes = [C.c_long, C.c_long, _u8p, _f64p, _f64p, C.c_double, C.c_double, C.c_double,
                                      C.c_void_p, C.c_void_p, _f64p]
         L.ref_load_npm_2d.argtypes = [C.c_char_p, _f32p, C.c_long, C.POINTER(C.c_int)]
@@ -261,6 +263,15 @@ class Ref:
         out = np.empty(n, np.float32)
         self._check(self.lib.ref_init_params_2d(depth, seed, out))
         return out
+
+    def pcg_solve(self, types, b, precond=0, tol_reduction=1e-6, max_iters=1000) -> dict:
+        dim, (nx, ny, nz) = _dims_of(types)
+        b = np.ascontiguousarray(b, np.float64)
+        x, hist = np.empty_like(b), np.zeros(max_iters + 1)
+        it, conv, hl = C.c_long(), C.c_int(), C.c_long()
+        self._check(self.lib.ref_pcg_solve(dim, nx, ny, nz, _u8(types), precond, b, tol_reduction, max_iters, x, hist,
+                                           C.byref(it), C.byref(conv), C.byref(hl)))
+        return {"x": x, "iterations": it.value, "converged": bool(conv.value), "residual_history": hist[:hl.value]}
 
     def mac_rhs_2d(self, types, u, v, h=1.0, dt=0.05, rho=1.0, bc=None) -> np.ndarray:
         ny, nx = types.shape

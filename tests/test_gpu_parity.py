@@ -388,3 +388,21 @@ def test_mac_rhs_device_pipeline(b200, oracle):
     assert np.array_equal(xf[t.reshape(-1) == 0], host.x)
     for bf in (*bufs, db, dx):
         bf.free()
+
+
+@pytest.mark.parametrize("name,n,precond", [("C1", 32, "identity"), ("C3", 32, "jacobi"), ("C2", 32, "jacobi")])
+def test_pcg_iteration_parity_vs_reference(b200, oracle, ref, name, n, precond):
+    """pcg_solve (solver.cpp:36-102) on the device, identity (cg_solve) and
+    Jacobi: iterations to 1e-6 within +-1 of the reference's own pcg_solve on
+    the reference assembly; residual histories agree early and closely."""
+    t, seed = scenes.config(name, n)
+    b = oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    want = ref.pcg_solve(t, b, precond=1 if precond == "jacobi" else 0, max_iters=3000)
+    ctx = b200.Context(3, t.shape, b200.identity_params(4))
+    ctx.set_mask(t)
+    got = ctx.pcg_solve(b, b200.SolveConfig(max_iters=3000), precond=precond)
+    assert got.report.converged and want["converged"]
+    assert abs(got.report.iterations - want["iterations"]) <= 1
+    h, w = got.report.residual_history, want["residual_history"]
+    assert np.max(np.abs(h[:30] - w[:30]) / w[:30]) <= 1e-9
+    assert rel_l2(got.x, want["x"]) <= 1e-5
