@@ -140,17 +140,34 @@ def workload(args):
     return types, seed
 
 
-def iteration_count_fixture(config: str) -> int | None:
+WEIGHTS = ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm"
+
+
+def load_weights(kind: str, depth: int):
+    import paper_2310_00177_b200 as b200
+
+    if kind == "trained":
+        w = b200.load_npm(WEIGHTS)
+        if w.depth != depth:
+            raise SystemExit(f"trained weights have depth {w.depth}, not {depth}")
+        return w
+    if kind == "random":
+        return b200.init_params(depth, 42)
+    return b200.identity_params(depth)
+
+
+def iteration_count_fixture(config: str, weights: str = "identity") -> int | None:
     p = ROOT / "tests" / "golden" / "iteration_counts.json"
+    key = f"{config}_trained" if weights == "trained" else config
     if p.exists():
         d = json.loads(p.read_text())
-        if config in d:
-            return int(d[config]["iterations"])
+        if key in d:
+            return int(d[key]["iterations"])
     return None
 
 
 # ------------------------------------------------------------- CPU legs
-def cpu_reference_sample(types, seed, depth, iters_to_solution, sample_iters, cores):
+def cpu_reference_sample(types, seed, depth, iters_to_solution, sample_iters, cores, weights="identity"):
     """Reference psdo_solve (oracle/_ref: the unmodified reference solver,
     assembly and reduce, with the 3D network restatement as its
     Preconditioner) on a bounded sample: full setup + `sample_iters` PSDO
@@ -163,7 +180,7 @@ def cpu_reference_sample(types, seed, depth, iters_to_solution, sample_iters, co
     ref = Ref()
     import paper_2310_00177_b200 as b200
 
-    p = b200.identity_params(depth).flat
+    p = load_weights(weights, depth).flat
     b = ref.rhs_normal(seed, types.size)[types.reshape(-1) == 0]
     t0 = time.perf_counter()
     r = ref.psdo_solve(types, b, mode="neural", params=p, depth=depth, max_iters=sample_iters,
@@ -176,7 +193,8 @@ def cpu_reference_sample(types, seed, depth, iters_to_solution, sample_iters, co
         "unit": UNIT,
         "cores": cores,
         "kind": "reference",
-        "sample": (f"{types.shape[0]}^3 {args_config_name}: reference assemble_poisson_3d+reduce+NeuralPrecond3D setup "
+        "sample": (f"{types.shape[0]}^3 {args_config_name}, {weights} weights: reference assemble_poisson_3d+reduce+"
+                   "NeuralPrecond3D setup "
                    f"({setup_ms:.0f} ms) + {sample_iters} PSDO iterations ({per_iter_ms:.1f} ms/iter); TTS = setup + "
                    f"{iters_to_solution} iterations x per-iter (extrapolated); {wall:.1f} s wall"),
         "setup_ms": setup_ms,
@@ -195,13 +213,13 @@ def run_reference(args) -> None:
     global args_config_name
     args_config_name = args.config
     types, seed = workload(args)
-    n_iters = iteration_count_fixture(args.config) if args.n is None else None
+    n_iters = iteration_count_fixture(args.config, args.weights) if args.n is None else None
     if n_iters is None:
         n_iters = args.ref_iters
     cores = os.cpu_count() or 1
     vals, samples = [], []
     for step in range(args.warmup + args.steps):
-        s = cpu_reference_sample(types, seed, args.depth, n_iters, args.cpu_sample_iters, cores)
+        s = cpu_reference_sample(types, seed, args.depth, n_iters, args.cpu_sample_iters, cores, args.weights)
         if step >= args.warmup:
             vals.append(s["value"])
             samples.append(s)
@@ -210,9 +228,10 @@ def run_reference(args) -> None:
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 solver / f32 network", "data": "synthetic",
-        "config": {"workload": f"{args.config} {types.shape[0]}^3 (SURVEY §8d)", "weights": "identity-equivalent",
+        "config": {"workload": f"{args.config} {types.shape[0]}^3 (SURVEY §8d)", "weights": args.weights,
                    "depth": args.depth, "iterations_to_solution": n_iters,
-                   "iterations_source": "tests/golden/iteration_counts.json (reference psdo_solve run to 1e-6)"},
+                   "iterations_source": "tests/golden/iteration_counts.json (reference psdo_solve run to 1e-6 with "
+                                        "the same weights)"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": samples[-1]["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -241,7 +260,7 @@ def run_b200(args) -> None:
     types, seed = workload(args)
     n_c = types.size
     depth = args.depth
-    params = b200.identity_params(depth) if args.weights == "identity" else b200.init_params(depth, 42)
+    params = load_weights(args.weights, depth)
     ctx = b200.Context(3, types.shape, params, device=local)
     bfull = scenes.full_rhs(types, seed, b200.rhs_normal)
     cfg = b200.SolveConfig(tol_reduction=1e-6, max_iters=args.max_iters, n_ortho=2)
@@ -332,6 +351,17 @@ def run_b200(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # the same frame with identity-equivalent weights (PSDO == CG, the network
+    # still runs in full): what the trained model buys
+    alt = {}
+    if args.weights != "identity":
+        ctx.set_params(b200.identity_params(depth))
+        t_alt = [step() for _ in range(2)][-1]
+        alt = {"weights": "identity", "tts_ms": t_alt[0], "iterations": int(t_alt[1].iterations),
+               "per_iter_ms": t_alt[2] / max(t_alt[1].iterations, 1)}
+        ctx.set_params(params)
+        ctx.set_mask_device(d_types.ptr)
+
     # the paper's comparison columns on the same device and frame: GPU CG and
     # Jacobi-PCG (pcg_solve, solver.cpp:36-109), device-resident inputs
     baselines = {}
@@ -348,7 +378,8 @@ def run_b200(args) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_sample(types, seed, depth, n_it, args.cpu_sample_iters, os.cpu_count() or 1)
+            cpu = cpu_reference_sample(types, seed, depth, n_it, args.cpu_sample_iters, os.cpu_count() or 1,
+                                       args.weights)
             cpu.pop("setup_ms", None)
             cpu.pop("per_iter_ms", None)
         except Exception as e:  # the baseline is reported, never required
@@ -389,6 +420,7 @@ def run_b200(args) -> None:
             "clocks": clocks,
             "cpu_baseline": cpu,
             "baselines_same_gpu": baselines,
+            "identity_weights_same_gpu": alt,
         }
         print(json.dumps(line), flush=True)
     for buf in (d_types, d_b, d_x):
@@ -436,7 +468,7 @@ def run_b200_slab(args, world: int, rank: int, local: int) -> None:
     depth = args.depth
     z0, nk = b200.partition(nz, world, depth)[rank]
     own = np.ascontiguousarray(types[z0:z0 + nk])
-    params = b200.identity_params(depth) if args.weights == "identity" else b200.init_params(depth, 42)
+    params = load_weights(args.weights, depth)
     ctx = b200.Context.slab(comm, rank, types.shape, z0, nk, params, device=local)
     bfull = scenes.full_rhs(types, seed, b200.rhs_normal)
     bown = np.ascontiguousarray(bfull.reshape(nz, ny, nx)[z0:z0 + nk]).reshape(-1)
@@ -560,7 +592,7 @@ def main() -> None:
     ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
     ap.add_argument("--n", type=int, default=None, help="override the grid size of the config")
     ap.add_argument("--depth", type=int, default=4)
-    ap.add_argument("--weights", default="identity", choices=["identity", "random"])
+    ap.add_argument("--weights", default="trained", choices=["trained", "identity", "random"])
     ap.add_argument("--max-iters", type=int, default=20000)
     ap.add_argument("--profile-iters", type=int, default=5)
     ap.add_argument("--cpu-sample-iters", type=int, default=2)

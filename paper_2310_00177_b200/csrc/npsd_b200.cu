@@ -1651,6 +1651,7 @@ void do_set_params(npsd_b200_ctx* c, const float* params, size_t n) {
     else
         upload_params_and_kconst<2>(c);
     c->mask_ok = false;  // tables depend on the weights
+    ++c->buf_gen;        // captured graphs hold the uniform-window kernels by value
 }
 
 }  // namespace

@@ -3,7 +3,11 @@ REFERENCE psdo_solve (oracle/_ref: solver.cpp:189-276 on assemble_poisson_3d +
 reduce, IdentityPrecond — what identity-equivalent network weights reduce to,
 SURVEY.md §0.4) on the benchmark domains. bench.py's --impl reference arm uses
 the count to turn its bounded per-iteration sample into a time-to-solution.
-Run here (needs oracle/_ref); takes minutes at 256^3."""
+Run here (needs oracle/_ref); takes minutes at 256^3.
+
+With --trained: the reference psdo_solve with the 3D network restatement
+(NeuralPrecond3D) as its preconditioner and the committed trained weights
+(paper_2310_00177_b200/weights/npsd3d_L4.npm), entries "<name>_trained"."""
 import json
 import sys
 import time
@@ -19,14 +23,26 @@ from paper_2310_00177_b200 import scenes  # noqa: E402
 out = ROOT / "tests" / "golden" / "iteration_counts.json"
 res = json.loads(out.read_text()) if out.exists() else {}
 ref = Ref()
-for name in sys.argv[1:] or ["C1", "C2", "C3"]:
+args = [a for a in sys.argv[1:] if a != "--trained"]
+trained = "--trained" in sys.argv
+if trained:
+    import paper_2310_00177_b200 as b200
+
+    W = b200.load_npm(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm")
+for name in args or ["C1", "C2", "C3"]:
     t, seed = scenes.config(name)
     b = ref.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
     t0 = time.time()
-    r = ref.psdo_solve(t, b, mode="identity", max_iters=20000, tol_reduction=1e-6, n_ortho=2)
-    res[name] = {"n": int(t.shape[0]), "n_fluid": int(b.size), "iterations": r["iterations"],
-                 "converged": r["converged"], "final_rel_res": float(r["residual_history"][-1] / r["residual_history"][0]),
-                 "solver": "reference psdo_solve + IdentityPrecond, n_ortho=2, tol 1e-6",
-                 "cpu_seconds": time.time() - t0}
-    print(name, res[name], flush=True)
+    if trained:
+        r = ref.psdo_solve(t, b, mode="neural", params=W.flat, depth=W.depth, max_iters=20000, tol_reduction=1e-6,
+                           n_ortho=2)
+        key, solver = f"{name}_trained", ("reference psdo_solve + NeuralPrecond3D (restatement) with "
+                                          "weights/npsd3d_L4.npm, n_ortho=2, tol 1e-6")
+    else:
+        r = ref.psdo_solve(t, b, mode="identity", max_iters=20000, tol_reduction=1e-6, n_ortho=2)
+        key, solver = name, "reference psdo_solve + IdentityPrecond, n_ortho=2, tol 1e-6"
+    res[key] = {"n": int(t.shape[0]), "n_fluid": int(b.size), "iterations": r["iterations"],
+                "converged": r["converged"], "final_rel_res": float(r["residual_history"][-1] / r["residual_history"][0]),
+                "solver": solver, "cpu_seconds": time.time() - t0}
+    print(key, res[key], flush=True)
     out.write_text(json.dumps(res, indent=1) + "\n")

@@ -406,3 +406,48 @@ def test_pcg_iteration_parity_vs_reference(b200, oracle, ref, name, n, precond):
     h, w = got.report.residual_history, want["residual_history"]
     assert np.max(np.abs(h[:30] - w[:30]) / w[:30]) <= 1e-9
     assert rel_l2(got.x, want["x"]) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_trained_weights_iteration_parity(b200, name):
+    """The committed trained 3D model (weights/npsd3d_L4.npm): iterations to
+    1e-6 on the benchmark domains at their full sizes within +-1 of the
+    reference psdo_solve with the same weights (tests/golden/iteration_counts.json,
+    "<name>_trained", made by tests/golden/make_iteration_counts.py --trained)."""
+    import json
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    want = json.loads((root / "tests" / "golden" / "iteration_counts.json").read_text())[f"{name}_trained"]
+    W = b200.load_npm(root / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm")
+    t, seed = scenes.config(name)
+    ctx = b200.Context(3, t.shape, W)
+    ctx.set_mask(t)
+    b = b200.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    res = ctx.psdo_solve(b, b200.SolveConfig(max_iters=2000))
+    assert res.report.converged
+    assert abs(res.report.iterations - want["iterations"]) <= 1
+
+
+def test_set_params_between_solves(b200, oracle):
+    """set_params replaces every weight-dependent table and the captured solve
+    graph (it holds the uniform-window kernels by value): solving with weights
+    A, then B, then A again equals fresh contexts of A and B."""
+    t, seed = scenes.config("C3", 32)
+    b = oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    cfg = b200.SolveConfig(max_iters=30, tol_reduction=1e-300)
+    pa, pb = b200.init_params(4, 3), b200.identity_params(4)
+
+    def fresh(p):
+        c = b200.Context(3, t.shape, p)
+        c.set_mask(t)
+        return c.psdo_solve(b, cfg).report.residual_history
+
+    ha, hb = fresh(pa), fresh(pb)
+    ctx = b200.Context(3, t.shape, pa)
+    ctx.set_mask(t)
+    assert np.array_equal(ctx.psdo_solve(b, cfg).report.residual_history, ha)
+    for p, h in ((pb, hb), (pa, ha)):
+        ctx.set_params(p)
+        ctx.set_mask(t)
+        assert np.array_equal(ctx.psdo_solve(b, cfg).report.residual_history, h)
