@@ -103,9 +103,14 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "25"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # the timed region starts once samples are flowing (a step is ~20 ms)
+        t0 = time.time()
+        while time.time() - t0 < 5.0 and not Path(self.path).read_text().strip():
+            time.sleep(0.02)
 
     def stop(self) -> dict:
         if self.proc is None:
