@@ -300,6 +300,7 @@ struct npsd_b200_ctx {
     double *red_a = nullptr, *red_b = nullptr;
     float *xin_f = nullptr, *out_f = nullptr;  // raw-network buffers (lazy)
     double* mac = nullptr;                      // face arrays of the host mac_divergence_rhs (lazy)
+    unsigned int* check_flag = nullptr;         // device input checks
     char* l2pool = nullptr;                     // levels >= 1 per-cell arrays, L2-persisting window
     long long tab_cap[kMaxDepth] = {};          // kernel-row table capacity (rows) per level
     // pcg (cg.cuh): two direction buffers, A p, z (Jacobi); graph per preconditioner
@@ -1381,6 +1382,18 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
     return NPSD_OK;
 }
 
+// true when the device check kernel found nothing (one 4-byte readback)
+template <typename K, typename... Args>
+bool device_check(npsd_b200_ctx* c, K kernel, long long items, Args... args) {
+    unsigned int* flag = c->check_flag;
+    CK(cudaMemsetAsync(flag, 0, sizeof(unsigned int), c->s));
+    LAUNCH(c, c->s, kernel, items, args..., flag);
+    unsigned int h = 0;
+    CK(cudaMemcpyAsync(&h, flag, sizeof h, cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    return h == 0;
+}
+
 // ------------------------------------------------------------------- pcg
 // pcg_solve (solver.cpp:36-102) on the device: identity (cg_solve) or Jacobi.
 long long first_zero_diag_row(npsd_b200_ctx* c) {
@@ -1561,6 +1574,7 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->slab.all);
     F(c->slab.allu);
     F(c->mac);
+    F(c->check_flag);
     F(c->cgP0);
     F(c->cgP1);
     F(c->cgAp);
@@ -1805,6 +1819,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->crep = dalloc<uint32_t>((size_t)std::max<long long>(c->depth > 1 ? c->L[1].g.n : 1, 1));
         c->cnpat = dalloc<uint32_t>(1);
         c->cflag = dalloc<uint32_t>(1);
+        c->check_flag = dalloc<unsigned int>(1);
         c->ucnt0 = dalloc<uint32_t>(1);
         c->npat0 = dalloc<uint32_t>(1);
         const size_t n = (size_t)c->g0.n;
@@ -2002,15 +2017,17 @@ int npsd_b200_set_mask(npsd_b200_ctx* c, const uint8_t* types) {
     return guarded(c, [&] {
         require(types != nullptr, "npsd_b200: cell types pointer is null");
         const size_t n = c->slab.on ? (size_t)(c->g0.zo1 - c->g0.zo0) * c->g0.nx * c->g0.ny : (size_t)c->g0.n;
-        uint8_t worst = 0;  // plain loop: no per-element message construction
-        for (size_t i = 0; i < n; ++i) worst = types[i] > worst ? types[i] : worst;
-        require(worst <= 2, "npsd_b200: cell type out of range (0 fluid, 1 air, 2 solid)");
+        // the range check runs on the device, on the uploaded bytes
+        uint8_t* chk = reinterpret_cast<uint8_t*>(c->red_b);
+        CK(cudaMemcpyAsync(chk, types, n, cudaMemcpyHostToDevice, c->s));
+        require(device_check(c, k_check_types, (long long)n, (const uint8_t*)chk, (long long)n),
+                "npsd_b200: cell type out of range (0 fluid, 1 air, 2 solid)");
         if (c->slab.on) {
-            slab_stage_types(c, types, cudaMemcpyHostToDevice);
+            slab_stage_types(c, chk, cudaMemcpyDeviceToDevice);
             return;
         }
         uint8_t* d = reinterpret_cast<uint8_t*>(c->red_a);  // staging (n bytes <= 8n)
-        CK(cudaMemcpyAsync(d, types, n, cudaMemcpyHostToDevice, c->s));
+        CK(cudaMemcpyAsync(d, chk, n, cudaMemcpyDeviceToDevice, c->s));
         if (c->dim == 3)
             set_mask_impl<3>(c, d);
         else
@@ -2230,10 +2247,10 @@ int npsd_b200_psdo_solve(npsd_b200_ctx* c, const double* b, const double* x0, co
         const Geom g = c->g0;
         const uint8_t* cls = c->L[0].cls;
         const size_t nf = (size_t)c->n_fluid;
-        bool finite = true;  // check_inputs (solver.cpp:28-33), without per-element messages
-        for (size_t i = 0; i < nf; ++i) finite &= std::isfinite(b[i]);
-        require(finite, "solve: rhs has non-finite entries");
+        // check_inputs (solver.cpp:28-33) on the device, on the uploaded vector
         CK(cudaMemcpyAsync(c->red_a, b, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        require(device_check(c, k_check_finite, (long long)nf, (const double*)c->red_a, (long long)nf),
+                "solve: rhs has non-finite entries");
         LAUNCH(c, c->s, k_scatter, g.n, g, cls, c->fmask, c->fbase, c->red_a, c->Bf);
         if (x0) {
             CK(cudaMemcpyAsync(c->red_b, x0, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
@@ -2266,10 +2283,9 @@ int npsd_b200_pcg_solve(npsd_b200_ctx* c, const double* b, const double* x0, con
         const Geom g = c->g0;
         const uint8_t* cls = c->L[0].cls;
         const size_t nf = (size_t)c->n_fluid;
-        bool finite = true;
-        for (size_t i = 0; i < nf; ++i) finite &= std::isfinite(b[i]);
-        require(finite, "solve: rhs has non-finite entries");
         CK(cudaMemcpyAsync(c->red_a, b, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        require(device_check(c, k_check_finite, (long long)nf, (const double*)c->red_a, (long long)nf),
+                "solve: rhs has non-finite entries");
         LAUNCH(c, c->s, k_scatter, g.n, g, cls, c->fmask, c->fbase, c->red_a, c->Bf);
         if (x0) {
             CK(cudaMemcpyAsync(c->red_b, x0, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));

@@ -103,6 +103,31 @@ __global__ void __launch_bounds__(kBlock) k_mac_rhs(Geom g, const uint8_t* __res
     }
 }
 
+// Input checks on the device right after upload (check_inputs, solver.cpp:28-33;
+// the cell-type range): flag |= 1 for a non-finite value / a type > 2.
+__global__ void __launch_bounds__(kBlock) k_check_finite(const double* __restrict__ v, long long n,
+                                                         unsigned int* __restrict__ flag) {
+    bool bad = false;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        bad |= !isfinite(v[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+__global__ void __launch_bounds__(kBlock) k_check_types(const uint8_t* __restrict__ t, long long n,
+                                                        unsigned int* __restrict__ flag) {
+    bool bad = false;
+    const long long n4 = n / 4;
+    const uint32_t* t4 = reinterpret_cast<const uint32_t*>(t);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        const uint32_t w = t4[i];
+        bad |= ((w & 0xffu) > 2u) | (((w >> 8) & 0xffu) > 2u) | (((w >> 16) & 0xffu) > 2u) | ((w >> 24) > 2u);
+    }
+    for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        bad |= t[i] > 2;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
 // JacobiPrecond's check (precond.cpp:15-18): the smallest reduced row index of
 // a fluid cell with a zero diagonal (no non-solid face neighbour), or none
 __global__ void __launch_bounds__(kBlock) k_zero_diag(Geom g, const uint8_t* __restrict__ cls,
