@@ -582,7 +582,14 @@ template <int D>
 void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     cudaStream_t s = c->s;
     LevelBufs& L0 = c->L[0];
-    LAUNCH(c, s, k_setup_l0<D>, c->g0.n, c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
+    if (D == 3 && c->g0.nx % 32 == 0) {
+        const dim3 grid(c->g0.nx / 32, (c->g0.ny + 7) / 8, c->g0.nz);
+        k_setup_l0_tiled<<<grid, dim3(32, 8), 0, s>>>(c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
+        CK(cudaGetLastError());
+        ++c->launches;
+    } else {
+        LAUNCH(c, s, k_setup_l0<D>, c->g0.n, c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
+    }
     scan_u32(c, L0.mcount, L0.mbase, L0.nseg);
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
     LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
@@ -700,9 +707,9 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         }
         if (l < c->depth - 1) {
             const LevelOffsets& o = c->offs[(size_t)l];
-            LAUNCH(c, s, k_build_rows<D>, rows_cap, L.g, st, im, cells, ncells, c->d_params + o.down_W,
+            LAUNCH(c, s, k_build_rows<D>, rows_cap * 32, L.g, st, im, cells, ncells, c->d_params + o.down_W,
                    c->d_params + o.down_B, L.tab_down);
-            LAUNCH(c, s, k_build_rows<D>, rows_cap, L.g, st, im, cells, ncells, c->d_params + o.up_W,
+            LAUNCH(c, s, k_build_rows<D>, rows_cap * 32, L.g, st, im, cells, ncells, c->d_params + o.up_W,
                    c->d_params + o.up_B, L.tab_up);
             constexpr int NC = (D == 3) ? 27 : 9;
             CK(cudaMemsetAsync(L.zG, 0, 3 * NC * sizeof(unsigned long long), s));
@@ -714,7 +721,7 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
             CK(cudaGetLastError());
             ++c->launches;
         } else {
-            LAUNCH(c, s, k_build_rows<D>, rows_cap, L.g, st, im, cells, ncells, c->d_params + c->coarse_W,
+            LAUNCH(c, s, k_build_rows<D>, rows_cap * 32, L.g, st, im, cells, ncells, c->d_params + c->coarse_W,
                    c->d_params + c->coarse_B, L.tab_down);
         }
     }

@@ -74,6 +74,57 @@ __global__ void __launch_bounds__(kBlock) k_setup_l0(Geom g, const uint8_t* __re
     }
 }
 
+// The same cell bytes and masks, tiled (3D, nx a multiple of 32): a 32 x 8
+// block owns a 32 x 8 tile of one plane and stages the types of planes z-1..z+1
+// with a one-cell halo (outside the domain: solid) in shared memory; a warp is
+// one 32-cell row, i.e. one mask segment.
+__global__ void __launch_bounds__(256) k_setup_l0_tiled(Geom g, const uint8_t* __restrict__ types,
+                                                        uint8_t* __restrict__ cls, uint32_t* __restrict__ mmask,
+                                                        uint32_t* __restrict__ mcount, uint32_t* __restrict__ fmask,
+                                                        uint32_t* __restrict__ fcount) {
+    __shared__ uint8_t st[3][10][34];
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+    const int X0 = blockIdx.x * 32, Y0 = blockIdx.y * 8, z = blockIdx.z;
+    for (int i = tid; i < 3 * 10 * 34; i += 256) {
+        const int lx = i % 34, ly = (i / 34) % 10, lz = i / 340;
+        const int xx = X0 - 1 + lx, yy = Y0 - 1 + ly, zz = z - 1 + lz;
+        const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
+        st[lz][ly][lx] = in ? types[lin(g, xx, yy, zz)] : (uint8_t)2;
+    }
+    __syncthreads();
+    const int x = X0 + tx, y = Y0 + ty;
+    if (y >= g.ny) return;  // whole warp (rows)
+    const long long c = lin(g, x, y, z);
+    const int t = st[1][ty + 1][tx + 1];
+    bool uniform = true, wfluid = false;
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+                const int tt = st[dz][ty + dy][tx + dx];
+                uniform &= (tt == t);
+                wfluid |= (tt == 0);
+            }
+    // stencil diagonal: non-solid in-domain face neighbours (discretization.cpp:105-113);
+    // the staged outside is solid, so in-domain and non-solid is one test
+    const int diag = (st[0][ty + 1][tx + 1] != 2) + (st[1][ty][tx + 1] != 2) + (st[1][ty + 1][tx] != 2) +
+                     (st[1][ty + 1][tx + 2] != 2) + (st[1][ty + 2][tx + 1] != 2) + (st[2][ty + 1][tx + 1] != 2);
+    const int w = uniform ? t : 3;
+    cls[c] = (uint8_t)(w | (t << 2) | (diag << 4) | ((int)wfluid << 7));
+    const bool owned = c >= owned_lo(g) && c < owned_hi(g);
+    const uint32_t mm = __ballot_sync(0xffffffffu, !uniform && owned);
+    const uint32_t fm = __ballot_sync(0xffffffffu, t == 0 && owned);
+    if (tx == 0) {
+        const long long seg = c >> 5;
+        mmask[seg] = mm;
+        mcount[seg] = __popc(mm);
+        fmask[seg] = fm;
+        fcount[seg] = __popc(fm);
+    }
+}
+
 // Tile occupancy at L0: flags[(z * nty + ty) * ntx + tx] = any fluid cell in
 // the 32 x 8 tile (tx, ty) of plane z dilated by one cell in x and y. Kernels
 // OR the flags of their region (plus one plane each side in z) and skip
@@ -236,53 +287,59 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(Geom g, const uint8_t* __
                                                        const uint32_t* __restrict__ cells,
                                                        const uint32_t* __restrict__ count, const float* __restrict__ W,
                                                        const float* __restrict__ B, float* __restrict__ tab) {
+    // one warp per row: lanes t < S stage the window (3 channels), then lane s
+    // accumulates slot s in the reference order B[s] + sum_{ch, t} W[s,ch,t] I
     constexpr int S = Sh<D>::S;
+    constexpr int NW = kBlock / 32;
     __shared__ float sW[S * 3 * S];
     __shared__ float sB[S];
-    if ((long long)blockIdx.x * blockDim.x >= (long long)*count) return;  // grid sized for the capacity
+    __shared__ float win[NW][3][S];
+    const long long n = *count;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if ((long long)blockIdx.x * NW >= n) return;  // grid sized for the capacity
     for (int i = threadIdx.x; i < S * 3 * S; i += blockDim.x) sW[i] = W[i];
     for (int i = threadIdx.x; i < S; i += blockDim.x) sB[i] = B[i];
     __syncthreads();
-    const long long n = *count;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long ii = (long long)blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
+    for (long long ii = (long long)blockIdx.x * NW + wid; ii < n; ii += (long long)gridDim.x * NW) {
         const long long c = cells[ii];
         const int x = (int)(c % g.nx);
         const int y = (int)((c / g.nx) % g.ny);
         const int z = (int)(c / ((long long)g.nx * g.ny));
-        float win[3][S];
-#pragma unroll
-        for (int t = 0; t < S; ++t) {
+        if (lane < S) {
+            const int t = lane;
             const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = (D == 3) ? t / 9 - 1 : 0;
             const int xx = x + dx, yy = y + dy, zz = z + dz;
             const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
-            if (!in) {
-                win[0][t] = 0.0f;
-                win[1][t] = 0.0f;
-                win[2][t] = 1.0f;  // solid ring
-            } else {
+            float w0 = 0.0f, w1 = 0.0f, w2 = 1.0f;  // outside: the solid ring
+            if (in) {
                 const long long q = lin(g, xx, yy, zz);
                 if (src_types) {
                     const int tt = src_types[q];
-                    win[0][t] = (tt == 0) ? 1.0f : 0.0f;
-                    win[1][t] = (tt == 1) ? 1.0f : 0.0f;
-                    win[2][t] = (tt == 2) ? 1.0f : 0.0f;
+                    w0 = (tt == 0) ? 1.0f : 0.0f;
+                    w1 = (tt == 1) ? 1.0f : 0.0f;
+                    w2 = (tt == 2) ? 1.0f : 0.0f;
                 } else {
-                    win[0][t] = img[q];
-                    win[1][t] = img[g.n + q];
-                    win[2][t] = img[2 * g.n + q];
+                    w0 = img[q];
+                    w1 = img[g.n + q];
+                    w2 = img[2 * g.n + q];
                 }
             }
+            win[wid][0][t] = w0;
+            win[wid][1][t] = w1;
+            win[wid][2][t] = w2;
         }
-        for (int s = 0; s < S; ++s) {
-            float acc = sB[s];
-            const float* w = sW + s * 3 * S;
+        __syncwarp();
+        if (lane < S) {
+            const int sl = lane;
+            float acc = sB[sl];
+            const float* w = sW + sl * 3 * S;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
-                for (int t = 0; t < S; ++t) acc = __fadd_rn(acc, __fmul_rn(w[ch * S + t], win[ch][t]));
-            tab[ii * kRowW + s] = acc;
+                for (int t = 0; t < S; ++t) acc = __fadd_rn(acc, __fmul_rn(w[ch * S + t], win[wid][ch][t]));
+            tab[ii * kRowW + sl] = acc;
         }
+        __syncwarp();
     }
 }
 
