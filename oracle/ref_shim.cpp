@@ -15,6 +15,7 @@
 #include <memory>
 #include <string>
 
+#include "npsd/bench.hpp"
 #include "npsd/discretization.hpp"
 #include "npsd/net/forward.hpp"
 #include "npsd/net/precond.hpp"
@@ -153,6 +154,19 @@ int ref_mac_rhs_2d(long nx, long ny, const unsigned char* types, const double* u
         }
         const auto b = npsd::mac_divergence_rhs(vel, image_from_types(nx, ny, types), bu ? &bc : nullptr);
         std::memcpy(out, b.data(), b.size() * sizeof(double));
+    });
+}
+
+// the reference's bench CSV contract (bench.cpp:139-263): parse a rows.csv
+// with load_bench_rows, then write rows.csv / summary.csv / speedup_hist.csv
+// with the reference's writers into out_dir
+int ref_bench_roundtrip(const char* rows_csv, const char* out_dir) {
+    return guarded([&] {
+        npsd::BenchReport rep;
+        rep.rows = npsd::load_bench_rows(rows_csv);
+        rep.traces.resize(rep.rows.size());
+        npsd::write_bench_outputs(rep, out_dir);
+        npsd::write_bench_report(rep.rows, out_dir);
     });
 }
 

@@ -234,6 +234,7 @@ class Ref:
         L.ref_rhs_normal.argtypes = [C.c_ulonglong, C.c_long, _f64p]
         L.ref_init_params_2d.argtypes = [C.c_int, C.c_ulonglong, _f32p]
         L.ref_save_npm_2d.argtypes = [C.c_int, C.c_ulonglong, C.c_char_p]
+        L.ref_bench_roundtrip.argtypes = [C.c_char_p, C.c_char_p]
         L.ref_pcg_solve.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, C.c_int, _f64p, C.c_double, C.c_long,
                                     _f64p, _f64p, C.POINTER(C.c_long), C.POINTER(C.c_int), C.POINTER(C.c_long)]
         L.ref_mac_rhs_2d.argtypes = [C.c_long, C.c_long, _u8p, _f64p, _f64p, C.c_double, C.c_double, C.c_double,
@@ -282,6 +283,9 @@ class Ref:
                                             None if bu is None else bu.ctypes.data_as(C.c_void_p),
                                             None if bv is None else bv.ctypes.data_as(C.c_void_p), out))
         return out
+
+    def bench_roundtrip(self, rows_csv, out_dir) -> None:
+        self._check(self.lib.ref_bench_roundtrip(str(rows_csv).encode(), str(out_dir).encode()))
 
     def save_npm_2d(self, depth: int, seed: int, path) -> None:
         self._check(self.lib.ref_save_npm_2d(depth, seed, str(path).encode()))

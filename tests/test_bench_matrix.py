@@ -1,0 +1,35 @@
+"""The bench harness contract (bench.cpp:139-263) on the B200 side: our CSV
+writers produce the reference's bytes — the reference's own load_bench_rows
+parses our rows.csv and its writers reproduce rows.csv, summary.csv and
+speedup_hist.csv exactly; method tokens parse like parse_method_token."""
+import pytest
+
+from paper_2310_00177_b200 import bench_matrix as bm
+
+
+def test_method_tokens():
+    assert bm.parse_method_token("cg") == (True, "cg", "none")
+    assert bm.parse_method_token("psdo+neural") == (True, "psdo", "neural")
+    assert bm.parse_method_token("pcg+jacobi") == (True, "pcg", "jacobi")
+    assert bm.parse_method_token("pcg+foo")[0] is False
+    assert bm.parse_method_token("gmres")[0] is False
+
+
+@pytest.mark.ref
+def test_csv_bytes_match_reference_writers(ref, tmp_path):
+    rows = []
+    for si, system in enumerate(["C1_f000", "C2_f000", "C3_f001"]):
+        for mi, m in enumerate(["cg", "pcg+jacobi", "psdo+neural", "pcg+ic0"]):
+            r = bm.BenchRow(system, m, n_f=1000 + si, iterations=10 * (mi + 1) + si, converged=(m != "pcg+ic0"),
+                            setup_seconds=0.001 * (si + 1), iterate_seconds=0.25 / (mi + 1) + 0.01 * si,
+                            precond_seconds=0.0, final_rel_residual=9.7e-7 / (mi + 1))
+            r.total_seconds = r.setup_seconds + r.iterate_seconds
+            if m == "pcg+ic0":
+                r.error = "pcg+ic0: not available on the B200 device path"
+            rows.append(r)
+    ours, theirs = tmp_path / "ours", tmp_path / "theirs"
+    bm.write_bench_outputs(rows, ours)
+    bm.write_bench_report(rows, ours)
+    ref.bench_roundtrip(ours / "rows.csv", theirs)
+    for name in ("rows.csv", "summary.csv", "speedup_hist.csv"):
+        assert (ours / name).read_bytes() == (theirs / name).read_bytes(), name
