@@ -219,4 +219,225 @@ __global__ void __launch_bounds__(kKT, COARSE_MINB) k_cup(Geom g, Geom gc, const
     outl[c] = __fadd_rn(__fmul_rn(za, yv), __fmul_rn(zb, u));
 }
 
+
+// ---------------------------------------------------------------------------
+// z-marching variants (the launchers' default): a 32 x 8 block owns a 32 x 8
+// x-y tile and ZC consecutive planes; each thread marches its (x, y) column
+// through the ZC planes. The input box (tile + one-cell halo, ZC + 2 planes) is
+// staged once; the 3 x 3 x 3 window rolls through registers (9 new shared
+// loads per cell instead of 27) and the per-block index work is spread over
+// ZC cells per thread. Warps are 16 x 2 cells (lane = x + 16 y), so a 2 x 2
+// pooling quad sits inside one warp and the pool is summed with shuffles in
+// the reference order (no barrier). Shared rows are padded to 48 floats
+// (= 16 mod 32 banks): the two half-warps' rows fall on disjoint banks.
+// Accumulation order and rounding are those of the one-thread-per-cell
+// kernels above (slot order, __fmul_rn/__fadd_rn): bit-identical outputs.
+constexpr int kZX = 32, kZY = 8, kZT = kZX * kZY;  // block tile (x, y) = 256 threads
+constexpr int kZSP = 48;                           // padded shared row stride (floats)
+
+// (NZ x NY x NX) box at (bx, by, bz) of gg, zero outside the grid, staged
+// into dst[NZ][NY][kZSP]; one warp per row. load() issues every load (into
+// registers) so that other independent loads can be issued before store().
+template <int NX, int NY, int NZ>
+struct ZStager {
+    static constexpr int NW = kZT / 32, ROWS = NY * NZ, RPW = (ROWS + NW - 1) / NW, EPL = (NX + 31) / 32;
+    float v[RPW][EPL];
+    __device__ __forceinline__ void load(const float* __restrict__ src, const Geom& gg, int bx, int by, int bz,
+                                         int warp, int lane) {
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int r = warp + NW * k;
+            const int ly = r % NY, lz = r / NY;
+            const int gy = by + ly, gz = bz + lz;
+            const bool rin = r < ROWS && gy >= 0 && gy < gg.ny && gz >= 0 && gz < gg.nz;
+            const float* rowp = src + ((long long)(rin ? gz : 0) * gg.ny + (rin ? gy : 0)) * gg.nx;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+                const int lx = lane + 32 * e, gx = bx + lx;
+                v[k][e] = (rin && lx < NX && gx >= 0 && gx < gg.nx) ? __ldg(rowp + gx) : 0.0f;
+            }
+        }
+    }
+    __device__ __forceinline__ void store(float* dst, int warp, int lane) const {
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int r = warp + NW * k;
+            if (r < ROWS) {
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const int lx = lane + 32 * e;
+                    if (lx < NX) dst[r * kZSP + lx] = v[k][e];
+                }
+            }
+        }
+    }
+};
+
+// A cell's row code before its row pointer: levels >= 1 carry per-cell codes
+// (window class << 30 | row); the raw level-0 network has class bytes and the
+// mixed-index maps instead.
+__device__ __forceinline__ uint32_t cell_code(const ConvTab& ct, long long c, bool own) {
+    if (!own) return 1u << 30;  // uniform air
+    if (ct.rcode) return __ldg(ct.rcode + c);
+    return (uint32_t)cls_window(__ldg(ct.cls + c)) << 30;
+}
+__device__ __forceinline__ const float4* code_row(const ConvTab& ct, const UniRows& U, uint32_t rc, long long c) {
+    const int wc = (int)(rc >> 30);
+    if (wc < 3) return &U.r[wc][0];
+    if (ct.rcode) return reinterpret_cast<const float4*>(ct.tab + (long long)(rc & 0x3fffffffu) * kRowW);
+    return reinterpret_cast<const float4*>(kernel_row(ct, c));
+}
+
+// grid (ceil(nx/32), ceil(ny/8), ceil(owned planes/ZC)), block 256
+template <bool POOL, int ZC>
+__global__ void __launch_bounds__(kZT) k_cdownz(Geom g, const float* __restrict__ x, ConvTab ct,
+                                                const __grid_constant__ KC kc, float* __restrict__ y,
+                                                float* __restrict__ xnext, Geom gc, const int* __restrict__ done) {
+    pdl_launch_wait();
+    if (done && *done) return;  // z-slab chunked loop: the solve has finished
+    static_assert(!POOL || ZC % 2 == 0, "pooling pairs planes");
+    constexpr int SX = kZX + 2, SY = kZY + 2, SZ = ZC + 2, PL = SY * kZSP;
+    __shared__ __align__(16) float sx[SZ * PL];
+    __shared__ UniRows U;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tx = 16 * (warp & 1) + (lane & 15), ty = 2 * (warp >> 1) + (lane >> 4);
+    const int X0 = blockIdx.x * kZX, Y0 = blockIdx.y * kZY, Z0 = g.zo0 + blockIdx.z * ZC;
+    const int cx = X0 + tx, cy = Y0 + ty;
+    const bool oxy = cx < g.nx && cy < g.ny;
+    const long long plane = (long long)g.nx * g.ny;
+    const long long c0 = oxy ? lin(g, cx, cy, Z0) : 0;
+    const int nown = oxy ? min(ZC, g.zo1 - Z0) : 0;  // planes of this column the rank owns
+    // every load of the prologue is in flight before the first use
+    ZStager<SX, SY, SZ> box;
+    box.load(x, g, X0 - 1, Y0 - 1, Z0 - 1, warp, lane);
+    uint32_t rc[ZC];
+#pragma unroll
+    for (int k = 0; k < ZC; ++k) rc[k] = cell_code(ct, c0 + k * plane, k < nown);
+    load_uni_rows(U, kc, tid);
+    box.store(sx, warp, lane);
+    __syncthreads();
+    float kr[28];  // the next cell's kernel row (prefetched one cell ahead)
+    load_row(code_row(ct, U, rc[0], c0), kr);
+    const float* base = sx + ty * kZSP + tx;  // window (dz, dy, dx) at plane p: base[p*PL + (1+dy)*kZSP + 1+dx]
+    float P[3][9];                            // rolling planes: P[p % 3] = plane p's 3 x 3
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int j = 0; j < 9; ++j) P[p][j] = base[p * PL + (j / 3) * kZSP + (j % 3)];
+    float yprev = 0.0f;
+#pragma unroll
+    for (int k = 0; k < ZC; ++k) {
+#pragma unroll
+        for (int j = 0; j < 9; ++j) P[(k + 2) % 3][j] = base[(k + 2) * PL + (j / 3) * kZSP + (j % 3)];
+        const int z = Z0 + k;
+        const bool own = k < nown;
+        const long long c = c0 + k * plane;
+        float w[27];
+#pragma unroll
+        for (int s = 0; s < 27; ++s) w[s] = P[(k + s / 9) % 3][s % 9];
+        // branch-free (a cell outside the rank's planes reads the uniform-air
+        // row and is not stored), so the cells' chains can interleave
+        float yv = 0.0f;
+#pragma unroll
+        for (int s = 0; s < 27; ++s) yv = __fadd_rn(yv, __fmul_rn(kr[s], w[s]));
+        if (k + 1 < ZC) load_row(code_row(ct, U, rc[k + 1], c + plane), kr);
+        if (!own) yv = 0.0f;
+        if (own) y[c] = yv;
+        if (POOL) {
+            if (k & 1) {
+                // quad (x, y), (x+1, y), (x, y+1), (x+1, y+1) of planes z-1, z:
+                // lanes l, l+1, l+16, l+17; avg_pool2 order (x, then y, then z)
+                const float a1 = __shfl_down_sync(0xffffffffu, yprev, 1), a2 = __shfl_down_sync(0xffffffffu, yprev, 16),
+                            a3 = __shfl_down_sync(0xffffffffu, yprev, 17);
+                const float b1 = __shfl_down_sync(0xffffffffu, yv, 1), b2 = __shfl_down_sync(0xffffffffu, yv, 16),
+                            b3 = __shfl_down_sync(0xffffffffu, yv, 17);
+                const int qx = cx >> 1, qy = cy >> 1, qz = (z - 1) >> 1;
+                if ((lane & 17) == 0 && qx < gc.nx && qy < gc.ny && z - 1 < g.zo1) {
+                    float ps = yprev;
+                    ps = __fadd_rn(ps, a1);
+                    ps = __fadd_rn(ps, a2);
+                    ps = __fadd_rn(ps, a3);
+                    ps = __fadd_rn(ps, yv);
+                    ps = __fadd_rn(ps, b1);
+                    ps = __fadd_rn(ps, b2);
+                    ps = __fadd_rn(ps, b3);
+                    xnext[lin(gc, qx, qy, qz)] = __fmul_rn(0.125f, ps);
+                }
+            }
+            yprev = yv;
+        }
+    }
+}
+
+// grid (ceil(nx/32), ceil(ny/8), ceil(owned planes/ZC)), block 256; outc is level l+1
+template <int ZC>
+__global__ void __launch_bounds__(kZT) k_cupz(Geom g, Geom gc, const float* __restrict__ outc,
+                                              const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
+                                              const __grid_constant__ KC kc, float* __restrict__ outl,
+                                              const int* __restrict__ done) {
+    pdl_launch_wait();
+    if (done && *done) return;  // z-slab chunked loop: the solve has finished
+    static_assert(ZC % 2 == 0, "fine planes come in coarse pairs");
+    // coarse box: (X0/2 - 1 .. X0/2 + 16) x (Y0/2 - 1 .. Y0/2 + 4) x (Z0/2 - 1 .. Z0/2 + ZC/2)
+    constexpr int CX = kZX / 2 + 2, CY = kZY / 2 + 2, CZ = ZC / 2 + 2, PL = CY * kZSP;
+    __shared__ __align__(16) float sc[CZ * PL];
+    __shared__ UniRows U;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tx = 16 * (warp & 1) + (lane & 15), ty = 2 * (warp >> 1) + (lane >> 4);
+    const int X0 = blockIdx.x * kZX, Y0 = blockIdx.y * kZY, Z0 = g.zo0 + blockIdx.z * ZC;
+    const int cx = X0 + tx, cy = Y0 + ty;
+    const bool oxy = cx < g.nx && cy < g.ny;
+    const long long plane = (long long)g.nx * g.ny;
+    const long long c0 = oxy ? lin(g, cx, cy, Z0) : 0;
+    const int nown = oxy ? min(ZC, g.zo1 - Z0) : 0;  // planes of this column the rank owns
+    // every load of the prologue is in flight before the first use
+    ZStager<CX, CY, CZ> box;
+    box.load(outc, gc, (X0 >> 1) - 1, (Y0 >> 1) - 1, (Z0 >> 1) - 1, warp, lane);
+    uint32_t rc[ZC];
+    float yv[ZC];
+#pragma unroll
+    for (int k = 0; k < ZC; ++k) {
+        rc[k] = cell_code(ct, c0 + k * plane, k < nown);
+        yv[k] = k < nown ? __ldg(yl + c0 + k * plane) : 0.0f;
+    }
+    load_uni_rows(U, kc, tid);
+    const float za = zab[0], zb = zab[1];
+    box.store(sc, warp, lane);
+    __syncthreads();
+    float kr[28];  // the next cell's kernel row (prefetched one cell ahead)
+    load_row(code_row(ct, U, rc[0], c0), kr);
+    // fine tap (cx + dx, cy + dy) -> staged coarse ((cx + dx) >> 1) - (X0/2 - 1), likewise y;
+    // out-of-domain fine cells map to out-of-domain coarse cells (dims even): staged zeros
+    int off[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        const int dy = j / 3 - 1, dx = j % 3 - 1;
+        off[j] = (((ty + dy) >> 1) + 1) * kZSP + ((tx + dx) >> 1) + 1;  // X0, Y0 even
+    }
+    // coarse plane of fine tap (k + dz): ((k + dz) >> 1) + 1 in the box (Z0 even)
+    float Q[3][9];  // rolling coarse planes: Q[q % 3] = staged coarse plane q's 9 taps
+#pragma unroll
+    for (int j = 0; j < 9; ++j) Q[0][j] = sc[off[j]];
+#pragma unroll
+    for (int k = 0; k < ZC; ++k) {
+        const int qn = ((k + 1) >> 1) + 1;  // the new coarse plane this fine plane reaches
+        if (k == 0 || (k & 1)) {
+#pragma unroll
+            for (int j = 0; j < 9; ++j) Q[qn % 3][j] = sc[qn * PL + off[j]];
+        }
+        const long long c = c0 + k * plane;
+        float w[27];
+#pragma unroll
+        for (int s = 0; s < 27; ++s) {
+            const int dz = s / 9 - 1;
+            w[s] = Q[(((k + dz) >> 1) + 1) % 3][s % 9];
+        }
+        float u = 0.0f;
+#pragma unroll
+        for (int s = 0; s < 27; ++s) u = __fadd_rn(u, __fmul_rn(kr[s], w[s]));
+        if (k + 1 < ZC) load_row(code_row(ct, U, rc[k + 1], c + plane), kr);
+        if (k < nown) outl[c] = __fadd_rn(__fmul_rn(za, yv[k]), __fmul_rn(zb, u));
+    }
+}
+
 }  // namespace nb2

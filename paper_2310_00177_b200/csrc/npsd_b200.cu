@@ -257,6 +257,8 @@ struct npsd_b200_ctx {
     // programmatic dependent launch of the iteration kernels: measured neutral
     // in the solve graph (C3 256^3: 386.0 vs 384.8 ms), so opt-in (NPSD_PDL=1)
     bool pdl = false;
+    bool coarse_old = false;  // NPSD_COARSE_OLD=1: one-thread-per-cell coarse kernels (A/B)
+    int coarse_zc_max = 4;    // NPSD_COARSE_ZC: planes per block of the z-marching coarse kernels
     long long slab_chunk_launches = 0;
     cudaStream_t s = nullptr, s2 = nullptr;
     std::vector<float> params;
@@ -799,6 +801,16 @@ int zchunk_for(npsd_b200_ctx* c, K kernel, int threads, long long tiles_xy, int 
     return (int)zc;
 }
 
+// planes per block of the z-marching coarse kernels: as many as still leave
+// about four blocks per SM (small levels: short marches, more blocks)
+inline int coarse_zc(const npsd_b200_ctx* c, const Geom& g) {
+    const long long tiles = (long long)((g.nx + kZX - 1) / kZX) * ((g.ny + kZY - 1) / kZY);
+    const int nzo = g.zo1 - g.zo0;
+    int zc = c->coarse_zc_max;
+    while (zc > 2 && tiles * ((nzo + zc - 1) / zc) < 4LL * c->num_sms) zc /= 2;
+    return zc;
+}
+
 template <int D, bool L0, bool POOL>
 void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, const double* in_d) {
     LevelBufs& L = c->L[l];
@@ -807,9 +819,21 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
     if (D == 3 && !L0) {
         // f32 input (levels >= 1, raw level 0): one thread per cell (coarse.cuh)
         const KC& kc = (l == c->depth - 1) ? c->kc_coarse : c->kc_down[l];
-        const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
-        launch_pdl(c, s, k_cdown<POOL>, grid, dim3(kKX, kKY, kKZ), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc,
-                   c->slab.on ? &c->st->done : nullptr);
+        const int* dn = c->slab.on ? &c->st->done : nullptr;
+        if (c->coarse_old) {
+            const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
+            launch_pdl(c, s, k_cdown<POOL>, grid, dim3(kKX, kKY, kKZ), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext,
+                       gc, dn);
+            return;
+        }
+        const int zc = coarse_zc(c, L.g);
+        const dim3 grid((L.g.nx + kZX - 1) / kZX, (L.g.ny + kZY - 1) / kZY, (L.g.zo1 - L.g.zo0 + zc - 1) / zc);
+        if (zc == 8)
+            launch_pdl(c, s, k_cdownz<POOL, 8>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc, dn);
+        else if (zc == 4)
+            launch_pdl(c, s, k_cdownz<POOL, 4>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc, dn);
+        else
+            launch_pdl(c, s, k_cdownz<POOL, 2>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc, dn);
         return;
     }
     const dim3 block(kNX, kNY);
@@ -830,9 +854,24 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
     const LevelBufs& Lc = c->L[l + 1];
     const float* outc = (l + 1 == c->depth - 1) ? Lc.y : Lc.out;
     if (D == 3 && MODE == kUpMid) {
-        const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
-        launch_pdl(c, s, k_cup<3>, grid, dim3(kKX, kKY, kKZ), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
-                   c->kc_up[l], outl, c->slab.on ? &c->st->done : nullptr);
+        const int* dn = c->slab.on ? &c->st->done : nullptr;
+        if (c->coarse_old) {
+            const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
+            launch_pdl(c, s, k_cup<3>, grid, dim3(kKX, kKY, kKZ), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l,
+                       tab_up(c, l), c->kc_up[l], outl, dn);
+            return;
+        }
+        const int zc = coarse_zc(c, L.g);
+        const dim3 grid((L.g.nx + kZX - 1) / kZX, (L.g.ny + kZY - 1) / kZY, (L.g.zo1 - L.g.zo0 + zc - 1) / zc);
+        if (zc == 8)
+            launch_pdl(c, s, k_cupz<8>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
+                       c->kc_up[l], outl, dn);
+        else if (zc == 4)
+            launch_pdl(c, s, k_cupz<4>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
+                       c->kc_up[l], outl, dn);
+        else
+            launch_pdl(c, s, k_cupz<2>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
+                       c->kc_up[l], outl, dn);
         return;
     }
     const dim3 block(kNX, kNY);
@@ -1708,6 +1747,11 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->S = (dim == 3) ? 27 : 9;
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
+        if (const char* e = std::getenv("NPSD_COARSE_OLD")) c->coarse_old = (e[0] == '1');
+        if (const char* e = std::getenv("NPSD_COARSE_ZC")) {
+            const int v = std::atoi(e);
+            if (v == 2 || v == 4 || v == 8) c->coarse_zc_max = v;
+        }
         if (slab) {
             c->slab = *slab;
             for (int l = 0; l < depth; ++l) c->slab.ghost[l] = 1 << (depth - 1 - l);
@@ -1741,6 +1785,9 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
             }
             if (bytes) {
                 CK(cudaMalloc(&c->l2pool, bytes));
+                // zero: the z-slab ghost planes at the domain faces are never
+                // written and must read as the zero outside of the domain
+                CK(cudaMemset(c->l2pool, 0, bytes));
                 c->l2pool_bytes = bytes;
             }
         }
@@ -1777,7 +1824,10 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
             L.mcnt = dalloc<uint32_t>(1);
             L.kc_down = dalloc<float>(3 * (size_t)c->S);
             L.kc_up = dalloc<float>(3 * (size_t)c->S);
-            if (l == 0) L.y = dalloc<float>((size_t)L.g.n);
+            if (l == 0) {
+                L.y = dalloc<float>((size_t)L.g.n);
+                CK(cudaMemset(L.y, 0, (size_t)L.g.n * sizeof(float)));
+            }
             L.zG = dalloc<unsigned long long>(81);
         }
         if (c->l2pool) {
