@@ -413,10 +413,10 @@ def run_b200(args) -> None:
         ctx.set_params(params)
         ctx.set_mask_device(d_types.ptr)
 
-    # the paper's comparison columns on the same device and frame: GPU CG and
-    # Jacobi-PCG (pcg_solve, solver.cpp:36-109), device-resident inputs
+    # the paper's comparison columns on the same device and frame: GPU CG,
+    # Jacobi-PCG and IC0-PCG (pcg_solve, solver.cpp:36-109), device-resident inputs
     baselines = {}
-    for kind, name in (("identity", "gpu_cg"), ("jacobi", "gpu_pcg_jacobi")):
+    for kind, name in (("identity", "gpu_cg"), ("jacobi", "gpu_pcg_jacobi"), ("ic0", "gpu_pcg_ic0")):
         ms_k, it_k = [], []
         for i in range(2):
             rep_k = ctx.pcg_solve_device(d_b.ptr, d_x.ptr, cfg, precond=kind)
@@ -425,6 +425,8 @@ def run_b200(args) -> None:
                 it_k.append(rep_k.iterations)
         baselines[name] = {"solve_ms": float(np.mean(ms_k)), "iterations": int(it_k[-1]),
                            "per_iter_ms": float(np.mean(ms_k)) / max(it_k[-1], 1), "converged": bool(rep_k.converged)}
+    baselines["gpu_pcg_ic0"]["note"] = ("IC0 factor (per solve, level-scheduled) outside solve_ms; each apply is two "
+                                        "sweeps of one launch per hyperplane x+y+z=h (766 at 256^3)")
 
     seq = None
     if world == 1 and args.config == "C3" and args.n is None and not args.no_sequence:

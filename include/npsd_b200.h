@@ -137,13 +137,22 @@ void npsd_b200_rhs_normal(uint64_t seed, int64_t n, double* out);
 /* Preconditioned CG on the device, replacing pcg_solve / cg_solve
  * (solver.cpp:36-109): precond 0 = identity (cg_solve), 1 = Jacobi
  * (precond.cpp:12-26; NPSD_INVALID_ARGUMENT "jacobi precond: zero diagonal"
- * like the reference's constructor). Same vectors, report and errors as
+ * like the reference's constructor), 2 = IC0 (precond.cpp:28-112, see
+ * npsd_b200_ic0_apply; factored per solve on the current frame). Same vectors, report and errors as
  * psdo_solve; n_ortho and normalize_before_precond are ignored, nullspace
  * projection is not supported. The baseline the paper compares NPSDO with. */
 int npsd_b200_pcg_solve(npsd_b200_ctx* ctx, const double* b, const double* x0, const npsd_b200_solve_cfg* cfg,
                         int precond, double* x, npsd_b200_report* rep);
 int npsd_b200_pcg_solve_device(npsd_b200_ctx* ctx, const double* d_b, const double* d_x0,
                                const npsd_b200_solve_cfg* cfg, int precond, double* d_x, npsd_b200_report* rep);
+
+/* Ic0Precond (precond.cpp:28-112) on the current frame: the constructor's
+ * factorization (diagonal-shift retries; *shift_retries may be NULL) then
+ * apply(r, z): forward L y = r and backward L^T z = y, level-scheduled over
+ * the hyperplanes x + y + z = const. Bit-identical to the reference's loops;
+ * NPSD_INVALID_ARGUMENT "ic0: factorization failed after diagonal-shift
+ * retries" where the reference throws. */
+int npsd_b200_ic0_apply(npsd_b200_ctx* ctx, const double* r, double* z, int64_t n_f, int* shift_retries);
 
 /* Right-hand side from a MAC velocity field, replacing mac_divergence_rhs
  * (discretization.cpp:193-227) + reduce: b = -(rho*h/dt) * (signed sum of face

@@ -295,7 +295,7 @@ int ref_psdo_solve(int dim, long nx, long ny, long nz, const unsigned char* type
 }
 
 // Reference pcg_solve (solver.cpp:36-102) on the reference assembly:
-// precond 0 = IdentityPrecond (cg_solve), 1 = JacobiPrecond.
+// precond 0 = IdentityPrecond (cg_solve), 1 = JacobiPrecond, 2 = Ic0Precond.
 int ref_pcg_solve(int dim, long nx, long ny, long nz, const unsigned char* types, int precond, const double* b,
                   double tol_reduction, long max_iters, double* x_out, double* hist, long* iterations, int* converged,
                   long* hist_len) {
@@ -304,7 +304,9 @@ int ref_pcg_solve(int dim, long nx, long ny, long nz, const unsigned char* types
         const auto I = image_from_types(nx, rows, types);
         const auto A = assemble(dim, nx, ny, nz, I, types);
         const auto sys = npsd::reduce(A, npsd::Vector(static_cast<std::size_t>(A.n_rows), 0.0), I);
-        auto P = precond ? npsd::jacobi_precond(sys.A) : npsd::identity_precond(sys.A.n_rows);
+        auto P = precond == 2 ? npsd::ic0_precond(sys.A)
+                 : precond == 1 ? npsd::jacobi_precond(sys.A)
+                                : npsd::identity_precond(sys.A.n_rows);
         npsd::SolveConfig cfg;
         cfg.tol_reduction = tol_reduction;
         cfg.max_iters = max_iters;
@@ -316,6 +318,24 @@ int ref_pcg_solve(int dim, long nx, long ny, long nz, const unsigned char* types
         *iterations = static_cast<long>(res.report.iterations);
         *converged = res.report.converged ? 1 : 0;
         *hist_len = static_cast<long>(res.report.residual_history.size());
+    });
+}
+
+// Reference Ic0Precond (precond.cpp:28-112) on the reference assembly:
+// constructor (factorization with shift retries) + apply.
+int ref_ic0_apply(int dim, long nx, long ny, long nz, const unsigned char* types, const double* r, double* z,
+                  int* shift_retries) {
+    return guarded([&] {
+        const long rows = (dim == 3) ? ny * nz : ny;
+        const auto I = image_from_types(nx, rows, types);
+        const auto A = assemble(dim, nx, ny, nz, I, types);
+        const auto sys = npsd::reduce(A, npsd::Vector(static_cast<std::size_t>(A.n_rows), 0.0), I);
+        npsd::Ic0Precond P(sys.A);
+        const std::size_t nf = static_cast<std::size_t>(sys.A.n_rows);
+        npsd::Vector rv(r, r + nf), zv;
+        P.apply(rv, zv);
+        std::memcpy(z, zv.data(), nf * sizeof(double));
+        *shift_retries = P.shift_retries();
     });
 }
 

@@ -213,6 +213,10 @@ class Comm:
             self.h = None
 
 
+_PCG_KINDS = {"identity": 0, "jacobi": 1, "ic0": 2}
+_PCG_METHOD = {0: "cg", 1: "pcg+jacobi", 2: "pcg+ic0"}
+
+
 class Context:
     """One B200 context: grid, weights and (after set_mask) one frame."""
 
@@ -333,6 +337,15 @@ class Context:
         self._ck(self.lib.npsd_b200_precond_apply(self.h, r, z, r.size))
         return z
 
+    def ic0_apply(self, r: np.ndarray) -> tuple[np.ndarray, int]:
+        """Ic0Precond (precond.cpp:28-112) on the current frame: factor (with
+        the reference's diagonal-shift retries), then apply(r) -> (z, retries)."""
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        retries = C.c_int()
+        self._ck(self.lib.npsd_b200_ic0_apply(self.h, r, z, r.size, C.byref(retries)))
+        return z, retries.value
+
     def spmv(self, x: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(x, np.float64)
         y = np.empty_like(x)
@@ -397,8 +410,8 @@ class Context:
     def pcg_solve(self, b: np.ndarray, cfg: SolveConfig, precond: str = "identity", x0: np.ndarray | None = None,
                   out: np.ndarray | None = None) -> SolveResult:
         """pcg_solve / cg_solve (solver.cpp:36-109) on the device: precond
-        "identity" (method "cg") or "jacobi" ("pcg+jacobi")."""
-        kind = {"identity": 0, "jacobi": 1}[precond]
+        "identity" (method "cg"), "jacobi" ("pcg+jacobi") or "ic0" ("pcg+ic0")."""
+        kind = _PCG_KINDS[precond]
         b = np.ascontiguousarray(b, np.float64)
         if b.size != self.n_fluid:
             raise ValueError("solve: rhs length mismatch")
@@ -411,16 +424,16 @@ class Context:
         c = cfg._c()
         st = self.lib.npsd_b200_pcg_solve(self.h, b, x0p, C.byref(c), kind, x, C.byref(rep))
         self._ck(st)
-        return SolveResult(x, self._report(rep, "cg" if kind == 0 else "pcg+jacobi"))
+        return SolveResult(x, self._report(rep, _PCG_METHOD[kind]))
 
     def pcg_solve_device(self, b_ptr: int, x_ptr: int, cfg: SolveConfig, precond: str = "identity",
                          x0_ptr: int | None = None) -> SolveReport:
-        kind = {"identity": 0, "jacobi": 1}[precond]
+        kind = _PCG_KINDS[precond]
         rep = _native.Report()
         c = cfg._c()
         self._ck(self.lib.npsd_b200_pcg_solve_device(self.h, C.c_void_p(b_ptr), C.c_void_p(x0_ptr) if x0_ptr else None,
                                                      C.byref(c), kind, C.c_void_p(x_ptr), C.byref(rep)))
-        return self._report(rep, "cg" if kind == 0 else "pcg+jacobi")
+        return self._report(rep, _PCG_METHOD[kind])
 
     def psdo_solve_device(self, b_ptr: int, x_ptr: int, cfg: SolveConfig, x0_ptr: int | None = None,
                           method: str = "psdo+neural") -> SolveReport:

@@ -24,7 +24,7 @@ EXPORTED_SYMBOLS = (
     "npsd_b200_nccl_unique_id", "npsd_b200_comm_create_nccl", "npsd_b200_comm_create_local",
     "npsd_b200_comm_destroy", "npsd_b200_comm_last_error", "npsd_b200_create_slab", "npsd_b200_slab_graph",
     "npsd_b200_mac_divergence_rhs", "npsd_b200_mac_divergence_rhs_device", "npsd_b200_pcg_solve",
-    "npsd_b200_pcg_solve_device",
+    "npsd_b200_pcg_solve_device", "npsd_b200_ic0_apply",
 )
 
 
@@ -70,6 +70,7 @@ def lib() -> C.CDLL:
     L.npsd_b200_slab_graph.argtypes = [_vp]
     L.npsd_b200_pcg_solve.argtypes = [_vp, _f64p, _vp, C.c_void_p, C.c_int, _f64p, C.c_void_p]
     L.npsd_b200_pcg_solve_device.argtypes = [_vp, _vp, _vp, C.c_void_p, C.c_int, _vp, C.c_void_p]
+    L.npsd_b200_ic0_apply.argtypes = [_vp, _f64p, _f64p, C.c_int64, C.POINTER(C.c_int)]
     L.npsd_b200_mac_divergence_rhs.argtypes = [_vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp,
                                                _vp, _vp]
     L.npsd_b200_mac_divergence_rhs_device.argtypes = [_vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double, _vp,

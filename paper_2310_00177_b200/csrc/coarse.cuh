@@ -242,19 +242,24 @@ template <int NX, int NY, int NZ>
 struct ZStager {
     static constexpr int NW = kZT / 32, ROWS = NY * NZ, RPW = (ROWS + NW - 1) / NW, EPL = (NX + 31) / 32;
     float v[RPW][EPL];
+    // 32-bit offsets from the box's first plane (a box spans NZ planes, so
+    // they fit for any grid this library allocates)
     __device__ __forceinline__ void load(const float* __restrict__ src, const Geom& gg, int bx, int by, int bz,
                                          int warp, int lane) {
+        const float* p0 = src + (long long)bz * gg.nx * gg.ny + bx;
+        const int wly = warp % NY, wlz = warp / NY;
 #pragma unroll
         for (int k = 0; k < RPW; ++k) {
-            const int r = warp + NW * k;
-            const int ly = r % NY, lz = r / NY;
+            // row r = warp + NW k: (ly, lz) advanced from the warp's own (ly, lz)
+            const int t = wly + (NW * k) % NY;
+            const int ly = t - (t >= NY ? NY : 0), lz = wlz + (NW * k) / NY + (t >= NY ? 1 : 0);
             const int gy = by + ly, gz = bz + lz;
-            const bool rin = r < ROWS && gy >= 0 && gy < gg.ny && gz >= 0 && gz < gg.nz;
-            const float* rowp = src + ((long long)(rin ? gz : 0) * gg.ny + (rin ? gy : 0)) * gg.nx;
+            const bool rin = (warp + NW * k) < ROWS && (unsigned)gy < (unsigned)gg.ny && (unsigned)gz < (unsigned)gg.nz;
+            const float* rowp = p0 + (lz * gg.ny + gy) * gg.nx;
 #pragma unroll
             for (int e = 0; e < EPL; ++e) {
-                const int lx = lane + 32 * e, gx = bx + lx;
-                v[k][e] = (rin && lx < NX && gx >= 0 && gx < gg.nx) ? __ldg(rowp + gx) : 0.0f;
+                const int lx = lane + 32 * e;
+                v[k][e] = (rin && lx < NX && (unsigned)(bx + lx) < (unsigned)gg.nx) ? __ldg(rowp + lx) : 0.0f;
             }
         }
     }

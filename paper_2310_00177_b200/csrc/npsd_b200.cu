@@ -257,6 +257,9 @@ struct npsd_b200_ctx {
     // programmatic dependent launch of the iteration kernels: measured neutral
     // in the solve graph (C3 256^3: 386.0 vs 384.8 ms), so opt-in (NPSD_PDL=1)
     bool pdl = false;
+    double* icD = nullptr;    // IC0 factor diagonal (full grid)
+    int* icFail = nullptr;    // IC0 factorization failure flag (+ scratch)
+    int ic0_shift_retries = 0;
     bool coarse_old = false;  // NPSD_COARSE_OLD=1: one-thread-per-cell coarse kernels (A/B)
     int coarse_zc_max = 4;    // NPSD_COARSE_ZC: planes per block of the z-marching coarse kernels
     long long slab_chunk_launches = 0;
@@ -1453,8 +1456,58 @@ long long first_zero_diag_row(npsd_b200_ctx* c) {
     return row == none ? -1 : (long long)row;
 }
 
-template <int D, bool J>
+// ---- IC0 (precond.cpp:28-112): level-scheduled factor and sweeps
+inline int ic0_levels(const Geom& g) { return (g.nx - 1) + (g.ny - 1) + (g.nz - 1) + 1; }
+
+// one sweep (MODE 0 factor, 1 forward, 2 backward) as one launch per hyperplane
+template <int MODE>
+void ic0_sweep(npsd_b200_ctx* c, cudaStream_t s, double shift, const double* r, const SolverState* st) {
+    const Geom g = c->g0;
+    const int nl = ic0_levels(g);
+    const int blocks = (int)(((long long)g.ny * g.nz + kBlock - 1) / kBlock);
+    for (int i = 0; i < nl; ++i) {
+        const int h = (MODE == 2) ? nl - 1 - i : i;
+        k_ic0_level<MODE><<<blocks, kBlock, 0, s>>>(g, c->L[0].cls, h, shift, c->icD, r, c->cgZ, c->icFail, st);
+        CK(cudaGetLastError());
+        ++c->launches;
+    }
+}
+
+// Ic0Precond's constructor: factor with shift 0, then 1e-3 * mean diagonal,
+// doubling, at most 5 retries (precond.cpp:28-46); throws like the reference
+void ic0_factor(npsd_b200_ctx* c) {
+    cudaStream_t s = c->s;
+    if (!c->icD) {
+        c->icD = dalloc<double>((size_t)c->g0.n);
+        c->icFail = dalloc<int>(4);  // [0] failure flag, [2..3] diagonal sum
+    }
+    // sum of the diagonal over fluid rows: small integers, exact in any order
+    unsigned long long* dsum = reinterpret_cast<unsigned long long*>(c->icFail + 2);
+    CK(cudaMemsetAsync(c->icFail, 0, 4 * sizeof(int), s));
+    LAUNCH(c, s, k_diag_sum, c->g0.n, c->g0, c->L[0].cls, dsum);
+    unsigned long long sum = 0;
+    CK(cudaMemcpyAsync(&sum, dsum, sizeof sum, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double diag_mean = (double)sum / (double)std::max<long long>(c->n_fluid, 1);
+    double shift = 0.0;
+    for (int attempt = 0; attempt <= 5; ++attempt) {
+        CK(cudaMemsetAsync(c->icFail, 0, sizeof(int), s));
+        ic0_sweep<0>(c, s, shift, nullptr, nullptr);
+        int fail = 0;
+        CK(cudaMemcpyAsync(&fail, c->icFail, sizeof fail, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (!fail) {
+            c->ic0_shift_retries = attempt;
+            return;
+        }
+        shift = (shift == 0.0) ? 1e-3 * diag_mean : 2.0 * shift;
+    }
+    throw InvalidArgument("ic0: factorization failed after diagonal-shift retries");
+}
+
+template <int D, int M>
 void capture_cg_graph(npsd_b200_ctx* c) {
+    constexpr bool J = (M == kCgJacobi);
     if (c->cg_exec) {
         CK(cudaGraphExecDestroy(c->cg_exec));
         c->cg_exec = nullptr;
@@ -1462,7 +1515,7 @@ void capture_cg_graph(npsd_b200_ctx* c) {
     cudaStream_t s = c->s, s2 = c->s2;
     const Geom g = c->g0;
     const uint8_t* cls = c->L[0].cls;
-    double* z = J ? c->cgZ : c->R;
+    double* z = (M != kCgIdentity) ? c->cgZ : c->R;
     const long long before = c->launches;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     cudaStreamCaptureStatus cs;
@@ -1474,8 +1527,13 @@ void capture_cg_graph(npsd_b200_ctx* c) {
     CK(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
     // prologue: r0 = b - A x0, z0 = M r0, ||r0||, r0.z0
     LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R);
-    LAUNCH(c, s, (k_cg_update<J, true>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st, c->hist,
-           c->times, c->partials, c->counter, h, 1);
+    LAUNCH(c, s, (k_cg_update<M, true>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st, c->hist,
+           c->times, c->partials, c->counter, h, M == kCgIc0 ? 0 : 1);
+    if (M == kCgIc0) {
+        ic0_sweep<1>(c, s, 0.0, c->R, c->st);
+        ic0_sweep<2>(c, s, 0.0, c->R, c->st);
+        LAUNCH(c, s, k_cg_rz<true>, g.n, g, cls, c->R, c->cgZ, c->st, c->partials, c->counter, h, 1);
+    }
     CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
@@ -1493,8 +1551,13 @@ void capture_cg_graph(npsd_b200_ctx* c) {
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         LAUNCH3S(c, s2, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, g, cls, (const double*)z,
                  c->cgP0, c->cgP1, c->cgAp, c->st, c->partials, c->counter, c->sch_stencil.view());
-        LAUNCH(c, s2, (k_cg_update<J, false>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st,
-               c->hist, c->times, c->partials, c->counter, h, 1);
+        LAUNCH(c, s2, (k_cg_update<M, false>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st,
+               c->hist, c->times, c->partials, c->counter, h, M == kCgIc0 ? 0 : 1);
+        if (M == kCgIc0) {
+            ic0_sweep<1>(c, s2, 0.0, c->R, c->st);
+            ic0_sweep<2>(c, s2, 0.0, c->R, c->st);
+            LAUNCH(c, s2, k_cg_rz<false>, g.n, g, cls, c->R, c->cgZ, c->st, c->partials, c->counter, h, 1);
+        }
     }
     cudaGraph_t body_out = nullptr;
     CK(cudaStreamEndCapture(s2, &body_out));
@@ -1503,7 +1566,7 @@ void capture_cg_graph(npsd_b200_ctx* c) {
     CK(cudaGraphInstantiate(&c->cg_exec, graph, 0));
     CK(cudaGraphDestroy(graph));
     c->launches = before;
-    c->cg_exec_kind = J ? 1 : 0;
+    c->cg_exec_kind = M;
     c->cg_exec_gen = c->buf_gen;
     c->cg_exec_key = c->hist;
 }
@@ -1511,7 +1574,7 @@ void capture_cg_graph(npsd_b200_ctx* c) {
 // the solve on c->Bf / c->X0 (masked); x ends in c->X0
 int pcg_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, int precond, npsd_b200_report* rep) {
     require(cfg->tol_reduction > 0.0 && cfg->tol_reduction < 1.0, "SolveConfig: tol_reduction must lie in (0,1)");
-    require(precond == 0 || precond == 1, "pcg: preconditioner must be 0 (identity) or 1 (jacobi)");
+    require(precond >= 0 && precond <= 2, "pcg: preconditioner must be 0 (identity), 1 (jacobi) or 2 (ic0)");
     require(!cfg->nullspace_projection, "pcg: nullspace projection is not supported by the B200 build");
     require(!c->slab.on, "pcg: not available on a z-slab context");
     cudaStream_t s = c->s;
@@ -1529,15 +1592,21 @@ int pcg_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, int precond
         const long long row = first_zero_diag_row(c);
         require(row < 0, "jacobi precond: zero diagonal at row " + std::to_string(row));
     }
+    if (precond == 2) ic0_factor(c);  // Ic0Precond(A): per solve, on this frame
     const long long max_iters = cfg->max_iters < 0 ? 0 : cfg->max_iters;
     ensure_hist(c, max_iters + 1);
     // the zero invariant of the directions, A p and z on this frame
     for (double* v : {c->cgP0, c->cgP1, c->cgAp, c->cgZ}) CK(cudaMemsetAsync(v, 0, nb, s));
     if (!c->cg_exec || c->cg_exec_kind != precond || c->cg_exec_gen != c->buf_gen || c->cg_exec_key != c->hist) {
-        if (c->dim == 3)
-            precond ? capture_cg_graph<3, true>(c) : capture_cg_graph<3, false>(c);
-        else
-            precond ? capture_cg_graph<2, true>(c) : capture_cg_graph<2, false>(c);
+        if (c->dim == 3) {
+            if (precond == 0) capture_cg_graph<3, kCgIdentity>(c);
+            else if (precond == 1) capture_cg_graph<3, kCgJacobi>(c);
+            else capture_cg_graph<3, kCgIc0>(c);
+        } else {
+            if (precond == 0) capture_cg_graph<2, kCgIdentity>(c);
+            else if (precond == 1) capture_cg_graph<2, kCgJacobi>(c);
+            else capture_cg_graph<2, kCgIc0>(c);
+        }
     }
     SolverState* h = c->st_host;
     std::memset(h, 0, sizeof(SolverState));
@@ -1559,7 +1628,8 @@ int pcg_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, int precond
     CK(cudaStreamSynchronize(s));
     c->report_hist.assign(c->hist_host, c->hist_host + hl);
     c->report_times.assign(c->times_host, c->times_host + hl);
-    c->last_launches = 2 + 2 * iters;
+    const long long sweeps = (precond == 2) ? 2LL * ic0_levels(g) + 1 : 0;  // per preconditioner apply
+    c->last_launches = 2 + sweeps + (2 + sweeps) * iters;
     c->launches += c->last_launches;
     if (rep) {
         rep->iterations = iters;
@@ -1625,6 +1695,8 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->cgP1);
     F(c->cgAp);
     F(c->cgZ);
+    F(c->icD);
+    F(c->icFail);
     if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
     if (c->slab_exec) cudaGraphExecDestroy(c->slab_exec);
     for (SchedBufs* sb : {&c->sch_stencil, &c->sch_down0}) {
@@ -2148,6 +2220,32 @@ int npsd_b200_precond_apply(npsd_b200_ctx* c, const double* r, double* z, int64_
         else
             launch_network<2>(c, c->s, false, nullptr);
         LAUNCH(c, c->s, k_gather, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->Dtmp, c->red_b);
+        CK(cudaMemcpyAsync(z, c->red_b, (size_t)n_f * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_ic0_apply(npsd_b200_ctx* c, const double* r, double* z, int64_t n_f, int* shift_retries) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(!c->slab.on, "ic0: not available on a z-slab context");
+        require(n_f == c->n_fluid, "ic0: size mismatch");
+        if (n_f == 0) return;
+        const Geom g = c->g0;
+        if (!c->cgZ) {
+            c->cgP0 = dalloc<double>((size_t)g.n);
+            c->cgP1 = dalloc<double>((size_t)g.n);
+            c->cgAp = dalloc<double>((size_t)g.n);
+            c->cgZ = dalloc<double>((size_t)g.n);
+            ++c->buf_gen;
+        }
+        ic0_factor(c);
+        if (shift_retries) *shift_retries = c->ic0_shift_retries;
+        CK(cudaMemcpyAsync(c->red_a, r, (size_t)n_f * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        LAUNCH(c, c->s, k_scatter, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->red_a, c->R);
+        ic0_sweep<1>(c, c->s, 0.0, c->R, nullptr);
+        ic0_sweep<2>(c, c->s, 0.0, c->R, nullptr);
+        LAUNCH(c, c->s, k_gather, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->cgZ, c->red_b);
         CK(cudaMemcpyAsync(z, c->red_b, (size_t)n_f * sizeof(double), cudaMemcpyDeviceToHost, c->s));
         CK(cudaStreamSynchronize(c->s));
     });

@@ -237,6 +237,7 @@ class Ref:
         L.ref_bench_roundtrip.argtypes = [C.c_char_p, C.c_char_p]
         L.ref_pcg_solve.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, C.c_int, _f64p, C.c_double, C.c_long,
                                     _f64p, _f64p, C.POINTER(C.c_long), C.POINTER(C.c_int), C.POINTER(C.c_long)]
+        L.ref_ic0_apply.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, _f64p, _f64p, C.POINTER(C.c_int)]
         L.ref_mac_rhs_2d.argtypes = [C.c_long, C.c_long, _u8p, _f64p, _f64p, C.c_double, C.c_double, C.c_double,
                                      C.c_void_p, C.c_void_p, _f64p]
         L.ref_load_npm_2d.argtypes = [C.c_char_p, _f32p, C.c_long, C.POINTER(C.c_int)]
@@ -273,6 +274,14 @@ class Ref:
         self._check(self.lib.ref_pcg_solve(dim, nx, ny, nz, _u8(types), precond, b, tol_reduction, max_iters, x, hist,
                                            C.byref(it), C.byref(conv), C.byref(hl)))
         return {"x": x, "iterations": it.value, "converged": bool(conv.value), "residual_history": hist[:hl.value]}
+
+    def ic0_apply(self, types, r) -> tuple[np.ndarray, int]:
+        """Ic0Precond(A).apply(r) on the reference assembly -> (z, shift retries)."""
+        dim, (nx, ny, nz) = _dims_of(types)
+        r = np.ascontiguousarray(r, np.float64)
+        z, ret = np.empty_like(r), C.c_int()
+        self._check(self.lib.ref_ic0_apply(dim, nx, ny, nz, _u8(types), r, z, C.byref(ret)))
+        return z, ret.value
 
     def mac_rhs_2d(self, types, u, v, h=1.0, dt=0.05, rho=1.0, bc=None) -> np.ndarray:
         ny, nx = types.shape

@@ -390,14 +390,16 @@ def test_mac_rhs_device_pipeline(b200, oracle):
         bf.free()
 
 
-@pytest.mark.parametrize("name,n,precond", [("C1", 32, "identity"), ("C3", 32, "jacobi"), ("C2", 32, "jacobi")])
+@pytest.mark.parametrize("name,n,precond", [("C1", 32, "identity"), ("C3", 32, "jacobi"), ("C2", 32, "jacobi"),
+                                             ("C1", 32, "ic0"), ("C2", 32, "ic0"), ("C3", 48, "ic0")])
 def test_pcg_iteration_parity_vs_reference(b200, oracle, ref, name, n, precond):
-    """pcg_solve (solver.cpp:36-102) on the device, identity (cg_solve) and
-    Jacobi: iterations to 1e-6 within +-1 of the reference's own pcg_solve on
-    the reference assembly; residual histories agree early and closely."""
+    """pcg_solve (solver.cpp:36-102) on the device, identity (cg_solve),
+    Jacobi and IC0: iterations to 1e-6 within +-1 of the reference's own
+    pcg_solve on the reference assembly; residual histories agree early and
+    closely."""
     t, seed = scenes.config(name, n)
     b = oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
-    want = ref.pcg_solve(t, b, precond=1 if precond == "jacobi" else 0, max_iters=3000)
+    want = ref.pcg_solve(t, b, precond={"identity": 0, "jacobi": 1, "ic0": 2}[precond], max_iters=3000)
     ctx = b200.Context(3, t.shape, b200.identity_params(4))
     ctx.set_mask(t)
     got = ctx.pcg_solve(b, b200.SolveConfig(max_iters=3000), precond=precond)
@@ -406,6 +408,56 @@ def test_pcg_iteration_parity_vs_reference(b200, oracle, ref, name, n, precond):
     h, w = got.report.residual_history, want["residual_history"]
     assert np.max(np.abs(h[:30] - w[:30]) / w[:30]) <= 1e-9
     assert rel_l2(got.x, want["x"]) <= 1e-5
+
+
+def _ic0_cases():
+    yield scenes.config("C1", 16)[0]
+    yield scenes.config("C2", 32)[0]
+    yield scenes.config("C3", 24)[0]
+    yield scenes.config("C5", 32)[0]
+    t = scenes.random_types((12, 20, 28), 5, p=(0.7, 0.25, 0.05))
+    yield t
+    yield scenes.droplet_pool(16)[8]  # 2D slice (ny, nx)
+
+
+@pytest.mark.parametrize("k", range(6))
+def test_ic0_apply_bitwise_vs_reference(b200, ref, k):
+    """Ic0Precond (precond.cpp:28-112): the device factorization (level-
+    scheduled over hyperplanes) and both triangular sweeps equal the
+    reference's constructor + apply bit for bit, including its shift-retry
+    count."""
+    t = list(_ic0_cases())[k]
+    dim = t.ndim
+    ctx = b200.Context(dim, t.shape, b200.identity_params(2, dim))
+    ctx.set_mask(t)
+    r = np.random.default_rng(k).standard_normal(ctx.n_fluid)
+    try:
+        want, wret = ref.ic0_apply(t, r)
+    except Exception as e:  # the reference cannot factor this frame: neither may we
+        with pytest.raises(ValueError, match="ic0: factorization failed"):
+            ctx.ic0_apply(r)
+        pytest.skip(f"reference: {e}")
+    got, gret = ctx.ic0_apply(r)
+    assert gret == wret
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_ic0_isolated_cell_fails_like_reference(b200, ref):
+    """A fluid cell with only solid neighbours has no diagonal in its row: the
+    reference's factorization fails on every shift retry and throws."""
+    t = np.full((8, 8, 8), 2, np.uint8)
+    t[1:4, 1:7, 1:7] = 0
+    t[0, :, :] = 1
+    t[6, 4, 4] = 0  # isolated
+    ctx = b200.Context(3, t.shape, b200.identity_params(2))
+    ctx.set_mask(t)
+    r = np.ones(ctx.n_fluid)
+    with pytest.raises(Exception, match="ic0: factorization failed"):
+        ref.ic0_apply(t, r)
+    with pytest.raises(ValueError, match="ic0: factorization failed after diagonal-shift retries"):
+        ctx.ic0_apply(r)
+    with pytest.raises(ValueError, match="ic0: factorization failed"):
+        ctx.pcg_solve(r, b200.SolveConfig(max_iters=10), precond="ic0")
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3"])
