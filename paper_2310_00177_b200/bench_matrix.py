@@ -8,11 +8,11 @@ means) and `speedup_hist.csv` (speedup over `cg` on the same system, converged
 rows, bins 0 .. 64 and overflow) with the reference's column order and number
 formats, so the reference's own `load_bench_rows` reads them.
 
-Device methods: `cg`, `pcg+none|jacobi` (cg.cuh), `psd+neural|none`,
-`psdo+neural|none` (the network solve; `none` = identity-equivalent weights,
-the network's form of IdentityPrecond). `ic0` (level-scheduled triangular
-solves) and `fpcg` are not on the device path; their rows carry an error, like
-the reference's rows for failed methods.
+Device methods: `cg`, `pcg+none|jacobi|ic0` (cg.cuh; IC0 by level-scheduled
+triangular sweeps), `psd+neural|none`, `psdo+neural|none` (the network solve;
+`none` = identity-equivalent weights, the network's form of IdentityPrecond).
+`fpcg` and the classical preconditioners under psd/psdo are not on the device
+path; their rows carry an error, like the reference's rows for failed methods.
 
     python -m paper_2310_00177_b200.bench_matrix out_dir [--systems C1,C2,C3] [--methods cg,pcg+jacobi,psdo+neural]
 """
@@ -64,7 +64,7 @@ def run_one(ctx_for, system: str, types: np.ndarray, b: np.ndarray, token: str, 
     if not ok:
         row.error = "unknown method token"
         return row
-    if precond == "ic0" or solver == "fpcg":
+    if solver == "fpcg" or (precond == "ic0" and solver != "pcg"):
         row.error = f"{token}: not available on the B200 device path"
         return row
     try:
@@ -74,7 +74,7 @@ def run_one(ctx_for, system: str, types: np.ndarray, b: np.ndarray, token: str, 
         setup = time.perf_counter() - t0
         scfg = b200.SolveConfig(tol_reduction=cfg.tol_reduction, max_iters=cfg.max_iters, n_ortho=cfg.n_ortho)
         if solver in ("cg", "pcg"):
-            res = ctx.pcg_solve(b, scfg, precond="jacobi" if precond == "jacobi" else "identity")
+            res = ctx.pcg_solve(b, scfg, precond=precond if precond in ("jacobi", "ic0") else "identity")
         else:
             if solver == "psd":
                 scfg = b200.SolveConfig(tol_reduction=cfg.tol_reduction, max_iters=cfg.max_iters, n_ortho=0)

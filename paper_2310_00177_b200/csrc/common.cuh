@@ -312,15 +312,23 @@ struct Sched {
     const int* pre;  // [npiece + 1] exclusive prefix of the live lengths
     const int* zlo;  // [npiece] first live unit
     int npiece;      // pieces p = chunk * ncol + column
-    int ncol, ntx;   // columns x fastest: t = ty * ntx + tx
+    int ncol, ntx;   // (group) columns x fastest: t = ty * ntx + tx
+    int gx, gy;      // tiles per group column (x, y): its gx*gy blocks march together
+    int tnx, tny;    // tiles of the grid
 };
 
-// f(tx, ty, u0, u1) for each column segment of this block's share (block-uniform)
+// f(tx, ty, u0, u1) for each column segment of this block's share (block-uniform).
+// Columns are groups of gx x gy tiles; the gx*gy consecutive blocks of a group
+// take the same share of group-column units, one tile each, so neighbouring
+// tiles are marched at the same time and their halo rows and columns come
+// from L2 instead of DRAM.
 template <typename F>
 __device__ __forceinline__ void sched_for_each(const Sched& sc, F f) {
+    const int G = sc.gx * sc.gy, Q = gridDim.x / G, q = blockIdx.x / G, m = blockIdx.x - q * G;
+    if (q >= Q) return;
     const long long W = sc.pre[sc.npiece];
-    long long s = W * blockIdx.x / gridDim.x;
-    const long long e = W * (blockIdx.x + 1) / gridDim.x;
+    long long s = W * q / Q;
+    const long long e = W * (q + 1) / Q;
     if (s >= e) return;
     int lo = 0, hi = sc.npiece - 1;  // last piece with pre[t] <= s
     while (lo < hi) {
@@ -336,7 +344,8 @@ __device__ __forceinline__ void sched_for_each(const Sched& sc, F f) {
         const long long n = min(cend, e) - s;
         const int u0 = sc.zlo[t] + (int)(s - sc.pre[t]);
         const int col = t % sc.ncol;
-        f(col % sc.ntx, col / sc.ntx, u0, u0 + (int)n);
+        const int tx = (col % sc.ntx) * sc.gx + m % sc.gx, ty = (col / sc.ntx) * sc.gy + m / sc.gx;
+        if (tx < sc.tnx && ty < sc.tny) f(tx, ty, u0, u0 + (int)n);
         s += n;
     }
 }

@@ -88,7 +88,8 @@ struct LevelBufs {
 struct SchedBufs {
     int *pre = nullptr, *zlo = nullptr, *len = nullptr, *first = nullptr, *last = nullptr;
     int ncol = 0, ntx = 0, nchunk = 0, hu = 0, npiece = 0;
-    Sched view() const { return Sched{pre, zlo, npiece, ncol, ntx}; }
+    int gx = 1, gy = 1, tnx = 0, tny = 0;
+    Sched view() const { return Sched{pre, zlo, npiece, ncol, ntx, gx, gy, tnx, tny}; }
 };
 
 // offsets of one level's blocks inside the flat parameter vector
@@ -260,6 +261,8 @@ struct npsd_b200_ctx {
     double* icD = nullptr;    // IC0 factor diagonal (full grid)
     int* icFail = nullptr;    // IC0 factorization failure flag (+ scratch)
     int ic0_shift_retries = 0;
+    // tiles per schedule group (common.cuh Sched): stencil/up0 and down0 schedules
+    int sched_gx = 1, sched_gy = 1, sched0_gx = 1, sched0_gy = 1;
     bool coarse_old = false;  // NPSD_COARSE_OLD=1: one-thread-per-cell coarse kernels (A/B)
     int coarse_zc_max = 4;    // NPSD_COARSE_ZC: planes per block of the z-marching coarse kernels
     long long slab_chunk_launches = 0;
@@ -501,8 +504,9 @@ ConvTab tab_up(const npsd_b200_ctx* c, int l) {
 // Balanced schedule over the L0 tile columns of a tx x ty tiling (units of
 // `unit` planes, live within zdil planes of a fluid flag): k_sched_cols then
 // the prefix. Sizes are fixed per context; buffers are made on first use.
-void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int zdil) {
-    const int ntx = (c->g0.nx + tx - 1) / tx, nty = (c->g0.ny + ty - 1) / ty;
+void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int zdil, int gx, int gy) {
+    const int tnx = (c->g0.nx + tx - 1) / tx, tny = (c->g0.ny + ty - 1) / ty;
+    const int ntx = (tnx + gx - 1) / gx, nty = (tny + gy - 1) / gy;  // group columns
     // one piece per column: chunking columns into z pieces (chunk-major, so
     // halo rows come from L2) was measured slower — every piece restarts the
     // pipeline — so a piece is a whole column's live range
@@ -514,6 +518,10 @@ void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int 
         sb.nchunk = nchunk;
         sb.hu = hu;
         sb.npiece = sb.ncol * nchunk;
+        sb.gx = gx;
+        sb.gy = gy;
+        sb.tnx = tnx;
+        sb.tny = tny;
         sb.pre = dalloc<int>((size_t)sb.npiece + 1);
         sb.zlo = dalloc<int>((size_t)sb.npiece);
         sb.len = dalloc<int>((size_t)sb.npiece);
@@ -522,8 +530,8 @@ void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int 
     }
     const Geom& g = c->g0;
     k_col_range<<<(sb.ncol * 32 + kBlock - 1) / kBlock, kBlock, 0, c->s>>>(
-        c->tflags, c->tf_ntx, c->tf_nty, g.nz, g.zo0, g.zo1, tx / kFlagTX, ty / kFlagTY, ntx, nty, zdil, sb.first,
-        sb.last);
+        c->tflags, c->tf_ntx, c->tf_nty, g.nz, g.zo0, g.zo1, gx * tx / kFlagTX, gy * ty / kFlagTY, ntx, nty, zdil,
+        sb.first, sb.last);
     k_sched_pieces<<<(sb.npiece + kBlock - 1) / kBlock, kBlock, 0, c->s>>>(sb.first, sb.last, sb.ncol, sb.nchunk, sb.hu,
                                                                          g.zo0, g.zo1, unit, zdil, sb.zlo, sb.len);
     CK(cudaGetLastError());
@@ -599,8 +607,8 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
     LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
            c->tflags);
-    build_sched(c, c->sch_stencil, kTX, kTY, 1, 0);
-    if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1);
+    build_sched(c, c->sch_stencil, kTX, kTY, 1, 0, c->sched_gx, c->sched_gy);
+    if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1, c->sched0_gx, c->sched0_gy);
     c->x1_clean = false;
     for (int l = 1; l < c->depth; ++l) {
         LevelBufs& Lf = c->L[l - 1];
@@ -1820,6 +1828,16 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
         if (const char* e = std::getenv("NPSD_COARSE_OLD")) c->coarse_old = (e[0] == '1');
+        auto env_int = [](const char* n, int& v) {
+            if (const char* e = std::getenv(n)) {
+                const int x = std::atoi(e);
+                if (x >= 1 && x <= 16) v = x;
+            }
+        };
+        env_int("NPSD_SCHED_GX", c->sched_gx);
+        env_int("NPSD_SCHED_GY", c->sched_gy);
+        env_int("NPSD_SCHED0_GX", c->sched0_gx);
+        env_int("NPSD_SCHED0_GY", c->sched0_gy);
         if (const char* e = std::getenv("NPSD_COARSE_ZC")) {
             const int v = std::atoi(e);
             if (v == 2 || v == 4 || v == 8) c->coarse_zc_max = v;

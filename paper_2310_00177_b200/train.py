@@ -152,7 +152,7 @@ def smooth_rhs(geo: Geometry, nb: int, gen: torch.Generator, sweeps: int) -> tor
 
 
 def train(frames, depth: int, steps: int, lr: float, init: np.ndarray, nb: int, seed: int, device,
-          log=print) -> np.ndarray:
+          log=print, max_sweeps: int = 40) -> np.ndarray:
     """Adam on the flat parameter vector (adam_update, train.cpp:25-56)."""
     flat = torch.tensor(init, dtype=torch.float32, device=device, requires_grad=True)
     opt = torch.optim.Adam([flat], lr=lr, betas=(0.9, 0.999), eps=1e-8)
@@ -162,7 +162,7 @@ def train(frames, depth: int, steps: int, lr: float, init: np.ndarray, nb: int, 
     gen.manual_seed(seed)
     for step in range(steps):
         geo = geos[step % len(geos)]
-        sweeps = int(torch.randint(0, 40, (1,), generator=gen, device=device).item())
+        sweeps = int(torch.randint(0, max_sweeps, (1,), generator=gen, device=device).item())
         b = smooth_rhs(geo, nb, gen, sweeps)
         opt.zero_grad()
         L = loss(unflatten(flat, depth), geo, b, depth)

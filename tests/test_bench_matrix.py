@@ -19,13 +19,13 @@ def test_method_tokens():
 def test_csv_bytes_match_reference_writers(ref, tmp_path):
     rows = []
     for si, system in enumerate(["C1_f000", "C2_f000", "C3_f001"]):
-        for mi, m in enumerate(["cg", "pcg+jacobi", "psdo+neural", "pcg+ic0"]):
-            r = bm.BenchRow(system, m, n_f=1000 + si, iterations=10 * (mi + 1) + si, converged=(m != "pcg+ic0"),
+        for mi, m in enumerate(["cg", "pcg+jacobi", "psdo+neural", "fpcg+ic0"]):
+            r = bm.BenchRow(system, m, n_f=1000 + si, iterations=10 * (mi + 1) + si, converged=(m != "fpcg+ic0"),
                             setup_seconds=0.001 * (si + 1), iterate_seconds=0.25 / (mi + 1) + 0.01 * si,
                             precond_seconds=0.0, final_rel_residual=9.7e-7 / (mi + 1))
             r.total_seconds = r.setup_seconds + r.iterate_seconds
-            if m == "pcg+ic0":
-                r.error = "pcg+ic0: not available on the B200 device path"
+            if m == "fpcg+ic0":
+                r.error = "fpcg+ic0: not available on the B200 device path"
             rows.append(r)
     ours, theirs = tmp_path / "ours", tmp_path / "theirs"
     bm.write_bench_outputs(rows, ours)

@@ -61,7 +61,8 @@ def main() -> None:
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--depth", type=int, default=4)
-    ap.add_argument("--init", default="random", choices=["random", "identity"])
+    ap.add_argument("--init", default="random", help="random | identity | path of a dim-3 .npm to fine-tune")
+    ap.add_argument("--max-sweeps", type=int, default=40, help="RHS smoothing: 0..max damped-Jacobi sweeps")
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--big", type=int, default=0, help="extra 2n^3 training frames (scale robustness)")
     ap.add_argument("--eval256", action="store_true")
@@ -81,15 +82,21 @@ def main() -> None:
             if i % k == k - 1 and big:
                 frames.append(big.pop())
         frames += big
-    init = (b200.init_params(a.depth, a.seed) if a.init == "random" else b200.identity_params(a.depth)).flat
+    if a.init == "random":
+        init = b200.init_params(a.depth, a.seed).flat
+    elif a.init == "identity":
+        init = b200.identity_params(a.depth).flat
+    else:
+        init = b200.load_npm(a.init).flat
     t0 = time.time()
-    flat = train.train(frames, a.depth, a.steps, a.lr, init, a.batch, a.seed, dev)
+    flat = train.train(frames, a.depth, a.steps, a.lr, init, a.batch, a.seed, dev, max_sweeps=a.max_sweeps)
     wall = time.time() - t0
     params = b200.NetParams(3, a.depth, flat.astype(np.float32))
     out = Path(a.out)
     out.parent.mkdir(parents=True, exist_ok=True)
     b200.save_npm(params, out)
-    report = {"train_seconds": wall, "steps": a.steps, "frames": a.frames, "n": a.n, "init": a.init, "eval": {}}
+    report = {"train_seconds": wall, "steps": a.steps, "frames": a.frames, "n": a.n, "big_frames": a.big,
+              "init": a.init, "lr": a.lr, "batch": a.batch, "max_sweeps": a.max_sweeps, "seed": a.seed, "eval": {}}
     ident = b200.identity_params(a.depth)
     evals = [("C3", 64), ("C3", 128), ("C1", 64), ("C2", 128)] + ([("C3", 256)] if a.eval256 else [])
     for name, n in evals:
