@@ -263,6 +263,10 @@ struct npsd_b200_ctx {
     int ic0_shift_retries = 0;
     // tiles per schedule group (common.cuh Sched): stencil/up0 and down0 schedules
     int sched_gx = 1, sched_gy = 1, sched0_gx = 1, sched0_gy = 1;
+    unsigned long long* htk = nullptr;  // pattern hash table: keys, values (dedup_patterns)
+    uint32_t* htv = nullptr;
+    unsigned long long ht_cap = 0;
+    bool dict_sort = false;   // NPSD_DICT_SORT=1: pattern ids by radix sort + run heads (A/B)
     bool coarse_old = false;  // NPSD_COARSE_OLD=1: one-thread-per-cell coarse kernels (A/B)
     int coarse_zc_max = 4;    // NPSD_COARSE_ZC: planes per block of the z-marching coarse kernels
     long long slab_chunk_launches = 0;
@@ -557,11 +561,41 @@ int wave_blocks(npsd_b200_ctx* c, K kernel, int threads, size_t smem) {
 // Hashed window-pattern dictionary of coarse level l (setup.cuh): L.pid[mixed
 // index] = pattern, c->crep / c->cnpat = representative cells. Returns false
 // (per-cell rows) when any window differs from its pattern's representative.
+// Pattern ids of n keys (c->dkeys) by the hash table (setup.cuh k_dedup_*):
+// pid[i], rep[pattern] = its representative (list[i] of the inserting i), *npat.
+// The table (htk / htv, grow-only) holds > 2n slots; slots per key go to dvals.
+void dedup_patterns(npsd_b200_ctx* c, cudaStream_t s, uint32_t n, const uint32_t* count, const uint32_t* list,
+                    uint32_t* pid, uint32_t* rep, uint32_t* npat) {
+    // capacity > 2n: the table never holds more than n distinct keys, so probing ends
+    unsigned long long cap = 1;
+    while (cap < 2ull * n + 2) cap <<= 1;
+    if (cap > c->ht_cap) {  // grow only
+        if (c->htk) CK(cudaFree(c->htk));
+        if (c->htv) CK(cudaFree(c->htv));
+        c->htk = dalloc<unsigned long long>((size_t)cap);
+        c->htv = dalloc<uint32_t>((size_t)cap);
+        c->ht_cap = cap;
+    }
+    CK(cudaMemsetAsync(c->htk, 0xff, cap * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(npat, 0, sizeof(uint32_t), s));
+    LAUNCH(c, s, k_dedup_insert, (long long)n, c->dkeys, count, list, c->htk, c->htv, cap - 1, c->dvals, rep, npat);
+    LAUNCH(c, s, k_dedup_ids, (long long)n, c->dvals, count, c->htv, pid);
+}
+
 template <int D>
 bool coarse_dictionary(npsd_b200_ctx* c, int l, uint32_t n) {
     cudaStream_t s = c->s;
     LevelBufs& L = c->L[l];
     LAUNCH(c, s, k_window_hash<D>, (long long)n, L.g, L.img, L.mlist, L.mcnt, c->dkeys, c->dvals);
+    if (!c->dict_sort) {
+        dedup_patterns(c, s, n, L.mcnt, L.mlist, L.pid, c->crep, c->cnpat);
+        CK(cudaMemsetAsync(c->cflag, 0, sizeof(uint32_t), s));
+        LAUNCH(c, s, k_verify_windows<D>, (long long)n, L.g, L.img, L.mlist, L.mcnt, L.pid, c->crep, c->cflag);
+        uint32_t bad = 1;
+        CK(cudaMemcpyAsync(&bad, c->cflag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return bad == 0;
+    }
     size_t bytes = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n, 0, 64, s));
     if (bytes > c->cub_bytes) {
@@ -595,26 +629,43 @@ template <int D>
 void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     cudaStream_t s = c->s;
     LevelBufs& L0 = c->L[0];
-    if (D == 3 && c->g0.nx % 32 == 0) {
-        const dim3 grid(c->g0.nx / 32, (c->g0.ny + 7) / 8, c->g0.nz);
-        k_setup_l0_tiled<<<grid, dim3(32, 8), 0, s>>>(c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
+    constexpr int NCW = (D == 3) ? 27 : 9;
+    // window counts of the linear blocks, levels l < depth - 1 (k_zfinal below)
+    for (int l = 0; l + 1 < c->depth; ++l) CK(cudaMemsetAsync(c->L[l].zG, 0, 3 * NCW * sizeof(unsigned long long), s));
+    const bool march0 = D == 3 && c->g0.nx % 32 == 0 && c->depth - 1 <= kMaxDepth - 1;
+    if (march0) {
+        // cell bytes, masks, tile flags and every level's window counts in one z-marching pass
+        constexpr int ZC = 16;
+        ZsumArgs za{};
+        for (int l = 0; l + 1 < c->depth; ++l) za.G[l] = c->L[l].zG;
+        za.nzs = c->depth - 1;
+        za.zg_off = zg_offset(c, 0);
+        za.nxg = c->gglob[0].nx;
+        za.nyg = c->gglob[0].ny;
+        za.nzg = c->gglob[0].nz;
+        const dim3 grid(c->g0.nx / 32, (c->g0.ny + 7) / 8, (c->g0.nz + ZC - 1) / ZC);
+        k_classify_march<ZC, true><<<grid, dim3(32, 8), 0, s>>>(c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask,
+                                                                c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za);
         CK(cudaGetLastError());
         ++c->launches;
     } else {
         LAUNCH(c, s, k_setup_l0<D>, c->g0.n, c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
+        LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
+               c->tflags);
     }
     scan_u32(c, L0.mcount, L0.mbase, L0.nseg);
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
-    LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
-           c->tflags);
     build_sched(c, c->sch_stencil, kTX, kTY, 1, 0, c->sched_gx, c->sched_gy);
     if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1, c->sched0_gx, c->sched0_gy);
     c->x1_clean = false;
     for (int l = 1; l < c->depth; ++l) {
         LevelBufs& Lf = c->L[l - 1];
         LevelBufs& Lc = c->L[l];
+        // pure-type bytes for the z-marching classifier (scratch: this level's row codes, written later)
+        const bool marchc = D == 3 && !c->slab.on && Lc.g.nx % 32 == 0;
+        uint8_t* pure = marchc ? reinterpret_cast<uint8_t*>(Lc.rcode) : nullptr;
         LAUNCH(c, s, k_pool_image<D>, Lc.g.n, Lf.g, Lc.g, (l == 1) ? dtypes : nullptr, (l == 1) ? nullptr : Lf.img,
-               Lc.img);
+               Lc.img, pure);
         if (c->slab.on) {
             // ghost planes: the outside of the domain, then the neighbours' planes
             if (Lc.g.zo0 > 0) LAUNCH(c, s, k_solid_planes, (long long)Lc.g.zo0 * Lc.g.nx * Lc.g.ny, Lc.g, Lc.img, 0, Lc.g.zo0);
@@ -623,7 +674,16 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
                        Lc.g.nz);
             for (int ch = 0; ch < 3; ++ch) slab_exchange(c, s, Lc.img + (size_t)ch * Lc.g.n, sizeof(float), l);
         }
-        LAUNCH(c, s, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
+        if (marchc) {
+            constexpr int ZC = 8;
+            const dim3 grid(Lc.g.nx / 32, (Lc.g.ny + 7) / 8, (Lc.g.nz + ZC - 1) / ZC);
+            k_classify_march<ZC, false><<<grid, dim3(32, 8), 0, s>>>(Lc.g, pure, Lc.cls, Lc.mmask, Lc.mcount, nullptr,
+                                                                     nullptr, 0, 0, nullptr, ZsumArgs{});
+            CK(cudaGetLastError());
+            ++c->launches;
+        } else {
+            LAUNCH(c, s, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
+        }
         scan_u32(c, Lc.mcount, Lc.mbase, Lc.nseg);
     }
     // compact mixed-cell lists per level
@@ -643,6 +703,9 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     const uint32_t n_mixed0 = n_mixed[0];
     if (n_mixed0 > 0) {
         LAUNCH(c, s, k_window_keys<D>, (long long)n_mixed0, c->g0, dtypes, L0.mlist, L0.mcnt, c->dkeys, c->dvals);
+        if (!c->dict_sort) {
+            dedup_patterns(c, s, n_mixed0, L0.mcnt, L0.mlist, c->pid0, c->repcell0, c->npat0);
+        } else {
         size_t bytes = 0;
         const int nbits = 2 * Sh<D>::S;
         CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n_mixed0, 0,
@@ -667,6 +730,7 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         c->launches += 2;
         LAUNCH(c, s, k_pattern_ids, (long long)n_mixed0, c->dsidx, c->dscan, c->dhead, L0.mlist, L0.mcnt, c->pid0,
                c->repcell0, c->npat0);
+        }
         // split into the solve's down/up sublists (dictionary scratch reused)
         uint32_t *fd = c->dvals, *fu = c->dsidx, *sd = c->dhead, *su = c->dscan;
         LAUNCH(c, s, k_mixed_flags, (long long)n_mixed0, L0.mlist, L0.mcnt, L0.cls, fd, fu);
@@ -725,9 +789,15 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
             LAUNCH(c, s, k_build_rows<D>, rows_cap * 32, L.g, st, im, cells, ncells, c->d_params + o.up_W,
                    c->d_params + o.up_B, L.tab_up);
             constexpr int NC = (D == 3) ? 27 : 9;
-            CK(cudaMemsetAsync(L.zG, 0, 3 * NC * sizeof(unsigned long long), s));
             const double scale = std::ldexp(1.0, D * l);
-            LAUNCH(c, s, k_zsums<D>, L.g.n, L.g, st, im, (float)scale, zg_offset(c, l), c->gglob[l].nz, L.zG);
+            if (!march0) {
+                const int nrows = L.g.ny * (L.g.zo1 - L.g.zo0);
+                const int blocks = std::max(1, std::min(nrows, 8 * c->num_sms));
+                k_zsums_rows<D><<<blocks, kBlock, 0, s>>>(L.g, st, im, (float)scale, zg_offset(c, l), c->gglob[l].nz,
+                                                          L.zG);
+                CK(cudaGetLastError());
+                ++c->launches;
+            }
             if (c->slab.on) slab_allreduce_u64(c, s, L.zG, 3 * NC);
             k_zfinal<D><<<1, 128, 0, s>>>(c->gglob[l], L.zG, scale, c->d_params + o.a_K, c->params[o.a_bias],
                                          c->d_params + o.b_K, c->params[o.b_bias], c->zab + 2 * l, c->zab + 2 * l + 1);
@@ -1704,6 +1774,8 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->cgAp);
     F(c->cgZ);
     F(c->icD);
+    F(c->htk);
+    F(c->htv);
     F(c->icFail);
     if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
     if (c->slab_exec) cudaGraphExecDestroy(c->slab_exec);
@@ -1828,6 +1900,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
         if (const char* e = std::getenv("NPSD_COARSE_OLD")) c->coarse_old = (e[0] == '1');
+        if (const char* e = std::getenv("NPSD_DICT_SORT")) c->dict_sort = (e[0] == '1');
         auto env_int = [](const char* n, int& v) {
             if (const char* e = std::getenv(n)) {
                 const int x = std::atoi(e);

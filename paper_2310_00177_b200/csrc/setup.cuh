@@ -125,6 +125,190 @@ __global__ void __launch_bounds__(256) k_setup_l0_tiled(Geom g, const uint8_t* _
     }
 }
 
+// Window classes by z-march over a byte grid (3D, nx a multiple of 32): a
+// 32 x 8 block owns a 32 x 8 tile and ZC planes. Each staged plane (tile +
+// one-cell halo, outside the domain solid = 2) is reduced at once to per-cell
+// 3 x 3 summaries (min, max, centre, non-solid face neighbours in the plane),
+// which roll through registers along z: a window is uniform iff its min equals
+// its max (types 0..2; a coarse cell that is not pure reads 3, which never
+// equals a uniform window's type), and holds fluid iff its min is 0.
+//   L0: src = the cell types. Writes the cell bytes (w | t << 2 | diag << 4 |
+//       wfluid << 7), mixed and fluid segment masks, the tile flags (a staged
+//       plane's "any fluid" is the tile dilated by one cell in x and y,
+//       k_tile_flags' definition) and the linear-block window counts of every
+//       level l < nzs (k_zsums, but counted from the L0 types: a level-l
+//       cell's pooled value times 8^l is the count of its L0 cells of that
+//       type, so the totals are the same integers).
+//   coarse: src = pure-type bytes (k_pool_image). Writes cls = uniform ? t : 3
+//       and the mixed masks (k_classify).
+struct ZsumArgs {
+    unsigned long long* G[kMaxDepth];  // per level: [3][27] counts (k_zsums layout)
+    int nzs;                           // levels with window counts (depth - 1)
+    int zg_off;                        // global plane of local plane 0 (level 0)
+    int nxg, nyg, nzg;                 // the full grid (level 0)
+};
+
+template <int ZC, bool L0>
+__global__ void __launch_bounds__(256) k_classify_march(Geom g, const uint8_t* __restrict__ src,
+                                                        uint8_t* __restrict__ cls, uint32_t* __restrict__ mmask,
+                                                        uint32_t* __restrict__ mcount, uint32_t* __restrict__ fmask,
+                                                        uint32_t* __restrict__ fcount, int ftx, int fty,
+                                                        uint8_t* __restrict__ tflags, ZsumArgs za) {
+    static_assert(kFlagTX == 32 && kFlagTY == 8, "the block tile is the flag tile");
+    __shared__ uint8_t st[2][10][36];
+    __shared__ unsigned long long sG[L0 ? kMaxDepth * 81 : 1];
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+    const int X0 = blockIdx.x * 32, Y0 = blockIdx.y * 8, Z0 = blockIdx.z * ZC;
+    const long long plane = (long long)g.nx * g.ny;
+    if (L0) {
+        for (int i = tid; i < za.nzs * 81; i += 256) sG[i] = 0ull;
+    }
+    // staging: my (up to) two bytes of the 10 x 34 plane
+    int off[2], sidx[2];
+    bool inxy[2], use[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int i = tid + 256 * j, ly = i / 34, lx = i - 34 * ly;
+        const int xx = X0 - 1 + lx, yy = Y0 - 1 + ly;
+        use[j] = i < 340;
+        inxy[j] = use[j] && (unsigned)xx < (unsigned)g.nx && (unsigned)yy < (unsigned)g.ny;
+        off[j] = inxy[j] ? yy * g.nx + xx : 0;
+        sidx[j] = ly * 36 + lx;
+    }
+    // per-plane summaries (min, max, centre, in-plane non-solid face
+    // neighbours) of my cell's 3 x 3 for planes z - 1 (P), z (M), z + 1 (N),
+    // rotated by value each step: a runtime loop, no unrolled copies of the body
+    int mnP = 0, mxP = 0, cvP = 0, mnM = 0, mxM = 0, cvM = 0, nbM = 0, mnN = 0, mxN = 0, cvN = 0, nbN = 0;
+    // my staging bytes of a plane, loaded one plane ahead of their store
+    uint8_t pv[2];
+    auto load_plane = [&](int p) {
+        const bool zin = p >= 0 && p < g.nz;
+        const uint8_t* sp = src + (zin ? (long long)p * plane : 0);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) pv[j] = (zin && inxy[j]) ? __ldg(sp + off[j]) : (uint8_t)2;
+    };
+    load_plane(Z0 - 1);
+    // stage plane p (its bytes are in pv) into buffer (p - Z0 + 1) & 1, issue the loads of
+    // plane p + 1, and summarise plane p into N; returns "any fluid" of plane p
+    auto plane_step = [&](int p) -> bool {
+        const int buf = (p - Z0 + 1) & 1;
+        uint8_t* dst = &st[buf][0][0];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (!use[j]) continue;
+            dst[sidx[j]] = pv[j];
+            any |= (pv[j] == 0);
+        }
+        load_plane(p + 1);
+        const bool anyb = __syncthreads_or(any) != 0;
+        int lo = 255, hi = 0, n4 = 0, ctr = 0;
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+                const int v = st[buf][ty + dy][tx + dx];
+                lo = min(lo, v);
+                hi = max(hi, v);
+                if (dy == 1 && dx == 1) ctr = v;
+                if ((dy == 1) != (dx == 1)) n4 += (v != 2);
+            }
+        mnP = mnM, mxP = mxM, cvP = cvM;
+        mnM = mnN, mxM = mxN, cvM = cvN, nbM = nbN;
+        mnN = lo, mxN = hi, cvN = ctr, nbN = n4;
+        return anyb;
+    };
+    auto flag = [&](int zz, bool any) {
+        if (L0 && tid == 0) tflags[((long long)zz * fty + blockIdx.y) * ftx + blockIdx.x] = any ? 1 : 0;
+    };
+    __shared__ uint32_t zin_cnt[L0 ? 8 : 1][3];  // per warp: counts of warps interior at every level
+    if (L0 && tx == 0)
+        for (int i = 0; i < 3; ++i) zin_cnt[ty][i] = 0;
+    const int x = X0 + tx, y = Y0 + ty;
+    plane_step(Z0 - 1);
+#pragma unroll 1
+    for (int p = Z0; p <= Z0 + ZC; ++p) {
+        if (p - 1 >= g.nz) break;  // block-uniform
+        const bool anyp = plane_step(p);  // now P, M, N = planes p - 2, p - 1, p
+        if (p < Z0 + ZC && p < g.nz) flag(p, anyp);
+        const int z = p - 1;
+        if (z < Z0) continue;
+        if (y >= g.ny) continue;  // whole warp (rows)
+        const int lo = min(mnP, min(mnM, mnN)), hi = max(mxP, max(mxM, mxN));
+        const int t = cvM;
+        const bool uniform = lo == hi && (L0 || t != 3);  // every window cell is the centre's pure type
+        const long long c = (long long)z * plane + (long long)y * g.nx + x;
+        const bool owned = c >= owned_lo(g) && c < owned_hi(g);
+        const uint32_t mm = __ballot_sync(0xffffffffu, !uniform && owned);
+        if (L0) {
+            // stencil diagonal: non-solid in-domain face neighbours (discretization.cpp:105-113)
+            const int diag = nbM + (cvP != 2) + (cvN != 2);
+            const bool wfluid = lo == 0;
+            cls[c] = (uint8_t)((uniform ? t : 3) | (t << 2) | (diag << 4) | ((int)wfluid << 7));
+            const uint32_t fm = __ballot_sync(0xffffffffu, t == 0 && owned);
+            if (tx == 0) {
+                const long long seg = c >> 5;
+                mmask[seg] = mm;
+                mcount[seg] = __popc(mm);
+                fmask[seg] = fm;
+                fcount[seg] = __popc(fm);
+            }
+            // window counts of every level l < nzs: classes by the level's
+            // global (x, y, z) position (k_zsums), warp-aggregated. A warp
+            // interior at the coarsest counted level is interior at every
+            // level (the boundary bands grow with l): one update for all.
+            const uint32_t b0 = __ballot_sync(0xffffffffu, owned && t == 0);
+            const uint32_t b1 = __ballot_sync(0xffffffffu, owned && t == 1);
+            const uint32_t b2 = __ballot_sync(0xffffffffu, owned && t == 2);
+            const int zg = z + za.zg_off, Lc = za.nzs - 1;
+            const int x0c = X0 >> Lc, x1c = (X0 + 31) >> Lc, ycl = y >> Lc, zcl = zg >> Lc;
+            const bool all_inner = x0c > 0 && x1c < (za.nxg >> Lc) - 1 && ycl > 0 && ycl < (za.nyg >> Lc) - 1 &&
+                                   zcl > 0 && zcl < (za.nzg >> Lc) - 1;
+            if (all_inner) {
+                if (tx == 0) {
+                    zin_cnt[ty][0] += __popc(b0);
+                    zin_cnt[ty][1] += __popc(b1);
+                    zin_cnt[ty][2] += __popc(b2);
+                }
+            } else {
+#pragma unroll 1
+                for (int l = 0; l < za.nzs; ++l) {
+                    const int xl = x >> l, yl = y >> l, zl = zg >> l;
+                    const int kx = (xl == 0) ? 0 : ((xl == (za.nxg >> l) - 1) ? 2 : 1);
+                    const int ky = (yl == 0) ? 0 : ((yl == (za.nyg >> l) - 1) ? 2 : 1);
+                    const int kz = (zl == 0) ? 0 : ((zl == (za.nzg >> l) - 1) ? 2 : 1);
+#pragma unroll
+                    for (int kv = 0; kv < 3; ++kv) {
+                        const uint32_t mk = __ballot_sync(0xffffffffu, kx == kv);
+                        if (tx == 0 && mk) {
+                            const int cl = (kz * 3 + ky) * 3 + kv;
+                            const uint32_t n0 = __popc(b0 & mk), n1 = __popc(b1 & mk), n2 = __popc(b2 & mk);
+                            if (n0) atomicAdd(&sG[l * 81 + 0 * 27 + cl], (unsigned long long)n0);
+                            if (n1) atomicAdd(&sG[l * 81 + 1 * 27 + cl], (unsigned long long)n1);
+                            if (n2) atomicAdd(&sG[l * 81 + 2 * 27 + cl], (unsigned long long)n2);
+                        }
+                    }
+                }
+            }
+        } else {
+            cls[c] = (uint8_t)(uniform ? t : 3);
+            if (tx == 0) {
+                const long long seg = c >> 5;
+                mmask[seg] = mm;
+                mcount[seg] = __popc(mm);
+            }
+        }
+    }
+    if (L0) {
+        if (tx == 0)  // the all-interior counts go to the interior class (13) of every level
+            for (int i = 0; i < za.nzs * 3; ++i)
+                if (zin_cnt[ty][i % 3]) atomicAdd(&sG[(i / 3) * 81 + (i % 3) * 27 + 13], (unsigned long long)zin_cnt[ty][i % 3]);
+        __syncthreads();
+        for (int i = tid; i < za.nzs * 81; i += 256)
+            if (sG[i]) atomicAdd(&za.G[i / 81][i % 81], sG[i]);
+    }
+}
+
 // Tile occupancy at L0: flags[(z * nty + ty) * ntx + tx] = any fluid cell in
 // the 32 x 8 tile (tx, ty) of plane z dilated by one cell in x and y. Kernels
 // OR the flags of their region (plus one plane each side in z) and skip
@@ -214,12 +398,14 @@ __global__ void k_sched_prefix(const int* __restrict__ len, int n, int* __restri
 // plane; from the L0 one-hot types (src_types) or a pooled level (src_img).
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_pool_image(Geom gf, Geom gc, const uint8_t* __restrict__ src_types,
-                                                       const float* __restrict__ src_img, float* __restrict__ dst) {
+                                                       const float* __restrict__ src_img, float* __restrict__ dst,
+                                                       uint8_t* __restrict__ pure) {
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < gc.n; c += stride) {
         const int x = (int)(c % gc.nx);
         const int y = (int)((c / gc.nx) % gc.ny);
         const int z = (int)(c / ((long long)gc.nx * gc.ny));
+        float vals[3];
         for (int ch = 0; ch < 3; ++ch) {
             float acc = 0.0f;
             bool first = true;
@@ -231,7 +417,16 @@ __global__ void __launch_bounds__(kBlock) k_pool_image(Geom gf, Geom gc, const u
                         acc = first ? v : __fadd_rn(acc, v);
                         first = false;
                     }
-            dst[ch * gc.n + c] = __fmul_rn((D == 3) ? 0.125f : 0.25f, acc);
+            const float v = __fmul_rn((D == 3) ? 0.125f : 0.25f, acc);
+            dst[ch * gc.n + c] = v;
+            vals[ch] = v;
+        }
+        if (pure) {  // k_classify's pure(): the one-hot type, else 3
+            const float a = vals[0], b = vals[1], sd = vals[2];
+            pure[c] = (a == 1.0f && b == 0.0f && sd == 0.0f)   ? 0
+                      : (a == 0.0f && b == 1.0f && sd == 0.0f) ? 1
+                      : (a == 0.0f && b == 0.0f && sd == 1.0f) ? 2
+                                                                : 3;
         }
     }
 }
@@ -465,6 +660,51 @@ __global__ void __launch_bounds__(kBlock) k_pattern_ids(const uint32_t* __restri
     if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) *npat = 0;
 }
 
+// Pattern ids by hashing instead of sorting (the launchers' default): keys go
+// into an open-addressing table (linear probing); the thread that inserts a
+// key gives it the next id and makes its cell the representative. Ids come out
+// in a nondeterministic order, but a pattern's row depends only on the
+// pattern (level 0: the exact key; coarse levels: every member's window is
+// compared with its representative's bit for bit), so the kernels' outputs
+// are the same bits whichever order or representative wins.
+constexpr unsigned long long kEmptyKey = ~0ull;
+
+__global__ void __launch_bounds__(kBlock) k_dedup_insert(const unsigned long long* __restrict__ keys,
+                                                         const uint32_t* __restrict__ count,
+                                                         const uint32_t* __restrict__ list,
+                                                         unsigned long long* __restrict__ tk, uint32_t* __restrict__ tv,
+                                                         unsigned long long mask, uint32_t* __restrict__ slot,
+                                                         uint32_t* __restrict__ repcell, uint32_t* __restrict__ npat) {
+    const long long n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        unsigned long long k = keys[i];
+        if (k == kEmptyKey) k = kEmptyKey - 1;  // a coarse hash; collisions are caught by k_verify_windows
+        unsigned long long h = mix64(k) & mask;
+        while (true) {
+            unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(tk + h);
+            if (cur == kEmptyKey) cur = atomicCAS(tk + h, kEmptyKey, k);
+            if (cur == kEmptyKey) {  // inserted: new pattern
+                const uint32_t id = atomicAdd(npat, 1u);
+                tv[h] = id;
+                repcell[id] = list[i];
+                break;
+            }
+            if (cur == k) break;
+            h = (h + 1) & mask;
+        }
+        slot[i] = (uint32_t)h;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_dedup_ids(const uint32_t* __restrict__ slot,
+                                                      const uint32_t* __restrict__ count,
+                                                      const uint32_t* __restrict__ tv, uint32_t* __restrict__ pid) {
+    const long long n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) pid[i] = tv[slot[i]];
+}
+
 // The three uniform-window kernels of a conv (same arithmetic as
 // build_kernels on a pure window: I = 1 on channel T, 0 elsewhere).
 template <int D>
@@ -484,6 +724,51 @@ __global__ void k_kconst(const float* __restrict__ W, const float* __restrict__ 
 // (per axis: first plane, interior, last plane) over the owned cells; a z-slab
 // classifies by global plane (zg_off: global index of local plane 0, nzg: the
 // level's global plane count) so the ranks' counts add up to the full grid's.
+// k_zsums by rows (the launcher's default): a row's y / z class is
+// block-uniform and no 64-bit division sits in the per-cell path.
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_zsums_rows(Geom g, const uint8_t* __restrict__ src_types,
+                                                       const float* __restrict__ img, float scale, int zg_off, int nzg,
+                                                       unsigned long long* __restrict__ G) {
+    constexpr int NC = (D == 3) ? 27 : 9;
+    __shared__ unsigned long long sG[3 * NC];
+    for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x) sG[i] = 0ull;
+    __syncthreads();
+    constexpr int kInterior = (D == 3) ? 13 : 4;
+    unsigned long long inner[3] = {0ull, 0ull, 0ull};
+    const int nrows = g.ny * (g.zo1 - g.zo0);
+    for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
+        const int y = row % g.ny, zl = g.zo0 + row / g.ny, z = zl + zg_off;  // global plane
+        const int ky = (y == 0) ? 0 : ((y == g.ny - 1) ? 2 : 1);
+        const int kz = (D == 3) ? ((z == 0) ? 0 : ((z == nzg - 1) ? 2 : 1)) : 0;
+        const long long base = ((long long)zl * g.ny + y) * g.nx;
+        for (int x = threadIdx.x; x < g.nx; x += blockDim.x) {
+            const int kx = (x == 0) ? 0 : ((x == g.nx - 1) ? 2 : 1);
+            const int cl = (kz * 3 + ky) * 3 + kx;
+            const long long c = base + x;
+            uint8_t t = 0;
+            if (src_types) t = src_types[c];
+            for (int ch = 0; ch < 3; ++ch) {
+                const unsigned long long v = src_types ? ((t == ch) ? 1ull : 0ull)
+                                                       : (unsigned long long)__fmul_rn(img[ch * g.n + c], scale);
+                if (cl == kInterior)
+                    inner[ch] += v;
+                else if (v)
+                    atomicAdd(&sG[ch * NC + cl], v);
+            }
+        }
+    }
+    for (int ch = 0; ch < 3; ++ch) {
+        unsigned long long v = inner[ch];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sG[ch * NC + kInterior], v);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x)
+        if (sG[i]) atomicAdd(&G[i], sG[i]);
+}
+
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_zsums(Geom g, const uint8_t* __restrict__ src_types,
                                                   const float* __restrict__ img, float scale, int zg_off, int nzg,
