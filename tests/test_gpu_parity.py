@@ -80,7 +80,9 @@ def test_precond_apply(b200, oracle, shape, depth, seed):
     p = oracle.init_params(len(shape), depth, 80 + seed)
     ctx, octx = make(b200, oracle, t, depth, p)
     r = np.random.default_rng(seed).standard_normal(ctx.n_fluid)
-    assert rel_l2(ctx.precond_apply(r), octx.precond_apply(r)) <= REL_L2
+    err = rel_l2(ctx.precond_apply(r), octx.precond_apply(r))
+    assert err <= REL_L2
+    assert err <= 1e-12  # bit-identical f32 network; f64 norm rounding only
     assert np.all(ctx.precond_apply(np.zeros_like(r)) == 0.0)  # test_neural.cpp:258-261
 
 
@@ -94,7 +96,10 @@ def test_precond_apply_interior_tiles(b200, oracle, shape, depth, seed):
     r = np.random.default_rng(seed).standard_normal(ctx.n_fluid)
     z = ctx.precond_apply(r)
     assert np.all(np.isfinite(z))
-    assert rel_l2(z, octx.precond_apply(r)) <= REL_L2
+    # the f32 network of the solve path is bit-identical to the restatement: only
+    # the f64 residual norm (tree vs serial sum) differs, ~1e-16; a single f32 ulp
+    # at one cell would show as ~1e-10
+    assert rel_l2(z, octx.precond_apply(r)) <= 1e-12
 
 
 def test_psdo_history_c3_64_random_weights(b200, oracle):
