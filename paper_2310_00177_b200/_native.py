@@ -3,11 +3,13 @@ library is missing the import of the product path fails loudly."""
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libnpsd_b200.so"
+# NPSD_B200_LIB: another build of the same library (A/B measurements of compile-time variants)
+LIB_PATH = Path(os.environ.get("NPSD_B200_LIB") or Path(__file__).resolve().parent / "libnpsd_b200.so")
 
 NPSD_OK, NPSD_INVALID_ARGUMENT, NPSD_BREAKDOWN, NPSD_EMPTY_SYSTEM, NPSD_CUDA_ERROR, NPSD_IO_ERROR = range(6)
 

@@ -29,7 +29,11 @@ struct KC0 {
 // Two planes per step: planes z, z+1 (z even) are convolved after ONE barrier
 // (four independent accumulation chains per thread), and their 2x2x2 pools
 // are summed after the next step's barrier.
-constexpr int kD0R = 4;  // raw (f64) plane stages: planes z+1 .. z+4
+#ifndef D0_AHEAD
+#define D0_AHEAD 2  // planes in flight beyond the step's two (4 and 6 measured slower at C3 256^3: 69.8 / 70.2 vs 66.2 us)
+#endif
+constexpr int kD0A = D0_AHEAD;
+constexpr int kD0R = kD0A + 2;  // raw (f64) plane stages: planes z+1 .. z+2+kD0A
 constexpr int kD0X = 8;  // x_0 (f32) plane ring: z-3 .. z+2 in use around a barrier
 
 struct Down0Smem {
@@ -135,10 +139,9 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
 #pragma unroll
     for (int k = 0; k < 8; ++k) ob[k] = own_bytes(zc0 + k);
     issue(zc0 - 1, own_bytes(zc0 - 1));
-    issue(zc0, ob[0]);
-    issue(zc0 + 1, ob[1]);
-    issue(zc0 + 2, ob[2]);
-    cp_wait<2>();
+#pragma unroll
+    for (int k = 0; k <= kD0A; ++k) issue(zc0 + k, ob[k]);
+    cp_wait<kD0A>();  // planes zc0-1, zc0 landed
     form(zc0 - 1);
     form(zc0);
     float my[2][2];
@@ -147,9 +150,9 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
     int pb = 0;  // yp buffer of this step
 #pragma unroll 4
     for (int z = zc0; z < zc1; z += 2) {
-        issue(z + 3, ob[3]);
-        issue(z + 4, ob[4]);
-        cp_wait<2>();  // planes z+1, z+2 landed (own copies)
+        issue(z + kD0A + 1, ob[kD0A + 1]);
+        issue(z + kD0A + 2, ob[kD0A + 2]);
+        cp_wait<kD0A>();  // planes z+1, z+2 landed (own copies)
         form(z + 1);
         form(z + 2);
         float ny[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
