@@ -5,7 +5,7 @@ bench.py's roofline "traffic" field).
 Capture (one GPU; ncu_target runs a 1-iteration warm-up, then the measured
 iterations, kernels launched one by one in the body order below):
 
-    ncu --set full --clock-control none -k regex:"k_mixed|k_down3|k_up3|k_ortho2|k_update2" \
+    ncu --set full --clock-control none -k regex:"k_mixed_down0|k_down_l0|k_cdownz|k_cupz|k_up_l0|k_mixed_up0|k_ortho2|k_update2" \
         -s 11 -c 11 -o prof python tools/ncu_target.py
 
     python tools/ncu_traffic.py prof.ncu-rep 256
