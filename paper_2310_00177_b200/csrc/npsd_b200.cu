@@ -2022,7 +2022,8 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->fcount = dalloc<uint32_t>((size_t)nseg0);
         c->tf_ntx = (nx + kFlagTX - 1) / kFlagTX;
         c->tf_nty = (ny + kFlagTY - 1) / kFlagTY;
-        c->tflags = dalloc<uint8_t>((size_t)c->tf_ntx * c->tf_nty * nz);
+        // every local plane: a z-slab's ghost planes are flagged too (k_classify_march, k_tile_flags)
+        c->tflags = dalloc<uint8_t>((size_t)c->tf_ntx * c->tf_nty * c->L[0].g.nz);
         c->dkeys = dalloc<unsigned long long>((size_t)c->g0.n);
         c->dskeys = dalloc<unsigned long long>((size_t)c->g0.n);
         c->dvals = dalloc<uint32_t>((size_t)c->g0.n);
