@@ -233,6 +233,9 @@ __global__ void __launch_bounds__(kKT, COARSE_MINB) k_cup(Geom g, Geom gc, const
 // Accumulation order and rounding are those of the one-thread-per-cell
 // kernels above (slot order, __fmul_rn/__fadd_rn): bit-identical outputs.
 constexpr int kZX = 32, kZY = 8, kZT = kZX * kZY;  // block tile (x, y) = 256 threads
+#ifndef COARSEZ_MINB
+#define COARSEZ_MINB 4  // min resident blocks per SM of the z-marching kernels: a 64-register cap (1: 84 registers, 3 blocks; measured 3-4 us slower per L1 kernel)
+#endif
 constexpr int kZSP = 48;                           // padded shared row stride (floats)
 
 // (NZ x NY x NX) box at (bx, by, bz) of gg, zero outside the grid, staged
@@ -295,7 +298,7 @@ __device__ __forceinline__ const float4* code_row(const ConvTab& ct, const UniRo
 
 // grid (ceil(nx/32), ceil(ny/8), ceil(owned planes/ZC)), block 256
 template <bool POOL, int ZC>
-__global__ void __launch_bounds__(kZT) k_cdownz(Geom g, const float* __restrict__ x, ConvTab ct,
+__global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cdownz(Geom g, const float* __restrict__ x, ConvTab ct,
                                                 const __grid_constant__ KC kc, float* __restrict__ y,
                                                 float* __restrict__ xnext, Geom gc, const int* __restrict__ done) {
     pdl_launch_wait();
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(kZT) k_cdownz(Geom g, const float* __restrict_
 
 // grid (ceil(nx/32), ceil(ny/8), ceil(owned planes/ZC)), block 256; outc is level l+1
 template <int ZC>
-__global__ void __launch_bounds__(kZT) k_cupz(Geom g, Geom gc, const float* __restrict__ outc,
+__global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cupz(Geom g, Geom gc, const float* __restrict__ outc,
                                               const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
                                               const __grid_constant__ KC kc, float* __restrict__ outl,
                                               const int* __restrict__ done) {
