@@ -215,7 +215,10 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
 // Balanced schedule (Sched, units of two planes: pooling pairs stay inside a
 // segment); dynamic smem = sizeof(Down0Smem). Units outside the schedule have
 // an all-zero window: their x_1 cells keep the zeros set before the solve.
-__global__ void __launch_bounds__(kSX* kSY) k_down_l0(Geom g, const uint8_t* __restrict__ cls,
+#ifndef D0_MINB
+#define D0_MINB 3  // 3 blocks/SM (77 registers; 116 uncapped, 2 blocks): 67 -> 61 us at C3 256^3
+#endif
+__global__ void __launch_bounds__(kSX* kSY, D0_MINB) k_down_l0(Geom g, const uint8_t* __restrict__ cls,
                                                       const double* __restrict__ r, const SolverState* __restrict__ st,
                                                       const __grid_constant__ KC0 kc, float* __restrict__ y,
                                                       float* __restrict__ xnext, Geom gc, Sched sc) {

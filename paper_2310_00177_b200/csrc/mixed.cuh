@@ -99,7 +99,10 @@ __device__ __forceinline__ void decode32(const Geom& g, uint32_t c, int& x, int&
 }
 
 template <int D>
-__global__ void __launch_bounds__(kBlock) k_mixed_down0(Geom g, const uint32_t* __restrict__ list,
+#ifndef MIXDN_MINB
+#define MIXDN_MINB 5  // register cap for 5 blocks/SM (measured 37 -> 29 us on the same box)
+#endif
+__global__ void __launch_bounds__(kBlock, MIXDN_MINB) k_mixed_down0(Geom g, const uint32_t* __restrict__ list,
                                                         const uint32_t* __restrict__ count, const double* __restrict__ r,
                                                         const SolverState* __restrict__ st,
                                                         const float* __restrict__ tab, const uint32_t* __restrict__ kid,
@@ -145,7 +148,10 @@ __device__ __forceinline__ void fin_projections(SolverState* st, const double* d
 }
 
 template <int D, int NO>
-__global__ void __launch_bounds__(kBlock) k_mixed_up0(Geom g, Geom gc, const uint32_t* __restrict__ list,
+#ifndef MIXUP_MINB
+#define MIXUP_MINB 4  // register cap for 4 blocks/SM (measured 26 -> 24 us)
+#endif
+__global__ void __launch_bounds__(kBlock, MIXUP_MINB) k_mixed_up0(Geom g, Geom gc, const uint32_t* __restrict__ list,
                                                       const uint32_t* __restrict__ count,
                                                       const float* __restrict__ outc, const float* __restrict__ y0,
                                                       const float* __restrict__ zab, const float* __restrict__ tab,
