@@ -137,10 +137,10 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Grid size is fixed per kernel and context, so results are run-to-run
 // bitwise reproducible.
 // ---------------------------------------------------------------------------
-template <int NV>
+template <int NV, int NT = kBlock>
 __device__ __forceinline__ bool grid_reduce(double (&v)[NV], double* __restrict__ partials,
                                             unsigned int* __restrict__ counter, double (&tot)[NV]) {
-    __shared__ double sred[kBlock / 32][NV];
+    __shared__ double sred[NT / 32][NV];  // NT >= threads per block
     __shared__ bool s_last;
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const int nthr = blockDim.x * blockDim.y * blockDim.z;

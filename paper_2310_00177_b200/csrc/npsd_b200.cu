@@ -280,7 +280,8 @@ struct npsd_b200_ctx {
     KC kc_down[kMaxDepth], kc_up[kMaxDepth], kc_coarse;  // host copies of the uniform kernels
     uint32_t *fmask = nullptr, *fbase = nullptr, *fcount = nullptr;
     uint8_t* tflags = nullptr;  // L0 tile occupancy (k_tile_flags)
-    SchedBufs sch_stencil;      // 64 x 8 tile columns, plane units (k_ortho2, k_update2)
+    SchedBufs sch_stencil;      // 64 x 8 tile columns, plane units (k_up_l0, k_cg_dir; k_ortho2 at n_ortho > 2)
+    SchedBufs sch_march;        // 64 x kMarchSY tile columns, plane units (k_ortho2, k_update2)
     SchedBufs sch_down0;        // 64 x 8 tile columns, plane-pair units, window dilation (k_down_l0)
     bool x1_clean = false;      // L1.x is zero outside sch_down0's units
     // level-0 window-pattern dictionary (setup.cuh)
@@ -656,6 +657,7 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     scan_u32(c, L0.mcount, L0.mbase, L0.nseg);
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
     build_sched(c, c->sch_stencil, kTX, kTY, 1, 0, c->sched_gx, c->sched_gy);
+    if (kMarchSY != kSY) build_sched(c, c->sch_march, kTX, kMarchSY, 1, 0, c->sched_gx, c->sched_gy);
     if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1, c->sched0_gx, c->sched0_gy);
     c->x1_clean = false;
     for (int l = 1; l < c->depth; ++l) {
@@ -1002,13 +1004,14 @@ void launch_up0_no(npsd_b200_ctx* c, cudaStream_t s, int no) {
 template <int D, int NO>
 void launch_ortho(npsd_b200_ctx* c, cudaStream_t s) {
     const Geom g = c->g0;
-    const dim3 block(kSX, kSY);
-    auto k = k_ortho2<D, NO>;
-    const size_t sm = march_smem_bytes<OrthoOp<NO>>();
+    constexpr int SY = march_sy<OrthoOp<NO>>();
+    const dim3 block(kSX, SY);
+    auto k = k_ortho2<D, NO, SY>;
+    const size_t sm = march_smem_bytes<OrthoOp<NO>, SY>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const dim3 grid(wave_blocks(c, k, kSX * kSY, sm));
+    const dim3 grid(wave_blocks(c, k, kSX * SY, sm));
     launch_pdl(c, s, k, grid, block, sm, g, c->L[0].cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
-               c->counter, c->sch_stencil.view());
+               c->counter, (SY == kSY ? c->sch_stencil : c->sch_march).view());
 }
 
 template <int D>
@@ -1026,13 +1029,14 @@ void launch_ortho_no(npsd_b200_ctx* c, cudaStream_t s, int no) {
 template <int D>
 void launch_update(npsd_b200_ctx* c, cudaStream_t s, cudaGraphConditionalHandle h, int use_cond, int do_norm) {
     const Geom g = c->g0;
-    const dim3 block(kSX, kSY);
-    auto k = k_update2<D>;
-    const size_t sm = march_smem_bytes<UpdateOp>();
+    constexpr int SY = march_sy<UpdateOp>();
+    const dim3 block(kSX, SY);
+    auto k = k_update2<D, SY>;
+    const size_t sm = march_smem_bytes<UpdateOp, SY>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const dim3 grid(wave_blocks(c, k, kSX * kSY, sm));
+    const dim3 grid(wave_blocks(c, k, kSX * SY, sm));
     launch_pdl(c, s, k, grid, block, sm, g, c->L[0].cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist,
-               c->times, c->partials, c->counter, h, use_cond, do_norm, c->sch_stencil.view());
+               c->times, c->partials, c->counter, h, use_cond, do_norm, (SY == kSY ? c->sch_stencil : c->sch_march).view());
 }
 
 // One named launcher per kernel of an iteration: the graph body is captured
@@ -1779,7 +1783,7 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->icFail);
     if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
     if (c->slab_exec) cudaGraphExecDestroy(c->slab_exec);
-    for (SchedBufs* sb : {&c->sch_stencil, &c->sch_down0}) {
+    for (SchedBufs* sb : {&c->sch_stencil, &c->sch_march, &c->sch_down0}) {
         F(sb->pre);
         F(sb->zlo);
         F(sb->len);

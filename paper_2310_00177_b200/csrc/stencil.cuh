@@ -32,6 +32,14 @@ constexpr int kPF = 2;                     // planes prefetched ahead (down0.cuh
 #define STENCIL_PF_UPDATE 2
 #endif
 constexpr int kST = kPF + 1;               // input ring stages
+// rows of the ortho/update tile (64 x SY cells, 32 x SY threads). A taller
+// tile reads fewer halo rows per cell (2/SY), but SY = 16 (one 512-thread
+// block per SM, half the schedule columns) measured slower at C3 256^3:
+// ortho 100 -> 107 us, update 76 -> 93 us. Kept as a compile-time knob.
+#ifndef STENCIL_SY
+#define STENCIL_SY 8
+#endif
+constexpr int kMarchSY = STENCIL_SY;
 constexpr unsigned kOut2 = 0x0C0Cu;        // pair bytes outside the domain: type 3
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
@@ -102,20 +110,23 @@ struct UpdateOp {
     }
 };
 
-template <typename Op>
+template <typename Op, int SY = kSY>
 struct MarchSmem {
-    double raw[Op::PF + 1][Op::NA][kVH][kVW];  // operand inputs, tile + halo
-    double ctr[Op::PF + 1][Op::NC > 0 ? Op::NC : 1][kTY][kTX];  // centre-only inputs
-    double v[4][kVH][kVW];              // operand ring
+    static constexpr int VH = SY + 2;
+    double raw[Op::PF + 1][Op::NA][VH][kVW];  // operand inputs, tile + halo
+    double ctr[Op::PF + 1][Op::NC > 0 ? Op::NC : 1][SY][kTX];  // centre-only inputs
+    double v[4][VH][kVW];              // operand ring
 };
 
 // Epi(q, v2 own pair, s2 rows, pair bytes, own raw inputs [NA] x 2, centre [NC] x 2, acc)
-template <int D, int NV, typename Op, typename Epi>
+template <int D, int NV, int SY = kSY, typename Op, typename Epi>
 __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __restrict__ cls, const Op& op, int tx,
                                               int ty, int zc0, int zc1, double (&acc)[NV], Epi epi) {
     constexpr int PF = Op::PF, ST = PF + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    MarchSmem<Op>& S = *reinterpret_cast<MarchSmem<Op>*>(smem_raw);
+    constexpr int kTY = SY, kVH = SY + 2;
+    static_assert(2 * SY <= 32, "column halos: one lane per row and side");
+    MarchSmem<Op, SY>& S = *reinterpret_cast<MarchSmem<Op, SY>*>(smem_raw);
     __syncthreads();  // the previous segment's last reads of S are done
     const int lane = threadIdx.x, row = threadIdx.y;
     const int X0 = tx * kTX, Y0 = ty * kTY;
@@ -288,8 +299,8 @@ __device__ __forceinline__ void fin_ortho(SolverState* st, const double* tot) {
 }
 
 // d' = MGS(d); Ad'; dots d'.Ad', r.d', d_j.Ad'. NO = n_ortho (cache bound).
-template <int D, int NO>
-__global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __restrict__ cls,
+template <int D, int NO, int SY>
+__global__ void __launch_bounds__(kSX* SY) k_ortho2(Geom g, const uint8_t* __restrict__ cls,
                                                      const double* __restrict__ dtmp, const double* __restrict__ r,
                                                      double* __restrict__ Dring, double* __restrict__ ADring,
                                                      SolverState* st, double* __restrict__ partials,
@@ -316,7 +327,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc[j] = 0.0;
     sched_for_each(sc, [&](int tx, int ty, int zc0, int zc1) {
-    stencil_march<D, NV>(g, cls, op, tx, ty, zc0, zc1, acc,
+    stencil_march<D, NV, SY>(g, cls, op, tx, ty, zc0, zc1, acc,
                          [&](long long q, double2 v, double2 s, unsigned bc, const double(&i0)[Op::NA],
                              const double(&i1)[Op::NA], const double(&c0)[1], const double(&c1)[1], double(&a)[NV]) {
                              *reinterpret_cast<double2*>(dnew + q) = v;
@@ -335,7 +346,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
                          });
     });
     double tot[NV];
-    if (grid_reduce<NV>(acc, partials, counter, tot)) {
+    if (grid_reduce<NV, kSX * SY>(acc, partials, counter, tot)) {
         if (threadIdx.x == 0 && threadIdx.y == 0) {
             if (st->dist) {
                 for (int j = 0; j < kPart; ++j) st->part[j] = (j < NV) ? tot[j] : 0.0;
@@ -347,8 +358,8 @@ __global__ void __launch_bounds__(kSX* kSY) k_ortho2(Geom g, const uint8_t* __re
 }
 
 // x' = x + alpha d'; r = b - A x'; ||r||^2 (solver.cpp:252-260).
-template <int D>
-__global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __restrict__ cls,
+template <int D, int SY>
+__global__ void __launch_bounds__(kSX* SY) k_update2(Geom g, const uint8_t* __restrict__ cls,
                                                       const double* __restrict__ b, double* __restrict__ X0,
                                                       double* __restrict__ X1, const double* __restrict__ Dring,
                                                       double* __restrict__ r, SolverState* st, double* __restrict__ hist,
@@ -372,7 +383,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
     double* xn = st->xcur ? X0 : X1;
     double acc[1] = {0.0};
     sched_for_each(sc, [&](int tx, int ty, int zc0, int zc1) {
-    stencil_march<D, 1>(g, cls, op, tx, ty, zc0, zc1, acc,
+    stencil_march<D, 1, SY>(g, cls, op, tx, ty, zc0, zc1, acc,
                         [&](long long q, double2 v, double2 s, unsigned bc, const double(&)[2], const double(&)[2],
                             const double(&c0)[1], const double(&c1)[1], double(&a)[1]) {
                             double2 rv;
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
     });
     if (!do_norm) return;
     double tot[1];
-    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0) {
+    if (grid_reduce<1, kSX * SY>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0) {
         if (st->dist)
             st->part[0] = tot[0];
         else
@@ -394,9 +405,15 @@ __global__ void __launch_bounds__(kSX* kSY) k_update2(Geom g, const uint8_t* __r
     }
 }
 
-template <typename Op>
+template <typename Op, int SY = kSY>
 constexpr size_t march_smem_bytes() {
-    return sizeof(MarchSmem<Op>);
+    return sizeof(MarchSmem<Op, SY>);
+}
+// tile rows for an ortho/update operand: kMarchSY while its stages fit the
+// shared memory of one block, else kSY
+template <typename Op>
+constexpr int march_sy() {
+    return march_smem_bytes<Op, kMarchSY>() <= 220 * 1024 ? kMarchSY : kSY;
 }
 
 }  // namespace nb2
