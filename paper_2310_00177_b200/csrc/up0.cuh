@@ -142,8 +142,11 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
     cp_wait<0>();
 }
 
+#ifndef UP0_MINB
+#define UP0_MINB 1
+#endif
 template <int NO>
-__global__ void __launch_bounds__(kSX* kSY) k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ cls,
+__global__ void __launch_bounds__(kSX* kSY, UP0_MINB) k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ cls,
                                                     const float* __restrict__ outc, const float* __restrict__ y0,
                                                     const float* __restrict__ zab, const __grid_constant__ KC0 kc,
                                                     double* __restrict__ dout, SolverState* st,
