@@ -27,6 +27,7 @@ struct CgOp {
     static constexpr int NA = 2;  // z, p
     static constexpr int NC = 0;
     static constexpr int PF = STENCIL_PF_UPDATE;
+    static constexpr int CS = 0;  // no centre inputs
     const double* in[NA];
     const double* ctr[1];
     double beta;

@@ -40,6 +40,9 @@ constexpr int kST = kPF + 1;               // input ring stages
 #define STENCIL_SY 8
 #endif
 constexpr int kMarchSY = STENCIL_SY;
+#ifndef STENCIL_UPDATE_CTR_DIRECT
+#define STENCIL_UPDATE_CTR_DIRECT 1
+#endif
 constexpr unsigned kOut2 = 0x0C0Cu;        // pair bytes outside the domain: type 3
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
@@ -85,6 +88,7 @@ struct OrthoOp {
     static constexpr int NA = 1 + NO;  // d, d_1..d_NO
     static constexpr int NC = 1;       // r (centre only)
     static constexpr int PF = STENCIL_PF_ORTHO;  // planes prefetched ahead
+    static constexpr int CS = PF + 1;            // centre inputs staged in the ring
     const double* in[NA];
     const double* ctr[NC];
     double mp[NO > 0 ? NO : 1];
@@ -102,6 +106,9 @@ struct UpdateOp {
     static constexpr int NA = 2;  // x, d'
     static constexpr int NC = 1;  // b (centre only)
     static constexpr int PF = STENCIL_PF_UPDATE;
+    // b read straight into registers, one step ahead of its use: without its
+    // ring stages the block fits four per SM instead of three
+    static constexpr int CS = STENCIL_UPDATE_CTR_DIRECT ? 0 : PF + 1;
     const double* in[NA];
     const double* ctr[NC];
     double alpha;
@@ -110,12 +117,20 @@ struct UpdateOp {
     }
 };
 
-template <typename Op, int SY = kSY>
+// Op::CS: stages of centre-only inputs in shared memory (0: none staged; the
+// epilogue reads them from global memory into registers)
+template <typename Op, int SY = kSY, bool Staged = (Op::CS > 0)>
 struct MarchSmem {
     static constexpr int VH = SY + 2;
     double raw[Op::PF + 1][Op::NA][VH][kVW];  // operand inputs, tile + halo
     double ctr[Op::PF + 1][Op::NC > 0 ? Op::NC : 1][SY][kTX];  // centre-only inputs
     double v[4][VH][kVW];              // operand ring
+};
+template <typename Op, int SY>
+struct MarchSmem<Op, SY, false> {
+    static constexpr int VH = SY + 2;
+    double raw[Op::PF + 1][Op::NA][VH][kVW];
+    double v[4][VH][kVW];
 };
 
 // Epi(q, v2 own pair, s2 rows, pair bytes, own raw inputs [NA] x 2, centre [NC] x 2, acc)
@@ -175,9 +190,11 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
                 else if (hkind == 2)
                     cp_async8(&S.raw[s][a][hsr][hsc], op.in[a] + (hl ? qz + qh : 0), hl);
             }
+            if constexpr (Op::CS > 0) {
 #pragma unroll
-            for (int a = 0; a < Op::NC; ++a)
-                cp_async16(&S.ctr[s][a][row][2 * lane], op.ctr[a] + (ol ? qz + qo : 0), ol);
+                for (int a = 0; a < Op::NC; ++a)
+                    cp_async16(&S.ctr[s][a][row][2 * lane], op.ctr[a] + (ol ? qz + qo : 0), ol);
+            }
         }
         cp_commit();
     };
@@ -233,6 +250,14 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
     // renaming instead of moves that would wait on the in-flight byte loads
 #pragma unroll(PF + 2)
     for (int z = zc0; z < zc1; ++z) {
+        constexpr int NCD = (Op::CS == 0 && Op::NC > 0) ? Op::NC : 0;
+        double2 cdir[NCD > 0 ? NCD : 1];
+        if constexpr (NCD > 0) {
+            const bool l = own && pair_live(ob[0]);
+#pragma unroll
+            for (int a = 0; a < NCD; ++a)
+                cdir[a] = l ? __ldg(reinterpret_cast<const double2*>(op.ctr[a] + z * plane + qo)) : make_double2(0.0, 0.0);
+        }
         if (D == 3) {
             issue(z + PF, ob[PF]);  // the plane PF steps ahead
             cp_wait<PF - 1>();                 // plane z+1 landed
@@ -260,10 +285,18 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
                 raw0[a] = S.raw[sl][a][r0][c0];
                 raw1[a] = S.raw[sl][a][r0][c0 + 1];
             }
+            if constexpr (Op::CS > 0) {
 #pragma unroll
-            for (int a = 0; a < Op::NC; ++a) {
-                c0v[a] = S.ctr[sl][a][row][2 * lane];
-                c1v[a] = S.ctr[sl][a][row][2 * lane + 1];
+                for (int a = 0; a < Op::NC; ++a) {
+                    c0v[a] = S.ctr[sl][a][row][2 * lane];
+                    c1v[a] = S.ctr[sl][a][row][2 * lane + 1];
+                }
+            } else if constexpr (NCD > 0) {
+#pragma unroll
+                for (int a = 0; a < NCD; ++a) {
+                    c0v[a] = cdir[a].x;
+                    c1v[a] = cdir[a].y;
+                }
             }
             epi(z * plane + qo, make_double2(v0, v1), s, bc, raw0, raw1, c0v, c1v, acc);
         }
