@@ -26,7 +26,7 @@ constexpr int kTX = 2 * kSX, kTY = kSY;    // cells per block tile (64 x 8)
 constexpr int kVW = kTX + 4, kVH = kTY + 2;  // staged plane: cols x0-2..x0+65, rows y0-1..y0+8
 constexpr int kPF = 2;                     // planes prefetched ahead (down0.cuh)
 #ifndef STENCIL_PF_ORTHO
-#define STENCIL_PF_ORTHO 3
+#define STENCIL_PF_ORTHO 2
 #endif
 #ifndef STENCIL_PF_UPDATE
 #define STENCIL_PF_UPDATE 2
@@ -40,6 +40,15 @@ constexpr int kST = kPF + 1;               // input ring stages
 #define STENCIL_SY 8
 #endif
 constexpr int kMarchSY = STENCIL_SY;
+// ortho: r read into registers (no ring stages) and a 2-plane prefetch bring
+// the block to 70 KB, and a register cap (79) to three blocks per SM instead
+// of two: 100.7 -> 89.8 us at C3 256^3 (r only: 94.6 us; tools/runs/o3_ab.sh)
+#ifndef STENCIL_ORTHO_CTR_DIRECT
+#define STENCIL_ORTHO_CTR_DIRECT 1
+#endif
+#ifndef ORTHO_MINB
+#define ORTHO_MINB 3
+#endif
 #ifndef STENCIL_UPDATE_CTR_DIRECT
 #define STENCIL_UPDATE_CTR_DIRECT 1
 #endif
@@ -88,7 +97,7 @@ struct OrthoOp {
     static constexpr int NA = 1 + NO;  // d, d_1..d_NO
     static constexpr int NC = 1;       // r (centre only)
     static constexpr int PF = STENCIL_PF_ORTHO;  // planes prefetched ahead
-    static constexpr int CS = PF + 1;            // centre inputs staged in the ring
+    static constexpr int CS = STENCIL_ORTHO_CTR_DIRECT ? 0 : PF + 1;  // centre inputs staged in the ring
     const double* in[NA];
     const double* ctr[NC];
     double mp[NO > 0 ? NO : 1];
@@ -333,7 +342,7 @@ __device__ __forceinline__ void fin_ortho(SolverState* st, const double* tot) {
 
 // d' = MGS(d); Ad'; dots d'.Ad', r.d', d_j.Ad'. NO = n_ortho (cache bound).
 template <int D, int NO, int SY>
-__global__ void __launch_bounds__(kSX* SY) k_ortho2(Geom g, const uint8_t* __restrict__ cls,
+__global__ void __launch_bounds__(kSX* SY, SY == kSY ? ORTHO_MINB : 1) k_ortho2(Geom g, const uint8_t* __restrict__ cls,
                                                      const double* __restrict__ dtmp, const double* __restrict__ r,
                                                      double* __restrict__ Dring, double* __restrict__ ADring,
                                                      SolverState* st, double* __restrict__ partials,
