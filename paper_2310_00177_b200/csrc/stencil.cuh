@@ -49,8 +49,12 @@ constexpr int kMarchSY = STENCIL_SY;
 #ifndef ORTHO_MINB
 #define ORTHO_MINB 3
 #endif
-#ifndef UPDATE_MINB
-#define UPDATE_MINB 1
+// UPDATE_MINB: optional register cap for update (unset: no block count in
+// the bound, 64 registers; an explicit 1 gives 86 and two blocks per SM)
+#ifdef UPDATE_MINB
+#define UPDATE_BOUNDS __launch_bounds__(kSX* SY, SY == kSY ? UPDATE_MINB : 1)
+#else
+#define UPDATE_BOUNDS __launch_bounds__(kSX* SY)
 #endif
 #ifndef STENCIL_UPDATE_CTR_DIRECT
 #define STENCIL_UPDATE_CTR_DIRECT 1
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__(kSX* SY, SY == kSY ? ORTHO_MINB : 1) k_ortho2(
 
 // x' = x + alpha d'; r = b - A x'; ||r||^2 (solver.cpp:252-260).
 template <int D, int SY>
-__global__ void __launch_bounds__(kSX* SY, SY == kSY ? UPDATE_MINB : 1) k_update2(Geom g, const uint8_t* __restrict__ cls,
+__global__ void UPDATE_BOUNDS k_update2(Geom g, const uint8_t* __restrict__ cls,
                                                       const double* __restrict__ b, double* __restrict__ X0,
                                                       double* __restrict__ X1, const double* __restrict__ Dring,
                                                       double* __restrict__ r, SolverState* st, double* __restrict__ hist,

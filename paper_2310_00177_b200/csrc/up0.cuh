@@ -142,11 +142,16 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
     cp_wait<0>();
 }
 
-#ifndef UP0_MINB
-#define UP0_MINB 1  // register caps measured slower: 4 blocks/SM (48 regs) 61 -> 64 us, 5 (42) -> 66 us
+// UP0_MINB: optional register cap. Unset, the bound has no block count and
+// ptxas settles at 64 registers (4 blocks/SM); an explicit 1 gives 80 (3 blocks,
+// 54.6 -> 56.1 us), 4 gives 48 (61 -> 64 us), 5 gives 42 (-> 66 us).
+#ifdef UP0_MINB
+#define UP0_BOUNDS __launch_bounds__(kSX* kSY, UP0_MINB)
+#else
+#define UP0_BOUNDS __launch_bounds__(kSX* kSY)
 #endif
 template <int NO>
-__global__ void __launch_bounds__(kSX* kSY, UP0_MINB) k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ cls,
+__global__ void UP0_BOUNDS k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ cls,
                                                     const float* __restrict__ outc, const float* __restrict__ y0,
                                                     const float* __restrict__ zab, const __grid_constant__ KC0 kc,
                                                     double* __restrict__ dout, SolverState* st,
