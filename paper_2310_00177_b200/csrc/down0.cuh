@@ -216,7 +216,7 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
 // segment); dynamic smem = sizeof(Down0Smem). Units outside the schedule have
 // an all-zero window: their x_1 cells keep the zeros set before the solve.
 #ifndef D0_MINB
-#define D0_MINB 3  // 3 blocks/SM (77 registers; 116 uncapped, 2 blocks): 67 -> 61 us at C3 256^3
+#define D0_MINB 3  // 3 blocks/SM (77 registers; 116 uncapped, 2 blocks): 67 -> 61 us at C3 256^3; 4 (64 registers): 62.3 us
 #endif
 __global__ void __launch_bounds__(kSX* kSY, D0_MINB) k_down_l0(Geom g, const uint8_t* __restrict__ cls,
                                                       const double* __restrict__ r, const SolverState* __restrict__ st,
