@@ -23,6 +23,7 @@ summed in rank order. `--slab` forces that path at N=1
 from __future__ import annotations
 
 import argparse
+import functools
 import json
 import math
 import os
@@ -51,6 +52,25 @@ def canonical_bytes_per_cell(depth: int) -> dict[str, float]:
         m[f"P2_down_L{l}"] = 20.5 / 8 ** l
         m[f"P2_up_L{l}"] = 20.5 / 8 ** l
     m[f"P2_coarse_L{depth - 1}"] = 20.0 / 8 ** (depth - 1)
+    return m
+
+
+def processed_bytes(depth: int, n_c: int, n_f: int) -> dict[str, float]:
+    """Algorithmic bytes per phase over the cells the launches actually
+    process: the f64 solver vectors, the cell byte and the
+    level-0 activation y0 exist only at fluid cells (the zero invariant:
+    non-fluid entries are exact zeros that are never read); the coarse
+    activations x1/out1 and the coarse levels cover their whole grids (the
+    network processes all of D).
+      P1  r 8 + cell 1 + y0 4 per fluid cell; x1 0.5 per fine cell
+      P2  SURVEY §8d per coarse kernel (all cells)
+      P3  out1 0.5 per fine cell; cell 1 + y0 4 + d1,Ad1,d2,Ad2 32 + d 8 per fluid cell
+      P4  49 per fluid cell (d, d1, d2, r, cell; d', Ad')
+      P5  41 per fluid cell (x, d', b, cell; x, r)"""
+    m = {"P1": 13.0 * n_f + 0.5 * n_c, "P3": 45.0 * n_f + 0.5 * n_c, "P4": 49.0 * n_f, "P5": 41.0 * n_f}
+    for k, v in canonical_bytes_per_cell(depth).items():
+        if k.startswith("P2"):
+            m[k] = v * n_c
     return m
 
 
@@ -140,11 +160,33 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- workload
-def workload(args):
-    from paper_2310_00177_b200 import scenes
+@functools.lru_cache(maxsize=None)
+def scenes_module():
+    """paper_2310_00177_b200/scenes.py (pure numpy geometry) loaded by path, so
+    the reference arm never imports the product package or its library."""
+    import importlib.util
 
-    types, seed = scenes.config(args.config, args.n)
+    spec = importlib.util.spec_from_file_location("npsd_bench_scenes", ROOT / "paper_2310_00177_b200" / "scenes.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def workload(args):
+    types, seed = scenes_module().config(args.config, args.n)
     return types, seed
+
+
+def read_npm(path) -> tuple[int, int, np.ndarray]:
+    """Model file ("NPMW", u32 version 1, u32 dim, u32 depth, f32 LE weights;
+    net_params.cpp:42-52 layout) parsed with numpy: (dim, depth, weights)."""
+    raw = Path(path).read_bytes()
+    if raw[:4] != b"NPMW":
+        raise ValueError(f"{path}: bad magic")
+    ver, dim, depth = np.frombuffer(raw[4:16], "<u4")
+    if ver != 1:
+        raise ValueError(f"{path}: bad version {ver}")
+    return int(dim), int(depth), np.frombuffer(raw[16:], "<f4").copy()
 
 
 WEIGHTS = ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm"
@@ -163,49 +205,52 @@ def load_weights(kind: str, depth: int):
     return b200.identity_params(depth)
 
 
-def iteration_count_fixture(config: str, weights: str = "identity") -> int | None:
-    p = ROOT / "tests" / "golden" / "iteration_counts.json"
-    key = f"{config}_trained" if weights == "trained" else config
-    if p.exists():
-        d = json.loads(p.read_text())
-        if key in d:
-            return int(d[key]["iterations"])
-    return None
-
-
 # ------------------------------------------------------------- CPU legs
-def cpu_reference_sample(types, seed, depth, iters_to_solution, sample_iters, cores, weights="identity"):
-    """Reference psdo_solve (oracle/_ref: the unmodified reference solver,
-    assembly and reduce, with the 3D network restatement as its
-    Preconditioner) on a bounded sample: full setup + `sample_iters` PSDO
-    iterations on the same 256^3 frame. Time-to-solution = setup +
-    iterations-to-solution x measured per-iteration time."""
+def reference_weights(kind: str, depth: int) -> np.ndarray:
+    """The same weights the B200 arm uses, obtained without the product
+    library: the model file parsed with numpy, or the oracle's init/identity
+    (bitwise equal to the product's, tests/test_abi.py)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import Oracle  # checker / baseline only
+
+    if kind == "trained":
+        dim, d, w = read_npm(WEIGHTS)
+        if (dim, d) != (3, depth):
+            raise SystemExit(f"trained weights are dim {dim} depth {d}, not 3/{depth}")
+        return w
+    if kind == "random":
+        return Oracle().init_params(3, depth, 42)
+    return Oracle().identity_params(3, depth)
+
+
+def cpu_reference_solve(types, seed, depth, cores, weights="trained", max_iters=20000):
+    """One reference time-to-solution, measured (not extrapolated): the
+    unmodified reference psdo_solve (solver.cpp:189-276) on its own
+    assemble_poisson_3d + reduce (oracle/_ref), with the 3D network
+    restatement as its Preconditioner and the B200 arm's weights, run to
+    rel-res 1e-6 on all `cores` host threads. TTS = setup (assembly, reduce,
+    NetContext build) + solve, the two spans the reference solver reports."""
     os.environ["OMP_NUM_THREADS"] = str(cores)
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_lib import Ref  # checker / baseline only
 
     ref = Ref()
-    import paper_2310_00177_b200 as b200
-
-    p = load_weights(weights, depth).flat
+    p = reference_weights(weights, depth)
     b = ref.rhs_normal(seed, types.size)[types.reshape(-1) == 0]
     t0 = time.perf_counter()
-    r = ref.psdo_solve(types, b, mode="neural", params=p, depth=depth, max_iters=sample_iters,
-                       tol_reduction=1e-300)
+    r = ref.psdo_solve(types, b, mode="neural", params=p, depth=depth, max_iters=max_iters, tol_reduction=1e-6,
+                       n_ortho=2)
     wall = time.perf_counter() - t0
-    per_iter_ms = 1e3 * r["solve_seconds"] / sample_iters
-    setup_ms = 1e3 * r["setup_seconds"]
+    setup_ms, solve_ms = 1e3 * r["setup_seconds"], 1e3 * r["solve_seconds"]
+    it = int(r["iterations"])
     return {
-        "value": setup_ms + iters_to_solution * per_iter_ms,
-        "unit": UNIT,
-        "cores": cores,
-        "kind": "reference",
-        "sample": (f"{types.shape[0]}^3 {args_config_name}, {weights} weights: reference assemble_poisson_3d+reduce+"
-                   "NeuralPrecond3D setup "
-                   f"({setup_ms:.0f} ms) + {sample_iters} PSDO iterations ({per_iter_ms:.1f} ms/iter); TTS = setup + "
-                   f"{iters_to_solution} iterations x per-iter (extrapolated); {wall:.1f} s wall"),
-        "setup_ms": setup_ms,
-        "per_iter_ms": per_iter_ms,
+        "value": setup_ms + solve_ms, "unit": UNIT, "cores": cores, "kind": "reference",
+        "sample": (f"{types.shape[0]}^3 {args_config_name}, {weights} weights: one full reference solve to rel-res "
+                   f"1e-6 (measured, not extrapolated): setup {setup_ms:.0f} ms (assemble_poisson_3d + reduce + "
+                   f"NeuralPrecond3D build) + {it} PSDO iterations {solve_ms:.0f} ms ({solve_ms / max(it, 1):.1f} "
+                   f"ms/iter); {wall:.1f} s wall"),
+        "setup_ms": setup_ms, "solve_ms": solve_ms, "iterations": it, "converged": bool(r["converged"]),
+        "per_iter_ms": solve_ms / max(it, 1), "wall_s": wall,
     }
 
 
@@ -214,36 +259,46 @@ args_config_name = "C3"
 
 # ------------------------------------------------------------- reference arm
 def run_reference(args) -> None:
+    """The reference's CPU implementation of the path (oracle/_ref: the
+    unmodified reference solver with the 3D network restatement), each step a
+    full measured time-to-solution on the B200 arm's config and weights. The
+    steps run until --ref-budget-s is spent (at least one), so `steps` is the
+    number actually timed. Nothing here loads the product library."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     global args_config_name
     args_config_name = args.config
     types, seed = workload(args)
-    n_iters = iteration_count_fixture(args.config, args.weights) if args.n is None else None
-    if n_iters is None:
-        n_iters = args.ref_iters
     cores = os.cpu_count() or 1
+    t_start = time.perf_counter()
+    warm = []
+    for _ in range(min(args.warmup, 1)):
+        warm.append(cpu_reference_solve(types, seed, args.depth, cores, args.weights))
     vals, samples = [], []
-    for step in range(args.warmup + args.steps):
-        s = cpu_reference_sample(types, seed, args.depth, n_iters, args.cpu_sample_iters, cores, args.weights)
-        if step >= args.warmup:
-            vals.append(s["value"])
-            samples.append(s)
+    while len(vals) < args.steps:
+        s = cpu_reference_solve(types, seed, args.depth, cores, args.weights)
+        vals.append(s["value"])
+        samples.append(s)
+        if time.perf_counter() - t_start + s["wall_s"] > args.ref_budget_s:
+            break
     v = float(np.mean(vals))
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": len(vals),
+        "warmup": len(warm), "ms_per_step": v, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 solver / f32 network", "data": "synthetic",
-        "config": {"workload": f"{args.config} {types.shape[0]}^3 (SURVEY §8d)", "weights": args.weights,
-                   "depth": args.depth, "iterations_to_solution": n_iters,
-                   "iterations_source": "tests/golden/iteration_counts.json (reference psdo_solve run to 1e-6 with "
-                                        "the same weights)"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": samples[-1]["sample"]},
+        "config": {"workload": f"{args.config} {types.shape[0]}^3 {scenes_module().DESCRIPTION[args.config]} "
+                               "(SURVEY §8d), one frame per step: setup + PSDO to rel-res 1e-6",
+                   "weights": args.weights, "depth": args.depth, "iterations": samples[-1]["iterations"],
+                   "converged": all(x["converged"] for x in samples),
+                   "steps_requested": args.steps, "warmup_requested": args.warmup,
+                   "budget": f"full solves until {args.ref_budget_s:.0f} s are spent (at least one)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": samples[-1]["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "per_iter_ms": float(np.mean([s["per_iter_ms"] for s in samples])),
-        "setup_ms": float(np.mean([s["setup_ms"] for s in samples])),
+        "per_iter_ms": float(np.mean([x["per_iter_ms"] for x in samples])),
+        "setup_ms": float(np.mean([x["setup_ms"] for x in samples])),
+        "step_ms": vals,
+        "product_library_loaded": "libnpsd_b200" in Path("/proc/self/maps").read_text(),
     }
     print(json.dumps(line), flush=True)
 
@@ -292,27 +347,92 @@ def sequence_c4(params, cfg, device: int, frames: int = 32, n: int = 128, repeat
 
 
 # ------------------------------------------------------------------ B200 arm
-def run_b200(args) -> None:
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    if world > 1:
-        import torch.distributed as dist  # plumbing only: barrier + max over ranks (CPU/gloo)
+def timed_frames(ctx, d_types, d_b, d_x, cfg, steps: int, warmup: int, clk=None) -> dict:
+    """W untimed frames, then K timed ones: set_mask + PSDO to 1e-6 per step
+    between CUDA events on the context stream (inputs resident in HBM)."""
+    def step():
+        ctx.event_record(0)
+        ctx.set_mask_device(d_types.ptr)
+        rep = ctx.psdo_solve_device(d_b.ptr, d_x.ptr, cfg)
+        ctx.event_record(1)
+        return ctx.event_elapsed_ms(0, 1), rep, ctx.last_solve_ms
 
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("gloo")
+    for _ in range(warmup):
+        step()
+    ctx.synchronize()
+    if clk:
+        clk.start()
+    launches0 = ctx.launch_count
+    ms, iters, solve_ms, converged = [], [], [], []
+    for _ in range(steps):
+        t, rep, sm = step()
+        ms.append(t)
+        iters.append(rep.iterations)
+        solve_ms.append(sm)
+        converged.append(rep.converged)
+    ctx.synchronize()
+    out = {"launches": (ctx.launch_count - launches0) / steps, "clocks": clk.stop() if clk else None}
+    out["step_ms"] = float(np.mean(ms))
+    out["iterations"] = int(np.median(iters))
+    out["converged"] = bool(all(converged))
+    out["per_iter_ms"] = float(np.mean([s / max(i, 1) for s, i in zip(solve_ms, iters)]))
+    out["set_mask_ms"] = out["step_ms"] - float(np.mean(solve_ms))
+    return out
+
+
+def iteration_roofline(depth: int, n_c: int, n_f: int, per_iter_ms: float, peaks: dict) -> dict:
+    proc = sum(processed_bytes(depth, n_c, n_f).values())
+    canon = sum(canonical_bytes_per_cell(depth).values()) * n_c
+    gbs = proc / (per_iter_ms * 1e-3) / 1e9
+    cgbs = canon / (per_iter_ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": gbs / peaks["hbm_gbs"], "bytes": proc,
+            "bytes_model": "processed cells: solver vectors at fluid cells, coarse levels over all cells (DESIGN §4)",
+            "canonical_achieved": cgbs, "canonical_frac": cgbs / peaks["hbm_gbs"],
+            "canonical_bytes": f"SURVEY §8d B_iter = {canon / n_c:.2f} B x n_c (counts air/solid cells never read)",
+            "peak_source": peaks["source"]}
+
+
+def config_line(name: str, params, cfg, device: int, steps: int, warmup: int, cpu: bool) -> dict:
+    """A secondary north_star config (C1 64^3, C2 128^3) measured the same way
+    as the headline: TTS, per-iteration time, iteration roofline, and the
+    reference CPU solve to convergence beside it."""
     import paper_2310_00177_b200 as b200
-    from paper_2310_00177_b200 import scenes
+
+    types, seed = scenes_module().config(name)
+    n_c, n_f = types.size, int((types == 0).sum())
+    ctx = b200.Context(3, types.shape, params, device=device)
+    d_types, d_b, d_x = b200.DeviceBuffer(ctx, n_c), b200.DeviceBuffer(ctx, 8 * n_c), b200.DeviceBuffer(ctx, 8 * n_c)
+    d_types.upload(np.ascontiguousarray(types.reshape(-1)))
+    d_b.upload(scenes_module().full_rhs(types, seed, b200.rhs_normal))
+    ctx.synchronize()
+    m = timed_frames(ctx, d_types, d_b, d_x, cfg, steps, warmup)
+    for buf in (d_types, d_b, d_x):
+        buf.free()
+    ctx.close()
+    out = {"workload": f"{name} {types.shape[0]}^3 {scenes_module().DESCRIPTION[name]} (SURVEY §8d)",
+           "n_fluid": n_f, "tts_ms": m["step_ms"], "set_mask_ms": m["set_mask_ms"], "per_iter_ms": m["per_iter_ms"],
+           "iterations": m["iterations"], "converged": m["converged"], "gpu_launches": int(round(m["launches"])),
+           "steps": steps, "warmup": warmup,
+           "iteration_roofline": iteration_roofline(4, n_c, n_f, m["per_iter_ms"], load_peaks())}
+    if cpu:
+        c = cpu_reference_solve(types, seed, 4, os.cpu_count() or 1, "trained")
+        out["cpu_baseline"] = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    return out
+
+
+def run_b200(args) -> None:
+    import paper_2310_00177_b200 as b200
 
     global args_config_name
     args_config_name = args.config
     types, seed = workload(args)
     n_c = types.size
+    n_f = int((types == 0).sum())
     depth = args.depth
     params = load_weights(args.weights, depth)
-    ctx = b200.Context(3, types.shape, params, device=local)
-    bfull = scenes.full_rhs(types, seed, b200.rhs_normal)
+    ctx = b200.Context(3, types.shape, params, device=0)
+    bfull = scenes_module().full_rhs(types, seed, b200.rhs_normal)
     cfg = b200.SolveConfig(tol_reduction=1e-6, max_iters=args.max_iters, n_ortho=2)
 
     # device-resident inputs
@@ -322,46 +442,10 @@ def run_b200(args) -> None:
     d_types.upload(np.ascontiguousarray(types.reshape(-1)))
     d_b.upload(bfull)
     ctx.synchronize()
-
-    def step():
-        ctx.event_record(0)
-        ctx.set_mask_device(d_types.ptr)
-        rep = ctx.psdo_solve_device(d_b.ptr, d_x.ptr, cfg)
-        ctx.event_record(1)
-        return ctx.event_elapsed_ms(0, 1), rep, ctx.last_solve_ms
-
-    for _ in range(args.warmup):
-        step()
-    if dist:
-        dist.barrier()
-    ctx.synchronize()
-    clk = ClockSampler(local)
-    clk.start()
-    launches0 = ctx.launch_count
-    ms, iters, solve_ms, converged = [], [], [], []
-    for _ in range(args.steps):
-        t, rep, sm = step()
-        ms.append(t)
-        iters.append(rep.iterations)
-        solve_ms.append(sm)
-        converged.append(rep.converged)
-    ctx.synchronize()
-    launches = (ctx.launch_count - launches0) / args.steps
-    clocks = clk.stop()
-    step_ms = float(np.mean(ms))
-    if dist:
-        import torch
-
-        t = torch.tensor([step_ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms = float(t.item())
-    n_it = int(np.median(iters))
-    per_iter_ms = float(np.mean([s / max(i, 1) for s, i in zip(solve_ms, iters)]))
-    setup_ms = step_ms - float(np.mean(solve_ms))
-    model = canonical_bytes_per_cell(depth)
-    b_iter = sum(model.values()) * n_c
+    m = timed_frames(ctx, d_types, d_b, d_x, cfg, args.steps, args.warmup, ClockSampler(0))
+    step_ms, n_it, per_iter_ms = m["step_ms"], m["iterations"], m["per_iter_ms"]
     peaks = load_peaks()
-    iter_gbs = b_iter / (per_iter_ms * 1e-3) / 1e9
+    it_roof = iteration_roofline(depth, n_c, n_f, per_iter_ms, peaks)
 
     # per-kernel device times (kernels launched one by one between events)
     prof = ctx.profile_iterations(d_b.ptr, cfg, args.profile_iters)
@@ -372,14 +456,14 @@ def run_b200(args) -> None:
         phase_ms[ph] = phase_ms.get(ph, 0.0) + v
         phase_kernels.setdefault(ph, []).append(k)
     dom = max(phase_ms, key=phase_ms.get)
-    dom_bytes = model.get(dom, 0.0) * n_c
+    dom_bytes = processed_bytes(depth, n_c, n_f)[dom]
+    dom_canon = canonical_bytes_per_cell(depth)[dom] * n_c
     dom_gbs = dom_bytes / (phase_ms[dom] * 1e-3) / 1e9
     prof_total = sum(prof.values())
     dom_traffic = ncu_traffic(phase_kernels[dom], types.shape[0])
 
     # end to end through the public host API: pinned host inputs, H2D each step,
     # solution read back each step (host wall clock around the synchronous calls)
-    n_f = int((types == 0).sum())
     p_types = b200.PinnedBuffer(ctx, n_c, np.uint8)
     p_b = b200.PinnedBuffer(ctx, n_f, np.float64)
     p_x = b200.PinnedBuffer(ctx, n_f, np.float64)
@@ -395,28 +479,24 @@ def run_b200(args) -> None:
             e2e.append(1e3 * (t1 - t0))
     e2e_ms = float(np.mean(e2e))
     hist_bytes = 8 * (res.report.iterations + 1) * 2
-    if dist:
-        import torch
-
-        t = torch.tensor([e2e_ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
 
     # the same frame with identity-equivalent weights (PSDO == CG, the network
     # still runs in full): what the trained model buys
     alt = {}
     if args.weights != "identity":
         ctx.set_params(b200.identity_params(depth))
-        t_alt = [step() for _ in range(2)][-1]
-        alt = {"weights": "identity", "tts_ms": t_alt[0], "iterations": int(t_alt[1].iterations),
-               "per_iter_ms": t_alt[2] / max(t_alt[1].iterations, 1)}
+        a = timed_frames(ctx, d_types, d_b, d_x, cfg, 1, 1)
+        alt = {"weights": "identity", "tts_ms": a["step_ms"], "iterations": a["iterations"],
+               "per_iter_ms": a["per_iter_ms"]}
         ctx.set_params(params)
         ctx.set_mask_device(d_types.ptr)
 
-    # the paper's comparison columns on the same device and frame: GPU CG,
-    # Jacobi-PCG and IC0-PCG (pcg_solve, solver.cpp:36-109), device-resident inputs
+    # the paper's comparison columns on the same device and frame: GPU CG and
+    # Jacobi-PCG (pcg_solve, solver.cpp:36-109), device-resident inputs. IC0-PCG
+    # is parity-tested but not timed here: its level-scheduled sweeps (766
+    # launches per apply at 256^3) are latency-bound by construction.
     baselines = {}
-    for kind, name in (("identity", "gpu_cg"), ("jacobi", "gpu_pcg_jacobi"), ("ic0", "gpu_pcg_ic0")):
+    for kind, name in (("identity", "gpu_cg"), ("jacobi", "gpu_pcg_jacobi")):
         ms_k, it_k = [], []
         for i in range(2):
             rep_k = ctx.pcg_solve_device(d_b.ptr, d_x.ptr, cfg, precond=kind)
@@ -425,76 +505,70 @@ def run_b200(args) -> None:
                 it_k.append(rep_k.iterations)
         baselines[name] = {"solve_ms": float(np.mean(ms_k)), "iterations": int(it_k[-1]),
                            "per_iter_ms": float(np.mean(ms_k)) / max(it_k[-1], 1), "converged": bool(rep_k.converged)}
-    baselines["gpu_pcg_ic0"]["note"] = ("IC0 factor (per solve, level-scheduled) outside solve_ms; each apply is two "
-                                        "sweeps of one launch per hyperplane x+y+z=h (766 at 256^3)")
-
-    seq = None
-    if world == 1 and args.config == "C3" and args.n is None and not args.no_sequence:
-        seq = sequence_c4(params, cfg, local)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_reference_sample(types, seed, depth, n_it, args.cpu_sample_iters, os.cpu_count() or 1,
-                                       args.weights)
-            cpu.pop("setup_ms", None)
-            cpu.pop("per_iter_ms", None)
-        except Exception as e:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"unavailable: {e}"}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": step_ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64 solver / f32 network", "data": "synthetic",
-            "config": {
-                "workload": f"{args.config} {types.shape[0]}^3 droplet-in-pool (SURVEY §8d), one frame per step: "
-                            "set_mask + PSDO to rel-res 1e-6",
-                "n_fluid": n_f, "depth": depth, "n_ortho": 2, "weights": args.weights,
-                "iterations": n_it, "converged": bool(all(converged)),
-                "parallelism": "replicas" if world > 1 else "single",
-                "l2": "inputs larger than L2 (solver vectors 8 B x n_c each, ~134 MB at 256^3, >= 126 MB L2)",
-            },
-            "per_iter_ms": per_iter_ms,
-            "setup_ms": setup_ms,
-            "hbm_gbs_iteration": iter_gbs,
-            "iteration_roofline": {"bound": "hbm", "achieved": iter_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                                   "frac": iter_gbs / peaks["hbm_gbs"],
-                                   "bytes": f"canonical B_iter = {sum(model.values()):.2f} B x n_c (SURVEY §8d)",
-                                   "peak_source": peaks["source"]},
-            "roofline": {"bound": "hbm", "kernel": "+".join(phase_kernels[dom]), "phase": dom, "achieved": dom_gbs,
-                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": dom_gbs / peaks["hbm_gbs"],
-                         "traffic": dom_traffic,
-                         "dram_gbs": (dom_traffic / (phase_ms[dom] * 1e-3) / 1e9) if dom_traffic else None,
-                         "dram_frac": (dom_traffic / (phase_ms[dom] * 1e-3) / 1e9 / peaks["hbm_gbs"])
-                         if dom_traffic else None,
-                         "note": "achieved/frac use SURVEY §8d's canonical bytes, which count every cell; the kernel "
-                                 "skips air/solid cells (exact zeros, never read), so its DRAM traffic is below the "
-                                 "model and frac can exceed 1. dram_gbs/dram_frac use the ncu-measured traffic.",
-                         "bytes_per_launch": dom_bytes, "ms_per_launch": phase_ms[dom],
-                         "share_of_iteration": phase_ms[dom] / prof_total, "peak_source": peaks["source"],
-                         "bytes_model": f"SURVEY §8d canonical {model[dom]:.3f} B/cell x {n_c} cells ({dom})"},
-            "kernel_ms": prof,
-            "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(n_c + 8 * n_f),
-                    "d2h_bytes_per_step": int(8 * n_f + hist_bytes),
-                    "how": "Context.set_mask(pinned types) + Context.psdo_solve(pinned b) -> pinned x; host wall clock"},
-            "gpu_launches": int(round(launches)),
-            "clocks": clocks,
-            "cpu_baseline": cpu,
-            "baselines_same_gpu": baselines,
-            "identity_weights_same_gpu": alt,
-            "sequence_c4": seq,
-        }
-        print(json.dumps(line), flush=True)
     for buf in (d_types, d_b, d_x):
         buf.free()
     for buf in (p_types, p_b, p_x):
         buf.free()
     ctx.close()
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+
+    headline = args.config == "C3" and args.n is None
+    seq = sequence_c4(params, cfg, 0) if headline and not args.no_sequence else None
+    others = {}
+    if headline and not args.no_configs:
+        for name in ("C1", "C2"):
+            others[name] = config_line(name, params, cfg, 0, args.steps, args.warmup, not args.no_cpu_baseline)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_solve(types, seed, depth, os.cpu_count() or 1, args.weights)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": METRIC, "value": step_ms, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 solver / f32 network", "data": "synthetic",
+        "config": {
+            "workload": f"{args.config} {types.shape[0]}^3 {scenes_module().DESCRIPTION[args.config]} (SURVEY §8d), "
+                        "one frame per step: set_mask + PSDO to rel-res 1e-6",
+            "n_fluid": n_f, "depth": depth, "n_ortho": 2, "weights": args.weights,
+            "iterations": n_it, "converged": m["converged"], "parallelism": "single",
+            "l2": "inputs larger than L2 (solver vectors 8 B x n_c each, ~134 MB at 256^3, >= 126 MB L2)",
+        },
+        "per_iter_ms": per_iter_ms,
+        "setup_ms": m["set_mask_ms"],
+        "hbm_gbs_iteration": it_roof["achieved"],
+        "iteration_roofline": it_roof,
+        "roofline": {"bound": "hbm", "kernel": "+".join(phase_kernels[dom]), "phase": dom, "achieved": dom_gbs,
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": dom_gbs / peaks["hbm_gbs"],
+                     "traffic": dom_traffic,
+                     "dram_gbs": (dom_traffic / (phase_ms[dom] * 1e-3) / 1e9) if dom_traffic else None,
+                     "dram_frac": (dom_traffic / (phase_ms[dom] * 1e-3) / 1e9 / peaks["hbm_gbs"])
+                     if dom_traffic else None,
+                     "canonical_achieved": dom_canon / (phase_ms[dom] * 1e-3) / 1e9,
+                     "canonical_frac": dom_canon / (phase_ms[dom] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                     "note": "achieved/frac: algorithmic bytes over the cells the launch processes (fluid cells for "
+                             "the solver vectors; DESIGN §4). canonical_*: SURVEY §8d bytes over every cell, "
+                             "including air/solid cells the kernel never reads. dram_*: ncu-measured traffic "
+                             "(profiles/ncu_traffic_<n>.json).",
+                     "bytes_per_launch": dom_bytes, "ms_per_launch": phase_ms[dom],
+                     "share_of_iteration": phase_ms[dom] / prof_total, "peak_source": peaks["source"]},
+        "kernel_ms": prof,
+        "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(n_c + 8 * n_f),
+                "d2h_bytes_per_step": int(8 * n_f + hist_bytes),
+                "how": "Context.set_mask(pinned types) + Context.psdo_solve(pinned b) -> pinned x; host wall clock"},
+        "gpu_launches": int(round(m["launches"])),
+        "clocks": m["clocks"],
+        "cpu_baseline": cpu,
+        "baselines_same_gpu": baselines,
+        "identity_weights_same_gpu": alt,
+        "sequence_c4": seq,
+        "configs": others,
+    }
+    print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------- B200 arm, z-slab
@@ -659,8 +733,9 @@ def main() -> None:
     ap.add_argument("--weights", default="trained", choices=["trained", "identity", "random"])
     ap.add_argument("--max-iters", type=int, default=20000)
     ap.add_argument("--profile-iters", type=int, default=5)
-    ap.add_argument("--cpu-sample-iters", type=int, default=2)
-    ap.add_argument("--ref-iters", type=int, default=1000, help="iterations-to-solution if no fixture exists")
+    ap.add_argument("--ref-budget-s", type=float, default=300.0,
+                    help="reference arm: full solves until this many seconds are spent (at least one)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1/C2 lines of the N=1 run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sequence", action="store_true", help="skip the C4 32-frame 128^3 sequence")
     ap.add_argument("--slab", action="store_true", help="z-slab path even at N=1 (one-rank NCCL)")

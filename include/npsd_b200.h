@@ -67,7 +67,9 @@ typedef struct {
     int32_t n_ortho;              /* A-orthogonalise against the last n_ortho directions (0..8) */
     int32_t nullspace_projection; /* bool */
     int32_t normalize_before_precond; /* bool */
-    int32_t reserved;
+    int32_t precond;              /* psdo: 0 = the network (NeuralPrecond), 1 = IdentityPrecond
+                                     (precond.cpp:7-10: d = r / ||r||), 2 = JacobiPrecond
+                                     (precond.cpp:12-26; single-domain); pcg takes its own argument */
 } npsd_b200_solve_cfg;
 
 /* SolveReport (include/npsd/solver.hpp:28-37). residual_history and
@@ -77,11 +79,14 @@ typedef struct {
     int32_t converged;
     int32_t breakdown;
     const double* residual_history;   /* ||r_0|| ... ||r_k||, length history_len = iterations + 1 */
-    const double* cumulative_seconds; /* device %globaltimer at each history entry, from solve start */
+    const double* cumulative_seconds; /* device %globaltimer at each history entry, from the solve's first
+                                         kernel (solver.cpp:192,212,263); entry 0 = setup_seconds */
     int64_t history_len;
-    double setup_seconds;    /* set_mask excluded: r0 = b - A x0 and the first norm */
-    double iterate_seconds;
-    double precond_seconds;  /* not separable inside the device loop: 0 */
+    double setup_seconds;    /* set_mask excluded: projections, r0 = b - A x0 and its norm (solver.cpp:211) */
+    double iterate_seconds;  /* device solve time minus setup_seconds (solver.cpp:275) */
+    double precond_seconds;  /* sum of the per-iteration preconditioner spans (solver.cpp:230-237), from
+                                %globaltimer stamps: end of the previous iteration -> start of the first
+                                kernel after the network (includes the launch gaps between them) */
 } npsd_b200_report;
 
 /* Weights: n_params f32 in for_each_span order for (dim, depth).
@@ -102,6 +107,22 @@ int npsd_b200_set_mask_device(npsd_b200_ctx* ctx, const uint8_t* d_cell_types);
 int64_t npsd_b200_n_fluid(const npsd_b200_ctx* ctx);
 /* Ascending fluid cell linear indices (length n_fluid). */
 int npsd_b200_fluid_indices(npsd_b200_ctx* ctx, int64_t* out);
+
+/* is_pure_neumann (discretization.cpp:180-191) of the current mask, 3D with
+ * six face neighbours: *out = 1 when no fluid cell has an air face neighbour
+ * (outside the domain is solid), i.e. the reduced system is singular and the
+ * caller should set nullspace_projection (bench.cpp:52, npsd_cli.cpp:280). */
+int npsd_b200_is_pure_neumann(npsd_b200_ctx* ctx, int* out);
+
+/* Checks a caller's reduced CSR matrix (SparseMatrix, sparse.hpp:11-18:
+ * n_rows, row_offsets[n_rows+1], col_indices/values[nnz]) against the
+ * flag-derived operator the solve uses (assemble_poisson[_3d] + reduce,
+ * discretization.cpp:21-160): row count, every row's nnz, diagonal value and
+ * -1 off-diagonals; with full != 0 also A v for a fixed pseudo-random v,
+ * computed here in CSR order like spmv (sparse.cpp:100-117), bitwise against
+ * the device operator. NPSD_INVALID_ARGUMENT names the first mismatching row. */
+int npsd_b200_check_operator(npsd_b200_ctx* ctx, int64_t n_rows, const int64_t* row_offsets,
+                             const int64_t* col_indices, const double* values, int64_t nnz, int full);
 
 /* Preconditioner::apply on reduced host vectors (NeuralPrecond semantics). */
 int npsd_b200_precond_apply(npsd_b200_ctx* ctx, const double* r_reduced, double* z_reduced, int64_t n_f);
@@ -139,8 +160,9 @@ void npsd_b200_rhs_normal(uint64_t seed, int64_t n, double* out);
  * (precond.cpp:12-26; NPSD_INVALID_ARGUMENT "jacobi precond: zero diagonal"
  * like the reference's constructor), 2 = IC0 (precond.cpp:28-112, see
  * npsd_b200_ic0_apply; factored per solve on the current frame). Same vectors, report and errors as
- * psdo_solve; n_ortho and normalize_before_precond are ignored, nullspace
- * projection is not supported. The baseline the paper compares NPSDO with. */
+ * psdo_solve (nullspace projection as pcg_solve :45-48, 82); n_ortho,
+ * normalize_before_precond and precond of the cfg are ignored. The baseline the
+ * paper compares NPSDO with. */
 int npsd_b200_pcg_solve(npsd_b200_ctx* ctx, const double* b, const double* x0, const npsd_b200_solve_cfg* cfg,
                         int precond, double* x, npsd_b200_report* rep);
 int npsd_b200_pcg_solve_device(npsd_b200_ctx* ctx, const double* d_b, const double* d_x0,

@@ -4,6 +4,7 @@
 //   npsd::b200::NeuralPrecond  : npsd::Preconditioner      (precond.hpp:12-29;
 //                                same ctor as net::NeuralPrecond, net/precond.hpp:14-30)
 //   npsd::b200::neural_precond                                (net/precond.hpp:32-33)
+//   npsd::b200::IdentityPrecond : npsd::Preconditioner     (precond.hpp:35-43)
 //   npsd::b200::psdo_solve / psd_solve                        (solver.hpp:64-69)
 //
 // The reference's psdo_solve can drive a b200::NeuralPrecond unchanged (host
@@ -42,6 +43,20 @@ inline std::vector<float> flatten(const net::NetParams& p) {
     out.reserve(static_cast<std::size_t>(p.parameter_count()));
     p.for_each_span([&](const float* s, std::size_t n) { out.insert(out.end(), s, s + n); });
     return out;
+}
+
+// cell types (0 fluid, 1 air, 2 solid) of an image / volume, x fastest
+inline std::vector<uint8_t> types_of(const IndicatorImage& I) {
+    std::vector<uint8_t> t(static_cast<std::size_t>(I.cells()));
+    for (index_t y = 0; y < I.ny; ++y)
+        for (index_t x = 0; x < I.nx; ++x)
+            t[static_cast<std::size_t>(y * I.nx + x)] = static_cast<uint8_t>(cell_type(I, x, y));
+    return t;
+}
+inline std::vector<uint8_t> types_of(const IndicatorVolume& V) {
+    std::vector<uint8_t> t(V.cells.size());
+    for (std::size_t i = 0; i < t.size(); ++i) t[i] = static_cast<uint8_t>(V.cells[i]);
+    return t;
 }
 
 class NeuralPrecond : public Preconditioner {
@@ -87,20 +102,58 @@ private:
             throw std::invalid_argument(msg);
         }
     }
-    static std::vector<uint8_t> types_of(const IndicatorImage& I) {
-        std::vector<uint8_t> t(static_cast<std::size_t>(I.cells()));
-        for (index_t y = 0; y < I.ny; ++y)
-            for (index_t x = 0; x < I.nx; ++x)
-                t[static_cast<std::size_t>(y * I.nx + x)] = static_cast<uint8_t>(cell_type(I, x, y));
-        return t;
+    npsd_b200_ctx* ctx_ = nullptr;
+};
+
+// IdentityPrecond (precond.hpp:35-43, precond.cpp:7-10) for b200::psdo_solve:
+// apply copies like the reference's; inside b200::psdo_solve the device loop
+// forms d = r / ||r|| without the network. The image gives the device its
+// matrix-free operator (an IdentityPrecond alone carries no grid).
+class IdentityPrecond : public Preconditioner {
+public:
+    explicit IdentityPrecond(const IndicatorImage& I, int device = 0) : IdentityPrecond(2, I.nx, I.ny, 1, types_of(I), device) {}
+    explicit IdentityPrecond(const IndicatorVolume& V, int device = 0)
+        : IdentityPrecond(3, V.nx, V.ny, V.nz, types_of(V), device) {}
+    IdentityPrecond(const IdentityPrecond&) = delete;
+    IdentityPrecond& operator=(const IdentityPrecond&) = delete;
+    ~IdentityPrecond() override { npsd_b200_destroy(ctx_); }
+
+    using Preconditioner::apply;
+    void apply(const Vector& r, Vector& z) const override {
+        require(static_cast<index_t>(r.size()) == size(), "IdentityPrecond::apply: size mismatch");
+        z = r;
     }
-    static std::vector<uint8_t> types_of(const IndicatorVolume& V) {
-        std::vector<uint8_t> t(V.cells.size());
-        for (std::size_t i = 0; i < t.size(); ++i) t[i] = static_cast<uint8_t>(V.cells[i]);
-        return t;
+    bool is_linear() const override { return true; }
+    bool is_symmetric() const override { return true; }
+    index_t size() const override { return static_cast<index_t>(npsd_b200_n_fluid(ctx_)); }
+    std::string name() const override { return "identity"; }
+    npsd_b200_ctx* context() const { return ctx_; }
+
+private:
+    IdentityPrecond(int dim, index_t nx, index_t ny, index_t nz, const std::vector<uint8_t>& types, int device) {
+        std::vector<float> p(npsd_b200_param_count(dim, 1));  // the network is never run: depth 1
+        check(npsd_b200_identity_params(dim, 1, p.data()), nullptr);
+        check(npsd_b200_create(dim, static_cast<int>(nx), static_cast<int>(ny), static_cast<int>(nz), 1, p.data(),
+                               p.size(), &device, 1, &ctx_),
+              nullptr);
+        const int st = npsd_b200_set_mask(ctx_, types.data());
+        if (st != NPSD_OK) {
+            const std::string msg = npsd_b200_last_error(ctx_);
+            npsd_b200_destroy(ctx_);
+            throw std::invalid_argument(msg);
+        }
     }
     npsd_b200_ctx* ctx_ = nullptr;
 };
+
+// How b200::psdo_solve checks the caller's A against the flag-derived operator
+// (npsd_b200_check_operator): rows = every row's nnz, diagonal and -1
+// off-diagonals (always, O(nnz) on the host); full = also A v bitwise (debug).
+enum class OperatorCheck { rows, full };
+inline OperatorCheck& operator_check() {
+    static OperatorCheck mode = OperatorCheck::rows;
+    return mode;
+}
 
 inline std::unique_ptr<Preconditioner> neural_precond(const net::NetParams& params, const IndicatorImage& I,
                                                       const ReductionMap& map) {
@@ -108,23 +161,37 @@ inline std::unique_ptr<Preconditioner> neural_precond(const net::NetParams& para
 }
 
 // psdo_solve (solver.cpp:189-276) with the loop on the device. The operator is
-// the flag-derived mixed-BC Laplacian of P's grid, i.e. the matrix
-// assemble_poisson[_3d] + reduce would build; A is checked for its size only.
-// P must be a b200::NeuralPrecond (no CPU path).
+// the flag-derived mixed-BC Laplacian of P's grid — the matrix
+// assemble_poisson[_3d] + reduce build — and A is checked against it
+// (operator_check()): a different A throws invalid_argument rather than
+// solving another system. P must be a b200::NeuralPrecond or a
+// b200::IdentityPrecond (no CPU path).
 inline SolveResult psdo_solve(const SparseMatrix& A, const Vector& b, const Preconditioner& P, const SolveConfig& cfg,
                               const Vector* x0 = nullptr) {
-    const auto* np = dynamic_cast<const NeuralPrecond*>(&P);
-    require(np != nullptr, "b200::psdo_solve: P must be a b200::NeuralPrecond");
+    npsd_b200_ctx* ctx = nullptr;
+    int precond = 0;
+    if (const auto* np = dynamic_cast<const NeuralPrecond*>(&P)) {
+        ctx = np->context();
+    } else if (const auto* ip = dynamic_cast<const IdentityPrecond*>(&P)) {
+        ctx = ip->context();
+        precond = 1;
+    }
+    require(ctx != nullptr, "b200::psdo_solve: P must be a b200::NeuralPrecond or b200::IdentityPrecond");
     require(A.n_rows == A.n_cols, "solve: matrix not square");
-    require(static_cast<index_t>(b.size()) == A.n_rows && A.n_rows == np->size(), "solve: rhs length mismatch");
+    require(static_cast<index_t>(b.size()) == A.n_rows && A.n_rows == P.size(), "solve: rhs length mismatch");
     if (x0) require(static_cast<index_t>(x0->size()) == A.n_rows, "solve: x0 length mismatch");
+    static_assert(sizeof(index_t) == sizeof(int64_t), "CSR indices are int64");
+    check(npsd_b200_check_operator(ctx, A.n_rows, reinterpret_cast<const int64_t*>(A.row_offsets.data()),
+                                   reinterpret_cast<const int64_t*>(A.col_indices.data()), A.values.data(),
+                                   static_cast<int64_t>(A.values.size()), operator_check() == OperatorCheck::full),
+          ctx);
     npsd_b200_solve_cfg c{cfg.tol_reduction, cfg.tol_abs, static_cast<int64_t>(cfg.max_iters), cfg.n_ortho,
-                          cfg.nullspace_projection ? 1 : 0, cfg.normalize_before_precond ? 1 : 0, 0};
+                          cfg.nullspace_projection ? 1 : 0, cfg.normalize_before_precond ? 1 : 0, precond};
     SolveResult res;
     res.x.assign(b.size(), 0.0);
     npsd_b200_report rep{};
-    const int st = npsd_b200_psdo_solve(np->context(), b.data(), x0 ? x0->data() : nullptr, &c, res.x.data(), &rep);
-    check(st, np->context());
+    const int st = npsd_b200_psdo_solve(ctx, b.data(), x0 ? x0->data() : nullptr, &c, res.x.data(), &rep);
+    check(st, ctx);
     res.report.iterations = rep.iterations;
     res.report.converged = rep.converged != 0;
     res.report.residual_history.assign(rep.residual_history, rep.residual_history + rep.history_len);

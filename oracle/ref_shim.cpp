@@ -298,7 +298,7 @@ int ref_psdo_solve(int dim, long nx, long ny, long nz, const unsigned char* type
 // precond 0 = IdentityPrecond (cg_solve), 1 = JacobiPrecond, 2 = Ic0Precond.
 int ref_pcg_solve(int dim, long nx, long ny, long nz, const unsigned char* types, int precond, const double* b,
                   double tol_reduction, long max_iters, double* x_out, double* hist, long* iterations, int* converged,
-                  long* hist_len) {
+                  long* hist_len, int nullspace) {
     return guarded([&] {
         const long rows = (dim == 3) ? ny * nz : ny;
         const auto I = image_from_types(nx, rows, types);
@@ -310,6 +310,7 @@ int ref_pcg_solve(int dim, long nx, long ny, long nz, const unsigned char* types
         npsd::SolveConfig cfg;
         cfg.tol_reduction = tol_reduction;
         cfg.max_iters = max_iters;
+        cfg.nullspace_projection = nullspace != 0;
         const std::size_t nf = static_cast<std::size_t>(sys.A.n_rows);
         npsd::Vector bv(b, b + nf);
         const auto res = npsd::pcg_solve(sys.A, bv, *P, cfg, nullptr);

@@ -67,10 +67,12 @@ class SolveConfig:
     nullspace_projection: bool = False
     normalize_before_precond: bool = True
 
-    def _c(self) -> _native.SolveCfg:
+    def _c(self, precond: int = 0) -> _native.SolveCfg:
+        """precond: 0 the network (NeuralPrecond), 1 IdentityPrecond (the
+        reference passes the preconditioner as psdo_solve's P argument)."""
         return _native.SolveCfg(float(self.tol_reduction), float(self.tol_abs), int(self.max_iters),
                                 int(self.n_ortho), int(bool(self.nullspace_projection)),
-                                int(bool(self.normalize_before_precond)), 0)
+                                int(bool(self.normalize_before_precond)), int(precond))
 
 
 @dataclass
@@ -321,6 +323,24 @@ class Context:
     def set_mask_device(self, ptr: int) -> None:
         self._ck(self.lib.npsd_b200_set_mask_device(self.h, C.c_void_p(ptr)))
 
+    def check_operator(self, row_offsets, col_indices, values, full: bool = False) -> None:
+        """Raise ValueError unless the reduced CSR matrix is the flag-derived
+        operator of the current mask (npsd_b200_check_operator)."""
+        ro = np.ascontiguousarray(row_offsets, np.int64)
+        ci = np.ascontiguousarray(col_indices, np.int64)
+        va = np.ascontiguousarray(values, np.float64)
+        if ci.size != va.size:
+            raise ValueError("check_operator: col_indices and values differ in length")
+        self._ck(self.lib.npsd_b200_check_operator(self.h, ro.size - 1, ro, ci, va, va.size, int(full)))
+
+    def is_pure_neumann(self) -> bool:
+        """is_pure_neumann (discretization.cpp:180-191) of the current mask: no
+        fluid cell has an air face neighbour (outside the domain is solid), so
+        the reduced system is singular and needs nullspace projection."""
+        out = C.c_int(0)
+        self._ck(self.lib.npsd_b200_is_pure_neumann(self.h, C.byref(out)))
+        return bool(out.value)
+
     @property
     def n_fluid(self) -> int:
         return int(self.lib.npsd_b200_n_fluid(self.h))
@@ -386,7 +406,7 @@ class Context:
                            float(rep.iterate_seconds), float(rep.precond_seconds), method)
 
     def psdo_solve(self, b: np.ndarray, cfg: SolveConfig, x0: np.ndarray | None = None,
-                   method: str = "psdo+neural", out: np.ndarray | None = None) -> SolveResult:
+                   method: str = "psdo+neural", out: np.ndarray | None = None, precond: str = "neural") -> SolveResult:
         b = np.ascontiguousarray(b, np.float64)
         x = np.empty_like(b) if out is None else out
         if x.dtype != np.float64 or x.size != b.size or not x.flags.c_contiguous:
@@ -400,7 +420,7 @@ class Context:
             x0p = x0a.ctypes.data_as(C.c_void_p)
         if b.size != self.n_fluid:
             raise ValueError("solve: rhs length mismatch")
-        c = cfg._c()
+        c = cfg._c(_PSDO_PRECOND[precond])
         st = self.lib.npsd_b200_psdo_solve(self.h, b, x0p, C.byref(c), x, C.byref(rep))
         if st == NPSD_BREAKDOWN:
             _raise(st, self.lib.npsd_b200_last_error(self.h).decode())
@@ -416,9 +436,13 @@ class Context:
         if b.size != self.n_fluid:
             raise ValueError("solve: rhs length mismatch")
         x = np.empty_like(b) if out is None else out
+        if x.dtype != np.float64 or x.size != b.size or not x.flags.c_contiguous:
+            raise ValueError("solve: out must be a contiguous f64 array of the rhs length")
         x0p = None
         if x0 is not None:
             x0a = np.ascontiguousarray(x0, np.float64)
+            if x0a.size != b.size:
+                raise ValueError("solve: x0 length mismatch")
             x0p = x0a.ctypes.data_as(C.c_void_p)
         rep = _native.Report()
         c = cfg._c()
@@ -436,9 +460,9 @@ class Context:
         return self._report(rep, _PCG_METHOD[kind])
 
     def psdo_solve_device(self, b_ptr: int, x_ptr: int, cfg: SolveConfig, x0_ptr: int | None = None,
-                          method: str = "psdo+neural") -> SolveReport:
+                          method: str = "psdo+neural", precond: str = "neural") -> SolveReport:
         rep = _native.Report()
-        c = cfg._c()
+        c = cfg._c(_PSDO_PRECOND[precond])
         self._ck(self.lib.npsd_b200_psdo_solve_device(self.h, C.c_void_p(b_ptr),
                                                       C.c_void_p(x0_ptr) if x0_ptr else None, C.byref(c),
                                                       C.c_void_p(x_ptr), C.byref(rep)))
@@ -526,6 +550,9 @@ class PinnedBuffer:
 
 
 # -------------------------------------------------------- preconditioner API
+_PSDO_PRECOND = {"neural": 0, "identity": 1, "none": 1, "jacobi": 2}
+
+
 class NeuralPrecond:
     """net::NeuralPrecond (net/precond.hpp:14-30) on a B200.
 
@@ -569,6 +596,43 @@ class NeuralPrecond:
         return "neural"
 
 
+class IdentityPrecond:
+    """IdentityPrecond (precond.hpp:35-43, precond.cpp:7-10) for the B200
+    psdo_solve: apply copies (z = r) like the reference; inside psdo_solve the
+    device loop forms d = r / ||r|| without the network. The image (cell
+    types) gives the device its matrix-free operator."""
+
+    def __init__(self, image: np.ndarray, device: int = 0):
+        image = np.asarray(image)
+        dim = 3 if image.ndim == 3 else 2
+        depth = 1  # the network is never run; the smallest context
+        self.ctx = Context(dim, image.shape, identity_params(depth, dim), device)
+        self.ctx.set_mask(image)
+
+    def apply(self, r: np.ndarray, z: np.ndarray | None = None) -> np.ndarray:
+        r = np.asarray(r, np.float64)
+        if r.size != self.size():
+            raise ValueError("IdentityPrecond::apply: size mismatch")
+        if z is not None:
+            z[...] = r
+            return z
+        return r.copy()
+
+    __call__ = apply
+
+    def is_linear(self) -> bool:
+        return True
+
+    def is_symmetric(self) -> bool:
+        return True
+
+    def size(self) -> int:
+        return self.ctx.n_fluid
+
+    def name(self) -> str:
+        return "identity"
+
+
 def neural_precond(params: NetParams, image: np.ndarray, map: np.ndarray | None = None) -> NeuralPrecond:
     """net/precond.hpp:32-33."""
     return NeuralPrecond(params, image, map)
@@ -584,29 +648,46 @@ def _rows(A) -> int | None:
     return None
 
 
-def psdo_solve(A, b: np.ndarray, P: NeuralPrecond, cfg: SolveConfig | None = None,
-               x0: np.ndarray | None = None) -> SolveResult:
+def _csr(A):
+    """(row_offsets, col_indices, values) of a reduced CSR matrix: the
+    reference's SparseMatrix fields or scipy.sparse's indptr/indices/data."""
+    for names in (("row_offsets", "col_indices", "values"), ("indptr", "indices", "data")):
+        if all(hasattr(A, n) for n in names):
+            return tuple(np.asarray(getattr(A, n)) for n in names)
+    return None
+
+
+def psdo_solve(A, b: np.ndarray, P, cfg: SolveConfig | None = None, x0: np.ndarray | None = None,
+               check_a: str = "rows") -> SolveResult:
     """psdo_solve (solver.hpp:64-65, solver.cpp:189-276) on the B200.
 
-    The operator is matrix-free: it is the mixed-BC Laplacian that
-    assemble_poisson[_3d] + reduce would build from P's image, so ``A`` is only
-    checked for its size (pass None to skip). P must be a B200 NeuralPrecond.
+    The operator is matrix-free: the mixed-BC Laplacian that
+    assemble_poisson[_3d] + reduce build from P's image. A CSR ``A``
+    (row_offsets/col_indices/values, or scipy indptr/indices/data) is checked
+    against it — ``check_a`` "rows": every row's nnz, diagonal and -1
+    off-diagonals; "full": also A v bitwise against the device operator — and a
+    different A raises ValueError instead of solving another system. ``A`` =
+    None skips the check. P is a B200 NeuralPrecond or IdentityPrecond; there
+    is no CPU path.
     """
     cfg = cfg or SolveConfig()
-    if not isinstance(P, NeuralPrecond):
-        raise ValueError("psdo_solve (B200): P must be a B200 NeuralPrecond; there is no CPU path")
+    if not isinstance(P, (NeuralPrecond, IdentityPrecond)):
+        raise ValueError("psdo_solve (B200): P must be a B200 NeuralPrecond or IdentityPrecond; there is no CPU path")
     n = _rows(A)
     if n is not None and n != P.size():
         raise ValueError("solve: matrix not square / rhs length mismatch")
+    csr = _csr(A) if A is not None else None
+    if csr is not None:
+        P.ctx.check_operator(*csr, full=(check_a == "full"))
     b = np.asarray(b, np.float64)
     if b.size != P.size():
         raise ValueError("solve: rhs length mismatch")
     if not np.all(np.isfinite(b)):
         raise ValueError("solve: rhs has non-finite entries")
-    return P.ctx.psdo_solve(b, cfg, x0, method="psdo+" + P.name())
+    return P.ctx.psdo_solve(b, cfg, x0, method="psdo+" + P.name(), precond=P.name())
 
 
-def psd_solve(A, b: np.ndarray, P: NeuralPrecond, cfg: SolveConfig | None = None,
+def psd_solve(A, b: np.ndarray, P, cfg: SolveConfig | None = None,
               x0: np.ndarray | None = None) -> SolveResult:
     """PSDO with n_ortho forced to 0 (solver.hpp:68-69)."""
     cfg = SolveConfig(**{**(cfg or SolveConfig()).__dict__, "n_ortho": 0})

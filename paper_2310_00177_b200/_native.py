@@ -26,14 +26,14 @@ EXPORTED_SYMBOLS = (
     "npsd_b200_nccl_unique_id", "npsd_b200_comm_create_nccl", "npsd_b200_comm_create_local",
     "npsd_b200_comm_destroy", "npsd_b200_comm_last_error", "npsd_b200_create_slab", "npsd_b200_slab_graph",
     "npsd_b200_mac_divergence_rhs", "npsd_b200_mac_divergence_rhs_device", "npsd_b200_pcg_solve",
-    "npsd_b200_pcg_solve_device", "npsd_b200_ic0_apply",
+    "npsd_b200_pcg_solve_device", "npsd_b200_ic0_apply", "npsd_b200_is_pure_neumann", "npsd_b200_check_operator",
 )
 
 
 class SolveCfg(C.Structure):
     _fields_ = [("tol_reduction", C.c_double), ("tol_abs", C.c_double), ("max_iters", C.c_int64),
                 ("n_ortho", C.c_int32), ("nullspace_projection", C.c_int32),
-                ("normalize_before_precond", C.c_int32), ("reserved", C.c_int32)]
+                ("normalize_before_precond", C.c_int32), ("precond", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -91,6 +91,8 @@ def lib() -> C.CDLL:
     L.npsd_b200_n_fluid.restype = C.c_int64
     L.npsd_b200_n_fluid.argtypes = [_vp]
     L.npsd_b200_fluid_indices.argtypes = [_vp, _i64p]
+    L.npsd_b200_is_pure_neumann.argtypes = [_vp, C.POINTER(C.c_int)]
+    L.npsd_b200_check_operator.argtypes = [_vp, C.c_int64, _i64p, _i64p, _f64p, C.c_int64, C.c_int]
     L.npsd_b200_precond_apply.argtypes = [_vp, _f64p, _f64p, C.c_int64]
     L.npsd_b200_psdo_solve.argtypes = [_vp, _f64p, _vp, C.POINTER(SolveCfg), _f64p, C.POINTER(Report)]
     L.npsd_b200_psdo_solve_device.argtypes = [_vp, _vp, _vp, C.POINTER(SolveCfg), _vp, C.POINTER(Report)]

@@ -9,10 +9,11 @@ rows, bins 0 .. 64 and overflow) with the reference's column order and number
 formats, so the reference's own `load_bench_rows` reads them.
 
 Device methods: `cg`, `pcg+none|jacobi|ic0` (cg.cuh; IC0 by level-scheduled
-triangular sweeps), `psd+neural|none`, `psdo+neural|none` (the network solve;
-`none` = identity-equivalent weights, the network's form of IdentityPrecond).
-`fpcg` and the classical preconditioners under psd/psdo are not on the device
-path; their rows carry an error, like the reference's rows for failed methods.
+triangular sweeps), `psd|psdo+neural|none|jacobi` (the device PSDO loop with
+the network, IdentityPrecond or JacobiPrecond). Every solve sets
+nullspace_projection = is_pure_neumann(frame) like bench.cpp:52. `fpcg` and
+IC0 under psd/psdo are not on the device path; their rows carry an error, like
+the reference's rows for failed methods.
 
     python -m paper_2310_00177_b200.bench_matrix out_dir [--systems C1,C2,C3] [--methods cg,pcg+jacobi,psdo+neural]
 """
@@ -72,13 +73,15 @@ def run_one(ctx_for, system: str, types: np.ndarray, b: np.ndarray, token: str, 
         t0 = time.perf_counter()
         ctx.set_mask(types)
         setup = time.perf_counter() - t0
-        scfg = b200.SolveConfig(tol_reduction=cfg.tol_reduction, max_iters=cfg.max_iters, n_ortho=cfg.n_ortho)
-        if solver in ("cg", "pcg"):
+        ns = ctx.is_pure_neumann()  # bench.cpp:52
+        scfg = b200.SolveConfig(tol_reduction=cfg.tol_reduction, max_iters=cfg.max_iters,
+                                n_ortho=0 if solver == "psd" else cfg.n_ortho, nullspace_projection=ns)
+        if solver == "cg":
+            res = ctx.pcg_solve(b, scfg, precond="identity")
+        elif solver == "pcg":
             res = ctx.pcg_solve(b, scfg, precond=precond if precond in ("jacobi", "ic0") else "identity")
         else:
-            if solver == "psd":
-                scfg = b200.SolveConfig(tol_reduction=cfg.tol_reduction, max_iters=cfg.max_iters, n_ortho=0)
-            res = ctx.psdo_solve(b, scfg)
+            res = ctx.psdo_solve(b, scfg, precond=precond)
         rep = res.report
         row.iterations, row.converged = rep.iterations, rep.converged
         row.setup_seconds = setup + rep.setup_seconds

@@ -88,7 +88,10 @@ __device__ __forceinline__ double cg_precond(double r, uint8_t b) {
 // INIT, of the prologue: r0 is r, history[0], threshold, beta = -0.0).
 // MODE kCgIc0: z needs the triangular sweeps that follow, so this kernel only
 // updates x, r, ||r|| and the convergence state; k_cg_rz finishes.
-template <int MODE, bool INIT>
+// PH: 0 the whole step; with nullspace projection (pcg_solve :82) the step
+// splits around mean_project(r): 1 = the two axpys only, 2 = the rest on the
+// projected r.
+template <int MODE, bool INIT, int PH = 0>
 __global__ void __launch_bounds__(kBlock) k_cg_update(Geom g, const uint8_t* __restrict__ cls,
                                                       const double* __restrict__ P0, const double* __restrict__ P1,
                                                       const double* __restrict__ Ap, double* __restrict__ x,
@@ -107,11 +110,12 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(Geom g, const uint8_t* __r
         const uint8_t b = cls[c];
         if (cls_type(b) != 0) continue;
         double rv = r[c];
-        if (!INIT) {
+        if (!INIT && PH != 2) {
             x[c] = __dadd_rn(x[c], __dmul_rn(alpha, p[c]));     // axpy_inplace(alpha, p, x)
             rv = __dadd_rn(rv, __dmul_rn(-alpha, Ap[c]));       // axpy_inplace(-alpha, Ap, r)
             r[c] = rv;
         }
+        if (PH == 1) continue;
         acc[0] += rv * rv;
         if (MODE != kCgIc0) {
             const double zv = cg_precond<MODE == kCgJacobi>(rv, b);
@@ -119,15 +123,18 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(Geom g, const uint8_t* __r
             acc[1] += rv * zv;
         }
     }
+    if (PH == 1) return;
     double tot[2];
     if (grid_reduce<2>(acc, partials, counter, tot) && threadIdx.x == 0) {
         const double rn = sqrt(tot[0]);
         st->rnorm = rn;
         const unsigned long long now = globaltimer();
+        st->t_mark = now;
         if (INIT) {
-            st->t0 = now;
+            const double setup = (double)(now - st->t0) * 1e-9;  // solver.cpp:57-58
+            st->setup_s = setup;
             hist[0] = rn;
-            times[0] = 0.0;
+            times[0] = setup;
             double thr = st->tol_reduction * rn;
             if (st->tol_abs > 0.0) thr = fmax(thr, st->tol_abs);
             st->thr = thr;
@@ -247,6 +254,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_rz(Geom g, const uint8_t* __restr
         if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cond, use_cond, 0u);
         return;
     }
+    precond_span_end(st);  // the IC0 sweeps since k_cg_update (solver.cpp:66-70, 94-96)
     double acc[1] = {0.0};
     FOR_OWNED(g, c) {
         if (cls_type(cls[c]) != 0) continue;

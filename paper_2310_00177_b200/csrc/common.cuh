@@ -109,7 +109,9 @@ struct SolverState {
     double rz, beta;                // pcg: r.z and the direction update's beta (cg.cuh)
     int pcur;                       // pcg: which p buffer holds the current direction
     double bad_value;               // curvature at breakdown
-    unsigned long long t0;          // %globaltimer at solve start
+    unsigned long long t0;          // %globaltimer at solve start (k_stamp_start)
+    unsigned long long t_mark;      // %globaltimer at the end of the last iteration (precond span start)
+    double setup_s, precond_s;      // SolveReport setup_seconds / precond_seconds (solver.cpp:211,237)
     double part[kPart];             // z-slab: this rank's totals at a reduction point
     int dist;                       // z-slab: reductions stop at part[], k_finalize finishes them;
                                     // iteration kernels return at once when done (chunked loop)

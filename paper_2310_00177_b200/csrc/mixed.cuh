@@ -147,6 +147,47 @@ __device__ __forceinline__ void fin_projections(SolverState* st, const double* d
     }
 }
 
+// IdentityPrecond (precond.cpp:7-10) in the device loop: d = r / ||r|| as
+// psdo_solve forms it (scale_inplace(1/||r||), solver.cpp:230-233; d = r
+// without normalize_before_precond), then the dots d.Ad_j and the MGS
+// projections, like the network's last kernel. JAC: JacobiPrecond
+// (precond.cpp:12-26), d = (r / ||r||) * (1 / A_ii).
+template <int NO, bool JAC>
+__global__ void __launch_bounds__(kBlock) k_ident_dir(Geom g, const uint8_t* __restrict__ cls,
+                                                      const double* __restrict__ r, double* __restrict__ dout,
+                                                      SolverState* st, const double* __restrict__ ADring,
+                                                      double* __restrict__ partials, unsigned int* __restrict__ counter) {
+    constexpr int NA = (NO > 0) ? NO : 1;
+    if (st->dist && st->done) return;
+    const bool scale = st->normalize != 0;
+    const double inv = st->inv1;
+    const int nc = st->n_cache, R = st->ring;
+    const double* adp[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) adp[j] = ADring + (long long)((st->head - (nc - 1) + j + 2 * R) % R) * g.n;
+    double acc[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+    FOR_OWNED(g, c) {
+        const uint8_t b = cls[c];
+        if (cls_type(b) != 0) continue;
+        double dv = scale ? __dmul_rn(r[c], inv) : r[c];
+        if (JAC) dv = __dmul_rn(dv, 1.0 / (double)cls_diag(b));
+        dout[c] = dv;
+#pragma unroll
+        for (int j = 0; j < NO; ++j)
+            if (j < nc) acc[j] += dv * __ldg(adp[j] + c);
+    }
+    double tot[NA];
+    if (grid_reduce<NA>(acc, partials, counter, tot) && threadIdx.x == 0) {
+        if (st->dist) {
+            for (int j = 0; j < kMaxOrtho; ++j) st->part[j] = (j < nc && j < NO) ? tot[j] : 0.0;
+        } else {
+            fin_projections(st, tot);
+        }
+    }
+}
+
 template <int D, int NO>
 #ifndef MIXUP_MINB
 #define MIXUP_MINB 4  // register cap for 4 blocks/SM (measured 26 -> 24 us)

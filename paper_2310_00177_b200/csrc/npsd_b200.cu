@@ -253,7 +253,7 @@ struct npsd_b200_ctx {
     SlabInfo slab;                // z-slab decomposition (single domain: off)
     Geom gglob[kMaxDepth] = {};   // the full grid per level (z-slab: all ranks)
     cudaGraphExec_t slab_exec = nullptr;  // z-slab: a chunk of iterations (NCCL ranks)
-    int slab_exec_no = -1, slab_exec_k0 = -1;
+    int slab_exec_no = -1, slab_exec_k0 = -1, slab_exec_ns = 0, slab_exec_ident = 0;
     bool slab_no_graph = false;   // the chunk graph could not be captured: eager chunks
     // programmatic dependent launch of the iteration kernels: measured neutral
     // in the solve graph (C3 256^3: 386.0 vs 384.8 ms), so opt-in (NPSD_PDL=1)
@@ -320,6 +320,7 @@ struct npsd_b200_ctx {
     double *cgP0 = nullptr, *cgP1 = nullptr, *cgAp = nullptr, *cgZ = nullptr;
     cudaGraphExec_t cg_exec = nullptr;
     int cg_exec_kind = -1;
+    int cg_exec_ns = 0;
     unsigned cg_exec_gen = 0;
     const void* cg_exec_key = nullptr;
     unsigned buf_gen = 0;                       // bumped when a buffer a captured graph uses moves
@@ -331,7 +332,8 @@ struct npsd_b200_ctx {
     // solve graph
     cudaGraphExec_t exec = nullptr;
     const void* exec_key[4] = {nullptr, nullptr, nullptr, nullptr};
-    int exec_nullspace = -1, exec_no = -1;
+    int exec_nullspace = -1, exec_no = -1, exec_ident = -1;
+    int solve_ident = 0;  // the solve's preconditioner: 0 network, 1 IdentityPrecond (cfg->precond)
     int body_launches = 0, prologue_launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t user_ev[16] = {};
@@ -775,6 +777,7 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         const uint32_t* ncells = (l == 0) ? c->npat0 : L.mcnt;
         long long rows_cap = (l == 0) ? (long long)n_mixed0 : L.g.n;
         if (l > 0) {
+            const uint32_t* kid_before = L.kid;
             L.kid = nullptr;
             if (n_mixed[l] > 0 && coarse_dictionary<D>(c, l, n_mixed[l])) {
                 L.kid = L.pid;
@@ -782,6 +785,7 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
                 ncells = c->cnpat;
                 rows_cap = n_mixed[l];
             }
+            if (L.kid != kid_before) ++c->buf_gen;  // captured graphs hold kid by value (ConvTab)
             LAUNCH(c, s, k_row_codes, L.g.n, L.g, L.cls, L.mmask, L.mbase, L.kid, L.rcode);
         }
         if (l < c->depth - 1) {
@@ -1170,11 +1174,40 @@ void launch_network(npsd_b200_ctx* c, cudaStream_t s, bool raw, int* launches) {
     if (launches) *launches = (int)steps.size();
 }
 
+// d = P(r / ||r||): the network, IdentityPrecond (cfg precond = 1) or
+// JacobiPrecond (2)
+template <int D>
+std::vector<Step> direction_steps(npsd_b200_ctx* c, int no) {
+    if (!c->solve_ident) return network_steps<D>(c, false, no);
+    const Geom g = c->g0;
+    const bool jac = c->solve_ident == 2;
+    return {{jac ? "jacobi_dir" : "ident_dir", [c, g, no, jac](cudaStream_t s) {
+                 const uint8_t* cls = c->L[0].cls;
+#define NPSD_IDENT(NO_)                                                                                        \
+    if (jac)                                                                                                    \
+        LAUNCH(c, s, (k_ident_dir<NO_, true>), g.n, g, cls, (const double*)c->R, c->Dtmp, c->st,               \
+               (const double*)c->ADring, c->partials, c->counter);                                             \
+    else                                                                                                        \
+        LAUNCH(c, s, (k_ident_dir<NO_, false>), g.n, g, cls, (const double*)c->R, c->Dtmp, c->st,              \
+               (const double*)c->ADring, c->partials, c->counter)
+                 switch (no) {
+                     case 0: NPSD_IDENT(0); break;
+                     case 1: NPSD_IDENT(1); break;
+                     case 2: NPSD_IDENT(2); break;
+                     case 3: NPSD_IDENT(3); break;
+                     case 4: NPSD_IDENT(4); break;
+                     default: NPSD_IDENT(8); break;
+                 }
+#undef NPSD_IDENT
+             }}};
+}
+
 template <int D>
 std::vector<Step> prologue_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h, int use_cond, int nullspace) {
     std::vector<Step> v;
     const Geom g = c->g0;
     const uint8_t* cls = c->L[0].cls;
+    v.push_back({"stamp", [=](cudaStream_t s) { LAUNCH3(c, s, k_stamp_start, dim3(1), dim3(1), c->st); }});
     // projections (solver.cpp:197-201), r0 = b - A x0, ||r0||
     if (nullspace) {
         v.push_back({"proj_b_sum", [=](cudaStream_t s) {
@@ -1202,7 +1235,7 @@ std::vector<Step> prologue_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h,
 
 template <int D>
 std::vector<Step> body_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h, int use_cond, int nullspace, int no) {
-    std::vector<Step> v = network_steps<D>(c, false, no);
+    std::vector<Step> v = direction_steps<D>(c, no);
     const Geom g = c->g0;
     const uint8_t* cls = c->L[0].cls;
     v.push_back({"ortho", [=](cudaStream_t s) { launch_ortho_no<D>(c, s, no); }});
@@ -1293,11 +1326,14 @@ void capture_solve_graph(npsd_b200_ctx* c, int nullspace, int no) {
     c->exec_key[3] = c->partials;
     c->exec_nullspace = nullspace;
     c->exec_no = no;
+    c->exec_ident = c->solve_ident;
     c->exec_gen = c->buf_gen;
     c->body_launches = (int)bod.size();
     c->prologue_launches = (int)pro.size();
     c->launches -= (long long)(bod.size() + pro.size());  // captured, not executed
 }
+
+long long first_zero_diag_row(npsd_b200_ctx* c);
 
 // Runs the solve on c->Bf / c->X0 (already masked). Returns the status.
 template <int D>
@@ -1306,6 +1342,12 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
     require(cfg->tol_reduction > 0.0 && cfg->tol_reduction < 1.0, "SolveConfig: tol_reduction must lie in (0,1)");
     require(cfg->n_ortho >= 0, "psdo: n_ortho must be >= 0");
     require(cfg->n_ortho <= kMaxOrtho, "psdo: n_ortho > 8 is not supported by the B200 build");
+    require(cfg->precond >= 0 && cfg->precond <= 2, "psdo: precond must be 0 (network), 1 (identity) or 2 (jacobi)");
+    if (cfg->precond == 2) {
+        const long long row = first_zero_diag_row(c);  // JacobiPrecond's constructor check
+        require(row < 0, "jacobi precond: zero diagonal at row " + std::to_string(row));
+    }
+    c->solve_ident = cfg->precond;
     const long long max_iters = cfg->max_iters < 0 ? 0 : cfg->max_iters;
     const int ring = cfg->n_ortho + 1;
     ensure_ring(c, ring);
@@ -1313,7 +1355,7 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
     const int nullspace = cfg->nullspace_projection ? 1 : 0;
     if (!c->exec || c->exec_gen != c->buf_gen || c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist ||
         c->exec_key[2] != c->ADring ||
-        c->exec_nullspace != nullspace || c->exec_no != cfg->n_ortho)
+        c->exec_nullspace != nullspace || c->exec_no != cfg->n_ortho || c->exec_ident != c->solve_ident)
         capture_solve_graph<D>(c, nullspace, cfg->n_ortho);
     SolverState* h = c->st_host;
     std::memset(h, 0, sizeof(SolverState));
@@ -1351,9 +1393,9 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
         rep->residual_history = c->report_hist.data();
         rep->cumulative_seconds = c->report_times.data();
         rep->history_len = hl;
-        rep->setup_seconds = 0.0;
-        rep->iterate_seconds = c->last_ms * 1e-3;
-        rep->precond_seconds = 0.0;
+        rep->setup_seconds = h->setup_s;
+        rep->iterate_seconds = c->last_ms * 1e-3 - h->setup_s;  // solver.cpp:275
+        rep->precond_seconds = h->precond_s;
     }
     if (h->breakdown) {
         char buf[256];
@@ -1368,9 +1410,18 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
 // One iteration for iteration index k (1-based): the ring slot and the x
 // buffer an iteration writes follow from k (head and xcur advance once per
 // iteration), so a chunk of lcm(2, ring) * m iterations repeats exactly.
+// mean_project over all ranks (vector_ops.cpp:33-43): rank sums and counts,
+// rank-ordered totals, subtract
+void slab_project(npsd_b200_ctx* c, cudaStream_t s, double* v) {
+    const Geom g = c->g0;
+    LAUNCH(c, s, k_fluid_sum, g.n, g, c->L[0].cls, v, c->n_fluid, c->st, c->partials, c->counter);
+    slab_reduce(c, s, kFinMean);
+    LAUNCH(c, s, k_subtract_mean, g.n, g, c->L[0].cls, v, c->st);
+}
+
 template <int D>
-std::vector<Step> slab_body_steps(npsd_b200_ctx* c, int no, long long k) {
-    std::vector<Step> v = network_steps<D>(c, false, no);
+std::vector<Step> slab_body_steps(npsd_b200_ctx* c, int no, long long k, int ns) {
+    std::vector<Step> v = direction_steps<D>(c, no);
     const int R = no + 1;
     const int nw = (int)((R - 1 + k) % R);
     double* dnew = c->Dring + (size_t)nw * (size_t)c->g0.n;
@@ -1380,7 +1431,17 @@ std::vector<Step> slab_body_steps(npsd_b200_ctx* c, int no, long long k) {
     v.push_back({"ortho", [c, no](cudaStream_t s) { launch_ortho_no<D>(c, s, no); }});
     v.push_back(reduce_step(c, "reduce_ortho", kFinOrtho));
     v.push_back(xchg_step(c, "xchg_dnew", [dnew] { return (void*)dnew; }, sizeof(double), 0));
-    v.push_back({"update", [c](cudaStream_t s) { launch_update<D>(c, s, 0, 0, 1); }});
+    if (ns) {  // r = b - A x', mean_project(r), ||r|| (solver.cpp:255-260)
+        v.push_back({"update", [c](cudaStream_t s) { launch_update<D>(c, s, 0, 0, 0); }});
+        v.push_back({"project_r", [c](cudaStream_t s) { slab_project(c, s, c->R); }});
+        v.push_back({"norm", [c](cudaStream_t s) {
+                         const Geom g = c->g0;
+                         LAUNCH(c, s, k_residual_norm, g.n, g, c->R, c->st, c->hist, c->times, c->partials,
+                                c->counter, (cudaGraphConditionalHandle)0, 0, 0);
+                     }});
+    } else {
+        v.push_back({"update", [c](cudaStream_t s) { launch_update<D>(c, s, 0, 0, 1); }});
+    }
     v.push_back(reduce_step(c, "reduce_update", kFinUpdate));
     v.push_back(xchg_step(c, "xchg_xnew", [xnew] { return (void*)xnew; }, sizeof(double), 0));
     v.push_back(xchg_step(c, "xchg_r", [c] { return (void*)c->R; }, sizeof(double), 0));
@@ -1401,7 +1462,8 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
     require(cfg->tol_reduction > 0.0 && cfg->tol_reduction < 1.0, "SolveConfig: tol_reduction must lie in (0,1)");
     require(cfg->n_ortho >= 0, "psdo: n_ortho must be >= 0");
     require(cfg->n_ortho <= kMaxOrtho, "psdo: n_ortho > 8 is not supported by the B200 build");
-    require(!cfg->nullspace_projection, "psdo: nullspace projection is not supported on a z-slab context");
+    require(cfg->precond == 0 || cfg->precond == 1, "psdo: precond must be 0 (network) or 1 (identity) on a z-slab");
+    c->solve_ident = cfg->precond;
     cudaStream_t s = c->s;
     const long long max_iters = cfg->max_iters < 0 ? 0 : cfg->max_iters;
     const int no = cfg->n_ortho, ring = no + 1;
@@ -1416,14 +1478,23 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
     h->normalize = cfg->normalize_before_precond ? 1 : 0;
     h->ring = ring;
     h->dist = 1;
+    const int ns = cfg->nullspace_projection ? 1 : 0;
+    h->nullspace = ns;
     CK(cudaMemcpyAsync(c->st, h, sizeof(SolverState), cudaMemcpyHostToDevice, s));
     ensure_x1_clean(c, s);
     const Geom g = c->g0;
     const uint8_t* cls = c->L[0].cls;
     CK(cudaEventRecord(c->ev0, s));
-    // prologue: r0 = b - A x0 (x0's ghosts first), ||r0|| over all ranks
+    LAUNCH3(c, s, k_stamp_start, dim3(1), dim3(1), c->st);
+    // prologue: [projections of b and x0], r0 = b - A x0 (x0's ghosts first),
+    // [projection of r0], ||r0|| over all ranks (solver.cpp:197-209)
+    if (ns) {
+        slab_project(c, s, c->Bf);
+        slab_project(c, s, c->X0);
+    }
     slab_exchange(c, s, c->X0, sizeof(double), 0);
     LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R);
+    if (ns) slab_project(c, s, c->R);
     LAUNCH(c, s, k_residual_norm, g.n, g, c->R, c->st, c->hist, c->times, c->partials, c->counter,
            (cudaGraphConditionalHandle)0, 0, 1);
     slab_reduce(c, s, kFinNorm0);
@@ -1431,6 +1502,7 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
     const int K = slab_chunk(ring);
     bool graph = c->slab.comm->capturable() && !c->slab_no_graph;
     if (graph && (!c->slab_exec || c->slab_exec_gen != c->buf_gen || c->slab_exec_no != no ||
+                  c->slab_exec_ns != ns || c->slab_exec_ident != cfg->precond ||
                   c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist ||
                   c->exec_key[2] != c->ADring)) {
         if (c->slab_exec) CK(cudaGraphExecDestroy(c->slab_exec));
@@ -1443,7 +1515,7 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
             const long long before = c->launches;
             try {
                 for (long long k = 1; k <= K; ++k)
-                    for (const auto& st : slab_body_steps<D>(c, no, k)) st.run(s);
+                    for (const auto& st : slab_body_steps<D>(c, no, k, ns)) st.run(s);
                 c->slab_chunk_launches = c->launches - before;  // kernels per chunk replay
                 c->launches = before;                            // captured, not executed
             } catch (...) {
@@ -1458,6 +1530,8 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
             cudaGraphDestroy(gr);
             CK(ie);
             c->slab_exec_no = no;
+            c->slab_exec_ns = ns;
+            c->slab_exec_ident = cfg->precond;
             c->slab_exec_gen = c->buf_gen;
             c->exec_key[0] = c->Dring;
             c->exec_key[1] = c->hist;
@@ -1478,7 +1552,7 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
             c->launches += c->slab_chunk_launches;
         } else {
             for (long long k = k0; k < k0 + K; ++k)
-                for (const auto& st : slab_body_steps<D>(c, no, k)) st.run(s);
+                for (const auto& st : slab_body_steps<D>(c, no, k, ns)) st.run(s);
         }
     }
     CK(cudaEventRecord(c->ev1, s));
@@ -1500,9 +1574,9 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
         rep->residual_history = c->report_hist.data();
         rep->cumulative_seconds = c->report_times.data();
         rep->history_len = hl;
-        rep->setup_seconds = 0.0;
-        rep->iterate_seconds = c->last_ms * 1e-3;
-        rep->precond_seconds = 0.0;
+        rep->setup_seconds = h->setup_s;
+        rep->iterate_seconds = c->last_ms * 1e-3 - h->setup_s;  // solver.cpp:275
+        rep->precond_seconds = h->precond_s;
     }
     if (h->breakdown) {
         char buf[256];
@@ -1588,7 +1662,7 @@ void ic0_factor(npsd_b200_ctx* c) {
 }
 
 template <int D, int M>
-void capture_cg_graph(npsd_b200_ctx* c) {
+void capture_cg_graph(npsd_b200_ctx* c, int ns) {
     constexpr bool J = (M == kCgJacobi);
     if (c->cg_exec) {
         CK(cudaGraphExecDestroy(c->cg_exec));
@@ -1607,8 +1681,20 @@ void capture_cg_graph(npsd_b200_ctx* c) {
     CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
     cudaGraphConditionalHandle h;
     CK(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
-    // prologue: r0 = b - A x0, z0 = M r0, ||r0||, r0.z0
+    // mean_project(v) (vector_ops.cpp:33-43) as two kernels
+    auto project = [&](cudaStream_t st, double* v) {
+        LAUNCH(c, st, k_fluid_sum, g.n, g, cls, v, c->n_fluid, c->st, c->partials, c->counter);
+        LAUNCH(c, st, k_subtract_mean, g.n, g, cls, v, c->st);
+    };
+    // prologue (solver.cpp:38-58): [projections of b, x0], r0 = b - A x0,
+    // [projection of r0], z0 = M r0, ||r0||, r0.z0
+    LAUNCH3(c, s, k_stamp_start, dim3(1), dim3(1), c->st);
+    if (ns) {
+        project(s, c->Bf);
+        project(s, c->X0);
+    }
     LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R);
+    if (ns) project(s, c->R);
     LAUNCH(c, s, (k_cg_update<M, true>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st, c->hist,
            c->times, c->partials, c->counter, h, M == kCgIc0 ? 0 : 1);
     if (M == kCgIc0) {
@@ -1633,8 +1719,16 @@ void capture_cg_graph(npsd_b200_ctx* c) {
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         LAUNCH3S(c, s2, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, g, cls, (const double*)z,
                  c->cgP0, c->cgP1, c->cgAp, c->st, c->partials, c->counter, c->sch_stencil.view());
-        LAUNCH(c, s2, (k_cg_update<M, false>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st,
-               c->hist, c->times, c->partials, c->counter, h, M == kCgIc0 ? 0 : 1);
+        if (ns) {  // x, r axpys; mean_project(r) (solver.cpp:82); the rest on the projected r
+            LAUNCH(c, s2, (k_cg_update<M, false, 1>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st,
+                   c->hist, c->times, c->partials, c->counter, h, M == kCgIc0 ? 0 : 1);
+            project(s2, c->R);
+            LAUNCH(c, s2, (k_cg_update<M, false, 2>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st,
+                   c->hist, c->times, c->partials, c->counter, h, M == kCgIc0 ? 0 : 1);
+        } else {
+            LAUNCH(c, s2, (k_cg_update<M, false>), g.n, g, cls, c->cgP0, c->cgP1, c->cgAp, c->X0, c->R, z, c->st,
+                   c->hist, c->times, c->partials, c->counter, h, M == kCgIc0 ? 0 : 1);
+        }
         if (M == kCgIc0) {
             ic0_sweep<1>(c, s2, 0.0, c->R, c->st);
             ic0_sweep<2>(c, s2, 0.0, c->R, c->st);
@@ -1648,6 +1742,7 @@ void capture_cg_graph(npsd_b200_ctx* c) {
     CK(cudaGraphInstantiate(&c->cg_exec, graph, 0));
     CK(cudaGraphDestroy(graph));
     c->launches = before;
+    c->cg_exec_ns = ns;
     c->cg_exec_kind = M;
     c->cg_exec_gen = c->buf_gen;
     c->cg_exec_key = c->hist;
@@ -1657,7 +1752,6 @@ void capture_cg_graph(npsd_b200_ctx* c) {
 int pcg_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, int precond, npsd_b200_report* rep) {
     require(cfg->tol_reduction > 0.0 && cfg->tol_reduction < 1.0, "SolveConfig: tol_reduction must lie in (0,1)");
     require(precond >= 0 && precond <= 2, "pcg: preconditioner must be 0 (identity), 1 (jacobi) or 2 (ic0)");
-    require(!cfg->nullspace_projection, "pcg: nullspace projection is not supported by the B200 build");
     require(!c->slab.on, "pcg: not available on a z-slab context");
     cudaStream_t s = c->s;
     const Geom g = c->g0;
@@ -1679,15 +1773,17 @@ int pcg_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, int precond
     ensure_hist(c, max_iters + 1);
     // the zero invariant of the directions, A p and z on this frame
     for (double* v : {c->cgP0, c->cgP1, c->cgAp, c->cgZ}) CK(cudaMemsetAsync(v, 0, nb, s));
-    if (!c->cg_exec || c->cg_exec_kind != precond || c->cg_exec_gen != c->buf_gen || c->cg_exec_key != c->hist) {
+    const int ns = cfg->nullspace_projection ? 1 : 0;
+    if (!c->cg_exec || c->cg_exec_kind != precond || c->cg_exec_gen != c->buf_gen || c->cg_exec_key != c->hist ||
+        c->cg_exec_ns != ns) {
         if (c->dim == 3) {
-            if (precond == 0) capture_cg_graph<3, kCgIdentity>(c);
-            else if (precond == 1) capture_cg_graph<3, kCgJacobi>(c);
-            else capture_cg_graph<3, kCgIc0>(c);
+            if (precond == 0) capture_cg_graph<3, kCgIdentity>(c, ns);
+            else if (precond == 1) capture_cg_graph<3, kCgJacobi>(c, ns);
+            else capture_cg_graph<3, kCgIc0>(c, ns);
         } else {
-            if (precond == 0) capture_cg_graph<2, kCgIdentity>(c);
-            else if (precond == 1) capture_cg_graph<2, kCgJacobi>(c);
-            else capture_cg_graph<2, kCgIc0>(c);
+            if (precond == 0) capture_cg_graph<2, kCgIdentity>(c, ns);
+            else if (precond == 1) capture_cg_graph<2, kCgJacobi>(c, ns);
+            else capture_cg_graph<2, kCgIc0>(c, ns);
         }
     }
     SolverState* h = c->st_host;
@@ -1711,7 +1807,7 @@ int pcg_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, int precond
     c->report_hist.assign(c->hist_host, c->hist_host + hl);
     c->report_times.assign(c->times_host, c->times_host + hl);
     const long long sweeps = (precond == 2) ? 2LL * ic0_levels(g) + 1 : 0;  // per preconditioner apply
-    c->last_launches = 2 + sweeps + (2 + sweeps) * iters;
+    c->last_launches = 3 + 6 * ns + sweeps + (2 + 3 * ns + sweeps) * iters;
     c->launches += c->last_launches;
     if (rep) {
         rep->iterations = iters;
@@ -1720,9 +1816,9 @@ int pcg_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, int precond
         rep->residual_history = c->report_hist.data();
         rep->cumulative_seconds = c->report_times.data();
         rep->history_len = hl;
-        rep->setup_seconds = 0.0;
-        rep->iterate_seconds = c->last_ms * 1e-3;
-        rep->precond_seconds = 0.0;
+        rep->setup_seconds = h->setup_s;
+        rep->iterate_seconds = c->last_ms * 1e-3 - h->setup_s;  // solver.cpp:275
+        rep->precond_seconds = h->precond_s;
     }
     if (h->breakdown) {
         char buf[256];
@@ -2260,6 +2356,28 @@ int npsd_b200_set_mask(npsd_b200_ctx* c, const uint8_t* types) {
     });
 }
 
+int npsd_b200_is_pure_neumann(npsd_b200_ctx* c, int* out) {
+    return guarded(c, [&] {
+        require(out != nullptr, "is_pure_neumann: out is NULL");
+        check_mask(c);
+        const Geom g = c->g0;
+        bool none = (c->dim == 3) ? device_check(c, k_touches_air<3>, g.n, g, (const uint8_t*)c->L[0].cls)
+                                  : device_check(c, k_touches_air<2>, g.n, g, (const uint8_t*)c->L[0].cls);
+        if (c->slab.on) {  // any rank's fluid touching air
+            unsigned long long* v = reinterpret_cast<unsigned long long*>(c->red_b);
+            const unsigned long long mine = none ? 0ull : 1ull;
+            CK(cudaMemcpyAsync(v, &mine, sizeof mine, cudaMemcpyHostToDevice, c->s));
+            slab_allreduce_u64(c, c->s, v, 1);
+            unsigned long long tot = 0;
+            CK(cudaMemcpyAsync(&tot, v, sizeof tot, cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            none = (tot == 0);
+        }
+        *out = none ? 1 : 0;
+        return NPSD_OK;
+    });
+}
+
 int64_t npsd_b200_n_fluid(const npsd_b200_ctx* c) { return (c && c->mask_ok) ? c->n_fluid : -1; }
 
 int npsd_b200_fluid_indices(npsd_b200_ctx* c, int64_t* out) {
@@ -2367,6 +2485,84 @@ int npsd_b200_spmv(npsd_b200_ctx* c, const double* x, double* y, int64_t n_f) {
         CK(cudaMemsetAsync(c->Dtmp, 0, (size_t)g.n * sizeof(double), c->s));
         CK(cudaMemsetAsync(c->R, 0, (size_t)g.n * sizeof(double), c->s));
         CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int npsd_b200_check_operator(npsd_b200_ctx* c, int64_t n_rows, const int64_t* row_offsets,
+                             const int64_t* col_indices, const double* values, int64_t nnz, int full) {
+    return guarded(c, [&] {
+        check_mask(c);
+        require(!c->slab.on, "check_operator: not available on a z-slab context");
+        require(n_rows == c->n_fluid, "solve: matrix rows (" + std::to_string(n_rows) + ") != fluid cells of the mask (" +
+                                          std::to_string(c->n_fluid) + ")");
+        require(row_offsets != nullptr && (nnz == 0 || (col_indices && values)), "check_operator: null CSR arrays");
+        require(row_offsets[0] == 0 && row_offsets[n_rows] == nnz, "check_operator: row_offsets do not span nnz");
+        if (n_rows == 0) return;
+        // the flag-derived rows (assemble_poisson[_3d] + reduce, discretization.cpp:21-160)
+        const Geom g = c->g0;
+        uint8_t* d_info = reinterpret_cast<uint8_t*>(c->red_b);
+        if (c->dim == 3)
+            LAUNCH(c, c->s, k_row_info<3>, g.n, g, c->L[0].cls, c->fmask, c->fbase, d_info);
+        else
+            LAUNCH(c, c->s, k_row_info<2>, g.n, g, c->L[0].cls, c->fmask, c->fbase, d_info);
+        std::vector<uint8_t> info((size_t)n_rows);
+        CK(cudaMemcpyAsync(info.data(), d_info, (size_t)n_rows, cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        // nnz, the diagonal and the off-diagonal values of every row
+        long long want_nnz = 0;
+        for (int64_t r = 0; r < n_rows; ++r) {
+            const int diag = info[(size_t)r] & 15, nf = info[(size_t)r] >> 4;
+            want_nnz += (diag != 0) + nf;
+            const int64_t a = row_offsets[r], e = row_offsets[r + 1];
+            require(e - a == (diag != 0) + nf, "solve: A is not the mixed-BC Laplacian of the mask (row " +
+                                                   std::to_string(r) + " has " + std::to_string(e - a) +
+                                                   " entries, the flags give " + std::to_string((diag != 0) + nf) + ")");
+            bool seen_diag = false;
+            for (int64_t k = a; k < e; ++k) {
+                const int64_t col = col_indices[k];
+                require(col >= 0 && col < n_rows, "solve: A column index out of range at row " + std::to_string(r));
+                if (col == r) {
+                    seen_diag = true;
+                    require(values[k] == (double)diag, "solve: A's diagonal differs from the flags at row " +
+                                                           std::to_string(r));
+                } else {
+                    require(values[k] == -1.0, "solve: A's off-diagonal entry differs from -1 at row " +
+                                                   std::to_string(r));
+                }
+            }
+            require(seen_diag == (diag != 0), "solve: A's diagonal pattern differs from the flags at row " +
+                                                  std::to_string(r));
+        }
+        require(want_nnz == nnz, "solve: A's nnz differs from the flag-derived operator");
+        if (!full) return;
+        // debug: the whole operator, A v (CSR order, spmv's serial row sums,
+        // sparse.cpp:100-117) against the device operator, bitwise
+        std::vector<double> v((size_t)n_rows), ya((size_t)n_rows), yd((size_t)n_rows);
+        unsigned long long st = 0x9e3779b97f4a7c15ull;
+        for (auto& x : v) {
+            st = st * 6364136223846793005ull + 1442695040888963407ull;
+            x = (double)(st >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+        }
+        for (int64_t r = 0; r < n_rows; ++r) {
+            double acc = 0.0;
+            for (int64_t k = row_offsets[r]; k < row_offsets[r + 1]; ++k) acc += values[k] * v[(size_t)col_indices[k]];
+            ya[(size_t)r] = acc;
+        }
+        CK(cudaMemcpyAsync(c->red_a, v.data(), (size_t)n_rows * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        LAUNCH(c, c->s, k_scatter, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->red_a, c->Dtmp);
+        if (c->dim == 3)
+            LAUNCH(c, c->s, k_spmv<3>, g.n, g, c->L[0].cls, c->Dtmp, c->R);
+        else
+            LAUNCH(c, c->s, k_spmv<2>, g.n, g, c->L[0].cls, c->Dtmp, c->R);
+        LAUNCH(c, c->s, k_gather, g.n, g, c->L[0].cls, c->fmask, c->fbase, c->R, c->red_b);
+        CK(cudaMemcpyAsync(yd.data(), c->red_b, (size_t)n_rows * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        CK(cudaMemsetAsync(c->Dtmp, 0, (size_t)g.n * sizeof(double), c->s));
+        CK(cudaMemsetAsync(c->R, 0, (size_t)g.n * sizeof(double), c->s));
+        CK(cudaStreamSynchronize(c->s));
+        for (int64_t r = 0; r < n_rows; ++r)
+            require(std::memcmp(&ya[(size_t)r], &yd[(size_t)r], sizeof(double)) == 0,
+                    "solve: A v differs from the flag-derived operator at row " + std::to_string(r));
     });
 }
 
@@ -2691,6 +2887,8 @@ int npsd_b200_profile_iterations(npsd_b200_ctx* c, const double* d_b, const npsd
         h->ring = ring;
         CK(cudaMemcpyAsync(c->st, h, sizeof(SolverState), cudaMemcpyHostToDevice, c->s));
         const int ns = cfg->nullspace_projection ? 1 : 0;
+        require(cfg->precond >= 0 && cfg->precond <= 2, "psdo: precond must be 0, 1 or 2");
+        c->solve_ident = cfg->precond;
         ensure_x1_clean(c, c->s);
         std::vector<Step> pro, bod;
         if (c->dim == 3) {

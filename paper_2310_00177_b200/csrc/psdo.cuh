@@ -139,6 +139,47 @@ __global__ void __launch_bounds__(kBlock) k_zero_diag(Geom g, const uint8_t* __r
     }
 }
 
+// is_pure_neumann (discretization.cpp:180-191), negated: flag |= 1 when a fluid
+// cell has an air face neighbour (outside the domain is solid; a z-slab's
+// ghost planes hold the neighbours' cells or that outside)
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_touches_air(Geom g, const uint8_t* __restrict__ cls,
+                                                        unsigned int* __restrict__ flag) {
+    bool hit = false;
+    const long long nx = g.nx, plane = nx * g.ny;
+    FOR_OWNED(g, c) {
+        if (cls_type(cls[c]) != 0) continue;
+        int x, y, z;
+        decode(g, c, x, y, z);
+        auto air = [&](long long q) { return cls_type(cls[q]) == 1; };
+        hit |= (x > 0 && air(c - 1)) || (x + 1 < g.nx && air(c + 1)) || (y > 0 && air(c - nx)) ||
+               (y + 1 < g.ny && air(c + nx));
+        if (D == 3) hit |= (z > 0 && air(c - plane)) || (z + 1 < g.nz && air(c + plane));
+    }
+    if (__syncthreads_or(hit) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+// the flag-derived reduced row of every fluid cell, for checking a caller's
+// CSR matrix against it: out[row] = diagonal (number of non-solid face
+// neighbours, 0 = dropped, discretization.cpp:115-118) | fluid neighbours << 4
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_row_info(Geom g, const uint8_t* __restrict__ cls,
+                                                     const uint32_t* __restrict__ fmask,
+                                                     const uint32_t* __restrict__ fbase, uint8_t* __restrict__ out) {
+    const long long nx = g.nx, plane = nx * g.ny;
+    FOR_OWNED(g, c) {
+        const uint8_t b = cls[c];
+        if (cls_type(b) != 0) continue;
+        int x, y, z;
+        decode(g, c, x, y, z);
+        auto fl = [&](long long q) { return cls_type(cls[q]) == 0 ? 1 : 0; };
+        int nf = (x > 0 ? fl(c - 1) : 0) + (x + 1 < g.nx ? fl(c + 1) : 0) + (y > 0 ? fl(c - nx) : 0) +
+                 (y + 1 < g.ny ? fl(c + nx) : 0);
+        if (D == 3) nf += (z > 0 ? fl(c - plane) : 0) + (z + 1 < g.nz ? fl(c + plane) : 0);
+        out[mixed_index(fmask, fbase, c)] = (uint8_t)(cls_diag(b) | (nf << 4));
+    }
+}
+
 // ---------------------------------------------------------------- operator
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_spmv(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ v,
@@ -207,16 +248,25 @@ __device__ __forceinline__ void set_precond_scales(SolverState* st) {
 __global__ void __launch_bounds__(kBlock) k_fluid_sum(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ v,
                                                       long long n_fluid, SolverState* st, double* __restrict__ partials,
                                                       unsigned int* __restrict__ counter) {
+    if (st->dist && st->done) return;  // chunked z-slab loop after convergence
     double acc[1] = {0.0};
     FOR_OWNED(g, c) acc[0] += v[c];
     double tot[1];
-    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0) st->mean = tot[0] / (double)n_fluid;
+    if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0) {
+        if (st->dist) {  // z-slab: this rank's sum and count; k_finalize(kFinMean) divides the totals
+            st->part[0] = tot[0];
+            st->part[1] = (double)n_fluid;
+        } else {
+            st->mean = tot[0] / (double)n_fluid;
+        }
+    }
 }
 
 // pass 2: v -= mean at fluid cells; FINAL_NORM also finishes the residual norm
 // (and the iteration bookkeeping) exactly like k_update's finaliser.
 __global__ void __launch_bounds__(kBlock) k_subtract_mean(Geom g, const uint8_t* __restrict__ cls, double* __restrict__ v,
                                                           const SolverState* __restrict__ st) {
+    if (st->dist && st->done) return;
     const double m = st->mean;
     FOR_OWNED(g, c)
         if (cls_type(cls[c]) == 0) v[c] = __dadd_rn(v[c], -m);
@@ -238,6 +288,22 @@ __global__ void __launch_bounds__(kBlock) k_residual(Geom g, const uint8_t* __re
     }
 }
 
+// first node of every solve: the %globaltimer origin of cumulative_seconds
+// (solver.cpp:192, t0 = Clock::now()); precond_seconds starts at zero
+__global__ void k_stamp_start(SolverState* st) {
+    st->t0 = globaltimer();
+    st->precond_s = 0.0;
+}
+
+// precond_seconds (solver.cpp:230-237): the network span of an iteration, from
+// the end of the previous iteration (t_mark, set by finish_iteration) to the
+// first kernel after the network; one thread of that kernel, after its
+// dependency wait
+__device__ __forceinline__ void precond_span_end(SolverState* st) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0 && !st->done)
+        st->precond_s += (double)(globaltimer() - st->t_mark) * 1e-9;
+}
+
 __device__ __forceinline__ void set_cond(cudaGraphConditionalHandle cond, int use_cond, unsigned v) {
     if (use_cond) cudaGraphSetConditional(cond, v);
 }
@@ -247,10 +313,13 @@ __device__ __forceinline__ void finish_iteration(SolverState* st, double rsq, do
     const double rn = sqrt(rsq);
     st->rnorm = rn;
     const unsigned long long now = globaltimer();
+    st->t_mark = now;
     if (initial) {
-        st->t0 = now;
+        // setup_seconds = r0 and its norm, from the solve's first kernel (solver.cpp:211-212)
+        const double setup = (double)(now - st->t0) * 1e-9;
+        st->setup_s = setup;
         hist[0] = rn;
-        times[0] = 0.0;
+        times[0] = setup;
         double thr = st->tol_reduction * rn;
         if (st->tol_abs > 0.0) thr = fmax(thr, st->tol_abs);
         st->thr = thr;
@@ -289,6 +358,7 @@ __global__ void __launch_bounds__(kBlock) k_residual_norm(Geom g, const double* 
         if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cond, use_cond, 0u);
         return;
     }
+    if (!initial && st->dist && st->done) return;
     double acc[1] = {0.0};
     FOR_OWNED(g, c) {
         const double v = r[c];

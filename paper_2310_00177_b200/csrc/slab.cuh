@@ -16,13 +16,13 @@
 
 namespace nb2 {
 
-enum FinKind { kFinNorm0 = 0, kFinNormPrecond = 1, kFinProj = 2, kFinOrtho = 3, kFinUpdate = 4 };
+enum FinKind { kFinNorm0 = 0, kFinNormPrecond = 1, kFinProj = 2, kFinOrtho = 3, kFinUpdate = 4, kFinMean = 5 };
 
 __global__ void k_finalize(int kind, SolverState* st, const double* __restrict__ all, int nranks,
                            double* __restrict__ hist, double* __restrict__ times) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     // iteration reductions after the solve finished (chunked loop): nothing to do
-    if ((kind == kFinProj || kind == kFinOrtho || kind == kFinUpdate) && st->done) return;
+    if ((kind == kFinProj || kind == kFinOrtho || kind == kFinUpdate || kind == kFinMean) && st->done) return;
     double tot[kPart];
     for (int j = 0; j < kPart; ++j) {
         double t = 0.0;
@@ -36,6 +36,7 @@ __global__ void k_finalize(int kind, SolverState* st, const double* __restrict__
         case kFinProj: fin_projections(st, tot); break;
         case kFinOrtho: fin_ortho(st, tot); break;
         case kFinUpdate: finish_iteration(st, tot[0], hist, times, none, 0, false); break;
+        case kFinMean: st->mean = tot[0] / tot[1]; break;  // mean_project over all ranks' fluid cells
         default: break;
     }
 }

@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(kSX* SY, SY == kSY ? ORTHO_MINB : 1) k_ortho2(
                                                      unsigned int* __restrict__ counter, Sched sc) {
     pdl_launch_wait();
     if (st->dist && st->done) return;
+    precond_span_end(st);
     const int nc = st->n_cache, R = st->ring;
     const int nw = (st->head + 1) % R;
     using Op = OrthoOp<NO>;

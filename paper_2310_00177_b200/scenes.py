@@ -81,6 +81,14 @@ def dam_break_pillars(n: int) -> np.ndarray:
     return _shell(t)
 
 
+DESCRIPTION = {
+    "C1": "closed box, fluid lower half",
+    "C2": "dam break with obstacle",
+    "C3": "droplet-in-pool",
+    "C4": "droplet-in-pool sequence",
+    "C5": "dam break with obstacle and four pillars",
+}
+
 CONFIGS = {
     "C1": (64, closed_box_half, 1234),
     "C2": (128, dam_break, 1235),

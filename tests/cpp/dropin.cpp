@@ -80,11 +80,69 @@ int main() {
     } catch (const std::invalid_argument&) {
         threw = true;
     }
+    // IdentityPrecond: the reference psdo_solve + its IdentityPrecond against the
+    // device loop with b200::IdentityPrecond (d = r / ||r||, no network)
+    IdentityPrecond id_ref(sys.A.n_rows);
+    b200::IdentityPrecond id_gpu(I);
+    const SolveResult ia = psdo_solve(sys.A, sys.b, id_ref, tts);
+    const SolveResult ib = b200::psdo_solve(sys.A, sys.b, id_gpu, tts);
+    double id_hist = 0.0;
+    const std::size_t nh = std::min(ia.report.residual_history.size(), ib.report.residual_history.size());
+    for (std::size_t i = 0; i < std::min<std::size_t>(nh, 30); ++i)
+        id_hist = std::max(id_hist, std::abs(ia.report.residual_history[i] - ib.report.residual_history[i]) /
+                                        ia.report.residual_history[i]);
+
+    // A is checked against the flags: a scaled or structurally different A throws
+    auto throws_invalid = [&](const SparseMatrix& M) {
+        try {
+            (void)b200::psdo_solve(M, sys.b, gpu_i, tts);
+        } catch (const std::invalid_argument&) {
+            return true;
+        }
+        return false;
+    };
+    SparseMatrix scaled = sys.A;
+    for (auto& v : scaled.values) v *= 2.0;
+    SparseMatrix moved = sys.A;  // one off-diagonal column index changed
+    for (index_t k = moved.row_offsets[5]; k < moved.row_offsets[6]; ++k)
+        if (moved.col_indices[static_cast<std::size_t>(k)] != 5) {
+            moved.col_indices[static_cast<std::size_t>(k)] = (moved.col_indices[static_cast<std::size_t>(k)] + 7) % moved.n_rows;
+            break;
+        }
+    const bool scaled_rejected = throws_invalid(scaled);
+    b200::operator_check() = b200::OperatorCheck::full;
+    const bool moved_rejected = throws_invalid(moved);
+    const SolveResult full = b200::psdo_solve(sys.A, sys.b, gpu_i, tts);  // the right A passes the full check
+    b200::operator_check() = b200::OperatorCheck::rows;
+
+    // is_pure_neumann (discretization.cpp:180-191): this frame, and a closed box
+    IndicatorImage box(16, 16, CellType::fluid);
+    for (index_t i = 0; i < 16; ++i) {
+        box.set_cell(i, 0, CellType::solid);
+        box.set_cell(i, 15, CellType::solid);
+        box.set_cell(0, i, CellType::solid);
+        box.set_cell(15, i, CellType::solid);
+    }
+    int pn_frame = -1, pn_box = -1;
+    b200::check(npsd_b200_is_pure_neumann(gpu_i.context(), &pn_frame), gpu_i.context());
+    b200::IdentityPrecond box_p(box);
+    b200::check(npsd_b200_is_pure_neumann(box_p.context(), &pn_box), box_p.context());
+
     std::printf(
         "{\"n_fluid\": %lld, \"precond_rel_l2\": %.3e, \"budget_hist_max_rel\": %.3e, \"ref_iters\": %lld, "
-        "\"b200_iters\": %lld, \"ref_converged\": %d, \"b200_converged\": %d, \"invalid_argument_rethrown\": %d}\n",
+        "\"b200_iters\": %lld, \"ref_converged\": %d, \"b200_converged\": %d, \"invalid_argument_rethrown\": %d, "
+        "\"ident_ref_iters\": %lld, \"ident_b200_iters\": %lld, \"ident_hist_max_rel\": %.3e, "
+        "\"scaled_a_rejected\": %d, \"moved_a_rejected\": %d, \"full_check_iters\": %lld, "
+        "\"setup_seconds\": %.3e, \"iterate_seconds\": %.3e, \"precond_seconds\": %.3e, \"cum0\": %.3e, "
+        "\"cum_last\": %.3e, \"pure_neumann_frame\": %d, \"pure_neumann_frame_ref\": %d, \"pure_neumann_box\": %d, "
+        "\"pure_neumann_box_ref\": %d}\n",
         static_cast<long long>(sys.A.n_rows), std::sqrt(num / den), hist_rel,
         static_cast<long long>(a.report.iterations), static_cast<long long>(b.report.iterations),
-        a.report.converged ? 1 : 0, b.report.converged ? 1 : 0, threw ? 1 : 0);
+        a.report.converged ? 1 : 0, b.report.converged ? 1 : 0, threw ? 1 : 0,
+        static_cast<long long>(ia.report.iterations), static_cast<long long>(ib.report.iterations), id_hist,
+        scaled_rejected ? 1 : 0, moved_rejected ? 1 : 0, static_cast<long long>(full.report.iterations),
+        b.report.setup_seconds, b.report.iterate_seconds, b.report.precond_seconds,
+        b.report.cumulative_seconds.front(), b.report.cumulative_seconds.back(), pn_frame,
+        is_pure_neumann(I) ? 1 : 0, pn_box, is_pure_neumann(box) ? 1 : 0);
     return 0;
 }

@@ -29,18 +29,30 @@ if trained:
     import paper_2310_00177_b200 as b200
 
     W = b200.load_npm(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm")
-for name in args or ["C1", "C2", "C3"]:
-    t, seed = scenes.config(name)
+
+def frames(name):
+    """(key suffix, types, seed) per solve: one for C1/C2/C3/C5, 32 for C4
+    (droplet frames at 128^3, RHS seed 2000+f)."""
+    if name == "C4":
+        for f, t in enumerate(scenes.droplet_frames(128, 32)):
+            yield f"_f{f:02d}", t, 2000 + f
+    else:
+        t, seed = scenes.config(name)
+        yield "", t, seed
+
+
+todo = [(name, suf, t, seed) for name in (args or ["C1", "C2", "C3"]) for suf, t, seed in frames(name)]
+for name, suf, t, seed in todo:
     b = ref.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
     t0 = time.time()
     if trained:
         r = ref.psdo_solve(t, b, mode="neural", params=W.flat, depth=W.depth, max_iters=20000, tol_reduction=1e-6,
                            n_ortho=2)
-        key, solver = f"{name}_trained", ("reference psdo_solve + NeuralPrecond3D (restatement) with "
+        key, solver = f"{name}{suf}_trained", ("reference psdo_solve + NeuralPrecond3D (restatement) with "
                                           "weights/npsd3d_L4.npm, n_ortho=2, tol 1e-6")
     else:
         r = ref.psdo_solve(t, b, mode="identity", max_iters=20000, tol_reduction=1e-6, n_ortho=2)
-        key, solver = name, "reference psdo_solve + IdentityPrecond, n_ortho=2, tol 1e-6"
+        key, solver = name + suf, "reference psdo_solve + IdentityPrecond, n_ortho=2, tol 1e-6"
     res[key] = {"n": int(t.shape[0]), "n_fluid": int(b.size), "iterations": r["iterations"],
                 "converged": r["converged"], "final_rel_res": float(r["residual_history"][-1] / r["residual_history"][0]),
                 "solver": solver, "cpu_seconds": time.time() - t0}

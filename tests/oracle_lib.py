@@ -236,7 +236,7 @@ class Ref:
         L.ref_save_npm_2d.argtypes = [C.c_int, C.c_ulonglong, C.c_char_p]
         L.ref_bench_roundtrip.argtypes = [C.c_char_p, C.c_char_p]
         L.ref_pcg_solve.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, C.c_int, _f64p, C.c_double, C.c_long,
-                                    _f64p, _f64p, C.POINTER(C.c_long), C.POINTER(C.c_int), C.POINTER(C.c_long)]
+                                    _f64p, _f64p, C.POINTER(C.c_long), C.POINTER(C.c_int), C.POINTER(C.c_long), C.c_int]
         L.ref_ic0_apply.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, _f64p, _f64p, C.POINTER(C.c_int)]
         L.ref_mac_rhs_2d.argtypes = [C.c_long, C.c_long, _u8p, _f64p, _f64p, C.c_double, C.c_double, C.c_double,
                                      C.c_void_p, C.c_void_p, _f64p]
@@ -266,13 +266,13 @@ class Ref:
         self._check(self.lib.ref_init_params_2d(depth, seed, out))
         return out
 
-    def pcg_solve(self, types, b, precond=0, tol_reduction=1e-6, max_iters=1000) -> dict:
+    def pcg_solve(self, types, b, precond=0, tol_reduction=1e-6, max_iters=1000, nullspace_projection=False) -> dict:
         dim, (nx, ny, nz) = _dims_of(types)
         b = np.ascontiguousarray(b, np.float64)
         x, hist = np.empty_like(b), np.zeros(max_iters + 1)
         it, conv, hl = C.c_long(), C.c_int(), C.c_long()
         self._check(self.lib.ref_pcg_solve(dim, nx, ny, nz, _u8(types), precond, b, tol_reduction, max_iters, x, hist,
-                                           C.byref(it), C.byref(conv), C.byref(hl)))
+                                           C.byref(it), C.byref(conv), C.byref(hl), int(nullspace_projection)))
         return {"x": x, "iterations": it.value, "converged": bool(conv.value), "residual_history": hist[:hl.value]}
 
     def ic0_apply(self, types, r) -> tuple[np.ndarray, int]:
@@ -370,6 +370,41 @@ class Ref:
         self._check(st)
         return {"x": x, "iterations": it.value, "converged": bool(conv.value),
                 "residual_history": hist[: hl.value].copy(), "setup_seconds": secs[0], "solve_seconds": secs[1]}
+
+
+def reduced_csr(types: np.ndarray):
+    """assemble_poisson_3d + reduce (discretization.cpp:75-160) restated in
+    numpy: rows in ascending fluid order, columns ascending (lower
+    neighbours, the diagonal when non-zero, upper neighbours), -1 per fluid
+    neighbour, diagonal = number of non-solid face neighbours (outside solid)."""
+    nz, ny, nx = types.shape
+    pad = np.full((nz + 2, ny + 2, nx + 2), 2, np.uint8)
+    pad[1:-1, 1:-1, 1:-1] = types
+    fl = types.reshape(-1) == 0
+    red = np.full(types.size, -1, np.int64)
+    red[fl] = np.arange(int(fl.sum()))
+    z, y, x = np.nonzero(types == 0)
+    offs = [(-1, 0, 0), (0, -1, 0), (0, 0, -1), (0, 0, 0), (0, 0, 1), (0, 1, 0), (1, 0, 0)]
+    diag = np.zeros(z.size, np.int64)
+    for dz, dy, dx in offs:
+        if (dz, dy, dx) != (0, 0, 0):
+            diag += pad[z + 1 + dz, y + 1 + dy, x + 1 + dx] != 2
+    cols, vals, valid = [], [], []
+    for dz, dy, dx in offs:
+        if (dz, dy, dx) == (0, 0, 0):
+            cols.append(red[(z * ny + y) * nx + x])
+            vals.append(diag.astype(np.float64))
+            valid.append(diag > 0)
+        else:
+            t = pad[z + 1 + dz, y + 1 + dy, x + 1 + dx]
+            ok = t == 0
+            q = ((z + dz) * ny + (y + dy)) * nx + (x + dx)
+            cols.append(np.where(ok, red[np.clip(q, 0, types.size - 1)], -1))
+            vals.append(np.full(z.size, -1.0))
+            valid.append(ok)
+    cols, vals, valid = np.stack(cols, 1), np.stack(vals, 1), np.stack(valid, 1)
+    ro = np.concatenate([[0], np.cumsum(valid.sum(1))]).astype(np.int64)
+    return ro, cols[valid].astype(np.int64), vals[valid]
 
 
 def have_ref() -> bool:

@@ -1,0 +1,82 @@
+"""Parity pinned at the benchmark configurations themselves,
+collected before the slower GPU tests:
+
+- the preconditioner output (NeuralPrecond::apply, net_precond.cpp:14-35)
+  against the CPU restatement at C2 128^3 and C3 256^3, with init_params
+  (seed 42) and with the committed trained weights: <= 1e-5 relative L2
+  (north_star), on the same seeded inputs;
+- iterations to rel-res 1e-6 with identity-equivalent weights against the
+  reference psdo_solve's counts (tests/golden/iteration_counts.json: C1 270,
+  C2 451, C3 936), +-1, through the network and through IdentityPrecond;
+- C4: all 32 frames of the 128^3 sequence through one context (per-frame
+  set_mask only), per-frame iterations with the trained weights against the
+  reference's per-frame counts (C4_fNN_trained), +-1.
+"""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2310_00177_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+COUNTS = json.loads((ROOT / "tests" / "golden" / "iteration_counts.json").read_text())
+WEIGHTS = ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm"
+REL_L2 = 1e-5
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("name,weights", [("C2", "seed42"), ("C2", "trained"), ("C3", "seed42"), ("C3", "trained")])
+def test_precond_apply_at_bench_config(b200, oracle, name, weights):
+    t, seed = scenes.config(name)
+    P = b200.load_npm(WEIGHTS) if weights == "trained" else b200.init_params(4, 42)
+    ctx = b200.Context(3, t.shape, P)
+    ctx.set_mask(t)
+    octx = oracle.context(t, P.flat, 4)
+    # the solve's own input: the benchmark RHS, and a rough residual-like vector
+    b = oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    r = np.random.default_rng(7).standard_normal(b.size) * 1e-3
+    for v in (b, r):
+        got, want = ctx.precond_apply(v), octx.precond_apply(v)
+        err = rel_l2(got, want)
+        assert err <= REL_L2, (name, weights, err)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("precond", ["network", "identity"])
+def test_identity_iteration_counts_at_bench_config(b200, name, precond):
+    want = COUNTS[name]["iterations"]
+    t, seed = scenes.config(name)
+    b = b200.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    cfg = b200.SolveConfig(max_iters=5000)
+    if precond == "network":
+        ctx = b200.Context(3, t.shape, b200.identity_params(4))
+        ctx.set_mask(t)
+        rep = ctx.psdo_solve(b, cfg).report
+    else:
+        P = b200.IdentityPrecond(t)
+        rep = b200.psdo_solve(None, b, P, cfg).report
+    assert rep.converged
+    assert abs(rep.iterations - want) <= 1, (name, precond, rep.iterations, want)
+
+
+def test_c4_sequence_per_frame_iterations(b200):
+    W = b200.load_npm(WEIGHTS)
+    n = 128
+    ctx = b200.Context(3, (n, n, n), W)
+    cfg = b200.SolveConfig(max_iters=2000)
+    got, want = [], []
+    for f, t in enumerate(scenes.droplet_frames(n, 32)):
+        ctx.set_mask(t)  # no re-setup: one context for the whole sequence
+        b = b200.rhs_normal(2000 + f, t.size)[t.reshape(-1) == 0]
+        rep = ctx.psdo_solve(b, cfg).report
+        assert rep.converged
+        got.append(rep.iterations)
+        want.append(COUNTS[f"C4_f{f:02d}_trained"]["iterations"])
+    diff = np.abs(np.array(got) - np.array(want))
+    assert diff.max() <= 1, list(zip(got, want))

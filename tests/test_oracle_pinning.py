@@ -214,3 +214,19 @@ def test_mac_rhs_2d_bitwise_vs_reference(oracle, ref, with_bc):
     got = oracle.mac_rhs(t, u, v, h=0.5, dt=0.01, rho=2.0, bc=bc)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
     assert np.all(got[t.reshape(-1) != 0] == 0.0)
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("name,n", [("C1", 16), ("C2", 16), ("C3", 24)])
+def test_reduced_csr_restatement_spmv_bitwise(ref, name, n):
+    """oracle_lib.reduced_csr (the numpy assemble_poisson_3d + reduce used by
+    the operator-check tests) reproduces the reference's reduced matrix: its
+    CSR-order row sums equal the reference spmv bit for bit."""
+    from oracle_lib import reduced_csr
+    from paper_2310_00177_b200 import scenes
+
+    t, _ = scenes.config(name, n)
+    ro, ci, va = reduced_csr(t)
+    x = np.random.default_rng(3).standard_normal(ro.size - 1)
+    y = np.array([sum((va[k] * x[ci[k]] for k in range(ro[r], ro[r + 1])), 0.0) for r in range(ro.size - 1)])
+    assert np.array_equal(y, ref.spmv(t, x))
