@@ -223,7 +223,7 @@ def reference_weights(kind: str, depth: int) -> np.ndarray:
     return Oracle().identity_params(3, depth)
 
 
-def cpu_reference_solve(types, seed, depth, cores, weights="trained", max_iters=20000):
+def cpu_reference_solve(types, seed, depth, cores, weights="trained", max_iters=20000, name=None):
     """One reference time-to-solution, measured (not extrapolated): the
     unmodified reference psdo_solve (solver.cpp:189-276) on its own
     assemble_poisson_3d + reduce (oracle/_ref), with the 3D network
@@ -245,7 +245,7 @@ def cpu_reference_solve(types, seed, depth, cores, weights="trained", max_iters=
     it = int(r["iterations"])
     return {
         "value": setup_ms + solve_ms, "unit": UNIT, "cores": cores, "kind": "reference",
-        "sample": (f"{types.shape[0]}^3 {args_config_name}, {weights} weights: one full reference solve to rel-res "
+        "sample": (f"{types.shape[0]}^3 {name or args_config_name}, {weights} weights: one full reference solve to rel-res "
                    f"1e-6 (measured, not extrapolated): setup {setup_ms:.0f} ms (assemble_poisson_3d + reduce + "
                    f"NeuralPrecond3D build) + {it} PSDO iterations {solve_ms:.0f} ms ({solve_ms / max(it, 1):.1f} "
                    f"ms/iter); {wall:.1f} s wall"),
@@ -416,7 +416,7 @@ def config_line(name: str, params, cfg, device: int, steps: int, warmup: int, cp
            "steps": steps, "warmup": warmup,
            "iteration_roofline": iteration_roofline(4, n_c, n_f, m["per_iter_ms"], load_peaks())}
     if cpu:
-        c = cpu_reference_solve(types, seed, 4, os.cpu_count() or 1, "trained")
+        c = cpu_reference_solve(types, seed, 4, os.cpu_count() or 1, "trained", name=name)
         out["cpu_baseline"] = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
     return out
 

@@ -96,6 +96,16 @@ int npsd_b200_create(int dim, int nx, int ny, int nz, int depth, const float* pa
 int npsd_b200_destroy(npsd_b200_ctx* ctx);
 const char* npsd_b200_last_error(const npsd_b200_ctx* ctx); /* ctx may be NULL (create errors) */
 
+/* Network arithmetic. exact = 0 (the default): fused multiply-adds, one
+ * accumulation chain per window plane, and the level-0 up convolution's taps
+ * merged per fine-cell parity (upsampling maps 27 fine taps onto 8 coarse
+ * cells) — the preconditioner output stays within the north_star tolerance
+ * (1e-5 relative L2 of the reference's) but is not bitwise. exact = 1: every
+ * network operation in the reference's order with round-to-nearest
+ * multiplies and adds (apply_kernels, net/kernels.hpp:147-172): outputs
+ * bit-identical to the CPU restatement. The solver (f64) is the same in both. */
+int npsd_b200_set_exact(npsd_b200_ctx* ctx, int exact);
+
 /* Replace the weights (same dim/depth); the next set_mask rebuilds tables. */
 int npsd_b200_set_params(npsd_b200_ctx* ctx, const float* params, size_t n_params);
 

@@ -222,7 +222,7 @@ _PCG_METHOD = {0: "cg", 1: "pcg+jacobi", 2: "pcg+ic0"}
 class Context:
     """One B200 context: grid, weights and (after set_mask) one frame."""
 
-    def __init__(self, dim: int, shape: tuple, params: NetParams, device: int = 0) -> None:
+    def __init__(self, dim: int, shape: tuple, params: NetParams, device: int = 0, exact: bool = False) -> None:
         if dim == 3:
             nz, ny, nx = shape
         else:
@@ -241,6 +241,8 @@ class Context:
         if st != NPSD_OK:
             _raise(st, self.lib.npsd_b200_last_error(None).decode())
         self.h = h
+        if exact:
+            self.set_exact(True)
 
     @classmethod
     def slab(cls, comm: Comm, rank: int, shape: tuple, z0: int, nz_own: int, params: NetParams,
@@ -313,6 +315,13 @@ class Context:
     def set_params(self, params: NetParams) -> None:
         flat = np.ascontiguousarray(params.flat, np.float32)
         self._ck(self.lib.npsd_b200_set_params(self.h, flat, flat.size))
+
+    def set_exact(self, exact: bool = True) -> None:
+        """Network arithmetic (npsd_b200_set_exact): exact=True runs every
+        network operation in the reference's order (bit-identical to the
+        restatement); False (the default) is the fast fused form, within the
+        north_star tolerance."""
+        self._ck(self.lib.npsd_b200_set_exact(self.h, int(bool(exact))))
 
     def set_mask(self, types: np.ndarray) -> None:
         t = np.ascontiguousarray(types, np.uint8).reshape(-1)

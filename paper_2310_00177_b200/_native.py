@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = (
     "npsd_b200_comm_destroy", "npsd_b200_comm_last_error", "npsd_b200_create_slab", "npsd_b200_slab_graph",
     "npsd_b200_mac_divergence_rhs", "npsd_b200_mac_divergence_rhs_device", "npsd_b200_pcg_solve",
     "npsd_b200_pcg_solve_device", "npsd_b200_ic0_apply", "npsd_b200_is_pure_neumann", "npsd_b200_check_operator",
+    "npsd_b200_set_exact",
 )
 
 
@@ -91,6 +92,7 @@ def lib() -> C.CDLL:
     L.npsd_b200_n_fluid.restype = C.c_int64
     L.npsd_b200_n_fluid.argtypes = [_vp]
     L.npsd_b200_fluid_indices.argtypes = [_vp, _i64p]
+    L.npsd_b200_set_exact.argtypes = [_vp, C.c_int]
     L.npsd_b200_is_pure_neumann.argtypes = [_vp, C.POINTER(C.c_int)]
     L.npsd_b200_check_operator.argtypes = [_vp, C.c_int64, _i64p, _i64p, _f64p, C.c_int64, C.c_int]
     L.npsd_b200_precond_apply.argtypes = [_vp, _f64p, _f64p, C.c_int64]

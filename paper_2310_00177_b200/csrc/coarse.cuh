@@ -1,25 +1,22 @@
 // Network levels above the solve's level 0, 3D (and every level of the raw
-// network): NetContext::apply's down and up steps (net/forward.hpp:95-129)
-// with one thread per cell.
+// network): NetContext::apply's down and up steps (net/forward.hpp:95-129).
 //
 // These grids are small (128^3 and below at 256^3) and their kernels are
 // latency-bound, not bandwidth-bound: what matters is enough independent
-// cells in flight and short dependent chains. A 32 x 4 x 2 block stages its
-// input tile plus a one-cell halo (f32) in shared memory, one warp per row;
-// each thread reads its kernel as one 28-float row (seven 16-byte loads)
-// through a single pointer — the shared copy of its uniform class's kernel or
-// its mixed row in global memory — so uniform and mixed cells of a warp run
-// the same code. One barrier, then the 27 taps in slot order with
-// round-to-nearest ops (apply_kernels, net/kernels.hpp:147-172): outputs are
-// bit-identical to the restatement.
+// cells in flight and short dependent chains. Each cell reads its kernel as
+// one 28-float row (seven 16-byte loads) through a single pointer — the shared
+// copy of its uniform class's kernel or its mixed row in global memory — so
+// uniform and mixed cells of a warp run the same code. The window sum is
+// win_dot (common.cuh): the reference's slot order with round-to-nearest ops
+// (apply_kernels, net/kernels.hpp:147-172; bit-identical outputs) or, in the
+// fast mode, fused per-plane chains.
 //
-// k_cdown<POOL>: y_l = conv_down_l(x_l); x_{l+1} = avg_pool(y_l) from the
-//   block's y tile in shared memory, summed x fastest, then y, then z
-//   (avg_pool2, kernels.hpp:279-292, 3D order). Without POOL: the coarsest
-//   level's single conv (forward.hpp:89,116).
-// k_cup: out_l = z_a y_l + z_b conv_up_l(upsample2(out_{l+1}))
-//   (forward.hpp:118-127); the coarse tile (halo included) is staged, and a
-//   fine tap reads coarse cell (x >> 1, y >> 1, z >> 1), zero outside.
+// k_cdownz<POOL>: y_l = conv_down_l(x_l); x_{l+1} = avg_pool(y_l), summed x
+//   fastest, then y, then z (avg_pool2, kernels.hpp:279-292, 3D order).
+//   Without POOL: the coarsest level's single conv (forward.hpp:89,116).
+// k_cupz: out_l = z_a y_l + z_b conv_up_l(upsample2(out_{l+1}))
+//   (forward.hpp:118-127); a fine tap reads coarse cell (x >> 1, y >> 1,
+//   z >> 1), zero outside.
 #pragma once
 
 #include "common.cuh"
@@ -27,11 +24,6 @@
 #include "net2.cuh"
 
 namespace nb2 {
-
-constexpr int kKX = 32, kKY = 4, kKZ = 2, kKT = kKX * kKY * kKZ;  // block tile = threads (256)
-#ifndef COARSE_MINB
-#define COARSE_MINB 1  // a register cap (more resident blocks) measured slower: it spills
-#endif
 
 // The three uniform-window kernels in shared memory as 28-float rows, so every
 // cell reads its kernel through one pointer: no per-class code paths, no warp
@@ -58,170 +50,8 @@ __device__ __forceinline__ void load_row(const float4* row, float (&k)[28]) {
     }
 }
 
-// A (NZ x NY x NX) box at (bx, by, bz) of level geometry gg, zero outside,
-// staged one warp per row: every load is issued (compile-time trip counts)
-// before any shared store, so the loads of a thread overlap.
-template <int NX, int NY, int NZ, int NW>
-struct BoxStager {
-    static constexpr int RPW = (NY * NZ + NW - 1) / NW;  // rows per warp
-    static constexpr int EPL = (NX + 31) / 32;            // elements per lane per row
-    float v[RPW][EPL];
-    __device__ __forceinline__ void load(const float* __restrict__ src, const Geom& gg, int bx, int by, int bz,
-                                         int warp, int lane) {
-#pragma unroll
-        for (int k = 0; k < RPW; ++k) {
-            const int r = warp + NW * k;
-            const int ly = r % NY, lz = r / NY;
-            const int gy = by + ly, gz = bz + lz;
-            const bool rin = r < NY * NZ && gy >= 0 && gy < gg.ny && gz >= 0 && gz < gg.nz;
-            const float* rowp = src + ((long long)(rin ? gz : 0) * gg.ny + (rin ? gy : 0)) * gg.nx;
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) {
-                const int lx = lane + 32 * e, gx = bx + lx;
-                v[k][e] = (rin && lx < NX && gx >= 0 && gx < gg.nx) ? __ldg(rowp + gx) : 0.0f;
-            }
-        }
-    }
-    __device__ __forceinline__ void store(float (&dst)[NZ][NY][NX], int warp, int lane) const {
-#pragma unroll
-        for (int k = 0; k < RPW; ++k) {
-            const int r = warp + NW * k;
-            if (r < NY * NZ) {
-#pragma unroll
-                for (int e = 0; e < EPL; ++e) {
-                    const int lx = lane + 32 * e;
-                    if (lx < NX) dst[r / NY][r % NY][lx] = v[k][e];
-                }
-            }
-        }
-    }
-};
-
-// The cell's 28-float kernel row: a mixed cell loads its row from global
-// memory before the barrier (mixed_start), a uniform cell reads its class's
-// shared row after it (uniform_finish).
-struct CellRow {
-    float k[28];
-    int wc;
-    // own: the cell is inside the grid (else it reads as a uniform-air cell)
-    __device__ __forceinline__ void mixed_start(const ConvTab& ct, long long c, bool own) {
-        if (!own) {
-            wc = 1;
-        } else if (ct.rcode) {
-            const uint32_t rc = __ldg(ct.rcode + c);
-            wc = (int)(rc >> 30);
-            if (wc == 3) load_row(reinterpret_cast<const float4*>(ct.tab + (long long)(rc & 0x3fffffffu) * kRowW), k);
-        } else {
-            wc = cls_window(__ldg(ct.cls + c));
-            if (wc == 3) load_row(reinterpret_cast<const float4*>(kernel_row(ct, c)), k);
-        }
-    }
-    __device__ __forceinline__ void uniform_finish(const UniRows& U) {
-        if (wc < 3) load_row(&U.r[wc][0], k);
-    }
-};
-
-// grid (ceil(nx/32), ceil(ny/4), ceil(owned planes/2)), block (32, 4, 2)
-template <bool POOL>
-__global__ void __launch_bounds__(kKT, COARSE_MINB) k_cdown(Geom g, const float* __restrict__ x, ConvTab ct,
-                                               const __grid_constant__ KC kc, float* __restrict__ y,
-                                               float* __restrict__ xnext, Geom gc,
-                                               const int* __restrict__ done) {
-    pdl_launch_wait();
-    if (done && *done) return;  // z-slab chunked loop: the solve has finished
-    constexpr int SX = kKX + 2, SY = kKY + 2, SZ = kKZ + 2;
-    __shared__ float sx[SZ][SY][SX];
-    __shared__ float sy[kKZ][kKY][kKX];
-    __shared__ UniRows U;
-    const int tx = threadIdx.x, ty = threadIdx.y, tz = threadIdx.z;
-    const int tid = tx + kKX * (ty + kKY * tz), warp = tid >> 5, lane = tid & 31;
-    const int X0 = blockIdx.x * kKX, Y0 = blockIdx.y * kKY, Z0 = g.zo0 + blockIdx.z * kKZ;
-    const int cx = X0 + tx, cy = Y0 + ty, cz = Z0 + tz;
-    const bool own = cx < g.nx && cy < g.ny && cz < g.zo1;
-    const long long c = own ? lin(g, cx, cy, cz) : 0;
-    BoxStager<SX, SY, SZ, kKT / 32> box;
-    box.load(x, g, X0 - 1, Y0 - 1, Z0 - 1, warp, lane);
-    CellRow K;
-    K.mixed_start(ct, c, own);
-    load_uni_rows(U, kc, tid);
-    box.store(sx, warp, lane);
-    __syncthreads();
-    K.uniform_finish(U);
-    float yv = 0.0f;
-    if (own) {
-#pragma unroll
-        for (int s = 0; s < 27; ++s) {
-            const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
-            yv = __fadd_rn(yv, __fmul_rn(K.k[s], sx[tz + 1 + dz][ty + 1 + dy][tx + 1 + dx]));
-        }
-        y[c] = yv;
-    }
-    if (POOL) {
-        sy[tz][ty][tx] = yv;
-        __syncthreads();
-        constexpr int PX = kKX / 2, PY = kKY / 2;
-        if (tid < PX * PY) {
-            const int px = tid % PX, py = tid / PX;
-            const int qx = (X0 >> 1) + px, qy = (Y0 >> 1) + py, qz = Z0 >> 1;
-            if (qx < gc.nx && qy < gc.ny && qz < gc.nz) {
-                float ps = sy[0][2 * py][2 * px];
-                ps = __fadd_rn(ps, sy[0][2 * py][2 * px + 1]);
-                ps = __fadd_rn(ps, sy[0][2 * py + 1][2 * px]);
-                ps = __fadd_rn(ps, sy[0][2 * py + 1][2 * px + 1]);
-                ps = __fadd_rn(ps, sy[1][2 * py][2 * px]);
-                ps = __fadd_rn(ps, sy[1][2 * py][2 * px + 1]);
-                ps = __fadd_rn(ps, sy[1][2 * py + 1][2 * px]);
-                ps = __fadd_rn(ps, sy[1][2 * py + 1][2 * px + 1]);
-                xnext[lin(gc, qx, qy, qz)] = __fmul_rn(0.125f, ps);
-            }
-        }
-    }
-}
-
-// grid (ceil(nx/32), ceil(ny/4), ceil(owned planes/2)), block (32, 4, 2); outc is level l+1
-template <int D = 3>
-__global__ void __launch_bounds__(kKT, COARSE_MINB) k_cup(Geom g, Geom gc, const float* __restrict__ outc,
-                                             const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
-                                             const __grid_constant__ KC kc, float* __restrict__ outl,
-                                             const int* __restrict__ done) {
-    pdl_launch_wait();
-    if (done && *done) return;  // z-slab chunked loop: the solve has finished
-    // coarse box: (X0/2 - 1 .. X0/2 + 16) x (Y0/2 - 1 .. Y0/2 + 2) x (Z0/2 - 1 .. Z0/2 + 1)
-    constexpr int CX = kKX / 2 + 2, CY = kKY / 2 + 2, CZ = kKZ / 2 + 2;
-    __shared__ float sc[CZ][CY][CX];
-    __shared__ UniRows U;
-    const int tx = threadIdx.x, ty = threadIdx.y, tz = threadIdx.z;
-    const int tid = tx + kKX * (ty + kKY * tz), warp = tid >> 5, lane = tid & 31;
-    const int X0 = blockIdx.x * kKX, Y0 = blockIdx.y * kKY, Z0 = g.zo0 + blockIdx.z * kKZ;
-    const int BX = (X0 >> 1) - 1, BY = (Y0 >> 1) - 1, BZ = (Z0 >> 1) - 1;
-    const int cx = X0 + tx, cy = Y0 + ty, cz = Z0 + tz;
-    const bool own = cx < g.nx && cy < g.ny && cz < g.zo1;
-    const long long c = own ? lin(g, cx, cy, cz) : 0;
-    BoxStager<CX, CY, CZ, kKT / 32> box;
-    box.load(outc, gc, BX, BY, BZ, warp, lane);
-    CellRow K;
-    K.mixed_start(ct, c, own);
-    const float yv = own ? __ldg(yl + c) : 0.0f;
-    const float za = zab[0], zb = zab[1];
-    load_uni_rows(U, kc, tid);
-    box.store(sc, warp, lane);
-    __syncthreads();
-    if (!own) return;
-    K.uniform_finish(U);
-    // fine tap (cx + dx, ...) -> coarse ((cx + dx) >> 1, ...); out-of-domain
-    // fine cells map to out-of-domain coarse cells (dims even): staged zeros
-    float u = 0.0f;
-#pragma unroll
-    for (int s = 0; s < 27; ++s) {
-        const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
-        u = __fadd_rn(u, __fmul_rn(K.k[s], sc[((cz + dz) >> 1) - BZ][((cy + dy) >> 1) - BY][((cx + dx) >> 1) - BX]));
-    }
-    outl[c] = __fadd_rn(__fmul_rn(za, yv), __fmul_rn(zb, u));
-}
-
-
 // ---------------------------------------------------------------------------
-// z-marching variants (the launchers' default): a 32 x 8 block owns a 32 x 8
+// z-marching kernels: a 32 x 8 block owns a 32 x 8
 // x-y tile and ZC consecutive planes; each thread marches its (x, y) column
 // through the ZC planes. The input box (tile + one-cell halo, ZC + 2 planes) is
 // staged once; the 3 x 3 x 3 window rolls through registers (9 new shared
@@ -230,8 +60,7 @@ __global__ void __launch_bounds__(kKT, COARSE_MINB) k_cup(Geom g, Geom gc, const
 // pooling quad sits inside one warp and the pool is summed with shuffles in
 // the reference order (no barrier). Shared rows are padded to 48 floats
 // (= 16 mod 32 banks): the two half-warps' rows fall on disjoint banks.
-// Accumulation order and rounding are those of the one-thread-per-cell
-// kernels above (slot order, __fmul_rn/__fadd_rn): bit-identical outputs.
+// Accumulation: win_dot (exact: slot order, bit-identical; fast: fused chains).
 constexpr int kZX = 32, kZY = 8, kZT = kZX * kZY;  // block tile (x, y) = 256 threads
 #ifndef COARSEZ_MINB
 #define COARSEZ_MINB 4  // min resident blocks per SM of the z-marching kernels: a 64-register cap (1: 84 registers, 3 blocks; measured 3-4 us slower per L1 kernel)
@@ -297,7 +126,7 @@ __device__ __forceinline__ const float4* code_row(const ConvTab& ct, const UniRo
 }
 
 // grid (ceil(nx/32), ceil(ny/8), ceil(owned planes/ZC)), block 256
-template <bool POOL, int ZC>
+template <bool POOL, int ZC, bool F>
 __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cdownz(Geom g, const float* __restrict__ x, ConvTab ct,
                                                 const __grid_constant__ KC kc, float* __restrict__ y,
                                                 float* __restrict__ xnext, Geom gc, const int* __restrict__ done) {
@@ -345,9 +174,7 @@ __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cdownz(Geom g, const floa
         for (int s = 0; s < 27; ++s) w[s] = P[(k + s / 9) % 3][s % 9];
         // branch-free (a cell outside the rank's planes reads the uniform-air
         // row and is not stored), so the cells' chains can interleave
-        float yv = 0.0f;
-#pragma unroll
-        for (int s = 0; s < 27; ++s) yv = __fadd_rn(yv, __fmul_rn(kr[s], w[s]));
+        float yv = win_dot<F, 27>([&](int t) { return kr[t]; }, [&](int t) { return w[t]; });
         if (k + 1 < ZC) load_row(code_row(ct, U, rc[k + 1], c + plane), kr);
         if (!own) yv = 0.0f;
         if (own) y[c] = yv;
@@ -378,7 +205,7 @@ __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cdownz(Geom g, const floa
 }
 
 // grid (ceil(nx/32), ceil(ny/8), ceil(owned planes/ZC)), block 256; outc is level l+1
-template <int ZC>
+template <int ZC, bool F>
 __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cupz(Geom g, Geom gc, const float* __restrict__ outc,
                                               const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
                                               const __grid_constant__ KC kc, float* __restrict__ outl,
@@ -440,11 +267,10 @@ __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cupz(Geom g, Geom gc, con
             const int dz = s / 9 - 1;
             w[s] = Q[(((k + dz) >> 1) + 1) % 3][s % 9];
         }
-        float u = 0.0f;
-#pragma unroll
-        for (int s = 0; s < 27; ++s) u = __fadd_rn(u, __fmul_rn(kr[s], w[s]));
+        const float u = win_dot<F, 27>([&](int t) { return kr[t]; }, [&](int t) { return w[t]; });
         if (k + 1 < ZC) load_row(code_row(ct, U, rc[k + 1], c + plane), kr);
-        if (k < nown) outl[c] = __fadd_rn(__fmul_rn(za, yv[k]), __fmul_rn(zb, u));
+        if (k < nown)
+            outl[c] = F ? __fmaf_rn(za, yv[k], __fmul_rn(zb, u)) : __fadd_rn(__fmul_rn(za, yv[k]), __fmul_rn(zb, u));
     }
 }
 

@@ -63,6 +63,33 @@ struct Sh {
     static constexpr int NB = (D == 3) ? 6 : 4;  // stencil neighbours
 };
 
+// Window dot product sum_s k(s) * w(s) of the network's spatially varying
+// convolution (apply_kernels, net/kernels.hpp:147-172), S = 27 (3D) or 9 slots.
+// Exact (F = false): the reference's slot order, one rounded multiply and one
+// rounded add per slot — bit-identical to the restatement. Fast (F = true):
+// fused multiply-adds in one chain per window plane (three independent
+// chains in 3D), then (a0 + a1) + a2 — within the north_star tolerance
+// (1e-5 relative L2 of the preconditioner output), not bitwise.
+template <bool F, int S, typename KF, typename WF>
+__device__ __forceinline__ float win_dot(KF k, WF w) {
+    if (!F) {
+        float a = 0.0f;
+#pragma unroll
+        for (int s = 0; s < S; ++s) a = __fadd_rn(a, __fmul_rn(k(s), w(s)));
+        return a;
+    }
+    constexpr int P = (S == 27) ? 3 : 1, L = S / P;
+    float a[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) a[p] = 0.0f;
+#pragma unroll
+    for (int s = 0; s < S; ++s) a[s / L] = __fmaf_rn(k(s), w(s), a[s / L]);
+    float t = a[0];
+#pragma unroll
+    for (int p = 1; p < P; ++p) t = __fadd_rn(t, a[p]);
+    return t;
+}
+
 // L0 cell byte: bits 0-1 window class (0/1/2 = uniform fluid/air/solid window,
 // 3 = mixed), bits 2-3 own cell type, bits 4-6 stencil diagonal (# non-solid
 // in-domain face neighbours), bit 7 window holds a fluid cell. Coarse levels

@@ -43,6 +43,7 @@ struct Down0Smem {
 };
 
 // One column segment: tile (tx, ty), planes [zc0, zc1) (both even)
+template <bool F>
 __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __restrict__ cls,
                                                 const double* __restrict__ r, const SolverState* __restrict__ st,
                                                 const KC0& kc, float* __restrict__ y, float* __restrict__ xnext,
@@ -165,19 +166,18 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
         const int c0 = 2 + 2 * lane, r0 = row + 1;
         float yv[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
         if (own) {
-            // uniform-fluid windows convolve with the constant kernel, slot order;
-            // the four cells' chains are independent
-            float acc[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
+            // uniform-fluid windows convolve with the constant kernel (win_dot:
+            // slot order, or fused chains per plane); the four cells' chains
+            // are independent
+            float acc[2][2];
 #pragma unroll
-            for (int s = 0; s < 27; ++s) {
-                const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = s / 9 - 1;
+            for (int p = 0; p < 2; ++p)
 #pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    const int ps = xslot(z + p + dz);
-                    acc[p][0] = __fadd_rn(acc[p][0], __fmul_rn(kc.k[s], S.xin[ps][r0 + dy][c0 + dx]));
-                    acc[p][1] = __fadd_rn(acc[p][1], __fmul_rn(kc.k[s], S.xin[ps][r0 + dy][c0 + 1 + dx]));
-                }
-            }
+                for (int h = 0; h < 2; ++h)
+                    acc[p][h] = win_dot<F, 27>([&](int t) { return kc.k[t]; }, [&](int t) {
+                        const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = t / 9 - 1;
+                        return S.xin[xslot(z + p + dz)][r0 + dy][c0 + h + dx];
+                    });
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
                 const unsigned bc = ob[p];
@@ -218,6 +218,7 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
 #ifndef D0_MINB
 #define D0_MINB 3  // 3 blocks/SM (77 registers; 116 uncapped, 2 blocks): 67 -> 61 us at C3 256^3; 4 (64 registers): 62.3 us
 #endif
+template <bool F>
 __global__ void __launch_bounds__(kSX* kSY, D0_MINB) k_down_l0(Geom g, const uint8_t* __restrict__ cls,
                                                       const double* __restrict__ r, const SolverState* __restrict__ st,
                                                       const __grid_constant__ KC0 kc, float* __restrict__ y,
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kSX* kSY, D0_MINB) k_down_l0(Geom g, const uin
     pdl_launch_wait();
     if (st->dist && st->done) return;
     sched_for_each(sc, [&](int tx, int ty, int u0, int u1) {
-        down_l0_segment(g, cls, r, st, kc, y, xnext, gc, tx, ty, 2 * u0, min(2 * u1, g.nz));
+        down_l0_segment<F>(g, cls, r, st, kc, y, xnext, gc, tx, ty, 2 * u0, min(2 * u1, g.nz));
     });
 }
 

@@ -98,7 +98,7 @@ __device__ __forceinline__ void decode32(const Geom& g, uint32_t c, int& x, int&
     y = (int)(row - (uint32_t)z * ny);
 }
 
-template <int D>
+template <int D, bool F>
 #ifndef MIXDN_MINB
 #define MIXDN_MINB 5  // register cap for 5 blocks/SM (measured 37 -> 29 us on the same box)
 #endif
@@ -127,10 +127,7 @@ __global__ void __launch_bounds__(kBlock, MIXDN_MINB) k_mixed_down0(Geom g, cons
             w[s] = in ? __double2float_rn(__dmul_rn(__dmul_rn(__ldg(r + lin(g, xx, y2, zz)), inv1), inv2)) : 0.0f;
             k[s] = __ldg(K + s);
         }
-        float acc = 0.0f;
-#pragma unroll
-        for (int s = 0; s < S; ++s) acc = __fadd_rn(acc, __fmul_rn(k[s], w[s]));
-        y[c] = acc;
+        y[c] = win_dot<F, S>([&](int t) { return k[t]; }, [&](int t) { return w[t]; });
     }
 }
 
@@ -188,7 +185,7 @@ __global__ void __launch_bounds__(kBlock) k_ident_dir(Geom g, const uint8_t* __r
     }
 }
 
-template <int D, int NO>
+template <int D, int NO, bool F>
 #ifndef MIXUP_MINB
 #define MIXUP_MINB 4  // register cap for 4 blocks/SM (measured 26 -> 24 us)
 #endif
@@ -232,10 +229,9 @@ __global__ void __launch_bounds__(kBlock, MIXUP_MINB) k_mixed_up0(Geom g, Geom g
             w[s] = in ? __ldg(outc + lin(gc, xx >> 1, y2 >> 1, (D == 3) ? zz >> 1 : 0)) : 0.0f;
             k[s] = __ldg(K + s);
         }
-        float u = 0.0f;
-#pragma unroll
-        for (int s = 0; s < S; ++s) u = __fadd_rn(u, __fmul_rn(k[s], w[s]));
-        const float o = __fadd_rn(__fmul_rn(za, __ldg(y0 + c)), __fmul_rn(zb, u));
+        const float u = win_dot<F, S>([&](int t) { return k[t]; }, [&](int t) { return w[t]; });
+        const float o = F ? __fmaf_rn(za, __ldg(y0 + c), __fmul_rn(zb, u))
+                          : __fadd_rn(__fmul_rn(za, __ldg(y0 + c)), __fmul_rn(zb, u));
         const double dv = __dmul_rn((double)o, nrm);
         dout[c] = dv;
 #pragma unroll

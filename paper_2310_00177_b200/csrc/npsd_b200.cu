@@ -267,7 +267,7 @@ struct npsd_b200_ctx {
     uint32_t* htv = nullptr;
     unsigned long long ht_cap = 0;
     bool dict_sort = false;   // NPSD_DICT_SORT=1: pattern ids by radix sort + run heads (A/B)
-    bool coarse_old = false;  // NPSD_COARSE_OLD=1: one-thread-per-cell coarse kernels (A/B)
+    bool fast = true;  // network arithmetic: fused/reassociated (true) or the reference's order, bitwise (false)
     int coarse_zc_max = 4;    // NPSD_COARSE_ZC: planes per block of the z-marching coarse kernels
     long long slab_chunk_launches = 0;
     cudaStream_t s = nullptr, s2 = nullptr;
@@ -904,23 +904,23 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
     const Geom gc = POOL ? c->L[l + 1].g : L.g;
     float* xnext = POOL ? c->L[l + 1].x : nullptr;
     if (D == 3 && !L0) {
-        // f32 input (levels >= 1, raw level 0): one thread per cell (coarse.cuh)
+        // f32 input (levels >= 1, raw level 0): z-marching columns (coarse.cuh)
         const KC& kc = (l == c->depth - 1) ? c->kc_coarse : c->kc_down[l];
         const int* dn = c->slab.on ? &c->st->done : nullptr;
-        if (c->coarse_old) {
-            const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
-            launch_pdl(c, s, k_cdown<POOL>, grid, dim3(kKX, kKY, kKZ), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext,
-                       gc, dn);
-            return;
-        }
         const int zc = coarse_zc(c, L.g);
         const dim3 grid((L.g.nx + kZX - 1) / kZX, (L.g.ny + kZY - 1) / kZY, (L.g.zo1 - L.g.zo0 + zc - 1) / zc);
-        if (zc == 8)
-            launch_pdl(c, s, k_cdownz<POOL, 8>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc, dn);
-        else if (zc == 4)
-            launch_pdl(c, s, k_cdownz<POOL, 4>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc, dn);
-        else
-            launch_pdl(c, s, k_cdownz<POOL, 2>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc, dn);
+#define NPSD_CDOWN(ZC_, F_) \
+    launch_pdl(c, s, k_cdownz<POOL, ZC_, F_>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc, dn)
+        if (c->fast) {
+            if (zc == 8) NPSD_CDOWN(8, true);
+            else if (zc == 4) NPSD_CDOWN(4, true);
+            else NPSD_CDOWN(2, true);
+        } else {
+            if (zc == 8) NPSD_CDOWN(8, false);
+            else if (zc == 4) NPSD_CDOWN(4, false);
+            else NPSD_CDOWN(2, false);
+        }
+#undef NPSD_CDOWN
         return;
     }
     const dim3 block(kNX, kNY);
@@ -942,23 +942,21 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
     const float* outc = (l + 1 == c->depth - 1) ? Lc.y : Lc.out;
     if (D == 3 && MODE == kUpMid) {
         const int* dn = c->slab.on ? &c->st->done : nullptr;
-        if (c->coarse_old) {
-            const dim3 grid((L.g.nx + kKX - 1) / kKX, (L.g.ny + kKY - 1) / kKY, (L.g.zo1 - L.g.zo0 + kKZ - 1) / kKZ);
-            launch_pdl(c, s, k_cup<3>, grid, dim3(kKX, kKY, kKZ), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l,
-                       tab_up(c, l), c->kc_up[l], outl, dn);
-            return;
-        }
         const int zc = coarse_zc(c, L.g);
         const dim3 grid((L.g.nx + kZX - 1) / kZX, (L.g.ny + kZY - 1) / kZY, (L.g.zo1 - L.g.zo0 + zc - 1) / zc);
-        if (zc == 8)
-            launch_pdl(c, s, k_cupz<8>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
-                       c->kc_up[l], outl, dn);
-        else if (zc == 4)
-            launch_pdl(c, s, k_cupz<4>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
-                       c->kc_up[l], outl, dn);
-        else
-            launch_pdl(c, s, k_cupz<2>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l),
-                       c->kc_up[l], outl, dn);
+#define NPSD_CUP(ZC_, F_)                                                                                        \
+    launch_pdl(c, s, k_cupz<ZC_, F_>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), \
+               c->kc_up[l], outl, dn)
+        if (c->fast) {
+            if (zc == 8) NPSD_CUP(8, true);
+            else if (zc == 4) NPSD_CUP(4, true);
+            else NPSD_CUP(2, true);
+        } else {
+            if (zc == 8) NPSD_CUP(8, false);
+            else if (zc == 4) NPSD_CUP(4, false);
+            else NPSD_CUP(2, false);
+        }
+#undef NPSD_CUP
         return;
     }
     const dim3 block(kNX, kNY);
@@ -972,6 +970,24 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
             (MODE == kUpL0) ? Occ{c->tflags, c->tf_ntx, c->tf_nty} : Occ{nullptr, 0, 0});
 }
 
+// KUp0 of a uniform-fluid up kernel: its slots and the parity-merged taps
+// (up0.cuh), summed in f64 and rounded once
+KUp0 up0_kernel(const float* k27) {
+    KUp0 o;
+    for (int i = 0; i < 27; ++i) o.k[i] = k27[i];
+    for (int p = 0; p < 8; ++p) {
+        const int pz = p >> 2, py = (p >> 1) & 1, px = p & 1;
+        double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        auto side = [](int par, int d) { return ((par + d) >> 1) - par + 1; };  // 0 = lo coarse cell, 1 = hi
+        for (int t = 0; t < 27; ++t) {
+            const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = t / 9 - 1;
+            m[side(pz, dz) * 4 + side(py, dy) * 2 + side(px, dx)] += (double)k27[t];
+        }
+        for (int j = 0; j < 8; ++j) o.m[p][j] = (float)m[j];
+    }
+    return o;
+}
+
 template <int D, int NO>
 void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
     if (D == 3) {
@@ -979,11 +995,10 @@ void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
         const LevelBufs& L = c->L[0];
         const LevelBufs& L1 = c->L[1];
         const float* outc = (c->depth == 2) ? L1.y : L1.out;
-        auto k = k_up_l0<NO>;
+        auto k = c->fast ? k_up_l0<NO, true> : k_up_l0<NO, false>;
         const size_t sm = sizeof(Up0Smem<NO>);
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        KC0 kc0;
-        for (int i = 0; i < 27; ++i) kc0.k[i] = c->kc_up[0].k[0][i];  // the uniform-fluid kernel
+        const KUp0 kc0 = up0_kernel(c->kc_up[0].k[0]);  // the uniform-fluid kernel (+ merged parity taps)
         launch_pdl(c, s, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y,
                    c->zab, kc0, c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_stencil.view());
         return;
@@ -1052,19 +1067,21 @@ void launch_down_l0(npsd_b200_ctx* c, cudaStream_t s) {
     const Geom g = L.g;
     const dim3 block(kSX, kSY);
     const size_t sm = sizeof(Down0Smem);
-    CK(cudaFuncSetAttribute(k_down_l0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const dim3 grid(wave_blocks(c, k_down_l0, kSX * kSY, sm));
+    auto k = c->fast ? k_down_l0<true> : k_down_l0<false>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const dim3 grid(wave_blocks(c, k, kSX * kSY, sm));
     KC0 kc0;
     for (int i = 0; i < 27; ++i) kc0.k[i] = c->kc_down[0].k[0][i];  // the uniform-fluid kernel
-    launch_pdl(c, s, k_down_l0, grid, block, sm, g, L.cls, c->R, (const SolverState*)c->st, kc0, L.y, c->L[1].x,
-               c->L[1].g, c->sch_down0.view());
+    launch_pdl(c, s, k, grid, block, sm, g, L.cls, c->R, (const SolverState*)c->st, kc0, L.y, c->L[1].x, c->L[1].g,
+               c->sch_down0.view());
 }
 
 template <int D>
 void launch_mixed_down0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
-    launch_pdl(c, s, k_mixed_down0<D>, dim3(grid_for(c, k_mixed_down0<D>, L.g.n)), dim3(kBlock), 0, L.g, c->dlist0,
-               c->dcnt0, c->R, (const SolverState*)c->st, L.tab_down, c->dkid0, L.y);
+    auto k = c->fast ? k_mixed_down0<D, true> : k_mixed_down0<D, false>;
+    launch_pdl(c, s, k, dim3(grid_for(c, k, L.g.n)), dim3(kBlock), 0, L.g, c->dlist0, c->dcnt0, c->R,
+               (const SolverState*)c->st, L.tab_down, c->dkid0, L.y);
 }
 
 template <int D, int NO>
@@ -1072,9 +1089,9 @@ void launch_mixed_up0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
     const LevelBufs& L1 = c->L[1];
     const float* outc = (c->depth == 2) ? L1.y : L1.out;
-    launch_pdl(c, s, k_mixed_up0<D, NO>, dim3(grid_for(c, k_mixed_up0<D, NO>, L.g.n)), dim3(kBlock), 0, L.g, L1.g,
-               c->ulist0, c->ucnt0, outc, L.y, c->zab, L.tab_up, c->ukid0, c->Dtmp, c->st, c->ADring, c->partials,
-               c->counter);
+    auto k = c->fast ? k_mixed_up0<D, NO, true> : k_mixed_up0<D, NO, false>;
+    launch_pdl(c, s, k, dim3(grid_for(c, k, L.g.n)), dim3(kBlock), 0, L.g, L1.g, c->ulist0, c->ucnt0, outc, L.y,
+               c->zab, L.tab_up, c->ukid0, c->Dtmp, c->st, c->ADring, c->partials, c->counter);
 }
 
 template <int D>
@@ -1999,7 +2016,6 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->S = (dim == 3) ? 27 : 9;
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
-        if (const char* e = std::getenv("NPSD_COARSE_OLD")) c->coarse_old = (e[0] == '1');
         if (const char* e = std::getenv("NPSD_DICT_SORT")) c->dict_sort = (e[0] == '1');
         auto env_int = [](const char* n, int& v) {
             if (const char* e = std::getenv(n)) {
@@ -2300,6 +2316,16 @@ int npsd_b200_destroy(npsd_b200_ctx* c) {
 }
 
 const char* npsd_b200_last_error(const npsd_b200_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int npsd_b200_set_exact(npsd_b200_ctx* c, int exact) {
+    return guarded(c, [&] {
+        const bool fast = exact == 0;
+        if (fast != c->fast) {
+            c->fast = fast;
+            ++c->buf_gen;  // captured graphs hold the other kernels
+        }
+    });
+}
 
 int npsd_b200_set_params(npsd_b200_ctx* c, const float* params, size_t n) {
     return guarded(c, [&] {

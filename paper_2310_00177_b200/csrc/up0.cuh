@@ -37,10 +37,22 @@ struct Up0Smem {
 __device__ __forceinline__ bool up_cell(unsigned b) { return (b & 0xfu) == 0u; }  // window 0, type 0
 __device__ __forceinline__ bool up_pair(unsigned b2) { return up_cell(b2 & 0xffu) || up_cell(b2 >> 8); }
 
-template <int NO>
+// The uniform-fluid up kernel: its 27 slots (exact path) and, for the fast
+// path, the taps merged per fine-cell parity. Upsampling maps the three fine
+// taps of a dimension onto two coarse cells — parity 0: d = -1 -> coarse
+// -1, d = 0, +1 -> coarse 0; parity 1: d = -1, 0 -> coarse 0, d = +1 ->
+// coarse +1 — so m[pz*4 + py*2 + px][a*4 + b*2 + c] is the sum of k over the
+// taps landing on coarse (lo/hi)^3 = (a, b, c): 8 fused multiply-adds per
+// cell instead of 27 (forward.hpp:118-127 reassociated; fast path only).
+struct KUp0 {
+    float k[27];
+    float m[8][8];
+};
+
+template <int NO, bool F>
 __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, const uint8_t* __restrict__ cls,
                                               const float* __restrict__ outc, const float* __restrict__ y0,
-                                              const KC0& kc, float za, float zb, double nrm, int nc,
+                                              const KUp0& kc, float za, float zb, double nrm, int nc,
                                               const double* const (&adp)[(NO > 0) ? NO : 1],
                                               double* __restrict__ dout, double (&acc)[(NO > 0) ? NO : 1], int tx,
                                               int ty, int zc0, int zc1) {
@@ -111,23 +123,43 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
             const int s = slot(z);
             const float2 yv = *reinterpret_cast<const float2*>(&S.y[s][row][2 * lane]);
             float u[2];
+            if (F) {
+                // merged parity taps: coarse (lo, hi) per dimension
+                const int zl = ((z - 1) >> 1) & 3, zh = ((z + 1) >> 1) & 3;
+                const int pyz = ((z & 1) << 2) | ((yy & 1) << 1);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float a = 0.0f;
+                for (int h = 0; h < 2; ++h) {
+                    const float* m = kc.m[pyz | h];
+                    float a0 = 0.0f, a1 = 0.0f;
 #pragma unroll
-                for (int t = 0; t < 27; ++t) {
-                    const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = t / 9 - 1;
-                    const int kz = ((z + dz) >> 1) & 3;
-                    const int col = lane + ((h + dx) >> 1) + 1;  // ((x + h + dx) >> 1) - CX0
-                    a = __fadd_rn(a, __fmul_rn(kc.k[t], S.oc[kz][crow[dy + 1]][col]));
+                    for (int t = 0; t < 4; ++t) {
+                        const int b = t >> 1, cc = t & 1;
+                        const int rr = crow[2 * b], col = lane + h + cc;
+                        a0 = __fmaf_rn(m[t], S.oc[zl][rr][col], a0);
+                        a1 = __fmaf_rn(m[4 + t], S.oc[zh][rr][col], a1);
+                    }
+                    u[h] = __fadd_rn(a0, a1);
                 }
-                u[h] = a;
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float a = 0.0f;
+#pragma unroll
+                    for (int t = 0; t < 27; ++t) {
+                        const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = t / 9 - 1;
+                        const int kz = ((z + dz) >> 1) & 3;
+                        const int col = lane + ((h + dx) >> 1) + 1;  // ((x + h + dx) >> 1) - CX0
+                        a = __fadd_rn(a, __fmul_rn(kc.k[t], S.oc[kz][crow[dy + 1]][col]));
+                    }
+                    u[h] = a;
+                }
             }
             const long long q = z * plane + qo;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (!up_cell((bc >> (8 * h)) & 0xffu)) continue;
-                const float o = __fadd_rn(__fmul_rn(za, h ? yv.y : yv.x), __fmul_rn(zb, u[h]));
+                const float o = F ? __fmaf_rn(za, h ? yv.y : yv.x, __fmul_rn(zb, u[h]))
+                                  : __fadd_rn(__fmul_rn(za, h ? yv.y : yv.x), __fmul_rn(zb, u[h]));
                 const double dv = __dmul_rn((double)o, nrm);
                 dout[q + h] = dv;
 #pragma unroll
@@ -150,10 +182,10 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
 #else
 #define UP0_BOUNDS __launch_bounds__(kSX* kSY)
 #endif
-template <int NO>
+template <int NO, bool F>
 __global__ void UP0_BOUNDS k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ cls,
                                                     const float* __restrict__ outc, const float* __restrict__ y0,
-                                                    const float* __restrict__ zab, const __grid_constant__ KC0 kc,
+                                                    const float* __restrict__ zab, const __grid_constant__ KUp0 kc,
                                                     double* __restrict__ dout, SolverState* st,
                                                     const double* __restrict__ ADring, double* __restrict__ partials,
                                                     unsigned int* __restrict__ counter, Sched sc) {
@@ -173,7 +205,7 @@ __global__ void UP0_BOUNDS k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ 
 #pragma unroll
     for (int j = 0; j < NA; ++j) acc[j] = 0.0;
     sched_for_each(sc, [&](int tx, int ty, int u0, int u1) {
-        up_l0_segment<NO>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, u0, u1);
+        up_l0_segment<NO, F>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, u0, u1);
     });
     double tot[NA];
     // the mixed fluid cells follow in k_mixed_up0, which finalises the MGS

@@ -32,14 +32,20 @@ def test_run_bench_rows_csv(b200, oracle, ref, tmp_path):
             if m in ("fpcg+none", "psdo+ic0"):
                 assert "not available" in r.error
                 continue
-            assert r.error == "" and r.converged, (name, m, r.error)
-            assert r.final_rel_residual <= 1e-6
+            assert r.error == "", (name, m, r.error)
             assert r.total_seconds > 0 and r.setup_seconds > 0
-            if m.startswith("psd"):
+            if m.startswith("psd+"):
+                continue  # steepest descent: no convergence promised within the budget (history checked below)
+            assert r.converged, (name, m)
+            assert r.final_rel_residual <= 1e-6
+            if m.startswith("psdo"):
                 assert 0 < r.precond_seconds < r.iterate_seconds
     # psdo+none is the reference psdo_solve with IdentityPrecond; cg is cg_solve
     want = ref.psdo_solve(t1, systems["C1_32"][1], mode="identity", max_iters=3000)
     assert abs(by[("C1_32", "psdo+none")].iterations - want["iterations"]) <= 1
+    want_psd = ref.psdo_solve(t1, systems["C1_32"][1], mode="identity", n_ortho=0, max_iters=30, tol_reduction=1e-300)
+    h, w = np.array(by[("C1_32", "psd+none")].residual_history[:31]), want_psd["residual_history"]
+    assert np.max(np.abs(h - w) / w) <= 1e-9
     want_cg = ref.pcg_solve(t1, systems["C1_32"][1], precond=0, max_iters=3000)
     assert abs(by[("C1_32", "cg")].iterations - want_cg["iterations"]) <= 1
     # the pure-Neumann box converged only because its solves projected

@@ -2,8 +2,9 @@
 reference build, on identical seeded inputs.
 
 Bars (north_star): flag/mask coarsening bit-exact; network / preconditioner
-output within 1e-5 relative L2 (the kernels are in fact bitwise for a given f32
-input, asserted where it holds); iteration count to rel-res 1e-6 within +-1 of
+output within 1e-5 relative L2 — in the default (fast) network arithmetic, and
+bitwise in the exact mode (Context(exact=True): the reference's operation
+order), asserted for both; iteration count to rel-res 1e-6 within +-1 of
 the reference psdo_solve; residual history over a fixed budget within 1e-6
 relative (random weights)."""
 import numpy as np
@@ -22,10 +23,10 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def make(b200, oracle, types, depth, params):
+def make(b200, oracle, types, depth, params, exact=True):
     dim = types.ndim
     P = b200.NetParams(dim, depth, params)
-    ctx = b200.Context(dim, types.shape, P)
+    ctx = b200.Context(dim, types.shape, P, exact=exact)
     ctx.set_mask(types)
     octx = oracle.context(types, params, depth)
     return ctx, octx
@@ -51,16 +52,18 @@ def test_level_images_and_z_bitexact(b200, oracle, shape, depth, seed):
     assert np.array_equal(ctx.fluid_indices(), octx.fluid_indices())
 
 
+@pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("shape,depth,seed", CASES)
-def test_net_apply_bitwise(b200, oracle, shape, depth, seed):
+def test_net_apply_bitwise(b200, oracle, shape, depth, seed, exact):
     t = scenes.random_types(shape, 30 + seed)
     p = oracle.init_params(len(shape), depth, 40 + seed)
-    ctx, octx = make(b200, oracle, t, depth, p)
+    ctx, octx = make(b200, oracle, t, depth, p, exact)
     x = np.random.default_rng(seed).standard_normal(shape).astype(np.float32)
     got = ctx.net_apply(x)
     want = octx.net_apply(x)
     assert rel_l2(got, want) <= REL_L2
-    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    if exact:
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
 @pytest.mark.ref
@@ -74,32 +77,38 @@ def test_net_apply_2d_vs_reference_bitwise(b200, oracle, ref, shape, depth, seed
     assert np.array_equal(ctx.net_apply(x).view(np.uint32), want.view(np.uint32))
 
 
+@pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("shape,depth,seed", CASES)
-def test_precond_apply(b200, oracle, shape, depth, seed):
+def test_precond_apply(b200, oracle, shape, depth, seed, exact):
     t = scenes.random_types(shape, 70 + seed)
     p = oracle.init_params(len(shape), depth, 80 + seed)
-    ctx, octx = make(b200, oracle, t, depth, p)
+    ctx, octx = make(b200, oracle, t, depth, p, exact)
     r = np.random.default_rng(seed).standard_normal(ctx.n_fluid)
     err = rel_l2(ctx.precond_apply(r), octx.precond_apply(r))
     assert err <= REL_L2
-    assert err <= 1e-12  # bit-identical f32 network; f64 norm rounding only
+    if exact:
+        assert err <= 1e-12  # bit-identical f32 network; f64 norm rounding only
     assert np.all(ctx.precond_apply(np.zeros_like(r)) == 0.0)  # test_neural.cpp:258-261
 
 
+@pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("shape,depth,seed", [((64, 64, 128), 4, 0), ((48, 96, 64), 3, 1)])
-def test_precond_apply_interior_tiles(b200, oracle, shape, depth, seed):
+def test_precond_apply_interior_tiles(b200, oracle, shape, depth, seed, exact):
     """Grids large enough that tiles have interior halos on every side (the
     small cases above are all-boundary tiles)."""
     t = scenes.random_types(shape, 170 + seed, p=(0.6, 0.3, 0.1), blobs=6)
     p = oracle.init_params(3, depth, 180 + seed)
-    ctx, octx = make(b200, oracle, t, depth, p)
+    ctx, octx = make(b200, oracle, t, depth, p, exact)
     r = np.random.default_rng(seed).standard_normal(ctx.n_fluid)
     z = ctx.precond_apply(r)
     assert np.all(np.isfinite(z))
-    # the f32 network of the solve path is bit-identical to the restatement: only
-    # the f64 residual norm (tree vs serial sum) differs, ~1e-16; a single f32 ulp
-    # at one cell would show as ~1e-10
-    assert rel_l2(z, octx.precond_apply(r)) <= 1e-12
+    err = rel_l2(z, octx.precond_apply(r))
+    assert err <= REL_L2
+    # exact: the f32 network of the solve path is bit-identical to the
+    # restatement; only the f64 residual norm (tree vs serial sum) differs,
+    # ~1e-16; a single f32 ulp at one cell would show as ~1e-10
+    if exact:
+        assert err <= 1e-12
 
 
 def test_psdo_history_c3_64_random_weights(b200, oracle):
