@@ -219,90 +219,6 @@ __device__ __forceinline__ bool grid_reduce(double (&v)[NV], double* __restrict_
     return true;
 }
 
-// Two-level deterministic grid reduction for large grids: blocks are grouped
-// by 128 consecutive block ids; the last block of each group sums its group in
-// block order into partials2, and the last group-reducer sums the groups in
-// order. counters[0] = final, counters[1 + group] = per-group tickets.
-// partials1: NV * nblk, partials2: NV * ngroups.
-template <int NV>
-__device__ __forceinline__ bool grid_reduce2(double (&v)[NV], double* __restrict__ partials1,
-                                             double* __restrict__ partials2, unsigned int* __restrict__ counters,
-                                             double (&tot)[NV]) {
-    constexpr int GRP = 128;
-    __shared__ double sred[kBlock / 32][NV];
-    __shared__ int s_role;
-    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-    const int nthr = blockDim.x * blockDim.y * blockDim.z;
-    const int nwarp = nthr >> 5;
-    const unsigned int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const unsigned int nblk = gridDim.x * gridDim.y * gridDim.z;
-    const unsigned int ngrp = (nblk + GRP - 1) / GRP;
-    const unsigned int grp = bid / GRP;
-    const unsigned int g0 = grp * GRP, g1 = min(g0 + GRP, nblk);
-    const int lane = tid & 31, warp = tid >> 5;
-    auto block_sum = [&](double (&a)[NV]) {
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            double s = a[j];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) sred[warp][j] = s;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            double s = 0.0;
-            for (int w = 0; w < nwarp; ++w) s += sred[w][j];
-            a[j] = s;
-        }
-        __syncthreads();
-    };
-    double a[NV];
-#pragma unroll
-    for (int j = 0; j < NV; ++j) a[j] = v[j];
-    block_sum(a);
-    if (tid == 0) {
-#pragma unroll
-        for (int j = 0; j < NV; ++j) partials1[(long long)j * nblk + bid] = a[j];
-        __threadfence();
-        const unsigned int t = atomicAdd(counters + 1 + grp, 1u);
-        s_role = (t == g1 - g0 - 1) ? 1 : 0;
-    }
-    __syncthreads();
-    if (!s_role) return false;
-    __threadfence();
-    // group reducer: blocks g0..g1-1 in order
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-        double s = 0.0;
-        for (unsigned int bi = g0 + tid; bi < g1; bi += nthr) s += __ldcg(partials1 + (long long)j * nblk + bi);
-        a[j] = s;
-    }
-    block_sum(a);
-    if (tid == 0) {
-#pragma unroll
-        for (int j = 0; j < NV; ++j) partials2[(long long)j * ngrp + grp] = a[j];
-        counters[1 + grp] = 0u;
-        __threadfence();
-        const unsigned int t = atomicAdd(counters, 1u);
-        s_role = (t == ngrp - 1) ? 2 : 0;
-    }
-    __syncthreads();
-    if (s_role != 2) return false;
-    __threadfence();
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-        double s = 0.0;
-        for (unsigned int gi = tid; gi < ngrp; gi += nthr) s += __ldcg(partials2 + (long long)j * ngrp + gi);
-        a[j] = s;
-    }
-    block_sum(a);
-#pragma unroll
-    for (int j = 0; j < NV; ++j) tot[j] = a[j];
-    if (tid == 0) counters[0] = 0u;
-    return true;
-}
-
 // L0 tile occupancy (k_tile_flags): 32 x 8 tiles per plane, dilated by one
 // cell; flags == nullptr disables skipping (raw-network calls).
 constexpr int kFlagTX = 32, kFlagTY = 8;

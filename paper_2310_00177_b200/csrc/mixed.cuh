@@ -30,55 +30,76 @@ __global__ void __launch_bounds__(kBlock) k_mixed_list(Geom g, const uint8_t* __
 
 // The solve needs y_0 only at mixed cells whose window holds a fluid cell (the
 // input is zero over the others: y_0 = +0, never computed or read) and the up
-// output only at fluid cells. set_mask splits the level-0 list (and the cells'
-// pattern ids) into those two sublists, ascending cell order kept.
-__global__ void __launch_bounds__(kBlock) k_mixed_flags(const uint32_t* __restrict__ list,
-                                                        const uint32_t* __restrict__ count,
-                                                        const uint8_t* __restrict__ cls, uint32_t* __restrict__ fd,
-                                                        uint32_t* __restrict__ fu) {
-    const uint32_t n = *count;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint8_t b = cls[list[i]];
-        fd[i] = cls_wfluid(b) ? 1u : 0u;
-        fu[i] = (cls_type(b) == 0) ? 1u : 0u;
+// output only at fluid cells. Those two sublists of the level-0 mixed cells
+// (with their pattern ids), ascending cell order kept, come from segment masks
+// like every other cell list: k_sub_masks (one warp per 32-cell segment), a
+// scan of the counts, then k_mixed_sub places each mixed cell.
+__global__ void __launch_bounds__(kBlock) k_sub_masks(Geom g, const uint8_t* __restrict__ cls,
+                                                      uint32_t* __restrict__ dmask, uint32_t* __restrict__ dcount,
+                                                      uint32_t* __restrict__ umask, uint32_t* __restrict__ ucount) {
+    const long long nseg = (g.n + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    const long long wstride = (long long)gridDim.x * blockDim.x / 32;
+    for (long long seg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32; seg < nseg; seg += wstride) {
+        const long long c = seg * 32 + lane;
+        const bool in = c >= owned_lo(g) && c < owned_hi(g);
+        const uint8_t b = in ? cls[c] : 0;
+        const bool mixed = in && cls_window(b) == 3;
+        const uint32_t dm = __ballot_sync(0xffffffffu, mixed && cls_wfluid(b));
+        const uint32_t um = __ballot_sync(0xffffffffu, mixed && cls_type(b) == 0);
+        if (lane == 0) {
+            dmask[seg] = dm;
+            dcount[seg] = __popc(dm);
+            umask[seg] = um;
+            ucount[seg] = __popc(um);
+        }
     }
 }
 
-__global__ void __launch_bounds__(kBlock) k_mixed_split(const uint32_t* __restrict__ list,
-                                                        const uint32_t* __restrict__ kid,
-                                                        const uint32_t* __restrict__ count,
-                                                        const uint32_t* __restrict__ fd, const uint32_t* __restrict__ sd,
-                                                        const uint32_t* __restrict__ fu, const uint32_t* __restrict__ su,
-                                                        uint32_t* __restrict__ dlist, uint32_t* __restrict__ dkid,
-                                                        uint32_t* __restrict__ ulist, uint32_t* __restrict__ ukid) {
+__global__ void __launch_bounds__(kBlock) k_mixed_sub(const uint32_t* __restrict__ list,
+                                                      const uint32_t* __restrict__ pid,
+                                                      const uint32_t* __restrict__ count,
+                                                      const uint32_t* __restrict__ dmask, const uint32_t* __restrict__ dbase,
+                                                      const uint32_t* __restrict__ umask, const uint32_t* __restrict__ ubase,
+                                                      uint32_t* __restrict__ dlist, uint32_t* __restrict__ dkid,
+                                                      uint32_t* __restrict__ ulist, uint32_t* __restrict__ ukid) {
     const uint32_t n = *count;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint32_t c = list[i], k = kid[i];
-        if (fd[i]) {
-            dlist[sd[i]] = c;
-            dkid[sd[i]] = k;
+        const uint32_t c = list[i], k = pid[i];
+        const uint32_t bit = 1u << (c & 31);
+        if (dmask[c >> 5] & bit) {
+            const long long j = mixed_index(dmask, dbase, c);
+            dlist[j] = c;
+            dkid[j] = k;
         }
-        if (fu[i]) {
-            ulist[su[i]] = c;
-            ukid[su[i]] = k;
+        if (umask[c >> 5] & bit) {
+            const long long j = mixed_index(umask, ubase, c);
+            ulist[j] = c;
+            ukid[j] = k;
         }
     }
 }
 
 // levels >= 1: one word per cell, (window class << 30) | mixed row, so the
-// coarse kernels reach a mixed cell's row with one load (coarse.cuh)
+// coarse kernels reach a mixed cell's row with one load (coarse.cuh). The
+// row is the cell's dictionary pattern, or (*unverified) its mixed index;
+// rows at or beyond the table capacity read row 0 (the frame is redone, see
+// k_build_rows).
 __global__ void __launch_bounds__(kBlock) k_row_codes(Geom g, const uint8_t* __restrict__ cls,
                                                       const uint32_t* __restrict__ mmask,
                                                       const uint32_t* __restrict__ mbase,
-                                                      const uint32_t* __restrict__ kid, uint32_t* __restrict__ rcode) {
+                                                      const uint32_t* __restrict__ pid,
+                                                      const uint32_t* __restrict__ unverified, uint32_t rows_cap,
+                                                      uint32_t* __restrict__ rcode) {
+    const bool pc = *unverified != 0;
     FOR_OWNED(g, c) {
         const uint32_t w = (uint32_t)cls_window(cls[c]);
         uint32_t row = 0;
         if (w == 3) {
             row = (uint32_t)mixed_index(mmask, mbase, c);
-            if (kid) row = kid[row];
+            if (!pc) row = pid[row];
+            if (row >= rows_cap) row = 0;
         }
         rcode[c] = (w << 30) | row;
     }

@@ -24,8 +24,8 @@
 namespace nb2 {
 
 // Mixed-window kernels are AoS rows of kRowW floats (27 used). Row of a mixed
-// cell = kid[mixed_index] (level 0: window-pattern dictionary) or the mixed
-// index itself (kid == nullptr, coarse levels).
+// cell = kid[mixed_index] (level 0: window-pattern dictionary) or its row code
+// (levels >= 1, k_row_codes).
 constexpr int kRowW = 28;
 
 struct ConvTab {
@@ -38,7 +38,10 @@ struct ConvTab {
     const uint32_t* rcode;  // levels >= 1: per cell (window class << 30) | row, or nullptr
 };
 
+// levels >= 1: the cell's row code (k_row_codes); level 0: the cell's
+// window pattern (kid = the dictionary ids by mixed index)
 __device__ __forceinline__ const float* kernel_row(const ConvTab& ct, long long c) {
+    if (ct.rcode) return ct.tab + (long long)(__ldg(ct.rcode + c) & 0x3fffffffu) * kRowW;
     const long long idx = mixed_index(ct.mmask, ct.mbase, c);
     const long long row = ct.kid ? (long long)__ldg(ct.kid + idx) : idx;
     return ct.tab + row * kRowW;

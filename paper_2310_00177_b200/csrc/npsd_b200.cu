@@ -80,8 +80,7 @@ struct LevelBufs {
     uint32_t* mlist = nullptr;  // compact mixed cells (k_mixed_list)
     uint32_t* mcnt = nullptr;   // their number (device)
     uint32_t* rcode = nullptr;  // levels >= 1: (window class << 30) | row per cell (k_row_codes)
-    uint32_t* pid = nullptr;    // levels >= 1: mixed index -> dictionary row (coarse_dictionary)
-    const uint32_t* kid = nullptr;  // pid when the level's dictionary verified, else nullptr
+    uint32_t* pid = nullptr;    // levels >= 1: mixed index -> dictionary row (dedup_patterns)
 };
 
 // one balanced schedule (common.cuh Sched) over L0 tile columns
@@ -265,8 +264,23 @@ struct npsd_b200_ctx {
     int sched_gx = 1, sched_gy = 1, sched0_gx = 1, sched0_gy = 1;
     unsigned long long* htk = nullptr;  // pattern hash table: keys, values (dedup_patterns)
     uint32_t* htv = nullptr;
-    unsigned long long ht_cap = 0;
-    bool dict_sort = false;   // NPSD_DICT_SORT=1: pattern ids by radix sort + run heads (A/B)
+    unsigned long long ht_alloc = 0;            // slots allocated
+    unsigned long long cap_ht[kMaxDepth] = {};  // slots used per level (power of two; grown by setup_sync)
+    long long tab_alloc[kMaxDepth] = {};        // kernel-row table rows allocated per level
+    // set_mask without host synchronisation (setup.cuh SetupInfo): device
+    // results, their pinned readback and its event; the captured setup graph
+    SetupInfo* d_info = nullptr;
+    SetupInfo* info_host = nullptr;
+    cudaEvent_t ev_setup = nullptr;
+    bool setup_pending = false;
+    uint8_t* types_dev = nullptr;        // the frame's cell types (the setup graph reads them here)
+    const uint8_t* types_cur = nullptr;  // the buffer the last set_mask read (for a redo)
+    cudaGraphExec_t mask_exec = nullptr;
+    unsigned mask_exec_gen = ~0u;
+    long long mask_nodes = 0;
+    bool mask_graph_ok = true;
+    uint32_t *dmask = nullptr, *dcount = nullptr, *dbase = nullptr;  // L0 mixed cells whose window holds fluid
+    uint32_t *umask = nullptr, *ucount = nullptr, *ubase = nullptr;  // L0 mixed fluid cells
     bool fast = true;  // network arithmetic: fused/reassociated (true) or the reference's order, bitwise (false)
     int coarse_zc_max = 4;    // NPSD_COARSE_ZC: planes per block of the z-marching coarse kernels
     long long slab_chunk_launches = 0;
@@ -285,12 +299,12 @@ struct npsd_b200_ctx {
     SchedBufs sch_down0;        // 64 x 8 tile columns, plane-pair units, window dilation (k_down_l0)
     bool x1_clean = false;      // L1.x is zero outside sch_down0's units
     // level-0 window-pattern dictionary (setup.cuh)
-    unsigned long long *dkeys = nullptr, *dskeys = nullptr;
-    uint32_t *dvals = nullptr, *dsidx = nullptr, *dhead = nullptr, *dscan = nullptr;
+    unsigned long long* dkeys = nullptr;
+    uint32_t* dvals = nullptr;
     uint32_t *pid0 = nullptr, *repcell0 = nullptr, *npat0 = nullptr;
     // level-0 mixed sublists the solve reads (mixed.cuh): windows holding fluid
     // (down) and fluid cells (up), with their pattern ids
-    uint32_t *crep = nullptr, *cnpat = nullptr, *cflag = nullptr;  // coarse dictionaries (scratch)
+    uint32_t *crep = nullptr, *cnpat = nullptr;  // coarse dictionaries (scratch)
     uint32_t *dlist0 = nullptr, *dkid0 = nullptr, *dcnt0 = nullptr;
     uint32_t *ulist0 = nullptr, *ukid0 = nullptr, *ucnt0 = nullptr;
     int tf_ntx = 0, tf_nty = 0;
@@ -304,8 +318,6 @@ struct npsd_b200_ctx {
     SolverState* st_host = nullptr;  // pinned
     double* partials = nullptr;
     unsigned int* counter = nullptr;
-    double* partials2 = nullptr;      // grid_reduce2: group partials
-    unsigned int* counters2 = nullptr;  // grid_reduce2: [final, per-group]
     double *hist = nullptr, *times = nullptr;
     long long hist_cap = 0;
     double *hist_host = nullptr, *times_host = nullptr;
@@ -373,6 +385,24 @@ int grid_for(npsd_b200_ctx* c, K kernel, long long items) {
         auto kfn_ = kernel;                                                  \
         const int g_ = grid_for(c, kfn_, (items));                          \
         kfn_<<<g_, kBlock, 0, (stream)>>>(__VA_ARGS__);                      \
+        CK(cudaGetLastError());                                              \
+        ++(c)->launches;                                                     \
+    } while (0)
+
+// Launch of a tiled kernel on an explicit 3D grid.
+#define LAUNCH3(c, stream, kernel, grid, block, ...)                         \
+    do {                                                                     \
+        auto kfn_ = kernel;                                                  \
+        kfn_<<<(grid), (block), 0, (stream)>>>(__VA_ARGS__);                 \
+        CK(cudaGetLastError());                                              \
+        ++(c)->launches;                                                     \
+    } while (0)
+
+// Launch with dynamic shared memory.
+#define LAUNCH3S(c, stream, kernel, grid, block, smem, ...)                  \
+    do {                                                                     \
+        auto kfn_ = kernel;                                                  \
+        kfn_<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
         CK(cudaGetLastError());                                              \
         ++(c)->launches;                                                     \
     } while (0)
@@ -500,11 +530,11 @@ void upload_params_and_kconst(npsd_b200_ctx* c) {
 
 ConvTab tab_down(const npsd_b200_ctx* c, int l) {
     const LevelBufs& L = c->L[l];
-    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_down, (l == 0) ? c->pid0 : L.kid, L.kc_down, L.rcode};
+    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_down, (l == 0) ? c->pid0 : nullptr, L.kc_down, L.rcode};
 }
 ConvTab tab_up(const npsd_b200_ctx* c, int l) {
     const LevelBufs& L = c->L[l];
-    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_up, (l == 0) ? c->pid0 : L.kid, L.kc_up, L.rcode};
+    return ConvTab{L.cls, L.mmask, L.mbase, L.tab_up, (l == 0) ? c->pid0 : nullptr, L.kc_up, L.rcode};
 }
 
 // ---------------------------------------------------------------- set_mask
@@ -561,78 +591,31 @@ int wave_blocks(npsd_b200_ctx* c, K kernel, int threads, size_t smem) {
     return c->num_sms * occ;
 }
 
-// Hashed window-pattern dictionary of coarse level l (setup.cuh): L.pid[mixed
-// index] = pattern, c->crep / c->cnpat = representative cells. Returns false
-// (per-cell rows) when any window differs from its pattern's representative.
-// Pattern ids of n keys (c->dkeys) by the hash table (setup.cuh k_dedup_*):
-// pid[i], rep[pattern] = its representative (list[i] of the inserting i), *npat.
-// The table (htk / htv, grow-only) holds > 2n slots; slots per key go to dvals.
-void dedup_patterns(npsd_b200_ctx* c, cudaStream_t s, uint32_t n, const uint32_t* count, const uint32_t* list,
+// Pattern ids of level l's mixed cells (keys in c->dkeys) by the hash table
+// (setup.cuh k_dedup_*): pid[i], rep[pattern] = its representative, *npat.
+// The table's level-l capacity (c->cap_ht[l] slots, a power of two) is sized
+// from earlier frames; more than half full raises a flag instead of probing
+// (the host redoes the frame, setup_sync).
+void dedup_patterns(npsd_b200_ctx* c, cudaStream_t s, int l, const uint32_t* count, const uint32_t* list,
                     uint32_t* pid, uint32_t* rep, uint32_t* npat) {
-    // capacity > 2n: the table never holds more than n distinct keys, so probing ends
-    unsigned long long cap = 1;
-    while (cap < 2ull * n + 2) cap <<= 1;
-    if (cap > c->ht_cap) {  // grow only
-        if (c->htk) CK(cudaFree(c->htk));
-        if (c->htv) CK(cudaFree(c->htv));
-        c->htk = dalloc<unsigned long long>((size_t)cap);
-        c->htv = dalloc<uint32_t>((size_t)cap);
-        c->ht_cap = cap;
-    }
+    const unsigned long long cap = c->cap_ht[l];
+    const long long items = std::min<long long>(c->L[l].g.n, (long long)cap);
     CK(cudaMemsetAsync(c->htk, 0xff, cap * sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(npat, 0, sizeof(uint32_t), s));
-    LAUNCH(c, s, k_dedup_insert, (long long)n, c->dkeys, count, list, c->htk, c->htv, cap - 1, c->dvals, rep, npat);
-    LAUNCH(c, s, k_dedup_ids, (long long)n, c->dvals, count, c->htv, pid);
+    LAUNCH(c, s, k_dedup_insert, items, c->dkeys, count, list, c->htk, c->htv, cap - 1, c->dvals, rep, npat,
+           &c->d_info->flags, 1u << (2 * l));
+    LAUNCH(c, s, k_dedup_ids, items, c->dvals, count, c->htv, cap - 1, (uint32_t)c->tab_cap[l], pid);
 }
 
+// Every launch of a frame's setup, in stream order, with no host
+// synchronisation and no host decision on device data (graph-capturable):
+// sizes come from the device (counts), capacities from earlier frames.
 template <int D>
-bool coarse_dictionary(npsd_b200_ctx* c, int l, uint32_t n) {
-    cudaStream_t s = c->s;
-    LevelBufs& L = c->L[l];
-    LAUNCH(c, s, k_window_hash<D>, (long long)n, L.g, L.img, L.mlist, L.mcnt, c->dkeys, c->dvals);
-    if (!c->dict_sort) {
-        dedup_patterns(c, s, n, L.mcnt, L.mlist, L.pid, c->crep, c->cnpat);
-        CK(cudaMemsetAsync(c->cflag, 0, sizeof(uint32_t), s));
-        LAUNCH(c, s, k_verify_windows<D>, (long long)n, L.g, L.img, L.mlist, L.mcnt, L.pid, c->crep, c->cflag);
-        uint32_t bad = 1;
-        CK(cudaMemcpyAsync(&bad, c->cflag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        return bad == 0;
-    }
-    size_t bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n, 0, 64, s));
-    if (bytes > c->cub_bytes) {
-        if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
-        CK(cudaMalloc(&c->cub_tmp, bytes));
-        c->cub_bytes = bytes;
-    }
-    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n, 0, 64, s));
-    c->launches += 4;
-    LAUNCH(c, s, k_run_heads, (long long)n, c->dskeys, L.mcnt, c->dhead);
-    bytes = 0;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, c->dhead, c->dscan, (int)n, s));
-    if (bytes > c->cub_bytes) {
-        if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
-        CK(cudaMalloc(&c->cub_tmp, bytes));
-        c->cub_bytes = bytes;
-    }
-    CK(cub::DeviceScan::InclusiveSum(c->cub_tmp, bytes, c->dhead, c->dscan, (int)n, s));
-    c->launches += 2;
-    LAUNCH(c, s, k_pattern_ids, (long long)n, c->dsidx, c->dscan, c->dhead, L.mlist, L.mcnt, L.pid, c->crep,
-           c->cnpat);
-    CK(cudaMemsetAsync(c->cflag, 0, sizeof(uint32_t), s));
-    LAUNCH(c, s, k_verify_windows<D>, (long long)n, L.g, L.img, L.mlist, L.mcnt, L.pid, c->crep, c->cflag);
-    uint32_t bad = 1;
-    CK(cudaMemcpyAsync(&bad, c->cflag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return bad == 0;
-}
-
-template <int D>
-void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
+void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
     cudaStream_t s = c->s;
     LevelBufs& L0 = c->L[0];
     constexpr int NCW = (D == 3) ? 27 : 9;
+    CK(cudaMemsetAsync(c->d_info, 0, sizeof(SetupInfo), s));
     // window counts of the linear blocks, levels l < depth - 1 (k_zfinal below)
     for (int l = 0; l + 1 < c->depth; ++l) CK(cudaMemsetAsync(c->L[l].zG, 0, 3 * NCW * sizeof(unsigned long long), s));
     const bool march0 = D == 3 && c->g0.nx % 32 == 0 && c->depth - 1 <= kMaxDepth - 1;
@@ -647,10 +630,8 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         za.nyg = c->gglob[0].ny;
         za.nzg = c->gglob[0].nz;
         const dim3 grid(c->g0.nx / 32, (c->g0.ny + 7) / 8, (c->g0.nz + ZC - 1) / ZC);
-        k_classify_march<ZC, true><<<grid, dim3(32, 8), 0, s>>>(c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask,
-                                                                c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za);
-        CK(cudaGetLastError());
-        ++c->launches;
+        LAUNCH3(c, s, (k_classify_march<ZC, true>), grid, dim3(32, 8), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount,
+                c->fmask, c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za);
     } else {
         LAUNCH(c, s, k_setup_l0<D>, c->g0.n, c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
         LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
@@ -658,10 +639,10 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     }
     scan_u32(c, L0.mcount, L0.mbase, L0.nseg);
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
+    LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), c->fbase, c->fcount, L0.nseg, &c->d_info->n_fluid);
     build_sched(c, c->sch_stencil, kTX, kTY, 1, 0, c->sched_gx, c->sched_gy);
     if (kMarchSY != kSY) build_sched(c, c->sch_march, kTX, kMarchSY, 1, 0, c->sched_gx, c->sched_gy);
     if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1, c->sched0_gx, c->sched0_gy);
-    c->x1_clean = false;
     for (int l = 1; l < c->depth; ++l) {
         LevelBufs& Lf = c->L[l - 1];
         LevelBufs& Lc = c->L[l];
@@ -681,10 +662,8 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
         if (marchc) {
             constexpr int ZC = 8;
             const dim3 grid(Lc.g.nx / 32, (Lc.g.ny + 7) / 8, (Lc.g.nz + ZC - 1) / ZC);
-            k_classify_march<ZC, false><<<grid, dim3(32, 8), 0, s>>>(Lc.g, pure, Lc.cls, Lc.mmask, Lc.mcount, nullptr,
-                                                                     nullptr, 0, 0, nullptr, ZsumArgs{});
-            CK(cudaGetLastError());
-            ++c->launches;
+            LAUNCH3(c, s, (k_classify_march<ZC, false>), grid, dim3(32, 8), Lc.g, (const uint8_t*)pure, Lc.cls,
+                    Lc.mmask, Lc.mcount, (uint32_t*)nullptr, (uint32_t*)nullptr, 0, 0, (uint8_t*)nullptr, ZsumArgs{});
         } else {
             LAUNCH(c, s, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
         }
@@ -694,123 +673,67 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     for (int l = 0; l < c->depth; ++l) {
         LevelBufs& L = c->L[l];
         LAUNCH(c, s, k_mixed_list, L.g.n, L.g, L.cls, L.mmask, L.mbase, L.mlist);
-        k_seg_total<<<1, 32, 0, s>>>(L.mbase, L.mcount, L.nseg, L.mcnt);
-        CK(cudaGetLastError());
-        ++c->launches;
+        LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), L.mbase, L.mcount, L.nseg, L.mcnt);
+        CK(cudaMemcpyAsync(&c->d_info->n_mixed[l], L.mcnt, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     }
-    // mixed counts of every level (host: sort sizes)
-    uint32_t n_mixed[kMaxDepth] = {};
-    for (int l = 0; l < c->depth; ++l)
-        CK(cudaMemcpyAsync(&n_mixed[l], c->L[l].mcnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    // level 0: window-pattern dictionary (pid per mixed cell, one row per pattern)
-    const uint32_t n_mixed0 = n_mixed[0];
-    if (n_mixed0 > 0) {
-        LAUNCH(c, s, k_window_keys<D>, (long long)n_mixed0, c->g0, dtypes, L0.mlist, L0.mcnt, c->dkeys, c->dvals);
-        if (!c->dict_sort) {
-            dedup_patterns(c, s, n_mixed0, L0.mcnt, L0.mlist, c->pid0, c->repcell0, c->npat0);
-        } else {
-        size_t bytes = 0;
-        const int nbits = 2 * Sh<D>::S;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n_mixed0, 0,
-                                           nbits, s));
-        if (bytes > c->cub_bytes) {
-            if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
-            CK(cudaMalloc(&c->cub_tmp, bytes));
-            c->cub_bytes = bytes;
-        }
-        CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->dkeys, c->dskeys, c->dvals, c->dsidx, (int)n_mixed0,
-                                           0, nbits, s));
-        c->launches += 4;  // cub onesweep: histogram + passes (approximate)
-        LAUNCH(c, s, k_run_heads, (long long)n_mixed0, c->dskeys, L0.mcnt, c->dhead);
-        bytes = 0;
-        CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, c->dhead, c->dscan, (int)n_mixed0, s));
-        if (bytes > c->cub_bytes) {
-            if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
-            CK(cudaMalloc(&c->cub_tmp, bytes));
-            c->cub_bytes = bytes;
-        }
-        CK(cub::DeviceScan::InclusiveSum(c->cub_tmp, bytes, c->dhead, c->dscan, (int)n_mixed0, s));
-        c->launches += 2;
-        LAUNCH(c, s, k_pattern_ids, (long long)n_mixed0, c->dsidx, c->dscan, c->dhead, L0.mlist, L0.mcnt, c->pid0,
-               c->repcell0, c->npat0);
-        }
-        // split into the solve's down/up sublists (dictionary scratch reused)
-        uint32_t *fd = c->dvals, *fu = c->dsidx, *sd = c->dhead, *su = c->dscan;
-        LAUNCH(c, s, k_mixed_flags, (long long)n_mixed0, L0.mlist, L0.mcnt, L0.cls, fd, fu);
-        scan_u32(c, fd, sd, (long long)n_mixed0);
-        scan_u32(c, fu, su, (long long)n_mixed0);
-        LAUNCH(c, s, k_mixed_split, (long long)n_mixed0, L0.mlist, c->pid0, L0.mcnt, fd, sd, fu, su, c->dlist0,
-               c->dkid0, c->ulist0, c->ukid0);
-        k_seg_total<<<1, 32, 0, s>>>(sd, fd, (long long)n_mixed0, c->dcnt0);
-        k_seg_total<<<1, 32, 0, s>>>(su, fu, (long long)n_mixed0, c->ucnt0);
-        CK(cudaGetLastError());
-        c->launches += 2;
-    } else {
-        CK(cudaMemsetAsync(c->npat0, 0, sizeof(uint32_t), s));
-        CK(cudaMemsetAsync(c->dcnt0, 0, sizeof(uint32_t), s));
-        CK(cudaMemsetAsync(c->ucnt0, 0, sizeof(uint32_t), s));
-    }
-    // kernel-row tables: at most one row per mixed cell (grow only)
-    for (int l = 0; l < c->depth; ++l) {
-        LevelBufs& L = c->L[l];
-        const long long need = std::max<long long>(n_mixed[l], 1);
-        if (need > c->tab_cap[l]) {
-            const long long cap = need + need / 4;
-            CK(cudaFree(L.tab_down));
-            L.tab_down = dalloc<float>((size_t)kRowW * cap);
-            if (L.tab_up) {
-                CK(cudaFree(L.tab_up));
-                L.tab_up = dalloc<float>((size_t)kRowW * cap);
-            }
-            c->tab_cap[l] = cap;
-            ++c->buf_gen;
-        }
-    }
+    // level 0: window-pattern dictionary (pid per mixed cell, one row per pattern),
+    // then the solve's down / up sublists with their pattern ids
+    LAUNCH(c, s, k_window_keys<D>, std::min<long long>(c->g0.n, (long long)c->cap_ht[0]), c->g0, dtypes, L0.mlist,
+           L0.mcnt, c->dkeys, c->dvals);
+    dedup_patterns(c, s, 0, L0.mcnt, L0.mlist, c->pid0, c->repcell0, c->npat0);
+    CK(cudaMemcpyAsync(&c->d_info->npat[0], c->npat0, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    LAUNCH(c, s, k_sub_masks, L0.g.n, L0.g, L0.cls, c->dmask, c->dcount, c->umask, c->ucount);
+    scan_u32(c, c->dcount, c->dbase, L0.nseg);
+    scan_u32(c, c->ucount, c->ubase, L0.nseg);
+    LAUNCH(c, s, k_mixed_sub, std::min<long long>(c->g0.n, (long long)c->cap_ht[0]), L0.mlist, c->pid0, L0.mcnt,
+           c->dmask, c->dbase, c->umask, c->ubase, c->dlist0, c->dkid0, c->ulist0, c->ukid0);
+    LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), c->dbase, c->dcount, L0.nseg, c->dcnt0);
+    LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), c->ubase, c->ucount, L0.nseg, c->ucnt0);
     for (int l = 0; l < c->depth; ++l) {
         LevelBufs& L = c->L[l];
         const uint8_t* st = (l == 0) ? dtypes : nullptr;
         const float* im = (l == 0) ? nullptr : L.img;
+        const uint32_t rows_cap = (uint32_t)c->tab_cap[l];
+        const uint32_t rows_bit = 1u << (2 * l + 1);
         // rows: one per window pattern (level 0 always; above when the hashed
         // dictionary verifies), else one per mixed cell
-        const uint32_t* cells = (l == 0) ? c->repcell0 : L.mlist;
-        const uint32_t* ncells = (l == 0) ? c->npat0 : L.mcnt;
-        long long rows_cap = (l == 0) ? (long long)n_mixed0 : L.g.n;
+        const uint32_t* cells = (l == 0) ? c->repcell0 : c->crep;
+        const uint32_t* ncells = (l == 0) ? c->npat0 : c->cnpat;
+        const uint32_t* unver = (l == 0) ? nullptr : &c->d_info->unverified[l];
         if (l > 0) {
-            const uint32_t* kid_before = L.kid;
-            L.kid = nullptr;
-            if (n_mixed[l] > 0 && coarse_dictionary<D>(c, l, n_mixed[l])) {
-                L.kid = L.pid;
-                cells = c->crep;
-                ncells = c->cnpat;
-                rows_cap = n_mixed[l];
-            }
-            if (L.kid != kid_before) ++c->buf_gen;  // captured graphs hold kid by value (ConvTab)
-            LAUNCH(c, s, k_row_codes, L.g.n, L.g, L.cls, L.mmask, L.mbase, L.kid, L.rcode);
+            const long long items = std::min<long long>(L.g.n, (long long)c->cap_ht[l]);
+            LAUNCH(c, s, k_window_hash<D>, items, L.g, L.img, L.mlist, L.mcnt, c->dkeys, c->dvals);
+            dedup_patterns(c, s, l, L.mcnt, L.mlist, L.pid, c->crep, c->cnpat);
+            CK(cudaMemcpyAsync(&c->d_info->npat[l], c->cnpat, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+            LAUNCH(c, s, k_verify_windows<D>, items, L.g, L.img, L.mlist, L.mcnt, L.pid, c->crep,
+                   &c->d_info->unverified[l]);
+            LAUNCH(c, s, k_row_codes, L.g.n, L.g, L.cls, L.mmask, L.mbase, L.pid, (const uint32_t*)unver, rows_cap,
+                   L.rcode);
         }
+        const long long row_items = 32LL * std::min<long long>(rows_cap, L.g.n);
         if (l < c->depth - 1) {
             const LevelOffsets& o = c->offs[(size_t)l];
-            LAUNCH(c, s, k_build_rows<D>, rows_cap * 32, L.g, st, im, cells, ncells, c->d_params + o.down_W,
+            LAUNCH(c, s, k_build_rows<D>, row_items, L.g, st, im, cells, ncells, (const uint32_t*)L.mlist,
+                   (const uint32_t*)L.mcnt, unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + o.down_W,
                    c->d_params + o.down_B, L.tab_down);
-            LAUNCH(c, s, k_build_rows<D>, rows_cap * 32, L.g, st, im, cells, ncells, c->d_params + o.up_W,
+            LAUNCH(c, s, k_build_rows<D>, row_items, L.g, st, im, cells, ncells, (const uint32_t*)L.mlist,
+                   (const uint32_t*)L.mcnt, unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + o.up_W,
                    c->d_params + o.up_B, L.tab_up);
             constexpr int NC = (D == 3) ? 27 : 9;
             const double scale = std::ldexp(1.0, D * l);
             if (!march0) {
                 const int nrows = L.g.ny * (L.g.zo1 - L.g.zo0);
                 const int blocks = std::max(1, std::min(nrows, 8 * c->num_sms));
-                k_zsums_rows<D><<<blocks, kBlock, 0, s>>>(L.g, st, im, (float)scale, zg_offset(c, l), c->gglob[l].nz,
-                                                          L.zG);
-                CK(cudaGetLastError());
-                ++c->launches;
+                LAUNCH3(c, s, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), L.g, st, im, (float)scale, zg_offset(c, l),
+                        c->gglob[l].nz, L.zG);
             }
             if (c->slab.on) slab_allreduce_u64(c, s, L.zG, 3 * NC);
-            k_zfinal<D><<<1, 128, 0, s>>>(c->gglob[l], L.zG, scale, c->d_params + o.a_K, c->params[o.a_bias],
-                                         c->d_params + o.b_K, c->params[o.b_bias], c->zab + 2 * l, c->zab + 2 * l + 1);
-            CK(cudaGetLastError());
-            ++c->launches;
+            LAUNCH3(c, s, k_zfinal<D>, dim3(1), dim3(128), c->gglob[l], (const unsigned long long*)L.zG, scale,
+                    c->d_params + o.a_K, c->params[o.a_bias], c->d_params + o.b_K, c->params[o.b_bias], c->zab + 2 * l,
+                    c->zab + 2 * l + 1);
         } else {
-            LAUNCH(c, s, k_build_rows<D>, rows_cap * 32, L.g, st, im, cells, ncells, c->d_params + c->coarse_W,
+            LAUNCH(c, s, k_build_rows<D>, row_items, L.g, st, im, cells, ncells, (const uint32_t*)L.mlist,
+                   (const uint32_t*)L.mcnt, unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + c->coarse_W,
                    c->d_params + c->coarse_B, L.tab_down);
         }
     }
@@ -820,13 +743,147 @@ void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
     CK(cudaMemsetAsync(c->R, 0, nb, s));
     CK(cudaMemsetAsync(c->Dtmp, 0, nb, s));
     CK(cudaMemsetAsync(c->Dring, 0, nb * (size_t)c->ring_alloc, s));
-    // n_fluid = last base + last count
-    uint32_t tail[2];
-    CK(cudaMemcpyAsync(&tail[0], c->fbase + (L0.nseg - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&tail[1], c->fcount + (L0.nseg - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    c->n_fluid = (long long)tail[0] + tail[1];
+    if (c->slab.on) {  // the ranks redo a frame together
+        unsigned long long* v = reinterpret_cast<unsigned long long*>(c->red_b);
+        LAUNCH3(c, s, k_flags_u64, dim3(1), dim3(32), (const uint32_t*)&c->d_info->flags, v);
+        slab_allreduce_u64(c, s, v, 1);
+        LAUNCH3(c, s, k_u64_flags, dim3(1), dim3(32), (const unsigned long long*)v, &c->d_info->flags);
+    }
+}
+
+// cub scratch for every scan set_mask runs (allocated outside any capture)
+void ensure_cub(npsd_b200_ctx* c) {
+    long long nmax = c->L[0].nseg;
+    for (const SchedBufs* sb : {&c->sch_stencil, &c->sch_march, &c->sch_down0}) nmax = std::max<long long>(nmax, sb->npiece);
+    // the schedules' piece counts (build_sched allocates them on first use): bounded by the tile columns
+    nmax = std::max<long long>(nmax, (long long)((c->g0.nx + kTX - 1) / kTX) * ((c->g0.ny + kTY - 1) / kTY) + 1);
+    size_t bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)nmax, c->s));
+    if (bytes > c->cub_bytes) {
+        if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
+        CK(cudaMalloc(&c->cub_tmp, bytes));
+        c->cub_bytes = bytes;
+    }
+}
+
+// kernel-row tables (rows per level) and the pattern hash table at the
+// current capacities (grow only; the captured setup graph holds the pointers)
+void ensure_setup_capacity(npsd_b200_ctx* c) {
+    for (int l = 0; l < c->depth; ++l) {
+        LevelBufs& L = c->L[l];
+        if (c->tab_alloc[l] < c->tab_cap[l]) {
+            const size_t rows = (size_t)c->tab_cap[l];
+            if (L.tab_down) CK(cudaFree(L.tab_down));
+            L.tab_down = dalloc<float>((size_t)kRowW * rows);
+            if (l < c->depth - 1) {
+                if (L.tab_up) CK(cudaFree(L.tab_up));
+                L.tab_up = dalloc<float>((size_t)kRowW * rows);
+            }
+            c->tab_alloc[l] = c->tab_cap[l];
+            ++c->buf_gen;
+        }
+    }
+    unsigned long long ht = 0;
+    for (int l = 0; l < c->depth; ++l) ht = std::max(ht, c->cap_ht[l]);
+    if (ht > c->ht_alloc) {
+        if (c->htk) CK(cudaFree(c->htk));
+        if (c->htv) CK(cudaFree(c->htv));
+        c->htk = dalloc<unsigned long long>((size_t)ht);
+        c->htv = dalloc<uint32_t>((size_t)ht);
+        c->ht_alloc = ht;
+        ++c->buf_gen;
+    }
+}
+
+// One frame's setup from device cell types: the launches of set_mask_enqueue,
+// replayed as one captured graph per context (z-slab contexts: eager, their
+// exchanges run through the communicator), then an asynchronous readback of
+// the frame's SetupInfo. Nothing here waits for the device.
+template <int D>
+void set_mask_run(npsd_b200_ctx* c, const uint8_t* dtypes) {
+    ensure_setup_capacity(c);
+    c->x1_clean = false;
+    const bool graph = !c->slab.on && c->mask_graph_ok && dtypes == c->types_dev;
+    if (graph) {
+        if (!c->mask_exec || c->mask_exec_gen != c->buf_gen) {
+            if (c->mask_exec) CK(cudaGraphExecDestroy(c->mask_exec));
+            c->mask_exec = nullptr;
+            ensure_cub(c);
+            // schedules allocate their buffers on first use: once outside the capture
+            if (!c->sch_stencil.pre) set_mask_enqueue<D>(c, dtypes);
+            const long long before = c->launches;
+            CK(cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
+            try {
+                set_mask_enqueue<D>(c, dtypes);
+            } catch (...) {
+                cudaGraph_t junk = nullptr;
+                cudaStreamEndCapture(c->s, &junk);
+                if (junk) cudaGraphDestroy(junk);
+                cudaGetLastError();
+                c->mask_graph_ok = false;  // eager from now on
+                c->launches = before;
+                set_mask_enqueue<D>(c, dtypes);
+                goto readback;
+            }
+            cudaGraph_t gr = nullptr;
+            CK(cudaStreamEndCapture(c->s, &gr));
+            const cudaError_t ie = cudaGraphInstantiate(&c->mask_exec, gr, 0);
+            cudaGraphDestroy(gr);
+            CK(ie);
+            c->mask_nodes = c->launches - before;
+            c->launches = before;
+            c->mask_exec_gen = c->buf_gen;
+        }
+        CK(cudaGraphLaunch(c->mask_exec, c->s));
+        c->launches += c->mask_nodes;
+    } else {
+        set_mask_enqueue<D>(c, dtypes);
+    }
+readback:
+    CK(cudaMemcpyAsync(c->info_host, c->d_info, sizeof(SetupInfo), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaEventRecord(c->ev_setup, c->s));
+    c->setup_pending = true;
     c->mask_ok = true;
+}
+
+// Finishes the last set_mask on the host: waits for its SetupInfo; when a
+// capacity was too small, grows it from the frame's counts and redoes the
+// frame (a few times at most: the first frames of a context). Returns true
+// when the frame was redone (device work queued before the call saw the
+// smaller tables and must be repeated).
+bool setup_sync(npsd_b200_ctx* c) {
+    if (!c->setup_pending) return false;
+    bool redone = false;
+    for (int attempt = 0;; ++attempt) {
+        CK(cudaEventSynchronize(c->ev_setup));
+        const SetupInfo& h = *c->info_host;
+        if (h.flags == 0) break;
+        require(attempt < 4, "npsd_b200: set_mask capacities did not converge");
+        for (int l = 0; l < c->depth; ++l) {
+            const unsigned long long want_ht = std::max<unsigned long long>(1024, 2ull * h.n_mixed[l] + h.n_mixed[l] / 2);
+            while (c->cap_ht[l] < want_ht) c->cap_ht[l] <<= 1;
+            const long long rows = std::max<long long>(
+                {(long long)h.npat[l], (l > 0 && h.unverified[l]) ? (long long)h.n_mixed[l] : 0LL, 1LL});
+            if (rows > c->tab_cap[l]) c->tab_cap[l] = rows + rows / 4 + 64;
+            if ((h.flags >> (2 * l)) & 1u) {  // the table was skipped: npat unknown, allow every mixed cell a row
+                c->tab_cap[l] = std::max<long long>(c->tab_cap[l], (long long)h.n_mixed[l] + 64);
+            }
+        }
+        if (c->dim == 3)
+            set_mask_run<3>(c, c->types_cur);
+        else
+            set_mask_run<2>(c, c->types_cur);
+        redone = true;
+    }
+    c->n_fluid = c->info_host->n_fluid;
+    c->setup_pending = false;
+    return redone;
+}
+
+template <int D>
+void set_mask_impl(npsd_b200_ctx* c, const uint8_t* dtypes) {
+    c->types_cur = dtypes;
+    set_mask_run<D>(c, dtypes);
 }
 
 // ------------------------------------------------------------ network
@@ -836,24 +893,6 @@ struct Step {
     std::string name;
     std::function<void(cudaStream_t)> run;
 };
-
-// Launch of a tiled kernel on an explicit 3D grid.
-#define LAUNCH3(c, stream, kernel, grid, block, ...)                         \
-    do {                                                                     \
-        auto kfn_ = kernel;                                                  \
-        kfn_<<<(grid), (block), 0, (stream)>>>(__VA_ARGS__);                 \
-        CK(cudaGetLastError());                                              \
-        ++(c)->launches;                                                     \
-    } while (0)
-
-// Launch with dynamic shared memory.
-#define LAUNCH3S(c, stream, kernel, grid, block, smem, ...)                  \
-    do {                                                                     \
-        auto kfn_ = kernel;                                                  \
-        kfn_<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
-        CK(cudaGetLastError());                                              \
-        ++(c)->launches;                                                     \
-    } while (0)
 
 // Launch of an iteration kernel (one that starts with pdl_launch_wait()) with
 // programmatic stream serialisation: its blocks may launch while the previous
@@ -1228,18 +1267,18 @@ std::vector<Step> prologue_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h,
     // projections (solver.cpp:197-201), r0 = b - A x0, ||r0||
     if (nullspace) {
         v.push_back({"proj_b_sum", [=](cudaStream_t s) {
-                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->Bf, c->n_fluid, c->st, c->partials, c->counter);
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->Bf, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
                      }});
         v.push_back({"proj_b_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->Bf, c->st); }});
         v.push_back({"proj_x_sum", [=](cudaStream_t s) {
-                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->X0, c->n_fluid, c->st, c->partials, c->counter);
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->X0, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
                      }});
         v.push_back({"proj_x_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->X0, c->st); }});
     }
     v.push_back({"residual0", [=](cudaStream_t s) { LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R); }});
     if (nullspace) {
         v.push_back({"proj_r0_sum", [=](cudaStream_t s) {
-                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, c->n_fluid, c->st, c->partials, c->counter);
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
                      }});
         v.push_back({"proj_r0_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->R, c->st); }});
     }
@@ -1259,7 +1298,7 @@ std::vector<Step> body_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h, int
     v.push_back({"update", [=](cudaStream_t s) { launch_update<D>(c, s, h, use_cond, nullspace ? 0 : 1); }});
     if (nullspace) {
         v.push_back({"proj_r_sum", [=](cudaStream_t s) {
-                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, c->n_fluid, c->st, c->partials, c->counter);
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
                      }});
         v.push_back({"proj_r_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->R, c->st); }});
         v.push_back({"norm", [=](cudaStream_t s) {
@@ -1431,7 +1470,7 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
 // rank-ordered totals, subtract
 void slab_project(npsd_b200_ctx* c, cudaStream_t s, double* v) {
     const Geom g = c->g0;
-    LAUNCH(c, s, k_fluid_sum, g.n, g, c->L[0].cls, v, c->n_fluid, c->st, c->partials, c->counter);
+    LAUNCH(c, s, k_fluid_sum, g.n, g, c->L[0].cls, v, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
     slab_reduce(c, s, kFinMean);
     LAUNCH(c, s, k_subtract_mean, g.n, g, c->L[0].cls, v, c->st);
 }
@@ -1700,7 +1739,7 @@ void capture_cg_graph(npsd_b200_ctx* c, int ns) {
     CK(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
     // mean_project(v) (vector_ops.cpp:33-43) as two kernels
     auto project = [&](cudaStream_t st, double* v) {
-        LAUNCH(c, st, k_fluid_sum, g.n, g, cls, v, c->n_fluid, c->st, c->partials, c->counter);
+        LAUNCH(c, st, k_fluid_sum, g.n, g, cls, v, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
         LAUNCH(c, st, k_subtract_mean, g.n, g, cls, v, c->st);
     };
     // prologue (solver.cpp:38-58): [projections of b, x0], r0 = b - A x0,
@@ -1874,8 +1913,36 @@ int guarded(npsd_b200_ctx* c, Fn&& fn) {
     }
 }
 
-void check_mask(const npsd_b200_ctx* c) {
+// host API calls that need the frame's sizes: the last set_mask finished
+void check_mask(npsd_b200_ctx* c) {
     require(c->mask_ok, "npsd_b200: set_mask has not been called");
+    setup_sync(c);
+}
+
+// device-resident calls: the frame may still be in flight (setup_sync after)
+void check_mask_async(const npsd_b200_ctx* c) {
+    require(c->mask_ok, "npsd_b200: set_mask has not been called");
+}
+
+// A device-resident call after an asynchronous set_mask: run it, then finish
+// the set_mask; when the frame had to be redone with larger tables, run it
+// again (the first run saw the smaller tables; it may even have failed).
+// The reference's EmptySystemError comes last, from the frame's sizes.
+template <typename Fn>
+void run_after_setup(npsd_b200_ctx* c, Fn&& fn) {
+    const bool pending = c->setup_pending;
+    bool again = false;
+    try {
+        fn();
+    } catch (const InvalidArgument&) {
+        throw;
+    } catch (...) {
+        if (!(pending && setup_sync(c))) throw;
+        again = true;
+    }
+    if (!again && setup_sync(c)) again = true;
+    if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
+    if (again) fn();
 }
 
 void free_ctx(npsd_b200_ctx* c) {
@@ -1937,11 +2004,15 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->fbase);
     F(c->fcount);
     F(c->tflags);
-    for (void* p : {(void*)c->dkeys, (void*)c->dskeys, (void*)c->dvals, (void*)c->dsidx, (void*)c->dhead,
-                    (void*)c->dscan, (void*)c->pid0, (void*)c->repcell0, (void*)c->npat0,
+    for (void* p : {(void*)c->dkeys, (void*)c->dvals, (void*)c->pid0, (void*)c->repcell0, (void*)c->npat0,
                     (void*)c->dlist0, (void*)c->dkid0, (void*)c->dcnt0, (void*)c->ulist0, (void*)c->ukid0,
-                    (void*)c->ucnt0, (void*)c->crep, (void*)c->cnpat, (void*)c->cflag})
+                    (void*)c->ucnt0, (void*)c->crep, (void*)c->cnpat, (void*)c->dmask, (void*)c->dcount,
+                    (void*)c->dbase, (void*)c->umask, (void*)c->ucount, (void*)c->ubase, (void*)c->d_info,
+                    (void*)c->types_dev})
         F(p);
+    if (c->info_host) cudaFreeHost(c->info_host);
+    if (c->ev_setup) cudaEventDestroy(c->ev_setup);
+    if (c->mask_exec) cudaGraphExecDestroy(c->mask_exec);
     F(c->X0);
     F(c->X1);
     F(c->R);
@@ -1951,8 +2022,6 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->ADring);
     F(c->st);
     F(c->partials);
-    F(c->partials2);
-    F(c->counters2);
     F(c->counter);
     F(c->hist);
     F(c->times);
@@ -2016,7 +2085,6 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->S = (dim == 3) ? 27 : 9;
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
-        if (const char* e = std::getenv("NPSD_DICT_SORT")) c->dict_sort = (e[0] == '1');
         auto env_int = [](const char* n, int& v) {
             if (const char* e = std::getenv(n)) {
                 const int x = std::atoi(e);
@@ -2094,10 +2162,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
             L.mbase = dalloc<uint32_t>((size_t)L.nseg);
             L.mcount = dalloc<uint32_t>((size_t)L.nseg);
             if (l > 0) L.img = dalloc<float>(3 * (size_t)L.g.n);
-            // kernel-row tables grow with the frame's mixed-cell count (set_mask)
-            L.tab_down = dalloc<float>((size_t)kRowW);
-            if (l < depth - 1) L.tab_up = dalloc<float>((size_t)kRowW);
-            c->tab_cap[l] = 1;
+            // kernel-row tables: allocated at the capacities set_mask uses (ensure_setup_capacity)
             L.mlist = dalloc<uint32_t>((size_t)L.g.n);
             if (l > 0) L.pid = dalloc<uint32_t>((size_t)L.g.n);
             L.mcnt = dalloc<uint32_t>(1);
@@ -2141,11 +2206,18 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         // every local plane: a z-slab's ghost planes are flagged too (k_classify_march, k_tile_flags)
         c->tflags = dalloc<uint8_t>((size_t)c->tf_ntx * c->tf_nty * c->L[0].g.nz);
         c->dkeys = dalloc<unsigned long long>((size_t)c->g0.n);
-        c->dskeys = dalloc<unsigned long long>((size_t)c->g0.n);
         c->dvals = dalloc<uint32_t>((size_t)c->g0.n);
-        c->dsidx = dalloc<uint32_t>((size_t)c->g0.n);
-        c->dhead = dalloc<uint32_t>((size_t)c->g0.n);
-        c->dscan = dalloc<uint32_t>((size_t)c->g0.n);
+        for (uint32_t** v : {&c->dmask, &c->dcount, &c->dbase, &c->umask, &c->ucount, &c->ubase})
+            *v = dalloc<uint32_t>((size_t)nseg0);
+        c->d_info = dalloc<SetupInfo>(1);
+        CK(cudaMallocHost(&c->info_host, sizeof(SetupInfo)));
+        CK(cudaEventCreateWithFlags(&c->ev_setup, cudaEventDisableTiming));
+        c->types_dev = dalloc<uint8_t>((size_t)c->g0.n);
+        // first capacities of the per-frame tables; setup_sync grows them from a frame's counts
+        for (int l = 0; l < depth; ++l) {
+            c->cap_ht[l] = 1 << 14;
+            c->tab_cap[l] = 4096;
+        }
         c->pid0 = dalloc<uint32_t>((size_t)c->g0.n);
         c->repcell0 = dalloc<uint32_t>((size_t)c->g0.n);
         c->dlist0 = dalloc<uint32_t>((size_t)c->g0.n);
@@ -2155,7 +2227,6 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->dcnt0 = dalloc<uint32_t>(1);
         c->crep = dalloc<uint32_t>((size_t)std::max<long long>(c->depth > 1 ? c->L[1].g.n : 1, 1));
         c->cnpat = dalloc<uint32_t>(1);
-        c->cflag = dalloc<uint32_t>(1);
         c->check_flag = dalloc<unsigned int>(1);
         c->ucnt0 = dalloc<uint32_t>(1);
         c->npat0 = dalloc<uint32_t>(1);
@@ -2175,11 +2246,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         {
             // the pair-stencil grids: one block per 64 x 4 x 1 tile
             const long long nblk = ((long long)(nx + 63) / 64) * ((ny + 3) / 4) * nz;
-            const long long ngrp = (nblk + 127) / 128;
             c->partials = dalloc<double>((size_t)std::max<long long>(65536, nblk) * (2 + kMaxOrtho));
-            c->partials2 = dalloc<double>((size_t)ngrp * (2 + kMaxOrtho));
-            c->counters2 = dalloc<unsigned int>((size_t)ngrp + 1);
-            CK(cudaMemset(c->counters2, 0, ((size_t)ngrp + 1) * sizeof(unsigned int)));
         }
         ensure_ring(c, 3);
         ensure_hist(c, 1001);
@@ -2339,11 +2406,13 @@ int npsd_b200_set_params(npsd_b200_ctx* c, const float* params, size_t n) {
 void slab_stage_types(npsd_b200_ctx* c, const uint8_t* types, cudaMemcpyKind kind) {
     const Geom& g = c->g0;
     const size_t plane = (size_t)g.nx * g.ny;
-    uint8_t* d = reinterpret_cast<uint8_t*>(c->red_a);
+    uint8_t* d = c->types_dev;
     CK(cudaMemsetAsync(d, 2, (size_t)g.n, c->s));
     CK(cudaMemcpyAsync(d + (size_t)g.zo0 * plane, types, (size_t)(g.zo1 - g.zo0) * plane, kind, c->s));
     slab_exchange(c, c->s, d, 1, 0);
     set_mask_impl<3>(c, d);
+    // finished here, on every rank at once: a redo (setup_sync) is collective
+    setup_sync(c);
 }
 
 int npsd_b200_set_mask_device(npsd_b200_ctx* c, const uint8_t* d_types) {
@@ -2353,10 +2422,13 @@ int npsd_b200_set_mask_device(npsd_b200_ctx* c, const uint8_t* d_types) {
             slab_stage_types(c, d_types, cudaMemcpyDeviceToDevice);
             return;
         }
+        // the frame's types into the context's buffer (the captured setup graph
+        // reads them there; the caller's buffer is free once this returns)
+        CK(cudaMemcpyAsync(c->types_dev, d_types, (size_t)c->g0.n, cudaMemcpyDeviceToDevice, c->s));
         if (c->dim == 3)
-            set_mask_impl<3>(c, d_types);
+            set_mask_impl<3>(c, c->types_dev);
         else
-            set_mask_impl<2>(c, d_types);
+            set_mask_impl<2>(c, c->types_dev);
     });
 }
 
@@ -2373,12 +2445,11 @@ int npsd_b200_set_mask(npsd_b200_ctx* c, const uint8_t* types) {
             slab_stage_types(c, chk, cudaMemcpyDeviceToDevice);
             return;
         }
-        uint8_t* d = reinterpret_cast<uint8_t*>(c->red_a);  // staging (n bytes <= 8n)
-        CK(cudaMemcpyAsync(d, chk, n, cudaMemcpyDeviceToDevice, c->s));
+        CK(cudaMemcpyAsync(c->types_dev, chk, n, cudaMemcpyDeviceToDevice, c->s));
         if (c->dim == 3)
-            set_mask_impl<3>(c, d);
+            set_mask_impl<3>(c, c->types_dev);
         else
-            set_mask_impl<2>(c, d);
+            set_mask_impl<2>(c, c->types_dev);
     });
 }
 
@@ -2404,7 +2475,12 @@ int npsd_b200_is_pure_neumann(npsd_b200_ctx* c, int* out) {
     });
 }
 
-int64_t npsd_b200_n_fluid(const npsd_b200_ctx* c) { return (c && c->mask_ok) ? c->n_fluid : -1; }
+int64_t npsd_b200_n_fluid(const npsd_b200_ctx* cc) {
+    // the last set_mask may still be in flight: finish it (the count is device-side)
+    auto* c = const_cast<npsd_b200_ctx*>(cc);
+    if (!c || !c->mask_ok) return -1;
+    return guarded(c, [&] { setup_sync(c); }) == NPSD_OK ? c->n_fluid : -1;
+}
 
 int npsd_b200_fluid_indices(npsd_b200_ctx* c, int64_t* out) {
     return guarded(c, [&] {
@@ -2683,31 +2759,33 @@ int npsd_b200_net_apply(npsd_b200_ctx* c, const float* x, float* y) {
 int npsd_b200_psdo_solve_device(npsd_b200_ctx* c, const double* d_b, const double* d_x0,
                                 const npsd_b200_solve_cfg* cfg, double* d_x, npsd_b200_report* rep) {
     return guarded(c, [&] {
-        check_mask(c);
+        check_mask_async(c);
         require(cfg != nullptr && d_b != nullptr && d_x != nullptr, "solve: null argument");
-        if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
-        const Geom g = c->g0;
-        const uint8_t* cls = c->L[0].cls;
-        // z-slab: caller buffers hold the owned planes only
-        const size_t off = (size_t)owned_lo(g), cnt = (size_t)(owned_hi(g) - owned_lo(g));
-        if (c->slab.on) {
-            CK(cudaMemcpyAsync(c->Bf + off, d_b, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
-            d_b = c->Bf;
-            if (d_x0) {
-                CK(cudaMemcpyAsync(c->X0 + off, d_x0, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
-                d_x0 = c->X0;
+        run_after_setup(c, [&] {
+            const Geom g = c->g0;
+            const uint8_t* cls = c->L[0].cls;
+            const double* b_in = d_b;
+            const double* x0_in = d_x0;
+            // z-slab: caller buffers hold the owned planes only
+            const size_t off = (size_t)owned_lo(g), cnt = (size_t)(owned_hi(g) - owned_lo(g));
+            if (c->slab.on) {
+                CK(cudaMemcpyAsync(c->Bf + off, d_b, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
+                b_in = c->Bf;
+                if (d_x0) {
+                    CK(cudaMemcpyAsync(c->X0 + off, d_x0, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
+                    x0_in = c->X0;
+                }
             }
-        }
-        LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_b, c->Bf);
-        if (d_x0)
-            LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_x0, c->X0);
-        else
-            CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
-        int st = solve_any(c, cfg, rep);
-        (void)st;
-        const double* xr = c->st_host->xcur ? c->X1 : c->X0;
-        CK(cudaMemcpyAsync(d_x, xr + off, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
-        CK(cudaStreamSynchronize(c->s));
+            LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, b_in, c->Bf);
+            if (x0_in)
+                LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, x0_in, c->X0);
+            else
+                CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
+            solve_any(c, cfg, rep);
+            const double* xr = c->st_host->xcur ? c->X1 : c->X0;
+            CK(cudaMemcpyAsync(d_x, xr + off, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
+            CK(cudaStreamSynchronize(c->s));
+        });
     });
 }
 
@@ -2784,19 +2862,21 @@ int npsd_b200_pcg_solve(npsd_b200_ctx* c, const double* b, const double* x0, con
 int npsd_b200_pcg_solve_device(npsd_b200_ctx* c, const double* d_b, const double* d_x0,
                                const npsd_b200_solve_cfg* cfg, int precond, double* d_x, npsd_b200_report* rep) {
     return guarded(c, [&] {
-        check_mask(c);
+        check_mask_async(c);
         require(cfg != nullptr && d_b != nullptr && d_x != nullptr, "solve: null argument");
-        if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
-        const Geom g = c->g0;
-        const uint8_t* cls = c->L[0].cls;
-        LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_b, c->Bf);
-        if (d_x0)
-            LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_x0, c->X0);
-        else
-            CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
-        pcg_solve_impl(c, cfg, precond, rep);
-        CK(cudaMemcpyAsync(d_x, c->X0, (size_t)g.n * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
-        CK(cudaStreamSynchronize(c->s));
+        if (precond == 2) setup_sync(c);  // the IC0 factor's diagonal shift uses the frame's size
+        run_after_setup(c, [&] {
+            const Geom g = c->g0;
+            const uint8_t* cls = c->L[0].cls;
+            LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_b, c->Bf);
+            if (d_x0)
+                LAUNCH(c, c->s, k_mask_fluid, g.n, g, cls, d_x0, c->X0);
+            else
+                CK(cudaMemsetAsync(c->X0, 0, (size_t)g.n * sizeof(double), c->s));
+            pcg_solve_impl(c, cfg, precond, rep);
+            CK(cudaMemcpyAsync(d_x, c->X0, (size_t)g.n * sizeof(double), cudaMemcpyDeviceToDevice, c->s));
+            CK(cudaStreamSynchronize(c->s));
+        });
     });
 }
 

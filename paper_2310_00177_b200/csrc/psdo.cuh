@@ -246,18 +246,19 @@ __device__ __forceinline__ void set_precond_scales(SolverState* st) {
 
 // mean over fluid cells (mean_project, vector_ops.cpp:33-43): pass 1 sums.
 __global__ void __launch_bounds__(kBlock) k_fluid_sum(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ v,
-                                                      long long n_fluid, SolverState* st, double* __restrict__ partials,
-                                                      unsigned int* __restrict__ counter) {
+                                                      const uint32_t* __restrict__ n_fluid_dev, SolverState* st,
+                                                      double* __restrict__ partials, unsigned int* __restrict__ counter) {
     if (st->dist && st->done) return;  // chunked z-slab loop after convergence
     double acc[1] = {0.0};
     FOR_OWNED(g, c) acc[0] += v[c];
     double tot[1];
     if (grid_reduce<1>(acc, partials, counter, tot) && threadIdx.x == 0) {
+        const double n_fluid = (double)*n_fluid_dev;  // this frame's (set_mask, on the device)
         if (st->dist) {  // z-slab: this rank's sum and count; k_finalize(kFinMean) divides the totals
             st->part[0] = tot[0];
-            st->part[1] = (double)n_fluid;
+            st->part[1] = n_fluid;
         } else {
-            st->mean = tot[0] / (double)n_fluid;
+            st->mean = tot[0] / n_fluid;
         }
     }
 }

@@ -18,6 +18,20 @@
 
 namespace nb2 {
 
+// Device-side results of a set_mask that the host reads once, lazily
+// (setup_sync in npsd_b200.cu): set_mask itself never waits on the device.
+// Buffers sized from earlier frames may be too small for this one; the
+// kernels then clamp their writes and raise a flag, and the host redoes the
+// frame with grown capacities.
+struct SetupInfo {
+    uint32_t flags;                  // bit 2l: level l's hash table over half full; bit 2l+1: its rows over capacity
+    uint32_t n_fluid;                // the reduced system size
+    uint32_t n_mixed[kMaxDepth];     // mixed-window cells per level
+    uint32_t npat[kMaxDepth];        // dictionary rows (window patterns) per level
+    uint32_t unverified[kMaxDepth];  // levels >= 1: a window differs from its pattern's (per-cell rows)
+};
+
+
 // L0: cell byte (window class, own type, stencil diagonal) plus 32-cell
 // segment masks of mixed cells and of fluid cells.
 template <int D>
@@ -71,57 +85,6 @@ __global__ void __launch_bounds__(kBlock) k_setup_l0(Geom g, const uint8_t* __re
             fmask[seg] = fm;
             fcount[seg] = __popc(fm);
         }
-    }
-}
-
-// The same cell bytes and masks, tiled (3D, nx a multiple of 32): a 32 x 8
-// block owns a 32 x 8 tile of one plane and stages the types of planes z-1..z+1
-// with a one-cell halo (outside the domain: solid) in shared memory; a warp is
-// one 32-cell row, i.e. one mask segment.
-__global__ void __launch_bounds__(256) k_setup_l0_tiled(Geom g, const uint8_t* __restrict__ types,
-                                                        uint8_t* __restrict__ cls, uint32_t* __restrict__ mmask,
-                                                        uint32_t* __restrict__ mcount, uint32_t* __restrict__ fmask,
-                                                        uint32_t* __restrict__ fcount) {
-    __shared__ uint8_t st[3][10][34];
-    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-    const int X0 = blockIdx.x * 32, Y0 = blockIdx.y * 8, z = blockIdx.z;
-    for (int i = tid; i < 3 * 10 * 34; i += 256) {
-        const int lx = i % 34, ly = (i / 34) % 10, lz = i / 340;
-        const int xx = X0 - 1 + lx, yy = Y0 - 1 + ly, zz = z - 1 + lz;
-        const bool in = xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz;
-        st[lz][ly][lx] = in ? types[lin(g, xx, yy, zz)] : (uint8_t)2;
-    }
-    __syncthreads();
-    const int x = X0 + tx, y = Y0 + ty;
-    if (y >= g.ny) return;  // whole warp (rows)
-    const long long c = lin(g, x, y, z);
-    const int t = st[1][ty + 1][tx + 1];
-    bool uniform = true, wfluid = false;
-#pragma unroll
-    for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-        for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < 3; ++dx) {
-                const int tt = st[dz][ty + dy][tx + dx];
-                uniform &= (tt == t);
-                wfluid |= (tt == 0);
-            }
-    // stencil diagonal: non-solid in-domain face neighbours (discretization.cpp:105-113);
-    // the staged outside is solid, so in-domain and non-solid is one test
-    const int diag = (st[0][ty + 1][tx + 1] != 2) + (st[1][ty][tx + 1] != 2) + (st[1][ty + 1][tx] != 2) +
-                     (st[1][ty + 1][tx + 2] != 2) + (st[1][ty + 2][tx + 1] != 2) + (st[2][ty + 1][tx + 1] != 2);
-    const int w = uniform ? t : 3;
-    cls[c] = (uint8_t)(w | (t << 2) | (diag << 4) | ((int)wfluid << 7));
-    const bool owned = c >= owned_lo(g) && c < owned_hi(g);
-    const uint32_t mm = __ballot_sync(0xffffffffu, !uniform && owned);
-    const uint32_t fm = __ballot_sync(0xffffffffu, t == 0 && owned);
-    if (tx == 0) {
-        const long long seg = c >> 5;
-        mmask[seg] = mm;
-        mcount[seg] = __popc(mm);
-        fmask[seg] = fm;
-        fcount[seg] = __popc(fm);
     }
 }
 
@@ -476,12 +439,24 @@ __global__ void __launch_bounds__(kBlock) k_classify(Geom g, const float* __rest
 // cells of a coarse level, or one representative cell per window pattern at
 // level 0): K[s] = B[s] + sum_c sum_window W[s,c,w] * I(c, x+w), order
 // (c, dz, dy, dx); row i of `tab` (kRowW floats) for cells[i], i < *count.
+// Rows come from the dictionary (cells = representatives, count = patterns)
+// unless *unverified (coarse levels whose windows did not all match their
+// pattern): then one row per mixed cell (cells_pc / count_pc). At most
+// rows_cap rows are written; more raises flag_bit (the frame is redone).
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_build_rows(Geom g, const uint8_t* __restrict__ src_types,
                                                        const float* __restrict__ img,
-                                                       const uint32_t* __restrict__ cells,
-                                                       const uint32_t* __restrict__ count, const float* __restrict__ W,
-                                                       const float* __restrict__ B, float* __restrict__ tab) {
+                                                       const uint32_t* __restrict__ cells_dict,
+                                                       const uint32_t* __restrict__ count_dict,
+                                                       const uint32_t* __restrict__ cells_pc,
+                                                       const uint32_t* __restrict__ count_pc,
+                                                       const uint32_t* __restrict__ unverified, uint32_t rows_cap,
+                                                       uint32_t* __restrict__ flags, uint32_t flag_bit,
+                                                       const float* __restrict__ W, const float* __restrict__ B,
+                                                       float* __restrict__ tab) {
+    const bool pc = unverified && *unverified;
+    const uint32_t* cells = pc ? cells_pc : cells_dict;
+    const uint32_t* count = pc ? count_pc : count_dict;
     // one warp per row: lanes t < S stage the window (3 channels), then lane s
     // accumulates slot s in the reference order B[s] + sum_{ch, t} W[s,ch,t] I
     constexpr int S = Sh<D>::S;
@@ -489,7 +464,11 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(Geom g, const uint8_t* __
     __shared__ float sW[S * 3 * S];
     __shared__ float sB[S];
     __shared__ float win[NW][3][S];
-    const long long n = *count;
+    long long n = *count;
+    if (n > rows_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, flag_bit);
+        n = rows_cap;
+    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if ((long long)blockIdx.x * NW >= n) return;  // grid sized for the capacity
     for (int i = threadIdx.x; i < S * 3 * S; i += blockDim.x) sW[i] = W[i];
@@ -634,34 +613,7 @@ __global__ void __launch_bounds__(kBlock) k_verify_windows(Geom g, const float* 
     }
 }
 
-__global__ void __launch_bounds__(kBlock) k_run_heads(const unsigned long long* __restrict__ skeys,
-                                                      const uint32_t* __restrict__ count, uint32_t* __restrict__ head) {
-    const long long n = *count;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        head[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1u : 0u;
-}
-
-// pid[mixed idx] = pattern id; repcell[pattern] = its first cell; npat
-__global__ void __launch_bounds__(kBlock) k_pattern_ids(const uint32_t* __restrict__ sidx,
-                                                        const uint32_t* __restrict__ scan,
-                                                        const uint32_t* __restrict__ head,
-                                                        const uint32_t* __restrict__ list,
-                                                        const uint32_t* __restrict__ count, uint32_t* __restrict__ pid,
-                                                        uint32_t* __restrict__ repcell, uint32_t* __restrict__ npat) {
-    const long long n = *count;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint32_t p = scan[i] - 1;
-        pid[sidx[i]] = p;
-        if (head[i]) repcell[p] = list[sidx[i]];
-        if (i == n - 1) *npat = scan[i];
-    }
-    if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) *npat = 0;
-}
-
-// Pattern ids by hashing instead of sorting (the launchers' default): keys go
-// into an open-addressing table (linear probing); the thread that inserts a
+// Pattern ids by hashing: keys go into an open-addressing table (linear probing); the thread that inserts a
 // key gives it the next id and makes its cell the representative. Ids come out
 // in a nondeterministic order, but a pattern's row depends only on the
 // pattern (level 0: the exact key; coarse levels: every member's window is
@@ -674,8 +626,15 @@ __global__ void __launch_bounds__(kBlock) k_dedup_insert(const unsigned long lon
                                                          const uint32_t* __restrict__ list,
                                                          unsigned long long* __restrict__ tk, uint32_t* __restrict__ tv,
                                                          unsigned long long mask, uint32_t* __restrict__ slot,
-                                                         uint32_t* __restrict__ repcell, uint32_t* __restrict__ npat) {
+                                                         uint32_t* __restrict__ repcell, uint32_t* __restrict__ npat,
+                                                         uint32_t* __restrict__ flags, uint32_t flag_bit) {
     const long long n = *count;
+    // more than half full: probing could run long (or forever when full);
+    // skip, flag, and let the host redo the frame with a larger table
+    if (2 * (unsigned long long)n > mask + 1) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, flag_bit);
+        return;
+    }
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         unsigned long long k = keys[i];
@@ -697,12 +656,19 @@ __global__ void __launch_bounds__(kBlock) k_dedup_insert(const unsigned long lon
     }
 }
 
+// pid[i] = the pattern of key i, clamped below the row capacity (an
+// overflowing frame is redone; until then every row index stays in bounds)
 __global__ void __launch_bounds__(kBlock) k_dedup_ids(const uint32_t* __restrict__ slot,
                                                       const uint32_t* __restrict__ count,
-                                                      const uint32_t* __restrict__ tv, uint32_t* __restrict__ pid) {
+                                                      const uint32_t* __restrict__ tv, unsigned long long mask,
+                                                      uint32_t rows_cap, uint32_t* __restrict__ pid) {
     const long long n = *count;
+    const bool skipped = 2 * (unsigned long long)n > mask + 1;  // k_dedup_insert did not run
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) pid[i] = tv[slot[i]];
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t p = skipped ? 0u : tv[slot[i]];
+        pid[i] = p < rows_cap ? p : 0u;
+    }
 }
 
 // The three uniform-window kernels of a conv (same arithmetic as

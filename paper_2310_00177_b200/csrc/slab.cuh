@@ -51,6 +51,15 @@ __global__ void k_sum_u64(const unsigned long long* __restrict__ all, int nranks
     }
 }
 
+// set_mask capacity flags agreed over the ranks (any rank overflowing makes
+// every rank redo the frame: the redo runs the exchanges again)
+__global__ void k_flags_u64(const uint32_t* __restrict__ flags, unsigned long long* __restrict__ v) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *v = *flags;
+}
+__global__ void k_u64_flags(const unsigned long long* __restrict__ v, uint32_t* __restrict__ flags) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *flags = *v ? 0xffffffffu : 0u;
+}
+
 // planes [z0, z1) of a level's 3-channel image set to the outside of the
 // domain (solid: channels 0, 0, 1) — the ghost planes of a slab before the
 // neighbours' copies arrive
