@@ -130,6 +130,25 @@ def write_bench_outputs(rows: list[BenchRow], out_dir) -> None:
                 f.write(f"{i},{_g17(v)},{_f9(c)}\n")
 
 
+def load_bench_rows(csv_path) -> list[BenchRow]:
+    """load_bench_rows (bench.cpp:168-201): rows.csv back into rows (no
+    traces); the error field is the rest of the line."""
+    rows = []
+    with open(csv_path) as f:
+        next(f)  # header
+        for line in f:
+            line = line.rstrip("\n")
+            if not line:
+                continue
+            parts = line.split(",", 10)
+            rows.append(BenchRow(parts[0], parts[1], n_f=int(parts[2]), iterations=int(parts[3]),
+                                 converged=parts[4] == "1", setup_seconds=float(parts[5]),
+                                 iterate_seconds=float(parts[6]), precond_seconds=float(parts[7]),
+                                 total_seconds=float(parts[8]), final_rel_residual=float(parts[9]),
+                                 error=parts[10] if len(parts) > 10 else ""))
+    return rows
+
+
 def write_bench_report(rows: list[BenchRow], out_dir) -> None:
     """write_bench_report (bench.cpp:204-263): summary.csv, speedup_hist.csv."""
     d = Path(out_dir)

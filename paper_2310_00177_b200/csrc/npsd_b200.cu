@@ -4,7 +4,7 @@
 // iteration: 2*depth-1 network kernels + ortho + update) repeats under a
 // device-side conditional WHILE node, so the host never synchronises inside
 // the solve.
-#include <cub/device/device_radix_sort.cuh>
+#include <cudaTypedefs.h>
 #include <cub/device/device_scan.cuh>
 
 #include <dlfcn.h>
@@ -314,6 +314,7 @@ struct npsd_b200_ctx {
     double *X0 = nullptr, *X1 = nullptr, *R = nullptr, *Bf = nullptr, *Dtmp = nullptr;
     double *Dring = nullptr, *ADring = nullptr;
     int ring_alloc = 0;
+    TmaMaps* maps = nullptr;  // tensor maps of d, the ring slots, x0 / x1 (build_tma_maps)
     SolverState* st = nullptr;
     SolverState* st_host = nullptr;  // pinned
     double* partials = nullptr;
@@ -631,7 +632,8 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         za.nzg = c->gglob[0].nz;
         const dim3 grid(c->g0.nx / 32, (c->g0.ny + 7) / 8, (c->g0.nz + ZC - 1) / ZC);
         LAUNCH3(c, s, (k_classify_march<ZC, true>), grid, dim3(32, 8), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount,
-                c->fmask, c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za);
+                c->fmask, c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za,
+                SubMasks{c->dmask, c->dcount, c->umask, c->ucount});
     } else {
         LAUNCH(c, s, k_setup_l0<D>, c->g0.n, c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
         LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
@@ -663,7 +665,8 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
             constexpr int ZC = 8;
             const dim3 grid(Lc.g.nx / 32, (Lc.g.ny + 7) / 8, (Lc.g.nz + ZC - 1) / ZC);
             LAUNCH3(c, s, (k_classify_march<ZC, false>), grid, dim3(32, 8), Lc.g, (const uint8_t*)pure, Lc.cls,
-                    Lc.mmask, Lc.mcount, (uint32_t*)nullptr, (uint32_t*)nullptr, 0, 0, (uint8_t*)nullptr, ZsumArgs{});
+                    Lc.mmask, Lc.mcount, (uint32_t*)nullptr, (uint32_t*)nullptr, 0, 0, (uint8_t*)nullptr, ZsumArgs{},
+                    SubMasks{});
         } else {
             LAUNCH(c, s, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
         }
@@ -672,7 +675,7 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
     // compact mixed-cell lists per level
     for (int l = 0; l < c->depth; ++l) {
         LevelBufs& L = c->L[l];
-        LAUNCH(c, s, k_mixed_list, L.g.n, L.g, L.cls, L.mmask, L.mbase, L.mlist);
+        LAUNCH(c, s, k_mixed_list, L.nseg, L.nseg, (const uint32_t*)L.mmask, (const uint32_t*)L.mbase, L.mlist);
         LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), L.mbase, L.mcount, L.nseg, L.mcnt);
         CK(cudaMemcpyAsync(&c->d_info->n_mixed[l], L.mcnt, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     }
@@ -682,7 +685,7 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
            L0.mcnt, c->dkeys, c->dvals);
     dedup_patterns(c, s, 0, L0.mcnt, L0.mlist, c->pid0, c->repcell0, c->npat0);
     CK(cudaMemcpyAsync(&c->d_info->npat[0], c->npat0, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    LAUNCH(c, s, k_sub_masks, L0.g.n, L0.g, L0.cls, c->dmask, c->dcount, c->umask, c->ucount);
+    if (!march0) LAUNCH(c, s, k_sub_masks, L0.g.n, L0.g, L0.cls, c->dmask, c->dcount, c->umask, c->ucount);
     scan_u32(c, c->dcount, c->dbase, L0.nseg);
     scan_u32(c, c->ucount, c->ubase, L0.nseg);
     LAUNCH(c, s, k_mixed_sub, std::min<long long>(c->g0.n, (long long)c->cap_ht[0]), L0.mlist, c->pid0, L0.mcnt,
@@ -1065,11 +1068,11 @@ void launch_ortho(npsd_b200_ctx* c, cudaStream_t s) {
     constexpr int SY = march_sy<OrthoOp<NO>>();
     const dim3 block(kSX, SY);
     auto k = k_ortho2<D, NO, SY>;
-    const size_t sm = march_smem_bytes<OrthoOp<NO>, SY>();
+    const size_t sm = stencil_smem_bytes<D, OrthoOp<NO>, SY>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const dim3 grid(wave_blocks(c, k, kSX * SY, sm));
     launch_pdl(c, s, k, grid, block, sm, g, c->L[0].cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
-               c->counter, (SY == kSY ? c->sch_stencil : c->sch_march).view());
+               c->counter, (SY == kSY ? c->sch_stencil : c->sch_march).view(), *c->maps);
 }
 
 template <int D>
@@ -1090,11 +1093,12 @@ void launch_update(npsd_b200_ctx* c, cudaStream_t s, cudaGraphConditionalHandle 
     constexpr int SY = march_sy<UpdateOp>();
     const dim3 block(kSX, SY);
     auto k = k_update2<D, SY>;
-    const size_t sm = march_smem_bytes<UpdateOp, SY>();
+    const size_t sm = stencil_smem_bytes<D, UpdateOp, SY>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const dim3 grid(wave_blocks(c, k, kSX * SY, sm));
     launch_pdl(c, s, k, grid, block, sm, g, c->L[0].cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist,
-               c->times, c->partials, c->counter, h, use_cond, do_norm, (SY == kSY ? c->sch_stencil : c->sch_march).view());
+               c->times, c->partials, c->counter, h, use_cond, do_norm, (SY == kSY ? c->sch_stencil : c->sch_march).view(),
+               *c->maps);
 }
 
 // One named launcher per kernel of an iteration: the graph body is captured
@@ -1309,6 +1313,44 @@ std::vector<Step> body_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h, int
     return v;
 }
 
+// Tensor maps (tma.cuh) of the stencil kernels' TMA inputs: full-grid f64
+// vectors as (nx, ny, local nz) tensors, boxes of one 68 x (SY + 2) tile
+// plane (the 64 x SY tile, two columns and one row of halo each side); rebuilt
+// whenever one of the vectors moves (the solve graphs hold them by value).
+void build_tma_maps(npsd_b200_ctx* c) {
+    static PFN_cuTensorMapEncodeTiled encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }();
+    if (!c->maps) {
+        void* p = nullptr;
+        CK(cudaMallocHost(&p, sizeof(TmaMaps)));
+        c->maps = static_cast<TmaMaps*>(p);
+    }
+    std::memset(c->maps, 0, sizeof(TmaMaps));
+    if (c->dim != 3) return;
+    const Geom& g = c->g0;
+    auto make = [&](CUtensorMap* m, const double* base) {
+        if (!base) return;
+        const cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz};
+        const cuuint64_t strides[2] = {(cuuint64_t)g.nx * sizeof(double), (cuuint64_t)g.nx * g.ny * sizeof(double)};
+        const cuuint32_t box[3] = {(cuuint32_t)kVW, (cuuint32_t)(kMarchSY + 2), 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
+                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    };
+    make(&c->maps->m[kMapD], c->Dtmp);
+    for (int j = 0; j < c->ring_alloc && j < kRing; ++j) make(&c->maps->m[kMapRing + j], c->Dring + (size_t)j * g.n);
+    make(&c->maps->m[kMapX0], c->X0);
+    make(&c->maps->m[kMapX1], c->X1);
+    ++c->buf_gen;
+}
+
 void ensure_ring(npsd_b200_ctx* c, int ring) {
     if (ring <= c->ring_alloc) return;
     const size_t n = (size_t)c->g0.n;
@@ -1319,6 +1361,7 @@ void ensure_ring(npsd_b200_ctx* c, int ring) {
     CK(cudaMemsetAsync(c->Dring, 0, n * ring * sizeof(double), c->s));
     CK(cudaMemsetAsync(c->ADring, 0, n * ring * sizeof(double), c->s));
     c->ring_alloc = ring;
+    if (c->X1) build_tma_maps(c);
 }
 
 void ensure_hist(npsd_b200_ctx* c, long long need) {
@@ -2011,6 +2054,7 @@ void free_ctx(npsd_b200_ctx* c) {
                     (void*)c->types_dev})
         F(p);
     if (c->info_host) cudaFreeHost(c->info_host);
+    if (c->maps) cudaFreeHost(c->maps);
     if (c->ev_setup) cudaEventDestroy(c->ev_setup);
     if (c->mask_exec) cudaGraphExecDestroy(c->mask_exec);
     F(c->X0);

@@ -111,12 +111,18 @@ struct ZsumArgs {
     int nxg, nyg, nzg;                 // the full grid (level 0)
 };
 
+// L0 also writes the solve's mixed sublist masks (mixed.cuh k_sub_masks):
+// dmask = mixed windows holding fluid, umask = mixed fluid cells.
+struct SubMasks {
+    uint32_t *dmask, *dcount, *umask, *ucount;
+};
+
 template <int ZC, bool L0>
 __global__ void __launch_bounds__(256) k_classify_march(Geom g, const uint8_t* __restrict__ src,
                                                         uint8_t* __restrict__ cls, uint32_t* __restrict__ mmask,
                                                         uint32_t* __restrict__ mcount, uint32_t* __restrict__ fmask,
                                                         uint32_t* __restrict__ fcount, int ftx, int fty,
-                                                        uint8_t* __restrict__ tflags, ZsumArgs za) {
+                                                        uint8_t* __restrict__ tflags, ZsumArgs za, SubMasks sm) {
     static_assert(kFlagTX == 32 && kFlagTY == 8, "the block tile is the flag tile");
     __shared__ uint8_t st[2][10][36];
     __shared__ unsigned long long sG[L0 ? kMaxDepth * 81 : 1];
@@ -209,12 +215,18 @@ __global__ void __launch_bounds__(256) k_classify_march(Geom g, const uint8_t* _
             const bool wfluid = lo == 0;
             cls[c] = (uint8_t)((uniform ? t : 3) | (t << 2) | (diag << 4) | ((int)wfluid << 7));
             const uint32_t fm = __ballot_sync(0xffffffffu, t == 0 && owned);
+            const uint32_t dm = __ballot_sync(0xffffffffu, !uniform && owned && wfluid);
+            const uint32_t um = __ballot_sync(0xffffffffu, !uniform && owned && t == 0);
             if (tx == 0) {
                 const long long seg = c >> 5;
                 mmask[seg] = mm;
                 mcount[seg] = __popc(mm);
                 fmask[seg] = fm;
                 fcount[seg] = __popc(fm);
+                sm.dmask[seg] = dm;
+                sm.dcount[seg] = __popc(dm);
+                sm.umask[seg] = um;
+                sm.ucount[seg] = __popc(um);
             }
             // window counts of every level l < nzs: classes by the level's
             // global (x, y, z) position (k_zsums), warp-aggregated. A warp

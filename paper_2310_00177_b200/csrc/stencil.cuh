@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "psdo.cuh"
+#include "tma.cuh"
 
 namespace nb2 {
 
@@ -58,6 +59,16 @@ constexpr int kMarchSY = STENCIL_SY;
 #endif
 #ifndef STENCIL_UPDATE_CTR_DIRECT
 #define STENCIL_UPDATE_CTR_DIRECT 1
+#endif
+// TMA plane loads (stencil_march_tma) for the 3D ortho / update kernels: one
+// thread issues a tensor copy of each input's tile plane (halo included,
+// zeros outside the domain) into a ring of STENCIL_TMA_PF + 2 stages, all
+// threads wait on the stage's mbarrier. 0: the cp.async path.
+#ifndef STENCIL_TMA
+#define STENCIL_TMA 1
+#endif
+#ifndef STENCIL_TMA_PF
+#define STENCIL_TMA_PF 1
 #endif
 constexpr unsigned kOut2 = 0x0C0Cu;        // pair bytes outside the domain: type 3
 
@@ -105,7 +116,9 @@ struct OrthoOp {
     static constexpr int NC = 1;       // r (centre only)
     static constexpr int PF = STENCIL_PF_ORTHO;  // planes prefetched ahead
     static constexpr int CS = STENCIL_ORTHO_CTR_DIRECT ? 0 : PF + 1;  // centre inputs staged in the ring
+    static constexpr int TPF = STENCIL_TMA_PF;                        // TMA path: planes in flight ahead
     const double* in[NA];
+    const CUtensorMap* tin[NA];  // TMA path: the inputs' tensor maps
     const double* ctr[NC];
     double mp[NO > 0 ? NO : 1];
     int nc;
@@ -125,7 +138,9 @@ struct UpdateOp {
     // b read straight into registers, one step ahead of its use: without its
     // ring stages the block fits four per SM instead of three
     static constexpr int CS = STENCIL_UPDATE_CTR_DIRECT ? 0 : PF + 1;
+    static constexpr int TPF = STENCIL_TMA_PF;
     const double* in[NA];
+    const CUtensorMap* tin[NA];
     const double* ctr[NC];
     double alpha;
     __device__ __forceinline__ double value(const double (&a)[NA]) const {
@@ -324,6 +339,173 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
     cp_wait<0>();
 }
 
+// Shared memory of the TMA march: the input ring (each box a 128-byte aligned
+// 68 x VH plane of doubles), the operand ring, one mbarrier per stage.
+template <typename Op, int SY>
+struct TmaSmem {
+    static constexpr int VH = SY + 2;
+    static constexpr int PLANE = VH * kVW;                               // doubles in a box
+    static constexpr int PSTRIDE = ((PLANE * 8 + 127) / 128) * 128 / 8;  // box stride, 128-byte aligned
+    static constexpr int ST = Op::TPF + 2;
+    double raw[ST][Op::NA][PSTRIDE];
+    double v[4][VH][kVW];
+    uint64_t bar[ST];
+};
+template <typename Sm>
+__device__ __forceinline__ Sm& tma_smem() {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const unsigned a = smem_u32(smem_raw);
+    return *reinterpret_cast<Sm*>(smem_raw + (((a + 127u) & ~127u) - a));
+}
+template <typename Op, int SY>
+__host__ __device__ constexpr size_t tma_smem_bytes() {
+    return sizeof(TmaSmem<Op, SY>) + 128;
+}
+template <typename Op, int SY>
+__device__ __forceinline__ void tma_march_init() {
+    TmaSmem<Op, SY>& S = tma_smem<TmaSmem<Op, SY>>();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        for (int i = 0; i < TmaSmem<Op, SY>::ST; ++i) mbar_init(&S.bar[i], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+}
+
+// stencil_march with the inputs' planes loaded by TMA (3D). A stage holds a
+// plane until the epilogue of its step has read the own cells' inputs, so
+// the ring has TPF + 2 stages: the plane issued at step z (z + TPF) reuses
+// the stage of plane z - 2, whose last reads precede step z - 1's barrier.
+// seq numbers the planes a block has issued (mbarrier phases), across
+// segments. Same epilogue interface and arithmetic as stencil_march.
+template <int NV, int SY, typename Op, typename Epi>
+__device__ __forceinline__ void stencil_march_tma(const Geom& g, const uint8_t* __restrict__ cls, const Op& op, int tx,
+                                                  int ty, int zc0, int zc1, double (&acc)[NV], unsigned& seq, Epi epi) {
+    using Sm = TmaSmem<Op, SY>;
+    constexpr int PF = Op::TPF, ST = Sm::ST;
+    static_assert(PF >= 1, "the prologue forms planes zc0 - 1 and zc0");
+    Sm& S = tma_smem<Sm>();
+    __syncthreads();  // the previous segment's last reads of S are done
+    constexpr int kTY = SY, kVH = SY + 2;
+    const int lane = threadIdx.x, row = threadIdx.y;
+    const bool leader = lane == 0 && row == 0;
+    const int X0 = tx * kTX, Y0 = ty * kTY;
+    const int x = X0 + 2 * lane, y = Y0 + row;
+    const bool own = x < g.nx && y < g.ny;
+    const long long nx = g.nx, plane = nx * g.ny;
+    // the positions this thread forms: own pair; rows 0/1: the halo row pair
+    // above / below; row 2, lanes 0..2SY-1: the halo column cells
+    int hsr = 0, hsc = 0, hkind = 0;
+    if (row == 0 || row == 1) {
+        hkind = 1;
+        hsr = (row == 0) ? 0 : kVH - 1;
+        hsc = 2 + 2 * lane;
+    } else if (row == 2 && lane < 2 * kTY) {
+        hkind = 2;
+        hsr = 1 + (lane & (kTY - 1));
+        hsc = (lane < kTY) ? 1 : kTX + 2;
+    }
+    const long long qo = (long long)(own ? y : 0) * nx + (own ? x : 0);
+    auto own_bytes = [&](int z) -> unsigned {
+        return (own && z >= 0 && z < g.nz) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo))
+                                           : kOut2;
+    };
+    const unsigned q0 = seq;  // sequence number of plane zc0 - 1
+    auto pseq = [&](int z) { return q0 + (unsigned)(z - (zc0 - 1)); };
+    auto issue = [&](int z) {
+        if (z > zc1 || !leader) return;  // the last input plane of the segment is zc1
+        const unsigned k = pseq(z), st = k % ST;
+        fence_proxy_async_smem();
+        mbar_expect_tx(&S.bar[st], (unsigned)(Op::NA * Sm::PLANE * sizeof(double)));
+#pragma unroll
+        for (int a = 0; a < Op::NA; ++a) tma_load_3d(&S.raw[st][a][0], op.tin[a], X0 - 2, Y0 - 1, z, &S.bar[st]);
+    };
+    auto wait = [&](int z) {
+        const unsigned k = pseq(z);
+        mbar_wait(&S.bar[k % ST], (k / ST) & 1u);
+    };
+    auto rw = [&](int st, int a, int r, int c) -> double { return S.raw[st][a][r * kVW + c]; };
+    // v of plane z at this thread's positions (zeros outside the domain came with the box)
+    auto form = [&](int z) {
+        const int st = (int)(pseq(z) % ST), vs = (z + 1024) & 3;
+        double a0[Op::NA], a1[Op::NA];
+#pragma unroll
+        for (int a = 0; a < Op::NA; ++a) {
+            a0[a] = rw(st, a, row + 1, 2 + 2 * lane);
+            a1[a] = rw(st, a, row + 1, 3 + 2 * lane);
+        }
+        S.v[vs][row + 1][2 + 2 * lane] = op.value(a0);
+        S.v[vs][row + 1][3 + 2 * lane] = op.value(a1);
+        if (hkind != 0) {
+#pragma unroll
+            for (int a = 0; a < Op::NA; ++a) a0[a] = rw(st, a, hsr, hsc);
+            S.v[vs][hsr][hsc] = op.value(a0);
+            if (hkind == 1) {
+#pragma unroll
+                for (int a = 0; a < Op::NA; ++a) a1[a] = rw(st, a, hsr, hsc + 1);
+                S.v[vs][hsr][hsc + 1] = op.value(a1);
+            }
+        }
+    };
+#pragma unroll
+    for (int k = 0; k <= PF; ++k) issue(zc0 - 1 + k);
+    unsigned ob[PF + 2];  // own bytes of planes z .. z+PF+1 (rotating)
+#pragma unroll
+    for (int k = 0; k < PF + 2; ++k) ob[k] = own_bytes(zc0 + k);
+    wait(zc0 - 1);
+    form(zc0 - 1);
+    wait(zc0);
+    form(zc0);
+#pragma unroll(PF + 2)
+    for (int z = zc0; z < zc1; ++z) {
+        constexpr int NCD = (Op::NC > 0) ? Op::NC : 0;
+        double2 cdir[NCD > 0 ? NCD : 1];
+        if constexpr (NCD > 0) {
+            const bool l = own && pair_live(ob[0]);
+#pragma unroll
+            for (int a = 0; a < NCD; ++a)
+                cdir[a] = l ? __ldg(reinterpret_cast<const double2*>(op.ctr[a] + z * plane + qo)) : make_double2(0.0, 0.0);
+        }
+        issue(z + PF);
+        wait(z + 1);
+        form(z + 1);
+        __syncthreads();  // v of planes z-1, z, z+1 complete (halos included)
+        const unsigned bc = ob[0];
+        if (own && pair_live(bc)) {
+            const int vm = (z + 1023) & 3, vc = (z + 1024) & 3, vp = (z + 1025) & 3;
+            const int c0 = 2 + 2 * lane, r0 = row + 1;
+            const double v0 = S.v[vc][r0][c0], v1 = S.v[vc][r0][c0 + 1];
+            const double zm0 = S.v[vm][r0][c0], zm1 = S.v[vm][r0][c0 + 1];
+            const double zp0 = S.v[vp][r0][c0], zp1 = S.v[vp][r0][c0 + 1];
+            double2 sv;
+            sv.x = fluid(bc & 0xffu) ? row_sum(zm0, S.v[vc][r0 - 1][c0], S.v[vc][r0][c0 - 1], cls_diag(bc & 0xffu), v0,
+                                               v1, S.v[vc][r0 + 1][c0], zp0)
+                                     : 0.0;
+            sv.y = fluid(bc >> 8) ? row_sum(zm1, S.v[vc][r0 - 1][c0 + 1], v0, cls_diag(bc >> 8), v1,
+                                            S.v[vc][r0][c0 + 2], S.v[vc][r0 + 1][c0 + 1], zp1)
+                                  : 0.0;
+            const int sl = (int)(pseq(z) % ST);
+            double raw0[Op::NA], raw1[Op::NA], c0v[Op::NC > 0 ? Op::NC : 1] = {}, c1v[Op::NC > 0 ? Op::NC : 1] = {};
+#pragma unroll
+            for (int a = 0; a < Op::NA; ++a) {
+                raw0[a] = rw(sl, a, r0, c0);
+                raw1[a] = rw(sl, a, r0, c0 + 1);
+            }
+            if constexpr (NCD > 0) {
+#pragma unroll
+                for (int a = 0; a < NCD; ++a) {
+                    c0v[a] = cdir[a].x;
+                    c1v[a] = cdir[a].y;
+                }
+            }
+            epi(z * plane + qo, make_double2(v0, v1), sv, bc, raw0, raw1, c0v, c1v, acc);
+        }
+#pragma unroll
+        for (int k = 0; k < PF + 1; ++k) ob[k] = ob[k + 1];
+        ob[PF + 1] = own_bytes(z + PF + 2);
+    }
+    seq = pseq(zc1) + 1;  // planes zc0 - 1 .. zc1 were issued and waited on
+}
+
 // d'.Ad' and r.d' -> alpha, or a breakdown (solver.cpp:245-251); d_j.Ad' are
 // the cross terms of the direction's future projections. tot = {d'Ad', r.d',
 // d_1.Ad', ...}.
@@ -347,27 +529,37 @@ __device__ __forceinline__ void fin_ortho(SolverState* st, const double* tot) {
     }
 }
 
+// the 3D ortho / update kernels load their operand planes with TMA
+template <int D>
+__host__ __device__ constexpr bool stencil_tma() {
+    return STENCIL_TMA != 0 && D == 3;
+}
+
 // d' = MGS(d); Ad'; dots d'.Ad', r.d', d_j.Ad'. NO = n_ortho (cache bound).
 template <int D, int NO, int SY>
 __global__ void __launch_bounds__(kSX* SY, SY == kSY ? ORTHO_MINB : 1) k_ortho2(Geom g, const uint8_t* __restrict__ cls,
                                                      const double* __restrict__ dtmp, const double* __restrict__ r,
                                                      double* __restrict__ Dring, double* __restrict__ ADring,
                                                      SolverState* st, double* __restrict__ partials,
-                                                     unsigned int* __restrict__ counter, Sched sc) {
+                                                     unsigned int* __restrict__ counter, Sched sc,
+                                                     const __grid_constant__ TmaMaps maps) {
+    using Op = OrthoOp<NO>;
+    if constexpr (stencil_tma<D>()) tma_march_init<Op, SY>();
     pdl_launch_wait();
     if (st->dist && st->done) return;
     precond_span_end(st);
     const int nc = st->n_cache, R = st->ring;
     const int nw = (st->head + 1) % R;
-    using Op = OrthoOp<NO>;
     Op op;
     op.in[0] = dtmp;
+    op.tin[0] = &maps.m[kMapD];
     op.ctr[0] = r;
     op.nc = nc;
 #pragma unroll
     for (int j = 0; j < NO; ++j) {
         const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
         op.in[1 + j] = Dring + (long long)slot * g.n;
+        op.tin[1 + j] = &maps.m[kMapRing + slot];
         op.mp[j] = (j < nc) ? -st->p[j] : 0.0;
     }
     double* dnew = Dring + (long long)nw * g.n;
@@ -376,24 +568,28 @@ __global__ void __launch_bounds__(kSX* SY, SY == kSY ? ORTHO_MINB : 1) k_ortho2(
     double acc[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc[j] = 0.0;
-    sched_for_each(sc, [&](int tx, int ty, int zc0, int zc1) {
-    stencil_march<D, NV, SY>(g, cls, op, tx, ty, zc0, zc1, acc,
-                         [&](long long q, double2 v, double2 s, unsigned bc, const double(&i0)[Op::NA],
-                             const double(&i1)[Op::NA], const double(&c0)[1], const double(&c1)[1], double(&a)[NV]) {
-                             *reinterpret_cast<double2*>(dnew + q) = v;
-                             *reinterpret_cast<double2*>(adnew + q) = s;
-                             // non-fluid halves are exact zeros: their terms vanish
-                             a[0] += v.x * s.x;
-                             a[0] += v.y * s.y;
-                             a[1] += c0[0] * v.x;
-                             a[1] += c1[0] * v.y;
+    auto epi = [&](long long q, double2 v, double2 s, unsigned bc, const double(&i0)[Op::NA], const double(&i1)[Op::NA],
+                   const double(&c0)[1], const double(&c1)[1], double(&a)[NV]) {
+        *reinterpret_cast<double2*>(dnew + q) = v;
+        *reinterpret_cast<double2*>(adnew + q) = s;
+        // non-fluid halves are exact zeros: their terms vanish
+        a[0] += v.x * s.x;
+        a[0] += v.y * s.y;
+        a[1] += c0[0] * v.x;
+        a[1] += c1[0] * v.y;
 #pragma unroll
-                             for (int j = 0; j < NO; ++j)
-                                 if (j < nc) {
-                                     a[2 + j] += i0[1 + j] * s.x;
-                                     a[2 + j] += i1[1 + j] * s.y;
-                                 }
-                         });
+        for (int j = 0; j < NO; ++j)
+            if (j < nc) {
+                a[2 + j] += i0[1 + j] * s.x;
+                a[2 + j] += i1[1 + j] * s.y;
+            }
+    };
+    unsigned seq = 0;
+    sched_for_each(sc, [&](int tx, int ty, int zc0, int zc1) {
+        if constexpr (stencil_tma<D>())
+            stencil_march_tma<NV, SY>(g, cls, op, tx, ty, zc0, zc1, acc, seq, epi);
+        else
+            stencil_march<D, NV, SY>(g, cls, op, tx, ty, zc0, zc1, acc, epi);
     });
     double tot[NV];
     if (grid_reduce<NV, kSX * SY>(acc, partials, counter, tot)) {
@@ -416,7 +612,8 @@ __global__ void UPDATE_BOUNDS k_update2(Geom g, const uint8_t* __restrict__ cls,
                                                       double* __restrict__ times, double* __restrict__ partials,
                                                       unsigned int* __restrict__ counter,
                                                       cudaGraphConditionalHandle cond, int use_cond, int do_norm,
-                                                      Sched sc) {
+                                                      Sched sc, const __grid_constant__ TmaMaps maps) {
+    if constexpr (stencil_tma<D>()) tma_march_init<UpdateOp, SY>();
     pdl_launch_wait();
     if (st->breakdown) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0)
@@ -428,22 +625,28 @@ __global__ void UPDATE_BOUNDS k_update2(Geom g, const uint8_t* __restrict__ cls,
     UpdateOp op;
     op.in[0] = st->xcur ? X1 : X0;
     op.in[1] = Dring + (long long)nw * g.n;
+    op.tin[0] = &maps.m[st->xcur ? kMapX1 : kMapX0];
+    op.tin[1] = &maps.m[kMapRing + nw];
     op.ctr[0] = b;
     op.alpha = st->alpha;
     double* xn = st->xcur ? X0 : X1;
     double acc[1] = {0.0};
+    auto epi = [&](long long q, double2 v, double2 s, unsigned bc, const double(&)[2], const double(&)[2],
+                   const double(&c0)[1], const double(&c1)[1], double(&a)[1]) {
+        double2 rv;
+        rv.x = fluid(bc & 0xffu) ? __dadd_rn(c0[0], -s.x) : 0.0;
+        rv.y = fluid(bc >> 8) ? __dadd_rn(c1[0], -s.y) : 0.0;
+        *reinterpret_cast<double2*>(xn + q) = v;
+        *reinterpret_cast<double2*>(r + q) = rv;
+        a[0] += rv.x * rv.x;
+        a[0] += rv.y * rv.y;
+    };
+    unsigned seq = 0;
     sched_for_each(sc, [&](int tx, int ty, int zc0, int zc1) {
-    stencil_march<D, 1, SY>(g, cls, op, tx, ty, zc0, zc1, acc,
-                        [&](long long q, double2 v, double2 s, unsigned bc, const double(&)[2], const double(&)[2],
-                            const double(&c0)[1], const double(&c1)[1], double(&a)[1]) {
-                            double2 rv;
-                            rv.x = fluid(bc & 0xffu) ? __dadd_rn(c0[0], -s.x) : 0.0;
-                            rv.y = fluid(bc >> 8) ? __dadd_rn(c1[0], -s.y) : 0.0;
-                            *reinterpret_cast<double2*>(xn + q) = v;
-                            *reinterpret_cast<double2*>(r + q) = rv;
-                            a[0] += rv.x * rv.x;
-                            a[0] += rv.y * rv.y;
-                        });
+        if constexpr (stencil_tma<D>())
+            stencil_march_tma<1, SY>(g, cls, op, tx, ty, zc0, zc1, acc, seq, epi);
+        else
+            stencil_march<D, 1, SY>(g, cls, op, tx, ty, zc0, zc1, acc, epi);
     });
     if (!do_norm) return;
     double tot[1];
@@ -464,6 +667,11 @@ constexpr size_t march_smem_bytes() {
 template <typename Op>
 constexpr int march_sy() {
     return march_smem_bytes<Op, kMarchSY>() <= 220 * 1024 ? kMarchSY : kSY;
+}
+// dynamic shared memory of an ortho / update launch
+template <int D, typename Op, int SY>
+constexpr size_t stencil_smem_bytes() {
+    return stencil_tma<D>() ? tma_smem_bytes<Op, SY>() : march_smem_bytes<Op, SY>();
 }
 
 }  // namespace nb2

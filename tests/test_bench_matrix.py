@@ -33,3 +33,14 @@ def test_csv_bytes_match_reference_writers(ref, tmp_path):
     ref.bench_roundtrip(ours / "rows.csv", theirs)
     for name in ("rows.csv", "summary.csv", "speedup_hist.csv"):
         assert (ours / name).read_bytes() == (theirs / name).read_bytes(), name
+
+
+def test_load_bench_rows_roundtrip(tmp_path):
+    """load_bench_rows (bench.cpp:168-201) reads back what write_bench_outputs wrote."""
+    rows = [bm.BenchRow("C1", "psdo+neural", n_f=10, iterations=3, converged=True, setup_seconds=0.5,
+                        iterate_seconds=0.25, precond_seconds=0.125, total_seconds=0.75, final_rel_residual=1e-7),
+            bm.BenchRow("C1", "fpcg+none", error="fpcg+none: not available, on the B200 device path")]
+    bm.write_bench_outputs(rows, tmp_path)
+    back = bm.load_bench_rows(tmp_path / "rows.csv")
+    assert [(r.system, r.method, r.n_f, r.iterations, r.converged, r.total_seconds, r.error) for r in back] == \
+           [(r.system, r.method, r.n_f, r.iterations, r.converged, r.total_seconds, r.error) for r in rows]
