@@ -62,13 +62,19 @@ constexpr int kMarchSY = STENCIL_SY;
 #endif
 // TMA plane loads (stencil_march_tma) for the 3D ortho / update kernels: one
 // thread issues a tensor copy of each input's tile plane (halo included,
-// zeros outside the domain) into a ring of STENCIL_TMA_PF + 2 stages, all
-// threads wait on the stage's mbarrier. 0: the cp.async path.
-#ifndef STENCIL_TMA
-#define STENCIL_TMA 1
+// zeros outside the domain) into a ring of STENCIL_TMA_PF + 1 stages, all
+// threads wait on the stage's mbarrier. Per kernel, the measured faster path
+// (C3 256^3, tools/ab_tma.sh): update 75.0 -> 73.7 us with TMA; ortho 89.9 us
+// with cp.async vs 94.4 us with TMA (its three inputs' whole boxes: the
+// cp.async path skips air pairs, 7% less DRAM traffic). 0: the cp.async path.
+#ifndef STENCIL_TMA_ORTHO
+#define STENCIL_TMA_ORTHO 0
+#endif
+#ifndef STENCIL_TMA_UPDATE
+#define STENCIL_TMA_UPDATE 1
 #endif
 #ifndef STENCIL_TMA_PF
-#define STENCIL_TMA_PF 1
+#define STENCIL_TMA_PF 2
 #endif
 constexpr unsigned kOut2 = 0x0C0Cu;        // pair bytes outside the domain: type 3
 
@@ -117,6 +123,7 @@ struct OrthoOp {
     static constexpr int PF = STENCIL_PF_ORTHO;  // planes prefetched ahead
     static constexpr int CS = STENCIL_ORTHO_CTR_DIRECT ? 0 : PF + 1;  // centre inputs staged in the ring
     static constexpr int TPF = STENCIL_TMA_PF;                        // TMA path: planes in flight ahead
+    static constexpr bool TMA = STENCIL_TMA_ORTHO != 0;
     const double* in[NA];
     const CUtensorMap* tin[NA];  // TMA path: the inputs' tensor maps
     const double* ctr[NC];
@@ -139,6 +146,7 @@ struct UpdateOp {
     // ring stages the block fits four per SM instead of three
     static constexpr int CS = STENCIL_UPDATE_CTR_DIRECT ? 0 : PF + 1;
     static constexpr int TPF = STENCIL_TMA_PF;
+    static constexpr bool TMA = STENCIL_TMA_UPDATE != 0;
     const double* in[NA];
     const CUtensorMap* tin[NA];
     const double* ctr[NC];
@@ -346,7 +354,7 @@ struct TmaSmem {
     static constexpr int VH = SY + 2;
     static constexpr int PLANE = VH * kVW;                               // doubles in a box
     static constexpr int PSTRIDE = ((PLANE * 8 + 127) / 128) * 128 / 8;  // box stride, 128-byte aligned
-    static constexpr int ST = Op::TPF + 2;
+    static constexpr int ST = Op::TPF + 1;
     double raw[ST][Op::NA][PSTRIDE];
     double v[4][VH][kVW];
     uint64_t bar[ST];
@@ -371,12 +379,13 @@ __device__ __forceinline__ void tma_march_init() {
     __syncthreads();
 }
 
-// stencil_march with the inputs' planes loaded by TMA (3D). A stage holds a
-// plane until the epilogue of its step has read the own cells' inputs, so
-// the ring has TPF + 2 stages: the plane issued at step z (z + TPF) reuses
-// the stage of plane z - 2, whose last reads precede step z - 1's barrier.
-// seq numbers the planes a block has issued (mbarrier phases), across
-// segments. Same epilogue interface and arithmetic as stencil_march.
+// stencil_march with the inputs' planes loaded by TMA (3D). A plane's stage
+// is read only while its operand v is formed (the own cells' inputs the
+// epilogue needs stay in registers from there), so the ring has TPF + 1
+// stages: the plane issued at step z (z + TPF) reuses the stage of plane
+// z - 1, formed before step z - 1's barrier. seq numbers the planes a block
+// has issued (mbarrier phases), across segments. Same epilogue interface and
+// arithmetic as stencil_march.
 template <int NV, int SY, typename Op, typename Epi>
 __device__ __forceinline__ void stencil_march_tma(const Geom& g, const uint8_t* __restrict__ cls, const Op& op, int tx,
                                                   int ty, int zc0, int zc1, double (&acc)[NV], unsigned& seq, Epi epi) {
@@ -424,10 +433,10 @@ __device__ __forceinline__ void stencil_march_tma(const Geom& g, const uint8_t* 
         mbar_wait(&S.bar[k % ST], (k / ST) & 1u);
     };
     auto rw = [&](int st, int a, int r, int c) -> double { return S.raw[st][a][r * kVW + c]; };
-    // v of plane z at this thread's positions (zeros outside the domain came with the box)
-    auto form = [&](int z) {
+    // v of plane z at this thread's positions (zeros outside the domain came
+    // with the box); the own pair's inputs stay in a0 / a1 for the epilogue
+    auto form = [&](int z, double (&a0)[Op::NA], double (&a1)[Op::NA]) {
         const int st = (int)(pseq(z) % ST), vs = (z + 1024) & 3;
-        double a0[Op::NA], a1[Op::NA];
 #pragma unroll
         for (int a = 0; a < Op::NA; ++a) {
             a0[a] = rw(st, a, row + 1, 2 + 2 * lane);
@@ -436,13 +445,14 @@ __device__ __forceinline__ void stencil_march_tma(const Geom& g, const uint8_t* 
         S.v[vs][row + 1][2 + 2 * lane] = op.value(a0);
         S.v[vs][row + 1][3 + 2 * lane] = op.value(a1);
         if (hkind != 0) {
+            double h0[Op::NA], h1[Op::NA];
 #pragma unroll
-            for (int a = 0; a < Op::NA; ++a) a0[a] = rw(st, a, hsr, hsc);
-            S.v[vs][hsr][hsc] = op.value(a0);
+            for (int a = 0; a < Op::NA; ++a) h0[a] = rw(st, a, hsr, hsc);
+            S.v[vs][hsr][hsc] = op.value(h0);
             if (hkind == 1) {
 #pragma unroll
-                for (int a = 0; a < Op::NA; ++a) a1[a] = rw(st, a, hsr, hsc + 1);
-                S.v[vs][hsr][hsc + 1] = op.value(a1);
+                for (int a = 0; a < Op::NA; ++a) h1[a] = rw(st, a, hsr, hsc + 1);
+                S.v[vs][hsr][hsc + 1] = op.value(h1);
             }
         }
     };
@@ -451,23 +461,32 @@ __device__ __forceinline__ void stencil_march_tma(const Geom& g, const uint8_t* 
     unsigned ob[PF + 2];  // own bytes of planes z .. z+PF+1 (rotating)
 #pragma unroll
     for (int k = 0; k < PF + 2; ++k) ob[k] = own_bytes(zc0 + k);
+    double cur0[Op::NA], cur1[Op::NA];  // the own pair's inputs of plane z (from form)
     wait(zc0 - 1);
-    form(zc0 - 1);
+    form(zc0 - 1, cur0, cur1);
     wait(zc0);
-    form(zc0);
+    form(zc0, cur0, cur1);
+    __syncthreads();  // every thread has formed plane zc0 - 1: its stage takes plane zc0 + PF next
+    // centre-only inputs straight to registers, one plane ahead of their step
+    constexpr int NCD = (Op::NC > 0) ? Op::NC : 0;
+    auto cload = [&](int z, unsigned b2, double2 (&cd)[NCD > 0 ? NCD : 1]) {
+        const bool l = own && z < zc1 && pair_live(b2);
+#pragma unroll
+        for (int a = 0; a < NCD; ++a)
+            cd[a] = l ? __ldg(reinterpret_cast<const double2*>(op.ctr[a] + z * plane + qo)) : make_double2(0.0, 0.0);
+    };
+    double2 cnext[NCD > 0 ? NCD : 1];
+    cload(zc0, ob[0], cnext);
 #pragma unroll(PF + 2)
     for (int z = zc0; z < zc1; ++z) {
-        constexpr int NCD = (Op::NC > 0) ? Op::NC : 0;
         double2 cdir[NCD > 0 ? NCD : 1];
-        if constexpr (NCD > 0) {
-            const bool l = own && pair_live(ob[0]);
 #pragma unroll
-            for (int a = 0; a < NCD; ++a)
-                cdir[a] = l ? __ldg(reinterpret_cast<const double2*>(op.ctr[a] + z * plane + qo)) : make_double2(0.0, 0.0);
-        }
+        for (int a = 0; a < (NCD > 0 ? NCD : 1); ++a) cdir[a] = cnext[a];
+        cload(z + 1, ob[1], cnext);
         issue(z + PF);
+        double nxt0[Op::NA], nxt1[Op::NA];
         wait(z + 1);
-        form(z + 1);
+        form(z + 1, nxt0, nxt1);
         __syncthreads();  // v of planes z-1, z, z+1 complete (halos included)
         const unsigned bc = ob[0];
         if (own && pair_live(bc)) {
@@ -483,13 +502,7 @@ __device__ __forceinline__ void stencil_march_tma(const Geom& g, const uint8_t* 
             sv.y = fluid(bc >> 8) ? row_sum(zm1, S.v[vc][r0 - 1][c0 + 1], v0, cls_diag(bc >> 8), v1,
                                             S.v[vc][r0][c0 + 2], S.v[vc][r0 + 1][c0 + 1], zp1)
                                   : 0.0;
-            const int sl = (int)(pseq(z) % ST);
-            double raw0[Op::NA], raw1[Op::NA], c0v[Op::NC > 0 ? Op::NC : 1] = {}, c1v[Op::NC > 0 ? Op::NC : 1] = {};
-#pragma unroll
-            for (int a = 0; a < Op::NA; ++a) {
-                raw0[a] = rw(sl, a, r0, c0);
-                raw1[a] = rw(sl, a, r0, c0 + 1);
-            }
+            double c0v[Op::NC > 0 ? Op::NC : 1] = {}, c1v[Op::NC > 0 ? Op::NC : 1] = {};
             if constexpr (NCD > 0) {
 #pragma unroll
                 for (int a = 0; a < NCD; ++a) {
@@ -497,7 +510,12 @@ __device__ __forceinline__ void stencil_march_tma(const Geom& g, const uint8_t* 
                     c1v[a] = cdir[a].y;
                 }
             }
-            epi(z * plane + qo, make_double2(v0, v1), sv, bc, raw0, raw1, c0v, c1v, acc);
+            epi(z * plane + qo, make_double2(v0, v1), sv, bc, cur0, cur1, c0v, c1v, acc);
+        }
+#pragma unroll
+        for (int a = 0; a < Op::NA; ++a) {
+            cur0[a] = nxt0[a];
+            cur1[a] = nxt1[a];
         }
 #pragma unroll
         for (int k = 0; k < PF + 1; ++k) ob[k] = ob[k + 1];
@@ -530,9 +548,9 @@ __device__ __forceinline__ void fin_ortho(SolverState* st, const double* tot) {
 }
 
 // the 3D ortho / update kernels load their operand planes with TMA
-template <int D>
+template <int D, typename Op>
 __host__ __device__ constexpr bool stencil_tma() {
-    return STENCIL_TMA != 0 && D == 3;
+    return D == 3 && Op::TMA;
 }
 
 // d' = MGS(d); Ad'; dots d'.Ad', r.d', d_j.Ad'. NO = n_ortho (cache bound).
@@ -544,7 +562,7 @@ __global__ void __launch_bounds__(kSX* SY, SY == kSY ? ORTHO_MINB : 1) k_ortho2(
                                                      unsigned int* __restrict__ counter, Sched sc,
                                                      const __grid_constant__ TmaMaps maps) {
     using Op = OrthoOp<NO>;
-    if constexpr (stencil_tma<D>()) tma_march_init<Op, SY>();
+    if constexpr (stencil_tma<D, Op>()) tma_march_init<Op, SY>();
     pdl_launch_wait();
     if (st->dist && st->done) return;
     precond_span_end(st);
@@ -586,7 +604,7 @@ __global__ void __launch_bounds__(kSX* SY, SY == kSY ? ORTHO_MINB : 1) k_ortho2(
     };
     unsigned seq = 0;
     sched_for_each(sc, [&](int tx, int ty, int zc0, int zc1) {
-        if constexpr (stencil_tma<D>())
+        if constexpr (stencil_tma<D, Op>())
             stencil_march_tma<NV, SY>(g, cls, op, tx, ty, zc0, zc1, acc, seq, epi);
         else
             stencil_march<D, NV, SY>(g, cls, op, tx, ty, zc0, zc1, acc, epi);
@@ -613,7 +631,7 @@ __global__ void UPDATE_BOUNDS k_update2(Geom g, const uint8_t* __restrict__ cls,
                                                       unsigned int* __restrict__ counter,
                                                       cudaGraphConditionalHandle cond, int use_cond, int do_norm,
                                                       Sched sc, const __grid_constant__ TmaMaps maps) {
-    if constexpr (stencil_tma<D>()) tma_march_init<UpdateOp, SY>();
+    if constexpr (stencil_tma<D, UpdateOp>()) tma_march_init<UpdateOp, SY>();
     pdl_launch_wait();
     if (st->breakdown) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0)
@@ -643,7 +661,7 @@ __global__ void UPDATE_BOUNDS k_update2(Geom g, const uint8_t* __restrict__ cls,
     };
     unsigned seq = 0;
     sched_for_each(sc, [&](int tx, int ty, int zc0, int zc1) {
-        if constexpr (stencil_tma<D>())
+        if constexpr (stencil_tma<D, UpdateOp>())
             stencil_march_tma<1, SY>(g, cls, op, tx, ty, zc0, zc1, acc, seq, epi);
         else
             stencil_march<D, 1, SY>(g, cls, op, tx, ty, zc0, zc1, acc, epi);
@@ -671,7 +689,7 @@ constexpr int march_sy() {
 // dynamic shared memory of an ortho / update launch
 template <int D, typename Op, int SY>
 constexpr size_t stencil_smem_bytes() {
-    return stencil_tma<D>() ? tma_smem_bytes<Op, SY>() : march_smem_bytes<Op, SY>();
+    return stencil_tma<D, Op>() ? tma_smem_bytes<Op, SY>() : march_smem_bytes<Op, SY>();
 }
 
 }  // namespace nb2
