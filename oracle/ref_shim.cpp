@@ -23,6 +23,7 @@
 #include "npsd/rng.hpp"
 #include "npsd/scene.hpp"
 #include "npsd/solver.hpp"
+#include "npsd/train/train.hpp"
 #include "npsd_oracle.hpp"
 
 namespace {
@@ -214,6 +215,33 @@ int ref_net_apply_2d(long nx, long ny, int depth, const float* params, long n_pa
             if (za) za[l] = ctx.levels[static_cast<std::size_t>(l)].z_a;
             if (zb) zb[l] = ctx.levels[static_cast<std::size_t>(l)].z_b;
         }
+    });
+}
+
+// The reference's hand-written training gradient (train.hpp:94-150,
+// net/backward.hpp:46-169): backward_batch<float> on the reference assembly +
+// reduce of a 2D frame, for nb reduced right-hand sides (row-major nb x n_f);
+// the mean batch loss and the gradient in for_each_span order.
+int ref_backward_2d(long nx, long ny, int depth, const float* params, long n_params, const unsigned char* types,
+                    const double* rhs, int nb, double* loss, float* grads) {
+    return guarded([&] {
+        const auto I = image_from_types(nx, ny, types);
+        const auto A = npsd::assemble_poisson(I);
+        const auto sys = npsd::reduce(A, npsd::Vector(static_cast<std::size_t>(A.n_rows), 0.0), I);
+        const std::size_t nf = static_cast<std::size_t>(sys.A.n_rows);
+        std::vector<npsd::Vector> bs(static_cast<std::size_t>(nb));
+        std::vector<const npsd::Vector*> batch;
+        for (int i = 0; i < nb; ++i) {
+            bs[static_cast<std::size_t>(i)].assign(rhs + static_cast<std::size_t>(i) * nf, rhs + (static_cast<std::size_t>(i) + 1) * nf);
+            batch.push_back(&bs[static_cast<std::size_t>(i)]);
+        }
+        auto [l, g] = npsd::backward_batch<float>(params_2d(depth, params, n_params), I, sys.A, sys.map, batch);
+        *loss = l;
+        std::size_t o = 0;
+        g.for_each_span([&](float* src, std::size_t k) {
+            std::memcpy(grads + o, src, k * sizeof(float));
+            o += k;
+        });
     });
 }
 

@@ -261,7 +261,6 @@ struct npsd_b200_ctx {
     int* icFail = nullptr;    // IC0 factorization failure flag (+ scratch)
     int ic0_shift_retries = 0;
     // tiles per schedule group (common.cuh Sched): stencil/up0 and down0 schedules
-    int sched_gx = 1, sched_gy = 1, sched0_gx = 1, sched0_gy = 1;
     unsigned long long* htk = nullptr;  // pattern hash table: keys, values (dedup_patterns)
     uint32_t* htv = nullptr;
     unsigned long long ht_alloc = 0;            // slots allocated
@@ -282,7 +281,7 @@ struct npsd_b200_ctx {
     uint32_t *dmask = nullptr, *dcount = nullptr, *dbase = nullptr;  // L0 mixed cells whose window holds fluid
     uint32_t *umask = nullptr, *ucount = nullptr, *ubase = nullptr;  // L0 mixed fluid cells
     bool fast = true;  // network arithmetic: fused/reassociated (true) or the reference's order, bitwise (false)
-    int coarse_zc_max = 4;    // NPSD_COARSE_ZC: planes per block of the z-marching coarse kernels
+    int coarse_zc_max = 4;    // planes per block of the z-marching coarse kernels (at most)
     long long slab_chunk_launches = 0;
     cudaStream_t s = nullptr, s2 = nullptr;
     std::vector<float> params;
@@ -642,9 +641,9 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
     scan_u32(c, L0.mcount, L0.mbase, L0.nseg);
     scan_u32(c, c->fcount, c->fbase, L0.nseg);
     LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), c->fbase, c->fcount, L0.nseg, &c->d_info->n_fluid);
-    build_sched(c, c->sch_stencil, kTX, kTY, 1, 0, c->sched_gx, c->sched_gy);
-    if (kMarchSY != kSY) build_sched(c, c->sch_march, kTX, kMarchSY, 1, 0, c->sched_gx, c->sched_gy);
-    if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1, c->sched0_gx, c->sched0_gy);
+    build_sched(c, c->sch_stencil, kTX, kTY, 1, 0, 1, 1);
+    if (kMarchSY != kSY) build_sched(c, c->sch_march, kTX, kMarchSY, 1, 0, 1, 1);
+    if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1, 1, 1);
     for (int l = 1; l < c->depth; ++l) {
         LevelBufs& Lf = c->L[l - 1];
         LevelBufs& Lc = c->L[l];
@@ -2129,20 +2128,6 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->S = (dim == 3) ? 27 : 9;
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
-        auto env_int = [](const char* n, int& v) {
-            if (const char* e = std::getenv(n)) {
-                const int x = std::atoi(e);
-                if (x >= 1 && x <= 16) v = x;
-            }
-        };
-        env_int("NPSD_SCHED_GX", c->sched_gx);
-        env_int("NPSD_SCHED_GY", c->sched_gy);
-        env_int("NPSD_SCHED0_GX", c->sched0_gx);
-        env_int("NPSD_SCHED0_GY", c->sched0_gy);
-        if (const char* e = std::getenv("NPSD_COARSE_ZC")) {
-            const int v = std::atoi(e);
-            if (v == 2 || v == 4 || v == 8) c->coarse_zc_max = v;
-        }
         if (slab) {
             c->slab = *slab;
             for (int l = 0; l < depth; ++l) c->slab.ghost[l] = 1 << (depth - 1 - l);

@@ -50,10 +50,6 @@ __global__ void __launch_bounds__(kBlock) k_gather(Geom g, const uint8_t* __rest
         if (cls_type(cls[c]) == 0) red[mixed_index(fmask, fbase, c)] = full[c];
 }
 
-__global__ void __launch_bounds__(kBlock) k_scatter_f32(Geom g, const float* __restrict__ src, float* __restrict__ dst) {
-    FOR_OWNED(g, c) dst[c] = src[c];
-}
-
 // zero non-fluid entries (enforces the invariant on caller-provided full vectors)
 __global__ void __launch_bounds__(kBlock) k_mask_fluid(Geom g, const uint8_t* __restrict__ cls, const double* __restrict__ src,
                                                        double* __restrict__ dst) {

@@ -245,6 +245,8 @@ class Ref:
         L.ref_net_apply_2d.argtypes = [C.c_long, C.c_long, C.c_int, _f32p, C.c_long, _u8p, _f32p, _f32p,
                                        _f32p, _f32p]
         L.ref_precond_apply_2d.argtypes = [C.c_long, C.c_long, C.c_int, _f32p, C.c_long, _u8p, _f64p, _f64p]
+        L.ref_backward_2d.argtypes = [C.c_long, C.c_long, C.c_int, _f32p, C.c_long, _u8p, _f64p, C.c_int,
+                                      C.POINTER(C.c_double), _f32p]
         L.ref_spmv.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, _f64p, _f64p]
         L.ref_psdo_solve.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, _u8p, C.c_int, C.c_int, C.c_void_p,
                                      C.c_long, C.c_void_p, C.c_void_p, _f64p, C.c_void_p, C.c_double, C.c_double,
@@ -333,6 +335,18 @@ class Ref:
         self._check(self.lib.ref_precond_apply_2d(nx, ny, depth, np.ascontiguousarray(params, np.float32),
                                                   len(params), _u8(types), r, z))
         return z
+
+    def backward_2d(self, types, params, depth, rhs):
+        """backward_batch<float> (train.hpp:94-150): (mean batch loss, gradient
+        in for_each_span order) for reduced right-hand sides rhs (nb, n_f)."""
+        ny, nx = types.shape
+        params = np.ascontiguousarray(params, np.float32)
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        loss = C.c_double()
+        grads = np.zeros_like(params)
+        self._check(self.lib.ref_backward_2d(nx, ny, depth, params, params.size, _u8(types), rhs.reshape(-1),
+                                             rhs.shape[0], C.byref(loss), grads))
+        return loss.value, grads
 
     def spmv(self, types, x):
         dim, (nx, ny, nz) = _dims_of(types)

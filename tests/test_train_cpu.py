@@ -25,3 +25,37 @@ def test_torch_network_and_operator_match_oracle(oracle):
     full[t.reshape(-1) == 0] = v
     av = train.poisson(geo, torch.tensor(full.reshape(t.shape))[None])[0].numpy().reshape(-1)
     assert np.allclose(av[t.reshape(-1) == 0], oracle.spmv(t, v), rtol=0, atol=1e-12)
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("depth", [2, 3])
+def test_loss_and_gradient_match_reference_backward(ref, depth):
+    """The torch restatement's loss and autograd gradient against the
+    reference's hand-written backward pass (backward_batch<float>,
+    train.hpp:94-150 over net/backward.hpp:46-169) on a 2D mixed-BC frame:
+    same weights, same right-hand sides, the reference's un-normalised loss."""
+    from paper_2310_00177_b200 import train
+
+    n = 32
+    c = np.arange(n) + 0.5
+    y, x = np.meshgrid(c, c, indexing="ij")
+    t = np.zeros((n, n), np.uint8)
+    t[y >= 0.7 * n] = 1
+    t[(x < 0.3 * n) & (y < 0.25 * n)] = 2
+    t[0, :] = t[-1, :] = t[:, 0] = t[:, -1] = 2
+    p = ref.init_params_2d(depth, 5)
+    fl = t.reshape(-1) == 0
+    rhs = np.stack([ref.rhs_normal(100 + i, t.size)[fl] for i in range(4)])
+    want_loss, want_g = ref.backward_2d(t, p, depth, rhs)
+
+    geo = train.Geometry(t, depth, torch.device("cpu"))
+    flat = torch.tensor(p, requires_grad=True)
+    b = torch.zeros((4, t.size), dtype=torch.float64)
+    b[:, torch.tensor(fl)] = torch.tensor(rhs)
+    L = train.loss(train.unflatten(flat, depth, dim=2), geo, b.view(4, n, n), depth, normalize=False)
+    L.backward()
+    got = flat.grad.numpy()
+    assert abs(L.item() - want_loss) <= 1e-5 * want_loss
+    assert np.linalg.norm(got - want_g) <= 1e-4 * np.linalg.norm(want_g)
+    # the comparison is not vacuous: most weights get a gradient
+    assert np.count_nonzero(want_g) > 0.5 * want_g.size

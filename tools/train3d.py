@@ -66,6 +66,9 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--big", type=int, default=0, help="extra 2n^3 training frames (scale robustness)")
     ap.add_argument("--eval256", action="store_true")
+    ap.add_argument("--ritz-m", type=int, default=0, help="Lanczos steps of the Ritz-vector RHS sets (0: smoothed noise)")
+    ap.add_argument("--ritz-every", type=int, default=1, help="Ritz sets on every k-th frame")
+    ap.add_argument("--big-only", action="store_true", help="train on the 2n^3 frames only")
     ap.add_argument("--out", default=str(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm"))
     a = ap.parse_args()
     dev = torch.device("cuda")
@@ -89,14 +92,18 @@ def main() -> None:
     else:
         init = b200.load_npm(a.init).flat
     t0 = time.time()
-    flat = train.train(frames, a.depth, a.steps, a.lr, init, a.batch, a.seed, dev, max_sweeps=a.max_sweeps)
+    if a.big_only:
+        frames = [f for f in frames if f.shape[0] == 2 * a.n]
+    flat = train.train(frames, a.depth, a.steps, a.lr, init, a.batch, a.seed, dev, max_sweeps=a.max_sweeps,
+                       ritz_m=a.ritz_m, ritz_every=a.ritz_every)
     wall = time.time() - t0
     params = b200.NetParams(3, a.depth, flat.astype(np.float32))
     out = Path(a.out)
     out.parent.mkdir(parents=True, exist_ok=True)
     b200.save_npm(params, out)
     report = {"train_seconds": wall, "steps": a.steps, "frames": a.frames, "n": a.n, "big_frames": a.big,
-              "init": a.init, "lr": a.lr, "batch": a.batch, "max_sweeps": a.max_sweeps, "seed": a.seed, "eval": {}}
+              "big_only": a.big_only, "init": a.init, "lr": a.lr, "batch": a.batch, "max_sweeps": a.max_sweeps,
+              "ritz_m": a.ritz_m, "ritz_every": a.ritz_every, "seed": a.seed, "eval": {}}
     ident = b200.identity_params(a.depth)
     evals = [("C3", 64), ("C3", 128), ("C1", 64), ("C2", 128)] + ([("C3", 256)] if a.eval256 else [])
     for name, n in evals:
