@@ -84,7 +84,16 @@ def phase_of(kernel: str) -> str:
         return "P4"
     if kernel == "update":
         return "P5"
+    if kernel == "net_coarse_chain":
+        return "P2"  # every coarse level in one launch
     return "P2_" + kernel[len("net_"):]
+
+
+def phase_bytes(model: dict, phase: str) -> float:
+    """bytes of a phase in a per-kernel model; "P2" = all coarse kernels"""
+    if phase == "P2":
+        return sum(v for k, v in model.items() if k.startswith("P2_"))
+    return model[phase]
 
 
 def ncu_traffic(kernels: list, n: int):
@@ -456,8 +465,8 @@ def run_b200(args) -> None:
         phase_ms[ph] = phase_ms.get(ph, 0.0) + v
         phase_kernels.setdefault(ph, []).append(k)
     dom = max(phase_ms, key=phase_ms.get)
-    dom_bytes = processed_bytes(depth, n_c, n_f)[dom]
-    dom_canon = canonical_bytes_per_cell(depth)[dom] * n_c
+    dom_bytes = phase_bytes(processed_bytes(depth, n_c, n_f), dom)
+    dom_canon = phase_bytes(canonical_bytes_per_cell(depth), dom) * n_c
     dom_gbs = dom_bytes / (phase_ms[dom] * 1e-3) / 1e9
     prof_total = sum(prof.values())
     dom_traffic = ncu_traffic(phase_kernels[dom], types.shape[0])

@@ -282,6 +282,8 @@ struct npsd_b200_ctx {
     uint32_t *umask = nullptr, *ucount = nullptr, *ubase = nullptr;  // L0 mixed fluid cells
     bool fast = true;  // network arithmetic: fused/reassociated (true) or the reference's order, bitwise (false)
     int coarse_zc_max = 4;    // planes per block of the z-marching coarse kernels (at most)
+    bool chain = true;        // coarse levels as one cooperative launch (NPSD_CHAIN=0: one launch per level)
+    unsigned* chain_bar = nullptr;  // its grid barrier [count, generation]
     long long slab_chunk_launches = 0;
     cudaStream_t s = nullptr, s2 = nullptr;
     std::vector<float> params;
@@ -976,6 +978,56 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
     LAUNCH3(c, s, k, grid, block, L.g, in_f, in_d, c->st, tab_down(c, l), kc, L.y, xnext, gc, zc, occ);
 }
 
+// the coarse levels 1 .. L-1 of the solve's network as one cooperative launch
+// (coarse.cuh k_coarse_chain): used on single-domain 3D contexts of depth
+// 3 .. kChainMax + 1
+bool coarse_chain_on(const npsd_b200_ctx* c) {
+    return c->chain && !c->slab.on && c->dim == 3 && c->depth >= 3 && c->depth - 1 <= kChainMax;
+}
+
+void launch_coarse_chain(npsd_b200_ctx* c, cudaStream_t s) {
+    ChainArgs a{};
+    a.n = c->depth - 1;
+    int tiles = 1;
+    for (int i = 0; i < a.n; ++i) {
+        const int l = i + 1;
+        const LevelBufs& L = c->L[l];
+        const bool last = l == c->depth - 1;
+        ChainLevel& v = a.lv[i];
+        v.g = L.g;
+        v.gc = last ? L.g : c->L[l + 1].g;
+        v.x = L.x;
+        v.y = L.y;
+        v.xnext = last ? nullptr : c->L[l + 1].x;
+        v.out = L.out;
+        v.outc = last ? nullptr : ((l + 1 == c->depth - 1) ? c->L[l + 1].y : c->L[l + 1].out);
+        v.zab = c->zab + 2 * l;
+        v.ctd = tab_down(c, l);
+        v.ctu = last ? ConvTab{} : tab_up(c, l);
+        v.kcd = last ? c->kc_coarse : c->kc_down[l];
+        v.kcu = c->kc_up[l];
+        v.zc = coarse_zc(c, L.g);
+        tiles = std::max(tiles, ((L.g.nx + kZX - 1) / kZX) * ((L.g.ny + kZY - 1) / kZY) *
+                                    ((L.g.zo1 - L.g.zo0 + v.zc - 1) / v.zc));
+    }
+    a.bar = c->chain_bar;
+    auto k = c->fast ? k_coarse_chain<true> : k_coarse_chain<false>;
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kZT, 0));
+    const int grid = std::max(1, std::min(tiles, c->num_sms * std::max(occ, 1)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kZT);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;  // every block resident: the grid barriers
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k, a));
+    ++c->launches;
+}
+
 template <int D, int MODE, int NO>
 void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dout) {
     LevelBufs& L = c->L[l];
@@ -1164,7 +1216,12 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     const bool xg = c->slab.on && !raw;  // z-slab: halos before every conv level
     // solve path: level-0 mixed-window cells are computed apart (mixed.cuh)
     if (!raw) v.push_back({"net_mixed_down_L0", [c](cudaStream_t s) { launch_mixed_down0<D>(c, s); }});
+    const bool chain = !raw && coarse_chain_on(c);
     for (int l = 0; l < Ld; ++l) {
+        if (chain && l >= 1) {
+            if (l == 1) v.push_back({"net_coarse_chain", [c](cudaStream_t s) { launch_coarse_chain(c, s); }});
+            continue;
+        }
         const bool pool = (l + 1 < Ld);
         const std::string nm = (l == Ld - 1) ? "net_coarse_L" + std::to_string(l) : "net_down_L" + std::to_string(l);
         v.push_back({nm, [c, l, pool, raw](cudaStream_t s) {
@@ -1191,6 +1248,7 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
                                   l));
     }
     for (int l = Ld - 2; l >= 0; --l) {
+        if (chain && l >= 1) continue;  // inside the chain
         v.push_back({"net_up_L" + std::to_string(l), [c, l, raw, no](cudaStream_t s) {
                          if (l == 0 && !raw)
                              launch_up0_no<D>(c, s, no);
@@ -1995,6 +2053,7 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->slab.allu);
     F(c->mac);
     F(c->check_flag);
+    F(c->chain_bar);
     F(c->cgP0);
     F(c->cgP1);
     F(c->cgAp);
@@ -2128,6 +2187,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->S = (dim == 3) ? 27 : 9;
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
+        if (const char* e = std::getenv("NPSD_CHAIN")) c->chain = (e[0] != '0');
         if (slab) {
             c->slab = *slab;
             for (int l = 0; l < depth; ++l) c->slab.ghost[l] = 1 << (depth - 1 - l);
@@ -2267,6 +2327,8 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->Dtmp = dalloc<double>(n);
         c->red_a = dalloc<double>(n);
         c->red_b = dalloc<double>(n);
+        c->chain_bar = dalloc<unsigned>(2);
+        CK(cudaMemset(c->chain_bar, 0, 2 * sizeof(unsigned)));
         c->st = dalloc<SolverState>(1);
         CK(cudaMemset(c->st, 0, sizeof(SolverState)));
         CK(cudaMallocHost(&c->st_host, sizeof(SolverState)));

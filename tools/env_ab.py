@@ -1,6 +1,6 @@
-"""Per-iteration device time of the solve graph with and without programmatic
-dependent launch (NPSD_PDL, read at context creation) on C1/C2/C3:
-    python tools/pdl_ab.py"""
+"""Per-iteration device time of the solve graph under a context-creation
+environment switch (NPSD_PDL, NPSD_CHAIN, ...) on C1/C2/C3:
+    python tools/pdl_ab.py [VAR] [values...]   (default: NPSD_PDL 0 1)"""
 import os
 import sys
 from pathlib import Path
@@ -16,8 +16,9 @@ W = b200.load_npm(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm")
 for name in ("C1", "C2", "C3"):
     t, seed = scenes.config(name)
     b = b200.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
-    for pdl in ("0", "1"):
-        os.environ["NPSD_PDL"] = pdl
+    var = sys.argv[1] if len(sys.argv) > 1 else "NPSD_PDL"
+    for pdl in (sys.argv[2:] or ["0", "1"]):
+        os.environ[var] = pdl
         ctx = b200.Context(3, t.shape, W)
         ctx.set_mask(t)
         ms = []
@@ -25,5 +26,5 @@ for name in ("C1", "C2", "C3"):
             rep = ctx.psdo_solve(b, b200.SolveConfig(max_iters=2000)).report
             if i:
                 ms.append(ctx.last_solve_ms / rep.iterations)
-        print(f"{name} pdl={pdl} iters={rep.iterations} per-iter {np.median(ms) * 1e3:.1f} us", flush=True)
+        print(f"{name} {var}={pdl} iters={rep.iterations} per-iter {np.median(ms) * 1e3:.1f} us", flush=True)
         ctx.close()
