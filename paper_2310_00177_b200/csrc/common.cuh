@@ -267,9 +267,10 @@ struct Sched {
 // take the same share of group-column units, one tile each, so neighbouring
 // tiles are marched at the same time and their halo rows and columns come
 // from L2 instead of DRAM.
+// bid / nblk: this block's index among the nblk blocks sharing the schedule
 template <typename F>
-__device__ __forceinline__ void sched_for_each(const Sched& sc, F f) {
-    const int G = sc.gx * sc.gy, Q = gridDim.x / G, q = blockIdx.x / G, m = blockIdx.x - q * G;
+__device__ __forceinline__ void sched_for_each_n(const Sched& sc, int bid, int nblk, F f) {
+    const int G = sc.gx * sc.gy, Q = nblk / G, q = bid / G, m = bid - q * G;
     if (q >= Q) return;
     const long long W = sc.pre[sc.npiece];
     long long s = W * q / Q;
@@ -293,6 +294,10 @@ __device__ __forceinline__ void sched_for_each(const Sched& sc, F f) {
         if (tx < sc.tnx && ty < sc.tny) f(tx, ty, u0, u0 + (int)n);
         s += n;
     }
+}
+template <typename F>
+__device__ __forceinline__ void sched_for_each(const Sched& sc, F f) {
+    sched_for_each_n(sc, blockIdx.x, gridDim.x, f);
 }
 
 }  // namespace nb2

@@ -217,6 +217,44 @@ __global__ void __launch_bounds__(kBlock) k_ident_dir(Geom g, const uint8_t* __r
     }
 }
 
+// d at the mixed fluid cells i = start, start + stride, ... of the up list, with
+// their dots d.Ad_j accumulated into acc (k_mixed_up0, and the mixed blocks
+// of k_up_l0m)
+template <int D, int NO, bool F>
+__device__ __forceinline__ void mixed_up_cells(const Geom& g, const Geom& gc, const uint32_t* __restrict__ list,
+                                               uint32_t n, const float* __restrict__ outc,
+                                               const float* __restrict__ y0, float za, float zb,
+                                               const float* __restrict__ tab, const uint32_t* __restrict__ kid,
+                                               double* __restrict__ dout, double nrm, int nc,
+                                               const double* const (&adp)[(NO > 0) ? NO : 1],
+                                               double (&acc)[(NO > 0) ? NO : 1], long long start, long long stride) {
+    constexpr int S = Sh<D>::S;
+    for (long long i = start; i < n; i += stride) {
+        const uint32_t c = list[i];
+        const float* K = tab + (long long)__ldg(kid + i) * kRowW;
+        int x, yy, z;
+        decode32(g, c, x, yy, z);
+        float w[S], k[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
+            const int xx = x + dx, y2 = yy + dy, zz = z + dz;
+            // upsample2: fine (xx, y2, zz) -> coarse (xx>>1, y2>>1, zz>>1); zero outside
+            const bool in = xx >= 0 && xx < g.nx && y2 >= 0 && y2 < g.ny && zz >= 0 && zz < g.nz;
+            w[s] = in ? __ldg(outc + lin(gc, xx >> 1, y2 >> 1, (D == 3) ? zz >> 1 : 0)) : 0.0f;
+            k[s] = __ldg(K + s);
+        }
+        const float u = win_dot<F, S>([&](int t) { return k[t]; }, [&](int t) { return w[t]; });
+        const float o = F ? __fmaf_rn(za, __ldg(y0 + c), __fmul_rn(zb, u))
+                          : __fadd_rn(__fmul_rn(za, __ldg(y0 + c)), __fmul_rn(zb, u));
+        const double dv = __dmul_rn((double)o, nrm);
+        dout[c] = dv;
+#pragma unroll
+        for (int j = 0; j < NO; ++j)
+            if (j < nc) acc[j] += dv * __ldg(adp[j] + c);
+    }
+}
+
 template <int D, int NO, bool F>
 #ifndef MIXUP_MINB
 #define MIXUP_MINB 4  // register cap for 4 blocks/SM (measured 26 -> 24 us)
@@ -246,30 +284,8 @@ __global__ void __launch_bounds__(kBlock, MIXUP_MINB) k_mixed_up0(Geom g, Geom g
 #pragma unroll
     for (int j = 0; j < NA; ++j) acc[j] = 0.0;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint32_t c = list[i];
-        const float* K = tab + (long long)__ldg(kid + i) * kRowW;
-        int x, yy, z;
-        decode32(g, c, x, yy, z);
-        float w[S], k[S];
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
-            const int xx = x + dx, y2 = yy + dy, zz = z + dz;
-            // upsample2: fine (xx, y2, zz) -> coarse (xx>>1, y2>>1, zz>>1); zero outside
-            const bool in = xx >= 0 && xx < g.nx && y2 >= 0 && y2 < g.ny && zz >= 0 && zz < g.nz;
-            w[s] = in ? __ldg(outc + lin(gc, xx >> 1, y2 >> 1, (D == 3) ? zz >> 1 : 0)) : 0.0f;
-            k[s] = __ldg(K + s);
-        }
-        const float u = win_dot<F, S>([&](int t) { return k[t]; }, [&](int t) { return w[t]; });
-        const float o = F ? __fmaf_rn(za, __ldg(y0 + c), __fmul_rn(zb, u))
-                          : __fadd_rn(__fmul_rn(za, __ldg(y0 + c)), __fmul_rn(zb, u));
-        const double dv = __dmul_rn((double)o, nrm);
-        dout[c] = dv;
-#pragma unroll
-        for (int j = 0; j < NO; ++j)
-            if (j < nc) acc[j] += dv * __ldg(adp[j] + c);
-    }
+    mixed_up_cells<D, NO, F>(g, gc, list, n, outc, y0, za, zb, tab, kid, dout, nrm, nc, adp, acc,
+                             (long long)blockIdx.x * blockDim.x + threadIdx.x, stride);
     double tot[NA];
     if (grid_reduce<NA>(acc, partials, counter, tot) && threadIdx.x == 0) {
         // totals of the tiled kernel first, then this kernel's (fixed order)

@@ -283,6 +283,7 @@ struct npsd_b200_ctx {
     bool fast = true;  // network arithmetic: fused/reassociated (true) or the reference's order, bitwise (false)
     int coarse_zc_max = 4;    // planes per block of the z-marching coarse kernels (at most)
     bool chain = true;        // coarse levels as one cooperative launch (NPSD_CHAIN=0: one launch per level)
+    bool merge_up0 = true;    // level-0 up: tiled and mixed cells in one launch (NPSD_MERGE_UP0=0: two)
     unsigned* chain_bar = nullptr;  // its grid barrier [count, generation]
     long long slab_chunk_launches = 0;
     cudaStream_t s = nullptr, s2 = nullptr;
@@ -1088,10 +1089,22 @@ void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
         const LevelBufs& L = c->L[0];
         const LevelBufs& L1 = c->L[1];
         const float* outc = (c->depth == 2) ? L1.y : L1.out;
-        auto k = c->fast ? k_up_l0<NO, true> : k_up_l0<NO, false>;
-        const size_t sm = sizeof(Up0Smem<NO>);
-        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         const KUp0 kc0 = up0_kernel(c->kc_up[0].k[0]);  // the uniform-fluid kernel (+ merged parity taps)
+        const size_t sm = sizeof(Up0Smem<NO>);
+        if (c->merge_up0) {
+            // tiled and mixed cells in one launch (k_up_l0m): a wave of tile
+            // blocks plus one block per SM for the mixed list
+            auto k = c->fast ? k_up_l0m<NO, true> : k_up_l0m<NO, false>;
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            const int nt = wave_blocks(c, k, kSX * kSY, sm);
+            launch_pdl(c, s, k, dim3(nt + c->num_sms), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y, c->zab, kc0,
+                       c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_stencil.view(), nt,
+                       (const uint32_t*)c->ulist0, (const uint32_t*)c->ucnt0, (const float*)L.tab_up,
+                       (const uint32_t*)c->ukid0);
+            return;
+        }
+        auto k = c->fast ? k_up_l0<NO, true> : k_up_l0<NO, false>;
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         launch_pdl(c, s, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y,
                    c->zab, kc0, c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_stencil.view());
         return;
@@ -1259,7 +1272,7 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
             v.push_back(xchg_step(c, "xchg_out_L" + std::to_string(l), [c, l] { return (void*)c->L[l].out; },
                                   sizeof(float), l));
     }
-    if (!raw && Ld > 1)
+    if (!raw && Ld > 1 && !(D == 3 && c->merge_up0))
         v.push_back({"net_mixed_up_L0", [c, no](cudaStream_t s) { launch_mixed_up0_no<D>(c, s, no); }});
     if (Ld == 1 && !raw) {
         v.push_back({"net_out_L0", [c](cudaStream_t s) {
@@ -2188,6 +2201,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
         if (const char* e = std::getenv("NPSD_CHAIN")) c->chain = (e[0] != '0');
+        if (const char* e = std::getenv("NPSD_MERGE_UP0")) c->merge_up0 = (e[0] != '0');
         if (slab) {
             c->slab = *slab;
             for (int l = 0; l < depth; ++l) c->slab.ghost[l] = 1 << (depth - 1 - l);

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "down0.cuh"
+#include "mixed.cuh"
 #include "stencil.cuh"
 
 namespace nb2 {
@@ -212,6 +213,53 @@ __global__ void UP0_BOUNDS k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ 
     // projections from these totals plus its own
     if (grid_reduce<NA>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0)
         for (int j = 0; j < NA; ++j) st->dot_main[j] = tot[j];
+}
+
+// k_up_l0 and k_mixed_up0 as one launch: blocks [0, nb_tiled) march the
+// uniform-fluid tiles, the others take the mixed fluid cells of the up list;
+// one grid reduction over all blocks gives the dots d.Ad_j and the MGS
+// projections (the two kernels' cell sets are disjoint, so nothing waits).
+template <int NO, bool F>
+__global__ void UP0_BOUNDS k_up_l0m(Geom g, Geom gc, const uint8_t* __restrict__ cls, const float* __restrict__ outc,
+                                     const float* __restrict__ y0, const float* __restrict__ zab,
+                                     const __grid_constant__ KUp0 kc, double* __restrict__ dout, SolverState* st,
+                                     const double* __restrict__ ADring, double* __restrict__ partials,
+                                     unsigned int* __restrict__ counter, Sched sc, int nb_tiled,
+                                     const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
+                                     const float* __restrict__ tab, const uint32_t* __restrict__ ukid) {
+    constexpr int NA = (NO > 0) ? NO : 1;
+    pdl_launch_wait();
+    if (st->dist && st->done) return;
+    const float za = zab[0], zb = zab[1];
+    const double nrm = st->nrm;
+    const int nc = st->n_cache, R = st->ring;
+    const double* adp[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+        const int slot = (st->head - (nc - 1) + j + 2 * R) % R;
+        adp[j] = ADring + (long long)slot * g.n;
+    }
+    double acc[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+    if ((int)blockIdx.x < nb_tiled) {
+        sched_for_each_n(sc, blockIdx.x, nb_tiled, [&](int tx, int ty, int u0, int u1) {
+            up_l0_segment<NO, F>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, u0, u1);
+        });
+    } else {
+        const int tid = threadIdx.y * kSX + threadIdx.x;
+        const long long nthr = (long long)(gridDim.x - nb_tiled) * (kSX * kSY);
+        mixed_up_cells<3, NO, F>(g, gc, ulist, *ucount, outc, y0, za, zb, tab, ukid, dout, nrm, nc, adp, acc,
+                                 (long long)(blockIdx.x - nb_tiled) * (kSX * kSY) + tid, nthr);
+    }
+    double tot[NA];
+    if (grid_reduce<NA, kSX * kSY>(acc, partials, counter, tot) && threadIdx.x == 0 && threadIdx.y == 0) {
+        if (st->dist) {
+            for (int j = 0; j < kMaxOrtho; ++j) st->part[j] = (j < nc && j < NO) ? tot[j] : 0.0;
+        } else {
+            fin_projections(st, tot);
+        }
+    }
 }
 
 }  // namespace nb2

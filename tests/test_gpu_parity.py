@@ -536,3 +536,23 @@ def test_coarse_chain_equals_per_level_launches(b200, oracle, exact, monkeypatch
         ctx.close()
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1].report.residual_history, out[1][1].report.residual_history)
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_merged_up0_equals_two_launches(b200, oracle, exact, monkeypatch):
+    """Level-0 up: tiled and mixed cells in one launch (k_up_l0m) give the
+    same direction as two launches; the MGS dots are one deterministic
+    reduction instead of two (histories agree to rounding)."""
+    t, seed = scenes.config("C3", 64)
+    p = b200.init_params(4, 29)
+    b = oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
+    out = []
+    for merge in ("1", "0"):
+        monkeypatch.setenv("NPSD_MERGE_UP0", merge)
+        ctx = b200.Context(3, t.shape, p, exact=exact)
+        ctx.set_mask(t)
+        out.append((ctx.precond_apply(b), ctx.psdo_solve(b, b200.SolveConfig(max_iters=15, tol_reduction=1e-300))))
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    h, w = out[0][1].report.residual_history, out[1][1].report.residual_history
+    assert np.max(np.abs(h - w) / w) <= 1e-9
