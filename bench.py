@@ -84,8 +84,6 @@ def phase_of(kernel: str) -> str:
         return "P4"
     if kernel == "update":
         return "P5"
-    if kernel == "net_coarse_chain":
-        return "P2"  # every coarse level in one launch
     return "P2_" + kernel[len("net_"):]
 
 

@@ -70,9 +70,7 @@ constexpr int kZSP = 48;                           // padded shared row stride (
 // (NZ x NY x NX) box at (bx, by, bz) of gg, zero outside the grid, staged
 // into dst[NZ][NY][kZSP]; one warp per row. load() issues every load (into
 // registers) so that other independent loads can be issued before store().
-// NC: read-only (non-coherent) loads; false inside the fused coarse chain,
-// whose phases read what earlier phases of the same launch wrote (L2 loads)
-template <int NX, int NY, int NZ, bool NC = true>
+template <int NX, int NY, int NZ>
 struct ZStager {
     static constexpr int NW = kZT / 32, ROWS = NY * NZ, RPW = (ROWS + NW - 1) / NW, EPL = (NX + 31) / 32;
     float v[RPW][EPL];
@@ -93,9 +91,7 @@ struct ZStager {
 #pragma unroll
             for (int e = 0; e < EPL; ++e) {
                 const int lx = lane + 32 * e;
-                v[k][e] = (rin && lx < NX && (unsigned)(bx + lx) < (unsigned)gg.nx)
-                              ? (NC ? __ldg(rowp + lx) : __ldcg(rowp + lx))
-                              : 0.0f;
+                v[k][e] = (rin && lx < NX && (unsigned)(bx + lx) < (unsigned)gg.nx) ? __ldg(rowp + lx) : 0.0f;
             }
         }
     }
@@ -144,7 +140,7 @@ struct CUpSmem {
 };
 
 // one 32 x 8 x ZC tile (bx, by, bz) of a down step; S in shared memory
-template <bool POOL, int ZC, bool F, bool NC>
+template <bool POOL, int ZC, bool F>
 __device__ __forceinline__ void cdownz_tile(const Geom& g, const float* __restrict__ x, const ConvTab& ct, const KC& kc,
                                             float* __restrict__ y, float* __restrict__ xnext, const Geom& gc, int bx,
                                             int by, int bz, CDownSmem<ZC>& S) {
@@ -161,7 +157,7 @@ __device__ __forceinline__ void cdownz_tile(const Geom& g, const float* __restri
     const long long c0 = oxy ? lin(g, cx, cy, Z0) : 0;
     const int nown = oxy ? min(ZC, g.zo1 - Z0) : 0;  // planes of this column the rank owns
     // every load of the prologue is in flight before the first use
-    ZStager<SX, SY, SZ, NC> box;
+    ZStager<SX, SY, SZ> box;
     box.load(x, g, X0 - 1, Y0 - 1, Z0 - 1, warp, lane);
     uint32_t rc[ZC];
 #pragma unroll
@@ -228,11 +224,11 @@ __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cdownz(Geom g, const floa
     pdl_launch_wait();
     if (done && *done) return;  // z-slab chunked loop: the solve has finished
     __shared__ __align__(16) CDownSmem<ZC> S;
-    cdownz_tile<POOL, ZC, F, true>(g, x, ct, kc, y, xnext, gc, blockIdx.x, blockIdx.y, blockIdx.z, S);
+    cdownz_tile<POOL, ZC, F>(g, x, ct, kc, y, xnext, gc, blockIdx.x, blockIdx.y, blockIdx.z, S);
 }
 
 // one tile of an up step (outc is level l+1)
-template <int ZC, bool F, bool NC>
+template <int ZC, bool F>
 __device__ __forceinline__ void cupz_tile(const Geom& g, const Geom& gc, const float* __restrict__ outc,
                                           const float* __restrict__ yl, const float* __restrict__ zab,
                                           const ConvTab& ct, const KC& kc, float* __restrict__ outl, int bx, int by,
@@ -251,14 +247,14 @@ __device__ __forceinline__ void cupz_tile(const Geom& g, const Geom& gc, const f
     const long long c0 = oxy ? lin(g, cx, cy, Z0) : 0;
     const int nown = oxy ? min(ZC, g.zo1 - Z0) : 0;  // planes of this column the rank owns
     // every load of the prologue is in flight before the first use
-    ZStager<CX, CY, CZ, NC> box;
+    ZStager<CX, CY, CZ> box;
     box.load(outc, gc, (X0 >> 1) - 1, (Y0 >> 1) - 1, (Z0 >> 1) - 1, warp, lane);
     uint32_t rc[ZC];
     float yv[ZC];
 #pragma unroll
     for (int k = 0; k < ZC; ++k) {
         rc[k] = cell_code(ct, c0 + k * plane, k < nown);
-        yv[k] = k < nown ? (NC ? __ldg(yl + c0 + k * plane) : __ldcg(yl + c0 + k * plane)) : 0.0f;
+        yv[k] = k < nown ? __ldg(yl + c0 + k * plane) : 0.0f;
     }
     load_uni_rows(U, kc, tid);
     const float za = zab[0], zb = zab[1];
@@ -308,102 +304,7 @@ __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cupz(Geom g, Geom gc, con
     pdl_launch_wait();
     if (done && *done) return;  // z-slab chunked loop: the solve has finished
     __shared__ __align__(16) CUpSmem<ZC> S;
-    cupz_tile<ZC, F, true>(g, gc, outc, yl, zab, ct, kc, outl, blockIdx.x, blockIdx.y, blockIdx.z, S);
-}
-
-// ---------------------------------------------------------------------------
-// The coarse levels as one launch (single-domain solve): down steps l = 1 ..
-// L-2 (with pooling), the coarsest conv, up steps L-2 .. 1, with a grid-wide
-// barrier between dependent steps instead of a kernel boundary. The blocks
-// (all resident: cooperative launch) walk each step's tiles; the tile bodies
-// are those of k_cdownz / k_cupz with L2 loads for data the launch itself
-// wrote. Small grids are latency-bound and pay a kernel boundary per level;
-// here they pay a barrier.
-constexpr int kChainMax = 4;  // coarse levels fused (depth <= 5)
-struct ChainLevel {
-    Geom g, gc;                // level l and l+1
-    const float* x;            // down input (l = 1: the L0 kernel's pooled x_1)
-    float *y, *xnext, *out;    // y_l, x_{l+1}, out_l (levels < L-1)
-    const float* outc;         // up input: out_{l+1} (or y of the coarsest level)
-    const float* zab;          // z_a, z_b of level l
-    ConvTab ctd, ctu;
-    KC kcd, kcu;
-    int zc;                    // planes per tile (2, 4, 8)
-};
-struct ChainArgs {
-    ChainLevel lv[kChainMax];  // levels 1 .. L-1 (lv[0] is level 1)
-    int n;                     // coarse levels: L - 1
-    unsigned* bar;             // grid barrier: [count, generation]
-};
-
-// sense-reversing grid barrier (every block resident)
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0u;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g) __nanosleep(32);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ int chain_tiles(const ChainLevel& L) {
-    return ((L.g.nx + kZX - 1) / kZX) * ((L.g.ny + kZY - 1) / kZY) * ((L.g.zo1 - L.g.zo0 + L.zc - 1) / L.zc);
-}
-
-template <bool F>
-__global__ void __launch_bounds__(kZT, 2) k_coarse_chain(const __grid_constant__ ChainArgs a) {
-    pdl_launch_wait();
-    __shared__ __align__(16) union {
-        CDownSmem<8> d8;
-        CDownSmem<4> d4;
-        CDownSmem<2> d2;
-        CUpSmem<8> u8;
-        CUpSmem<4> u4;
-        CUpSmem<2> u2;
-    } S;
-    auto walk = [&](const ChainLevel& L, auto body) {
-        const int gx = (L.g.nx + kZX - 1) / kZX, gy = (L.g.ny + kZY - 1) / kZY, nt = chain_tiles(L);
-        for (int t = blockIdx.x; t < nt; t += gridDim.x) {
-            __syncthreads();  // the previous tile's reads of S are done
-            body(t % gx, (t / gx) % gy, t / (gx * gy));
-        }
-    };
-    // down steps with pooling, then the coarsest conv
-    for (int i = 0; i < a.n; ++i) {
-        const ChainLevel& L = a.lv[i];
-        const bool pool = i + 1 < a.n;
-        walk(L, [&](int bx, int by, int bz) {
-            if (pool) {
-                if (L.zc == 8) cdownz_tile<true, 8, F, false>(L.g, L.x, L.ctd, L.kcd, L.y, L.xnext, L.gc, bx, by, bz, S.d8);
-                else if (L.zc == 4) cdownz_tile<true, 4, F, false>(L.g, L.x, L.ctd, L.kcd, L.y, L.xnext, L.gc, bx, by, bz, S.d4);
-                else cdownz_tile<true, 2, F, false>(L.g, L.x, L.ctd, L.kcd, L.y, L.xnext, L.gc, bx, by, bz, S.d2);
-            } else {
-                if (L.zc == 8) cdownz_tile<false, 8, F, false>(L.g, L.x, L.ctd, L.kcd, L.y, nullptr, L.g, bx, by, bz, S.d8);
-                else if (L.zc == 4) cdownz_tile<false, 4, F, false>(L.g, L.x, L.ctd, L.kcd, L.y, nullptr, L.g, bx, by, bz, S.d4);
-                else cdownz_tile<false, 2, F, false>(L.g, L.x, L.ctd, L.kcd, L.y, nullptr, L.g, bx, by, bz, S.d2);
-            }
-        });
-        grid_barrier(a.bar);
-    }
-    // up steps, coarse to fine (level 1's output is the L0 kernels' input)
-    for (int i = a.n - 2; i >= 0; --i) {
-        const ChainLevel& L = a.lv[i];
-        walk(L, [&](int bx, int by, int bz) {
-            if (L.zc == 8) cupz_tile<8, F, false>(L.g, L.gc, L.outc, L.y, L.zab, L.ctu, L.kcu, L.out, bx, by, bz, S.u8);
-            else if (L.zc == 4) cupz_tile<4, F, false>(L.g, L.gc, L.outc, L.y, L.zab, L.ctu, L.kcu, L.out, bx, by, bz, S.u4);
-            else cupz_tile<2, F, false>(L.g, L.gc, L.outc, L.y, L.zab, L.ctu, L.kcu, L.out, bx, by, bz, S.u2);
-        });
-        if (i > 0) grid_barrier(a.bar);
-    }
+    cupz_tile<ZC, F>(g, gc, outc, yl, zab, ct, kc, outl, blockIdx.x, blockIdx.y, blockIdx.z, S);
 }
 
 }  // namespace nb2

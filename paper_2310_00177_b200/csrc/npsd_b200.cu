@@ -282,9 +282,8 @@ struct npsd_b200_ctx {
     uint32_t *umask = nullptr, *ucount = nullptr, *ubase = nullptr;  // L0 mixed fluid cells
     bool fast = true;  // network arithmetic: fused/reassociated (true) or the reference's order, bitwise (false)
     int coarse_zc_max = 4;    // planes per block of the z-marching coarse kernels (at most)
-    bool chain = true;        // coarse levels as one cooperative launch (NPSD_CHAIN=0: one launch per level)
     bool merge_up0 = true;    // level-0 up: tiled and mixed cells in one launch (NPSD_MERGE_UP0=0: two)
-    unsigned* chain_bar = nullptr;  // its grid barrier [count, generation]
+    int up0_mixb = 0;         // its mixed-list blocks per SM (NPSD_UP0_MIXB; 0: by grid size, up0_mixed_blocks)
     long long slab_chunk_launches = 0;
     cudaStream_t s = nullptr, s2 = nullptr;
     std::vector<float> params;
@@ -979,56 +978,6 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
     LAUNCH3(c, s, k, grid, block, L.g, in_f, in_d, c->st, tab_down(c, l), kc, L.y, xnext, gc, zc, occ);
 }
 
-// the coarse levels 1 .. L-1 of the solve's network as one cooperative launch
-// (coarse.cuh k_coarse_chain): used on single-domain 3D contexts of depth
-// 3 .. kChainMax + 1
-bool coarse_chain_on(const npsd_b200_ctx* c) {
-    return c->chain && !c->slab.on && c->dim == 3 && c->depth >= 3 && c->depth - 1 <= kChainMax;
-}
-
-void launch_coarse_chain(npsd_b200_ctx* c, cudaStream_t s) {
-    ChainArgs a{};
-    a.n = c->depth - 1;
-    int tiles = 1;
-    for (int i = 0; i < a.n; ++i) {
-        const int l = i + 1;
-        const LevelBufs& L = c->L[l];
-        const bool last = l == c->depth - 1;
-        ChainLevel& v = a.lv[i];
-        v.g = L.g;
-        v.gc = last ? L.g : c->L[l + 1].g;
-        v.x = L.x;
-        v.y = L.y;
-        v.xnext = last ? nullptr : c->L[l + 1].x;
-        v.out = L.out;
-        v.outc = last ? nullptr : ((l + 1 == c->depth - 1) ? c->L[l + 1].y : c->L[l + 1].out);
-        v.zab = c->zab + 2 * l;
-        v.ctd = tab_down(c, l);
-        v.ctu = last ? ConvTab{} : tab_up(c, l);
-        v.kcd = last ? c->kc_coarse : c->kc_down[l];
-        v.kcu = c->kc_up[l];
-        v.zc = coarse_zc(c, L.g);
-        tiles = std::max(tiles, ((L.g.nx + kZX - 1) / kZX) * ((L.g.ny + kZY - 1) / kZY) *
-                                    ((L.g.zo1 - L.g.zo0 + v.zc - 1) / v.zc));
-    }
-    a.bar = c->chain_bar;
-    auto k = c->fast ? k_coarse_chain<true> : k_coarse_chain<false>;
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kZT, 0));
-    const int grid = std::max(1, std::min(tiles, c->num_sms * std::max(occ, 1)));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kZT);
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;  // every block resident: the grid barriers
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, k, a));
-    ++c->launches;
-}
-
 template <int D, int MODE, int NO>
 void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dout) {
     LevelBufs& L = c->L[l];
@@ -1097,7 +1046,10 @@ void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
             auto k = c->fast ? k_up_l0m<NO, true> : k_up_l0m<NO, false>;
             CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             const int nt = wave_blocks(c, k, kSX * kSY, sm);
-            launch_pdl(c, s, k, dim3(nt + c->num_sms), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y, c->zab, kc0,
+            // mixed-list blocks per SM: measured best 1 at 64^3, 2 at 128^3, 4 at 256^3
+            // (C1/C2/C3, tools/env_ab.py NPSD_UP0_MIXB): about one per 2^20 cells, 1..4
+            const int mixb = c->up0_mixb ? c->up0_mixb : (int)std::max(1LL, std::min(4LL, L.g.n >> 20));
+            launch_pdl(c, s, k, dim3(nt + mixb * c->num_sms), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y, c->zab, kc0,
                        c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_stencil.view(), nt,
                        (const uint32_t*)c->ulist0, (const uint32_t*)c->ucnt0, (const float*)L.tab_up,
                        (const uint32_t*)c->ukid0);
@@ -1229,12 +1181,7 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     const bool xg = c->slab.on && !raw;  // z-slab: halos before every conv level
     // solve path: level-0 mixed-window cells are computed apart (mixed.cuh)
     if (!raw) v.push_back({"net_mixed_down_L0", [c](cudaStream_t s) { launch_mixed_down0<D>(c, s); }});
-    const bool chain = !raw && coarse_chain_on(c);
     for (int l = 0; l < Ld; ++l) {
-        if (chain && l >= 1) {
-            if (l == 1) v.push_back({"net_coarse_chain", [c](cudaStream_t s) { launch_coarse_chain(c, s); }});
-            continue;
-        }
         const bool pool = (l + 1 < Ld);
         const std::string nm = (l == Ld - 1) ? "net_coarse_L" + std::to_string(l) : "net_down_L" + std::to_string(l);
         v.push_back({nm, [c, l, pool, raw](cudaStream_t s) {
@@ -1261,7 +1208,6 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
                                   l));
     }
     for (int l = Ld - 2; l >= 0; --l) {
-        if (chain && l >= 1) continue;  // inside the chain
         v.push_back({"net_up_L" + std::to_string(l), [c, l, raw, no](cudaStream_t s) {
                          if (l == 0 && !raw)
                              launch_up0_no<D>(c, s, no);
@@ -2066,7 +2012,6 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->slab.allu);
     F(c->mac);
     F(c->check_flag);
-    F(c->chain_bar);
     F(c->cgP0);
     F(c->cgP1);
     F(c->cgAp);
@@ -2200,8 +2145,8 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->S = (dim == 3) ? 27 : 9;
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
-        if (const char* e = std::getenv("NPSD_CHAIN")) c->chain = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_MERGE_UP0")) c->merge_up0 = (e[0] != '0');
+        if (const char* e = std::getenv("NPSD_UP0_MIXB")) c->up0_mixb = std::max(0, std::min(16, std::atoi(e)));
         if (slab) {
             c->slab = *slab;
             for (int l = 0; l < depth; ++l) c->slab.ghost[l] = 1 << (depth - 1 - l);
@@ -2341,8 +2286,6 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->Dtmp = dalloc<double>(n);
         c->red_a = dalloc<double>(n);
         c->red_b = dalloc<double>(n);
-        c->chain_bar = dalloc<unsigned>(2);
-        CK(cudaMemset(c->chain_bar, 0, 2 * sizeof(unsigned)));
         c->st = dalloc<SolverState>(1);
         CK(cudaMemset(c->st, 0, sizeof(SolverState)));
         CK(cudaMallocHost(&c->st_host, sizeof(SolverState)));

@@ -520,25 +520,6 @@ def test_set_params_between_solves(b200, oracle):
 
 
 @pytest.mark.parametrize("exact", [True, False])
-def test_coarse_chain_equals_per_level_launches(b200, oracle, exact, monkeypatch):
-    """The coarse levels as one cooperative launch (k_coarse_chain, grid
-    barriers between levels) compute the same bits as one launch per level."""
-    t, seed = scenes.config("C2", 64)
-    p = b200.init_params(4, 23)
-    r = np.random.default_rng(9).standard_normal(int((t == 0).sum()))
-    out = []
-    for chain in ("1", "0"):
-        monkeypatch.setenv("NPSD_CHAIN", chain)
-        ctx = b200.Context(3, t.shape, p, exact=exact)
-        ctx.set_mask(t)
-        out.append((ctx.precond_apply(r), ctx.psdo_solve(oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0],
-                                                         b200.SolveConfig(max_iters=10, tol_reduction=1e-300))))
-        ctx.close()
-    assert np.array_equal(out[0][0], out[1][0])
-    assert np.array_equal(out[0][1].report.residual_history, out[1][1].report.residual_history)
-
-
-@pytest.mark.parametrize("exact", [True, False])
 def test_merged_up0_equals_two_launches(b200, oracle, exact, monkeypatch):
     """Level-0 up: tiled and mixed cells in one launch (k_up_l0m) give the
     same direction as two launches; the MGS dots are one deterministic
