@@ -116,12 +116,6 @@ __global__ void __launch_bounds__(kBlock) k_row_codes(Geom g, const uint8_t* __r
     }
 }
 
-// number of mixed cells = last exclusive base + last count
-__global__ void k_seg_total(const uint32_t* __restrict__ base, const uint32_t* __restrict__ cnt, long long nseg,
-                            uint32_t* __restrict__ out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) *out = base[nseg - 1] + cnt[nseg - 1];
-}
-
 __device__ __forceinline__ void decode32(const Geom& g, uint32_t c, int& x, int& y, int& z) {
     const uint32_t nx = (uint32_t)g.nx, ny = (uint32_t)g.ny;
     const uint32_t row = c / nx;

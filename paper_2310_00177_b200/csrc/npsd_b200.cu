@@ -563,7 +563,8 @@ void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int 
         sb.tny = tny;
         sb.pre = dalloc<int>((size_t)sb.npiece + 1);
         sb.zlo = dalloc<int>((size_t)sb.npiece);
-        sb.len = dalloc<int>((size_t)sb.npiece);
+        sb.len = dalloc<int>((size_t)sb.npiece + 1);  // len[npiece] = 0: the scan leaves the total in pre[npiece]
+        CK(cudaMemset(sb.len, 0, ((size_t)sb.npiece + 1) * sizeof(int)));
         sb.first = dalloc<int>((size_t)sb.ncol);
         sb.last = dalloc<int>((size_t)sb.ncol);
     }
@@ -575,13 +576,10 @@ void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int 
                                                                          g.zo0, g.zo1, unit, zdil, sb.zlo, sb.len);
     CK(cudaGetLastError());
     c->launches += 2;
-    // exclusive prefix (lengths are non-negative: scanned as u32), then the total
+    // exclusive prefix (lengths are non-negative: scanned as u32), total included
     auto* len = reinterpret_cast<uint32_t*>(sb.len);
     auto* pre = reinterpret_cast<uint32_t*>(sb.pre);
-    scan_u32(c, len, pre, sb.npiece);
-    k_seg_total<<<1, 32, 0, c->s>>>(pre, len, sb.npiece, pre + sb.npiece);
-    CK(cudaGetLastError());
-    ++c->launches;
+    scan_u32(c, len, pre, sb.npiece + 1);
 }
 
 // one wave of k's blocks (the schedule's grid)
@@ -640,9 +638,8 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
                c->tflags);
     }
-    scan_u32(c, L0.mcount, L0.mbase, L0.nseg);
-    scan_u32(c, c->fcount, c->fbase, L0.nseg);
-    LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), c->fbase, c->fcount, L0.nseg, &c->d_info->n_fluid);
+    scan_u32(c, L0.mcount, L0.mbase, L0.nseg + 1);  // totals land in base[nseg]
+    scan_u32(c, c->fcount, c->fbase, L0.nseg + 1);
     build_sched(c, c->sch_stencil, kTX, kTY, 1, 0, 1, 1);
     if (kMarchSY != kSY) build_sched(c, c->sch_march, kTX, kMarchSY, 1, 0, 1, 1);
     if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1, 1, 1);
@@ -671,14 +668,12 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         } else {
             LAUNCH(c, s, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
         }
-        scan_u32(c, Lc.mcount, Lc.mbase, Lc.nseg);
+        scan_u32(c, Lc.mcount, Lc.mbase, Lc.nseg + 1);
     }
     // compact mixed-cell lists per level
     for (int l = 0; l < c->depth; ++l) {
         LevelBufs& L = c->L[l];
         LAUNCH(c, s, k_mixed_list, L.nseg, L.nseg, (const uint32_t*)L.mmask, (const uint32_t*)L.mbase, L.mlist);
-        LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), L.mbase, L.mcount, L.nseg, L.mcnt);
-        CK(cudaMemcpyAsync(&c->d_info->n_mixed[l], L.mcnt, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     }
     // level 0: window-pattern dictionary (pid per mixed cell, one row per pattern),
     // then the solve's down / up sublists with their pattern ids
@@ -687,12 +682,11 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
     dedup_patterns(c, s, 0, L0.mcnt, L0.mlist, c->pid0, c->repcell0, c->npat0);
     CK(cudaMemcpyAsync(&c->d_info->npat[0], c->npat0, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     if (!march0) LAUNCH(c, s, k_sub_masks, L0.g.n, L0.g, L0.cls, c->dmask, c->dcount, c->umask, c->ucount);
-    scan_u32(c, c->dcount, c->dbase, L0.nseg);
-    scan_u32(c, c->ucount, c->ubase, L0.nseg);
+    scan_u32(c, c->dcount, c->dbase, L0.nseg + 1);
+    scan_u32(c, c->ucount, c->ubase, L0.nseg + 1);
     LAUNCH(c, s, k_mixed_sub, std::min<long long>(c->g0.n, (long long)c->cap_ht[0]), L0.mlist, c->pid0, L0.mcnt,
            c->dmask, c->dbase, c->umask, c->ubase, c->dlist0, c->dkid0, c->ulist0, c->ukid0);
-    LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), c->dbase, c->dcount, L0.nseg, c->dcnt0);
-    LAUNCH3(c, s, k_seg_total, dim3(1), dim3(32), c->ubase, c->ucount, L0.nseg, c->ucnt0);
+    ZfinArgs zf{};
     for (int l = 0; l < c->depth; ++l) {
         LevelBufs& L = c->L[l];
         const uint8_t* st = (l == 0) ? dtypes : nullptr;
@@ -716,13 +710,12 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         }
         const long long row_items = 32LL * std::min<long long>(rows_cap, L.g.n);
         if (l < c->depth - 1) {
+            // the down and up kernels' rows of the same windows, one launch
             const LevelOffsets& o = c->offs[(size_t)l];
             LAUNCH(c, s, k_build_rows<D>, row_items, L.g, st, im, cells, ncells, (const uint32_t*)L.mlist,
                    (const uint32_t*)L.mcnt, unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + o.down_W,
-                   c->d_params + o.down_B, L.tab_down);
-            LAUNCH(c, s, k_build_rows<D>, row_items, L.g, st, im, cells, ncells, (const uint32_t*)L.mlist,
-                   (const uint32_t*)L.mcnt, unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + o.up_W,
-                   c->d_params + o.up_B, L.tab_up);
+                   c->d_params + o.down_B, L.tab_down, (const float*)(c->d_params + o.up_W),
+                   (const float*)(c->d_params + o.up_B), L.tab_up);
             constexpr int NC = (D == 3) ? 27 : 9;
             const double scale = std::ldexp(1.0, D * l);
             if (!march0) {
@@ -732,15 +725,22 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
                         c->gglob[l].nz, L.zG);
             }
             if (c->slab.on) slab_allreduce_u64(c, s, L.zG, 3 * NC);
-            LAUNCH3(c, s, k_zfinal<D>, dim3(1), dim3(128), c->gglob[l], (const unsigned long long*)L.zG, scale,
-                    c->d_params + o.a_K, c->params[o.a_bias], c->d_params + o.b_K, c->params[o.b_bias], c->zab + 2 * l,
-                    c->zab + 2 * l + 1);
+            zf.lv[l] = ZfinLevel{c->gglob[l], L.zG, scale, c->d_params + o.a_K, c->d_params + o.b_K,
+                                 c->params[o.a_bias], c->params[o.b_bias], c->zab + 2 * l, c->zab + 2 * l + 1};
         } else {
             LAUNCH(c, s, k_build_rows<D>, row_items, L.g, st, im, cells, ncells, (const uint32_t*)L.mlist,
                    (const uint32_t*)L.mcnt, unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + c->coarse_W,
-                   c->d_params + c->coarse_B, L.tab_down);
+                   c->d_params + c->coarse_B, L.tab_down, (const float*)nullptr, (const float*)nullptr,
+                   (float*)nullptr);
         }
     }
+    // linear-block coefficients of every level (k_zfinal: one block per level)
+    if (c->depth > 1) LAUNCH3(c, s, k_zfinal<D>, dim3(c->depth - 1), dim3(128), zf);
+    InfoSources src{};
+    src.n_fluid = c->fbase + L0.nseg;
+    src.depth = c->depth;
+    for (int l = 0; l < c->depth; ++l) src.n_mixed[l] = c->L[l].mcnt;
+    LAUNCH3(c, s, k_setup_info, dim3(1), dim3(32), src, c->d_info);
     // zero invariant of the solver vectors at the new non-fluid cells
     const size_t nb = (size_t)c->g0.n * sizeof(double);
     CK(cudaMemsetAsync(c->X1, 0, nb, s));
@@ -1287,18 +1287,18 @@ std::vector<Step> prologue_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h,
     // projections (solver.cpp:197-201), r0 = b - A x0, ||r0||
     if (nullspace) {
         v.push_back({"proj_b_sum", [=](cudaStream_t s) {
-                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->Bf, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->Bf, (const uint32_t*)(c->fbase + c->L[0].nseg), c->st, c->partials, c->counter);
                      }});
         v.push_back({"proj_b_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->Bf, c->st); }});
         v.push_back({"proj_x_sum", [=](cudaStream_t s) {
-                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->X0, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->X0, (const uint32_t*)(c->fbase + c->L[0].nseg), c->st, c->partials, c->counter);
                      }});
         v.push_back({"proj_x_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->X0, c->st); }});
     }
     v.push_back({"residual0", [=](cudaStream_t s) { LAUNCH(c, s, k_residual<D>, g.n, g, cls, c->Bf, c->X0, c->R); }});
     if (nullspace) {
         v.push_back({"proj_r0_sum", [=](cudaStream_t s) {
-                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, (const uint32_t*)(c->fbase + c->L[0].nseg), c->st, c->partials, c->counter);
                      }});
         v.push_back({"proj_r0_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->R, c->st); }});
     }
@@ -1318,7 +1318,7 @@ std::vector<Step> body_steps(npsd_b200_ctx* c, cudaGraphConditionalHandle h, int
     v.push_back({"update", [=](cudaStream_t s) { launch_update<D>(c, s, h, use_cond, nullspace ? 0 : 1); }});
     if (nullspace) {
         v.push_back({"proj_r_sum", [=](cudaStream_t s) {
-                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
+                         LAUNCH(c, s, k_fluid_sum, g.n, g, cls, c->R, (const uint32_t*)(c->fbase + c->L[0].nseg), c->st, c->partials, c->counter);
                      }});
         v.push_back({"proj_r_sub", [=](cudaStream_t s) { LAUNCH(c, s, k_subtract_mean, g.n, g, cls, c->R, c->st); }});
         v.push_back({"norm", [=](cudaStream_t s) {
@@ -1529,7 +1529,7 @@ int solve_device_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b20
 // rank-ordered totals, subtract
 void slab_project(npsd_b200_ctx* c, cudaStream_t s, double* v) {
     const Geom g = c->g0;
-    LAUNCH(c, s, k_fluid_sum, g.n, g, c->L[0].cls, v, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
+    LAUNCH(c, s, k_fluid_sum, g.n, g, c->L[0].cls, v, (const uint32_t*)(c->fbase + c->L[0].nseg), c->st, c->partials, c->counter);
     slab_reduce(c, s, kFinMean);
     LAUNCH(c, s, k_subtract_mean, g.n, g, c->L[0].cls, v, c->st);
 }
@@ -1798,7 +1798,7 @@ void capture_cg_graph(npsd_b200_ctx* c, int ns) {
     CK(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
     // mean_project(v) (vector_ops.cpp:33-43) as two kernels
     auto project = [&](cudaStream_t st, double* v) {
-        LAUNCH(c, st, k_fluid_sum, g.n, g, cls, v, (const uint32_t*)&c->d_info->n_fluid, c->st, c->partials, c->counter);
+        LAUNCH(c, st, k_fluid_sum, g.n, g, cls, v, (const uint32_t*)(c->fbase + c->L[0].nseg), c->st, c->partials, c->counter);
         LAUNCH(c, st, k_subtract_mean, g.n, g, cls, v, c->st);
     };
     // prologue (solver.cpp:38-58): [projections of b, x0], r0 = b - A x0,
@@ -2055,7 +2055,6 @@ void free_ctx(npsd_b200_ctx* c) {
         F(L.mlist);
         F(L.rcode);
         F(L.pid);
-        F(L.mcnt);
     }
     F(c->d_params);
     F(c->zab);
@@ -2064,8 +2063,7 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->fcount);
     F(c->tflags);
     for (void* p : {(void*)c->dkeys, (void*)c->dvals, (void*)c->pid0, (void*)c->repcell0, (void*)c->npat0,
-                    (void*)c->dlist0, (void*)c->dkid0, (void*)c->dcnt0, (void*)c->ulist0, (void*)c->ukid0,
-                    (void*)c->ucnt0, (void*)c->crep, (void*)c->cnpat, (void*)c->dmask, (void*)c->dcount,
+                    (void*)c->dlist0, (void*)c->dkid0, (void*)c->ulist0, (void*)c->ukid0, (void*)c->crep, (void*)c->cnpat, (void*)c->dmask, (void*)c->dcount,
                     (void*)c->dbase, (void*)c->umask, (void*)c->ucount, (void*)c->ubase, (void*)c->d_info,
                     (void*)c->types_dev})
         F(p);
@@ -2206,14 +2204,17 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
             } else {
                 L.cls = dalloc<uint8_t>(nl);
             }
+            // counts and bases carry one trailing entry: count 0, so the scan
+            // leaves the total in base[nseg] (mcnt points there)
             L.mmask = dalloc<uint32_t>((size_t)L.nseg);
-            L.mbase = dalloc<uint32_t>((size_t)L.nseg);
-            L.mcount = dalloc<uint32_t>((size_t)L.nseg);
+            L.mbase = dalloc<uint32_t>((size_t)L.nseg + 1);
+            L.mcount = dalloc<uint32_t>((size_t)L.nseg + 1);
+            CK(cudaMemset(L.mcount, 0, ((size_t)L.nseg + 1) * sizeof(uint32_t)));
             if (l > 0) L.img = dalloc<float>(3 * (size_t)L.g.n);
             // kernel-row tables: allocated at the capacities set_mask uses (ensure_setup_capacity)
             L.mlist = dalloc<uint32_t>((size_t)L.g.n);
             if (l > 0) L.pid = dalloc<uint32_t>((size_t)L.g.n);
-            L.mcnt = dalloc<uint32_t>(1);
+            L.mcnt = L.mbase + L.nseg;
             L.kc_down = dalloc<float>(3 * (size_t)c->S);
             L.kc_up = dalloc<float>(3 * (size_t)c->S);
             if (l == 0) {
@@ -2247,16 +2248,21 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         CK(cudaMemset(c->zab, 0, 2 * (size_t)depth * sizeof(float)));
         const long long nseg0 = c->L[0].nseg;
         c->fmask = dalloc<uint32_t>((size_t)nseg0);
-        c->fbase = dalloc<uint32_t>((size_t)nseg0);
-        c->fcount = dalloc<uint32_t>((size_t)nseg0);
+        c->fbase = dalloc<uint32_t>((size_t)nseg0 + 1);
+        c->fcount = dalloc<uint32_t>((size_t)nseg0 + 1);
+        CK(cudaMemset(c->fcount, 0, ((size_t)nseg0 + 1) * sizeof(uint32_t)));
         c->tf_ntx = (nx + kFlagTX - 1) / kFlagTX;
         c->tf_nty = (ny + kFlagTY - 1) / kFlagTY;
         // every local plane: a z-slab's ghost planes are flagged too (k_classify_march, k_tile_flags)
         c->tflags = dalloc<uint8_t>((size_t)c->tf_ntx * c->tf_nty * c->L[0].g.nz);
         c->dkeys = dalloc<unsigned long long>((size_t)c->g0.n);
         c->dvals = dalloc<uint32_t>((size_t)c->g0.n);
-        for (uint32_t** v : {&c->dmask, &c->dcount, &c->dbase, &c->umask, &c->ucount, &c->ubase})
-            *v = dalloc<uint32_t>((size_t)nseg0);
+        for (uint32_t** v : {&c->dmask, &c->dcount, &c->dbase, &c->umask, &c->ucount, &c->ubase}) {
+            *v = dalloc<uint32_t>((size_t)nseg0 + 1);
+            CK(cudaMemset(*v, 0, ((size_t)nseg0 + 1) * sizeof(uint32_t)));
+        }
+        c->dcnt0 = c->dbase + nseg0;  // the scans' trailing totals
+        c->ucnt0 = c->ubase + nseg0;
         c->d_info = dalloc<SetupInfo>(1);
         CK(cudaMallocHost(&c->info_host, sizeof(SetupInfo)));
         CK(cudaEventCreateWithFlags(&c->ev_setup, cudaEventDisableTiming));
@@ -2272,11 +2278,9 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->dkid0 = dalloc<uint32_t>((size_t)c->g0.n);
         c->ulist0 = dalloc<uint32_t>((size_t)c->g0.n);
         c->ukid0 = dalloc<uint32_t>((size_t)c->g0.n);
-        c->dcnt0 = dalloc<uint32_t>(1);
         c->crep = dalloc<uint32_t>((size_t)std::max<long long>(c->depth > 1 ? c->L[1].g.n : 1, 1));
         c->cnpat = dalloc<uint32_t>(1);
         c->check_flag = dalloc<unsigned int>(1);
-        c->ucnt0 = dalloc<uint32_t>(1);
         c->npat0 = dalloc<uint32_t>(1);
         const size_t n = (size_t)c->g0.n;
         c->X0 = dalloc<double>(n);

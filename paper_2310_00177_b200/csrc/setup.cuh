@@ -31,6 +31,18 @@ struct SetupInfo {
     uint32_t unverified[kMaxDepth];  // levels >= 1: a window differs from its pattern's (per-cell rows)
 };
 
+// the frame's totals (scans' trailing entries) into SetupInfo, one launch
+struct InfoSources {
+    const uint32_t* n_fluid;
+    const uint32_t* n_mixed[kMaxDepth];
+    int depth;
+};
+__global__ void k_setup_info(InfoSources src, SetupInfo* info) {
+    const int t = threadIdx.x;
+    if (t == 0) info->n_fluid = *src.n_fluid;
+    if (t < src.depth) info->n_mixed[t] = *src.n_mixed[t];
+}
+
 
 // L0: cell byte (window class, own type, stencil diagonal) plus 32-cell
 // segment masks of mixed cells and of fluid cells.
@@ -465,7 +477,8 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(Geom g, const uint8_t* __
                                                        const uint32_t* __restrict__ unverified, uint32_t rows_cap,
                                                        uint32_t* __restrict__ flags, uint32_t flag_bit,
                                                        const float* __restrict__ W, const float* __restrict__ B,
-                                                       float* __restrict__ tab) {
+                                                       float* __restrict__ tab, const float* __restrict__ W2,
+                                                       const float* __restrict__ B2, float* __restrict__ tab2) {
     const bool pc = unverified && *unverified;
     const uint32_t* cells = pc ? cells_pc : cells_dict;
     const uint32_t* count = pc ? count_pc : count_dict;
@@ -473,8 +486,8 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(Geom g, const uint8_t* __
     // accumulates slot s in the reference order B[s] + sum_{ch, t} W[s,ch,t] I
     constexpr int S = Sh<D>::S;
     constexpr int NW = kBlock / 32;
-    __shared__ float sW[S * 3 * S];
-    __shared__ float sB[S];
+    __shared__ float sW[2][S * 3 * S];  // the conv's weights; [1]: the optional second conv (W2)
+    __shared__ float sB[2][S];
     __shared__ float win[NW][3][S];
     long long n = *count;
     if (n > rows_cap) {
@@ -483,8 +496,15 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(Geom g, const uint8_t* __
     }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if ((long long)blockIdx.x * NW >= n) return;  // grid sized for the capacity
-    for (int i = threadIdx.x; i < S * 3 * S; i += blockDim.x) sW[i] = W[i];
-    for (int i = threadIdx.x; i < S; i += blockDim.x) sB[i] = B[i];
+    const int nconv = W2 ? 2 : 1;
+    for (int i = threadIdx.x; i < S * 3 * S; i += blockDim.x) {
+        sW[0][i] = W[i];
+        if (W2) sW[1][i] = W2[i];
+    }
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        sB[0][i] = B[i];
+        if (B2) sB[1][i] = B2[i];
+    }
     __syncthreads();
     for (long long ii = (long long)blockIdx.x * NW + wid; ii < n; ii += (long long)gridDim.x * NW) {
         const long long c = cells[ii];
@@ -517,13 +537,15 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(Geom g, const uint8_t* __
         __syncwarp();
         if (lane < S) {
             const int sl = lane;
-            float acc = sB[sl];
-            const float* w = sW + sl * 3 * S;
+            for (int v = 0; v < nconv; ++v) {
+                float acc = sB[v][sl];
+                const float* w = sW[v] + sl * 3 * S;
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch)
+                for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
-                for (int t = 0; t < S; ++t) acc = __fadd_rn(acc, __fmul_rn(w[ch * S + t], win[wid][ch][t]));
-            tab[ii * kRowW + sl] = acc;
+                    for (int t = 0; t < S; ++t) acc = __fadd_rn(acc, __fmul_rn(w[ch * S + t], win[wid][ch][t]));
+                (v ? tab2 : tab)[ii * kRowW + sl] = acc;
+            }
         }
         __syncwarp();
     }
@@ -591,13 +613,14 @@ __global__ void __launch_bounds__(kBlock) k_window_hash(Geom g, const float* __r
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const long long c = list[i];
         const int x = (int)(c % g.nx), y = (int)((c / g.nx) % g.ny), z = (int)(c / ((long long)g.nx * g.ny));
-        unsigned long long h = 0x6a09e667f3bcc909ull;
+        // multiply-xor over the 81 values (FNV-1a order), one avalanche at the
+        // end: collisions only cost the dictionary (k_verify_windows)
+        unsigned long long h = 0xcbf29ce484222325ull;
+#pragma unroll 3
         for (int t = 0; t < Sh<D>::S; ++t)
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch)
-                h = mix64(h ^ ((unsigned long long)window_bits<D>(g, img, x, y, z, t, ch) +
-                               ((unsigned long long)(3 * t + ch) << 40)));
-        keys[i] = h;
+            for (int ch = 0; ch < 3; ++ch) h = (h ^ window_bits<D>(g, img, x, y, z, t, ch)) * 0x100000001b3ull;
+        keys[i] = mix64(h);
         vals[i] = (uint32_t)i;
     }
 }
@@ -792,15 +815,33 @@ __global__ void __launch_bounds__(kBlock) k_zsums(Geom g, const uint8_t* __restr
 
 // z_a / z_b of one level (net/forward.hpp:78-86) from the class counts.
 // F[c,w] = sum of I_pad(c, p + w) over interior p, exact in f64, then f32.
+// every level's linear-block coefficients in one launch: block l = level l
+struct ZfinLevel {
+    Geom g;                          // the level's full grid
+    const unsigned long long* G;     // window-class counts
+    double scale;                    // 8^l (4^l in 2D)
+    const float *KA, *KB;            // lin_a / lin_b kernels
+    float biasA, biasB;
+    float *za, *zb;
+};
+struct ZfinArgs {
+    ZfinLevel lv[kMaxDepth];
+};
+
 template <int D>
-__global__ void k_zfinal(Geom g, const unsigned long long* __restrict__ G, double scale,
-                         const float* __restrict__ KA, float biasA, const float* __restrict__ KB, float biasB,
-                         float* __restrict__ za_out, float* __restrict__ zb_out) {
+__global__ void k_zfinal(const __grid_constant__ ZfinArgs a) {
     constexpr int S = Sh<D>::S;
     constexpr int NC = (D == 3) ? 27 : 9;
+    const ZfinLevel& L = a.lv[blockIdx.x];
+    const Geom g = L.g;
+    const double scale = L.scale;
     __shared__ unsigned long long sG[3 * NC];
-    __shared__ float F[3 * S];
-    for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x) sG[i] = G[i];
+    __shared__ float F[3 * S], sKA[3 * S], sKB[3 * S];
+    for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x) sG[i] = L.G[i];
+    for (int i = threadIdx.x; i < 3 * S; i += blockDim.x) {
+        sKA[i] = L.KA[i];
+        sKB[i] = L.KB[i];
+    }
     __syncthreads();
     // one thread per (channel, tap): F = the exact count of the shifted box
     for (int i = threadIdx.x; i < 3 * S; i += blockDim.x) {
@@ -827,16 +868,16 @@ __global__ void k_zfinal(Geom g, const unsigned long long* __restrict__ G, doubl
         F[i] = (float)f;
     }
     __syncthreads();
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (threadIdx.x != 0) return;
     // z = bias + sum_t (norm * K[t]) * F[t], serial in t (forward.hpp:78-86)
     const float norm = __fdiv_rn(1.0f, __fmul_rn((float)S, __ll2float_rn(g.n)));
-    float za = biasA, zb = biasB;
+    float za = L.biasA, zb = L.biasB;
     for (int t = 0; t < 3 * S; ++t) {
-        za = __fadd_rn(za, __fmul_rn(__fmul_rn(norm, KA[t]), F[t]));
-        zb = __fadd_rn(zb, __fmul_rn(__fmul_rn(norm, KB[t]), F[t]));
+        za = __fadd_rn(za, __fmul_rn(__fmul_rn(norm, sKA[t]), F[t]));
+        zb = __fadd_rn(zb, __fmul_rn(__fmul_rn(norm, sKB[t]), F[t]));
     }
-    *za_out = za;
-    *zb_out = zb;
+    *L.za = za;
+    *L.zb = zb;
 }
 
 }  // namespace nb2
