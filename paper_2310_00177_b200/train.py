@@ -222,7 +222,12 @@ class RitzSet:
         T = torch.diag(alpha) + torch.diag(beta[: m - 1], 1) + torch.diag(beta[: m - 1], -1)
         theta, S = torch.linalg.eigh(T)  # ascending
         self.theta = theta
-        self.Y = (Q.T @ S).float()  # (nf, m), Ritz vectors by ascending Ritz value
+        # Ritz vectors Y = Q^T S by ascending Ritz value, (nf, m), in row chunks
+        # and stored as bf16 (a training set of random combinations needs no more)
+        self.Y = torch.empty((nf, m), dtype=torch.bfloat16, device=dev)
+        for r0 in range(0, nf, 1 << 20):
+            self.Y[r0:r0 + (1 << 20)] = (Q[:, r0:r0 + (1 << 20)].T @ S).to(torch.bfloat16)
+        del Q
         w = torch.ones(m, dtype=torch.float32, device=dev)
         w[: m // 2] = low_weight
         self.weight = w
@@ -234,7 +239,7 @@ class RitzSet:
 
     def sample(self, nb: int, gen: torch.Generator) -> torch.Tensor:
         c = torch.randn((self.Y.shape[1], nb), generator=gen, device=self.Y.device) * self.weight[:, None]
-        bf = (self.Y @ c).double().T  # (nb, nf)
+        bf = (self.Y @ c.to(torch.bfloat16)).double().T  # (nb, nf)
         bf = bf / bf.norm(dim=1, keepdim=True)
         out = torch.zeros((nb, self.geo.fluid.numel()), dtype=torch.float64, device=bf.device)
         out[:, self.idx] = bf

@@ -1,3 +1,3 @@
-python tools/env_ab.py NPSD_UP0_MIXB 1 2 4 > gpurun_out/r2_ab_mixb.log 2>&1
-python tools/env_ab.py NPSD_CHAIN 0 1 > gpurun_out/r2_ab_chain2.log 2>&1
-NPSD_B200_LIB=$PWD/variants/libnpsd_b200_chain4.so python tools/env_ab.py NPSD_CHAIN 1 > gpurun_out/r2_ab_chain4.log 2>&1
+python -m pytest tests -m gpu -q -x --timeout 900 -p no:cacheprovider > gpurun_out/r2_gputest7.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r2_gputest7.log
+python tools/setmask_target.py --reps 5 > gpurun_out/r2_sm7.log 2>&1; python tools/setmask_target.py --config C2 --reps 5 >> gpurun_out/r2_sm7.log 2>&1; python tools/setmask_target.py --config C1 --reps 5 >> gpurun_out/r2_sm7.log 2>&1
+python tools/env_ab.py NPSD_PDL 0 > gpurun_out/r2_iter7.log 2>&1
