@@ -283,6 +283,7 @@ struct npsd_b200_ctx {
     bool fast = true;  // network arithmetic: fused/reassociated (true) or the reference's order, bitwise (false)
     int coarse_zc_max = 4;    // planes per block of the z-marching coarse kernels (at most)
     bool merge_up0 = true;    // level-0 up: tiled and mixed cells in one launch (NPSD_MERGE_UP0=0: two)
+    bool classify_simd = true;  // level-0 classification with byte SIMD (NPSD_CLASSIFY_SIMD=0: one cell per thread)
     int up0_mixb = 0;         // its mixed-list blocks per SM (NPSD_UP0_MIXB; 0: by grid size, up0_mixed_blocks)
     long long slab_chunk_launches = 0;
     cudaStream_t s = nullptr, s2 = nullptr;
@@ -629,10 +630,21 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         za.nxg = c->gglob[0].nx;
         za.nyg = c->gglob[0].ny;
         za.nzg = c->gglob[0].nz;
-        const dim3 grid(c->g0.nx / 32, (c->g0.ny + 7) / 8, (c->g0.nz + ZC - 1) / ZC);
-        LAUNCH3(c, s, (k_classify_march<ZC, true>), grid, dim3(32, 8), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount,
-                c->fmask, c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za,
-                SubMasks{c->dmask, c->dcount, c->umask, c->ucount});
+        const SubMasks sub{c->dmask, c->dcount, c->umask, c->ucount};
+        if (c->classify_simd && c->g0.nx % 128 == 0 && c->g0.ny % 8 == 0) {
+            // byte SIMD, 4 cells per thread, 128 x 8 tiles (setup.cuh k_classify_simd)
+            const dim3 grid(c->g0.nx / 128, c->g0.ny / 8, (c->g0.nz + ZC - 1) / ZC);
+            LAUNCH3(c, s, (k_classify_simd<32, ZC>), grid, dim3(256), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount,
+                    c->fmask, c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za, sub);
+        } else if (c->classify_simd && c->g0.nx % 64 == 0 && c->g0.ny % 16 == 0) {
+            const dim3 grid(c->g0.nx / 64, c->g0.ny / 16, (c->g0.nz + ZC - 1) / ZC);
+            LAUNCH3(c, s, (k_classify_simd<16, ZC>), grid, dim3(256), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount,
+                    c->fmask, c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za, sub);
+        } else {
+            const dim3 grid(c->g0.nx / 32, (c->g0.ny + 7) / 8, (c->g0.nz + ZC - 1) / ZC);
+            LAUNCH3(c, s, (k_classify_march<ZC, true>), grid, dim3(32, 8), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount,
+                    c->fmask, c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za, sub);
+        }
     } else {
         LAUNCH(c, s, k_setup_l0<D>, c->g0.n, c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
         LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
@@ -2144,6 +2156,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->dev = device;
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
         if (const char* e = std::getenv("NPSD_MERGE_UP0")) c->merge_up0 = (e[0] != '0');
+        if (const char* e = std::getenv("NPSD_CLASSIFY_SIMD")) c->classify_simd = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_UP0_MIXB")) c->up0_mixb = std::max(0, std::min(16, std::atoi(e)));
         if (slab) {
             c->slab = *slab;

@@ -296,6 +296,199 @@ __global__ void __launch_bounds__(256) k_classify_march(Geom g, const uint8_t* _
     }
 }
 
+// ---------------------------------------------------------------------------
+// Level-0 classification with byte SIMD (k_classify_simd): the outputs of
+// k_classify_march<ZC, true>, bit for bit, four cells per thread. A thread
+// owns a 32-bit word of cell types (x .. x+3) and marches z. Per staged plane
+// its 3 x 3 window summaries are whole-word ops: the column min / max of the
+// three rows (__vminu4 / __vmaxu4), the left / right neighbours by byte
+// permutes of the adjacent words, non-solid face-neighbour indicators as
+// byte adds. A block is LX lanes x (256 / LX) rows: a tile of 4 LX x (256 / LX)
+// cells (128 x 8 or 64 x 16), i.e. whole 32-cell mask segments (8 lanes) and
+// whole 32 x 8 flag tiles.
+__device__ __forceinline__ uint32_t nonsolid4(uint32_t v) {  // per byte: type != 2 (types 0..2)
+    const uint32_t x = v ^ 0x02020202u;
+    return (x | (x >> 1)) & 0x01010101u;
+}
+__device__ __forceinline__ uint32_t nib4(uint32_t b) {  // bytes' bit 0 -> 4-bit mask (byte i -> bit i)
+    return ((b & 0x01010101u) * 0x00204081u) >> 21 & 0xFu;
+}
+
+template <int LX, int ZC>
+__global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __restrict__ src,
+                                                       uint8_t* __restrict__ cls, uint32_t* __restrict__ mmask,
+                                                       uint32_t* __restrict__ mcount, uint32_t* __restrict__ fmask,
+                                                       uint32_t* __restrict__ fcount, int ftx, int fty,
+                                                       uint8_t* __restrict__ tflags, ZsumArgs za, SubMasks sm) {
+    constexpr int H = 256 / LX, W = 4 * LX;       // tile rows, tile cells in x
+    constexpr int SW = LX + 2, SH = H + 2;        // staged words per row (one halo word each side), rows
+    constexpr int NFX = W / kFlagTX, NFY = H / kFlagTY;  // flag tiles of the block tile
+    static_assert(W % kFlagTX == 0 && H % kFlagTY == 0, "whole flag tiles");
+    __shared__ uint32_t st[2][SH][SW];
+    __shared__ unsigned long long sG[kMaxDepth * 81];
+    __shared__ uint32_t sflag[NFX * NFY];
+    __shared__ uint32_t sint[kMaxDepth][3];  // interior-class counts
+    const int lane = threadIdx.x % LX, row = threadIdx.x / LX, tid = threadIdx.x;
+    // the lanes of my tile row (a warp is one row at LX = 32, two at LX = 16)
+    const unsigned rmask = (LX == 32) ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
+    const int X0 = blockIdx.x * W, Y0 = blockIdx.y * H, Z0 = blockIdx.z * ZC;
+    const long long plane = (long long)g.nx * g.ny;
+    for (int i = tid; i < za.nzs * 81; i += 256) sG[i] = 0ull;
+    if (tid < kMaxDepth * 3) sint[tid / 3][tid % 3] = 0u;
+    // staging: my (up to) two words of the SH x SW plane window
+    int off[2], sidx[2];
+    bool use[2], inxy[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int i = tid + 256 * j, ly = i / SW, lw = i - SW * ly;
+        const int xx = X0 - 4 + 4 * lw, yy = Y0 - 1 + ly;
+        use[j] = i < SH * SW;
+        inxy[j] = use[j] && xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny;
+        off[j] = inxy[j] ? yy * g.nx + xx : 0;
+        sidx[j] = i;
+    }
+    uint32_t pv[2];
+    auto load_plane = [&](int p) {
+        const bool zin = p >= 0 && p < g.nz;
+        const uint8_t* sp = src + (zin ? (long long)p * plane : 0);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+            pv[j] = (zin && inxy[j]) ? __ldg(reinterpret_cast<const uint32_t*>(sp + off[j])) : 0x02020202u;
+    };
+    uint32_t mnP = 0, mxP = 0, cvP = 0, mnM = 0, mxM = 0, cvM = 0, nbM = 0, mnN = 0, mxN = 0, cvN = 0, nbN = 0;
+    load_plane(Z0 - 1);
+    // stage plane p, issue plane p + 1, summarise plane p into N; returns
+    // (in sflag) the flag tiles of plane p holding fluid in their dilation
+    auto plane_step = [&](int p) {
+        const int buf = (p - Z0 + 1) & 1;
+        uint32_t* dst = &st[buf][0][0];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+            if (use[j]) dst[sidx[j]] = pv[j];
+        if (tid < NFX * NFY) sflag[tid] = 0u;
+        load_plane(p + 1);
+        __syncthreads();
+        const uint32_t U0 = st[buf][row][lane], U1 = st[buf][row][lane + 1], U2 = st[buf][row][lane + 2];
+        const uint32_t M0 = st[buf][row + 1][lane], M1 = st[buf][row + 1][lane + 1], M2 = st[buf][row + 1][lane + 2];
+        const uint32_t D0 = st[buf][row + 2][lane], D1 = st[buf][row + 2][lane + 1], D2 = st[buf][row + 2][lane + 2];
+        const uint32_t n0 = __vminu4(__vminu4(U0, M0), D0), n1 = __vminu4(__vminu4(U1, M1), D1),
+                       n2 = __vminu4(__vminu4(U2, M2), D2);
+        const uint32_t x0 = __vmaxu4(__vmaxu4(U0, M0), D0), x1 = __vmaxu4(__vmaxu4(U1, M1), D1),
+                       x2 = __vmaxu4(__vmaxu4(U2, M2), D2);
+        // bytes x-1 .. x+2 and x+1 .. x+4 of a row: permutes of adjacent words
+        const uint32_t lo = __vminu4(__vminu4(__byte_perm(n0, n1, 0x6543), n1), __byte_perm(n1, n2, 0x4321));
+        const uint32_t hi = __vmaxu4(__vmaxu4(__byte_perm(x0, x1, 0x6543), x1), __byte_perm(x1, x2, 0x4321));
+        const uint32_t n4 = nonsolid4(U1) + nonsolid4(D1) + nonsolid4(__byte_perm(M0, M1, 0x6543)) +
+                            nonsolid4(__byte_perm(M1, M2, 0x4321));
+        // flag tiles: a cell whose in-plane 3 x 3 holds fluid (min 0)
+        if (__vcmpeq4(lo, 0u)) atomicOr(&sflag[(row / kFlagTY) * NFX + (4 * lane) / kFlagTX], 1u);
+        mnP = mnM, mxP = mxM, cvP = cvM;
+        mnM = mnN, mxM = mxN, cvM = cvN, nbM = nbN;
+        mnN = lo, mxN = hi, cvN = M1, nbN = n4;
+        __syncthreads();  // sflag complete; every read of this staging buffer done before its reuse
+    };
+    const int x = X0 + 4 * lane, y = Y0 + row;
+    const int zoff = za.zg_off, Lc = za.nzs - 1;
+    uint32_t cnt_int[3] = {0u, 0u, 0u};  // this warp row's interior-class counts (lane 0)
+    plane_step(Z0 - 1);
+#pragma unroll 1
+    for (int p = Z0; p <= Z0 + ZC; ++p) {
+        if (p - 1 >= g.nz) break;  // block-uniform
+        plane_step(p);  // now P, M, N = planes p - 2, p - 1, p
+        if (p < Z0 + ZC && p < g.nz && tid < NFX * NFY)
+            tflags[((long long)p * fty + blockIdx.y * NFY + tid / NFX) * ftx + blockIdx.x * NFX + tid % NFX] =
+                sflag[tid] ? 1 : 0;
+        const int z = p - 1;
+        if (z < Z0) continue;
+        if (y >= g.ny) continue;  // whole warp rows
+        const long long c = (long long)z * plane + (long long)y * g.nx + x;
+        const bool owned = z >= g.zo0 && z < g.zo1;
+        const uint32_t lo = __vminu4(mnP, __vminu4(mnM, mnN)), hi = __vmaxu4(mxP, __vmaxu4(mxM, mxN));
+        const uint32_t eq = __vcmpeq4(lo, hi), t = cvM;
+        const uint32_t diag = nbM + nonsolid4(cvP) + nonsolid4(cvN);
+        const uint32_t wf = __vcmpeq4(lo, 0u) & 0x80808080u;
+        *reinterpret_cast<uint32_t*>(cls + c) = (t & eq) | (0x03030303u & ~eq) | (t << 2) | (diag << 4) | wf;
+        // masks of the 32-cell segment of 8 lanes
+        const uint32_t mixed = owned ? (~eq & 0x01010101u) : 0u;
+        const uint32_t t0 = owned ? (__vcmpeq4(t, 0u) & 0x01010101u) : 0u;
+        const uint32_t t1 = owned ? (__vcmpeq4(t, 0x01010101u) & 0x01010101u) : 0u;
+        const uint32_t t2 = owned ? (__vcmpeq4(t, 0x02020202u) & 0x01010101u) : 0u;
+        const int sh = 4 * (lane & 7);
+        uint32_t mm = nib4(mixed) << sh, fm = nib4(t0) << sh, dm = nib4(mixed & (wf >> 7)) << sh,
+                 um = nib4(mixed & t0) << sh;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            mm |= __shfl_xor_sync(rmask, mm, o);
+            fm |= __shfl_xor_sync(rmask, fm, o);
+            dm |= __shfl_xor_sync(rmask, dm, o);
+            um |= __shfl_xor_sync(rmask, um, o);
+        }
+        if ((lane & 7) == 0) {
+            const long long seg = c >> 5;
+            mmask[seg] = mm;
+            mcount[seg] = __popc(mm);
+            fmask[seg] = fm;
+            fcount[seg] = __popc(fm);
+            sm.dmask[seg] = dm;
+            sm.dcount[seg] = __popc(dm);
+            sm.umask[seg] = um;
+            sm.ucount[seg] = __popc(um);
+        }
+        // linear-block window counts of every level l < nzs (k_zsums classes by
+        // global position): the warp row shares y and z; x classes differ only
+        // at the grid's ends
+        if (za.nzs == 0) continue;
+        const uint32_t c0 = __popc(nib4(t0)), c1 = __popc(nib4(t1)), c2 = __popc(nib4(t2));
+        const int zg = z + zoff;
+        const bool row_inner = (y >> Lc) > 0 && (y >> Lc) < (za.nyg >> Lc) - 1 && (zg >> Lc) > 0 &&
+                               (zg >> Lc) < (za.nzg >> Lc) - 1;
+        const bool x_inner = (X0 >> Lc) > 0 && ((X0 + W - 1) >> Lc) < (za.nxg >> Lc) - 1;
+        if (row_inner && x_inner) {
+            cnt_int[0] += c0;
+            cnt_int[1] += c1;
+            cnt_int[2] += c2;
+        } else {
+#pragma unroll 1
+            for (int l = 0; l < za.nzs; ++l) {
+                const int yl = y >> l, zl = zg >> l;
+                const int ky = (yl == 0) ? 0 : ((yl == (za.nyg >> l) - 1) ? 2 : 1);
+                const int kz = (zl == 0) ? 0 : ((zl == (za.nzg >> l) - 1) ? 2 : 1);
+                // my four cells' x classes at level l (x .. x+3 global = local: slabs split z)
+                uint32_t cc[3][3] = {};  // [type][kx]
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int xl = (x + k) >> l;
+                    const int kx = (xl == 0) ? 0 : ((xl == (za.nxg >> l) - 1) ? 2 : 1);
+                    const uint32_t tb = (t >> (8 * k)) & 0xffu;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+#pragma unroll
+                        for (int b = 0; b < 3; ++b) cc[a][b] += (owned && tb == (uint32_t)a && kx == b) ? 1u : 0u;
+                }
+#pragma unroll
+                for (int ty = 0; ty < 3; ++ty)
+#pragma unroll
+                    for (int kx = 0; kx < 3; ++kx) {
+                        const uint32_t v = __reduce_add_sync(rmask, cc[ty][kx]);
+                        if (lane == 0 && v) atomicAdd(&sG[l * 81 + ty * 27 + (kz * 3 + ky) * 3 + kx], (unsigned long long)v);
+                    }
+            }
+        }
+    }
+    // interior rows: the interior class (13) of every level
+#pragma unroll
+    for (int ty = 0; ty < 3; ++ty) {
+        const uint32_t v = __reduce_add_sync(rmask, cnt_int[ty]);
+        if (lane == 0 && v) atomicAdd(&sint[0][ty], v);
+    }
+    __syncthreads();
+    if (tid < 3)
+        for (int l = 0; l < za.nzs; ++l) sG[l * 81 + tid * 27 + 13] += sint[0][tid];
+    __syncthreads();
+    for (int i = tid; i < za.nzs * 81; i += 256)
+        if (sG[i]) atomicAdd(&za.G[i / 81][i % 81], sG[i]);
+}
+
 // Tile occupancy at L0: flags[(z * nty + ty) * ntx + tx] = any fluid cell in
 // the 32 x 8 tile (tx, ty) of plane z dilated by one cell in x and y. Kernels
 // OR the flags of their region (plus one plane each side in z) and skip

@@ -537,3 +537,34 @@ def test_merged_up0_equals_two_launches(b200, oracle, exact, monkeypatch):
     assert np.array_equal(out[0][0], out[1][0])
     h, w = out[0][1].report.residual_history, out[1][1].report.residual_history
     assert np.max(np.abs(h - w) / w) <= 1e-9
+
+
+@pytest.mark.parametrize("case", ["C1", "C2", "random128", "random64x128x256"])
+def test_classify_simd_equals_scalar(b200, monkeypatch, case):
+    """Level-0 classification with byte SIMD (4 cells per thread) writes the
+    same cell bytes, masks, tile flags and window counts as one cell per
+    thread: every set_mask product compares equal."""
+    if case in ("C1", "C2"):
+        t, _ = scenes.config(case)
+    elif case == "random128":
+        t = scenes.random_types((128, 128, 128), 77, p=(0.5, 0.3, 0.2), blobs=8)
+    else:
+        t = scenes.random_types((64, 128, 256), 78, p=(0.6, 0.25, 0.15), blobs=6)
+    p = b200.init_params(4, 31)
+    r = np.random.default_rng(3).standard_normal(int((t == 0).sum()))
+    out = []
+    for simd in ("1", "0"):
+        monkeypatch.setenv("NPSD_CLASSIFY_SIMD", simd)
+        ctx = b200.Context(3, t.shape, p, exact=True)
+        ctx.set_mask(t)
+        za, zb = ctx.linear_coeffs()
+        out.append((ctx.fluid_indices(), ctx.mixed_counts(), za, zb, [ctx.level_image(l) for l in range(4)],
+                    ctx.precond_apply(r), ctx.is_pure_neumann()))
+        ctx.close()
+    a, b = out
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(a[2].view(np.uint32), b[2].view(np.uint32))
+    assert np.array_equal(a[3].view(np.uint32), b[3].view(np.uint32))
+    for la, lb in zip(a[4], b[4]):
+        assert np.array_equal(la, lb)
+    assert np.array_equal(a[5], b[5]) and a[6] == b[6]
