@@ -106,6 +106,7 @@ def main() -> None:
               "ritz_m": a.ritz_m, "ritz_every": a.ritz_every, "seed": a.seed, "eval": {}}
     ident = b200.identity_params(a.depth)
     evals = [("C3", 64), ("C3", 128), ("C1", 64), ("C2", 128)] + ([("C3", 256)] if a.eval256 else [])
+    evals = [(nm, n) for nm, n in evals if n % (1 << a.depth) == 0]
     for name, n in evals:
         t, seed = scenes.config(name, n)
         it_i, _, ms_i = iterations(t, ident, seed)
