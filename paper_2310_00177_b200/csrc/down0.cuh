@@ -86,20 +86,24 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
     auto own_bytes = [&](int z) -> unsigned {
         return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
     };
-    auto rslot = [&](int z) { return (z - zc0 + 1 + kD0R * 1024) % kD0R; };
-    auto xslot = [&](int z) { return (z + kD0X * 1024) % kD0X; };
-    // own pairs without fluid zero-filled; halo always copied (exact zeros)
+    // ring slots of non-negative arguments (unsigned: cheaper modulo)
+    auto rslot = [&](int z) { return (int)((unsigned)(z - zc0 + 1 + kD0R * 1024) % (unsigned)kD0R); };
+    auto xslot = [&](int z) { return (int)((unsigned)(z + kD0X * 1024) % (unsigned)kD0X); };
+    // own pairs without fluid zero-filled; halo always copied (exact zeros).
+    // The source address is in the grid whatever the predicate (qo / qh are
+    // 0 for a lane without a pair / halo cell): src-size 0 reads nothing.
+    const double* r_own = r + qo;
+    const double* r_halo = r + qh;
     auto issue = [&](int z, unsigned ob) {
         if (zin(z)) {
-            const bool hl = h_in;
             const int s = rslot(z);
             const bool ol = own && pair_live(ob);
             const long long qz = z * plane;
-            cp_async16(&S.raw[s][row + 1][2 + 2 * lane], r + (ol ? qz + qo : 0), ol);
+            cp_async16(&S.raw[s][row + 1][2 + 2 * lane], r_own + qz, ol);
             if (hkind == 1)
-                cp_async16(&S.raw[s][hsr][hsc], r + (hl ? qz + qh : 0), hl);
+                cp_async16(&S.raw[s][hsr][hsc], r_halo + qz, h_in);
             else if (hkind == 2)
-                cp_async8(&S.raw[s][hsr][hsc], r + (hl ? qz + qh : 0), hl);
+                cp_async8(&S.raw[s][hsr][hsc], r_halo + qz, h_in);
         }
         cp_commit();
     };

@@ -210,29 +210,29 @@ __device__ __forceinline__ void stencil_march(const Geom& g, const uint8_t* __re
     auto own_bytes = [&](int z) -> unsigned {
         return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
     };
-    auto slot = [&](int z) { return (z - zc0 + 1 + ST * 1024) % ST; };
+    auto slot = [&](int z) { return (int)((unsigned)(z - zc0 + 1 + ST * 1024) % (unsigned)ST); };
     // issue the copies of plane z (one commit group per plane, even if empty).
     // Own pairs without fluid are zero-filled (no traffic); halo cells are
     // always copied when in the domain: their non-fluid values are the exact
     // zeros of the solver vectors, so no byte test sits on the issue path.
+    // the source address is in the grid whatever the predicate (qo / qh are 0
+    // for a lane without a pair / halo cell): src-size 0 reads nothing
     auto issue = [&](int z, unsigned ob) {
         if (zin(z)) {
-            const bool hl = h_in;
             const int s = slot(z);
             const bool ol = own && pair_live(ob);
             const long long qz = z * plane;
 #pragma unroll
             for (int a = 0; a < Op::NA; ++a) {
-                cp_async16(&S.raw[s][a][row + 1][2 + 2 * lane], op.in[a] + (ol ? qz + qo : 0), ol);
+                cp_async16(&S.raw[s][a][row + 1][2 + 2 * lane], op.in[a] + (qz + qo), ol);
                 if (hkind == 1)
-                    cp_async16(&S.raw[s][a][hsr][hsc], op.in[a] + (hl ? qz + qh : 0), hl);
+                    cp_async16(&S.raw[s][a][hsr][hsc], op.in[a] + (qz + qh), h_in);
                 else if (hkind == 2)
-                    cp_async8(&S.raw[s][a][hsr][hsc], op.in[a] + (hl ? qz + qh : 0), hl);
+                    cp_async8(&S.raw[s][a][hsr][hsc], op.in[a] + (qz + qh), h_in);
             }
             if constexpr (Op::CS > 0) {
 #pragma unroll
-                for (int a = 0; a < Op::NC; ++a)
-                    cp_async16(&S.ctr[s][a][row][2 * lane], op.ctr[a] + (ol ? qz + qo : 0), ol);
+                for (int a = 0; a < Op::NC; ++a) cp_async16(&S.ctr[s][a][row][2 * lane], op.ctr[a] + (qz + qo), ol);
             }
         }
         cp_commit();

@@ -84,17 +84,17 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
             cp_async4(&S.oc[k & 3][cr][ccol], outc + (ok ? k * cplane + cqo : 0), ok);
         }
     };
-    auto slot = [&](int z) { return (z - zc0 + kUST * 1024) % kUST; };
+    auto slot = [&](int z) { return (int)((unsigned)(z - zc0 + kUST * 1024) % (unsigned)kUST); };
     auto issue = [&](int z, unsigned ob) {
         if (zin(z)) {
             const int s = slot(z);
             const bool ol = own && up_pair(ob);
             const long long q = z * plane + qo;
-            cp_async8(&S.y[s][row][2 * lane], y0 + (ol ? q : 0), ol);
+            cp_async8(&S.y[s][row][2 * lane], y0 + q, ol);  // q in the grid: src-size 0 reads nothing
 #pragma unroll
             for (int j = 0; j < NO; ++j) {
                 const bool lj = ol && j < nc;
-                cp_async16(&S.ad[s][j][row][2 * lane], adp[j] + (lj ? q : 0), lj);
+                cp_async16(&S.ad[s][j][row][2 * lane], adp[j] + q, lj);
             }
             if (z == zc0) {
                 for (int k = (z - 1) >> 1; k <= (z + 1) >> 1; ++k) coarse(k);
