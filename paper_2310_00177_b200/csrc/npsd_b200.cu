@@ -252,6 +252,8 @@ struct npsd_b200_ctx {
     SlabInfo slab;                // z-slab decomposition (single domain: off)
     Geom gglob[kMaxDepth] = {};   // the full grid per level (z-slab: all ranks)
     cudaGraphExec_t slab_exec = nullptr;  // z-slab: a chunk of iterations (NCCL ranks)
+    cudaGraphExec_t slab_exec_short = nullptr;  // z-slab: a chunk of one ring period (the last chunks)
+    long long slab_short_launches = 0;
     int slab_exec_no = -1, slab_exec_k0 = -1, slab_exec_ns = 0, slab_exec_ident = 0;
     bool slab_no_graph = false;   // the chunk graph could not be captured: eager chunks
     // programmatic dependent launch of the iteration kernels: measured neutral
@@ -1626,36 +1628,43 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
            (cudaGraphConditionalHandle)0, 0, 1);
     slab_reduce(c, s, kFinNorm0);
     slab_exchange(c, s, c->R, sizeof(double), 0);
-    const int K = slab_chunk(ring);
+    // chunks: K iterations, or P (the ring period) when the residual's decay
+    // predicts the end within P iterations — fewer dead iterations after
+    // convergence (their kernels return at once; their exchanges still run)
+    const int K = slab_chunk(ring), P = (ring % 2 == 0) ? ring : 2 * ring;
     bool graph = c->slab.comm->capturable() && !c->slab_no_graph;
+    auto capture = [&](int kc, cudaGraphExec_t& exec, long long& nlaunch) {
+        if (exec) CK(cudaGraphExecDestroy(exec));
+        exec = nullptr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const long long before = c->launches;
+        try {
+            for (long long k = 1; k <= kc; ++k)
+                for (const auto& st : slab_body_steps<D>(c, no, k, ns)) st.run(s);
+            nlaunch = c->launches - before;  // kernels per chunk replay
+            c->launches = before;            // captured, not executed
+        } catch (...) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(s, &junk);
+            if (junk) cudaGraphDestroy(junk);
+            throw;
+        }
+        cudaGraph_t gr = nullptr;
+        CK(cudaStreamEndCapture(s, &gr));
+        const cudaError_t ie = cudaGraphInstantiate(&exec, gr, 0);
+        cudaGraphDestroy(gr);
+        CK(ie);
+    };
     if (graph && (!c->slab_exec || c->slab_exec_gen != c->buf_gen || c->slab_exec_no != no ||
                   c->slab_exec_ns != ns || c->slab_exec_ident != cfg->precond ||
                   c->exec_key[0] != c->Dring || c->exec_key[1] != c->hist ||
                   c->exec_key[2] != c->ADring)) {
-        if (c->slab_exec) CK(cudaGraphExecDestroy(c->slab_exec));
-        c->slab_exec = nullptr;
-        // the chunk: K iterations of kernels and NCCL calls in one graph; if the
-        // capture is refused, the chunk runs as eager launches instead
+        // the chunks: iterations of kernels and NCCL calls in one graph each; if
+        // the capture is refused, the chunks run as eager launches instead
         CK(cudaStreamSynchronize(s));
         try {
-            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-            const long long before = c->launches;
-            try {
-                for (long long k = 1; k <= K; ++k)
-                    for (const auto& st : slab_body_steps<D>(c, no, k, ns)) st.run(s);
-                c->slab_chunk_launches = c->launches - before;  // kernels per chunk replay
-                c->launches = before;                            // captured, not executed
-            } catch (...) {
-                cudaGraph_t junk = nullptr;
-                cudaStreamEndCapture(s, &junk);
-                if (junk) cudaGraphDestroy(junk);
-                throw;
-            }
-            cudaGraph_t gr = nullptr;
-            CK(cudaStreamEndCapture(s, &gr));
-            const cudaError_t ie = cudaGraphInstantiate(&c->slab_exec, gr, 0);
-            cudaGraphDestroy(gr);
-            CK(ie);
+            capture(K, c->slab_exec, c->slab_chunk_launches);
+            capture(P, c->slab_exec_short, c->slab_short_launches);
             c->slab_exec_no = no;
             c->slab_exec_ns = ns;
             c->slab_exec_ident = cfg->precond;
@@ -1670,17 +1679,28 @@ int slab_solve_impl(npsd_b200_ctx* c, const npsd_b200_solve_cfg* cfg, npsd_b200_
             graph = false;
         }
     }
-    for (long long k0 = 1;; k0 += K) {
-        CK(cudaMemcpyAsync(&h->done, &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    double prev_rn = 0.0;
+    int prev_kc = 0;
+    for (long long k0 = 1;;) {
+        CK(cudaMemcpyAsync(h, c->st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (h->done) break;
+        int kc = K;
+        if (prev_kc > 0 && prev_rn > 0.0 && h->rnorm > 0.0 && h->rnorm < prev_rn) {
+            const double rate = std::pow(h->rnorm / prev_rn, 1.0 / prev_kc);  // per-iteration decay
+            const double left = std::log(h->thr / h->rnorm) / std::log(rate);
+            if (left <= P) kc = P;
+        }
+        prev_rn = h->rnorm;
+        prev_kc = kc;
         if (graph) {
-            CK(cudaGraphLaunch(c->slab_exec, s));
-            c->launches += c->slab_chunk_launches;
+            CK(cudaGraphLaunch(kc == K ? c->slab_exec : c->slab_exec_short, s));
+            c->launches += (kc == K) ? c->slab_chunk_launches : c->slab_short_launches;
         } else {
-            for (long long k = k0; k < k0 + K; ++k)
+            for (long long k = k0; k < k0 + kc; ++k)
                 for (const auto& st : slab_body_steps<D>(c, no, k, ns)) st.run(s);
         }
+        k0 += kc;
     }
     CK(cudaEventRecord(c->ev1, s));
     CK(cudaMemcpyAsync(h, c->st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
@@ -2034,6 +2054,7 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->icFail);
     if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
     if (c->slab_exec) cudaGraphExecDestroy(c->slab_exec);
+    if (c->slab_exec_short) cudaGraphExecDestroy(c->slab_exec_short);
     for (SchedBufs* sb : {&c->sch_stencil, &c->sch_march, &c->sch_down0}) {
         F(sb->pre);
         F(sb->zlo);
