@@ -5,8 +5,8 @@ bench.py's roofline "traffic" field).
 Capture (one GPU; ncu_target runs a 1-iteration warm-up, then the measured
 iterations, kernels launched one by one in the body order below):
 
-    ncu --set full --clock-control none -k regex:"k_mixed_down0|k_down_l0|k_cdownz|k_cupz|k_up_l0|k_mixed_up0|k_ortho2|k_update2" \
-        -s 11 -c 11 -o prof python tools/ncu_target.py
+    ncu --set full --clock-control none -k regex:"k_mixed_down0|k_down_l0|k_cdownz|k_cupz|k_up_l0|k_ortho2|k_update2" \
+        -s 10 -c 10 -o prof python tools/ncu_target.py
 
     python tools/ncu_traffic.py prof.ncu-rep 256
 """
@@ -19,7 +19,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 BODY = ["net_mixed_down_L0", "net_down_L0", "net_down_L1", "net_down_L2", "net_coarse_L3", "net_up_L2", "net_up_L1",
-        "net_up_L0", "net_mixed_up_L0", "ortho", "update"]  # depth 4
+        "net_up_L0", "ortho", "update"]  # depth 4 (net_up_L0: tiled and mixed cells, k_up_l0m)
 
 
 def main() -> None:
