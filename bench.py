@@ -6,7 +6,7 @@ Metric (BASELINE.json): time-to-solution in ms to relative residual 1e-6 at
 iteration ms and HBM GB/s. One step = one frame: set_mask (flags, coarsened
 masks, mixed-window kernel tables, linear-block coefficients) + the whole PSDO
 solve to 1e-6, with the cell types and the RHS already resident in HBM.
-Weights: the repo's trained 3D model (weights/npsd3d_L4.npm) by
+Weights: the repo's trained 3D model (weights/npsd3d_L5.npm) by
 default; `--weights identity` gives the identity-equivalent network (PSDO == CG,
 the network still runs in full every iteration). The N=1 line also carries the
 C4 sequence (32 time-varying 128^3 masks through one context, per-frame
@@ -196,7 +196,12 @@ def read_npm(path) -> tuple[int, int, np.ndarray]:
     return int(dim), int(depth), np.frombuffer(raw[16:], "<f4").copy()
 
 
-WEIGHTS = ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm"
+WEIGHTS = ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L5.npm"  # = paper_2310_00177_b200.DEFAULT_MODEL
+
+
+def model_depth() -> int:
+    """the depth of the committed model file (its header; no library needed)"""
+    return read_npm(WEIGHTS)[1]
 
 
 def load_weights(kind: str, depth: int):
@@ -421,9 +426,9 @@ def config_line(name: str, params, cfg, device: int, steps: int, warmup: int, cp
            "n_fluid": n_f, "tts_ms": m["step_ms"], "set_mask_ms": m["set_mask_ms"], "per_iter_ms": m["per_iter_ms"],
            "iterations": m["iterations"], "converged": m["converged"], "gpu_launches": int(round(m["launches"])),
            "steps": steps, "warmup": warmup,
-           "iteration_roofline": iteration_roofline(4, n_c, n_f, m["per_iter_ms"], load_peaks())}
+           "iteration_roofline": iteration_roofline(params.depth, n_c, n_f, m["per_iter_ms"], load_peaks())}
     if cpu:
-        c = cpu_reference_solve(types, seed, 4, os.cpu_count() or 1, "trained", name=name)
+        c = cpu_reference_solve(types, seed, params.depth, os.cpu_count() or 1, "trained", name=name)
         out["cpu_baseline"] = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
     return out
 
@@ -736,7 +741,7 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
     ap.add_argument("--n", type=int, default=None, help="override the grid size of the config")
-    ap.add_argument("--depth", type=int, default=4)
+    ap.add_argument("--depth", type=int, default=None, help="network depth (default: the trained model's)")
     ap.add_argument("--weights", default="trained", choices=["trained", "identity", "random"])
     ap.add_argument("--max-iters", type=int, default=20000)
     ap.add_argument("--profile-iters", type=int, default=5)
@@ -748,6 +753,8 @@ def main() -> None:
     ap.add_argument("--slab", action="store_true", help="z-slab path even at N=1 (one-rank NCCL)")
     ap.add_argument("--watchdog-s", type=float, default=900.0)
     args = ap.parse_args()
+    if args.depth is None:
+        args.depth = model_depth() if args.weights == "trained" else 4
     if args.impl == "reference":
         run_reference(args)
         return

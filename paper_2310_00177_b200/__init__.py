@@ -17,6 +17,7 @@ raises if the library or the device is unavailable.
 from __future__ import annotations
 
 import ctypes as C
+from pathlib import Path
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -147,6 +148,16 @@ def load_npm(path) -> NetParams:
         raise RuntimeError(L.npsd_b200_npm_last_error().decode())
     _raise(st, L.npsd_b200_npm_last_error().decode())
     return NetParams(dim.value, depth.value, out)
+
+
+# The repo's trained 3D model: the weights every benchmark and
+# the trained-weight parity fixtures use. npsd3d_L4.npm is the depth-4 model.
+DEFAULT_MODEL = Path(__file__).resolve().parent / "weights" / "npsd3d_L5.npm"
+
+
+def default_model() -> NetParams:
+    """load_npm(DEFAULT_MODEL)."""
+    return load_npm(DEFAULT_MODEL)
 
 
 def identity_params(depth: int, dim: int = 3) -> NetParams:

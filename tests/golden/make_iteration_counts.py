@@ -7,7 +7,7 @@ Run here (needs oracle/_ref); takes minutes at 256^3.
 
 With --trained: the reference psdo_solve with the 3D network restatement
 (NeuralPrecond3D) as its preconditioner and the committed trained weights
-(paper_2310_00177_b200/weights/npsd3d_L4.npm), entries "<name>_trained"."""
+(paper_2310_00177_b200.DEFAULT_MODEL), entries "<name>_trained"."""
 import json
 import sys
 import time
@@ -28,7 +28,7 @@ trained = "--trained" in sys.argv
 if trained:
     import paper_2310_00177_b200 as b200
 
-    W = b200.load_npm(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm")
+    W = b200.default_model()
 
 def frames(name):
     """(key suffix, types, seed) per solve: one for C1/C2/C3/C5, 32 for C4
@@ -49,7 +49,7 @@ for name, suf, t, seed in todo:
         r = ref.psdo_solve(t, b, mode="neural", params=W.flat, depth=W.depth, max_iters=20000, tol_reduction=1e-6,
                            n_ortho=2)
         key, solver = f"{name}{suf}_trained", ("reference psdo_solve + NeuralPrecond3D (restatement) with "
-                                          "weights/npsd3d_L4.npm, n_ortho=2, tol 1e-6")
+                                          f"weights/{b200.DEFAULT_MODEL.name} (depth {W.depth}), n_ortho=2, tol 1e-6")
     else:
         r = ref.psdo_solve(t, b, mode="identity", max_iters=20000, tol_reduction=1e-6, n_ortho=2)
         key, solver = name + suf, "reference psdo_solve + IdentityPrecond, n_ortho=2, tol 1e-6"

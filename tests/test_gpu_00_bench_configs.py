@@ -23,7 +23,7 @@ from paper_2310_00177_b200 import scenes
 pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 COUNTS = json.loads((ROOT / "tests" / "golden" / "iteration_counts.json").read_text())
-WEIGHTS = ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm"
+
 REL_L2 = 1e-5
 
 
@@ -34,10 +34,10 @@ def rel_l2(a, b):
 @pytest.mark.parametrize("name,weights", [("C2", "seed42"), ("C2", "trained"), ("C3", "seed42"), ("C3", "trained")])
 def test_precond_apply_at_bench_config(b200, oracle, name, weights):
     t, seed = scenes.config(name)
-    P = b200.load_npm(WEIGHTS) if weights == "trained" else b200.init_params(4, 42)
+    P = b200.default_model() if weights == "trained" else b200.init_params(4, 42)
     ctx = b200.Context(3, t.shape, P)
     ctx.set_mask(t)
-    octx = oracle.context(t, P.flat, 4)
+    octx = oracle.context(t, P.flat, P.depth)
     # the solve's own input: the benchmark RHS, and a rough residual-like vector
     b = oracle.rhs_normal(seed, t.size)[t.reshape(-1) == 0]
     r = np.random.default_rng(7).standard_normal(b.size) * 1e-3
@@ -66,7 +66,7 @@ def test_identity_iteration_counts_at_bench_config(b200, name, precond):
 
 
 def test_c4_sequence_per_frame_iterations(b200):
-    W = b200.load_npm(WEIGHTS)
+    W = b200.default_model()
     n = 128
     ctx = b200.Context(3, (n, n, n), W)
     cfg = b200.SolveConfig(max_iters=2000)

@@ -476,7 +476,7 @@ def test_ic0_isolated_cell_fails_like_reference(b200, ref):
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3"])
 def test_trained_weights_iteration_parity(b200, name):
-    """The committed trained 3D model (weights/npsd3d_L4.npm): iterations to
+    """The committed trained 3D model (b200.DEFAULT_MODEL): iterations to
     1e-6 on the benchmark domains at their full sizes within +-1 of the
     reference psdo_solve with the same weights (tests/golden/iteration_counts.json,
     "<name>_trained", made by tests/golden/make_iteration_counts.py --trained)."""
@@ -485,7 +485,7 @@ def test_trained_weights_iteration_parity(b200, name):
 
     root = Path(__file__).resolve().parents[1]
     want = json.loads((root / "tests" / "golden" / "iteration_counts.json").read_text())[f"{name}_trained"]
-    W = b200.load_npm(root / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm")
+    W = b200.default_model()
     t, seed = scenes.config(name)
     ctx = b200.Context(3, t.shape, W)
     ctx.set_mask(t)

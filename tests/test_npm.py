@@ -68,15 +68,15 @@ def test_npm_errors(tmp_path):
         b200.save_npm(p, tmp_path / "no_such_dir" / "x.npm")
 
 
-def test_committed_trained_model_loads():
-    """weights/npsd3d_L4.npm: a dim-3 depth-4 model file of the right size, with
-    its training report (tools/train3d.py)."""
+def test_committed_trained_models_load():
+    """The trained 3D model files (DEFAULT_MODEL, depth 5, and the depth-4
+    model npsd3d_L4.npm): dim-3 files of the right size, each with its training
+    report (tools/train3d.py)."""
     import json
-    from pathlib import Path
 
-    d = Path(b200.__file__).parent / "weights"
-    W = b200.load_npm(d / "npsd3d_L4.npm")
-    assert (W.dim, W.depth, W.flat.size) == (3, 4, 15990)
-    assert np.all(np.isfinite(W.flat))
-    rep = json.loads((d / "npsd3d_L4.json").read_text())
-    assert rep["eval"]["C3@256"]["trained_converged"]
+    for path, depth in ((b200.DEFAULT_MODEL, 5), (b200.DEFAULT_MODEL.parent / "npsd3d_L4.npm", 4)):
+        W = b200.load_npm(path)
+        assert (W.dim, W.depth, W.flat.size) == (3, depth, b200.param_count(3, depth))
+        assert np.all(np.isfinite(W.flat))
+        rep = json.loads(path.with_suffix(".json").read_text())
+        assert rep["eval"]["C3@256"]["trained_converged"]

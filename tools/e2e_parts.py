@@ -11,7 +11,7 @@ import paper_2310_00177_b200 as b200  # noqa: E402
 from paper_2310_00177_b200 import scenes  # noqa: E402
 
 t, seed = scenes.config("C3")
-W = b200.load_npm(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm")
+W = b200.default_model()
 ctx = b200.Context(3, t.shape, W)
 n_f = int((t == 0).sum())
 pt = b200.PinnedBuffer(ctx, t.size, np.uint8)

@@ -12,7 +12,7 @@ import numpy as np  # noqa: E402
 import paper_2310_00177_b200 as b200  # noqa: E402
 from paper_2310_00177_b200 import scenes  # noqa: E402
 
-W = b200.load_npm(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm")
+W = b200.default_model()
 for name in ("C1", "C2", "C3"):
     t, seed = scenes.config(name)
     b = b200.rhs_normal(seed, t.size)[t.reshape(-1) == 0]

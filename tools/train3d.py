@@ -1,6 +1,6 @@
 """Train 3D network weights and measure them in the solve.
 
-    python tools/train3d.py [--steps 3000] [--n 64] [--out paper_2310_00177_b200/weights/npsd3d_L4.npm]
+    python tools/train3d.py [--depth 5] [--steps 8000] [--n 128] [--big 8] [--ritz-m 300] [--out ...npm]
 
 Training frames are 64^3 free-surface geometries drawn at random (pool levels,
 droplets, obstacles, columns, pillars) — not the C3 benchmark frame. The
@@ -69,7 +69,7 @@ def main() -> None:
     ap.add_argument("--ritz-m", type=int, default=0, help="Lanczos steps of the Ritz-vector RHS sets (0: smoothed noise)")
     ap.add_argument("--ritz-every", type=int, default=1, help="Ritz sets on every k-th frame")
     ap.add_argument("--big-only", action="store_true", help="train on the 2n^3 frames only")
-    ap.add_argument("--out", default=str(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L4.npm"))
+    ap.add_argument("--out", default=str(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L5.npm"))
     a = ap.parse_args()
     dev = torch.device("cuda")
     rng = np.random.default_rng(a.seed)
