@@ -6,7 +6,7 @@ Metric (BASELINE.json): time-to-solution in ms to relative residual 1e-6 at
 iteration ms and HBM GB/s. One step = one frame: set_mask (flags, coarsened
 masks, mixed-window kernel tables, linear-block coefficients) + the whole PSDO
 solve to 1e-6, with the cell types and the RHS already resident in HBM.
-Weights: the repo's trained 3D model (weights/npsd3d_L5.npm) by
+Weights: the repo's trained 3D model (weights/npsd3d_L6.npm) by
 default; `--weights identity` gives the identity-equivalent network (PSDO == CG,
 the network still runs in full every iteration). The N=1 line also carries the
 C4 sequence (32 time-varying 128^3 masks through one context, per-frame
@@ -196,7 +196,7 @@ def read_npm(path) -> tuple[int, int, np.ndarray]:
     return int(dim), int(depth), np.frombuffer(raw[16:], "<f4").copy()
 
 
-WEIGHTS = ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L5.npm"  # = paper_2310_00177_b200.DEFAULT_MODEL
+WEIGHTS = ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L6.npm"  # = paper_2310_00177_b200.DEFAULT_MODEL
 
 
 def model_depth() -> int:

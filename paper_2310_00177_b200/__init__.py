@@ -152,7 +152,7 @@ def load_npm(path) -> NetParams:
 
 # The repo's trained 3D model: the weights every benchmark and
 # the trained-weight parity fixtures use. npsd3d_L4.npm is the depth-4 model.
-DEFAULT_MODEL = Path(__file__).resolve().parent / "weights" / "npsd3d_L5.npm"
+DEFAULT_MODEL = Path(__file__).resolve().parent / "weights" / "npsd3d_L6.npm"
 
 
 def default_model() -> NetParams:

@@ -224,7 +224,7 @@ def main() -> None:
     ap.add_argument("out_dir")
     ap.add_argument("--systems", default="C1,C2,C3")
     ap.add_argument("--methods", default="cg,pcg+jacobi,psd+neural,psdo+neural,psdo+none,pcg+ic0")
-    ap.add_argument("--model", default=str(Path(__file__).parent / "weights" / "npsd3d_L5.npm"))
+    ap.add_argument("--model", default=str(Path(__file__).parent / "weights" / "npsd3d_L6.npm"))
     a = ap.parse_args()
     model = b200.load_npm(a.model) if a.model and os.path.exists(a.model) else None
     systems = {}

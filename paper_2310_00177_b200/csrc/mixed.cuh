@@ -39,6 +39,69 @@ __global__ void __launch_bounds__(kBlock) k_mixed_list(long long nseg, const uin
     }
 }
 
+// Exclusive scans of up to four segment-count arrays of nseg entries (the
+// total left in base[nseg]) and, optionally, the compacted list of the set
+// bits of array 0's mask (k_mixed_list) — one block, one launch: for the small
+// arrays of the coarse levels and of small grids, where two cub launches per
+// scan plus the list's launch cost more than the work.
+struct SmallScan {
+    const uint32_t* cnt[4];
+    uint32_t* base[4];
+    int n;
+    const uint32_t* mask;  // nullptr: no list
+    uint32_t* list;
+};
+constexpr int kScanSmallT = 1024;
+constexpr long long kScanSmallMax = 16384;  // segments (16 per thread)
+
+__global__ void __launch_bounds__(kScanSmallT) k_scan_small(long long nseg, SmallScan a) {
+    __shared__ uint32_t wsum[kScanSmallT / 32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const long long per = (nseg + kScanSmallT - 1) / kScanSmallT;
+    const long long s0 = min(nseg, per * t), s1 = min(nseg, s0 + per);
+    for (int k = 0; k < a.n; ++k) {
+        const uint32_t* __restrict__ cnt = a.cnt[k];
+        uint32_t sum = 0;
+        for (long long i = s0; i < s1; ++i) sum += cnt[i];
+        uint32_t v = sum;  // inclusive warp scan, then the warps' totals
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane == 31) wsum[w] = v;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t x = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            wsum[lane] = x;
+        }
+        __syncthreads();
+        uint32_t run = v - sum + (w ? wsum[w - 1] : 0u);
+        uint32_t* __restrict__ base = a.base[k];
+        const bool lst = k == 0 && a.mask;
+        for (long long i = s0; i < s1; ++i) {
+            base[i] = run;
+            if (lst) {
+                uint32_t m = a.mask[i];
+                uint32_t j = run;
+                const uint32_t c0 = (uint32_t)(i << 5);
+                while (m) {
+                    a.list[j++] = c0 + (uint32_t)(__ffs(m) - 1);
+                    m &= m - 1;
+                }
+            }
+            run += cnt[i];
+        }
+        if (t == kScanSmallT - 1) base[nseg] = run;
+        __syncthreads();  // wsum is reused by the next array
+    }
+}
+
 // The solve needs y_0 only at mixed cells whose window holds a fluid cell (the
 // input is zero over the others: y_0 = +0, never computed or read) and the up
 // output only at fluid cells. Those two sublists of the level-0 mixed cells

@@ -308,7 +308,10 @@ struct npsd_b200_ctx {
     uint32_t *pid0 = nullptr, *repcell0 = nullptr, *npat0 = nullptr;
     // level-0 mixed sublists the solve reads (mixed.cuh): windows holding fluid
     // (down) and fluid cells (up), with their pattern ids
-    uint32_t *crep = nullptr, *cnpat = nullptr;  // coarse dictionaries (scratch)
+    uint32_t *crep = nullptr, *cnpat = nullptr;  // coarse dictionaries (scratch; level l at roff[l], cnpat[l])
+    size_t koff[kMaxDepth] = {}, roff[kMaxDepth] = {};  // level l's window keys (dkeys/dvals) and crep offsets
+    unsigned long long htoff[kMaxDepth] = {};          // level l's hash-table slots (htk/htv)
+    unsigned long long cap_ht_graph[kMaxDepth] = {};   // the capacities the setup graph was built with
     uint32_t *dlist0 = nullptr, *dkid0 = nullptr, *dcnt0 = nullptr;
     uint32_t *ulist0 = nullptr, *ukid0 = nullptr, *ucnt0 = nullptr;
     int tf_ntx = 0, tf_nty = 0;
@@ -344,8 +347,17 @@ struct npsd_b200_ctx {
     unsigned exec_gen = 0, slab_exec_gen = 0;
     size_t l2pool_bytes = 0;
     size_t mac_cap = 0;
-    void* cub_tmp = nullptr;
-    size_t cub_bytes = 0;
+    void* cub_tmp[3] = {};  // cub scratch per setup stream that scans (main, schedules, coarse chain)
+    size_t cub_bytes[3] = {};
+    // set_mask's independent chains run as branches of its graph (fork/join
+    // through events): aux streams sx[0] solver memsets, sx[1] schedules,
+    // sx[2] the coarse image chain, sx[2 + l] level l's dictionary
+    bool setup_par = true;  // NPSD_SETUP_SERIAL=1: one stream
+    cudaStreamAttrValue apw = {};  // the L2 access-policy window of the streams (l2pool)
+    bool apw_on = false;
+    cudaStream_t sx[kMaxDepth + 2] = {};
+    cudaEvent_t evf[4 * kMaxDepth + 8] = {};
+    int nev = 0;
     // solve graph
     cudaGraphExec_t exec = nullptr;
     const void* exec_key[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -481,16 +493,36 @@ size_t param_count_impl(int dim, int depth) {
     return (size_t)(depth - 1) * (2 * conv + 2 * lin) + conv;
 }
 
-void scan_u32(npsd_b200_ctx* c, const uint32_t* in, uint32_t* out, long long n) {
+// exclusive scan on stream s with cub scratch `slot` (one per setup stream that scans)
+void scan_u32(npsd_b200_ctx* c, cudaStream_t s, int slot, const uint32_t* in, uint32_t* out, long long n) {
     size_t bytes = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, c->s));
-    if (bytes > c->cub_bytes) {
-        if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
-        CK(cudaMalloc(&c->cub_tmp, bytes));
-        c->cub_bytes = bytes;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, s));
+    if (bytes > c->cub_bytes[slot]) {
+        if (c->cub_tmp[slot]) CK(cudaFree(c->cub_tmp[slot]));
+        CK(cudaMalloc(&c->cub_tmp[slot], bytes));
+        c->cub_bytes[slot] = bytes;
     }
-    CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, in, out, (int)n, c->s));
+    CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp[slot], bytes, in, out, (int)n, s));
     c->launches += 2;  // cub: tile-state init + scan
+}
+
+// set_mask branches: aux stream k continues after `from`'s work so far, and
+// is joined back into the main stream before the frame's summary. Serial
+// mode (z-slab contexts, NPSD_SETUP_SERIAL): everything on the main stream.
+cudaStream_t setup_fork(npsd_b200_ctx* c, cudaStream_t from, int k) {
+    if (!c->setup_par) return c->s;
+    require(c->nev < (int)(sizeof(c->evf) / sizeof(c->evf[0])), "npsd_b200: set_mask events");
+    cudaEvent_t e = c->evf[c->nev++];
+    CK(cudaEventRecord(e, from));
+    CK(cudaStreamWaitEvent(c->sx[k], e, 0));
+    return c->sx[k];
+}
+void setup_join(npsd_b200_ctx* c, int k) {
+    if (!c->setup_par) return;
+    require(c->nev < (int)(sizeof(c->evf) / sizeof(c->evf[0])), "npsd_b200: set_mask events");
+    cudaEvent_t e = c->evf[c->nev++];
+    CK(cudaEventRecord(e, c->sx[k]));
+    CK(cudaStreamWaitEvent(c->s, e, 0));
 }
 
 template <int D>
@@ -546,7 +578,7 @@ ConvTab tab_up(const npsd_b200_ctx* c, int l) {
 // Balanced schedule over the L0 tile columns of a tx x ty tiling (units of
 // `unit` planes, live within zdil planes of a fluid flag): k_sched_cols then
 // the prefix. Sizes are fixed per context; buffers are made on first use.
-void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int zdil, int gx, int gy) {
+void build_sched(npsd_b200_ctx* c, cudaStream_t s, SchedBufs& sb, int tx, int ty, int unit, int zdil, int gx, int gy) {
     const int tnx = (c->g0.nx + tx - 1) / tx, tny = (c->g0.ny + ty - 1) / ty;
     const int ntx = (tnx + gx - 1) / gx, nty = (tny + gy - 1) / gy;  // group columns
     // one piece per column: chunking columns into z pieces (chunk-major, so
@@ -572,17 +604,17 @@ void build_sched(npsd_b200_ctx* c, SchedBufs& sb, int tx, int ty, int unit, int 
         sb.last = dalloc<int>((size_t)sb.ncol);
     }
     const Geom& g = c->g0;
-    k_col_range<<<(sb.ncol * 32 + kBlock - 1) / kBlock, kBlock, 0, c->s>>>(
+    k_col_range<<<(sb.ncol * 32 + kBlock - 1) / kBlock, kBlock, 0, s>>>(
         c->tflags, c->tf_ntx, c->tf_nty, g.nz, g.zo0, g.zo1, gx * tx / kFlagTX, gy * ty / kFlagTY, ntx, nty, zdil,
         sb.first, sb.last);
-    k_sched_pieces<<<(sb.npiece + kBlock - 1) / kBlock, kBlock, 0, c->s>>>(sb.first, sb.last, sb.ncol, sb.nchunk, sb.hu,
+    k_sched_pieces<<<(sb.npiece + kBlock - 1) / kBlock, kBlock, 0, s>>>(sb.first, sb.last, sb.ncol, sb.nchunk, sb.hu,
                                                                          g.zo0, g.zo1, unit, zdil, sb.zlo, sb.len);
     CK(cudaGetLastError());
     c->launches += 2;
     // exclusive prefix (lengths are non-negative: scanned as u32), total included
     auto* len = reinterpret_cast<uint32_t*>(sb.len);
     auto* pre = reinterpret_cast<uint32_t*>(sb.pre);
-    scan_u32(c, len, pre, sb.npiece + 1);
+    scan_u32(c, s, 1, len, pre, sb.npiece + 1);
 }
 
 // one wave of k's blocks (the schedule's grid)
@@ -603,24 +635,114 @@ void dedup_patterns(npsd_b200_ctx* c, cudaStream_t s, int l, const uint32_t* cou
                     uint32_t* pid, uint32_t* rep, uint32_t* npat) {
     const unsigned long long cap = c->cap_ht[l];
     const long long items = std::min<long long>(c->L[l].g.n, (long long)cap);
-    CK(cudaMemsetAsync(c->htk, 0xff, cap * sizeof(unsigned long long), s));
+    unsigned long long* htk = c->htk + c->htoff[l];  // level l's own table and keys: levels run concurrently
+    uint32_t* htv = c->htv + c->htoff[l];
+    CK(cudaMemsetAsync(htk, 0xff, cap * sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(npat, 0, sizeof(uint32_t), s));
-    LAUNCH(c, s, k_dedup_insert, items, c->dkeys, count, list, c->htk, c->htv, cap - 1, c->dvals, rep, npat,
-           &c->d_info->flags, 1u << (2 * l));
-    LAUNCH(c, s, k_dedup_ids, items, c->dvals, count, c->htv, cap - 1, (uint32_t)c->tab_cap[l], pid);
+    LAUNCH(c, s, k_dedup_insert, items, c->dkeys + c->koff[l], count, list, htk, htv, cap - 1, c->dvals + c->koff[l],
+           rep, npat, &c->d_info->flags, 1u << (2 * l));
+    LAUNCH(c, s, k_dedup_ids, items, c->dvals + c->koff[l], count, htv, cap - 1, (uint32_t)c->tab_cap[l], pid);
 }
 
-// Every launch of a frame's setup, in stream order, with no host
-// synchronisation and no host decision on device data (graph-capturable):
-// sizes come from the device (counts), capacities from earlier frames.
+// Every launch of a frame's setup, with no host synchronisation and no host
+// decision on device data (graph-capturable): sizes come from the device
+// (counts), capacities from earlier frames. The independent chains are
+// branches (setup_fork / setup_join), so the captured graph's critical path
+// is the longest chain, not the sum of ~80 small launches:
+//   main        level-0 classification, scans, dictionary, sublists, rows
+//   sx[0]       the solver vectors' zero invariant (memsets)
+//   sx[1]       the tile-column schedules (tile flags of the classification)
+//   sx[2]       pooled images, classification and lists of levels >= 1
+//   sx[2 + l]   level l's dictionary and rows (after sx[2]'s level l)
 template <int D>
 void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
     cudaStream_t s = c->s;
+    c->nev = 0;
     LevelBufs& L0 = c->L[0];
     constexpr int NCW = (D == 3) ? 27 : 9;
     CK(cudaMemsetAsync(c->d_info, 0, sizeof(SetupInfo), s));
     // window counts of the linear blocks, levels l < depth - 1 (k_zfinal below)
     for (int l = 0; l + 1 < c->depth; ++l) CK(cudaMemsetAsync(c->L[l].zG, 0, 3 * NCW * sizeof(unsigned long long), s));
+    {  // zero invariant of the solver vectors at the new non-fluid cells
+        cudaStream_t sm = setup_fork(c, s, 0);
+        const size_t nb = (size_t)c->g0.n * sizeof(double);
+        CK(cudaMemsetAsync(c->X1, 0, nb, sm));
+        CK(cudaMemsetAsync(c->R, 0, nb, sm));
+        CK(cudaMemsetAsync(c->Dtmp, 0, nb, sm));
+        CK(cudaMemsetAsync(c->Dring, 0, nb * (size_t)c->ring_alloc, sm));
+    }
+    // levels >= 1: pooled images (from the cell types: independent of level 0's classification)
+    const cudaStream_t sc = setup_fork(c, s, 2);
+    for (int l = 1; l < c->depth; ++l) {
+        LevelBufs& Lf = c->L[l - 1];
+        LevelBufs& Lc = c->L[l];
+        // pure-type bytes for the z-marching classifier (scratch: this level's row codes, written later)
+        const bool marchc = D == 3 && !c->slab.on && Lc.g.nx % 32 == 0;
+        uint8_t* pure = marchc ? reinterpret_cast<uint8_t*>(Lc.rcode) : nullptr;
+        LAUNCH(c, sc, k_pool_image<D>, Lc.g.n, Lf.g, Lc.g, (l == 1) ? dtypes : nullptr, (l == 1) ? nullptr : Lf.img,
+               Lc.img, pure);
+        if (c->slab.on) {
+            // ghost planes: the outside of the domain, then the neighbours' planes
+            if (Lc.g.zo0 > 0)
+                LAUNCH(c, sc, k_solid_planes, (long long)Lc.g.zo0 * Lc.g.nx * Lc.g.ny, Lc.g, Lc.img, 0, Lc.g.zo0);
+            if (Lc.g.zo1 < Lc.g.nz)
+                LAUNCH(c, sc, k_solid_planes, (long long)(Lc.g.nz - Lc.g.zo1) * Lc.g.nx * Lc.g.ny, Lc.g, Lc.img,
+                       Lc.g.zo1, Lc.g.nz);
+            for (int ch = 0; ch < 3; ++ch) slab_exchange(c, sc, Lc.img + (size_t)ch * Lc.g.n, sizeof(float), l);
+        }
+        if (marchc) {
+            constexpr int ZC = 8;
+            const dim3 grid(Lc.g.nx / 32, (Lc.g.ny + 7) / 8, (Lc.g.nz + ZC - 1) / ZC);
+            LAUNCH3(c, sc, (k_classify_march<ZC, false>), grid, dim3(32, 8), Lc.g, (const uint8_t*)pure, Lc.cls,
+                    Lc.mmask, Lc.mcount, (uint32_t*)nullptr, (uint32_t*)nullptr, 0, 0, (uint8_t*)nullptr, ZsumArgs{},
+                    SubMasks{});
+        } else {
+            LAUNCH(c, sc, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
+        }
+        if (Lc.nseg <= kScanSmallMax) {
+            SmallScan ss{};
+            ss.cnt[0] = Lc.mcount;
+            ss.base[0] = Lc.mbase;
+            ss.n = 1;
+            ss.mask = Lc.mmask;
+            ss.list = Lc.mlist;
+            LAUNCH3(c, sc, k_scan_small, dim3(1), dim3(kScanSmallT), Lc.nseg, ss);
+        } else {
+            scan_u32(c, sc, 2, Lc.mcount, Lc.mbase, Lc.nseg + 1);
+            LAUNCH(c, sc, k_mixed_list, Lc.nseg, Lc.nseg, (const uint32_t*)Lc.mmask, (const uint32_t*)Lc.mbase,
+                   Lc.mlist);
+        }
+        // level l's dictionary (hashed windows, verified) and rows
+        const cudaStream_t sl = setup_fork(c, sc, 2 + l);
+        const uint32_t rows_cap = (uint32_t)c->tab_cap[l];
+        const uint32_t rows_bit = 1u << (2 * l + 1);
+        uint32_t* rep = c->crep + c->roff[l];
+        uint32_t* npat = c->cnpat + l;
+        const uint32_t* unver = &c->d_info->unverified[l];
+        const long long items = std::min<long long>(Lc.g.n, (long long)c->cap_ht[l]);
+        LAUNCH(c, sl, k_window_hash<D>, items, Lc.g, Lc.img, Lc.mlist, Lc.mcnt, c->dkeys + c->koff[l],
+               c->dvals + c->koff[l]);
+        dedup_patterns(c, sl, l, Lc.mcnt, Lc.mlist, Lc.pid, rep, npat);
+        CK(cudaMemcpyAsync(&c->d_info->npat[l], npat, sizeof(uint32_t), cudaMemcpyDeviceToDevice, sl));
+        LAUNCH(c, sl, k_verify_windows<D>, items, Lc.g, Lc.img, Lc.mlist, Lc.mcnt, Lc.pid, (const uint32_t*)rep,
+               &c->d_info->unverified[l]);
+        LAUNCH(c, sl, k_row_codes, Lc.g.n, Lc.g, Lc.cls, Lc.mmask, Lc.mbase, Lc.pid, unver, rows_cap, Lc.rcode);
+        // rows: one per window pattern when the hashed dictionary verifies, else one per mixed cell
+        const long long row_items = 32LL * std::min<long long>(rows_cap, Lc.g.n);
+        if (l < c->depth - 1) {
+            const LevelOffsets& o = c->offs[(size_t)l];
+            LAUNCH(c, sl, k_build_rows<D>, row_items, Lc.g, (const uint8_t*)nullptr, (const float*)Lc.img,
+                   (const uint32_t*)rep, (const uint32_t*)npat, (const uint32_t*)Lc.mlist, (const uint32_t*)Lc.mcnt,
+                   unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + o.down_W, c->d_params + o.down_B,
+                   Lc.tab_down, (const float*)(c->d_params + o.up_W), (const float*)(c->d_params + o.up_B), Lc.tab_up);
+        } else {
+            LAUNCH(c, sl, k_build_rows<D>, row_items, Lc.g, (const uint8_t*)nullptr, (const float*)Lc.img,
+                   (const uint32_t*)rep, (const uint32_t*)npat, (const uint32_t*)Lc.mlist, (const uint32_t*)Lc.mcnt,
+                   unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + c->coarse_W, c->d_params + c->coarse_B,
+                   Lc.tab_down, (const float*)nullptr, (const float*)nullptr, (float*)nullptr);
+        }
+    }
+    // level 0
     const bool march0 = D == 3 && c->g0.nx % 32 == 0 && c->depth - 1 <= kMaxDepth - 1;
     if (march0) {
         // cell bytes, masks, tile flags and every level's window counts in one z-marching pass
@@ -652,115 +774,77 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
                c->tflags);
     }
-    scan_u32(c, L0.mcount, L0.mbase, L0.nseg + 1);  // totals land in base[nseg]
-    scan_u32(c, c->fcount, c->fbase, L0.nseg + 1);
-    build_sched(c, c->sch_stencil, kTX, kTY, 1, 0, 1, 1);
-    if (kMarchSY != kSY) build_sched(c, c->sch_march, kTX, kMarchSY, 1, 0, 1, 1);
-    if (D == 3 && c->depth > 1) build_sched(c, c->sch_down0, kTX, kTY, 2, 1, 1, 1);
-    for (int l = 1; l < c->depth; ++l) {
-        LevelBufs& Lf = c->L[l - 1];
-        LevelBufs& Lc = c->L[l];
-        // pure-type bytes for the z-marching classifier (scratch: this level's row codes, written later)
-        const bool marchc = D == 3 && !c->slab.on && Lc.g.nx % 32 == 0;
-        uint8_t* pure = marchc ? reinterpret_cast<uint8_t*>(Lc.rcode) : nullptr;
-        LAUNCH(c, s, k_pool_image<D>, Lc.g.n, Lf.g, Lc.g, (l == 1) ? dtypes : nullptr, (l == 1) ? nullptr : Lf.img,
-               Lc.img, pure);
-        if (c->slab.on) {
-            // ghost planes: the outside of the domain, then the neighbours' planes
-            if (Lc.g.zo0 > 0) LAUNCH(c, s, k_solid_planes, (long long)Lc.g.zo0 * Lc.g.nx * Lc.g.ny, Lc.g, Lc.img, 0, Lc.g.zo0);
-            if (Lc.g.zo1 < Lc.g.nz)
-                LAUNCH(c, s, k_solid_planes, (long long)(Lc.g.nz - Lc.g.zo1) * Lc.g.nx * Lc.g.ny, Lc.g, Lc.img, Lc.g.zo1,
-                       Lc.g.nz);
-            for (int ch = 0; ch < 3; ++ch) slab_exchange(c, s, Lc.img + (size_t)ch * Lc.g.n, sizeof(float), l);
+    if (!march0) LAUNCH(c, s, k_sub_masks, L0.g.n, L0.g, L0.cls, c->dmask, c->dcount, c->umask, c->ucount);
+    const bool small0 = L0.nseg <= kScanSmallMax;
+    {
+        const cudaStream_t sb = setup_fork(c, s, 1);
+        if (!small0) {  // the down / up prefixes (k_mixed_sub, after a join)
+            scan_u32(c, sb, 1, c->dcount, c->dbase, L0.nseg + 1);
+            scan_u32(c, sb, 1, c->ucount, c->ubase, L0.nseg + 1);
         }
-        if (marchc) {
-            constexpr int ZC = 8;
-            const dim3 grid(Lc.g.nx / 32, (Lc.g.ny + 7) / 8, (Lc.g.nz + ZC - 1) / ZC);
-            LAUNCH3(c, s, (k_classify_march<ZC, false>), grid, dim3(32, 8), Lc.g, (const uint8_t*)pure, Lc.cls,
-                    Lc.mmask, Lc.mcount, (uint32_t*)nullptr, (uint32_t*)nullptr, 0, 0, (uint8_t*)nullptr, ZsumArgs{},
-                    SubMasks{});
-        } else {
-            LAUNCH(c, s, k_classify<D>, Lc.g.n, Lc.g, Lc.img, Lc.cls, Lc.mmask, Lc.mcount);
-        }
-        scan_u32(c, Lc.mcount, Lc.mbase, Lc.nseg + 1);
+        build_sched(c, sb, c->sch_stencil, kTX, kTY, 1, 0, 1, 1);
+        if (kMarchSY != kSY) build_sched(c, sb, c->sch_march, kTX, kMarchSY, 1, 0, 1, 1);
+        if (D == 3 && c->depth > 1) build_sched(c, sb, c->sch_down0, kTX, kTY, 2, 1, 1, 1);
     }
-    // compact mixed-cell lists per level
-    for (int l = 0; l < c->depth; ++l) {
-        LevelBufs& L = c->L[l];
-        LAUNCH(c, s, k_mixed_list, L.nseg, L.nseg, (const uint32_t*)L.mmask, (const uint32_t*)L.mbase, L.mlist);
+    // the mixed, fluid, down and up prefixes (totals land in base[nseg]) and the mixed list
+    if (small0) {
+        SmallScan ss{{L0.mcount, c->fcount, c->dcount, c->ucount}, {L0.mbase, c->fbase, c->dbase, c->ubase}, 4,
+                     L0.mmask, L0.mlist};
+        LAUNCH3(c, s, k_scan_small, dim3(1), dim3(kScanSmallT), L0.nseg, ss);
+    } else {
+        scan_u32(c, s, 0, L0.mcount, L0.mbase, L0.nseg + 1);
+        scan_u32(c, s, 0, c->fcount, c->fbase, L0.nseg + 1);
+        LAUNCH(c, s, k_mixed_list, L0.nseg, L0.nseg, (const uint32_t*)L0.mmask, (const uint32_t*)L0.mbase, L0.mlist);
     }
-    // level 0: window-pattern dictionary (pid per mixed cell, one row per pattern),
+    // window-pattern dictionary (pid per mixed cell, one row per pattern),
     // then the solve's down / up sublists with their pattern ids
     LAUNCH(c, s, k_window_keys<D>, std::min<long long>(c->g0.n, (long long)c->cap_ht[0]), c->g0, dtypes, L0.mlist,
            L0.mcnt, c->dkeys, c->dvals);
     dedup_patterns(c, s, 0, L0.mcnt, L0.mlist, c->pid0, c->repcell0, c->npat0);
     CK(cudaMemcpyAsync(&c->d_info->npat[0], c->npat0, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    if (!march0) LAUNCH(c, s, k_sub_masks, L0.g.n, L0.g, L0.cls, c->dmask, c->dcount, c->umask, c->ucount);
-    scan_u32(c, c->dcount, c->dbase, L0.nseg + 1);
-    scan_u32(c, c->ucount, c->ubase, L0.nseg + 1);
+    if (!small0) setup_join(c, 1);
     LAUNCH(c, s, k_mixed_sub, std::min<long long>(c->g0.n, (long long)c->cap_ht[0]), L0.mlist, c->pid0, L0.mcnt,
            c->dmask, c->dbase, c->umask, c->ubase, c->dlist0, c->dkid0, c->ulist0, c->ukid0);
-    ZfinArgs zf{};
-    for (int l = 0; l < c->depth; ++l) {
-        LevelBufs& L = c->L[l];
-        const uint8_t* st = (l == 0) ? dtypes : nullptr;
-        const float* im = (l == 0) ? nullptr : L.img;
-        const uint32_t rows_cap = (uint32_t)c->tab_cap[l];
-        const uint32_t rows_bit = 1u << (2 * l + 1);
-        // rows: one per window pattern (level 0 always; above when the hashed
-        // dictionary verifies), else one per mixed cell
-        const uint32_t* cells = (l == 0) ? c->repcell0 : c->crep;
-        const uint32_t* ncells = (l == 0) ? c->npat0 : c->cnpat;
-        const uint32_t* unver = (l == 0) ? nullptr : &c->d_info->unverified[l];
-        if (l > 0) {
-            const long long items = std::min<long long>(L.g.n, (long long)c->cap_ht[l]);
-            LAUNCH(c, s, k_window_hash<D>, items, L.g, L.img, L.mlist, L.mcnt, c->dkeys, c->dvals);
-            dedup_patterns(c, s, l, L.mcnt, L.mlist, L.pid, c->crep, c->cnpat);
-            CK(cudaMemcpyAsync(&c->d_info->npat[l], c->cnpat, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-            LAUNCH(c, s, k_verify_windows<D>, items, L.g, L.img, L.mlist, L.mcnt, L.pid, c->crep,
-                   &c->d_info->unverified[l]);
-            LAUNCH(c, s, k_row_codes, L.g.n, L.g, L.cls, L.mmask, L.mbase, L.pid, (const uint32_t*)unver, rows_cap,
-                   L.rcode);
-        }
-        const long long row_items = 32LL * std::min<long long>(rows_cap, L.g.n);
-        if (l < c->depth - 1) {
-            // the down and up kernels' rows of the same windows, one launch
-            const LevelOffsets& o = c->offs[(size_t)l];
-            LAUNCH(c, s, k_build_rows<D>, row_items, L.g, st, im, cells, ncells, (const uint32_t*)L.mlist,
-                   (const uint32_t*)L.mcnt, unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + o.down_W,
-                   c->d_params + o.down_B, L.tab_down, (const float*)(c->d_params + o.up_W),
-                   (const float*)(c->d_params + o.up_B), L.tab_up);
-            constexpr int NC = (D == 3) ? 27 : 9;
-            const double scale = std::ldexp(1.0, D * l);
-            if (!march0) {
-                const int nrows = L.g.ny * (L.g.zo1 - L.g.zo0);
-                const int blocks = std::max(1, std::min(nrows, 8 * c->num_sms));
-                LAUNCH3(c, s, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), L.g, st, im, (float)scale, zg_offset(c, l),
-                        c->gglob[l].nz, L.zG);
-            }
-            if (c->slab.on) slab_allreduce_u64(c, s, L.zG, 3 * NC);
-            zf.lv[l] = ZfinLevel{c->gglob[l], L.zG, scale, c->d_params + o.a_K, c->d_params + o.b_K,
-                                 c->params[o.a_bias], c->params[o.b_bias], c->zab + 2 * l, c->zab + 2 * l + 1};
-        } else {
-            LAUNCH(c, s, k_build_rows<D>, row_items, L.g, st, im, cells, ncells, (const uint32_t*)L.mlist,
-                   (const uint32_t*)L.mcnt, unver, rows_cap, &c->d_info->flags, rows_bit, c->d_params + c->coarse_W,
-                   c->d_params + c->coarse_B, L.tab_down, (const float*)nullptr, (const float*)nullptr,
-                   (float*)nullptr);
-        }
+    if (c->depth > 1) {
+        const uint32_t rows_cap = (uint32_t)c->tab_cap[0];
+        const LevelOffsets& o = c->offs[0];
+        LAUNCH(c, s, k_build_rows<D>, 32LL * std::min<long long>(rows_cap, L0.g.n), L0.g, dtypes, (const float*)nullptr,
+               (const uint32_t*)c->repcell0, (const uint32_t*)c->npat0, (const uint32_t*)L0.mlist,
+               (const uint32_t*)L0.mcnt, (const uint32_t*)nullptr, rows_cap, &c->d_info->flags, 1u << 1,
+               c->d_params + o.down_W, c->d_params + o.down_B, L0.tab_down, (const float*)(c->d_params + o.up_W),
+               (const float*)(c->d_params + o.up_B), L0.tab_up);
+    } else {
+        const uint32_t rows_cap = (uint32_t)c->tab_cap[0];
+        LAUNCH(c, s, k_build_rows<D>, 32LL * std::min<long long>(rows_cap, L0.g.n), L0.g, dtypes, (const float*)nullptr,
+               (const uint32_t*)c->repcell0, (const uint32_t*)c->npat0, (const uint32_t*)L0.mlist,
+               (const uint32_t*)L0.mcnt, (const uint32_t*)nullptr, rows_cap, &c->d_info->flags, 1u << 1,
+               c->d_params + c->coarse_W, c->d_params + c->coarse_B, L0.tab_down, (const float*)nullptr,
+               (const float*)nullptr, (float*)nullptr);
     }
+    for (int k = 0; k < 2 + c->depth; ++k) setup_join(c, k);  // memsets, schedules, coarse chain, levels 1..
     // linear-block coefficients of every level (k_zfinal: one block per level)
+    ZfinArgs zf{};
+    for (int l = 0; l + 1 < c->depth; ++l) {
+        LevelBufs& L = c->L[l];
+        constexpr int NC = (D == 3) ? 27 : 9;
+        const double scale = std::ldexp(1.0, D * l);
+        if (!march0) {
+            const int nrows = L.g.ny * (L.g.zo1 - L.g.zo0);
+            const int blocks = std::max(1, std::min(nrows, 8 * c->num_sms));
+            LAUNCH3(c, s, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), L.g, (l == 0) ? dtypes : nullptr,
+                    (l == 0) ? nullptr : (const float*)L.img, (float)scale, zg_offset(c, l), c->gglob[l].nz, L.zG);
+        }
+        if (c->slab.on) slab_allreduce_u64(c, s, L.zG, 3 * NC);
+        const LevelOffsets& o = c->offs[(size_t)l];
+        zf.lv[l] = ZfinLevel{c->gglob[l], L.zG, scale, c->d_params + o.a_K, c->d_params + o.b_K,
+                             c->params[o.a_bias], c->params[o.b_bias], c->zab + 2 * l, c->zab + 2 * l + 1};
+    }
     if (c->depth > 1) LAUNCH3(c, s, k_zfinal<D>, dim3(c->depth - 1), dim3(128), zf);
     InfoSources src{};
     src.n_fluid = c->fbase + L0.nseg;
     src.depth = c->depth;
     for (int l = 0; l < c->depth; ++l) src.n_mixed[l] = c->L[l].mcnt;
     LAUNCH3(c, s, k_setup_info, dim3(1), dim3(32), src, c->d_info);
-    // zero invariant of the solver vectors at the new non-fluid cells
-    const size_t nb = (size_t)c->g0.n * sizeof(double);
-    CK(cudaMemsetAsync(c->X1, 0, nb, s));
-    CK(cudaMemsetAsync(c->R, 0, nb, s));
-    CK(cudaMemsetAsync(c->Dtmp, 0, nb, s));
-    CK(cudaMemsetAsync(c->Dring, 0, nb * (size_t)c->ring_alloc, s));
     if (c->slab.on) {  // the ranks redo a frame together
         unsigned long long* v = reinterpret_cast<unsigned long long*>(c->red_b);
         LAUNCH3(c, s, k_flags_u64, dim3(1), dim3(32), (const uint32_t*)&c->d_info->flags, v);
@@ -769,7 +853,7 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
     }
 }
 
-// cub scratch for every scan set_mask runs (allocated outside any capture)
+// cub scratch for every scan set_mask runs, per scanning stream (allocated outside any capture)
 void ensure_cub(npsd_b200_ctx* c) {
     long long nmax = c->L[0].nseg;
     for (const SchedBufs* sb : {&c->sch_stencil, &c->sch_march, &c->sch_down0}) nmax = std::max<long long>(nmax, sb->npiece);
@@ -777,11 +861,12 @@ void ensure_cub(npsd_b200_ctx* c) {
     nmax = std::max<long long>(nmax, (long long)((c->g0.nx + kTX - 1) / kTX) * ((c->g0.ny + kTY - 1) / kTY) + 1);
     size_t bytes = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)nmax, c->s));
-    if (bytes > c->cub_bytes) {
-        if (c->cub_tmp) CK(cudaFree(c->cub_tmp));
-        CK(cudaMalloc(&c->cub_tmp, bytes));
-        c->cub_bytes = bytes;
-    }
+    for (int k = 0; k < 3; ++k)
+        if (bytes > c->cub_bytes[k]) {
+            if (c->cub_tmp[k]) CK(cudaFree(c->cub_tmp[k]));
+            CK(cudaMalloc(&c->cub_tmp[k], bytes));
+            c->cub_bytes[k] = bytes;
+        }
 }
 
 // kernel-row tables (rows per level) and the pattern hash table at the
@@ -801,8 +886,16 @@ void ensure_setup_capacity(npsd_b200_ctx* c) {
             ++c->buf_gen;
         }
     }
+    // one table per level (the levels' dictionaries run concurrently)
     unsigned long long ht = 0;
-    for (int l = 0; l < c->depth; ++l) ht = std::max(ht, c->cap_ht[l]);
+    bool moved = false;
+    for (int l = 0; l < c->depth; ++l) {
+        c->htoff[l] = ht;
+        ht += c->cap_ht[l];
+        moved |= c->cap_ht[l] != c->cap_ht_graph[l];  // a captured setup graph holds the sizes too
+        c->cap_ht_graph[l] = c->cap_ht[l];
+    }
+    if (moved) ++c->buf_gen;
     if (ht > c->ht_alloc) {
         if (c->htk) CK(cudaFree(c->htk));
         if (c->htv) CK(cudaFree(c->htv));
@@ -2120,7 +2213,11 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->red_b);
     F(c->xin_f);
     F(c->out_f);
-    F(c->cub_tmp);
+    for (void* p : c->cub_tmp) F(p);
+    for (auto x : c->sx)
+        if (x) cudaStreamDestroy(x);
+    for (auto e : c->evf)
+        if (e) cudaEventDestroy(e);
     if (c->st_host) cudaFreeHost(c->st_host);
     if (c->hist_host) cudaFreeHost(c->hist_host);
     if (c->times_host) cudaFreeHost(c->times_host);
@@ -2276,6 +2373,9 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
                 v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
                 CK(cudaStreamSetAttribute(c->s, cudaStreamAttributeAccessPolicyWindow, &v));
                 CK(cudaStreamSetAttribute(c->s2, cudaStreamAttributeAccessPolicyWindow, &v));
+                // set_mask's branches (created below) take the window in ctx_create's stream loop
+                c->apw = v;
+                c->apw_on = true;
             }
         }
         c->zab = dalloc<float>(2 * (size_t)depth);
@@ -2289,8 +2389,26 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->tf_nty = (ny + kFlagTY - 1) / kFlagTY;
         // every local plane: a z-slab's ghost planes are flagged too (k_classify_march, k_tile_flags)
         c->tflags = dalloc<uint8_t>((size_t)c->tf_ntx * c->tf_nty * c->L[0].g.nz);
-        c->dkeys = dalloc<unsigned long long>((size_t)c->g0.n);
-        c->dvals = dalloc<uint32_t>((size_t)c->g0.n);
+        {  // window keys of every level, and the coarse levels' pattern representatives
+            size_t nk = 0, nr = 0;
+            for (int l = 0; l < depth; ++l) {
+                c->koff[l] = nk;
+                nk += (size_t)c->L[l].g.n;
+                c->roff[l] = nr;
+                if (l > 0) nr += (size_t)c->L[l].g.n;
+            }
+            c->dkeys = dalloc<unsigned long long>(nk);
+            c->dvals = dalloc<uint32_t>(nk);
+            c->crep = dalloc<uint32_t>(std::max<size_t>(nr, 1));
+            c->cnpat = dalloc<uint32_t>((size_t)kMaxDepth);
+        }
+        if (const char* e = std::getenv("NPSD_SETUP_SERIAL")) c->setup_par = (e[0] == '0');
+        if (c->slab.on) c->setup_par = false;  // the communicator's exchanges run on the main stream
+        for (auto& x : c->sx) {
+            CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            if (c->apw_on) CK(cudaStreamSetAttribute(x, cudaStreamAttributeAccessPolicyWindow, &c->apw));
+        }
+        for (auto& e : c->evf) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         for (uint32_t** v : {&c->dmask, &c->dcount, &c->dbase, &c->umask, &c->ucount, &c->ubase}) {
             *v = dalloc<uint32_t>((size_t)nseg0 + 1);
             CK(cudaMemset(*v, 0, ((size_t)nseg0 + 1) * sizeof(uint32_t)));
@@ -2312,8 +2430,6 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->dkid0 = dalloc<uint32_t>((size_t)c->g0.n);
         c->ulist0 = dalloc<uint32_t>((size_t)c->g0.n);
         c->ukid0 = dalloc<uint32_t>((size_t)c->g0.n);
-        c->crep = dalloc<uint32_t>((size_t)std::max<long long>(c->depth > 1 ? c->L[1].g.n : 1, 1));
-        c->cnpat = dalloc<uint32_t>(1);
         c->check_flag = dalloc<unsigned int>(1);
         c->npat0 = dalloc<uint32_t>(1);
         const size_t n = (size_t)c->g0.n;

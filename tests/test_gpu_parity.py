@@ -568,3 +568,31 @@ def test_classify_simd_equals_scalar(b200, monkeypatch, case):
     for la, lb in zip(a[4], b[4]):
         assert np.array_equal(la, lb)
     assert np.array_equal(a[5], b[5]) and a[6] == b[6]
+
+
+def test_setup_branches_equal_serial(b200, monkeypatch):
+    """set_mask's graph runs its independent chains as branches (aux streams
+    forked and joined through events); one stream (NPSD_SETUP_SERIAL=1) gives
+    the same frame bit for bit, across a frame sequence through one context
+    whose capacities grow on the way (a simple frame, then a random one)."""
+    n = 64
+    frames = list(scenes.droplet_frames(n, 3))
+    frames.insert(1, scenes.random_types((n, n, n), 91, p=(0.5, 0.3, 0.2), blobs=8))
+    p = b200.default_model()
+    out = {}
+    for serial in ("1", "0"):
+        monkeypatch.setenv("NPSD_SETUP_SERIAL", serial)
+        ctx = b200.Context(3, (n, n, n), p)
+        res = []
+        for f, t in enumerate(frames):
+            ctx.set_mask(t)
+            r = np.random.default_rng(f).standard_normal(int((t == 0).sum()))
+            b = b200.rhs_normal(50 + f, t.size)[t.reshape(-1) == 0]
+            rep = ctx.psdo_solve(b, b200.SolveConfig(max_iters=300)).report
+            res.append((ctx.mixed_counts(), ctx.precond_apply(r), rep.iterations, rep.residual_history))
+        out[serial] = res
+        ctx.close()
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a[0], b[0])
+        assert np.array_equal(a[1], b[1])
+        assert a[2] == b[2] and np.array_equal(a[3], b[3])

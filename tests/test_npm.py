@@ -69,12 +69,13 @@ def test_npm_errors(tmp_path):
 
 
 def test_committed_trained_models_load():
-    """The trained 3D model files (DEFAULT_MODEL, depth 5, and the depth-4
-    model npsd3d_L4.npm): dim-3 files of the right size, each with its training
-    report (tools/train3d.py)."""
+    """The trained 3D model files (DEFAULT_MODEL, depth 6, and the depth-5 and
+    depth-4 models npsd3d_L5.npm / npsd3d_L4.npm): dim-3 files of the right
+    size, each with its training report (tools/train3d.py)."""
     import json
 
-    for path, depth in ((b200.DEFAULT_MODEL, 5), (b200.DEFAULT_MODEL.parent / "npsd3d_L4.npm", 4)):
+    wdir = b200.DEFAULT_MODEL.parent
+    for path, depth in ((b200.DEFAULT_MODEL, 6), (wdir / "npsd3d_L5.npm", 5), (wdir / "npsd3d_L4.npm", 4)):
         W = b200.load_npm(path)
         assert (W.dim, W.depth, W.flat.size) == (3, depth, b200.param_count(3, depth))
         assert np.all(np.isfinite(W.flat))

@@ -15,9 +15,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--depth", type=int, default=None, help="network depth (default: the default model's)")
 a = ap.parse_args()
 types, _ = scenes.config(a.config, a.n)
-ctx = b200.Context(3, types.shape, b200.identity_params(4))
+depth = a.depth or b200.default_model().depth
+ctx = b200.Context(3, types.shape, b200.identity_params(depth))
 d = b200.DeviceBuffer(ctx, types.size)
 d.upload(types.reshape(-1).copy())
 ctx.set_mask_device(d.ptr)
@@ -28,4 +30,4 @@ for i in range(a.reps):
     ctx.set_mask_device(d.ptr)
     ctx.event_record(1)
     ms.append(ctx.event_elapsed_ms(0, 1))
-print(f"set_mask device ms: {' '.join(f'{m:.3f}' for m in ms)}")
+print(f"{a.config} depth {depth} set_mask device ms: {' '.join(f'{m:.3f}' for m in ms)}")

@@ -69,7 +69,7 @@ def main() -> None:
     ap.add_argument("--ritz-m", type=int, default=0, help="Lanczos steps of the Ritz-vector RHS sets (0: smoothed noise)")
     ap.add_argument("--ritz-every", type=int, default=1, help="Ritz sets on every k-th frame")
     ap.add_argument("--big-only", action="store_true", help="train on the 2n^3 frames only")
-    ap.add_argument("--out", default=str(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L5.npm"))
+    ap.add_argument("--out", default=str(ROOT / "paper_2310_00177_b200" / "weights" / "npsd3d_L6.npm"))
     a = ap.parse_args()
     dev = torch.device("cuda")
     rng = np.random.default_rng(a.seed)
