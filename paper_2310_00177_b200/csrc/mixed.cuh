@@ -52,52 +52,64 @@ struct SmallScan {
     uint32_t* list;
 };
 constexpr int kScanSmallT = 1024;
-constexpr long long kScanSmallMax = 16384;  // segments (16 per thread)
+constexpr int kScanSmallPer = 8;  // segments per thread, loaded at once (one latency round)
+constexpr long long kScanSmallMax = (long long)kScanSmallT * kScanSmallPer;
 
 __global__ void __launch_bounds__(kScanSmallT) k_scan_small(long long nseg, SmallScan a) {
     __shared__ uint32_t wsum[kScanSmallT / 32];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const long long per = (nseg + kScanSmallT - 1) / kScanSmallT;
-    const long long s0 = min(nseg, per * t), s1 = min(nseg, s0 + per);
-    for (int k = 0; k < a.n; ++k) {
-        const uint32_t* __restrict__ cnt = a.cnt[k];
+    const long long s0 = (long long)t * kScanSmallPer;
+    // every input this thread needs, issued before any is used
+    uint32_t v[4][kScanSmallPer], m[kScanSmallPer];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int j = 0; j < kScanSmallPer; ++j) v[k][j] = (k < a.n && s0 + j < nseg) ? a.cnt[k][s0 + j] : 0u;
+#pragma unroll
+    for (int j = 0; j < kScanSmallPer; ++j) m[j] = (a.mask && s0 + j < nseg) ? a.mask[s0 + j] : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k >= a.n) break;
         uint32_t sum = 0;
-        for (long long i = s0; i < s1; ++i) sum += cnt[i];
-        uint32_t v = sum;  // inclusive warp scan, then the warps' totals
+#pragma unroll
+        for (int j = 0; j < kScanSmallPer; ++j) sum += v[k][j];
+        uint32_t x = sum;  // inclusive warp scan, then the warps' totals
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += y;
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        if (lane == 31) wsum[w] = v;
+        if (lane == 31) wsum[w] = x;
         __syncthreads();
         if (w == 0) {
-            uint32_t x = wsum[lane];
+            uint32_t q = wsum[lane];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
+                const uint32_t y = __shfl_up_sync(0xffffffffu, q, o);
+                if (lane >= o) q += y;
             }
-            wsum[lane] = x;
+            wsum[lane] = q;
         }
         __syncthreads();
-        uint32_t run = v - sum + (w ? wsum[w - 1] : 0u);
+        uint32_t run = x - sum + (w ? wsum[w - 1] : 0u);
+        const uint32_t total = wsum[kScanSmallT / 32 - 1];
         uint32_t* __restrict__ base = a.base[k];
-        const bool lst = k == 0 && a.mask;
-        for (long long i = s0; i < s1; ++i) {
-            base[i] = run;
-            if (lst) {
-                uint32_t m = a.mask[i];
-                uint32_t j = run;
-                const uint32_t c0 = (uint32_t)(i << 5);
-                while (m) {
-                    a.list[j++] = c0 + (uint32_t)(__ffs(m) - 1);
-                    m &= m - 1;
+#pragma unroll
+        for (int j = 0; j < kScanSmallPer; ++j) {
+            if (s0 + j < nseg) {
+                base[s0 + j] = run;
+                if (k == 0) {
+                    uint32_t mm = m[j], q = run;
+                    const uint32_t c0 = (uint32_t)((s0 + j) << 5);
+                    while (mm) {
+                        a.list[q++] = c0 + (uint32_t)(__ffs(mm) - 1);
+                        mm &= mm - 1;
+                    }
                 }
             }
-            run += cnt[i];
+            run += v[k][j];
         }
-        if (t == kScanSmallT - 1) base[nseg] = run;
+        if (t == 0) base[nseg] = total;
         __syncthreads();  // wsum is reused by the next array
     }
 }

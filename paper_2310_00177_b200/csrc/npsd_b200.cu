@@ -730,6 +730,11 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         // rows: one per window pattern when the hashed dictionary verifies, else one per mixed cell
         const long long row_items = 32LL * std::min<long long>(rows_cap, Lc.g.n);
         if (l < c->depth - 1) {
+            // the linear block's window counts: the pooled image x 8^l (exact dyadic values)
+            const int nrows = Lc.g.ny * (Lc.g.zo1 - Lc.g.zo0);
+            const int blocks = std::max(1, std::min(nrows, 8 * c->num_sms));
+            LAUNCH3(c, sl, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), Lc.g, (const uint8_t*)nullptr,
+                    (const float*)Lc.img, (float)std::ldexp(1.0, D * l), zg_offset(c, l), c->gglob[l].nz, Lc.zG);
             const LevelOffsets& o = c->offs[(size_t)l];
             LAUNCH(c, sl, k_build_rows<D>, row_items, Lc.g, (const uint8_t*)nullptr, (const float*)Lc.img,
                    (const uint32_t*)rep, (const uint32_t*)npat, (const uint32_t*)Lc.mlist, (const uint32_t*)Lc.mcnt,
@@ -748,8 +753,9 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         // cell bytes, masks, tile flags and every level's window counts in one z-marching pass
         constexpr int ZC = 16;
         ZsumArgs za{};
-        for (int l = 0; l + 1 < c->depth; ++l) za.G[l] = c->L[l].zG;
-        za.nzs = c->depth - 1;
+        // level 0's window counts (levels >= 1 count their pooled images, below)
+        za.G[0] = L0.zG;
+        za.nzs = (c->depth > 1) ? 1 : 0;
         za.zg_off = zg_offset(c, 0);
         za.nxg = c->gglob[0].nx;
         za.nyg = c->gglob[0].ny;
@@ -828,11 +834,11 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         LevelBufs& L = c->L[l];
         constexpr int NC = (D == 3) ? 27 : 9;
         const double scale = std::ldexp(1.0, D * l);
-        if (!march0) {
+        if (l == 0 && !march0) {  // (levels >= 1: in their branches)
             const int nrows = L.g.ny * (L.g.zo1 - L.g.zo0);
             const int blocks = std::max(1, std::min(nrows, 8 * c->num_sms));
-            LAUNCH3(c, s, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), L.g, (l == 0) ? dtypes : nullptr,
-                    (l == 0) ? nullptr : (const float*)L.img, (float)scale, zg_offset(c, l), c->gglob[l].nz, L.zG);
+            LAUNCH3(c, s, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), L.g, dtypes, (const float*)nullptr,
+                    (float)scale, zg_offset(c, l), c->gglob[l].nz, L.zG);
         }
         if (c->slab.on) slab_allreduce_u64(c, s, L.zG, 3 * NC);
         const LevelOffsets& o = c->offs[(size_t)l];

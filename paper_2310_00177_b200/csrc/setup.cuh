@@ -435,19 +435,20 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
             sm.ucount[seg] = __popc(um);
         }
         // linear-block window counts of every level l < nzs (k_zsums classes by
-        // global position): the warp row shares y and z; x classes differ only
-        // at the grid's ends
+        // global position; set_mask passes nzs = 1, the coarser levels count
+        // their pooled images): a cell interior at the coarsest counted level
+        // is interior at every level (the boundary bands grow with l), counted
+        // in registers; the rest, per thread, in shared memory
         if (za.nzs == 0) continue;
-        const uint32_t c0 = __popc(nib4(t0)), c1 = __popc(nib4(t1)), c2 = __popc(nib4(t2));
         const int zg = z + zoff;
         const bool row_inner = (y >> Lc) > 0 && (y >> Lc) < (za.nyg >> Lc) - 1 && (zg >> Lc) > 0 &&
                                (zg >> Lc) < (za.nzg >> Lc) - 1;
-        const bool x_inner = (X0 >> Lc) > 0 && ((X0 + W - 1) >> Lc) < (za.nxg >> Lc) - 1;
+        const bool x_inner = (x >> Lc) > 0 && ((x + 3) >> Lc) < (za.nxg >> Lc) - 1;
         if (row_inner && x_inner) {
-            cnt_int[0] += c0;
-            cnt_int[1] += c1;
-            cnt_int[2] += c2;
-        } else {
+            cnt_int[0] += __popc(nib4(t0));
+            cnt_int[1] += __popc(nib4(t1));
+            cnt_int[2] += __popc(nib4(t2));
+        } else if (owned) {
 #pragma unroll 1
             for (int l = 0; l < za.nzs; ++l) {
                 const int yl = y >> l, zl = zg >> l;
@@ -463,15 +464,14 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
 #pragma unroll
                     for (int a = 0; a < 3; ++a)
 #pragma unroll
-                        for (int b = 0; b < 3; ++b) cc[a][b] += (owned && tb == (uint32_t)a && kx == b) ? 1u : 0u;
+                        for (int b = 0; b < 3; ++b) cc[a][b] += (tb == (uint32_t)a && kx == b) ? 1u : 0u;
                 }
 #pragma unroll
                 for (int ty = 0; ty < 3; ++ty)
 #pragma unroll
-                    for (int kx = 0; kx < 3; ++kx) {
-                        const uint32_t v = __reduce_add_sync(rmask, cc[ty][kx]);
-                        if (lane == 0 && v) atomicAdd(&sG[l * 81 + ty * 27 + (kz * 3 + ky) * 3 + kx], (unsigned long long)v);
-                    }
+                    for (int kx = 0; kx < 3; ++kx)
+                        if (cc[ty][kx])
+                            atomicAdd(&sG[l * 81 + ty * 27 + (kz * 3 + ky) * 3 + kx], (unsigned long long)cc[ty][kx]);
             }
         }
     }
