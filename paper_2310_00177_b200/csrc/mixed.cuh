@@ -52,27 +52,37 @@ struct SmallScan {
     uint32_t* list;
 };
 constexpr int kScanSmallT = 1024;
-constexpr int kScanSmallPer = 8;  // segments per thread, loaded at once (one latency round)
+constexpr int kScanSmallPer = 8;  // segments per thread
 constexpr long long kScanSmallMax = (long long)kScanSmallT * kScanSmallPer;
+__device__ __forceinline__ int ss_pad(int i) { return i + (i >> 5); }  // conflict-free chunk reads
 
-__global__ void __launch_bounds__(kScanSmallT) k_scan_small(long long nseg, SmallScan a) {
+// Global loads and stores are coalesced (thread t: segments t + 1024 i); the
+// scan reads each thread's 8 consecutive segments from shared memory.
+__global__ void __launch_bounds__(kScanSmallT) k_scan_small(long long nseg_ll, SmallScan a) {
+    __shared__ uint32_t buf[kScanSmallMax + kScanSmallMax / 32];
     __shared__ uint32_t wsum[kScanSmallT / 32];
+    const int nseg = (int)nseg_ll;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const long long s0 = (long long)t * kScanSmallPer;
-    // every input this thread needs, issued before any is used
-    uint32_t v[4][kScanSmallPer], m[kScanSmallPer];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int j = 0; j < kScanSmallPer; ++j) v[k][j] = (k < a.n && s0 + j < nseg) ? a.cnt[k][s0 + j] : 0u;
-#pragma unroll
-    for (int j = 0; j < kScanSmallPer; ++j) m[j] = (a.mask && s0 + j < nseg) ? a.mask[s0 + j] : 0u;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if (k >= a.n) break;
-        uint32_t sum = 0;
+        const uint32_t* __restrict__ cnt = a.cnt[k];
+        uint32_t v[kScanSmallPer], mk[kScanSmallPer];  // counts (and array 0's masks), issued together
 #pragma unroll
-        for (int j = 0; j < kScanSmallPer; ++j) sum += v[k][j];
+        for (int i = 0; i < kScanSmallPer; ++i) {
+            const int s = t + kScanSmallT * i;
+            v[i] = (s < nseg) ? cnt[s] : 0u;
+            mk[i] = (k == 0 && a.mask && s < nseg) ? a.mask[s] : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < kScanSmallPer; ++i) buf[ss_pad(t + kScanSmallT * i)] = v[i];
+        __syncthreads();
+        uint32_t c[kScanSmallPer], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kScanSmallPer; ++j) {
+            c[j] = buf[ss_pad(kScanSmallPer * t + j)];
+            sum += c[j];
+        }
         uint32_t x = sum;  // inclusive warp scan, then the warps' totals
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -92,25 +102,33 @@ __global__ void __launch_bounds__(kScanSmallT) k_scan_small(long long nseg, Smal
         }
         __syncthreads();
         uint32_t run = x - sum + (w ? wsum[w - 1] : 0u);
-        const uint32_t total = wsum[kScanSmallT / 32 - 1];
-        uint32_t* __restrict__ base = a.base[k];
 #pragma unroll
         for (int j = 0; j < kScanSmallPer; ++j) {
-            if (s0 + j < nseg) {
-                base[s0 + j] = run;
-                if (k == 0) {
-                    uint32_t mm = m[j], q = run;
-                    const uint32_t c0 = (uint32_t)((s0 + j) << 5);
-                    while (mm) {
-                        a.list[q++] = c0 + (uint32_t)(__ffs(mm) - 1);
-                        mm &= mm - 1;
-                    }
+            buf[ss_pad(kScanSmallPer * t + j)] = run;
+            run += c[j];
+        }
+        __syncthreads();
+        uint32_t* __restrict__ base = a.base[k];
+#pragma unroll
+        for (int i = 0; i < kScanSmallPer; ++i) {
+            const int s = t + kScanSmallT * i;
+            if (s < nseg) base[s] = buf[ss_pad(s)];
+        }
+        if (t == 0) base[nseg] = wsum[kScanSmallT / 32 - 1];
+        if (k == 0 && a.mask) {  // the list: adjacent lanes, adjacent segments
+#pragma unroll
+            for (int i = 0; i < kScanSmallPer; ++i) {
+                const int s = t + kScanSmallT * i;
+                if (s >= nseg) break;
+                uint32_t m = mk[i], q = buf[ss_pad(s)];
+                const uint32_t c0 = (uint32_t)s << 5;
+                while (m) {
+                    a.list[q++] = c0 + (uint32_t)(__ffs(m) - 1);
+                    m &= m - 1;
                 }
             }
-            run += v[k][j];
         }
-        if (t == 0) base[nseg] = total;
-        __syncthreads();  // wsum is reused by the next array
+        __syncthreads();  // buf and wsum are reused by the next array
     }
 }
 

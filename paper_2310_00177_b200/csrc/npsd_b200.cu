@@ -731,8 +731,8 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         const long long row_items = 32LL * std::min<long long>(rows_cap, Lc.g.n);
         if (l < c->depth - 1) {
             // the linear block's window counts: the pooled image x 8^l (exact dyadic values)
-            const int nrows = Lc.g.ny * (Lc.g.zo1 - Lc.g.zo0);
-            const int blocks = std::max(1, std::min(nrows, 8 * c->num_sms));
+            const int nrows = Lc.g.ny * (Lc.g.zo1 - Lc.g.zo0);  // a warp per row
+            const int blocks = std::max(1, std::min((nrows + kBlock / 32 - 1) / (kBlock / 32), 4 * c->num_sms));
             LAUNCH3(c, sl, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), Lc.g, (const uint8_t*)nullptr,
                     (const float*)Lc.img, (float)std::ldexp(1.0, D * l), zg_offset(c, l), c->gglob[l].nz, Lc.zG);
             const LevelOffsets& o = c->offs[(size_t)l];
@@ -761,15 +761,31 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         za.nyg = c->gglob[0].ny;
         za.nzg = c->gglob[0].nz;
         const SubMasks sub{c->dmask, c->dcount, c->umask, c->ucount};
-        if (c->classify_simd && c->g0.nx % 128 == 0 && c->g0.ny % 8 == 0) {
-            // byte SIMD, 4 cells per thread, 128 x 8 tiles (setup.cuh k_classify_simd)
-            const dim3 grid(c->g0.nx / 128, c->g0.ny / 8, (c->g0.nz + ZC - 1) / ZC);
-            LAUNCH3(c, s, (k_classify_simd<32, ZC>), grid, dim3(256), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount,
-                    c->fmask, c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za, sub);
-        } else if (c->classify_simd && c->g0.nx % 64 == 0 && c->g0.ny % 16 == 0) {
-            const dim3 grid(c->g0.nx / 64, c->g0.ny / 16, (c->g0.nz + ZC - 1) / ZC);
-            LAUNCH3(c, s, (k_classify_simd<16, ZC>), grid, dim3(256), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount,
-                    c->fmask, c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za, sub);
+        // byte SIMD, 4 cells per thread, 128 x 8 or 64 x 16 tiles (setup.cuh
+        // k_classify_simd); planes per block: the most that still fill two waves
+        const bool simd32 = c->classify_simd && c->g0.nx % 128 == 0 && c->g0.ny % 8 == 0;
+        const bool simd16 = !simd32 && c->classify_simd && c->g0.nx % 64 == 0 && c->g0.ny % 16 == 0;
+        if (simd32 || simd16) {
+            const long long tiles = simd32 ? (long long)(c->g0.nx / 128) * (c->g0.ny / 8)
+                                           : (long long)(c->g0.nx / 64) * (c->g0.ny / 16);
+            const int zc = (tiles * ((c->g0.nz + 15) / 16) >= 2 * c->num_sms)  ? 16
+                           : (tiles * ((c->g0.nz + 3) / 4) >= 2 * c->num_sms) ? 4
+                                                                              : 2;
+            const dim3 grid(simd32 ? c->g0.nx / 128 : c->g0.nx / 64, simd32 ? c->g0.ny / 8 : c->g0.ny / 16,
+                            (c->g0.nz + zc - 1) / zc);
+#define NPSD_CLASSIFY_SIMD(LX, Z)                                                                                     \
+    LAUNCH3(c, s, (k_classify_simd<LX, Z>), grid, dim3(256), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask,   \
+            c->fcount, c->tf_ntx, c->tf_nty, c->tflags, za, sub)
+            if (simd32) {
+                if (zc == 16) NPSD_CLASSIFY_SIMD(32, 16);
+                else if (zc == 4) NPSD_CLASSIFY_SIMD(32, 4);
+                else NPSD_CLASSIFY_SIMD(32, 2);
+            } else {
+                if (zc == 16) NPSD_CLASSIFY_SIMD(16, 16);
+                else if (zc == 4) NPSD_CLASSIFY_SIMD(16, 4);
+                else NPSD_CLASSIFY_SIMD(16, 2);
+            }
+#undef NPSD_CLASSIFY_SIMD
         } else {
             const dim3 grid(c->g0.nx / 32, (c->g0.ny + 7) / 8, (c->g0.nz + ZC - 1) / ZC);
             LAUNCH3(c, s, (k_classify_march<ZC, true>), grid, dim3(32, 8), c->g0, dtypes, L0.cls, L0.mmask, L0.mcount,
@@ -835,8 +851,8 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         constexpr int NC = (D == 3) ? 27 : 9;
         const double scale = std::ldexp(1.0, D * l);
         if (l == 0 && !march0) {  // (levels >= 1: in their branches)
-            const int nrows = L.g.ny * (L.g.zo1 - L.g.zo0);
-            const int blocks = std::max(1, std::min(nrows, 8 * c->num_sms));
+            const int nrows = L.g.ny * (L.g.zo1 - L.g.zo0);  // a warp per row
+            const int blocks = std::max(1, std::min((nrows + kBlock / 32 - 1) / (kBlock / 32), 4 * c->num_sms));
             LAUNCH3(c, s, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), L.g, dtypes, (const float*)nullptr,
                     (float)scale, zg_offset(c, l), c->gglob[l].nz, L.zG);
         }

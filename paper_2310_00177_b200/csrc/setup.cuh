@@ -381,7 +381,10 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
         const uint32_t n4 = nonsolid4(U1) + nonsolid4(D1) + nonsolid4(__byte_perm(M0, M1, 0x6543)) +
                             nonsolid4(__byte_perm(M1, M2, 0x4321));
         // flag tiles: a cell whose in-plane 3 x 3 holds fluid (min 0)
-        if (__vcmpeq4(lo, 0u)) atomicOr(&sflag[(row / kFlagTY) * NFX + (4 * lane) / kFlagTX], 1u);
+        // (one atomic per 8-lane group, i.e. per 32-cell flag-tile row)
+        const uint32_t fb = __ballot_sync(0xffffffffu, __vcmpeq4(lo, 0u) != 0u);
+        if ((tid & 7) == 0 && ((fb >> (tid & 24)) & 0xffu))
+            atomicOr(&sflag[(row / kFlagTY) * NFX + (4 * lane) / kFlagTX], 1u);
         mnP = mnM, mxP = mxM, cvP = cvM;
         mnM = mnN, mxM = mxN, cvM = cvN, nbM = nbN;
         mnN = lo, mxN = hi, cvN = M1, nbN = n4;
@@ -925,30 +928,48 @@ __global__ void __launch_bounds__(kBlock) k_zsums_rows(Geom g, const uint8_t* __
                                                        const float* __restrict__ img, float scale, int zg_off, int nzg,
                                                        unsigned long long* __restrict__ G) {
     constexpr int NC = (D == 3) ? 27 : 9;
+    constexpr int kInterior = (D == 3) ? 13 : 4;
     __shared__ unsigned long long sG[3 * NC];
     for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x) sG[i] = 0ull;
     __syncthreads();
-    constexpr int kInterior = (D == 3) ? 13 : 4;
+    // a warp per row: its y / z class is warp-uniform; the row's two end
+    // cells (x classes 0 and 2) go to shared atomics, the rest is summed in
+    // registers (interior rows) or reduced per warp at the end of the row
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     unsigned long long inner[3] = {0ull, 0ull, 0ull};
-    const int nrows = g.ny * (g.zo1 - g.zo0);
-    for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
-        const int y = row % g.ny, zl = g.zo0 + row / g.ny, z = zl + zg_off;  // global plane
+    const long long nrows = (long long)g.ny * (g.zo1 - g.zo0);
+    for (long long row = (long long)blockIdx.x * wpb + (threadIdx.x >> 5); row < nrows;
+         row += (long long)gridDim.x * wpb) {
+        const int y = (int)(row % g.ny), zl = g.zo0 + (int)(row / g.ny), z = zl + zg_off;  // global plane
         const int ky = (y == 0) ? 0 : ((y == g.ny - 1) ? 2 : 1);
         const int kz = (D == 3) ? ((z == 0) ? 0 : ((z == nzg - 1) ? 2 : 1)) : 0;
+        const int cl1 = (kz * 3 + ky) * 3 + 1;
         const long long base = ((long long)zl * g.ny + y) * g.nx;
-        for (int x = threadIdx.x; x < g.nx; x += blockDim.x) {
-            const int kx = (x == 0) ? 0 : ((x == g.nx - 1) ? 2 : 1);
-            const int cl = (kz * 3 + ky) * 3 + kx;
+        unsigned long long racc[3] = {0ull, 0ull, 0ull};
+        for (int x = lane; x < g.nx; x += 32) {
             const long long c = base + x;
-            uint8_t t = 0;
-            if (src_types) t = src_types[c];
+            const bool xend = x == 0 || x == g.nx - 1;
+            const uint8_t t = src_types ? src_types[c] : (uint8_t)0;
+#pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
                 const unsigned long long v = src_types ? ((t == ch) ? 1ull : 0ull)
                                                        : (unsigned long long)__fmul_rn(img[ch * g.n + c], scale);
-                if (cl == kInterior)
-                    inner[ch] += v;
+                if (!xend)
+                    racc[ch] += v;
                 else if (v)
-                    atomicAdd(&sG[ch * NC + cl], v);
+                    atomicAdd(&sG[ch * NC + cl1 - 1 + ((x == 0) ? 0 : 2)], v);
+            }
+        }
+        if (cl1 == kInterior) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) inner[ch] += racc[ch];
+        } else {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                unsigned long long v = racc[ch];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0 && v) atomicAdd(&sG[ch * NC + cl1], v);
             }
         }
     }
@@ -956,7 +977,7 @@ __global__ void __launch_bounds__(kBlock) k_zsums_rows(Geom g, const uint8_t* __
         unsigned long long v = inner[ch];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sG[ch * NC + kInterior], v);
+        if (lane == 0 && v) atomicAdd(&sG[ch * NC + kInterior], v);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 3 * NC; i += blockDim.x)
