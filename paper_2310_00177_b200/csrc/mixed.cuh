@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(kBlock) k_mixed_list(long long nseg, const uin
 // total left in base[nseg]) and, optionally, the compacted list of the set
 // bits of array 0's mask (k_mixed_list) — one block, one launch: for the small
 // arrays of the coarse levels and of small grids, where two cub launches per
-// scan plus the list's launch cost more than the work.
+// scan cost more than the work. (set_mask writes the lists with k_mixed_list:
+// one block's serial per-segment loops took 37 us for level 0 at 64^3.)
 struct SmallScan {
     const uint32_t* cnt[4];
     uint32_t* base[4];

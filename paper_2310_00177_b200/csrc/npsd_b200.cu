@@ -704,9 +704,9 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
             ss.cnt[0] = Lc.mcount;
             ss.base[0] = Lc.mbase;
             ss.n = 1;
-            ss.mask = Lc.mmask;
-            ss.list = Lc.mlist;
             LAUNCH3(c, sc, k_scan_small, dim3(1), dim3(kScanSmallT), Lc.nseg, ss);
+            LAUNCH(c, sc, k_mixed_list, Lc.nseg, Lc.nseg, (const uint32_t*)Lc.mmask, (const uint32_t*)Lc.mbase,
+                   Lc.mlist);
         } else {
             scan_u32(c, sc, 2, Lc.mcount, Lc.mbase, Lc.nseg + 1);
             LAUNCH(c, sc, k_mixed_list, Lc.nseg, Lc.nseg, (const uint32_t*)Lc.mmask, (const uint32_t*)Lc.mbase,
@@ -811,8 +811,9 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
     // the mixed, fluid, down and up prefixes (totals land in base[nseg]) and the mixed list
     if (small0) {
         SmallScan ss{{L0.mcount, c->fcount, c->dcount, c->ucount}, {L0.mbase, c->fbase, c->dbase, c->ubase}, 4,
-                     L0.mmask, L0.mlist};
+                     nullptr, nullptr};
         LAUNCH3(c, s, k_scan_small, dim3(1), dim3(kScanSmallT), L0.nseg, ss);
+        LAUNCH(c, s, k_mixed_list, L0.nseg, L0.nseg, (const uint32_t*)L0.mmask, (const uint32_t*)L0.mbase, L0.mlist);
     } else {
         scan_u32(c, s, 0, L0.mcount, L0.mbase, L0.nseg + 1);
         scan_u32(c, s, 0, c->fcount, c->fbase, L0.nseg + 1);

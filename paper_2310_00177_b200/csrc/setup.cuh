@@ -137,12 +137,12 @@ __global__ void __launch_bounds__(256) k_classify_march(Geom g, const uint8_t* _
                                                         uint8_t* __restrict__ tflags, ZsumArgs za, SubMasks sm) {
     static_assert(kFlagTX == 32 && kFlagTY == 8, "the block tile is the flag tile");
     __shared__ uint8_t st[2][10][36];
-    __shared__ unsigned long long sG[L0 ? kMaxDepth * 81 : 1];
+    __shared__ uint32_t sG[L0 ? kMaxDepth * 81 : 1];  // 32-bit block counts (64-bit shared atomics are CAS loops)
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
     const int X0 = blockIdx.x * 32, Y0 = blockIdx.y * 8, Z0 = blockIdx.z * ZC;
     const long long plane = (long long)g.nx * g.ny;
     if (L0) {
-        for (int i = tid; i < za.nzs * 81; i += 256) sG[i] = 0ull;
+        for (int i = tid; i < za.nzs * 81; i += 256) sG[i] = 0u;
     }
     // staging: my (up to) two bytes of the 10 x 34 plane
     int off[2], sidx[2];
@@ -270,9 +270,9 @@ __global__ void __launch_bounds__(256) k_classify_march(Geom g, const uint8_t* _
                         if (tx == 0 && mk) {
                             const int cl = (kz * 3 + ky) * 3 + kv;
                             const uint32_t n0 = __popc(b0 & mk), n1 = __popc(b1 & mk), n2 = __popc(b2 & mk);
-                            if (n0) atomicAdd(&sG[l * 81 + 0 * 27 + cl], (unsigned long long)n0);
-                            if (n1) atomicAdd(&sG[l * 81 + 1 * 27 + cl], (unsigned long long)n1);
-                            if (n2) atomicAdd(&sG[l * 81 + 2 * 27 + cl], (unsigned long long)n2);
+                            if (n0) atomicAdd(&sG[l * 81 + 0 * 27 + cl], n0);
+                            if (n1) atomicAdd(&sG[l * 81 + 1 * 27 + cl], n1);
+                            if (n2) atomicAdd(&sG[l * 81 + 2 * 27 + cl], n2);
                         }
                     }
                 }
@@ -289,10 +289,10 @@ __global__ void __launch_bounds__(256) k_classify_march(Geom g, const uint8_t* _
     if (L0) {
         if (tx == 0)  // the all-interior counts go to the interior class (13) of every level
             for (int i = 0; i < za.nzs * 3; ++i)
-                if (zin_cnt[ty][i % 3]) atomicAdd(&sG[(i / 3) * 81 + (i % 3) * 27 + 13], (unsigned long long)zin_cnt[ty][i % 3]);
+                if (zin_cnt[ty][i % 3]) atomicAdd(&sG[(i / 3) * 81 + (i % 3) * 27 + 13], zin_cnt[ty][i % 3]);
         __syncthreads();
         for (int i = tid; i < za.nzs * 81; i += 256)
-            if (sG[i]) atomicAdd(&za.G[i / 81][i % 81], sG[i]);
+            if (sG[i]) atomicAdd(&za.G[i / 81][i % 81], (unsigned long long)sG[i]);
     }
 }
 
@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
     constexpr int NFX = W / kFlagTX, NFY = H / kFlagTY;  // flag tiles of the block tile
     static_assert(W % kFlagTX == 0 && H % kFlagTY == 0, "whole flag tiles");
     __shared__ uint32_t st[2][SH][SW];
-    __shared__ unsigned long long sG[kMaxDepth * 81];
+    // block counts: 32-bit (a block holds < 2^32 cells; 64-bit shared atomics are CAS loops)
+    __shared__ uint32_t sG[kMaxDepth * 81];
     __shared__ uint32_t sflag[NFX * NFY];
     __shared__ uint32_t sint[kMaxDepth][3];  // interior-class counts
     const int lane = threadIdx.x % LX, row = threadIdx.x / LX, tid = threadIdx.x;
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
     const unsigned rmask = (LX == 32) ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
     const int X0 = blockIdx.x * W, Y0 = blockIdx.y * H, Z0 = blockIdx.z * ZC;
     const long long plane = (long long)g.nx * g.ny;
-    for (int i = tid; i < za.nzs * 81; i += 256) sG[i] = 0ull;
+    for (int i = tid; i < za.nzs * 81; i += 256) sG[i] = 0u;
     if (tid < kMaxDepth * 3) sint[tid / 3][tid % 3] = 0u;
     // staging: my (up to) two words of the SH x SW plane window
     int off[2], sidx[2];
@@ -473,8 +474,7 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
                 for (int ty = 0; ty < 3; ++ty)
 #pragma unroll
                     for (int kx = 0; kx < 3; ++kx)
-                        if (cc[ty][kx])
-                            atomicAdd(&sG[l * 81 + ty * 27 + (kz * 3 + ky) * 3 + kx], (unsigned long long)cc[ty][kx]);
+                        if (cc[ty][kx]) atomicAdd(&sG[l * 81 + ty * 27 + (kz * 3 + ky) * 3 + kx], cc[ty][kx]);
             }
         }
     }
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
         for (int l = 0; l < za.nzs; ++l) sG[l * 81 + tid * 27 + 13] += sint[0][tid];
     __syncthreads();
     for (int i = tid; i < za.nzs * 81; i += 256)
-        if (sG[i]) atomicAdd(&za.G[i / 81][i % 81], sG[i]);
+        if (sG[i]) atomicAdd(&za.G[i / 81][i % 81], (unsigned long long)sG[i]);
 }
 
 // Tile occupancy at L0: flags[(z * nty + ty) * ntx + tx] = any fluid cell in
