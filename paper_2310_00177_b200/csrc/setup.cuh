@@ -299,16 +299,21 @@ __global__ void __launch_bounds__(256) k_classify_march(Geom g, const uint8_t* _
 // ---------------------------------------------------------------------------
 // Level-0 classification with byte SIMD (k_classify_simd): the outputs of
 // k_classify_march<ZC, true>, bit for bit, four cells per thread. A thread
-// owns a 32-bit word of cell types (x .. x+3) and marches z. Per staged plane
-// its 3 x 3 window summaries are whole-word ops: the column min / max of the
-// three rows (__vminu4 / __vmaxu4), the left / right neighbours by byte
-// permutes of the adjacent words, non-solid face-neighbour indicators as
-// byte adds. A block is LX lanes x (256 / LX) rows: a tile of 4 LX x (256 / LX)
-// cells (128 x 8 or 64 x 16), i.e. whole 32-cell mask segments (8 lanes) and
-// whole 32 x 8 flag tiles.
-__device__ __forceinline__ uint32_t nonsolid4(uint32_t v) {  // per byte: type != 2 (types 0..2)
-    const uint32_t x = v ^ 0x02020202u;
-    return (x | (x >> 1)) & 0x01010101u;
+// owns a 32-bit word of cell types (x .. x+3) and marches z. Types are staged
+// as one-hot byte codes 1 << t (1 fluid, 2 air, 4 solid; outside the domain
+// solid), so a window's set of types is the plain 32-bit OR of its words: the
+// 3 x 3 in-plane OR (rows, then the left / right neighbours by byte permutes
+// of adjacent words), then across three planes. A window is uniform iff its
+// OR equals the centre's code; it holds fluid iff bit 0 is set. (Byte min /
+// max intrinsics are emulated on sm_100: ~6 instructions each.) A block is
+// LX lanes x (256 / LX) rows: a tile of 4 LX x (256 / LX) cells (128 x 8 or
+// 64 x 16), i.e. whole 32-cell mask segments (8 lanes) and whole 32 x 8 flag
+// tiles.
+__device__ __forceinline__ uint32_t type_code4(uint32_t v) {  // bytes t in 0..2 -> 1 << t
+    return 0x01010101u + v + ((v >> 1) & 0x01010101u);
+}
+__device__ __forceinline__ uint32_t code_nonsolid4(uint32_t c) {  // per byte: code != 4
+    return (c | (c >> 1)) & 0x01010101u;
 }
 __device__ __forceinline__ uint32_t nib4(uint32_t b) {  // bytes' bit 0 -> 4-bit mask (byte i -> bit i)
     return ((b & 0x01010101u) * 0x00204081u) >> 21 & 0xFu;
@@ -356,7 +361,8 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
         for (int j = 0; j < 2; ++j)
             pv[j] = (zin && inxy[j]) ? __ldg(reinterpret_cast<const uint32_t*>(sp + off[j])) : 0x02020202u;
     };
-    uint32_t mnP = 0, mxP = 0, cvP = 0, mnM = 0, mxM = 0, cvM = 0, nbM = 0, mnN = 0, mxN = 0, cvN = 0, nbN = 0;
+    // per plane: the 3 x 3 type set (OR of codes), the centre code, the in-plane non-solid face neighbours
+    uint32_t orP = 0, cvP = 0, orM = 0, cvM = 0, nbM = 0, orN = 0, cvN = 0, nbN = 0;
     load_plane(Z0 - 1);
     // stage plane p, issue plane p + 1, summarise plane p into N; returns
     // (in sflag) the flag tiles of plane p holding fluid in their dilation
@@ -365,30 +371,26 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
         uint32_t* dst = &st[buf][0][0];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
-            if (use[j]) dst[sidx[j]] = pv[j];
+            if (use[j]) dst[sidx[j]] = type_code4(pv[j]);
         if (tid < NFX * NFY) sflag[tid] = 0u;
         load_plane(p + 1);
         __syncthreads();
         const uint32_t U0 = st[buf][row][lane], U1 = st[buf][row][lane + 1], U2 = st[buf][row][lane + 2];
         const uint32_t M0 = st[buf][row + 1][lane], M1 = st[buf][row + 1][lane + 1], M2 = st[buf][row + 1][lane + 2];
         const uint32_t D0 = st[buf][row + 2][lane], D1 = st[buf][row + 2][lane + 1], D2 = st[buf][row + 2][lane + 2];
-        const uint32_t n0 = __vminu4(__vminu4(U0, M0), D0), n1 = __vminu4(__vminu4(U1, M1), D1),
-                       n2 = __vminu4(__vminu4(U2, M2), D2);
-        const uint32_t x0 = __vmaxu4(__vmaxu4(U0, M0), D0), x1 = __vmaxu4(__vmaxu4(U1, M1), D1),
-                       x2 = __vmaxu4(__vmaxu4(U2, M2), D2);
+        const uint32_t r0 = U0 | M0 | D0, r1 = U1 | M1 | D1, r2 = U2 | M2 | D2;
         // bytes x-1 .. x+2 and x+1 .. x+4 of a row: permutes of adjacent words
-        const uint32_t lo = __vminu4(__vminu4(__byte_perm(n0, n1, 0x6543), n1), __byte_perm(n1, n2, 0x4321));
-        const uint32_t hi = __vmaxu4(__vmaxu4(__byte_perm(x0, x1, 0x6543), x1), __byte_perm(x1, x2, 0x4321));
-        const uint32_t n4 = nonsolid4(U1) + nonsolid4(D1) + nonsolid4(__byte_perm(M0, M1, 0x6543)) +
-                            nonsolid4(__byte_perm(M1, M2, 0x4321));
-        // flag tiles: a cell whose in-plane 3 x 3 holds fluid (min 0)
+        const uint32_t orp = __byte_perm(r0, r1, 0x6543) | r1 | __byte_perm(r1, r2, 0x4321);
+        const uint32_t n4 = code_nonsolid4(U1) + code_nonsolid4(D1) + code_nonsolid4(__byte_perm(M0, M1, 0x6543)) +
+                            code_nonsolid4(__byte_perm(M1, M2, 0x4321));
+        // flag tiles: a cell whose in-plane 3 x 3 holds fluid
         // (one atomic per 8-lane group, i.e. per 32-cell flag-tile row)
-        const uint32_t fb = __ballot_sync(0xffffffffu, __vcmpeq4(lo, 0u) != 0u);
+        const uint32_t fb = __ballot_sync(0xffffffffu, (orp & 0x01010101u) != 0u);
         if ((tid & 7) == 0 && ((fb >> (tid & 24)) & 0xffu))
             atomicOr(&sflag[(row / kFlagTY) * NFX + (4 * lane) / kFlagTX], 1u);
-        mnP = mnM, mxP = mxM, cvP = cvM;
-        mnM = mnN, mxM = mxN, cvM = cvN, nbM = nbN;
-        mnN = lo, mxN = hi, cvN = M1, nbN = n4;
+        orP = orM, cvP = cvM;
+        orM = orN, cvM = cvN, nbM = nbN;
+        orN = orp, cvN = M1, nbN = n4;
         __syncthreads();  // sflag complete; every read of this staging buffer done before its reuse
     };
     const int x = X0 + 4 * lane, y = Y0 + row;
@@ -407,19 +409,19 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
         if (y >= g.ny) continue;  // whole warp rows
         const long long c = (long long)z * plane + (long long)y * g.nx + x;
         const bool owned = z >= g.zo0 && z < g.zo1;
-        const uint32_t lo = __vminu4(mnP, __vminu4(mnM, mnN)), hi = __vmaxu4(mxP, __vmaxu4(mxM, mxN));
-        const uint32_t eq = __vcmpeq4(lo, hi), t = cvM;
-        const uint32_t diag = nbM + nonsolid4(cvP) + nonsolid4(cvN);
-        const uint32_t wf = __vcmpeq4(lo, 0u) & 0x80808080u;
-        *reinterpret_cast<uint32_t*>(cls + c) = (t & eq) | (0x03030303u & ~eq) | (t << 2) | (diag << 4) | wf;
+        const uint32_t wor = orP | orM | orN;                                      // the window's type set
+        const uint32_t mixb = (((wor ^ cvM) + 0x7f7f7f7fu) & 0x80808080u) >> 7;    // 1 per non-uniform byte
+        const uint32_t t = (cvM >> 1) & 0x03030303u;                               // the centre's type
+        const uint32_t diag = nbM + code_nonsolid4(cvP) + code_nonsolid4(cvN);
+        const uint32_t wf = wor & 0x01010101u;                                     // fluid in the window
+        *reinterpret_cast<uint32_t*>(cls + c) = t | (mixb * 3u) | (t << 2) | (diag << 4) | (wf << 7);
         // masks of the 32-cell segment of 8 lanes
-        const uint32_t mixed = owned ? (~eq & 0x01010101u) : 0u;
-        const uint32_t t0 = owned ? (__vcmpeq4(t, 0u) & 0x01010101u) : 0u;
-        const uint32_t t1 = owned ? (__vcmpeq4(t, 0x01010101u) & 0x01010101u) : 0u;
-        const uint32_t t2 = owned ? (__vcmpeq4(t, 0x02020202u) & 0x01010101u) : 0u;
+        const uint32_t mixed = owned ? mixb : 0u;
+        const uint32_t t0 = owned ? (cvM & 0x01010101u) : 0u;
+        const uint32_t t1 = owned ? ((cvM >> 1) & 0x01010101u) : 0u;
+        const uint32_t t2 = owned ? ((cvM >> 2) & 0x01010101u) : 0u;
         const int sh = 4 * (lane & 7);
-        uint32_t mm = nib4(mixed) << sh, fm = nib4(t0) << sh, dm = nib4(mixed & (wf >> 7)) << sh,
-                 um = nib4(mixed & t0) << sh;
+        uint32_t mm = nib4(mixed) << sh, fm = nib4(t0) << sh, dm = nib4(mixed & wf) << sh, um = nib4(mixed & t0) << sh;
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
             mm |= __shfl_xor_sync(rmask, mm, o);
