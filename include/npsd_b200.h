@@ -141,6 +141,14 @@ int npsd_b200_precond_apply(npsd_b200_ctx* ctx, const double* r_reduced, double*
 int npsd_b200_psdo_solve(npsd_b200_ctx* ctx, const double* b_reduced, const double* x0_reduced,
                          const npsd_b200_solve_cfg* cfg, double* x_reduced, npsd_b200_report* rep);
 
+/* The same with the caller's vector length n_b (b, x0 and x hold n_b
+ * entries; NPSD_INVALID_ARGUMENT unless n_b equals the fluid count). With
+ * the length known up front, the rhs upload overlaps a set_mask still
+ * running on the device (npsd_b200_psdo_solve waits for the frame's setup
+ * to learn the length first). */
+int npsd_b200_psdo_solve_n(npsd_b200_ctx* ctx, const double* b_reduced, int64_t n_b, const double* x0_reduced,
+                           const npsd_b200_solve_cfg* cfg, double* x_reduced, npsd_b200_report* rep);
+
 /* Same solve on device-resident FULL-GRID vectors (n_c = nx*ny*nz doubles,
  * zero at non-fluid cells): b in, x0 in (may be NULL), x out. */
 int npsd_b200_psdo_solve_device(npsd_b200_ctx* ctx, const double* d_b_full, const double* d_x0_full,

@@ -438,10 +438,10 @@ class Context:
             if x0a.size != b.size:
                 raise ValueError("solve: x0 length mismatch")
             x0p = x0a.ctypes.data_as(C.c_void_p)
-        if b.size != self.n_fluid:
-            raise ValueError("solve: rhs length mismatch")
         c = cfg._c(_PSDO_PRECOND[precond])
-        st = self.lib.npsd_b200_psdo_solve(self.h, b, x0p, C.byref(c), x, C.byref(rep))
+        # sized entry point: the rhs upload overlaps a set_mask still in flight;
+        # the length is checked against the fluid count on the C side
+        st = self.lib.npsd_b200_psdo_solve_n(self.h, b, b.size, x0p, C.byref(c), x, C.byref(rep))
         if st == NPSD_BREAKDOWN:
             _raise(st, self.lib.npsd_b200_last_error(self.h).decode())
         self._ck(st)

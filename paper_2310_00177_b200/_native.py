@@ -16,7 +16,7 @@ NPSD_OK, NPSD_INVALID_ARGUMENT, NPSD_BREAKDOWN, NPSD_EMPTY_SYSTEM, NPSD_CUDA_ERR
 EXPORTED_SYMBOLS = (
     "npsd_b200_create", "npsd_b200_destroy", "npsd_b200_last_error", "npsd_b200_set_params",
     "npsd_b200_set_mask", "npsd_b200_set_mask_device", "npsd_b200_n_fluid", "npsd_b200_fluid_indices",
-    "npsd_b200_precond_apply", "npsd_b200_psdo_solve", "npsd_b200_psdo_solve_device", "npsd_b200_spmv",
+    "npsd_b200_precond_apply", "npsd_b200_psdo_solve", "npsd_b200_psdo_solve_n", "npsd_b200_psdo_solve_device", "npsd_b200_spmv",
     "npsd_b200_net_apply", "npsd_b200_level_image", "npsd_b200_linear_coeffs", "npsd_b200_mixed_counts",
     "npsd_b200_param_count", "npsd_b200_init_params", "npsd_b200_identity_params", "npsd_b200_rhs_normal",
     "npsd_b200_device_alloc", "npsd_b200_device_free", "npsd_b200_host_alloc", "npsd_b200_host_free",
@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
     L.npsd_b200_check_operator.argtypes = [_vp, C.c_int64, _i64p, _i64p, _f64p, C.c_int64, C.c_int]
     L.npsd_b200_precond_apply.argtypes = [_vp, _f64p, _f64p, C.c_int64]
     L.npsd_b200_psdo_solve.argtypes = [_vp, _f64p, _vp, C.POINTER(SolveCfg), _f64p, C.POINTER(Report)]
+    L.npsd_b200_psdo_solve_n.argtypes = [_vp, _f64p, C.c_int64, _vp, C.POINTER(SolveCfg), _f64p, C.POINTER(Report)]
     L.npsd_b200_psdo_solve_device.argtypes = [_vp, _vp, _vp, C.POINTER(SolveCfg), _vp, C.POINTER(Report)]
     L.npsd_b200_spmv.argtypes = [_vp, _f64p, _f64p, C.c_int64]
     L.npsd_b200_net_apply.argtypes = [_vp, _f32p, _f32p]

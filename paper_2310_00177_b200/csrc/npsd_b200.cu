@@ -273,6 +273,10 @@ struct npsd_b200_ctx {
     SetupInfo* d_info = nullptr;
     SetupInfo* info_host = nullptr;
     cudaEvent_t ev_setup = nullptr;
+    // psdo_solve_n: the rhs upload overlaps a set_mask in flight (its own
+    // stream, ordered after the work queued before that set_mask)
+    cudaStream_t s_up = nullptr;
+    cudaEvent_t ev_pre_mask = nullptr, ev_up = nullptr;
     bool setup_pending = false;
     uint8_t* types_dev = nullptr;        // the frame's cell types (the setup graph reads them here)
     const uint8_t* types_cur = nullptr;  // the buffer the last set_mask read (for a redo)
@@ -285,6 +289,8 @@ struct npsd_b200_ctx {
     bool fast = true;  // network arithmetic: fused/reassociated (true) or the reference's order, bitwise (false)
     int coarse_zc_max = 4;    // planes per block of the z-marching coarse kernels (at most)
     bool merge_up0 = true;    // level-0 up: tiled and mixed cells in one launch (NPSD_MERGE_UP0=0: two)
+    bool tail = true;         // the smallest levels in one cluster launch (k_tail; NPSD_TAIL=0: a launch per step)
+    int tail_ct = 8;          // its cluster size (NPSD_TAIL_CT: 1..16)
     bool classify_simd = true;  // level-0 classification with byte SIMD (NPSD_CLASSIFY_SIMD=0: one cell per thread)
     int up0_mixb = 0;         // its mixed-list blocks per SM (NPSD_UP0_MIXB; 0: by grid size, up0_mixed_blocks)
     long long slab_chunk_launches = 0;
@@ -935,6 +941,7 @@ void ensure_setup_capacity(npsd_b200_ctx* c) {
 // the frame's SetupInfo. Nothing here waits for the device.
 template <int D>
 void set_mask_run(npsd_b200_ctx* c, const uint8_t* dtypes) {
+    CK(cudaEventRecord(c->ev_pre_mask, c->s));
     ensure_setup_capacity(c);
     c->x1_clean = false;
     const bool graph = !c->slab.on && c->mask_graph_ok && dtypes == c->types_dev;
@@ -1304,6 +1311,57 @@ Step reduce_step(npsd_b200_ctx* c, const std::string& name, int kind) {
     return {name, [c, kind](cudaStream_t s) { slab_reduce(c, s, kind); }};
 }
 
+// First level of the tail (k_tail, coarse.cuh): the smallest l >= 1 from which
+// every level holds at most kTailMaxCells cells, when that leaves at least one
+// down step before the coarsest conv; else depth (no tail). 3D, one domain.
+int tail_level(const npsd_b200_ctx* c, int D) {
+    if (!c->tail || D != 3 || c->slab.on) return c->depth;
+    int lt = c->depth;
+    while (lt - 1 >= 1 && c->L[lt - 1].g.n <= kTailMaxCells) --lt;
+    return (lt <= c->depth - 2) ? lt : c->depth;
+}
+
+void launch_tail(npsd_b200_ctx* c, cudaStream_t s, int lt) {
+    TailArgs a{};
+    a.lt = lt;
+    a.depth = c->depth;
+    for (int l = lt; l < c->depth; ++l) {
+        TailLevel& T = a.lv[l];
+        LevelBufs& L = c->L[l];
+        const bool coarsest = l == c->depth - 1;
+        T.g = L.g;
+        T.gc = coarsest ? L.g : c->L[l + 1].g;
+        T.x = L.x;
+        T.y = L.y;
+        T.xnext = coarsest ? nullptr : c->L[l + 1].x;
+        T.outc = coarsest ? nullptr : ((l + 1 == c->depth - 1) ? c->L[l + 1].y : c->L[l + 1].out);
+        T.out = L.out;
+        T.zab = c->zab + 2 * l;
+        T.ctd = tab_down(c, l);
+        if (!coarsest) T.ctu = tab_up(c, l);
+        T.kd = coarsest ? c->kc_coarse : c->kc_down[l];
+        if (!coarsest) T.ku = c->kc_up[l];
+        T.zc = (L.g.nz >= 32) ? 4 : 2;
+    }
+    auto k = c->fast ? k_tail<true> : k_tail<false>;
+    const int ct = c->tail_ct;
+    if (ct > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ct);
+    cfg.blockDim = dim3(kZT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ct;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k, a));
+    ++c->launches;
+}
+
 template <int D>
 std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     std::vector<Step> v;
@@ -1311,7 +1369,8 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     const bool xg = c->slab.on && !raw;  // z-slab: halos before every conv level
     // solve path: level-0 mixed-window cells are computed apart (mixed.cuh)
     if (!raw) v.push_back({"net_mixed_down_L0", [c](cudaStream_t s) { launch_mixed_down0<D>(c, s); }});
-    for (int l = 0; l < Ld; ++l) {
+    const int lt = tail_level(c, D);  // levels lt .. Ld-1: one k_tail launch
+    for (int l = 0; l < lt; ++l) {
         const bool pool = (l + 1 < Ld);
         const std::string nm = (l == Ld - 1) ? "net_coarse_L" + std::to_string(l) : "net_down_L" + std::to_string(l);
         v.push_back({nm, [c, l, pool, raw](cudaStream_t s) {
@@ -1337,7 +1396,8 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
             v.push_back(xchg_step(c, "xchg_y_L" + std::to_string(l), [c, l] { return (void*)c->L[l].y; }, sizeof(float),
                                   l));
     }
-    for (int l = Ld - 2; l >= 0; --l) {
+    if (lt < Ld) v.push_back({"net_tail_L" + std::to_string(lt), [c, lt](cudaStream_t s) { launch_tail(c, s, lt); }});
+    for (int l = std::min(Ld, lt) - 2 + (lt < Ld ? 1 : 0); l >= 0; --l) {
         v.push_back({"net_up_L" + std::to_string(l), [c, l, raw, no](cudaStream_t s) {
                          if (l == 0 && !raw)
                              launch_up0_no<D>(c, s, no);
@@ -2219,6 +2279,9 @@ void free_ctx(npsd_b200_ctx* c) {
     if (c->info_host) cudaFreeHost(c->info_host);
     if (c->maps) cudaFreeHost(c->maps);
     if (c->ev_setup) cudaEventDestroy(c->ev_setup);
+    if (c->ev_pre_mask) cudaEventDestroy(c->ev_pre_mask);
+    if (c->ev_up) cudaEventDestroy(c->ev_up);
+    if (c->s_up) cudaStreamDestroy(c->s_up);
     if (c->mask_exec) cudaGraphExecDestroy(c->mask_exec);
     F(c->X0);
     F(c->X1);
@@ -2298,6 +2361,8 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
         if (const char* e = std::getenv("NPSD_MERGE_UP0")) c->merge_up0 = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_CLASSIFY_SIMD")) c->classify_simd = (e[0] != '0');
+        if (const char* e = std::getenv("NPSD_TAIL")) c->tail = (e[0] != '0');
+        if (const char* e = std::getenv("NPSD_TAIL_CT")) c->tail_ct = std::max(1, std::min(16, std::atoi(e)));
         if (const char* e = std::getenv("NPSD_UP0_MIXB")) c->up0_mixb = std::max(0, std::min(16, std::atoi(e)));
         if (slab) {
             c->slab = *slab;
@@ -2441,6 +2506,10 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->d_info = dalloc<SetupInfo>(1);
         CK(cudaMallocHost(&c->info_host, sizeof(SetupInfo)));
         CK(cudaEventCreateWithFlags(&c->ev_setup, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&c->s_up, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_pre_mask, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_up, cudaEventDisableTiming));
+        CK(cudaEventRecord(c->ev_pre_mask, c->s));
         c->types_dev = dalloc<uint8_t>((size_t)c->g0.n);
         // first capacities of the per-frame tables; setup_sync grows them from a frame's counts
         for (int l = 0; l < depth; ++l) {
@@ -3014,17 +3083,34 @@ int npsd_b200_psdo_solve_device(npsd_b200_ctx* c, const double* d_b, const doubl
     });
 }
 
-int npsd_b200_psdo_solve(npsd_b200_ctx* c, const double* b, const double* x0, const npsd_b200_solve_cfg* cfg,
-                         double* x, npsd_b200_report* rep) {
+// psdo_solve on reduced host vectors. Unsized: the length is the fluid count
+// (known once the frame's setup is finished). Sized: the caller's length,
+// checked against it, and the rhs upload starts before the setup has
+// finished (its own stream).
+static int psdo_solve_host(npsd_b200_ctx* c, const double* b, bool sized, long long nb, const double* x0,
+                           const npsd_b200_solve_cfg* cfg, double* x, npsd_b200_report* rep) {
     return guarded(c, [&] {
-        check_mask(c);
         require(cfg != nullptr && b != nullptr && x != nullptr, "solve: null argument");
+        bool uploaded = false;
+        if (sized) {
+            require(nb >= 0 && nb <= c->g0.n, "solve: rhs length mismatch");
+            if (!c->slab.on && nb > 0) {
+                CK(cudaStreamWaitEvent(c->s_up, c->ev_pre_mask, 0));
+                CK(cudaMemcpyAsync(c->red_a, b, (size_t)nb * sizeof(double), cudaMemcpyHostToDevice, c->s_up));
+                CK(cudaEventRecord(c->ev_up, c->s_up));
+                // the solve's stream is ordered after the upload (the setup already queued runs first)
+                CK(cudaStreamWaitEvent(c->s, c->ev_up, 0));
+                uploaded = true;
+            }
+        }
+        check_mask(c);
         if (c->n_fluid == 0) throw EmptySystem("reduce: image has no fluid cells");
+        require(!sized || nb == c->n_fluid, "solve: rhs length mismatch");
         const Geom g = c->g0;
         const uint8_t* cls = c->L[0].cls;
         const size_t nf = (size_t)c->n_fluid;
         // check_inputs (solver.cpp:28-33) on the device, on the uploaded vector
-        CK(cudaMemcpyAsync(c->red_a, b, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        if (!uploaded) CK(cudaMemcpyAsync(c->red_a, b, nf * sizeof(double), cudaMemcpyHostToDevice, c->s));
         require(device_check(c, k_check_finite, (long long)nf, (const double*)c->red_a, (long long)nf),
                 "solve: rhs has non-finite entries");
         LAUNCH(c, c->s, k_scatter, g.n, g, cls, c->fmask, c->fbase, c->red_a, c->Bf);
@@ -3048,6 +3134,16 @@ int npsd_b200_psdo_solve(npsd_b200_ctx* c, const double* b, const double* x0, co
         CK(cudaMemcpyAsync(x, c->red_b, nf * sizeof(double), cudaMemcpyDeviceToHost, c->s));
         CK(cudaStreamSynchronize(c->s));
     });
+}
+
+int npsd_b200_psdo_solve(npsd_b200_ctx* c, const double* b, const double* x0, const npsd_b200_solve_cfg* cfg,
+                         double* x, npsd_b200_report* rep) {
+    return psdo_solve_host(c, b, false, 0, x0, cfg, x, rep);
+}
+
+int npsd_b200_psdo_solve_n(npsd_b200_ctx* c, const double* b, int64_t nb, const double* x0,
+                           const npsd_b200_solve_cfg* cfg, double* x, npsd_b200_report* rep) {
+    return psdo_solve_host(c, b, true, (long long)nb, x0, cfg, x, rep);
 }
 
 int npsd_b200_pcg_solve(npsd_b200_ctx* c, const double* b, const double* x0, const npsd_b200_solve_cfg* cfg,

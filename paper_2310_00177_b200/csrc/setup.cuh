@@ -330,8 +330,8 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
     constexpr int NFX = W / kFlagTX, NFY = H / kFlagTY;  // flag tiles of the block tile
     static_assert(W % kFlagTX == 0 && H % kFlagTY == 0, "whole flag tiles");
     __shared__ uint32_t st[2][SH][SW];
-    // block counts: 32-bit (a block holds < 2^32 cells; 64-bit shared atomics are CAS loops)
-    __shared__ uint32_t sG[kMaxDepth * 81];
+    // level 0's block counts: 32-bit (a block holds < 2^32 cells; 64-bit shared atomics are CAS loops)
+    __shared__ uint32_t sG[81];
     __shared__ uint32_t sflag[NFX * NFY];
     __shared__ uint32_t sint[kMaxDepth][3];  // interior-class counts
     const int lane = threadIdx.x % LX, row = threadIdx.x / LX, tid = threadIdx.x;
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
     const unsigned rmask = (LX == 32) ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
     const int X0 = blockIdx.x * W, Y0 = blockIdx.y * H, Z0 = blockIdx.z * ZC;
     const long long plane = (long long)g.nx * g.ny;
-    for (int i = tid; i < za.nzs * 81; i += 256) sG[i] = 0u;
+    for (int i = tid; i < 81; i += 256) sG[i] = 0u;
     if (tid < kMaxDepth * 3) sint[tid / 3][tid % 3] = 0u;
     // staging: my (up to) two words of the SH x SW plane window
     int off[2], sidx[2];
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
         __syncthreads();  // sflag complete; every read of this staging buffer done before its reuse
     };
     const int x = X0 + 4 * lane, y = Y0 + row;
-    const int zoff = za.zg_off, Lc = za.nzs - 1;
+    const int zoff = za.zg_off;
     uint32_t cnt_int[3] = {0u, 0u, 0u};  // this warp row's interior-class counts (lane 0)
     plane_step(Z0 - 1);
 #pragma unroll 1
@@ -440,44 +440,38 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
             sm.umask[seg] = um;
             sm.ucount[seg] = __popc(um);
         }
-        // linear-block window counts of every level l < nzs (k_zsums classes by
-        // global position; set_mask passes nzs = 1, the coarser levels count
-        // their pooled images): a cell interior at the coarsest counted level
-        // is interior at every level (the boundary bands grow with l), counted
-        // in registers; the rest, per thread, in shared memory
-        if (za.nzs == 0) continue;
+        // level 0's linear-block window counts (k_zsums: classes by global
+        // position; za.nzs is 0 or 1 here, coarser levels count their pooled
+        // images): interior-class cells in registers, the two x-end cells of a
+        // row and the rows on the y / z faces in shared counters
+        if (za.nzs == 0 || !owned) continue;
         const int zg = z + zoff;
-        const bool row_inner = (y >> Lc) > 0 && (y >> Lc) < (za.nyg >> Lc) - 1 && (zg >> Lc) > 0 &&
-                               (zg >> Lc) < (za.nzg >> Lc) - 1;
-        const bool x_inner = (x >> Lc) > 0 && ((x + 3) >> Lc) < (za.nxg >> Lc) - 1;
-        if (row_inner && x_inner) {
-            cnt_int[0] += __popc(nib4(t0));
-            cnt_int[1] += __popc(nib4(t1));
-            cnt_int[2] += __popc(nib4(t2));
-        } else if (owned) {
-#pragma unroll 1
-            for (int l = 0; l < za.nzs; ++l) {
-                const int yl = y >> l, zl = zg >> l;
-                const int ky = (yl == 0) ? 0 : ((yl == (za.nyg >> l) - 1) ? 2 : 1);
-                const int kz = (zl == 0) ? 0 : ((zl == (za.nzg >> l) - 1) ? 2 : 1);
-                // my four cells' x classes at level l (x .. x+3 global = local: slabs split z)
-                uint32_t cc[3][3] = {};  // [type][kx]
+        const int ky = (y == 0) ? 0 : ((y == za.nyg - 1) ? 2 : 1);
+        const int kz = (zg == 0) ? 0 : ((zg == za.nzg - 1) ? 2 : 1);
+        const bool xe0 = x == 0, xe3 = x + 3 == za.nxg - 1;
+        if (ky == 1 && kz == 1) {
+            const uint32_t im = 0x01010101u & ~(xe0 ? 0x01u : 0u) & ~(xe3 ? 0x01000000u : 0u);
+            cnt_int[0] += __popc(nib4(t0 & im));
+            cnt_int[1] += __popc(nib4(t1 & im));
+            cnt_int[2] += __popc(nib4(t2 & im));
+            if (xe0) atomicAdd(&sG[(t & 0xffu) * 27 + 12 + 0], 1u);
+            if (xe3) atomicAdd(&sG[(t >> 24) * 27 + 12 + 2], 1u);
+        } else {
+            uint32_t cc[3][3] = {};  // [type][kx]
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int xl = (x + k) >> l;
-                    const int kx = (xl == 0) ? 0 : ((xl == (za.nxg >> l) - 1) ? 2 : 1);
-                    const uint32_t tb = (t >> (8 * k)) & 0xffu;
+            for (int k = 0; k < 4; ++k) {
+                const int kx = (k == 0 && xe0) ? 0 : ((k == 3 && xe3) ? 2 : 1);
+                const uint32_t tb = (t >> (8 * k)) & 0xffu;
 #pragma unroll
-                    for (int a = 0; a < 3; ++a)
+                for (int a = 0; a < 3; ++a)
 #pragma unroll
-                        for (int b = 0; b < 3; ++b) cc[a][b] += (tb == (uint32_t)a && kx == b) ? 1u : 0u;
-                }
-#pragma unroll
-                for (int ty = 0; ty < 3; ++ty)
-#pragma unroll
-                    for (int kx = 0; kx < 3; ++kx)
-                        if (cc[ty][kx]) atomicAdd(&sG[l * 81 + ty * 27 + (kz * 3 + ky) * 3 + kx], cc[ty][kx]);
+                    for (int b = 0; b < 3; ++b) cc[a][b] += (tb == (uint32_t)a && kx == b) ? 1u : 0u;
             }
+#pragma unroll
+            for (int ty = 0; ty < 3; ++ty)
+#pragma unroll
+                for (int kx = 0; kx < 3; ++kx)
+                    if (cc[ty][kx]) atomicAdd(&sG[ty * 27 + (kz * 3 + ky) * 3 + kx], cc[ty][kx]);
         }
     }
     // interior rows: the interior class (13) of every level
@@ -487,11 +481,10 @@ __global__ void __launch_bounds__(256) k_classify_simd(Geom g, const uint8_t* __
         if (lane == 0 && v) atomicAdd(&sint[0][ty], v);
     }
     __syncthreads();
-    if (tid < 3)
-        for (int l = 0; l < za.nzs; ++l) sG[l * 81 + tid * 27 + 13] += sint[0][tid];
+    if (tid < 3 && za.nzs) sG[tid * 27 + 13] += sint[0][tid];
     __syncthreads();
     for (int i = tid; i < za.nzs * 81; i += 256)
-        if (sG[i]) atomicAdd(&za.G[i / 81][i % 81], (unsigned long long)sG[i]);
+        if (sG[i]) atomicAdd(&za.G[0][i], (unsigned long long)sG[i]);
 }
 
 // Tile occupancy at L0: flags[(z * nty + ty) * ntx + tx] = any fluid cell in
