@@ -91,9 +91,6 @@ def phase_bytes(model: dict, phase: str) -> float:
     """bytes of a phase in a per-kernel model; "P2" = all coarse kernels"""
     if phase == "P2":
         return sum(v for k, v in model.items() if k.startswith("P2_"))
-    if phase.startswith("P2_tail_L"):  # k_tail: every coarse kernel from its first level on
-        lt = int(phase[len("P2_tail_L"):])
-        return sum(v for k, v in model.items() if k.startswith("P2_") and int(k.rsplit("L", 1)[1]) >= lt)
     return model[phase]
 
 

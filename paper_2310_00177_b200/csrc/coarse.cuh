@@ -19,8 +19,6 @@
 //   z >> 1), zero outside.
 #pragma once
 
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 #include "net.cuh"
 #include "net2.cuh"
@@ -307,89 +305,6 @@ __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cupz(Geom g, Geom gc, con
     if (done && *done) return;  // z-slab chunked loop: the solve has finished
     __shared__ __align__(16) CUpSmem<ZC> S;
     cupz_tile<ZC, F>(g, gc, outc, yl, zab, ct, kc, outl, blockIdx.x, blockIdx.y, blockIdx.z, S);
-}
-
-// ---------------------------------------------------------------------------
-// The smallest levels in one launch (k_tail): down steps l = lt .. depth-2,
-// the coarsest conv, up steps depth-2 .. lt, run by ONE thread-block cluster
-// whose CTAs split each step's tiles; a cluster barrier (release / acquire:
-// the step's global writes are visible to every CTA of the cluster) replaces
-// the kernel boundary between steps. These levels hold at most
-// kTailMaxCells cells each, so a step is a few tiles per CTA and the chain of
-// ~2(depth - lt) small launches (each a launch + drain) becomes one launch.
-// Same tile bodies (and arithmetic) as k_cdownz / k_cupz.
-constexpr long long kTailMaxCells = 32768;
-struct TailLevel {
-    Geom g, gc;           // this level, the next coarser one
-    const float* x;       // down input x_l
-    float* y;             // y_l
-    float* xnext;         // x_{l+1} (pool target; nullptr at the coarsest level)
-    const float* outc;    // up input: out_{l+1} (y_{l+1} at the coarsest)
-    float* out;           // out_l
-    const float* zab;     // z_a, z_b of level l
-    ConvTab ctd, ctu;
-    KC kd, ku;            // uniform kernels: down (coarse at the coarsest), up
-    int zc;               // planes per tile (2 or 4)
-};
-struct TailArgs {
-    TailLevel lv[kMaxDepth];
-    int lt, depth;
-};
-
-__device__ __forceinline__ int tail_tiles(const Geom& g, int zc, int& ntx, int& nty) {
-    ntx = (g.nx + kZX - 1) / kZX;
-    nty = (g.ny + kZY - 1) / kZY;
-    return ntx * nty * ((g.zo1 - g.zo0 + zc - 1) / zc);
-}
-
-template <bool F>
-__global__ void __launch_bounds__(kZT, 1) k_tail(const __grid_constant__ TailArgs a) {
-    pdl_launch_wait();
-    __shared__ __align__(16) union {
-        CDownSmem<4> d4;
-        CDownSmem<2> d2;
-        CUpSmem<4> u4;
-        CUpSmem<2> u2;
-    } S;
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = (int)cl.block_rank(), nct = (int)cl.num_blocks();
-    for (int l = a.lt; l < a.depth; ++l) {
-        const TailLevel& L = a.lv[l];
-        const bool pool = l + 1 < a.depth;
-        int ntx, nty;
-        const int nt = tail_tiles(L.g, L.zc, ntx, nty);
-        for (int t = rank; t < nt; t += nct) {
-            const int bx = t % ntx, by = (t / ntx) % nty, bz = t / (ntx * nty);
-            if (pool) {
-                if (L.zc == 4)
-                    cdownz_tile<true, 4, F>(L.g, L.x, L.ctd, L.kd, L.y, L.xnext, L.gc, bx, by, bz, S.d4);
-                else
-                    cdownz_tile<true, 2, F>(L.g, L.x, L.ctd, L.kd, L.y, L.xnext, L.gc, bx, by, bz, S.d2);
-            } else {
-                if (L.zc == 4)
-                    cdownz_tile<false, 4, F>(L.g, L.x, L.ctd, L.kd, L.y, nullptr, L.g, bx, by, bz, S.d4);
-                else
-                    cdownz_tile<false, 2, F>(L.g, L.x, L.ctd, L.kd, L.y, nullptr, L.g, bx, by, bz, S.d2);
-            }
-            __syncthreads();  // S is restaged by the next tile
-        }
-        cl.sync();
-    }
-    for (int l = a.depth - 2; l >= a.lt; --l) {
-        const TailLevel& L = a.lv[l];
-        int ntx, nty;
-        const int nt = tail_tiles(L.g, L.zc, ntx, nty);
-        for (int t = rank; t < nt; t += nct) {
-            const int bx = t % ntx, by = (t / ntx) % nty, bz = t / (ntx * nty);
-            if (L.zc == 4)
-                cupz_tile<4, F>(L.g, L.gc, L.outc, L.y, L.zab, L.ctu, L.ku, L.out, bx, by, bz, S.u4);
-            else
-                cupz_tile<2, F>(L.g, L.gc, L.outc, L.y, L.zab, L.ctu, L.ku, L.out, bx, by, bz, S.u2);
-            __syncthreads();
-        }
-        if (l > a.lt) cl.sync();
-    }
 }
 
 }  // namespace nb2

@@ -289,8 +289,6 @@ struct npsd_b200_ctx {
     bool fast = true;  // network arithmetic: fused/reassociated (true) or the reference's order, bitwise (false)
     int coarse_zc_max = 4;    // planes per block of the z-marching coarse kernels (at most)
     bool merge_up0 = true;    // level-0 up: tiled and mixed cells in one launch (NPSD_MERGE_UP0=0: two)
-    bool tail = true;         // the smallest levels in one cluster launch (k_tail; NPSD_TAIL=0: a launch per step)
-    int tail_ct = 8;          // its cluster size (NPSD_TAIL_CT: 1..16)
     bool classify_simd = true;  // level-0 classification with byte SIMD (NPSD_CLASSIFY_SIMD=0: one cell per thread)
     int up0_mixb = 0;         // its mixed-list blocks per SM (NPSD_UP0_MIXB; 0: by grid size, up0_mixed_blocks)
     long long slab_chunk_launches = 0;
@@ -1311,57 +1309,6 @@ Step reduce_step(npsd_b200_ctx* c, const std::string& name, int kind) {
     return {name, [c, kind](cudaStream_t s) { slab_reduce(c, s, kind); }};
 }
 
-// First level of the tail (k_tail, coarse.cuh): the smallest l >= 1 from which
-// every level holds at most kTailMaxCells cells, when that leaves at least one
-// down step before the coarsest conv; else depth (no tail). 3D, one domain.
-int tail_level(const npsd_b200_ctx* c, int D) {
-    if (!c->tail || D != 3 || c->slab.on) return c->depth;
-    int lt = c->depth;
-    while (lt - 1 >= 1 && c->L[lt - 1].g.n <= kTailMaxCells) --lt;
-    return (lt <= c->depth - 2) ? lt : c->depth;
-}
-
-void launch_tail(npsd_b200_ctx* c, cudaStream_t s, int lt) {
-    TailArgs a{};
-    a.lt = lt;
-    a.depth = c->depth;
-    for (int l = lt; l < c->depth; ++l) {
-        TailLevel& T = a.lv[l];
-        LevelBufs& L = c->L[l];
-        const bool coarsest = l == c->depth - 1;
-        T.g = L.g;
-        T.gc = coarsest ? L.g : c->L[l + 1].g;
-        T.x = L.x;
-        T.y = L.y;
-        T.xnext = coarsest ? nullptr : c->L[l + 1].x;
-        T.outc = coarsest ? nullptr : ((l + 1 == c->depth - 1) ? c->L[l + 1].y : c->L[l + 1].out);
-        T.out = L.out;
-        T.zab = c->zab + 2 * l;
-        T.ctd = tab_down(c, l);
-        if (!coarsest) T.ctu = tab_up(c, l);
-        T.kd = coarsest ? c->kc_coarse : c->kc_down[l];
-        if (!coarsest) T.ku = c->kc_up[l];
-        T.zc = (L.g.nz >= 32) ? 4 : 2;
-    }
-    auto k = c->fast ? k_tail<true> : k_tail<false>;
-    const int ct = c->tail_ct;
-    if (ct > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ct);
-    cfg.blockDim = dim3(kZT);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = ct;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, k, a));
-    ++c->launches;
-}
-
 template <int D>
 std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     std::vector<Step> v;
@@ -1369,8 +1316,7 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
     const bool xg = c->slab.on && !raw;  // z-slab: halos before every conv level
     // solve path: level-0 mixed-window cells are computed apart (mixed.cuh)
     if (!raw) v.push_back({"net_mixed_down_L0", [c](cudaStream_t s) { launch_mixed_down0<D>(c, s); }});
-    const int lt = tail_level(c, D);  // levels lt .. Ld-1: one k_tail launch
-    for (int l = 0; l < lt; ++l) {
+    for (int l = 0; l < Ld; ++l) {
         const bool pool = (l + 1 < Ld);
         const std::string nm = (l == Ld - 1) ? "net_coarse_L" + std::to_string(l) : "net_down_L" + std::to_string(l);
         v.push_back({nm, [c, l, pool, raw](cudaStream_t s) {
@@ -1396,8 +1342,7 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
             v.push_back(xchg_step(c, "xchg_y_L" + std::to_string(l), [c, l] { return (void*)c->L[l].y; }, sizeof(float),
                                   l));
     }
-    if (lt < Ld) v.push_back({"net_tail_L" + std::to_string(lt), [c, lt](cudaStream_t s) { launch_tail(c, s, lt); }});
-    for (int l = std::min(Ld, lt) - 2 + (lt < Ld ? 1 : 0); l >= 0; --l) {
+    for (int l = Ld - 2; l >= 0; --l) {
         v.push_back({"net_up_L" + std::to_string(l), [c, l, raw, no](cudaStream_t s) {
                          if (l == 0 && !raw)
                              launch_up0_no<D>(c, s, no);
@@ -2361,8 +2306,6 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
         if (const char* e = std::getenv("NPSD_MERGE_UP0")) c->merge_up0 = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_CLASSIFY_SIMD")) c->classify_simd = (e[0] != '0');
-        if (const char* e = std::getenv("NPSD_TAIL")) c->tail = (e[0] != '0');
-        if (const char* e = std::getenv("NPSD_TAIL_CT")) c->tail_ct = std::max(1, std::min(16, std::atoi(e)));
         if (const char* e = std::getenv("NPSD_UP0_MIXB")) c->up0_mixb = std::max(0, std::min(16, std::atoi(e)));
         if (slab) {
             c->slab = *slab;

@@ -596,29 +596,3 @@ def test_setup_branches_equal_serial(b200, monkeypatch):
         assert np.array_equal(a[0], b[0])
         assert np.array_equal(a[1], b[1])
         assert a[2] == b[2] and np.array_equal(a[3], b[3])
-
-
-@pytest.mark.parametrize("exact", [True, False])
-@pytest.mark.parametrize("ct", ["8", "16"])
-def test_tail_equals_per_step_launches(b200, monkeypatch, exact, ct):
-    """The smallest levels in one cluster launch (k_tail: down, coarsest and
-    up steps separated by cluster barriers) write what one launch per step
-    writes, bit for bit (same tile bodies): the preconditioner, the raw
-    network and a 20-iteration solve history, at 64^3 (tail from level 1)
-    and 128^3 (from level 2)."""
-    p = b200.default_model()
-    for n, seed in ((64, 5), (128, 6)):
-        t = scenes.random_types((n, n, n), seed, p=(0.55, 0.3, 0.15), blobs=6)
-        r = np.random.default_rng(seed).standard_normal(int((t == 0).sum()))
-        xin = np.random.default_rng(seed + 1).standard_normal(t.size).astype(np.float32)
-        out = []
-        for tail in ("1", "0"):
-            monkeypatch.setenv("NPSD_TAIL", tail)
-            monkeypatch.setenv("NPSD_TAIL_CT", ct)
-            ctx = b200.Context(3, t.shape, p, exact=exact)
-            ctx.set_mask(t)
-            rep = ctx.psdo_solve(r, b200.SolveConfig(max_iters=20, tol_reduction=1e-300)).report
-            out.append((ctx.precond_apply(r), ctx.net_apply(xin), rep.residual_history))
-            ctx.close()
-        a, b = out
-        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]), n
