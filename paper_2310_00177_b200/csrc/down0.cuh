@@ -16,6 +16,8 @@
 // is apply_kernels' (net/kernels.hpp:147-172): bit-identical.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "net.cuh"
 #include "stencil.cuh"
@@ -42,12 +44,19 @@ struct Down0Smem {
     float yp[2][2][kTY][kTX];    // y_0 of a step's two planes, double-buffered (pooling)
 };
 
-// One column segment: tile (tx, ty), planes [zc0, zc1) (both even)
+// One column segment: tile (tx, ty), planes [zc0, zc1) (both even). The z
+// loop runs in chunks of 8 planes (4 steps of 2) with the step index a
+// compile-time constant, so every ring slot (raw stages, x_0 planes, own cell
+// bytes, pooling buffers) is a constant offset: no per-plane slot arithmetic.
+// Every thread issues one own copy and at most one halo copy per plane, both
+// 16-byte pairs (column halos as the aligned pair holding the halo cell), so
+// the issue and conversion code has no per-role branches.
 template <bool F>
 __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __restrict__ cls,
                                                 const double* __restrict__ r, const SolverState* __restrict__ st,
                                                 const KC0& kc, float* __restrict__ y, float* __restrict__ xnext,
                                                 const Geom& gc, int tx, int ty, int zc0, int zc1) {
+    static_assert(kD0R == 4 && kD0X == 8, "the 8-plane chunk maps ring slots to constants");
     const int lane = threadIdx.x, row = threadIdx.y;
     const int X0 = tx * kTX, Y0 = ty * kTY;
     const int x = X0 + 2 * lane, yy = Y0 + row;
@@ -57,64 +66,62 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
     __syncthreads();  // the previous segment's last reads of S are done
     const long long nx = g.nx, plane = nx * g.ny;
     const double inv1 = st->inv1, inv2 = st->inv2;
-    // halo assignment (as stencil_march)
-    int hx = 0, hy = 0, hsr = 0, hsc = 0, hkind = 0;
+    // halo pair (even x, 16 bytes): rows above / below (rows 0, 1), the column
+    // pairs holding x0-1 / x0+64 (row 2, lanes < 16) and the four corners
+    // (row 3, lanes < 4); staged at (hsr, hsc .. hsc+1)
+    bool hk = false;
+    int hx = 0, hy = 0, hsr = 0, hsc = 0;
     if (row == 0 || row == 1) {
-        hkind = 1;
+        hk = true;
         hx = x;
         hy = (row == 0) ? Y0 - 1 : Y0 + kTY;
         hsr = (row == 0) ? 0 : kVH - 1;
         hsc = 2 + 2 * lane;
     } else if (row == 2 && lane < 2 * kTY) {
-        hkind = 2;
-        hx = (lane < kTY) ? X0 - 1 : X0 + kTX;
+        hk = true;
+        hx = (lane < kTY) ? X0 - 2 : X0 + kTX;
         hy = Y0 + (lane & (kTY - 1));
         hsr = 1 + (lane & (kTY - 1));
-        hsc = (lane < kTY) ? 1 : kTX + 2;
+        hsc = (lane < kTY) ? 0 : kTX + 2;
     } else if (row == 3 && lane < 4) {
-        // the 27-point window also reads the four corners of the halo ring
-        hkind = 2;
-        hx = (lane & 1) ? X0 + kTX : X0 - 1;
+        hk = true;
+        hx = (lane & 1) ? X0 + kTX : X0 - 2;
         hy = (lane & 2) ? Y0 + kTY : Y0 - 1;
         hsr = (lane & 2) ? kVH - 1 : 0;
-        hsc = (lane & 1) ? kTX + 2 : 1;
+        hsc = (lane & 1) ? kTX + 2 : 0;
     }
-    const bool h_in = hkind != 0 && hx >= 0 && hx < g.nx && hy >= 0 && hy < g.ny;
+    const bool h_in = hk && hx >= 0 && hx < g.nx && hy >= 0 && hy < g.ny;
     const long long qo = (long long)(own ? yy : 0) * nx + (own ? x : 0);
     const long long qh = h_in ? (long long)hy * nx + hx : 0;
     auto zin = [&](int z) { return z >= 0 && z < g.nz; };
     auto own_bytes = [&](int z) -> unsigned {
         return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
     };
-    // ring slots of non-negative arguments (unsigned: cheaper modulo)
-    auto rslot = [&](int z) { return (int)((unsigned)(z - zc0 + 1 + kD0R * 1024) % (unsigned)kD0R); };
-    auto xslot = [&](int z) { return (int)((unsigned)(z + kD0X * 1024) % (unsigned)kD0X); };
     // own pairs without fluid zero-filled; halo always copied (exact zeros).
-    // The source address is in the grid whatever the predicate (qo / qh are
-    // 0 for a lane without a pair / halo cell): src-size 0 reads nothing.
+    // The source address is in the grid whatever the predicate: src-size 0 reads nothing.
     const double* r_own = r + qo;
     const double* r_halo = r + qh;
-    auto issue = [&](int z, unsigned ob) {
+    // plane z into raw stage RS
+    auto issue = [&](int z, int rs, unsigned ob) {
         if (zin(z)) {
-            const int s = rslot(z);
-            const bool ol = own && pair_live(ob);
             const long long qz = z * plane;
-            cp_async16(&S.raw[s][row + 1][2 + 2 * lane], r_own + qz, ol);
-            if (hkind == 1)
-                cp_async16(&S.raw[s][hsr][hsc], r_halo + qz, h_in);
-            else if (hkind == 2)
-                cp_async8(&S.raw[s][hsr][hsc], r_halo + qz, h_in);
+            cp_async16(&S.raw[rs][row + 1][2 + 2 * lane], r_own + qz, own && pair_live(ob));
+            if (hk) cp_async16(&S.raw[rs][hsr][hsc], r_halo + qz, h_in);
         }
         cp_commit();
     };
     auto cvt = [&](double v) { return __double2float_rn(__dmul_rn(__dmul_rn(v, inv1), inv2)); };
-    auto form = [&](int z) {
-        const int s = rslot(z), vs = xslot(z);
+    // raw stage RS -> x_0 plane slot XS (zeros outside the domain)
+    auto form = [&](int z, int rs, int xs) {
         const bool zi = zin(z);
-        S.xin[vs][row + 1][2 + 2 * lane] = zi ? cvt(S.raw[s][row + 1][2 + 2 * lane]) : 0.0f;
-        S.xin[vs][row + 1][3 + 2 * lane] = zi ? cvt(S.raw[s][row + 1][3 + 2 * lane]) : 0.0f;
-        if (hkind != 0) S.xin[vs][hsr][hsc] = zi ? cvt(S.raw[s][hsr][hsc]) : 0.0f;
-        if (hkind == 1) S.xin[vs][hsr][hsc + 1] = zi ? cvt(S.raw[s][hsr][hsc + 1]) : 0.0f;
+        const double2 o = *reinterpret_cast<const double2*>(&S.raw[rs][row + 1][2 + 2 * lane]);
+        *reinterpret_cast<float2*>(&S.xin[xs][row + 1][2 + 2 * lane]) =
+            zi ? make_float2(cvt(o.x), cvt(o.y)) : make_float2(0.0f, 0.0f);
+        if (hk) {
+            const double2 h = *reinterpret_cast<const double2*>(&S.raw[rs][hsr][hsc]);
+            *reinterpret_cast<float2*>(&S.xin[xs][hsr][hsc]) =
+                zi ? make_float2(cvt(h.x), cvt(h.y)) : make_float2(0.0f, 0.0f);
+        }
     };
     // mixed cells' y_0 (k_mixed_down0), loaded a step ahead
     auto mixed_y = [&](int z, unsigned b2, float& ya, float& yb) {
@@ -139,34 +146,38 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
         }
     };
 
-    // prologue: planes zc0-1 .. zc0+2 issued, zc0-1 and zc0 formed
-    unsigned ob[8];  // own bytes of planes z .. z+7 (shifted by two per step)
+    // ring slots relative to zc0: plane zc0 + k uses raw stage (k + 1) % 4 and
+    // x_0 slot (k + 1) % 8; ob[(k) % 8] holds plane zc0 + k's own bytes
+    unsigned ob[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) ob[k] = own_bytes(zc0 + k);
-    issue(zc0 - 1, own_bytes(zc0 - 1));
+    // prologue: planes zc0-1 .. zc0+2 issued, zc0-1 and zc0 formed
+    issue(zc0 - 1, 0, own_bytes(zc0 - 1));
 #pragma unroll
-    for (int k = 0; k <= kD0A; ++k) issue(zc0 + k, ob[k]);
+    for (int k = 0; k <= kD0A; ++k) issue(zc0 + k, (k + 1) % kD0R, ob[k]);
     cp_wait<kD0A>();  // planes zc0-1, zc0 landed
-    form(zc0 - 1);
-    form(zc0);
+    form(zc0 - 1, 0, 0);
+    form(zc0, 1, 1);
     float my[2][2];
     mixed_y(zc0, ob[0], my[0][0], my[0][1]);
     mixed_y(zc0 + 1, ob[1], my[1][0], my[1][1]);
-    int pb = 0;  // yp buffer of this step
-#pragma unroll 4
-    for (int z = zc0; z < zc1; z += 2) {
-        issue(z + kD0A + 1, ob[kD0A + 1]);
-        issue(z + kD0A + 2, ob[kD0A + 2]);
+    // one step: planes z = z8 + 2J, z + 1
+    auto step = [&](auto Jc, int z8) {
+        constexpr int J = decltype(Jc)::value;
+        constexpr int K = 2 * J;  // z - z8 (z8 - zc0 is a multiple of 8)
+        const int z = z8 + K;
+        issue(z + kD0A + 1, (K + kD0A + 2) % kD0R, ob[(K + kD0A + 1) % 8]);
+        issue(z + kD0A + 2, (K + kD0A + 3) % kD0R, ob[(K + kD0A + 2) % 8]);
         cp_wait<kD0A>();  // planes z+1, z+2 landed (own copies)
-        form(z + 1);
-        form(z + 2);
+        form(z + 1, (K + 2) % kD0R, (K + 2) % kD0X);
+        form(z + 2, (K + 3) % kD0R, (K + 3) % kD0X);
         float ny[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
         if (z + 2 < zc1) {
-            mixed_y(z + 2, ob[2], ny[0][0], ny[0][1]);
-            mixed_y(z + 3, ob[3], ny[1][0], ny[1][1]);
+            mixed_y(z + 2, ob[(K + 2) % 8], ny[0][0], ny[0][1]);
+            mixed_y(z + 3, ob[(K + 3) % 8], ny[1][0], ny[1][1]);
         }
         __syncthreads();  // x_0 of planes z-1 .. z+2 complete; yp of the last step too
-        if (z > zc0) pool(z - 2, pb ^ 1);
+        if (z > zc0) pool(z - 2, (J + 1) & 1);
         const int c0 = 2 + 2 * lane, r0 = row + 1;
         float yv[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
         if (own) {
@@ -180,11 +191,11 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
                 for (int h = 0; h < 2; ++h)
                     acc[p][h] = win_dot<F, 27>([&](int t) { return kc.k[t]; }, [&](int t) {
                         const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = t / 9 - 1;
-                        return S.xin[xslot(z + p + dz)][r0 + dy][c0 + h + dx];
+                        return S.xin[(K + p + dz + 1 + kD0X) % kD0X][r0 + dy][c0 + h + dx];
                     });
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
-                const unsigned bc = ob[p];
+                const unsigned bc = ob[(K + p) % 8];
                 const uint8_t ba = (uint8_t)(bc & 0xffu), bb = (uint8_t)(bc >> 8);
                 const int wa = cls_window(ba), wb = cls_window(bb);
                 yv[p][0] = (wa == 0) ? acc[p][0] : (wa == 3 ? my[p][0] : 0.0f);
@@ -196,24 +207,33 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
             }
         }
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            S.yp[pb][p][row][2 * lane] = yv[p][0];
-            S.yp[pb][p][row][2 * lane + 1] = yv[p][1];
-        }
-        pb ^= 1;
+        for (int p = 0; p < 2; ++p)
+            *reinterpret_cast<float2*>(&S.yp[J & 1][p][row][2 * lane]) = make_float2(yv[p][0], yv[p][1]);
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
             my[p][0] = ny[p][0];
             my[p][1] = ny[p][1];
         }
-#pragma unroll
-        for (int k = 0; k < 6; ++k) ob[k] = ob[k + 2];
-        ob[6] = own_bytes(z + 8);
-        ob[7] = own_bytes(z + 9);
+        ob[K % 8] = own_bytes(z + 8);
+        ob[(K + 1) % 8] = own_bytes(z + 9);
+    };
+    int last_pb = 0;
+    for (int z8 = zc0; z8 < zc1; z8 += 8) {
+        step(std::integral_constant<int, 0>{}, z8);
+        last_pb = 0;
+        if (z8 + 2 >= zc1) break;
+        step(std::integral_constant<int, 1>{}, z8);
+        last_pb = 1;
+        if (z8 + 4 >= zc1) break;
+        step(std::integral_constant<int, 2>{}, z8);
+        last_pb = 0;
+        if (z8 + 6 >= zc1) break;
+        step(std::integral_constant<int, 3>{}, z8);
+        last_pb = 1;
     }
     cp_wait<0>();
     __syncthreads();
-    pool(zc1 - 2, pb ^ 1);
+    pool(zc1 - 2, last_pb);
 }
 
 // Balanced schedule (Sched, units of two planes: pooling pairs stay inside a

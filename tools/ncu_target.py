@@ -19,10 +19,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--iters", type=int, default=3)
-ap.add_argument("--depth", type=int, default=4)
+ap.add_argument("--depth", type=int, default=None, help="default: the default model's depth")
 a = ap.parse_args()
 types, seed = scenes.config(a.config, a.n)
-ctx = b200.Context(3, types.shape, b200.identity_params(a.depth))
+W = b200.default_model()
+if a.depth and a.depth != W.depth:
+    W = b200.identity_params(a.depth)
+ctx = b200.Context(3, types.shape, W)
 ctx.set_mask(types)
 bf = scenes.full_rhs(types, seed)
 db = b200.DeviceBuffer(ctx, bf.nbytes)
