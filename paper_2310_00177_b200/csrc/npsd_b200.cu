@@ -1185,7 +1185,7 @@ void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
             // (C1/C2/C3, tools/env_ab.py NPSD_UP0_MIXB): about one per 2^20 cells, 1..4
             const int mixb = c->up0_mixb ? c->up0_mixb : (int)std::max(1LL, std::min(4LL, L.g.n >> 20));
             launch_pdl(c, s, k, dim3(nt + mixb * c->num_sms), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y, c->zab, kc0,
-                       c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_stencil.view(), nt,
+                       c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_down0.view(), nt,
                        (const uint32_t*)c->ulist0, (const uint32_t*)c->ucnt0, (const float*)L.tab_up,
                        (const uint32_t*)c->ukid0);
             return;
@@ -1193,7 +1193,7 @@ void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
         auto k = c->fast ? k_up_l0<NO, true> : k_up_l0<NO, false>;
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         launch_pdl(c, s, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y,
-                   c->zab, kc0, c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_stencil.view());
+                   c->zab, kc0, c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_down0.view());
         return;
     }
     launch_up<D, kUpL0, NO>(c, s, 0, nullptr, c->Dtmp);

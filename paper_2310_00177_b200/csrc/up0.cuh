@@ -16,6 +16,8 @@
 // round-to-nearest arithmetic: bit-identical to the restatement.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "down0.cuh"
 #include "mixed.cuh"
@@ -23,7 +25,7 @@
 
 namespace nb2 {
 
-constexpr int kUPF = 2, kUST = kUPF + 1;      // fine planes prefetched ahead, own-input stages
+constexpr int kUST = 4;  // own-input stages: the step's two planes and the next step's two in flight
 constexpr int kOW = kTX / 2 + 2, kOH = kTY / 2 + 2;  // coarse plane tile (34 x 6)
 
 template <int NO>
@@ -50,6 +52,14 @@ struct KUp0 {
     float m[8][8];
 };
 
+// floor(f / 2) mod 4 for small f >= -2 (coarse ring slot of fine offset f)
+__host__ __device__ constexpr int up_cslot(int f) { return ((f + 4) / 2 + 2) % 4; }
+
+// One column segment: tile (tx, ty), planes [zc0, zc1) (both even: the down
+// schedule's plane pairs). Two fine planes per step (one barrier), stepping
+// 8 planes per chunk with the step index a compile-time constant, so every
+// ring slot is a constant offset: own inputs of plane zc0 + k in stage k % 4,
+// coarse plane zc0/2 + m in slot m % 4 (one new coarse plane per step).
 template <int NO, bool F>
 __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, const uint8_t* __restrict__ cls,
                                               const float* __restrict__ outc, const float* __restrict__ y0,
@@ -74,60 +84,63 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
     const bool cxy_in = crole && cgx >= 0 && cgx < gc.nx && cgy >= 0 && cgy < gc.ny;
     const long long cqo = cxy_in ? (long long)cgy * gc.nx + cgx : 0;
     const long long cplane = (long long)gc.nx * gc.ny;
+    const int cz0 = zc0 >> 1;  // coarse plane of fine zc0, zc0 + 1
     auto zin = [&](int z) { return z >= 0 && z < g.nz; };
     auto own_bytes = [&](int z) -> unsigned {
         return (own && zin(z)) ? (unsigned)__ldg(reinterpret_cast<const unsigned short*>(cls + z * plane + qo)) : kOut2;
     };
-    auto coarse = [&](int k) {  // stage coarse plane k (zero outside)
+    auto coarse = [&](int k, int cs) {  // stage coarse plane k into slot cs (zero outside)
         if (crole) {
             const bool ok = cxy_in && k >= 0 && k < gc.nz;
-            cp_async4(&S.oc[k & 3][cr][ccol], outc + (ok ? k * cplane + cqo : 0), ok);
+            cp_async4(&S.oc[cs][cr][ccol], outc + (ok ? k * cplane + cqo : 0), ok);
         }
     };
-    auto slot = [&](int z) { return (int)((unsigned)(z - zc0 + kUST * 1024) % (unsigned)kUST); };
-    auto issue = [&](int z, unsigned ob) {
+    auto fine = [&](int z, int s, unsigned ob) {  // own inputs of plane z into stage s
         if (zin(z)) {
-            const int s = slot(z);
             const bool ol = own && up_pair(ob);
             const long long q = z * plane + qo;
             cp_async8(&S.y[s][row][2 * lane], y0 + q, ol);  // q in the grid: src-size 0 reads nothing
 #pragma unroll
-            for (int j = 0; j < NO; ++j) {
-                const bool lj = ol && j < nc;
-                cp_async16(&S.ad[s][j][row][2 * lane], adp[j] + q, lj);
-            }
-            if (z == zc0) {
-                for (int k = (z - 1) >> 1; k <= (z + 1) >> 1; ++k) coarse(k);
-            } else if (z & 1) {
-                coarse((z + 1) >> 1);
-            }
+            for (int j = 0; j < NO; ++j) cp_async16(&S.ad[s][j][row][2 * lane], adp[j] + q, ol && j < nc);
         }
-        cp_commit();
     };
     // fine row offsets into the coarse tile (per thread): (yy + dy) >> 1 - CY0
     int crow[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) crow[d] = ((yy + d - 1) >> 1) - CY0;
 
-    unsigned ob[kUPF + 2];
+    unsigned ob[8];  // ob[k % 8]: own bytes of plane zc0 + k (planes z .. z+7 at a step)
 #pragma unroll
-    for (int k = 0; k < kUPF + 2; ++k) ob[k] = own_bytes(zc0 + k);
-#pragma unroll
-    for (int k = 0; k < kUPF; ++k) issue(zc0 + k, ob[k]);
-#pragma unroll(kUPF + 2)
-    for (int z = zc0; z < zc1; ++z) {
-        issue(z + kUPF, ob[kUPF]);
-        cp_wait<kUPF>();  // plane z's group landed (own thread)
+    for (int k = 0; k < 8; ++k) ob[k] = own_bytes(zc0 + k);
+    // prologue group: planes zc0, zc0+1 and coarse planes cz0-1 .. cz0+1
+    fine(zc0, 0, ob[0]);
+    fine(zc0 + 1, 1, ob[1]);
+    coarse(cz0 - 1, up_cslot(-2));
+    coarse(cz0, up_cslot(0));
+    coarse(cz0 + 1, up_cslot(2));
+    cp_commit();
+    // one step: planes z = z8 + K, z + 1 (K = 2J; z8 - zc0 a multiple of 8)
+    auto step = [&](auto Jc, int z8) {
+        constexpr int J = decltype(Jc)::value, K = 2 * J;
+        const int z = z8 + K;
+        // the next step's group: planes z+2, z+3 and coarse plane (z + 4) / 2
+        fine(z + 2, (K + 2) % kUST, ob[(K + 2) % 8]);
+        fine(z + 3, (K + 3) % kUST, ob[(K + 3) % 8]);
+        coarse(cz0 + (z8 - zc0) / 2 + J + 2, up_cslot(K + 4));
+        cp_commit();
+        cp_wait<1>();     // this step's group landed (own thread)
         __syncthreads();  // and every thread's coarse copies
-        const unsigned bc = ob[0];
-        if (own && up_pair(bc)) {
-            const int s = slot(z);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const unsigned bc = ob[(K + p) % 8];
+            if (!(own && up_pair(bc))) continue;
+            const int s = (K + p) % kUST;
             const float2 yv = *reinterpret_cast<const float2*>(&S.y[s][row][2 * lane]);
             float u[2];
             if (F) {
                 // merged parity taps: coarse (lo, hi) per dimension
-                const int zl = ((z - 1) >> 1) & 3, zh = ((z + 1) >> 1) & 3;
-                const int pyz = ((z & 1) << 2) | ((yy & 1) << 1);
+                const int zl = up_cslot(K + p - 1), zh = up_cslot(K + p + 1);
+                const int pyz = (p << 2) | ((yy & 1) << 1);  // z + p has parity p (z even)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const float* m = kc.m[pyz | h];
@@ -148,14 +161,14 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
 #pragma unroll
                     for (int t = 0; t < 27; ++t) {
                         const int dx = t % 3 - 1, dy = (t / 3) % 3 - 1, dz = t / 9 - 1;
-                        const int kz = ((z + dz) >> 1) & 3;
+                        const int kz = up_cslot(K + p + dz);
                         const int col = lane + ((h + dx) >> 1) + 1;  // ((x + h + dx) >> 1) - CX0
                         a = __fadd_rn(a, __fmul_rn(kc.k[t], S.oc[kz][crow[dy + 1]][col]));
                     }
                     u[h] = a;
                 }
             }
-            const long long q = z * plane + qo;
+            const long long q = (z + p) * plane + qo;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (!up_cell((bc >> (8 * h)) & 0xffu)) continue;
@@ -168,9 +181,18 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
                     if (j < nc) acc[j] += dv * S.ad[s][j][row][2 * lane + h];
             }
         }
-#pragma unroll
-        for (int k = 0; k < kUPF + 1; ++k) ob[k] = ob[k + 1];
-        ob[kUPF + 1] = own_bytes(z + kUPF + 2);
+        ob[K % 8] = own_bytes(z + 8);
+        ob[(K + 1) % 8] = own_bytes(z + 9);
+        __syncthreads();  // the slots this step read are restaged by the next step's issue
+    };
+    for (int z8 = zc0; z8 < zc1; z8 += 8) {
+        step(std::integral_constant<int, 0>{}, z8);
+        if (z8 + 2 >= zc1) break;
+        step(std::integral_constant<int, 1>{}, z8);
+        if (z8 + 4 >= zc1) break;
+        step(std::integral_constant<int, 2>{}, z8);
+        if (z8 + 6 >= zc1) break;
+        step(std::integral_constant<int, 3>{}, z8);
     }
     cp_wait<0>();
 }
@@ -205,8 +227,9 @@ __global__ void UP0_BOUNDS k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ 
     double acc[NA];
 #pragma unroll
     for (int j = 0; j < NA; ++j) acc[j] = 0.0;
-    sched_for_each(sc, [&](int tx, int ty, int u0, int u1) {
-        up_l0_segment<NO, F>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, u0, u1);
+    sched_for_each(sc, [&](int tx, int ty, int u0, int u1) {  // units: plane pairs (the down schedule)
+        up_l0_segment<NO, F>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, 2 * u0,
+                             min(2 * u1, g.nz));
     });
     double tot[NA];
     // the mixed fluid cells follow in k_mixed_up0, which finalises the MGS
@@ -243,8 +266,9 @@ __global__ void UP0_BOUNDS k_up_l0m(Geom g, Geom gc, const uint8_t* __restrict__
 #pragma unroll
     for (int j = 0; j < NA; ++j) acc[j] = 0.0;
     if ((int)blockIdx.x < nb_tiled) {
-        sched_for_each_n(sc, blockIdx.x, nb_tiled, [&](int tx, int ty, int u0, int u1) {
-            up_l0_segment<NO, F>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, u0, u1);
+        sched_for_each_n(sc, blockIdx.x, nb_tiled, [&](int tx, int ty, int u0, int u1) {  // plane pairs
+            up_l0_segment<NO, F>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, 2 * u0,
+                                 min(2 * u1, g.nz));
         });
     } else {
         const int tid = threadIdx.y * kSX + threadIdx.x;
