@@ -354,7 +354,6 @@ __global__ void __launch_bounds__(kBlock, MIXUP_MINB) k_mixed_up0(Geom g, Geom g
                                                       const uint32_t* __restrict__ kid, double* __restrict__ dout, SolverState* st,
                                                       const double* __restrict__ ADring, double* __restrict__ partials,
                                                       unsigned int* __restrict__ counter) {
-    constexpr int S = Sh<D>::S;
     constexpr int NA = (NO > 0) ? NO : 1;
     pdl_launch_wait();
     if (st->dist && st->done) return;

@@ -1931,7 +1931,6 @@ void ic0_factor(npsd_b200_ctx* c) {
 
 template <int D, int M>
 void capture_cg_graph(npsd_b200_ctx* c, int ns) {
-    constexpr bool J = (M == kCgJacobi);
     if (c->cg_exec) {
         CK(cudaGraphExecDestroy(c->cg_exec));
         c->cg_exec = nullptr;
@@ -2761,13 +2760,11 @@ int npsd_b200_precond_apply(npsd_b200_ctx* c, const double* r, double* z, int64_
             slab_reduce(c, c->s, kFinNormPrecond);
             slab_exchange(c, c->s, c->R, sizeof(double), 0);
         }
-        SolverState* h = c->st_host;
         // no cached directions: the fused dots in the L0 up kernel are empty
         const int zero = 0;
         CK(cudaMemcpyAsync(&c->st->n_cache, &zero, sizeof(int), cudaMemcpyHostToDevice, c->s));
         const int one = 1;
         CK(cudaMemcpyAsync(&c->st->ring, &one, sizeof(int), cudaMemcpyHostToDevice, c->s));
-        (void)h;
         if (c->dim == 3)
             launch_network<3>(c, c->s, false, nullptr);
         else
