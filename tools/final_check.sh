@@ -10,5 +10,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
     python bench.py --steps 2 --warmup 1 --no-configs --no-sequence --no-cpu-baseline > gpurun_out/fin_ncu_launch.log 2>&1
 python tools/ncu_target.py --iters 1 > gpurun_out/fin_target.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k "regex:k_mixed_down0|k_down_l0|k_cdownz|k_cupz|k_up_l0|k_ortho2|k_update2" \
-    -s 10 -c 10 -o gpurun_out/fin_prof python tools/ncu_target.py --iters 1 > gpurun_out/fin_ncu_prof.log 2>&1
+    -s 14 -c 14 -o gpurun_out/fin_prof python tools/ncu_target.py --iters 1 > gpurun_out/fin_ncu_prof.log 2>&1
 echo done

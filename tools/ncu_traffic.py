@@ -6,9 +6,9 @@ Capture (one GPU; ncu_target runs a 1-iteration warm-up, then the measured
 iterations, kernels launched one by one in the body order below):
 
     ncu --set full --clock-control none -k regex:"k_mixed_down0|k_down_l0|k_cdownz|k_cupz|k_up_l0|k_ortho2|k_update2" \
-        -s 10 -c 10 -o prof python tools/ncu_target.py
+        -s 14 -c 14 -o prof python tools/ncu_target.py      (depth 6: 2 depth + 2 launches per iteration)
 
-    python tools/ncu_traffic.py prof.ncu-rep 256
+    python tools/ncu_traffic.py prof.ncu-rep 256 [depth]
 """
 import csv
 import io
@@ -18,12 +18,16 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-BODY = ["net_mixed_down_L0", "net_down_L0", "net_down_L1", "net_down_L2", "net_coarse_L3", "net_up_L2", "net_up_L1",
-        "net_up_L0", "ortho", "update"]  # depth 4 (net_up_L0: tiled and mixed cells, k_up_l0m)
+def body(depth: int) -> list[str]:
+    """the iteration's launches in order (net_up_L0: tiled and mixed cells, k_up_l0m)"""
+    return (["net_mixed_down_L0"] + [f"net_down_L{l}" for l in range(depth - 1)] + [f"net_coarse_L{depth - 1}"] +
+            [f"net_up_L{l}" for l in range(depth - 2, -1, -1)] + ["ortho", "update"])
 
 
 def main() -> None:
     rep, n = sys.argv[1], int(sys.argv[2])
+    depth = int(sys.argv[3]) if len(sys.argv) > 3 else 6
+    BODY = body(depth)
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[0]
