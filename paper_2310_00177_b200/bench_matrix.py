@@ -207,7 +207,11 @@ def run_bench(systems: dict, methods: list[str], cfg: BenchConfig | None = None,
             if key not in ctxs:
                 if key == "neural" and model is None:
                     raise RuntimeError("run_bench: neural method requested without --model")
-                p = model if key == "neural" else b200.identity_params(model.depth if model else 4)
+                # plain methods never run the network: any depth the grid divides
+                d = model.depth if model else 4
+                while d > 1 and any(n % (1 << (d - 1)) for n in types.shape):
+                    d -= 1
+                p = model if key == "neural" else b200.identity_params(d)
                 ctxs[key] = b200.Context(3, types.shape, p)
             return ctxs[key]
 

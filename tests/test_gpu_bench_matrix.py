@@ -21,7 +21,8 @@ def test_run_bench_rows_csv(b200, oracle, ref, tmp_path):
     box = np.zeros((16, 16, 16), np.uint8)  # all fluid, closed: pure Neumann
     systems = {"C1_32": (t1, oracle.rhs_normal(s1, t1.size)[t1.reshape(-1) == 0]),
                "box_16": (box, oracle.rhs_normal(5, box.size))}
-    model = b200.default_model()
+    # a harness test on small grids: the depth-4 model (32^3 and 16^3 hold whole depth-4 coarsest cells)
+    model = b200.load_npm(b200.DEFAULT_MODEL.parent / "npsd3d_L4.npm")
     rows = bm.run_bench(systems, METHODS, bm.BenchConfig(max_iters=3000), model=model)
     bm.write_bench_outputs(rows, tmp_path / "out")
     bm.write_bench_report(rows, tmp_path / "out")
