@@ -143,7 +143,7 @@ struct CUpSmem {
 template <bool POOL, int ZC, bool F>
 __device__ __forceinline__ void cdownz_tile(const Geom& g, const float* __restrict__ x, const ConvTab& ct, const KC& kc,
                                             float* __restrict__ y, float* __restrict__ xnext, const Geom& gc, int bx,
-                                            int by, int bz, CDownSmem<ZC>& S) {
+                                            int by, int bz, CDownSmem<ZC>& S, const int* __restrict__ done) {
     static_assert(!POOL || ZC % 2 == 0, "pooling pairs planes");
     constexpr int SX = kZX + 2, SY = kZY + 2, SZ = ZC + 2, PL = SY * kZSP;
     float* sx = S.sx;
@@ -156,17 +156,21 @@ __device__ __forceinline__ void cdownz_tile(const Geom& g, const float* __restri
     const long long plane = (long long)g.nx * g.ny;
     const long long c0 = oxy ? lin(g, cx, cy, Z0) : 0;
     const int nown = oxy ? min(ZC, g.zo1 - Z0) : 0;  // planes of this column the rank owns
-    // every load of the prologue is in flight before the first use
-    ZStager<SX, SY, SZ> box;
-    box.load(x, g, X0 - 1, Y0 - 1, Z0 - 1, warp, lane);
+    // setup data first (row codes, the uniform rows, the first cell's row):
+    // with programmatic launch it overlaps the previous kernel
     uint32_t rc[ZC];
 #pragma unroll
     for (int k = 0; k < ZC; ++k) rc[k] = cell_code(ct, c0 + k * plane, k < nown);
     load_uni_rows(U, kc, tid);
-    box.store(sx, warp, lane);
     __syncthreads();
     float kr[28];  // the next cell's kernel row (prefetched one cell ahead)
     load_row(code_row(ct, U, rc[0], c0), kr);
+    pdl_wait_then_trigger();  // x_l is the previous kernel's output
+    if (done && *done) return;  // z-slab chunked loop: the solve has finished (block-uniform)
+    ZStager<SX, SY, SZ> box;
+    box.load(x, g, X0 - 1, Y0 - 1, Z0 - 1, warp, lane);
+    box.store(sx, warp, lane);
+    __syncthreads();
     const float* base = sx + ty * kZSP + tx;  // window (dz, dy, dx) at plane p: base[p*PL + (1+dy)*kZSP + 1+dx]
     float P[3][9];                            // rolling planes: P[p % 3] = plane p's 3 x 3
 #pragma unroll
@@ -221,10 +225,8 @@ template <bool POOL, int ZC, bool F>
 __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cdownz(Geom g, const float* __restrict__ x, ConvTab ct,
                                                 const __grid_constant__ KC kc, float* __restrict__ y,
                                                 float* __restrict__ xnext, Geom gc, const int* __restrict__ done) {
-    pdl_launch_wait();
-    if (done && *done) return;  // z-slab chunked loop: the solve has finished
     __shared__ __align__(16) CDownSmem<ZC> S;
-    cdownz_tile<POOL, ZC, F>(g, x, ct, kc, y, xnext, gc, blockIdx.x, blockIdx.y, blockIdx.z, S);
+    cdownz_tile<POOL, ZC, F>(g, x, ct, kc, y, xnext, gc, blockIdx.x, blockIdx.y, blockIdx.z, S, done);
 }
 
 // one tile of an up step (outc is level l+1)
@@ -232,7 +234,7 @@ template <int ZC, bool F>
 __device__ __forceinline__ void cupz_tile(const Geom& g, const Geom& gc, const float* __restrict__ outc,
                                           const float* __restrict__ yl, const float* __restrict__ zab,
                                           const ConvTab& ct, const KC& kc, float* __restrict__ outl, int bx, int by,
-                                          int bz, CUpSmem<ZC>& S) {
+                                          int bz, CUpSmem<ZC>& S, const int* __restrict__ done) {
     static_assert(ZC % 2 == 0, "fine planes come in coarse pairs");
     // coarse box: (X0/2 - 1 .. X0/2 + 16) x (Y0/2 - 1 .. Y0/2 + 4) x (Z0/2 - 1 .. Z0/2 + ZC/2)
     constexpr int CX = kZX / 2 + 2, CY = kZY / 2 + 2, CZ = ZC / 2 + 2, PL = CY * kZSP;
@@ -246,22 +248,25 @@ __device__ __forceinline__ void cupz_tile(const Geom& g, const Geom& gc, const f
     const long long plane = (long long)g.nx * g.ny;
     const long long c0 = oxy ? lin(g, cx, cy, Z0) : 0;
     const int nown = oxy ? min(ZC, g.zo1 - Z0) : 0;  // planes of this column the rank owns
-    // every load of the prologue is in flight before the first use
-    ZStager<CX, CY, CZ> box;
-    box.load(outc, gc, (X0 >> 1) - 1, (Y0 >> 1) - 1, (Z0 >> 1) - 1, warp, lane);
+    // setup data first (row codes, the uniform rows, the first cell's row):
+    // with programmatic launch it overlaps the previous kernel
     uint32_t rc[ZC];
-    float yv[ZC];
 #pragma unroll
-    for (int k = 0; k < ZC; ++k) {
-        rc[k] = cell_code(ct, c0 + k * plane, k < nown);
-        yv[k] = k < nown ? __ldg(yl + c0 + k * plane) : 0.0f;
-    }
+    for (int k = 0; k < ZC; ++k) rc[k] = cell_code(ct, c0 + k * plane, k < nown);
     load_uni_rows(U, kc, tid);
-    const float za = zab[0], zb = zab[1];
-    box.store(sc, warp, lane);
     __syncthreads();
     float kr[28];  // the next cell's kernel row (prefetched one cell ahead)
     load_row(code_row(ct, U, rc[0], c0), kr);
+    pdl_wait_then_trigger();  // out_{l+1} is the previous kernel's output (y_l, z an earlier one's)
+    if (done && *done) return;  // z-slab chunked loop: the solve has finished (block-uniform)
+    ZStager<CX, CY, CZ> box;
+    box.load(outc, gc, (X0 >> 1) - 1, (Y0 >> 1) - 1, (Z0 >> 1) - 1, warp, lane);
+    float yv[ZC];
+#pragma unroll
+    for (int k = 0; k < ZC; ++k) yv[k] = k < nown ? __ldg(yl + c0 + k * plane) : 0.0f;
+    const float za = zab[0], zb = zab[1];
+    box.store(sc, warp, lane);
+    __syncthreads();
     // fine tap (cx + dx, cy + dy) -> staged coarse ((cx + dx) >> 1) - (X0/2 - 1), likewise y;
     // out-of-domain fine cells map to out-of-domain coarse cells (dims even): staged zeros
     int off[9];
@@ -301,10 +306,8 @@ __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cupz(Geom g, Geom gc, con
                                               const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
                                               const __grid_constant__ KC kc, float* __restrict__ outl,
                                               const int* __restrict__ done) {
-    pdl_launch_wait();
-    if (done && *done) return;  // z-slab chunked loop: the solve has finished
     __shared__ __align__(16) CUpSmem<ZC> S;
-    cupz_tile<ZC, F>(g, gc, outc, yl, zab, ct, kc, outl, blockIdx.x, blockIdx.y, blockIdx.z, S);
+    cupz_tile<ZC, F>(g, gc, outc, yl, zab, ct, kc, outl, blockIdx.x, blockIdx.y, blockIdx.z, S, done);
 }
 
 }  // namespace nb2

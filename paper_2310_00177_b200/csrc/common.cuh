@@ -153,6 +153,15 @@ __device__ __forceinline__ void pdl_launch_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// The coarse-level kernels: what they read before this point comes from the
+// frame's setup only (row codes, kernel rows, uniform kernels), so with the
+// launch attribute it overlaps the previous kernel; then wait for it, and
+// only then let the next kernel launch (at most one kernel runs ahead).
+__device__ __forceinline__ void pdl_wait_then_trigger() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

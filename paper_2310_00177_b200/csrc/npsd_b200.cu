@@ -259,6 +259,8 @@ struct npsd_b200_ctx {
     // programmatic dependent launch of the iteration kernels: measured neutral
     // in the solve graph (C3 256^3: 386.0 vs 384.8 ms), so opt-in (NPSD_PDL=1)
     bool pdl = false;
+    // the coarse-level kernels only (their setup loads overlap the previous kernel): NPSD_PDL_COARSE=0 disables
+    bool pdl_coarse = true;
     double* icD = nullptr;    // IC0 factor diagonal (full grid)
     int* icFail = nullptr;    // IC0 factorization failure flag (+ scratch)
     int ic0_shift_retries = 0;
@@ -1037,8 +1039,8 @@ struct Step {
 // programmatic stream serialisation: its blocks may launch while the previous
 // kernel drains; in a captured graph this becomes a programmatic edge.
 template <typename... KArgs, typename... Args>
-void launch_pdl(npsd_b200_ctx* c, cudaStream_t s, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                Args&&... args) {
+void launch_pdl_if(npsd_b200_ctx* c, cudaStream_t s, bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block,
+                   size_t smem, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -1048,10 +1050,17 @@ void launch_pdl(npsd_b200_ctx* c, cudaStream_t s, void (*k)(KArgs...), dim3 grid
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = c->pdl ? 1 : 0;
+    cfg.numAttrs = pdl ? 1 : 0;
     CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
     ++c->launches;
 }
+template <typename... KArgs, typename... Args>
+void launch_pdl(npsd_b200_ctx* c, cudaStream_t s, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                Args&&... args) {
+    launch_pdl_if(c, s, c->pdl, k, grid, block, smem, std::forward<Args>(args)...);
+}
+// the coarse-level kernels read only setup data before their wait (coarse.cuh)
+inline bool pdl_coarse(const npsd_b200_ctx* c) { return c->pdl || (c->pdl_coarse && !c->slab.on); }
 
 // z-chunk (in bricks or planes) so that a launch has about two waves of blocks.
 template <typename K>
@@ -1088,7 +1097,8 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
         const int zc = coarse_zc(c, L.g);
         const dim3 grid((L.g.nx + kZX - 1) / kZX, (L.g.ny + kZY - 1) / kZY, (L.g.zo1 - L.g.zo0 + zc - 1) / zc);
 #define NPSD_CDOWN(ZC_, F_) \
-    launch_pdl(c, s, k_cdownz<POOL, ZC_, F_>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, xnext, gc, dn)
+    launch_pdl_if(c, s, pdl_coarse(c), k_cdownz<POOL, ZC_, F_>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, \
+                  xnext, gc, dn)
         if (c->fast) {
             if (zc == 8) NPSD_CDOWN(8, true);
             else if (zc == 4) NPSD_CDOWN(4, true);
@@ -1123,8 +1133,8 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
         const int zc = coarse_zc(c, L.g);
         const dim3 grid((L.g.nx + kZX - 1) / kZX, (L.g.ny + kZY - 1) / kZY, (L.g.zo1 - L.g.zo0 + zc - 1) / zc);
 #define NPSD_CUP(ZC_, F_)                                                                                        \
-    launch_pdl(c, s, k_cupz<ZC_, F_>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, tab_up(c, l), \
-               c->kc_up[l], outl, dn)
+    launch_pdl_if(c, s, pdl_coarse(c), k_cupz<ZC_, F_>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, \
+                  tab_up(c, l), c->kc_up[l], outl, dn)
         if (c->fast) {
             if (zc == 8) NPSD_CUP(8, true);
             else if (zc == 4) NPSD_CUP(4, true);
@@ -2305,6 +2315,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
         if (const char* e = std::getenv("NPSD_MERGE_UP0")) c->merge_up0 = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_CLASSIFY_SIMD")) c->classify_simd = (e[0] != '0');
+        if (const char* e = std::getenv("NPSD_PDL_COARSE")) c->pdl_coarse = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_UP0_MIXB")) c->up0_mixb = std::max(0, std::min(16, std::atoi(e)));
         if (slab) {
             c->slab = *slab;
