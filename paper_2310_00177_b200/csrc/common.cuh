@@ -144,13 +144,14 @@ struct SolverState {
                                     // iteration kernels return at once when done (chunked loop)
 };
 
-// Programmatic dependent launch (the iteration kernels): let the next kernel
-// in the stream launch now, then wait for the previous one's completion and
-// memory before touching anything it wrote. Without the launch attribute both
-// are no-ops.
+// Programmatic dependent launch (the iteration kernels): wait for the
+// previous kernel's completion and memory, then let the next kernel in the
+// stream launch. At most one kernel runs ahead, so whatever a kernel reads
+// before its wait must not be written by its immediate predecessor (anything
+// older is complete). Without the launch attribute both are no-ops.
 __device__ __forceinline__ void pdl_launch_wait() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // The coarse-level kernels: what they read before this point comes from the

@@ -55,7 +55,7 @@ template <bool F>
 __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __restrict__ cls,
                                                 const double* __restrict__ r, const SolverState* __restrict__ st,
                                                 const KC0& kc, float* __restrict__ y, float* __restrict__ xnext,
-                                                const Geom& gc, int tx, int ty, int zc0, int zc1) {
+                                                const Geom& gc, int tx, int ty, int zc0, int zc1, bool& waited) {
     static_assert(kD0R == 4 && kD0X == 8, "the 8-plane chunk maps ring slots to constants");
     const int lane = threadIdx.x, row = threadIdx.y;
     const int X0 = tx * kTX, Y0 = ty * kTY;
@@ -155,6 +155,12 @@ __device__ __forceinline__ void down_l0_segment(const Geom& g, const uint8_t* __
     issue(zc0 - 1, 0, own_bytes(zc0 - 1));
 #pragma unroll
     for (int k = 0; k <= kD0A; ++k) issue(zc0 + k, (k + 1) % kD0R, ob[k]);
+    // r (the update two launches back) and the cell bytes are complete; the
+    // mixed cells' y_0 is the previous launch's (k_mixed_down0): wait for it
+    if (!waited) {
+        pdl_launch_wait();
+        waited = true;
+    }
     cp_wait<kD0A>();  // planes zc0-1, zc0 landed
     form(zc0 - 1, 0, 0);
     form(zc0, 1, 1);
@@ -247,11 +253,17 @@ __global__ void __launch_bounds__(kSX* kSY, D0_MINB) k_down_l0(Geom g, const uin
                                                       const double* __restrict__ r, const SolverState* __restrict__ st,
                                                       const __grid_constant__ KC0 kc, float* __restrict__ y,
                                                       float* __restrict__ xnext, Geom gc, Sched sc) {
-    pdl_launch_wait();
-    if (st->dist && st->done) return;
+    // reads before the programmatic wait: the solver state and r (written two
+    // launches back), cell bytes and the schedule (setup)
+    if (st->dist && st->done) {
+        pdl_launch_wait();
+        return;
+    }
+    bool waited = false;
     sched_for_each(sc, [&](int tx, int ty, int u0, int u1) {
-        down_l0_segment<F>(g, cls, r, st, kc, y, xnext, gc, tx, ty, 2 * u0, min(2 * u1, g.nz));
+        down_l0_segment<F>(g, cls, r, st, kc, y, xnext, gc, tx, ty, 2 * u0, min(2 * u1, g.nz), waited);
     });
+    if (!waited) pdl_launch_wait();
 }
 
 }  // namespace nb2

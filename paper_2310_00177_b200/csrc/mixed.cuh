@@ -228,24 +228,34 @@ __global__ void __launch_bounds__(kBlock, MIXDN_MINB) k_mixed_down0(Geom g, cons
                                                         const float* __restrict__ tab, const uint32_t* __restrict__ kid,
                                                         float* __restrict__ y) {
     constexpr int S = Sh<D>::S;
+    // the first cell's list entry and kernel row are setup data: loaded before
+    // the programmatic wait (the previous launch writes r)
+    const uint32_t n = *count;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t c = 0;
+    float k[S];
+    auto fetch = [&](long long j) {
+        c = list[j];
+        const float* K = tab + (long long)__ldg(kid + j) * kRowW;
+#pragma unroll
+        for (int s = 0; s < S; ++s) k[s] = __ldg(K + s);
+    };
+    if (i < n) fetch(i);
     pdl_launch_wait();
     if (st->dist && st->done) return;
-    const uint32_t n = *count;
     const double inv1 = st->inv1, inv2 = st->inv2;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint32_t c = list[i];
-        const float* K = tab + (long long)__ldg(kid + i) * kRowW;
+    for (; i < n; i += stride) {
+        if (i >= (long long)blockIdx.x * blockDim.x + threadIdx.x + stride) fetch(i);
         int x, yy, z;
         decode32(g, c, x, yy, z);
-        float w[S], k[S];
+        float w[S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
             const int xx = x + dx, y2 = yy + dy, zz = z + dz;
             const bool in = xx >= 0 && xx < g.nx && y2 >= 0 && y2 < g.ny && zz >= 0 && zz < g.nz;
             w[s] = in ? __double2float_rn(__dmul_rn(__dmul_rn(__ldg(r + lin(g, xx, y2, zz)), inv1), inv2)) : 0.0f;
-            k[s] = __ldg(K + s);
         }
         y[c] = win_dot<F, S>([&](int t) { return k[t]; }, [&](int t) { return w[t]; });
     }

@@ -256,9 +256,16 @@ struct npsd_b200_ctx {
     long long slab_short_launches = 0;
     int slab_exec_no = -1, slab_exec_k0 = -1, slab_exec_ns = 0, slab_exec_ident = 0;
     bool slab_no_graph = false;   // the chunk graph could not be captured: eager chunks
-    // programmatic dependent launch of the iteration kernels: measured neutral
-    // in the solve graph (C3 256^3: 386.0 vs 384.8 ms), so opt-in (NPSD_PDL=1)
-    bool pdl = false;
+    // programmatic dependent launch of the iteration kernels (NPSD_PDL=0
+    // disables): each waits for its predecessor, then lets the next launch;
+    // what a kernel reads before its wait is older than its predecessor
+    // (common.cuh pdl_launch_wait)
+    bool pdl = true;
+    // per launch site (pdl_on; NPSD_PDL_MASK): the level-0 network kernels.
+    // Measured per site (C1 / C2 / C3 us per iteration vs none): down L0
+    // -2.3 / -3.6 / -3.2, up L0 -1.0 / -1.2 / -1.9, mixed down and ortho
+    // neutral, update +0.5 / +7.8 / +25.6 (profiles/r02_ab_pdl_sites.txt)
+    unsigned pdl_mask = 0x7;
     // the coarse-level kernels only (their setup loads overlap the previous kernel): NPSD_PDL_COARSE=0 disables
     bool pdl_coarse = true;
     double* icD = nullptr;    // IC0 factor diagonal (full grid)
@@ -1061,6 +1068,8 @@ void launch_pdl(npsd_b200_ctx* c, cudaStream_t s, void (*k)(KArgs...), dim3 grid
 }
 // the coarse-level kernels read only setup data before their wait (coarse.cuh)
 inline bool pdl_coarse(const npsd_b200_ctx* c) { return c->pdl || (c->pdl_coarse && !c->slab.on); }
+// the level-0 / solver kernels: bit 0 mixed down, 1 down L0, 2 up L0 (+ mixed up), 3 ortho, 4 update
+inline bool pdl_on(const npsd_b200_ctx* c, int bit) { return c->pdl && ((c->pdl_mask >> bit) & 1); }
 
 // z-chunk (in bricks or planes) so that a launch has about two waves of blocks.
 template <typename K>
@@ -1194,7 +1203,7 @@ void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
             // mixed-list blocks per SM: measured best 1 at 64^3, 2 at 128^3, 4 at 256^3
             // (C1/C2/C3, tools/env_ab.py NPSD_UP0_MIXB): about one per 2^20 cells, 1..4
             const int mixb = c->up0_mixb ? c->up0_mixb : (int)std::max(1LL, std::min(4LL, L.g.n >> 20));
-            launch_pdl(c, s, k, dim3(nt + mixb * c->num_sms), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y, c->zab, kc0,
+            launch_pdl_if(c, s, pdl_on(c, 2), k, dim3(nt + mixb * c->num_sms), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y, c->zab, kc0,
                        c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_down0.view(), nt,
                        (const uint32_t*)c->ulist0, (const uint32_t*)c->ucnt0, (const float*)L.tab_up,
                        (const uint32_t*)c->ukid0);
@@ -1202,7 +1211,7 @@ void launch_up0(npsd_b200_ctx* c, cudaStream_t s) {
         }
         auto k = c->fast ? k_up_l0<NO, true> : k_up_l0<NO, false>;
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        launch_pdl(c, s, k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y,
+        launch_pdl_if(c, s, pdl_on(c, 2), k, dim3(wave_blocks(c, k, kSX * kSY, sm)), dim3(kSX, kSY), sm, L.g, L1.g, L.cls, outc, L.y,
                    c->zab, kc0, c->Dtmp, c->st, c->ADring, c->partials, c->counter, c->sch_down0.view());
         return;
     }
@@ -1232,7 +1241,7 @@ void launch_ortho(npsd_b200_ctx* c, cudaStream_t s) {
     const size_t sm = stencil_smem_bytes<D, OrthoOp<NO>, SY>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const dim3 grid(wave_blocks(c, k, kSX * SY, sm));
-    launch_pdl(c, s, k, grid, block, sm, g, c->L[0].cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
+    launch_pdl_if(c, s, pdl_on(c, 3), k, grid, block, sm, g, c->L[0].cls, c->Dtmp, c->R, c->Dring, c->ADring, c->st, c->partials,
                c->counter, (SY == kSY ? c->sch_stencil : c->sch_march).view(), *c->maps);
 }
 
@@ -1257,7 +1266,7 @@ void launch_update(npsd_b200_ctx* c, cudaStream_t s, cudaGraphConditionalHandle 
     const size_t sm = stencil_smem_bytes<D, UpdateOp, SY>();
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const dim3 grid(wave_blocks(c, k, kSX * SY, sm));
-    launch_pdl(c, s, k, grid, block, sm, g, c->L[0].cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist,
+    launch_pdl_if(c, s, pdl_on(c, 4), k, grid, block, sm, g, c->L[0].cls, c->Bf, c->X0, c->X1, c->Dring, c->R, c->st, c->hist,
                c->times, c->partials, c->counter, h, use_cond, do_norm, (SY == kSY ? c->sch_stencil : c->sch_march).view(),
                *c->maps);
 }
@@ -1276,7 +1285,7 @@ void launch_down_l0(npsd_b200_ctx* c, cudaStream_t s) {
     const dim3 grid(wave_blocks(c, k, kSX * kSY, sm));
     KC0 kc0;
     for (int i = 0; i < 27; ++i) kc0.k[i] = c->kc_down[0].k[0][i];  // the uniform-fluid kernel
-    launch_pdl(c, s, k, grid, block, sm, g, L.cls, c->R, (const SolverState*)c->st, kc0, L.y, c->L[1].x, c->L[1].g,
+    launch_pdl_if(c, s, pdl_on(c, 1), k, grid, block, sm, g, L.cls, c->R, (const SolverState*)c->st, kc0, L.y, c->L[1].x, c->L[1].g,
                c->sch_down0.view());
 }
 
@@ -1284,7 +1293,7 @@ template <int D>
 void launch_mixed_down0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L = c->L[0];
     auto k = c->fast ? k_mixed_down0<D, true> : k_mixed_down0<D, false>;
-    launch_pdl(c, s, k, dim3(grid_for(c, k, L.g.n)), dim3(kBlock), 0, L.g, c->dlist0, c->dcnt0, c->R,
+    launch_pdl_if(c, s, pdl_on(c, 0), k, dim3(grid_for(c, k, L.g.n)), dim3(kBlock), 0, L.g, c->dlist0, c->dcnt0, c->R,
                (const SolverState*)c->st, L.tab_down, c->dkid0, L.y);
 }
 
@@ -1294,7 +1303,7 @@ void launch_mixed_up0(npsd_b200_ctx* c, cudaStream_t s) {
     const LevelBufs& L1 = c->L[1];
     const float* outc = (c->depth == 2) ? L1.y : L1.out;
     auto k = c->fast ? k_mixed_up0<D, NO, true> : k_mixed_up0<D, NO, false>;
-    launch_pdl(c, s, k, dim3(grid_for(c, k, L.g.n)), dim3(kBlock), 0, L.g, L1.g, c->ulist0, c->ucnt0, outc, L.y,
+    launch_pdl_if(c, s, pdl_on(c, 2), k, dim3(grid_for(c, k, L.g.n)), dim3(kBlock), 0, L.g, L1.g, c->ulist0, c->ucnt0, outc, L.y,
                c->zab, L.tab_up, c->ukid0, c->Dtmp, c->st, c->ADring, c->partials, c->counter);
 }
 
@@ -2312,7 +2321,8 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->depth = depth;
         c->S = (dim == 3) ? 27 : 9;
         c->dev = device;
-        if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] == '1');
+        if (const char* e = std::getenv("NPSD_PDL")) c->pdl = (e[0] != '0');
+        if (const char* e = std::getenv("NPSD_PDL_MASK")) c->pdl_mask = (unsigned)std::strtoul(e, nullptr, 0);
         if (const char* e = std::getenv("NPSD_MERGE_UP0")) c->merge_up0 = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_CLASSIFY_SIMD")) c->classify_simd = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_PDL_COARSE")) c->pdl_coarse = (e[0] != '0');

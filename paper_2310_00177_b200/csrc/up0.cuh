@@ -66,7 +66,7 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
                                               const KUp0& kc, float za, float zb, double nrm, int nc,
                                               const double* const (&adp)[(NO > 0) ? NO : 1],
                                               double* __restrict__ dout, double (&acc)[(NO > 0) ? NO : 1], int tx,
-                                              int ty, int zc0, int zc1) {
+                                              int ty, int zc0, int zc1, bool& waited) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Up0Smem<NO>& S = *reinterpret_cast<Up0Smem<NO>*>(smem_raw);
     __syncthreads();  // the previous segment's last reads of S are done
@@ -115,6 +115,11 @@ __device__ __forceinline__ void up_l0_segment(const Geom& g, const Geom& gc, con
     // prologue group: planes zc0, zc0+1 and coarse planes cz0-1 .. cz0+1
     fine(zc0, 0, ob[0]);
     fine(zc0 + 1, 1, ob[1]);
+    // y_0 and Ad_j are older than the previous launch; out_1 is its output
+    if (!waited) {
+        pdl_launch_wait();
+        waited = true;
+    }
     coarse(cz0 - 1, up_cslot(-2));
     coarse(cz0, up_cslot(0));
     coarse(cz0 + 1, up_cslot(2));
@@ -213,8 +218,10 @@ __global__ void UP0_BOUNDS k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ 
                                                     const double* __restrict__ ADring, double* __restrict__ partials,
                                                     unsigned int* __restrict__ counter, Sched sc) {
     constexpr int NA = (NO > 0) ? NO : 1;
-    pdl_launch_wait();
-    if (st->dist && st->done) return;
+    if (st->dist && st->done) {  // (written by the update, three launches back)
+        pdl_launch_wait();
+        return;
+    }
     const float za = zab[0], zb = zab[1];
     const double nrm = st->nrm;
     const int nc = st->n_cache, R = st->ring;
@@ -227,10 +234,12 @@ __global__ void UP0_BOUNDS k_up_l0(Geom g, Geom gc, const uint8_t* __restrict__ 
     double acc[NA];
 #pragma unroll
     for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+    bool waited = false;  // reads before the programmatic wait: st, y_0, Ad_j, cell bytes (older launches)
     sched_for_each(sc, [&](int tx, int ty, int u0, int u1) {  // units: plane pairs (the down schedule)
         up_l0_segment<NO, F>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, 2 * u0,
-                             min(2 * u1, g.nz));
+                             min(2 * u1, g.nz), waited);
     });
+    if (!waited) pdl_launch_wait();
     double tot[NA];
     // the mixed fluid cells follow in k_mixed_up0, which finalises the MGS
     // projections from these totals plus its own
@@ -251,8 +260,10 @@ __global__ void UP0_BOUNDS k_up_l0m(Geom g, Geom gc, const uint8_t* __restrict__
                                      const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
                                      const float* __restrict__ tab, const uint32_t* __restrict__ ukid) {
     constexpr int NA = (NO > 0) ? NO : 1;
-    pdl_launch_wait();
-    if (st->dist && st->done) return;
+    if (st->dist && st->done) {  // (written by the update, three launches back)
+        pdl_launch_wait();
+        return;
+    }
     const float za = zab[0], zb = zab[1];
     const double nrm = st->nrm;
     const int nc = st->n_cache, R = st->ring;
@@ -265,12 +276,15 @@ __global__ void UP0_BOUNDS k_up_l0m(Geom g, Geom gc, const uint8_t* __restrict__
     double acc[NA];
 #pragma unroll
     for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+    bool waited = false;  // reads before the programmatic wait: st, y_0, Ad_j, cell bytes (older launches)
     if ((int)blockIdx.x < nb_tiled) {
         sched_for_each_n(sc, blockIdx.x, nb_tiled, [&](int tx, int ty, int u0, int u1) {  // plane pairs
             up_l0_segment<NO, F>(g, gc, cls, outc, y0, kc, za, zb, nrm, nc, adp, dout, acc, tx, ty, 2 * u0,
-                                 min(2 * u1, g.nz));
+                                 min(2 * u1, g.nz), waited);
         });
+        if (!waited) pdl_launch_wait();
     } else {
+        pdl_launch_wait();  // the mixed cells read out_1 at once
         const int tid = threadIdx.y * kSX + threadIdx.x;
         const long long nthr = (long long)(gridDim.x - nb_tiled) * (kSX * kSY);
         mixed_up_cells<3, NO, F>(g, gc, ulist, *ucount, outc, y0, za, zb, tab, ukid, dout, nrm, nc, adp, acc,
