@@ -224,7 +224,11 @@ __device__ __forceinline__ void cdownz_tile(const Geom& g, const float* __restri
 template <bool POOL, int ZC, bool F>
 __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cdownz(Geom g, const float* __restrict__ x, ConvTab ct,
                                                 const __grid_constant__ KC kc, float* __restrict__ y,
-                                                float* __restrict__ xnext, Geom gc, const int* __restrict__ done) {
+                                                float* __restrict__ xnext, Geom gc, const int* __restrict__ done,
+                                                const uint8_t* __restrict__ live) {
+    // solve path: a tile without fluid near it (k_coarse_live) keeps the zeros
+    // its outputs were given for the frame (setup data: read before the wait)
+    if (live && !live[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]) return;
     __shared__ __align__(16) CDownSmem<ZC> S;
     cdownz_tile<POOL, ZC, F>(g, x, ct, kc, y, xnext, gc, blockIdx.x, blockIdx.y, blockIdx.z, S, done);
 }
@@ -308,6 +312,28 @@ __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cupz(Geom g, Geom gc, con
                                               const int* __restrict__ done) {
     __shared__ __align__(16) CUpSmem<ZC> S;
     cupz_tile<ZC, F>(g, gc, outc, yl, zab, ct, kc, outl, blockIdx.x, blockIdx.y, blockIdx.z, S, done);
+}
+
+// Live tiles of a coarse down step (k_cdownz's 32 x 8 x zc tiles, level l >= 1),
+// for the solve path only: its input x_l is zero outside the cells within one
+// cell of a level-l cell holding fluid (x_0 = r vanishes off the fluid; a conv
+// of an all-zero window is zero; pooling keeps the bound), so a tile whose
+// window box (tile + 1) has no fluid within 2 cells has y_l = 0 and writes
+// zeros only. One block per tile scans the tile +- 2 for a fluid fraction > 0.
+__global__ void __launch_bounds__(kBlock) k_coarse_live(Geom g, const float* __restrict__ fluid, int zc,
+                                                        uint8_t* __restrict__ live) {
+    const int ntx = (g.nx + kZX - 1) / kZX, nty = (g.ny + kZY - 1) / kZY;
+    const int t = blockIdx.x, bx = t % ntx, by = (t / ntx) % nty, bz = t / (ntx * nty);
+    const int X0 = bx * kZX - 2, Y0 = by * kZY - 2, Z0 = bz * zc - 2;
+    const int BX = kZX + 4, BY = kZY + 4, BZ = zc + 4;
+    bool any = false;
+    for (int i = threadIdx.x; i < BX * BY * BZ && !any; i += blockDim.x) {
+        const int x = X0 + i % BX, y = Y0 + (i / BX) % BY, z = Z0 + i / (BX * BY);
+        if ((unsigned)x < (unsigned)g.nx && (unsigned)y < (unsigned)g.ny && (unsigned)z < (unsigned)g.nz)
+            any = fluid[((long long)z * g.ny + y) * g.nx + x] > 0.0f;
+    }
+    any = __syncthreads_or(any) != 0;
+    if (threadIdx.x == 0) live[t] = any ? 1 : 0;
 }
 
 }  // namespace nb2

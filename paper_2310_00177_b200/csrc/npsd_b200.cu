@@ -314,7 +314,11 @@ struct npsd_b200_ctx {
     SchedBufs sch_stencil;      // 64 x 8 tile columns, plane units (k_up_l0, k_cg_dir; k_ortho2 at n_ortho > 2)
     SchedBufs sch_march;        // 64 x kMarchSY tile columns, plane units (k_ortho2, k_update2)
     SchedBufs sch_down0;        // 64 x 8 tile columns, plane-pair units, window dilation (k_down_l0)
-    bool x1_clean = false;      // L1.x is zero outside sch_down0's units
+    bool x1_clean = false;      // L1.x is zero outside sch_down0's units (and the skipped coarse tiles' outputs zero)
+    // coarse down steps of the solve path: live tiles per level (k_coarse_live;
+    // NPSD_COARSE_SKIP=0: every tile runs)
+    bool coarse_skip = true;
+    uint8_t* clive[kMaxDepth] = {};
     // level-0 window-pattern dictionary (setup.cuh)
     unsigned long long* dkeys = nullptr;
     uint32_t* dvals = nullptr;
@@ -639,6 +643,16 @@ int wave_blocks(npsd_b200_ctx* c, K kernel, int threads, size_t smem) {
     return c->num_sms * occ;
 }
 
+// planes per block of the z-marching coarse kernels: as many as still leave
+// about four blocks per SM (small levels: short marches, more blocks)
+inline int coarse_zc(const npsd_b200_ctx* c, const Geom& g) {
+    const long long tiles = (long long)((g.nx + kZX - 1) / kZX) * ((g.ny + kZY - 1) / kZY);
+    const int nzo = g.zo1 - g.zo0;
+    int zc = c->coarse_zc_max;
+    while (zc > 2 && tiles * ((nzo + zc - 1) / zc) < 4LL * c->num_sms) zc /= 2;
+    return zc;
+}
+
 // Pattern ids of level l's mixed cells (keys in c->dkeys) by the hash table
 // (setup.cuh k_dedup_*): pid[i], rep[pattern] = its representative, *npat.
 // The table's level-l capacity (c->cap_ht[l] slots, a power of two) is sized
@@ -727,6 +741,11 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         }
         // level l's dictionary (hashed windows, verified) and rows
         const cudaStream_t sl = setup_fork(c, sc, 2 + l);
+        if (c->clive[l]) {
+            const int zc = coarse_zc(c, Lc.g);
+            const int nt = ((Lc.g.nx + kZX - 1) / kZX) * ((Lc.g.ny + kZY - 1) / kZY) * ((Lc.g.nz + zc - 1) / zc);
+            LAUNCH3(c, sl, k_coarse_live, dim3(nt), dim3(kBlock), Lc.g, (const float*)Lc.img, zc, c->clive[l]);
+        }
         const uint32_t rows_cap = (uint32_t)c->tab_cap[l];
         const uint32_t rows_bit = 1u << (2 * l + 1);
         uint32_t* rep = c->crep + c->roff[l];
@@ -1084,18 +1103,9 @@ int zchunk_for(npsd_b200_ctx* c, K kernel, int threads, long long tiles_xy, int 
     return (int)zc;
 }
 
-// planes per block of the z-marching coarse kernels: as many as still leave
-// about four blocks per SM (small levels: short marches, more blocks)
-inline int coarse_zc(const npsd_b200_ctx* c, const Geom& g) {
-    const long long tiles = (long long)((g.nx + kZX - 1) / kZX) * ((g.ny + kZY - 1) / kZY);
-    const int nzo = g.zo1 - g.zo0;
-    int zc = c->coarse_zc_max;
-    while (zc > 2 && tiles * ((nzo + zc - 1) / zc) < 4LL * c->num_sms) zc /= 2;
-    return zc;
-}
-
 template <int D, bool L0, bool POOL>
-void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, const double* in_d) {
+void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, const double* in_d,
+                 bool skip = false) {
     LevelBufs& L = c->L[l];
     const Geom gc = POOL ? c->L[l + 1].g : L.g;
     float* xnext = POOL ? c->L[l + 1].x : nullptr;
@@ -1105,9 +1115,10 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
         const int* dn = c->slab.on ? &c->st->done : nullptr;
         const int zc = coarse_zc(c, L.g);
         const dim3 grid((L.g.nx + kZX - 1) / kZX, (L.g.ny + kZY - 1) / kZY, (L.g.zo1 - L.g.zo0 + zc - 1) / zc);
+        const uint8_t* live = (skip && POOL) ? c->clive[l] : nullptr;
 #define NPSD_CDOWN(ZC_, F_) \
     launch_pdl_if(c, s, pdl_coarse(c), k_cdownz<POOL, ZC_, F_>, grid, dim3(kZT), 0, L.g, in_f, tab_down(c, l), kc, L.y, \
-                  xnext, gc, dn)
+                  xnext, gc, dn, live)
         if (c->fast) {
             if (zc == 8) NPSD_CDOWN(8, true);
             else if (zc == 4) NPSD_CDOWN(4, true);
@@ -1349,7 +1360,7 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
                          } else {
                              const float* in = (l == 0) ? c->xin_f : c->L[l].x;
                              if (pool)
-                                 launch_down<D, false, true>(c, s, l, in, nullptr);
+                                 launch_down<D, false, true>(c, s, l, in, nullptr, !raw);
                              else
                                  launch_down<D, false, false>(c, s, l, in, nullptr);
                          }
@@ -1390,6 +1401,11 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
 void ensure_x1_clean(npsd_b200_ctx* c, cudaStream_t s) {
     if (c->x1_clean || c->dim != 3 || c->depth < 2) return;
     CK(cudaMemsetAsync(c->L[1].x, 0, (size_t)c->L[1].g.n * sizeof(float), s));
+    for (int l = 1; l + 1 < c->depth; ++l)
+        if (c->clive[l]) {  // outputs of the coarse tiles the solve path skips
+            CK(cudaMemsetAsync(c->L[l].y, 0, (size_t)c->L[l].g.n * sizeof(float), s));
+            CK(cudaMemsetAsync(c->L[l + 1].x, 0, (size_t)c->L[l + 1].g.n * sizeof(float), s));
+        }
     c->x1_clean = true;
 }
 
@@ -2241,6 +2257,8 @@ void free_ctx(npsd_b200_ctx* c) {
         F(p);
     if (c->info_host) cudaFreeHost(c->info_host);
     if (c->maps) cudaFreeHost(c->maps);
+    for (auto p : c->clive)
+        if (p) cudaFree(p);
     if (c->ev_setup) cudaEventDestroy(c->ev_setup);
     if (c->ev_pre_mask) cudaEventDestroy(c->ev_pre_mask);
     if (c->ev_up) cudaEventDestroy(c->ev_up);
@@ -2325,6 +2343,7 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         if (const char* e = std::getenv("NPSD_PDL_MASK")) c->pdl_mask = (unsigned)std::strtoul(e, nullptr, 0);
         if (const char* e = std::getenv("NPSD_MERGE_UP0")) c->merge_up0 = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_CLASSIFY_SIMD")) c->classify_simd = (e[0] != '0');
+        if (const char* e = std::getenv("NPSD_COARSE_SKIP")) c->coarse_skip = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_PDL_COARSE")) c->pdl_coarse = (e[0] != '0');
         if (const char* e = std::getenv("NPSD_UP0_MIXB")) c->up0_mixb = std::max(0, std::min(16, std::atoi(e)));
         if (slab) {
@@ -2474,6 +2493,13 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         CK(cudaEventCreateWithFlags(&c->ev_up, cudaEventDisableTiming));
         CK(cudaEventRecord(c->ev_pre_mask, c->s));
         c->types_dev = dalloc<uint8_t>((size_t)c->g0.n);
+        if (dim == 3 && !c->slab.on && c->coarse_skip)
+            for (int l = 1; l + 1 < depth; ++l) {  // k_coarse_live flags per coarse down tile
+                const Geom& gl = c->L[l].g;
+                const int zc = coarse_zc(c, gl);
+                c->clive[l] = dalloc<uint8_t>((size_t)((gl.nx + kZX - 1) / kZX) * ((gl.ny + kZY - 1) / kZY) *
+                                              ((gl.nz + zc - 1) / zc));
+            }
         // first capacities of the per-frame tables; setup_sync grows them from a frame's counts
         for (int l = 0; l < depth; ++l) {
             c->cap_ht[l] = 1 << 14;

@@ -596,3 +596,33 @@ def test_setup_branches_equal_serial(b200, monkeypatch):
         assert np.array_equal(a[0], b[0])
         assert np.array_equal(a[1], b[1])
         assert a[2] == b[2] and np.array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_coarse_skip_equals_full(b200, monkeypatch, exact):
+    """Solve-path coarse down steps skip tiles with no fluid within two cells
+    (their outputs stay the frame's zeros): the preconditioner and a solve
+    history equal the full launches bit for bit, across frames whose fluid
+    moves and after a raw network call that writes every tile."""
+    p = b200.default_model()
+    n = 128
+    frames = list(scenes.droplet_frames(n, 3))
+    frames.insert(1, scenes.random_types((n, n, n), 93, p=(0.5, 0.3, 0.2), blobs=8))
+    xin = np.random.default_rng(4).standard_normal(n ** 3).astype(np.float32)
+    out = {}
+    for skip in ("1", "0"):
+        monkeypatch.setenv("NPSD_COARSE_SKIP", skip)
+        ctx = b200.Context(3, (n, n, n), p, exact=exact)
+        res = []
+        for f, t in enumerate(frames):
+            ctx.set_mask(t)
+            r = np.random.default_rng(f).standard_normal(int((t == 0).sum()))
+            a = ctx.precond_apply(r)
+            raw = ctx.net_apply(xin)  # writes every coarse tile
+            rep = ctx.psdo_solve(r, b200.SolveConfig(max_iters=15, tol_reduction=1e-300)).report
+            res.append((a, raw, ctx.precond_apply(r), rep.residual_history))
+        out[skip] = res
+        ctx.close()
+    for a, b in zip(out["1"], out["0"]):
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v)
