@@ -309,7 +309,12 @@ template <int ZC, bool F>
 __global__ void __launch_bounds__(kZT, COARSEZ_MINB) k_cupz(Geom g, Geom gc, const float* __restrict__ outc,
                                               const float* __restrict__ yl, const float* __restrict__ zab, ConvTab ct,
                                               const __grid_constant__ KC kc, float* __restrict__ outl,
-                                              const int* __restrict__ done) {
+                                              const int* __restrict__ done, const uint8_t* __restrict__ live) {
+    // solve path: only out_l within two cells of a level-l fluid cell is ever
+    // read (the level-0 up step reads out_1 within one coarse cell of a fluid
+    // cell; each up step reads out_{l+1} within one cell of its own reads), so
+    // a tile without fluid within two cells (k_coarse_live) is skipped
+    if (live && !live[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]) return;
     __shared__ __align__(16) CUpSmem<ZC> S;
     cupz_tile<ZC, F>(g, gc, outc, yl, zab, ct, kc, outl, blockIdx.x, blockIdx.y, blockIdx.z, S, done);
 }

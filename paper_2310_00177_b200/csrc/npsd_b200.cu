@@ -1144,7 +1144,7 @@ void launch_down(npsd_b200_ctx* c, cudaStream_t s, int l, const float* in_f, con
 }
 
 template <int D, int MODE, int NO>
-void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dout) {
+void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dout, bool skip = false) {
     LevelBufs& L = c->L[l];
     const LevelBufs& Lc = c->L[l + 1];
     const float* outc = (l + 1 == c->depth - 1) ? Lc.y : Lc.out;
@@ -1154,7 +1154,7 @@ void launch_up(npsd_b200_ctx* c, cudaStream_t s, int l, float* outl, double* dou
         const dim3 grid((L.g.nx + kZX - 1) / kZX, (L.g.ny + kZY - 1) / kZY, (L.g.zo1 - L.g.zo0 + zc - 1) / zc);
 #define NPSD_CUP(ZC_, F_)                                                                                        \
     launch_pdl_if(c, s, pdl_coarse(c), k_cupz<ZC_, F_>, grid, dim3(kZT), 0, L.g, Lc.g, outc, L.y, c->zab + 2 * l, \
-                  tab_up(c, l), c->kc_up[l], outl, dn)
+                  tab_up(c, l), c->kc_up[l], outl, dn, skip ? c->clive[l] : (const uint8_t*)nullptr)
         if (c->fast) {
             if (zc == 8) NPSD_CUP(8, true);
             else if (zc == 4) NPSD_CUP(4, true);
@@ -1377,7 +1377,7 @@ std::vector<Step> network_steps(npsd_b200_ctx* c, bool raw, int no) {
                          if (l == 0 && !raw)
                              launch_up0_no<D>(c, s, no);
                          else
-                             launch_up<D, kUpMid, 0>(c, s, l, (l == 0) ? c->out_f : c->L[l].out, nullptr);
+                             launch_up<D, kUpMid, 0>(c, s, l, (l == 0) ? c->out_f : c->L[l].out, nullptr, !raw);
                      }});
         if (xg && l > 0)
             v.push_back(xchg_step(c, "xchg_out_L" + std::to_string(l), [c, l] { return (void*)c->L[l].out; },
@@ -1404,6 +1404,7 @@ void ensure_x1_clean(npsd_b200_ctx* c, cudaStream_t s) {
     for (int l = 1; l + 1 < c->depth; ++l)
         if (c->clive[l]) {  // outputs of the coarse tiles the solve path skips
             CK(cudaMemsetAsync(c->L[l].y, 0, (size_t)c->L[l].g.n * sizeof(float), s));
+            CK(cudaMemsetAsync(c->L[l].out, 0, (size_t)c->L[l].g.n * sizeof(float), s));
             CK(cudaMemsetAsync(c->L[l + 1].x, 0, (size_t)c->L[l + 1].g.n * sizeof(float), s));
         }
     c->x1_clean = true;
