@@ -310,6 +310,7 @@ struct npsd_b200_ctx {
     float* zab = nullptr;  // [depth][2]
     KC kc_down[kMaxDepth], kc_up[kMaxDepth], kc_coarse;  // host copies of the uniform kernels
     uint32_t *fmask = nullptr, *fbase = nullptr, *fcount = nullptr;
+    uint32_t* fmask_prev = nullptr;  // the previous frame's fluid mask (k_zero_removed)
     uint8_t* tflags = nullptr;  // L0 tile occupancy (k_tile_flags)
     SchedBufs sch_stencil;      // 64 x 8 tile columns, plane units (k_up_l0, k_cg_dir; k_ortho2 at n_ortho > 2)
     SchedBufs sch_march;        // 64 x kMarchSY tile columns, plane units (k_ortho2, k_update2)
@@ -690,7 +691,7 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
     CK(cudaMemsetAsync(c->d_info, 0, sizeof(SetupInfo), s));
     // window counts of the linear blocks, levels l < depth - 1 (k_zfinal below)
     for (int l = 0; l + 1 < c->depth; ++l) CK(cudaMemsetAsync(c->L[l].zG, 0, 3 * NCW * sizeof(unsigned long long), s));
-    {  // zero invariant of the solver vectors at the new non-fluid cells
+    if (c->slab.on) {  // zero invariant of the solver vectors at the new non-fluid cells
         cudaStream_t sm = setup_fork(c, s, 0);
         const size_t nb = (size_t)c->g0.n * sizeof(double);
         CK(cudaMemsetAsync(c->X1, 0, nb, sm));
@@ -827,6 +828,11 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         LAUNCH(c, s, k_setup_l0<D>, c->g0.n, c->g0, dtypes, L0.cls, L0.mmask, L0.mcount, c->fmask, c->fcount);
         LAUNCH(c, s, k_tile_flags, (long long)c->tf_ntx * c->tf_nty * c->g0.nz, c->g0, dtypes, c->tf_ntx, c->tf_nty,
                c->tflags);
+    }
+    if (!c->slab.on) {  // zero invariant: only the cells the previous frame had as fluid and this one not
+        cudaStream_t sm = setup_fork(c, s, 0);
+        LAUNCH(c, sm, k_zero_removed, L0.nseg, L0.nseg, c->fmask_prev, (const uint32_t*)c->fmask, c->X1, c->R,
+               c->Dtmp, c->Dring, c->ring_alloc, c->g0.n);
     }
     if (!march0) LAUNCH(c, s, k_sub_masks, L0.g.n, L0.g, L0.cls, c->dmask, c->dcount, c->umask, c->ucount);
     const bool small0 = L0.nseg <= kScanSmallMax;
@@ -2248,6 +2254,7 @@ void free_ctx(npsd_b200_ctx* c) {
     F(c->d_params);
     F(c->zab);
     F(c->fmask);
+    F(c->fmask_prev);
     F(c->fbase);
     F(c->fcount);
     F(c->tflags);
@@ -2453,6 +2460,8 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         CK(cudaMemset(c->zab, 0, 2 * (size_t)depth * sizeof(float)));
         const long long nseg0 = c->L[0].nseg;
         c->fmask = dalloc<uint32_t>((size_t)nseg0);
+        c->fmask_prev = dalloc<uint32_t>((size_t)nseg0);
+        CK(cudaMemset(c->fmask_prev, 0, (size_t)nseg0 * sizeof(uint32_t)));
         c->fbase = dalloc<uint32_t>((size_t)nseg0 + 1);
         c->fcount = dalloc<uint32_t>((size_t)nseg0 + 1);
         CK(cudaMemset(c->fcount, 0, ((size_t)nseg0 + 1) * sizeof(uint32_t)));
@@ -2520,6 +2529,8 @@ int create_impl(int dim, int nx, int ny, int nz, int depth, const float* params,
         c->R = dalloc<double>(n);
         c->Bf = dalloc<double>(n);
         c->Dtmp = dalloc<double>(n);
+        // the zero invariant from the start (frames then zero what stops being fluid)
+        for (double* v : {c->X1, c->R, c->Dtmp}) CK(cudaMemset(v, 0, n * sizeof(double)));
         c->red_a = dalloc<double>(n);
         c->red_b = dalloc<double>(n);
         c->st = dalloc<SolverState>(1);

@@ -370,4 +370,28 @@ __global__ void __launch_bounds__(kBlock) k_residual_norm(Geom g, const double* 
     }
 }
 
+// The zero invariant across frames: the solver vectors are exactly zero at
+// every non-fluid cell. A frame's setup zeroes only the cells that were fluid
+// in the previous frame and are not now (then records the frame's fluid
+// mask); every vector starts zeroed at allocation.
+__global__ void __launch_bounds__(kBlock) k_zero_removed(long long nseg, uint32_t* __restrict__ prev,
+                                                         const uint32_t* __restrict__ cur, double* __restrict__ v0,
+                                                         double* __restrict__ v1, double* __restrict__ v2,
+                                                         double* __restrict__ ring, int nring, long long n) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long seg = (long long)blockIdx.x * blockDim.x + threadIdx.x; seg < nseg; seg += stride) {
+        const uint32_t now = cur[seg];
+        uint32_t m = prev[seg] & ~now;
+        prev[seg] = now;
+        while (m) {
+            const long long c = (seg << 5) + (__ffs(m) - 1);
+            m &= m - 1;
+            v0[c] = 0.0;
+            v1[c] = 0.0;
+            v2[c] = 0.0;
+            for (int j = 0; j < nring; ++j) ring[(long long)j * n + c] = 0.0;
+        }
+    }
+}
+
 }  // namespace nb2

@@ -626,3 +626,27 @@ def test_coarse_skip_equals_full(b200, monkeypatch, exact):
     for a, b in zip(out["1"], out["0"]):
         for u, v in zip(a, b):
             assert np.array_equal(u, v)
+
+
+def test_frame_after_larger_frame_equals_fresh_context(b200):
+    """A frame's setup zeroes only the cells that stopped being fluid (the
+    solver vectors' zero invariant): after solves on a frame with more fluid,
+    a frame with less gives the same solve as a fresh context, bit for bit."""
+    p = b200.default_model()
+    n = 64
+    big = scenes.random_types((n, n, n), 11, p=(0.8, 0.15, 0.05), blobs=4)
+    small = scenes.random_types((n, n, n), 12, p=(0.4, 0.4, 0.2), blobs=8)
+    cfg = b200.SolveConfig(max_iters=30, tol_reduction=1e-300)
+    bs = b200.rhs_normal(3, small.size)[small.reshape(-1) == 0]
+    ctx = b200.Context(3, (n, n, n), p)
+    ctx.set_mask(big)
+    ctx.psdo_solve(b200.rhs_normal(2, big.size)[big.reshape(-1) == 0], cfg)
+    ctx.set_mask(small)
+    got = ctx.psdo_solve(bs, cfg)
+    ctx.close()
+    fresh = b200.Context(3, (n, n, n), p)
+    fresh.set_mask(small)
+    want = fresh.psdo_solve(bs, cfg)
+    fresh.close()
+    assert np.array_equal(got.x, want.x)
+    assert np.array_equal(got.report.residual_history, want.report.residual_history)

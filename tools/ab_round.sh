@@ -1,3 +1,3 @@
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_00_bench_configs.py tests/test_gpu_slab.py -q -x -p no:cacheprovider > gpurun_out/v16_tests.log 2>&1; echo rc=$? >> gpurun_out/v16_tests.log
-python tools/env_ab.py NPSD_COARSE_SKIP 0 1 > gpurun_out/v16_ab_skip.txt 2>&1
-python tools/env_ab.py NPSD_COARSE_SKIP 1 0 >> gpurun_out/v16_ab_skip.txt 2>&1
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_00_bench_configs.py tests/test_gpu_slab.py tests/test_gpu_boundary.py tests/test_gpu_dropin.py -q -x -p no:cacheprovider > gpurun_out/v17_tests.log 2>&1; echo rc=$? >> gpurun_out/v17_tests.log
+bash tools/setmask_ab.sh > gpurun_out/v17_setmask.log 2>&1
+python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/v17_bench.json 2> gpurun_out/v17_bench.err
