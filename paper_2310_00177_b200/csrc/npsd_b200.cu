@@ -373,7 +373,7 @@ struct npsd_b200_ctx {
     bool setup_par = true;  // NPSD_SETUP_SERIAL=1: one stream
     cudaStreamAttrValue apw = {};  // the L2 access-policy window of the streams (l2pool)
     bool apw_on = false;
-    cudaStream_t sx[kMaxDepth + 2] = {};
+    cudaStream_t sx[2 * kMaxDepth + 2] = {};  // [2 + kMaxDepth + l]: level l's window counts and live tiles
     cudaEvent_t evf[4 * kMaxDepth + 8] = {};
     int nev = 0;
     // solve graph
@@ -742,10 +742,20 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         }
         // level l's dictionary (hashed windows, verified) and rows
         const cudaStream_t sl = setup_fork(c, sc, 2 + l);
-        if (c->clive[l]) {
-            const int zc = coarse_zc(c, Lc.g);
-            const int nt = ((Lc.g.nx + kZX - 1) / kZX) * ((Lc.g.ny + kZY - 1) / kZY) * ((Lc.g.nz + zc - 1) / zc);
-            LAUNCH3(c, sl, k_coarse_live, dim3(nt), dim3(kBlock), Lc.g, (const float*)Lc.img, zc, c->clive[l]);
+        {  // from the pooled image alone, beside the dictionary: live tiles and the linear block's counts
+            const cudaStream_t sz = setup_fork(c, sc, 2 + kMaxDepth + l);
+            if (c->clive[l]) {
+                const int zc = coarse_zc(c, Lc.g);
+                const int nt = ((Lc.g.nx + kZX - 1) / kZX) * ((Lc.g.ny + kZY - 1) / kZY) * ((Lc.g.nz + zc - 1) / zc);
+                LAUNCH3(c, sz, k_coarse_live, dim3(nt), dim3(kBlock), Lc.g, (const float*)Lc.img, zc, c->clive[l]);
+            }
+            if (l < c->depth - 1) {
+                // the window counts: the pooled image x 8^l (exact dyadic values)
+                const int nrows = Lc.g.ny * (Lc.g.zo1 - Lc.g.zo0);  // a warp per row
+                const int blocks = std::max(1, std::min((nrows + kBlock / 32 - 1) / (kBlock / 32), 4 * c->num_sms));
+                LAUNCH3(c, sz, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), Lc.g, (const uint8_t*)nullptr,
+                        (const float*)Lc.img, (float)std::ldexp(1.0, D * l), zg_offset(c, l), c->gglob[l].nz, Lc.zG);
+            }
         }
         const uint32_t rows_cap = (uint32_t)c->tab_cap[l];
         const uint32_t rows_bit = 1u << (2 * l + 1);
@@ -763,11 +773,6 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
         // rows: one per window pattern when the hashed dictionary verifies, else one per mixed cell
         const long long row_items = 32LL * std::min<long long>(rows_cap, Lc.g.n);
         if (l < c->depth - 1) {
-            // the linear block's window counts: the pooled image x 8^l (exact dyadic values)
-            const int nrows = Lc.g.ny * (Lc.g.zo1 - Lc.g.zo0);  // a warp per row
-            const int blocks = std::max(1, std::min((nrows + kBlock / 32 - 1) / (kBlock / 32), 4 * c->num_sms));
-            LAUNCH3(c, sl, k_zsums_rows<D>, dim3(blocks), dim3(kBlock), Lc.g, (const uint8_t*)nullptr,
-                    (const float*)Lc.img, (float)std::ldexp(1.0, D * l), zg_offset(c, l), c->gglob[l].nz, Lc.zG);
             const LevelOffsets& o = c->offs[(size_t)l];
             LAUNCH(c, sl, k_build_rows<D>, row_items, Lc.g, (const uint8_t*)nullptr, (const float*)Lc.img,
                    (const uint32_t*)rep, (const uint32_t*)npat, (const uint32_t*)Lc.mlist, (const uint32_t*)Lc.mcnt,
@@ -882,7 +887,8 @@ void set_mask_enqueue(npsd_b200_ctx* c, const uint8_t* dtypes) {
                c->d_params + c->coarse_W, c->d_params + c->coarse_B, L0.tab_down, (const float*)nullptr,
                (const float*)nullptr, (float*)nullptr);
     }
-    for (int k = 0; k < 2 + c->depth; ++k) setup_join(c, k);  // memsets, schedules, coarse chain, levels 1..
+    for (int k = 0; k < 2 + c->depth; ++k) setup_join(c, k);  // zeroing, schedules, coarse chain, dictionaries 1..
+    for (int l = 1; l < c->depth; ++l) setup_join(c, 2 + kMaxDepth + l);  // counts and live tiles 1..
     // linear-block coefficients of every level (k_zfinal: one block per level)
     ZfinArgs zf{};
     for (int l = 0; l + 1 < c->depth; ++l) {

@@ -865,20 +865,26 @@ __global__ void __launch_bounds__(kBlock) k_dedup_insert(const unsigned long lon
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         unsigned long long k = keys[i];
         if (k == kEmptyKey) k = kEmptyKey - 1;  // a coarse hash; collisions are caught by k_verify_windows
-        unsigned long long h = mix64(k) & mask;
-        while (true) {
-            unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(tk + h);
-            if (cur == kEmptyKey) cur = atomicCAS(tk + h, kEmptyKey, k);
-            if (cur == kEmptyKey) {  // inserted: new pattern
-                const uint32_t id = atomicAdd(npat, 1u);
-                tv[h] = id;
-                repcell[id] = list[i];
-                break;
+        // neighbouring cells often share a window: one probe per distinct key of the warp
+        const unsigned peers = __match_any_sync(__activemask(), k);
+        const int leader = __ffs(peers) - 1;
+        unsigned long long h = 0;
+        if ((int)(threadIdx.x & 31) == leader) {
+            h = mix64(k) & mask;
+            while (true) {
+                unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(tk + h);
+                if (cur == kEmptyKey) cur = atomicCAS(tk + h, kEmptyKey, k);
+                if (cur == kEmptyKey) {  // inserted: new pattern
+                    const uint32_t id = atomicAdd(npat, 1u);
+                    tv[h] = id;
+                    repcell[id] = list[i];
+                    break;
+                }
+                if (cur == k) break;
+                h = (h + 1) & mask;
             }
-            if (cur == k) break;
-            h = (h + 1) & mask;
         }
-        slot[i] = (uint32_t)h;
+        slot[i] = (uint32_t)__shfl_sync(peers, (unsigned)h, leader);
     }
 }
 
