@@ -1,6 +1,6 @@
 """Per-iteration device time of the solve graph under a context-creation
-environment switch (NPSD_PDL, NPSD_CHAIN, ...) on C1/C2/C3:
-    python tools/pdl_ab.py [VAR] [values...]   (default: NPSD_PDL 0 1)"""
+environment switch (NPSD_PDL, NPSD_PDL_MASK, NPSD_COARSE_SKIP, ...) on C1/C2/C3:
+    python tools/env_ab.py [VAR] [values...]   (default: NPSD_PDL 0 1)"""
 import os
 import sys
 from pathlib import Path
