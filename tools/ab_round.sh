@@ -1,3 +1,3 @@
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_00_bench_configs.py -q -x -p no:cacheprovider > gpurun_out/v21_tests.log 2>&1; echo rc=$? >> gpurun_out/v21_tests.log
-bash tools/setmask_ab.sh > gpurun_out/v21_setmask.log 2>&1
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_00_bench_configs.py -q -x -p no:cacheprovider > gpurun_out/v23_tests.log 2>&1; echo rc=$? >> gpurun_out/v23_tests.log
+bash tools/setmask_ab.sh > gpurun_out/v23_setmask.log 2>&1
 bash tools/ncu_setmask.sh
