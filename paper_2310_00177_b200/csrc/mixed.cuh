@@ -220,7 +220,7 @@ __device__ __forceinline__ void decode32(const Geom& g, uint32_t c, int& x, int&
 
 template <int D, bool F>
 #ifndef MIXDN_MINB
-#define MIXDN_MINB 5  // register cap for 5 blocks/SM (measured 37 -> 29 us on the same box)
+#define MIXDN_MINB 4  // register cap (64: no spills with the row-run path; round 1: 5 blocks/SM, 37 -> 29 us)
 #endif
 __global__ void __launch_bounds__(kBlock, MIXDN_MINB) k_mixed_down0(Geom g, const uint32_t* __restrict__ list,
                                                         const uint32_t* __restrict__ count, const double* __restrict__ r,
@@ -229,10 +229,13 @@ __global__ void __launch_bounds__(kBlock, MIXDN_MINB) k_mixed_down0(Geom g, cons
                                                         float* __restrict__ y) {
     constexpr int S = Sh<D>::S;
     // the first cell's list entry and kernel row are setup data: loaded before
-    // the programmatic wait (the previous launch writes r)
+    // the programmatic wait (the previous launch writes r). The loop is
+    // warp-uniform: a warp takes 32 consecutive list entries.
     const uint32_t n = *count;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long i = i0;
     uint32_t c = 0;
     float k[S];
     auto fetch = [&](long long j) {
@@ -245,19 +248,55 @@ __global__ void __launch_bounds__(kBlock, MIXDN_MINB) k_mixed_down0(Geom g, cons
     pdl_launch_wait();
     if (st->dist && st->done) return;
     const double inv1 = st->inv1, inv2 = st->inv2;
-    for (; i < n; i += stride) {
-        if (i >= (long long)blockIdx.x * blockDim.x + threadIdx.x + stride) fetch(i);
-        int x, yy, z;
-        decode32(g, c, x, yy, z);
-        float w[S];
+    const long long plane = (long long)g.nx * g.ny;
+    auto cvt = [&](double v) { return __double2float_rn(__dmul_rn(__dmul_rn(v, inv1), inv2)); };
+    for (; i - lane < n; i += stride) {
+        const bool valid = i < n;
+        if (valid && i != i0) fetch(i);
+        // 32 consecutive cells of one x row (a flat surface or wall): the 3 x 3
+        // rows of their windows are read once, coalesced, converted once, and
+        // handed to the neighbours by shuffles (the same values as the gather,
+        // summed in win_dot's order)
+        const uint32_t cf = __shfl_sync(0xffffffffu, c, 0), cl = __shfl_sync(0xffffffffu, c, 31);
+        const bool run = D == 3 && __all_sync(0xffffffffu, valid) && cl - cf == 31u &&
+                         (cf % (uint32_t)g.nx) + 31u < (uint32_t)g.nx;
+        float yv = 0.0f;
+        if (run) {
+            int x0, y0, z0;
+            decode32(g, cf, x0, y0, z0);
+            float a[3] = {0.0f, 0.0f, 0.0f};  // exact: a[0] only (slot order); fast: one chain per window plane
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
-            const int xx = x + dx, y2 = yy + dy, zz = z + dz;
-            const bool in = xx >= 0 && xx < g.nx && y2 >= 0 && y2 < g.ny && zz >= 0 && zz < g.nz;
-            w[s] = in ? __double2float_rn(__dmul_rn(__dmul_rn(__ldg(r + lin(g, xx, y2, zz)), inv1), inv2)) : 0.0f;
+            for (int rr = 0; rr < 9; ++rr) {
+                const int dy = rr % 3 - 1, dz = rr / 3 - 1;
+                const bool rin = (unsigned)(y0 + dy) < (unsigned)g.ny && (unsigned)(z0 + dz) < (unsigned)g.nz;
+                const double* rowp = r + ((long long)(z0 + dz) * plane + (long long)(y0 + dy) * g.nx + x0);
+                // v: x0 - 1 + lane; e: x0 + 31 (lane 0), x0 + 32 (lane 1)
+                const float v = (rin && x0 - 1 + lane >= 0) ? cvt(__ldg(rowp - 1 + lane)) : 0.0f;
+                const float e = (rin && lane < 2 && x0 + 31 + lane < g.nx) ? cvt(__ldg(rowp + 31 + lane)) : 0.0f;
+                const float v1 = __shfl_down_sync(0xffffffffu, v, 1), v2 = __shfl_down_sync(0xffffffffu, v, 2);
+                const float e0 = __shfl_sync(0xffffffffu, e, 0), e1 = __shfl_sync(0xffffffffu, e, 1);
+                const float t3[3] = {v, (lane < 31) ? v1 : e0, (lane < 30) ? v2 : (lane == 30 ? e0 : e1)};
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
+                    const int sl = rr * 3 + dx;
+                    if (F)
+                        a[dz + 1] = __fmaf_rn(k[sl], t3[dx], a[dz + 1]);
+                    else
+                        a[0] = __fadd_rn(a[0], __fmul_rn(k[sl], t3[dx]));
+                }
+            }
+            yv = F ? __fadd_rn(__fadd_rn(a[0], a[1]), a[2]) : a[0];
+        } else if (valid) {
+            int x, yy, z;
+            decode32(g, c, x, yy, z);
+            yv = win_dot<F, S>([&](int t) { return k[t]; }, [&](int s2) {
+                const int dx = s2 % 3 - 1, dy = (s2 / 3) % 3 - 1, dz = (D == 3) ? s2 / 9 - 1 : 0;
+                const int xx = x + dx, y2 = yy + dy, zz = z + dz;
+                const bool in = xx >= 0 && xx < g.nx && y2 >= 0 && y2 < g.ny && zz >= 0 && zz < g.nz;
+                return in ? cvt(__ldg(r + lin(g, xx, y2, zz))) : 0.0f;
+            });
         }
-        y[c] = win_dot<F, S>([&](int t) { return k[t]; }, [&](int t) { return w[t]; });
+        if (valid) y[c] = yv;
     }
 }
 
